@@ -1,0 +1,968 @@
+/*
+ * oracle/hd_oracle.c -- CPU ORACLE (TEST INFRASTRUCTURE ONLY; see hd_oracle.h).
+ *
+ * Plain C11, single-threaded, no blocking/fusion/reordering beyond what the
+ * paper's algorithm or the operation's definition states.  Compile with
+ * -ffp-contract=off (no FMA) so the floating-point encoder is the pinned
+ * operation order of DESIGN.md R15.
+ *
+ * Parity pins for every function live in tests/test_oracle_*.py ("not gpu").
+ */
+#define _GNU_SOURCE
+#include "hd_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef unsigned __int128 u128;
+
+/* ------------------------------------------------------------------------ */
+/* Modular arithmetic: the plain definitions.                               */
+/* ------------------------------------------------------------------------ */
+static uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) { return (uint64_t)(((u128)a * b) % m); }
+static uint64_t addmod(uint64_t a, uint64_t b, uint64_t m) { return (uint64_t)(((u128)a + b) % m); }
+static uint64_t submod(uint64_t a, uint64_t b, uint64_t m) { return (uint64_t)(((u128)a + m - b) % m); }
+static uint64_t powmod(uint64_t b, uint64_t e, uint64_t m) {
+  uint64_t r = 1 % m;
+  b %= m;
+  while (e) {
+    if (e & 1) r = mulmod(r, b, m);
+    b = mulmod(b, b, m);
+    e >>= 1;
+  }
+  return r;
+}
+/* inverse by Fermat (m prime) */
+static uint64_t invmod(uint64_t a, uint64_t m) { return powmod(a, m - 2, m); }
+/* signed integer -> residue in [0, m) */
+static uint64_t smod(int64_t x, uint64_t m) {
+  if (x >= 0) return (uint64_t)x % m;
+  uint64_t r = (uint64_t)(-(x + 1)) % m; /* -(x+1) >= 0, avoids INT64_MIN overflow */
+  r = (r + 1) % m;                        /* |x| mod m */
+  return r == 0 ? 0 : m - r;
+}
+/* centred representative of x in [0,q): (-q/2, q/2]  (R12) */
+static int64_t centre(uint64_t x, uint64_t q) {
+  if (x > q / 2) return -(int64_t)(q - x);
+  return (int64_t)x;
+}
+static uint32_t bitrev(uint32_t x, int bits) {
+  uint32_t r = 0;
+  for (int i = 0; i < bits; i++) r |= ((x >> i) & 1u) << (bits - 1 - i);
+  return r;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Parameters (R5, R13).                                                    */
+/* ------------------------------------------------------------------------ */
+int or_is_prime(uint64_t x) {
+  static const uint64_t bases[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+  if (x < 2) return 0;
+  for (int i = 0; i < 12; i++) {
+    if (x % bases[i] == 0) return x == bases[i];
+  }
+  uint64_t d = x - 1;
+  int s = 0;
+  while ((d & 1) == 0) { d >>= 1; s++; }
+  for (int i = 0; i < 12; i++) {
+    uint64_t y = powmod(bases[i], d, x);
+    if (y == 1 || y == x - 1) continue;
+    int composite = 1;
+    for (int r = 1; r < s; r++) {
+      y = mulmod(y, y, x);
+      if (y == x - 1) { composite = 0; break; }
+    }
+    if (composite) return 0;
+  }
+  return 1;
+}
+
+/* Largest prime c < below with c = 1 (mod two_n); candidates 2n*k+1, k descending. */
+static uint64_t prev_ntt_prime(uint64_t below, uint64_t two_n) {
+  uint64_t k = (below - 2) / two_n;
+  for (; k > 0; k--) {
+    uint64_t c = two_n * k + 1;
+    if (c < below && or_is_prime(c)) return c;
+  }
+  return 0;
+}
+
+/* Numerically smallest primitive 2n-th root of unity mod m (R13). */
+static uint64_t min_root(uint64_t m, uint64_t n) {
+  uint64_t y = 0;
+  for (uint64_t x = 2; x < m; x++) {
+    y = powmod(x, (m - 1) / (2 * n), m);
+    if (powmod(y, n, m) == m - 1) break; /* order exactly 2n */
+  }
+  uint64_t y2 = mulmod(y, y, m), cur = y, best = y;
+  for (uint64_t t = 1; t < n; t++) {
+    cur = mulmod(cur, y2, m); /* y^(2t+1): every primitive 2n-th root */
+    if (cur < best) best = cur;
+  }
+  return best;
+}
+
+int or_params_init(or_params *p, int32_t log_n, int32_t L, uint64_t seed) {
+  if (!p || log_n < 2 || log_n > 17 || L < 2 || L + 1 > OR_MAXMOD) return OR_E_PARAMS;
+  memset(p, 0, sizeof(*p));
+  p->log_n = log_n;
+  p->n = 1 << log_n;
+  p->num_slots = p->n / 2;
+  p->L = L;
+  p->q0_bits = 60;
+  p->scale_bits = 45;
+  p->special_bits = 60;
+  p->seed = seed;
+  uint64_t two_n = 2 * (uint64_t)p->n;
+  p->mod[0] = prev_ntt_prime((uint64_t)1 << p->q0_bits, two_n);
+  p->mod[L] = prev_ntt_prime(p->mod[0], two_n); /* P: next prime below q0 */
+  uint64_t below = (uint64_t)1 << p->scale_bits;
+  for (int i = 1; i < L; i++) {
+    p->mod[i] = prev_ntt_prime(below, two_n);
+    below = p->mod[i];
+  }
+  for (int i = 0; i <= L; i++) {
+    if (p->mod[i] == 0) return OR_E_PARAMS;
+    p->psi[i] = min_root(p->mod[i], (uint64_t)p->n);
+  }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* NTT (R13).  Definition: a^[i] = sum_j a_j psi^{(2 br(i)+1) j} mod m.      */
+/* ------------------------------------------------------------------------ */
+int or_ntt_definition(const or_params *p, int32_t l, const uint64_t *a, uint64_t *out) {
+  if (l < 0 || l > p->L) return OR_E_ARG;
+  uint64_t m = p->mod[l];
+  int n = p->n;
+  for (int i = 0; i < n; i++) {
+    uint64_t w = powmod(p->psi[l], 2 * (uint64_t)bitrev((uint32_t)i, p->log_n) + 1, m);
+    uint64_t acc = 0, pw = 1;
+    for (int j = 0; j < n; j++) {
+      acc = addmod(acc, mulmod(a[j], pw, m), m);
+      pw = mulmod(pw, w, m);
+    }
+    out[i] = acc;
+  }
+  return OR_OK;
+}
+
+/* psi_rev[k] = psi^{br(k)} (or psi^{-br(k)}), k in [0, n) */
+static uint64_t *psi_rev_table(const or_params *p, int32_t l, int inverse) {
+  int n = p->n;
+  uint64_t m = p->mod[l];
+  uint64_t base = inverse ? invmod(p->psi[l], m) : p->psi[l];
+  uint64_t *pw = malloc(sizeof(uint64_t) * n), *rev = malloc(sizeof(uint64_t) * n);
+  pw[0] = 1;
+  for (int k = 1; k < n; k++) pw[k] = mulmod(pw[k - 1], base, m);
+  for (int k = 0; k < n; k++) rev[k] = pw[bitrev((uint32_t)k, p->log_n)];
+  free(pw);
+  return rev;
+}
+
+/* Cooley-Tukey, natural order in, bit-reversed evaluation order out. */
+int or_ntt_forward(const or_params *p, int32_t l, uint64_t *a) {
+  if (l < 0 || l > p->L) return OR_E_ARG;
+  uint64_t m = p->mod[l];
+  int n = p->n;
+  uint64_t *S = psi_rev_table(p, l, 0);
+  int t = n;
+  for (int mm = 1; mm < n; mm <<= 1) {
+    t >>= 1;
+    for (int i = 0; i < mm; i++) {
+      uint64_t w = S[mm + i];
+      for (int j = 2 * i * t; j < 2 * i * t + t; j++) {
+        uint64_t U = a[j], V = mulmod(a[j + t], w, m);
+        a[j] = addmod(U, V, m);
+        a[j + t] = submod(U, V, m);
+      }
+    }
+  }
+  free(S);
+  return OR_OK;
+}
+
+/* Gentleman-Sande inverse of the above, then multiply by n^{-1}. */
+int or_ntt_inverse(const or_params *p, int32_t l, uint64_t *a) {
+  if (l < 0 || l > p->L) return OR_E_ARG;
+  uint64_t m = p->mod[l];
+  int n = p->n;
+  uint64_t *S = psi_rev_table(p, l, 1);
+  int t = 1;
+  for (int mm = n / 2; mm >= 1; mm >>= 1) {
+    for (int i = 0; i < mm; i++) {
+      uint64_t w = S[mm + i];
+      for (int j = 2 * i * t; j < 2 * i * t + t; j++) {
+        uint64_t U = a[j], V = a[j + t];
+        a[j] = addmod(U, V, m);
+        a[j + t] = mulmod(submod(U, V, m), w, m);
+      }
+    }
+    t <<= 1;
+  }
+  uint64_t ninv = invmod((uint64_t)n, m);
+  for (int j = 0; j < n; j++) a[j] = mulmod(a[j], ninv, m);
+  free(S);
+  return OR_OK;
+}
+
+/* Schoolbook product in Z_m[X]/(X^n+1): the textbook definition. */
+int or_negacyclic_schoolbook(const uint64_t *a, const uint64_t *b, int32_t n, uint64_t m,
+                             uint64_t *out) {
+  for (int k = 0; k < n; k++) out[k] = 0;
+  for (int i = 0; i < n; i++)
+    for (int j = 0; j < n; j++) {
+      uint64_t prod = mulmod(a[i], b[j], m);
+      int k = i + j;
+      if (k < n) out[k] = addmod(out[k], prod, m);
+      else out[k - n] = submod(out[k - n], prod, m); /* X^n = -1 */
+    }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Randomness (R14): Philox4x32-10, counter (j, l, obj, tag<<16|sub).        */
+/* ------------------------------------------------------------------------ */
+void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+  uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3];
+  uint32_t k0 = key[0], k1 = key[1];
+  for (int r = 0; r < 10; r++) {
+    if (r > 0) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c1 ^ k0, n1 = lo1, n2 = hi0 ^ c3 ^ k1, n3 = lo0;
+    c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5 };
+
+static void draw(uint64_t seed, uint32_t j, uint32_t l, uint32_t obj, uint32_t tag, uint32_t sub,
+                 uint64_t *w0, uint64_t *w1) {
+  uint32_t ctr[4] = {j, l, obj, (tag << 16) | sub};
+  uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+  uint32_t o[4];
+  or_philox4x32_10(ctr, key, o);
+  *w0 = (uint64_t)o[0] | ((uint64_t)o[1] << 32);
+  *w1 = (uint64_t)o[2] | ((uint64_t)o[3] << 32);
+}
+static uint64_t draw_uniform(uint64_t seed, uint32_t j, uint32_t l, uint32_t obj, uint32_t tag,
+                             uint32_t sub, uint64_t m) {
+  uint64_t w0, w1;
+  draw(seed, j, l, obj, tag, sub, &w0, &w1);
+  return (uint64_t)((((u128)w0 << 64) | w1) % m);
+}
+static int64_t draw_cbd21(uint64_t seed, uint32_t j, uint32_t obj, uint32_t tag, uint32_t sub) {
+  uint64_t w0, w1;
+  draw(seed, j, 0, obj, tag, sub, &w0, &w1);
+  return (int64_t)__builtin_popcountll(w0 & 0x1FFFFFull) -
+         (int64_t)__builtin_popcountll((w0 >> 21) & 0x1FFFFFull);
+}
+static int64_t draw_ternary(uint64_t seed, uint32_t j, uint32_t obj, uint32_t tag) {
+  uint64_t w0, w1;
+  draw(seed, j, 0, obj, tag, 0, &w0, &w1);
+  return (int64_t)(w0 % 3) - 1;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Galois automorphisms (R7).                                        */
+/* ------------------------------------------------------------------------ */
+uint64_t or_galois_elt(const or_params *p, int64_t step) {
+  uint64_t two_n = 2 * (uint64_t)p->n;
+  int64_t r = step % p->num_slots;
+  if (r < 0) r += p->num_slots;
+  return powmod(5, (uint64_t)r, two_n);
+}
+
+/* sigma_g on coefficients: X^j -> X^{jg mod 2n}, X^n = -1 (the definition). */
+int or_automorph_coeff(const or_params *p, uint64_t g, const int64_t *a, int64_t *out) {
+  int n = p->n;
+  uint64_t two_n = 2 * (uint64_t)n;
+  for (int j = 0; j < n; j++) {
+    uint64_t idx = ((uint64_t)j * g) % two_n;
+    if (idx < (uint64_t)n) out[idx] = a[j];
+    else out[idx - n] = -a[j];
+  }
+  return OR_OK;
+}
+
+/* sigma_g in the NTT domain: out[i] = a[pi_g(i)],
+ * pi_g(i) = br(((g (2 br(i)+1)) mod 2n - 1) / 2).  Pinned against
+ * or_automorph_coeff by tests/test_oracle_ring.py. */
+int or_automorph_ntt(const or_params *p, uint64_t g, const uint64_t *a, uint64_t *out) {
+  int n = p->n;
+  uint64_t two_n = 2 * (uint64_t)n;
+  for (int i = 0; i < n; i++) {
+    uint64_t e = (g * (2 * (uint64_t)bitrev((uint32_t)i, p->log_n) + 1)) % two_n;
+    uint32_t src = bitrev((uint32_t)((e - 1) / 2), p->log_n);
+    out[i] = a[src];
+  }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* CKKS encoding (R15): pinned special inverse FFT.              */
+/* xi^t = (cos(2 pi t / 2n), sin(2 pi t / 2n)); complex multiply without FMA. */
+/* ------------------------------------------------------------------------ */
+static void xi(const or_params *p, uint64_t t, double *re, double *im) {
+  double ang = (2.0 * 3.141592653589793 * (double)t) / (double)(2 * (uint64_t)p->n);
+  *re = cos(ang);
+  *im = sin(ang);
+}
+
+static void bitrev_permute(double *re, double *im, int size) {
+  int bits = 0;
+  while ((1 << bits) < size) bits++;
+  for (int i = 0; i < size; i++) {
+    int r = (int)bitrev((uint32_t)i, bits);
+    if (r > i) {
+      double t = re[i]; re[i] = re[r]; re[r] = t;
+      t = im[i]; im[i] = im[r]; im[r] = t;
+    }
+  }
+}
+
+/* Special inverse FFT (canonical-embedding inverse over slots zeta^{5^j}). */
+static void fft_special_inv(const or_params *p, double *re, double *im) {
+  int size = p->num_slots;
+  uint64_t M = 2 * (uint64_t)p->n;
+  for (int len = size; len >= 2; len >>= 1) {
+    int lenh = len >> 1;
+    uint64_t lenq = (uint64_t)len << 2;
+    for (int i = 0; i < size; i += len) {
+      for (int j = 0; j < lenh; j++) {
+        uint64_t rot = powmod(5, (uint64_t)j, M);
+        uint64_t idx = (lenq - (rot % lenq)) * (M / lenq);
+        double wr, wi;
+        xi(p, idx, &wr, &wi);
+        double ur = re[i + j] + re[i + j + lenh], ui = im[i + j] + im[i + j + lenh];
+        double vr = re[i + j] - re[i + j + lenh], vi = im[i + j] - im[i + j + lenh];
+        double tr = vr * wr - vi * wi;
+        double ti = vr * wi + vi * wr;
+        re[i + j] = ur; im[i + j] = ui;
+        re[i + j + lenh] = tr; im[i + j + lenh] = ti;
+      }
+    }
+  }
+  bitrev_permute(re, im, size);
+  for (int i = 0; i < size; i++) {
+    re[i] = re[i] / (double)size;
+    im[i] = im[i] / (double)size;
+  }
+}
+
+/* Special forward FFT (decode). */
+static void fft_special(const or_params *p, double *re, double *im) {
+  int size = p->num_slots;
+  uint64_t M = 2 * (uint64_t)p->n;
+  bitrev_permute(re, im, size);
+  for (int len = 2; len <= size; len <<= 1) {
+    int lenh = len >> 1;
+    uint64_t lenq = (uint64_t)len << 2;
+    for (int i = 0; i < size; i += len) {
+      for (int j = 0; j < lenh; j++) {
+        uint64_t rot = powmod(5, (uint64_t)j, M);
+        uint64_t idx = (rot % lenq) * (M / lenq);
+        double wr, wi;
+        xi(p, idx, &wr, &wi);
+        double ur = re[i + j], ui = im[i + j];
+        double xr = re[i + j + lenh], xim = im[i + j + lenh];
+        double vr = xr * wr - xim * wi;
+        double vi = xr * wi + xim * wr;
+        re[i + j] = ur + vr; im[i + j] = ui + vi;
+        re[i + j + lenh] = ur - vr; im[i + j + lenh] = ui - vi;
+      }
+    }
+  }
+}
+
+/* Integer coefficients coef_k = llrint(x_k * delta) (round-half-even). */
+int or_encode_coeffs(const or_params *p, const double *z, double delta, int64_t *coef) {
+  int ns = p->num_slots;
+  double *re = malloc(sizeof(double) * ns), *im = malloc(sizeof(double) * ns);
+  for (int i = 0; i < ns; i++) { re[i] = z[i]; im[i] = 0.0; }
+  fft_special_inv(p, re, im);
+  int rc = OR_OK;
+  for (int i = 0; i < ns; i++) {
+    double a = re[i] * delta, b = im[i] * delta;
+    if (!(fabs(a) < 4611686018427387904.0) || !(fabs(b) < 4611686018427387904.0)) rc = OR_E_RANGE;
+    coef[i] = llrint(a);
+    coef[i + ns] = llrint(b);
+  }
+  free(re);
+  free(im);
+  return rc;
+}
+
+int or_encode(const or_params *p, const double *z, double delta, int32_t nlimbs, uint64_t *pt) {
+  if (nlimbs < 1 || nlimbs > p->L) return OR_E_ARG;
+  int n = p->n;
+  int64_t *coef = malloc(sizeof(int64_t) * n);
+  int rc = or_encode_coeffs(p, z, delta, coef);
+  if (rc == OR_OK) {
+    for (int l = 0; l < nlimbs; l++) {
+      for (int j = 0; j < n; j++) pt[(size_t)l * n + j] = smod(coef[j], p->mod[l]);
+      or_ntt_forward(p, l, pt + (size_t)l * n);
+    }
+  }
+  free(coef);
+  return rc;
+}
+
+/* Centred CRT of one coefficient over q_0..q_{nlimbs-1} (Garner), as double. */
+static double crt_centred(const or_params *p, const uint64_t *x, int nlimbs) {
+  /* mixed-radix digits v_i */
+  uint64_t v[OR_MAXMOD];
+  for (int i = 0; i < nlimbs; i++) {
+    uint64_t qi = p->mod[i];
+    uint64_t t = x[i] % qi;
+    for (int k = 0; k < i; k++) t = mulmod(submod(t, v[k] % qi, qi), invmod(p->mod[k] % qi, qi), qi);
+    v[i] = t;
+  }
+  /* X = sum v_i prod_{k<i} q_k and Q = prod q_k as little-endian 64-bit words */
+  uint64_t X[OR_MAXMOD + 1] = {0}, Q[OR_MAXMOD + 1] = {0}, W[OR_MAXMOD + 1] = {0};
+  int words = nlimbs + 1;
+  W[0] = 1;
+  for (int i = 0; i < nlimbs; i++) {
+    u128 carry = 0; /* X += v_i * W */
+    for (int w = 0; w < words; w++) {
+      u128 s = (u128)v[i] * W[w] + X[w] + carry;
+      X[w] = (uint64_t)s;
+      carry = s >> 64;
+    }
+    carry = 0; /* W *= q_i */
+    for (int w = 0; w < words; w++) {
+      u128 s = (u128)W[w] * p->mod[i] + carry;
+      W[w] = (uint64_t)s;
+      carry = s >> 64;
+    }
+  }
+  memcpy(Q, W, sizeof(Q));
+  /* negative iff 2X > Q */
+  uint64_t X2[OR_MAXMOD + 1];
+  uint64_t c = 0;
+  for (int w = 0; w < words; w++) {
+    X2[w] = (X[w] << 1) | c;
+    c = X[w] >> 63;
+  }
+  int gt = 0;
+  for (int w = words - 1; w >= 0; w--) {
+    if (X2[w] != Q[w]) { gt = X2[w] > Q[w]; break; }
+  }
+  uint64_t mag[OR_MAXMOD + 1];
+  if (gt) { /* mag = Q - X */
+    u128 borrow = 0;
+    for (int w = 0; w < words; w++) {
+      u128 d = (u128)Q[w] - X[w] - borrow;
+      mag[w] = (uint64_t)d;
+      borrow = (d >> 64) ? 1 : 0;
+    }
+  } else {
+    memcpy(mag, X, sizeof(mag));
+  }
+  long double r = 0.0L;
+  for (int w = words - 1; w >= 0; w--) r = r * 18446744073709551616.0L + (long double)mag[w];
+  return gt ? -(double)r : (double)r;
+}
+
+int or_decode(const or_params *p, const uint64_t *pt, int32_t nlimbs, double delta, double *z) {
+  if (nlimbs < 1 || nlimbs > p->L) return OR_E_ARG;
+  int n = p->n, ns = p->num_slots;
+  uint64_t *c = malloc(sizeof(uint64_t) * (size_t)n * nlimbs);
+  memcpy(c, pt, sizeof(uint64_t) * (size_t)n * nlimbs);
+  for (int l = 0; l < nlimbs; l++) or_ntt_inverse(p, l, c + (size_t)l * n);
+  double *re = malloc(sizeof(double) * ns), *im = malloc(sizeof(double) * ns);
+  uint64_t x[OR_MAXMOD];
+  for (int k = 0; k < ns; k++) {
+    for (int l = 0; l < nlimbs; l++) x[l] = c[(size_t)l * n + k];
+    re[k] = crt_centred(p, x, nlimbs) / delta;
+    for (int l = 0; l < nlimbs; l++) x[l] = c[(size_t)l * n + k + ns];
+    im[k] = crt_centred(p, x, nlimbs) / delta;
+  }
+  fft_special(p, re, im);
+  for (int k = 0; k < ns; k++) z[k] = re[k];
+  free(c); free(re); free(im);
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Secret key, rotation keys, encryption.   */
+/* ------------------------------------------------------------------------ */
+int or_secret_key(const or_params *p, int64_t *s_coeff, uint64_t *s_ntt) {
+  int n = p->n;
+  for (int j = 0; j < n; j++) s_coeff[j] = draw_ternary(p->seed, (uint32_t)j, 0, TAG_SECRET);
+  for (int l = 0; l <= p->L; l++) {
+    uint64_t *row = s_ntt + (size_t)l * n;
+    for (int j = 0; j < n; j++) row[j] = smod(s_coeff[j], p->mod[l]);
+    or_ntt_forward(p, l, row);
+  }
+  return OR_OK;
+}
+
+/* Hybrid key-switching key for sigma_g(s) -> s, alpha = 1 limb per digit,
+ * one special prime P (R11):  b_d = -a_d s + e_d + [l == d] (P mod q_d) s'. */
+int or_rotation_key(const or_params *p, const uint64_t *s_ntt, int64_t step, uint64_t *key) {
+  int n = p->n, L = p->L;
+  if (step <= 0 || step >= p->num_slots) return OR_E_ARG;
+  uint64_t g = or_galois_elt(p, step);
+  /* s' = sigma_g(s) from the coefficient-domain definition */
+  int64_t *s = malloc(sizeof(int64_t) * n), *sp = malloc(sizeof(int64_t) * n);
+  uint64_t *sp_ntt = malloc(sizeof(uint64_t) * n);
+  uint64_t *e_ntt = malloc(sizeof(uint64_t) * n);
+  for (int j = 0; j < n; j++) s[j] = draw_ternary(p->seed, (uint32_t)j, 0, TAG_SECRET);
+  or_automorph_coeff(p, g, s, sp);
+  for (int d = 0; d < L; d++) {
+    for (int l = 0; l <= L; l++) {
+      uint64_t m = p->mod[l];
+      for (int j = 0; j < n; j++) sp_ntt[j] = smod(sp[j], m);
+      or_ntt_forward(p, l, sp_ntt);
+      for (int j = 0; j < n; j++)
+        e_ntt[j] = smod(draw_cbd21(p->seed, (uint32_t)j, (uint32_t)step, TAG_KEY_E, (uint32_t)d), m);
+      or_ntt_forward(p, l, e_ntt);
+      uint64_t *kb = key + (((size_t)d * 2 + 0) * (L + 1) + l) * n;
+      uint64_t *ka = key + (((size_t)d * 2 + 1) * (L + 1) + l) * n;
+      uint64_t gad = (l == d) ? p->mod[L] % m : 0; /* (P mod q_d) on limb d only */
+      for (int j = 0; j < n; j++) {
+        uint64_t a = draw_uniform(p->seed, (uint32_t)j, (uint32_t)l, (uint32_t)step, TAG_KEY_A,
+                                  (uint32_t)d, m);
+        uint64_t b = submod(e_ntt[j], mulmod(a, s_ntt[(size_t)l * n + j], m), m);
+        b = addmod(b, mulmod(gad, sp_ntt[j], m), m);
+        ka[j] = a;
+        kb[j] = b;
+      }
+    }
+  }
+  free(s); free(sp); free(sp_ntt); free(e_ntt);
+  return OR_OK;
+}
+
+/* Symmetric encryption c = (-a s + e + pt, a). */
+int or_encrypt(const or_params *p, const uint64_t *s_ntt, const uint64_t *pt, int32_t nlimbs,
+               uint64_t enc_seed, uint64_t *ct) {
+  int n = p->n;
+  if (nlimbs < 1 || nlimbs > p->L) return OR_E_ARG;
+  uint64_t *e_ntt = malloc(sizeof(uint64_t) * n);
+  for (int l = 0; l < nlimbs; l++) {
+    uint64_t m = p->mod[l];
+    for (int j = 0; j < n; j++) e_ntt[j] = smod(draw_cbd21(enc_seed, (uint32_t)j, 0, TAG_ENC_E, 0), m);
+    or_ntt_forward(p, l, e_ntt);
+    uint64_t *c0 = ct + (size_t)l * n, *c1 = ct + ((size_t)nlimbs + l) * n;
+    for (int j = 0; j < n; j++) {
+      uint64_t a = draw_uniform(enc_seed, (uint32_t)j, (uint32_t)l, 0, TAG_ENC_A, 0, m);
+      uint64_t v = submod(e_ntt[j], mulmod(a, s_ntt[(size_t)l * n + j], m), m);
+      c0[j] = addmod(v, pt[(size_t)l * n + j], m);
+      c1[j] = a;
+    }
+  }
+  free(e_ntt);
+  return OR_OK;
+}
+
+int or_decrypt(const or_params *p, const uint64_t *s_ntt, const uint64_t *ct, int32_t nlimbs,
+               uint64_t *pt) {
+  int n = p->n;
+  for (int l = 0; l < nlimbs; l++) {
+    uint64_t m = p->mod[l];
+    const uint64_t *c0 = ct + (size_t)l * n, *c1 = ct + ((size_t)nlimbs + l) * n;
+    for (int j = 0; j < n; j++)
+      pt[(size_t)l * n + j] = addmod(c0[j], mulmod(c1[j], s_ntt[(size_t)l * n + j], m), m);
+  }
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Key switching (P:L479-496 hoisting; R11, R12).                            */
+/* ext modulus index e in [0, ell]: e < ell -> q_e, e == ell -> P = mod[L].   */
+/* ------------------------------------------------------------------------ */
+static int ext_mod_index(const or_params *p, int ell, int e) { return e < ell ? e : p->L; }
+
+/* ModUp ("EvalFastRotationPrecompute"): digit d = centred INTT of limb d,
+ * lifted into every other modulus of Q_ell u {P}, then NTT. */
+int or_modup(const or_params *p, const uint64_t *c1, int32_t ell, uint64_t *dig) {
+  int n = p->n;
+  if (ell < 1 || ell > p->L) return OR_E_ARG;
+  uint64_t *x = malloc(sizeof(uint64_t) * n);
+  for (int d = 0; d < ell; d++) {
+    uint64_t qd = p->mod[d];
+    memcpy(x, c1 + (size_t)d * n, sizeof(uint64_t) * n);
+    or_ntt_inverse(p, d, x);
+    for (int e = 0; e <= ell; e++) {
+      uint64_t *row = dig + ((size_t)d * (ell + 1) + e) * n;
+      int mi = ext_mod_index(p, ell, e);
+      if (e == d) {
+        memcpy(row, c1 + (size_t)d * n, sizeof(uint64_t) * n);
+        continue;
+      }
+      for (int j = 0; j < n; j++) row[j] = smod(centre(x[j], qd), p->mod[mi]);
+      or_ntt_forward(p, mi, row);
+    }
+  }
+  free(x);
+  return OR_OK;
+}
+
+/* ModDown: u'[q] = (u[q] - NTT_q([INTT_P(u[P])]_centred)) * P^{-1} mod q. */
+static void moddown(const or_params *p, uint64_t *u /* (ell+1) x n */, int ell, uint64_t *out) {
+  int n = p->n;
+  uint64_t P = p->mod[p->L];
+  uint64_t *y = malloc(sizeof(uint64_t) * n), *t = malloc(sizeof(uint64_t) * n);
+  memcpy(y, u + (size_t)ell * n, sizeof(uint64_t) * n);
+  or_ntt_inverse(p, p->L, y);
+  for (int l = 0; l < ell; l++) {
+    uint64_t q = p->mod[l];
+    for (int j = 0; j < n; j++) t[j] = smod(centre(y[j], P), q);
+    or_ntt_forward(p, l, t);
+    uint64_t pinv = invmod(P % q, q);
+    for (int j = 0; j < n; j++) out[(size_t)l * n + j] = mulmod(submod(u[(size_t)l * n + j], t[j], q), pinv, q);
+  }
+  free(y); free(t);
+}
+
+/* "EvalFastRotation": permute digits by pi_g in the NTT domain, key
+ * inner product over Q_ell u {P}, ModDown, add pi_g(c0). */
+int or_rotate_hoisted(const or_params *p, const uint64_t *ct, const uint64_t *dig, int32_t ell,
+                      const uint64_t *key, int64_t step, uint64_t *out) {
+  int n = p->n, L = p->L;
+  if (ell < 1 || ell > L) return OR_E_ARG;
+  uint64_t g = or_galois_elt(p, step);
+  uint64_t *u = calloc((size_t)2 * (ell + 1) * n, sizeof(uint64_t));
+  uint64_t *perm = malloc(sizeof(uint64_t) * n);
+  for (int d = 0; d < ell; d++) {
+    for (int e = 0; e <= ell; e++) {
+      int mi = ext_mod_index(p, ell, e);
+      uint64_t m = p->mod[mi];
+      or_automorph_ntt(p, g, dig + ((size_t)d * (ell + 1) + e) * n, perm);
+      for (int pp = 0; pp < 2; pp++) {
+        const uint64_t *k = key + (((size_t)d * 2 + pp) * (L + 1) + mi) * n;
+        uint64_t *acc = u + ((size_t)pp * (ell + 1) + e) * n;
+        for (int j = 0; j < n; j++) acc[j] = addmod(acc[j], mulmod(perm[j], k[j], m), m);
+      }
+    }
+  }
+  uint64_t *u0 = malloc(sizeof(uint64_t) * (size_t)ell * n), *u1 = malloc(sizeof(uint64_t) * (size_t)ell * n);
+  moddown(p, u, ell, u0);
+  moddown(p, u + (size_t)(ell + 1) * n, ell, u1);
+  for (int l = 0; l < ell; l++) {
+    uint64_t q = p->mod[l];
+    or_automorph_ntt(p, g, ct + (size_t)l * n, perm);
+    for (int j = 0; j < n; j++) {
+      out[(size_t)l * n + j] = addmod(perm[j], u0[(size_t)l * n + j], q);
+      out[((size_t)ell + l) * n + j] = u1[(size_t)l * n + j];
+    }
+  }
+  free(u); free(perm); free(u0); free(u1);
+  return OR_OK;
+}
+
+int or_rotate(const or_params *p, const uint64_t *ct, int32_t ell, const uint64_t *key,
+              int64_t step, uint64_t *out) {
+  int n = p->n;
+  uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)ell * (ell + 1) * n);
+  int rc = or_modup(p, ct + (size_t)ell * n, ell, dig);
+  if (rc == OR_OK) rc = or_rotate_hoisted(p, ct, dig, ell, key, step, out);
+  free(dig);
+  return rc;
+}
+
+/* Rescale: drop q_{ell-1} with the centred lift (R12). */
+int or_rescale(const or_params *p, const uint64_t *ct, int32_t ell, uint64_t *out) {
+  int n = p->n;
+  if (ell < 2 || ell > p->L) return OR_E_ARG;
+  uint64_t ql = p->mod[ell - 1];
+  uint64_t *y = malloc(sizeof(uint64_t) * n), *t = malloc(sizeof(uint64_t) * n);
+  for (int pp = 0; pp < 2; pp++) {
+    memcpy(y, ct + ((size_t)pp * ell + ell - 1) * n, sizeof(uint64_t) * n);
+    or_ntt_inverse(p, ell - 1, y);
+    for (int l = 0; l < ell - 1; l++) {
+      uint64_t q = p->mod[l];
+      for (int j = 0; j < n; j++) t[j] = smod(centre(y[j], ql), q);
+      or_ntt_forward(p, l, t);
+      uint64_t inv = invmod(ql % q, q);
+      const uint64_t *src = ct + ((size_t)pp * ell + l) * n;
+      uint64_t *dst = out + ((size_t)pp * (ell - 1) + l) * n;
+      for (int j = 0; j < n; j++) dst[j] = mulmod(submod(src[j], t[j], q), inv, q);
+    }
+  }
+  free(y); free(t);
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Enrollment (Alg. enroller_bsgs) and the query.        */
+/* ------------------------------------------------------------------------ */
+/* Step 1: L2 normalisation, sequential double sum (R16). */
+int or_normalize(const float *v, int32_t dim, double *u) {
+  double s = 0.0;
+  for (int i = 0; i < dim; i++) {
+    double x = (double)v[i];
+    s = s + x * x;
+  }
+  if (s == 0.0) return OR_E_ZERO_VECTOR;
+  double nrm = sqrt(s);
+  for (int i = 0; i < dim; i++) u[i] = (double)v[i] / nrm;
+  return OR_OK;
+}
+
+static int layout_check(const or_params *p, int32_t dim, int32_t n1) {
+  int ns = p->num_slots;
+  if (dim < 2 || n1 < 1) return OR_E_ARG;
+  if ((dim & (dim - 1)) != 0) return OR_E_LAYOUT; /* R19 */
+  int N = dim < ns ? dim : ns;
+  if (ns % (2 * N) != 0) return OR_E_LAYOUT;       /* M even (R19) */
+  return OR_OK;
+}
+
+/* Query slots: numSlots/N replicated copies, period N over ALL slots (R8). */
+int or_query_slots(const or_params *p, const float *q, int32_t dim, double *z) {
+  int rc = layout_check(p, dim, 1);
+  if (rc) return rc;
+  double *u = malloc(sizeof(double) * dim);
+  rc = or_normalize(q, dim, u);
+  if (rc == OR_OK)
+    for (int j = 0; j < p->num_slots; j++) z[j] = u[j % dim];
+  free(u);
+  return rc;
+}
+
+/* Step 1 for a slice of rows: U[r] = Normalize(vecs[r]). */
+int or_normalize_rows(const float *vecs, int64_t rows, int32_t dim, double *U) {
+  for (int64_t r = 0; r < rows; r++) {
+    int rc = or_normalize(vecs + (size_t)r * dim, dim, U + (size_t)r * dim);
+    if (rc) return rc;
+  }
+  return OR_OK;
+}
+
+/* Slot vector of aggregate `agg`, diagonal k: Steps 2-5 of Alg. enroller_bsgs,
+ * literally (temporary M-block plaintext of the pair, then the stride-2N
+ * A/B replication); aggregate = output ciphertext (R4).
+ * U holds the Step-1-normalised rows [u_first, u_first + u_count) of the
+ * database; a row the step needs outside that slice is an OR_E_ARG. */
+int or_enroll_slots(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                    int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, int32_t k,
+                    double *z) {
+  int rc = layout_check(p, dim, n1);
+  if (rc) return rc;
+  int ns = p->num_slots;
+  /* Step 2 */
+  int N = dim < ns ? dim : ns;
+  int M = ns / N;
+  /* Step 3 */
+  int64_t G = (num_vectors + N - 1) / N;
+  int64_t A = (2 * G + M - 1) / M;
+  if (agg < 0 || agg >= A || k < 0 || k >= N) return OR_E_ARG;
+  int64_t a = agg - (agg % 2); /* pair start: "for a = 0 to A-1 step 2" */
+  int64_t g0 = a * (M / 2);
+  int64_t g1 = g0 + M < G ? g0 + M : G;
+  int64_t W = g1 - g0;
+  /* giant-step index of diagonal k (floor, R3) */
+  int k_signed = k < N / 2 ? k : k - N;
+  int j = (int)floor((double)k_signed / (double)n1);
+  int shiftN = ((n1 * j) % N + N) % N;
+  double *tmp = calloc((size_t)ns, sizeof(double));
+  for (int64_t b = 0; b < W; b++) {
+    int64_t g = g0 + b, offset = b * N;
+    for (int t = 0; t < N; t++) {
+      int src = (t - shiftN + N) % N;
+      /* Step 4: diagonal_g[k][src] = group_g[src][(src + k) mod N],
+       * zero when row src of group g is beyond the database (|group_g| < N). */
+      int64_t v = g * N + src;
+      double val = 0.0;
+      if (v < num_vectors) {
+        if (v < u_first || v >= u_first + u_count) { free(tmp); return OR_E_ARG; }
+        val = U[(size_t)(v - u_first) * dim + (src + k) % N];
+      }
+      tmp[offset + t] = val;
+    }
+  }
+  /* replicate with stride 2N into plaintextA / plaintextB */
+  for (int i = 0; i < ns; i++) z[i] = 0.0;
+  for (int b = 0; b < M / 2; b++)
+    for (int t = 0; t < N; t++) {
+      if (agg == a) z[b * 2 * N + t] = tmp[b * N + t];
+      else z[b * 2 * N + t] = tmp[b * N + t + ns / 2];
+    }
+  free(tmp);
+  return OR_OK;
+}
+
+/* Diagonal plaintexts D[agg][k], k in [0, N): Encode at scale q_{L-1} over L
+ * limbs (pt mode, R1; encoding R15).  Dagg = N x pt(L). */
+int or_enroll_aggregate(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                        int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg,
+                        uint64_t *Dagg) {
+  int ns = p->num_slots;
+  int N = dim < ns ? dim : ns;
+  double *z = malloc(sizeof(double) * ns);
+  int rc = OR_OK;
+  for (int k = 0; k < N && rc == OR_OK; k++) {
+    rc = or_enroll_slots(p, U, u_first, u_count, num_vectors, dim, n1, agg, k, z);
+    if (rc == OR_OK)
+      rc = or_encode(p, z, (double)p->mod[p->L - 1], p->L, Dagg + (size_t)k * p->L * p->n);
+  }
+  free(z);
+  return rc;
+}
+
+/* ------------------------------------------------------------------------ */
+/* Scan (Alg. sender-bsgs).                                      */
+/* ------------------------------------------------------------------------ */
+static int floordiv(int a, int b) { return (int)floor((double)a / (double)b); }
+
+/* giantSteps (R6): j in [floor(-(N/2)/n1), floor((N/2-1)/n1)]. */
+int or_giant_range(int32_t N, int32_t n1, int32_t *j_min, int32_t *j_max) {
+  *j_min = floordiv(-(N / 2), n1);
+  *j_max = floordiv(N / 2 - 1, n1);
+  return OR_OK;
+}
+/* preRot = ((n1 j) mod N + N) mod N */
+int32_t or_pre_rot(int32_t N, int32_t n1, int32_t j) { return ((n1 * j) % N + N) % N; }
+
+/* Rotation-key set of the fold schedule (R2): baby {1..n1-1}, giant {preRot(j) != 0},
+ * fold {numSlots - N}; sorted ascending, unique. */
+int or_rotation_steps(const or_params *p, int32_t N, int32_t n1, int32_t *steps, int32_t cap,
+                      int32_t *count) {
+  int ns = p->num_slots;
+  char *used = calloc((size_t)ns, 1);
+  for (int i = 1; i < n1; i++) used[i % ns] = 1;
+  int jmin, jmax;
+  or_giant_range(N, n1, &jmin, &jmax);
+  for (int j = jmin; j <= jmax; j++) {
+    int s = or_pre_rot(N, n1, j);
+    if (s) used[s] = 1;
+  }
+  used[ns - N] = 1;
+  int c = 0;
+  for (int s = 1; s < ns; s++)
+    if (used[s]) {
+      if (c < cap) steps[c] = s;
+      c++;
+    }
+  free(used);
+  *count = c;
+  return c <= cap ? OR_OK : OR_E_ARG;
+}
+
+static const uint64_t *find_key(const or_params *p, const int32_t *steps, int32_t nkeys,
+                                const uint64_t *keys, int64_t step) {
+  size_t ksz = (size_t)p->L * 2 * (p->L + 1) * p->n;
+  for (int i = 0; i < nkeys; i++)
+    if (steps[i] == step) return keys + ksz * i;
+  return NULL;
+}
+
+/* Step 1: r[i] = Rot_i(ct) for i in [0, n1), hoisted. */
+int or_baby_steps(const or_params *p, const uint64_t *q_ct, int32_t n1, const int32_t *steps,
+                  int32_t nkeys, const uint64_t *keys, uint64_t *r) {
+  int n = p->n, L = p->L;
+  size_t ctsz = (size_t)2 * L * n;
+  uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)L * (L + 1) * n);
+  or_modup(p, q_ct + (size_t)L * n, L, dig); /* preV */
+  memcpy(r, q_ct, sizeof(uint64_t) * ctsz);  /* r[0] = ct */
+  int rc = OR_OK;
+  for (int i = 1; i < n1 && rc == OR_OK; i++) {
+    const uint64_t *key = find_key(p, steps, nkeys, keys, i);
+    if (!key) { rc = OR_E_MISSING_KEY; break; }
+    rc = or_rotate_hoisted(p, q_ct, dig, L, key, i, r + ctsz * i);
+  }
+  free(dig);
+  return rc;
+}
+
+/* Steps 2a-2b: S_j = sum_{i=i_lo}^{i_hi} r[i] (.) diagonal k(j,i). */
+int or_giant_sum(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
+                 const uint64_t *Dagg, int32_t j, uint64_t *S) {
+  int n = p->n, L = p->L;
+  size_t ctsz = (size_t)2 * L * n, ptsz = (size_t)L * n;
+  int i_lo = 0 > -j * n1 - N / 2 ? 0 : -j * n1 - N / 2;
+  int i_hi = n1 - 1 < N / 2 - 1 - j * n1 ? n1 - 1 : N / 2 - 1 - j * n1;
+  memset(S, 0, sizeof(uint64_t) * ctsz);
+  if (i_lo > i_hi) return OR_E_RANGE; /* skipped giant step */
+  for (int i = i_lo; i <= i_hi; i++) {
+    int k_signed = j * n1 + i;
+    int k = ((k_signed % N) + N) % N;
+    const uint64_t *diag = Dagg + ptsz * k;
+    for (int pp = 0; pp < 2; pp++)
+      for (int l = 0; l < L; l++) {
+        uint64_t q = p->mod[l];
+        const uint64_t *ri = r + ctsz * i + ((size_t)pp * L + l) * n;
+        uint64_t *acc = S + ((size_t)pp * L + l) * n;
+        const uint64_t *dl = diag + (size_t)l * n;
+        for (int t = 0; t < n; t++) acc[t] = addmod(acc[t], mulmod(ri[t], dl[t], q), q);
+      }
+  }
+  return OR_OK;
+}
+
+/* One aggregate: steps 2a-2f with the fold reading (R2):
+ * y = sum_j Rot_{preRot(j)}(Rescale(S_j)); out = y + Rot_{numSlots-N}(y). */
+int or_scan_aggregate(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
+                      const uint64_t *Dagg, const int32_t *steps, int32_t nkeys,
+                      const uint64_t *keys, uint64_t *out, uint64_t *y_out) {
+  int n = p->n, L = p->L, ell = L - 1;
+  size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * ell * n;
+  uint64_t *S = malloc(sizeof(uint64_t) * ctL), *Sp = malloc(sizeof(uint64_t) * ct1);
+  uint64_t *T = malloc(sizeof(uint64_t) * ct1), *y = calloc(ct1, sizeof(uint64_t));
+  int jmin, jmax, rc = OR_OK;
+  or_giant_range(N, n1, &jmin, &jmax);
+  for (int j = jmin; j <= jmax && rc == OR_OK; j++) {
+    if (or_giant_sum(p, r, n1, N, Dagg, j, S) != OR_OK) continue; /* empty range */
+    or_rescale(p, S, L, Sp);                                      /* Step 2c */
+    int s = or_pre_rot(N, n1, j);                                 /* Step 2d */
+    if (s != 0) {
+      const uint64_t *key = find_key(p, steps, nkeys, keys, s);
+      if (!key) { rc = OR_E_MISSING_KEY; break; }
+      or_rotate(p, Sp, ell, key, s, T);
+    } else {
+      memcpy(T, Sp, sizeof(uint64_t) * ct1);
+    }
+    for (int pp = 0; pp < 2; pp++) /* Step 2e */
+      for (int l = 0; l < ell; l++)
+        for (int t = 0; t < n; t++) {
+          size_t o = ((size_t)pp * ell + l) * n + t;
+          y[o] = addmod(y[o], T[o], p->mod[l]);
+        }
+  }
+  if (rc == OR_OK) {
+    int fold = p->num_slots - N; /* Rot_{-N} (R2, App. A.4 of SURVEY) */
+    const uint64_t *key = find_key(p, steps, nkeys, keys, fold);
+    if (!key) rc = OR_E_MISSING_KEY;
+    else {
+      or_rotate(p, y, ell, key, fold, T);
+      for (int pp = 0; pp < 2; pp++)
+        for (int l = 0; l < ell; l++)
+          for (int t = 0; t < n; t++) {
+            size_t o = ((size_t)pp * ell + l) * n + t;
+            out[o] = addmod(y[o], T[o], p->mod[l]);
+          }
+      if (y_out) memcpy(y_out, y, sizeof(uint64_t) * ct1);
+    }
+  }
+  free(S); free(Sp); free(T); free(y);
+  return rc;
+}
+
+/* Decrypt + decode out_agg and read vector scores (R4):
+ * score(v) = slot (floor(v/N) mod M/2) * 2N + (v mod N). */
+int or_decrypt_scores(const or_params *p, const uint64_t *s_ntt, const uint64_t *out_ct,
+                      int32_t N, int64_t agg, int64_t num_vectors, double *scores) {
+  int n = p->n, ell = p->L - 1, ns = p->num_slots, M = ns / N;
+  uint64_t *pt = malloc(sizeof(uint64_t) * (size_t)ell * n);
+  double *z = malloc(sizeof(double) * ns);
+  or_decrypt(p, s_ntt, out_ct, ell, pt);
+  or_decode(p, pt, ell, ldexp(1.0, p->scale_bits), z);
+  for (int b = 0; b < M / 2; b++)
+    for (int t = 0; t < N; t++) {
+      int64_t v = (agg * (M / 2) + b) * N + t;
+      scores[(size_t)b * N + t] = v < num_vectors ? z[b * 2 * N + t] : 0.0;
+    }
+  free(pt); free(z);
+  return OR_OK;
+}

@@ -1,0 +1,133 @@
+/*
+ * oracle/hd_oracle.h -- CPU ORACLE for the encrypted BSGS similarity scan of
+ * arXiv 2604.00546 ("Lightweight, Practical Encrypted Face Recognition with GPU
+ * Support").
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference leg may load, call or link anything under
+ * oracle/.  The product path (paper_2604_00546_b200/, include/hd.h) shares no
+ * code, header, table or constant generator with this file and never calls it.
+ *
+ * Plain, slow, obviously-correct C: every modular product is
+ * (unsigned __int128)a*b % m, every step follows the paper's algorithm (or the
+ * plain definition of the operation) in the paper's order.  Citations:
+ * "P:Lxxx" = /root/reference/PAPER.md line, "S:Lxxx" = SPEC.md line; readings
+ * where the paper is silent are listed in DESIGN.md section 3 ("R#").
+ *
+ * Layouts (all arrays row-major, little-endian u64 residues in [0, m)):
+ *   polynomial limb ..... n coefficients; NTT form = bit-reversed evaluation
+ *                          order  a^[i] = sum_j a_j psi^{(2 br(i)+1) j}   (R13)
+ *   plaintext (ell limbs) [limb][n]
+ *   ciphertext (ell) .... [poly 0..1][limb][n]
+ *   rotation key ........ [digit d < L][poly (0=b,1=a)][modulus l <= L][n]
+ *                          modulus index L is the special prime P.
+ *   modup digits (ell) .. [digit d < ell][ext modulus e <= ell][n]
+ *                          ext index e < ell is q_e, e == ell is P.
+ *
+ * Every function returns 0 on success or a negative error code:
+ */
+#ifndef HD_ORACLE_H
+#define HD_ORACLE_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OR_OK 0
+#define OR_E_ARG (-1)
+#define OR_E_PARAMS (-2)
+#define OR_E_LAYOUT (-3)
+#define OR_E_ZERO_VECTOR (-4)
+#define OR_E_MISSING_KEY (-5)
+#define OR_E_RANGE (-6)
+
+#define OR_MAXMOD 8
+
+typedef struct {
+  int32_t log_n;      /* ring degree n = 2^log_n                         */
+  int32_t n;
+  int32_t num_slots;  /* n/2  ("packs N/2 complex values")    */
+  int32_t L;          /* ciphertext limbs q_0..q_{L-1} at the MAC (R5)   */
+  int32_t q0_bits;    /* 60                                              */
+  int32_t scale_bits; /* 45  ("scaling factor is set to 45")     */
+  int32_t special_bits; /* 60 */
+  int32_t pad_;
+  uint64_t mod[OR_MAXMOD]; /* mod[0..L-1] = q_i, mod[L] = P              */
+  uint64_t psi[OR_MAXMOD]; /* smallest primitive 2n-th root of unity      */
+  uint64_t seed;           /* Philox key for the secret / rotation keys   */
+} or_params;
+
+int or_params_init(or_params *p, int32_t log_n, int32_t L, uint64_t seed);
+int or_is_prime(uint64_t x);
+
+/* NTT over modulus index l (0..L); fast (textbook CT / GS) and definitional. */
+int or_ntt_forward(const or_params *p, int32_t l, uint64_t *a);
+int or_ntt_inverse(const or_params *p, int32_t l, uint64_t *a);
+int or_ntt_definition(const or_params *p, int32_t l, const uint64_t *a, uint64_t *out);
+int or_negacyclic_schoolbook(const uint64_t *a, const uint64_t *b, int32_t n, uint64_t m,
+                             uint64_t *out);
+
+/* Philox4x32-10 (Random123) and the pinned draws (R14). */
+void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+
+/* Galois machinery (R7): g = 5^r mod 2n; NTT-domain index permutation. */
+uint64_t or_galois_elt(const or_params *p, int64_t step);
+int or_automorph_coeff(const or_params *p, uint64_t g, const int64_t *a, int64_t *out);
+int or_automorph_ntt(const or_params *p, uint64_t g, const uint64_t *a, uint64_t *out);
+
+/* CKKS encode / decode (R15) over `nlimbs` leading q moduli. */
+int or_encode(const or_params *p, const double *z, double delta, int32_t nlimbs, uint64_t *pt);
+int or_encode_coeffs(const or_params *p, const double *z, double delta, int64_t *coef);
+int or_decode(const or_params *p, const uint64_t *pt, int32_t nlimbs, double delta, double *z);
+
+/* Keys and encryption (R11, R14). */
+int or_secret_key(const or_params *p, int64_t *s_coeff, uint64_t *s_ntt /* (L+1) x n */);
+int or_rotation_key(const or_params *p, const uint64_t *s_ntt, int64_t step, uint64_t *key);
+int or_encrypt(const or_params *p, const uint64_t *s_ntt, const uint64_t *pt, int32_t nlimbs,
+               uint64_t enc_seed, uint64_t *ct);
+int or_decrypt(const or_params *p, const uint64_t *s_ntt, const uint64_t *ct, int32_t nlimbs,
+               uint64_t *pt);
+
+/* Key switching pieces (R11, R12) at ciphertext level `ell` (limbs q_0..q_{ell-1}). */
+int or_modup(const or_params *p, const uint64_t *c1, int32_t ell, uint64_t *dig);
+int or_rotate_hoisted(const or_params *p, const uint64_t *ct, const uint64_t *dig, int32_t ell,
+                      const uint64_t *key, int64_t step, uint64_t *out);
+int or_rotate(const or_params *p, const uint64_t *ct, int32_t ell, const uint64_t *key,
+              int64_t step, uint64_t *out);
+int or_rescale(const or_params *p, const uint64_t *ct, int32_t ell, uint64_t *out);
+
+/* Enrollment (Alg. enroller_bsgs) and query slot layout (R8). */
+int or_normalize(const float *v, int32_t dim, double *u);
+int or_query_slots(const or_params *p, const float *q, int32_t dim, double *z);
+int or_normalize_rows(const float *vecs, int64_t rows, int32_t dim, double *U);
+int or_enroll_slots(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                    int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, int32_t k,
+                    double *z);
+int or_enroll_aggregate(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                        int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg,
+                        uint64_t *Dagg /* N x pt(L) */);
+
+/* Scan layout helpers (R6) */
+int or_giant_range(int32_t N, int32_t n1, int32_t *j_min, int32_t *j_max);
+int32_t or_pre_rot(int32_t N, int32_t n1, int32_t j);
+int or_rotation_steps(const or_params *p, int32_t N, int32_t n1, int32_t *steps, int32_t cap,
+                      int32_t *count);
+
+/* Scan (Alg. sender-bsgs; fold reading R2). */
+int or_baby_steps(const or_params *p, const uint64_t *q_ct, int32_t n1, const int32_t *steps,
+                  int32_t nkeys, const uint64_t *keys, uint64_t *r /* n1 x ct(L) */);
+int or_giant_sum(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
+                 const uint64_t *Dagg /* N x pt(L) */, int32_t j, uint64_t *S /* ct(L) */);
+int or_scan_aggregate(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
+                      const uint64_t *Dagg, const int32_t *steps, int32_t nkeys,
+                      const uint64_t *keys, uint64_t *out /* ct(L-1) */,
+                      uint64_t *y_out /* optional ct(L-1): sum before the fold */);
+
+/* Decrypt + decode one output ciphertext and read the scores of its vectors (R4). */
+int or_decrypt_scores(const or_params *p, const uint64_t *s_ntt, const uint64_t *out_ct,
+                      int32_t N, int64_t agg, int64_t num_vectors, double *scores /* M/2*N */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,93 @@
+"""End-to-end pins of the oracle's encrypted scan (not gpu).
+
+(1) the numpy plaintext-slot shadow of the schedule equals brute-force cosine
+    (<= 1e-12): pins the layout + schedule readings R2-R8;
+(2) the oracle's enrollment slot vectors equal the shadow's;
+(3) decrypted encrypted scores equal brute-force cosine within the
+    north-star tolerance 1e-3 (expected ~1e-8, SURVEY c.3 noise budget) and
+    the planted matches are the top scores;
+(4) special case n1 = N: every preRot is 0 (the plain diagonal method,
+    Eq. equ:diag P:L334-336).
+"""
+import numpy as np
+import pytest
+
+from synth_inputs import CONFIGS, make_dataset
+from tests._shadow import scores_from_slots, shadow_enroll, shadow_scan
+
+D45 = 2.0 ** 45
+
+
+def _cos(db, q):
+    d = db.astype(np.float64)
+    qq = q.astype(np.float64)
+    return d @ qq / (np.linalg.norm(d, axis=1) * np.linalg.norm(qq))
+
+
+@pytest.mark.parametrize("ns,N,K,n1", [(1024, 64, 256, 8), (1024, 64, 256, 23), (256, 16, 100, 4),
+                                        (128, 8, 64, 2), (128, 8, 40, 2), (512, 32, 320, 8)])
+def test_shadow_schedule_equals_cosine(ns, N, K, n1):
+    rng = np.random.default_rng(K + n1)
+    db = rng.integers(-99, 100, size=(K, N)).astype(np.float32)
+    q = rng.integers(-99, 100, size=N).astype(np.float32)
+    U = db.astype(np.float64) / np.linalg.norm(db.astype(np.float64), axis=1, keepdims=True)
+    u = q.astype(np.float64) / np.linalg.norm(q.astype(np.float64))
+    M = ns // N
+    A = -(-2 * (-(-K // N)) // M)
+    got = np.concatenate([scores_from_slots(shadow_scan(U, u, N, ns, n1, a), N, ns, a, K) for a in range(A)])
+    assert np.abs(got - _cos(db, q)).max() < 1e-12
+
+
+def test_oracle_layout_equals_shadow(oracle_mod):
+    o = oracle_mod.Oracle(9, 3)   # ns = 256
+    rng = np.random.default_rng(12)
+    K, N, n1 = 136, 16, 4         # G = 9, A = 2 with a partial second aggregate
+    db = rng.integers(-99, 100, size=(K, N)).astype(np.float32)
+    U = o.normalize_rows(db)
+    for a in range(2):
+        for k in range(N):
+            assert (o.enroll_slots(U, 0, K, n1, a, k) == shadow_enroll(U, N, o.ns, n1, a, k)).all()
+
+
+def _run_encrypted(o, db, q, N, n1, enc_seed=1000):
+    K = db.shape[0]
+    s, s_ntt = o.secret_key()
+    steps, keys = o.keyset(s_ntt, o.rotation_steps(N, n1))
+    qct = o.encrypt(s_ntt, o.encode(o.query_slots(q), D45, o.L), enc_seed)
+    r = o.baby_steps(qct, n1, steps, keys)
+    U = o.normalize_rows(db)
+    M = o.ns // N
+    A = -(-2 * (-(-K // N)) // M)
+    scores = []
+    for a in range(A):
+        D = o.enroll_aggregate(U, 0, K, n1, a)
+        out = o.scan_aggregate(r, n1, N, D, steps, keys)
+        sc = o.decrypt_scores(s_ntt, out, N, a, K)
+        nv = min(K - a * (M // 2) * N, (M // 2) * N)
+        scores.append(sc[:nv])
+    return np.concatenate(scores)
+
+
+def test_toy_config_scores(oracle_mod):
+    cfg = CONFIGS["C1"]
+    o = oracle_mod.Oracle(cfg.log_n, cfg.limbs, seed=1)
+    db, q, pos = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    sc = _run_encrypted(o, db, q, cfg.dim, cfg.n1)
+    err = np.abs(sc - _cos(db, q)).max()
+    assert err < 1e-3          # north-star tolerance
+    assert err < 1e-6          # noise budget (SURVEY c.3): a 1e-3 error would be a bug
+    assert sorted(np.argsort(-sc)[:len(pos)]) == sorted(pos.tolist())
+
+
+def test_multi_aggregate_partial_and_n1_equals_N(oracle_mod):
+    o = oracle_mod.Oracle(8, 3, seed=3)     # ns = 128, N = 8 -> M = 16, 8 groups per ct
+    rng = np.random.default_rng(13)
+    K, N = 150, 8                            # G = 19 -> A = 3, last aggregate partial
+    db = rng.integers(-99, 100, size=(K, N)).astype(np.float32)
+    q = rng.integers(-99, 100, size=N).astype(np.float32)
+    for n1 in (2, 3, N):
+        if n1 == N:
+            jmin, jmax = o.giant_range(N, n1)
+            assert all(o.pre_rot(N, n1, j) == 0 for j in range(jmin, jmax + 1))
+        sc = _run_encrypted(o, db, q, N, n1, enc_seed=7)
+        assert np.abs(sc - _cos(db, q)).max() < 1e-6
