@@ -1,0 +1,373 @@
+#!/usr/bin/env python
+"""bench.py -- encrypted BSGS similarity scan on B200 (arXiv 2604.00546).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+
+A "step" is one pass of the whole hot path for one encrypted
+query over the whole database: hoisted baby steps, the diagonal MAC over every
+aggregate, rescale, giant rotations, fold.  Default workload (N = 1): BASELINE.json's
+north-star configuration "ring 2^16, VECTOR_DIM = 512, 2^20 db vectors" (C4, n1 = 64,
+all 64 aggregates on one B200; 51.5 GB of diagonal plaintexts, larger than L2, so no
+L2 flush is needed between steps).  Under torchrun (N > 1) the database is sharded by
+aggregate (strong scaling: the 2^20 database is fixed); rank 0 broadcasts the query
+ciphertext and gathers the score ciphertexts over NCCL inside every timed step.
+
+Prints ONE JSON line on rank 0.  ``--impl reference`` times the CPU oracle (oracle/,
+plain C) on a bounded sample of the same workload (there is no reference code).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth_inputs import CONFIGS, ENC_SEED_BASE, dataset_rows, make_dataset  # noqa: E402
+
+METRIC = "encrypted queries/sec (2^20 x 512 database scan)"
+UNIT = "queries/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C4")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:  # noqa: BLE001
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cfg_dict(cfg, world, scaling_note):
+    return {"workload": f"{cfg.name}: ring 2^{cfg.log_n}, VECTOR_DIM={cfg.dim}, {cfg.num_vectors} db vectors, "
+                        f"n1={cfg.n1}, L={cfg.limbs} RNS limbs + 1 special prime",
+            "ring": 1 << cfg.log_n, "vector_dim": cfg.dim, "db_vectors": cfg.num_vectors, "n1": cfg.n1,
+            "limbs": cfg.limbs, "aggregates": cfg.aggregates, "parallelism": f"aggregate-shard x{world}",
+            "l2": "inputs > L2 (diagonal stream 51.5 GB at C4); no flush needed" if cfg.log_n >= 16 else
+                  "inputs > L2", "scaling_note": scaling_note}
+
+
+# --------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference): bounded sample, extrapolated
+# --------------------------------------------------------------------------------------------
+def oracle_sample(cfg, rng_seed=0):
+    """Time one sample of the oracle on uniform random residues of the C4 shapes:
+    one hoisted baby rotation, one giant-step MAC sum, one rescale, one giant rotation.
+    Per-query time = ModUp + (n1-1) t_baby + A (n_g (t_mac + t_rs) + (nnz+1) t_rot)."""
+    import oracle
+    o = oracle.Oracle(cfg.log_n, cfg.limbs, seed=1)
+    rng = np.random.default_rng(rng_seed)
+    n, L = o.n, o.L
+    mods = o.p.moduli
+
+    def rand(shape, lim):
+        return np.stack([rng.integers(0, m, size=shape[1:], dtype=np.uint64) for m in lim], axis=0)
+
+    N, n1 = cfg.dim, cfg.n1
+    jmin, jmax = o.giant_range(N, n1)
+    nj = jmax - jmin + 1
+    nnz = sum(1 for j in range(jmin, jmax + 1) if o.pre_rot(N, n1, j))
+    key = np.ascontiguousarray(np.stack([np.stack([rand((L + 1, n), mods) for _ in range(2)]) for _ in range(L)]))
+    q = np.ascontiguousarray(np.stack([rand((L, n), mods[:L]) for _ in range(2)]))
+    t0 = time.perf_counter()
+    dig = o.modup(np.ascontiguousarray(q[1]))
+    t_modup = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    o.rotate_hoisted(q, dig, key, 1)
+    t_baby = time.perf_counter() - t0
+    r = np.ascontiguousarray(np.stack([rand((L, n), mods[:L]) for _ in range(2 * n1)]).reshape(n1, 2, L, n))
+    D = np.zeros((N, L, n), np.uint64)
+    for k in set(((0 * n1 + i) % N) for i in range(n1)):
+        D[k] = rand((L, n), mods[:L])
+    t0 = time.perf_counter()
+    S = o.giant_sum(r, n1, N, D, 0)
+    t_mac = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Sp = o.rescale(S)
+    t_rs = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    o.rotate(Sp, key, 7)
+    t_rot = time.perf_counter() - t0
+    per_query = t_modup + (n1 - 1) * t_baby + cfg.aggregates * (nj * (t_mac + t_rs) + (nnz + 1) * t_rot)
+    sample_s = t_modup + t_baby + t_mac + t_rs + t_rot
+    return per_query, sample_s
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    times, samples = [], []
+    for i in range(args.warmup + args.steps):
+        pq, ss = oracle_sample(cfg, i)
+        if i >= args.warmup:
+            times.append(pq)
+            samples.append(ss)
+    pq = statistics.mean(times)
+    v = 1.0 / pq
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": pq * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64 (RNS residues)", "data": "synthetic",
+            "config": cfg_dict(cfg, 1, "CPU oracle, single thread"),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                             "sample": "per step: oracle ModUp + 1 hoisted baby rotation + 1 giant-step MAC sum + "
+                                       "1 rescale + 1 giant rotation at the workload's shapes on uniform random "
+                                       "residues (~%.1f s of CPU), extrapolated to the whole query" %
+                                       statistics.mean(samples)},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------------------
+# clocks
+# --------------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# --------------------------------------------------------------------------------------------
+# our arm
+# --------------------------------------------------------------------------------------------
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_00546_b200 as hd
+    from paper_2604_00546_b200 import dist as hdd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    stream = torch.cuda.current_stream()
+    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1, device=local, stream=stream)
+    A = cfg.aggregates
+    a0, a1 = hdd.shard_range(A, rank, world)
+    per = (cfg.num_slots // cfg.dim // 2) * cfg.dim
+    # ---- setup (untimed): keys on rank 0 -> NCCL broadcast; local enrollment of this shard ----
+    _, q, _ = make_dataset(16, cfg.dim, cfg.data_seed)  # query only (rows drawn per shard below)
+    steps = ctx.rotation_steps(cfg.dim, cfg.n1)
+    if rank == 0:
+        sk, evk = ctx.keygen(steps)
+    if world > 1:
+        kb = torch.from_numpy(ctx.eval_keys_export(evk)).to(dev) if rank == 0 else None
+        nbytes = torch.tensor([kb.numel() if rank == 0 else 0], device=dev)
+        dist.broadcast(nbytes, 0)
+        kb = hdd.broadcast_bytes(kb, int(nbytes.item()), dev)
+        if rank != 0:
+            evk = ctx.eval_keys_import(kb.cpu().numpy())
+        del kb
+    v0, v1 = hdd.rows_of_aggregates(a0, a1, per, cfg.num_vectors)
+    rows = dataset_rows(cfg.num_vectors, cfg.dim, cfg.data_seed, v0, v1)
+    db = enroll_rows(hd, ctx, rows, v0, cfg, a0, a1)
+    del rows
+    # ---- the query: encrypted on rank 0, exported into a device buffer (NCCL-broadcast each step) ----
+    ct_bytes = 0
+    if rank == 0:
+        qct = ctx.encrypt_query(sk, q, ENC_SEED_BASE)
+        ct_bytes = ctx.ciphertext_export_size(qct)
+    nb = torch.tensor([ct_bytes], device=dev)
+    if world > 1:
+        dist.broadcast(nb, 0)
+    ct_bytes = int(nb.item())
+    qbuf = torch.empty(ct_bytes, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        ctx.ciphertext_export(qct, (qbuf.data_ptr(), ct_bytes), on_device=True)
+    if world > 1:
+        dist.broadcast(qbuf, 0)
+        torch.cuda.synchronize()
+        if rank != 0:
+            qct = ctx.ciphertext_import(qbuf.data_ptr(), ct_bytes, on_device=True)  # setup-time allocation
+    torch.cuda.synchronize()
+    nloc = a1 - a0
+    outs = None
+    out_ct_bytes = None
+    gbuf = None
+
+    def step():
+        nonlocal outs, out_ct_bytes, gbuf
+        if world > 1:  # a1: query broadcast over NCCL, imported in place (no allocation)
+            dist.broadcast(qbuf, 0)
+            if rank != 0:
+                ctx.ciphertext_import_into(qct, qbuf.data_ptr(), ct_bytes, on_device=True)
+        outs = ctx.query(evk, db, qct, outs)
+        if world > 1:  # a9: score ciphertexts gathered to rank 0 over NCCL
+            if out_ct_bytes is None:
+                out_ct_bytes = ctx.ciphertext_export_size(outs[0])
+                gbuf = torch.empty(nloc * out_ct_bytes, dtype=torch.uint8, device=dev)
+            for i, o in enumerate(outs):
+                ctx.ciphertext_export(o, (gbuf.data_ptr() + i * out_ct_bytes, out_ct_bytes), on_device=True)
+            hdd.gather_bytes(gbuf, ((A + world - 1) // world) * out_ct_bytes, 0)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    launches0 = ctx.launch_count()
+    clk = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ctx.query_stats()  # resets the per-query phase-event ring before the timed region
+    clk.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    # per-phase CUDA-event times recorded on the context stream during the timed steps (avg)
+    phase = ctx.query_stats() * args.steps
+    mac_ms = [phase[1] / args.steps]
+    launches = (ctx.launch_count() - launches0) // args.steps
+    t_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t_ms = hdd.max_over_ranks(t_ms, dev)
+    ms_per_step = t_ms / args.steps
+    value = args.steps / (t_ms / 1e3)
+    # ---- e2e through the public API with host buffers: H2D query, scan, D2H of every output ----
+    e2e = None
+    if world == 1:
+        host_q = torch.from_numpy(ctx.ciphertext_export(qct)).pin_memory()
+        ob = ctx.ciphertext_export_size(outs[0])
+        host_out = torch.empty(nloc * ob, dtype=torch.uint8).pin_memory()
+        qin = ctx.ciphertext_import(host_q.numpy())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            ctx.ciphertext_import_into(qin, host_q.data_ptr(), host_q.numel(), on_device=False)
+            outs = ctx.query(evk, db, qin, outs)
+            for i, o in enumerate(outs):
+                ctx.ciphertext_export(o, (host_out.data_ptr() + i * ob, ob), on_device=False)
+        torch.cuda.synchronize()
+        t_e2e = time.perf_counter() - t0
+        e2e = {"value": args.e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(host_q.numel()),
+               "d2h_bytes_per_step": int(nloc * ob), "steps": args.e2e_steps,
+               "api": "hd_ciphertext_import_into(host) -> hd_query -> hd_ciphertext_export(host) x A"}
+    # ---- roofline of the dominant kernel (MAC, HBM-bound) ----
+    L, n, N = cfg.limbs, 1 << cfg.log_n, cfg.dim
+    nj = len(db_js(cfg))
+    mac_bytes = nloc * N * L * n * 8 + cfg.n1 * 2 * L * n * 8 + nloc * nj * 2 * L * n * 8
+    mac_avg_ms = statistics.mean(mac_ms)
+    peak, peak_src = peaks()
+    achieved = mac_bytes / (mac_avg_ms / 1e3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "mac_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(cfg.name)
+        except Exception:  # noqa: BLE001
+            traffic = None
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u64 (RNS residues, 64-bit modular integer arithmetic)",
+            "data": "synthetic (P:L2175-2179 generator, seeded)",
+            "config": cfg_dict(cfg, world, "fixed 2^20 database sharded by aggregate"),
+            "phase_ms": {"baby": phase[0] / args.steps, "mac": phase[1] / args.steps,
+                         "rescale": phase[2] / args.steps, "giant": phase[3] / args.steps,
+                         "fold": phase[4] / args.steps},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": "mac_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": mac_bytes, "avg_launch_ms": mac_avg_ms},
+            "clocks": clocks, "e2e": e2e}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import multiprocessing
+        pq, ss = oracle_sample(cfg)
+        line["cpu_baseline"] = {"value": 1.0 / pq, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "host_cores_available": multiprocessing.cpu_count(),
+                                "sample": "oracle ModUp + 1 hoisted baby rotation + 1 giant-step MAC sum + 1 rescale "
+                                          "+ 1 giant rotation at the workload's shapes on uniform random residues "
+                                          f"({ss:.1f} s of CPU), extrapolated to one whole query"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def db_js(cfg):
+    N, n1 = cfg.dim, cfg.n1
+    return list(range((-(N // 2)) // n1, (N // 2 - 1) // n1 + 1))
+
+
+def enroll_rows(hd, ctx, rows, v0, cfg, a0, a1):
+    """hd_enroll reads rows [a0*per, a1*per) of the array it is given (indexed from vector 0):
+    pass a pointer shifted back by v0 rows so this rank only materialises its own shard."""
+    import ctypes as C
+    out = C.c_void_p()
+    ptr = rows.ctypes.data - v0 * cfg.dim * 4
+    hd._check("hd_enroll", hd.load().hd_enroll(ctx.h, C.c_void_p(ptr), cfg.num_vectors, cfg.dim, cfg.n1, a0, a1,
+                                               C.byref(out)))
+    return hd.Database(out.value, ctx)
+
+
+if __name__ == "__main__":
+    main()

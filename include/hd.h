@@ -1,0 +1,197 @@
+/*
+ * include/hd.h -- C ABI of the B200-native encrypted BSGS similarity scan
+ * (arXiv 2604.00546, "Lightweight, Practical Encrypted Face Recognition with GPU
+ * Support").  Implemented by libhd.so (paper_2604_00546_b200/csrc, CUDA sm_100a).
+ *
+ * The calls follow the paper's problem statement (P = /root/reference/PAPER.md):
+ *   - the client holds the secret key, generates rotation keys and encrypts the
+ *     query                -> hd_keygen, hd_encrypt_query
+ *   - the enroller normalises, diagonalises, packs and encodes the database
+ *     (Alg. enroller_bsgs)                -> hd_enroll
+ *   - the server evaluates the BSGS scan (Alg. sender-bsgs)
+ *                                                     -> hd_query
+ *   - the client decrypts and reads the scores (reading R4 of DESIGN.md)
+ *                                                     -> hd_decrypt_scores
+ *
+ * Conventions
+ *   - Every function returns hd_status (HD_OK = 0).  No C++ exception crosses the
+ *     ABI.  A human-readable detail of the last failure of the calling thread is
+ *     in hd_last_error() (e.g. "missing rotation key for step 489").
+ *   - Ownership: every handle returned through an `out` pointer belongs to the
+ *     caller and is released by the matching *_destroy (NULL-safe).  Host input
+ *     arrays are read-only and never retained.  Output arrays are caller-owned
+ *     with an explicit capacity; too small -> HD_E_INVALID_ARG.  On error, out
+ *     handles are left NULL (no partial results).
+ *   - Device: one hd_context is bound to one CUDA device and one CUDA stream (the
+ *     caller's, e.g. torch.cuda.current_stream().cuda_stream; NULL = the legacy
+ *     default stream).  Calls on one context must be serialised by the caller.
+ *     All device memory of a context, its keys, databases and ciphertexts is
+ *     allocated at creation time of those objects (never inside hd_query).
+ *   - Residues: u64 in [0, q), NTT form (bit-reversed evaluation order, DESIGN.md
+ *     R13).  Ciphertext layout [poly 0..1][limb][coef]; plaintext [limb][coef];
+ *     rotation key [digit d < L][poly (0 = b, 1 = a)][modulus l <= L][coef]
+ *     where modulus index L is the special prime P.
+ *   - No CPU fallback: if no CUDA device is usable every call that computes
+ *     returns HD_E_CUDA.
+ */
+#ifndef HD_H
+#define HD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HD_OK = 0,
+  HD_E_INVALID_ARG = -1, /* NULL pointer, bad size or capacity              */
+  HD_E_PARAMS = -2,      /* unsupported ring / limb profile                 */
+  HD_E_LAYOUT = -3,      /* vector_dim not a power of two or numSlots % 2N  */
+  HD_E_ZERO_VECTOR = -4, /* an all-zero database or query vector (R17)      */
+  HD_E_MISSING_KEY = -5, /* rotation key absent; hd_last_error names it     */
+  HD_E_LEVEL = -6,       /* ciphertext at the wrong number of limbs         */
+  HD_E_CAPACITY = -7,    /* database / workspace exceeds device memory      */
+  HD_E_CUDA = -8,        /* CUDA error or no device                         */
+  HD_E_STATE = -9,       /* object from another context / not initialised   */
+  HD_E_FORMAT = -10      /* bad serialised header                           */
+} hd_status;
+
+const char *hd_status_string(hd_status s);
+const char *hd_last_error(void);
+
+typedef struct hd_context hd_context;       /* params + tables, one device      */
+typedef struct hd_secret_key hd_secret_key; /* client only                      */
+typedef struct hd_eval_keys hd_eval_keys;   /* rotation keys, device-resident   */
+typedef struct hd_database hd_database;     /* diagonal plaintexts of [agg_begin, agg_end) */
+typedef struct hd_ciphertext hd_ciphertext; /* device-resident ciphertext       */
+
+/* CKKS parameters (R5, R11).  Defaults (when a field is 0): num_limbs 3,
+ * q0_bits 60, scale_bits 45, special_bits 60, num_special 1, digit_limbs 1.
+ * Only num_special = 1 and digit_limbs = 1 are implemented (HD_E_PARAMS else).
+ * log_n in [4, 16].  seed keys the Philox stream of the secret / rotation keys. */
+typedef struct {
+  uint32_t log_n, num_limbs, q0_bits, scale_bits, special_bits, num_special, digit_limbs;
+  uint32_t reserved;
+  uint64_t seed;
+} hd_params;
+
+/* Enrollment layout (Alg. enroller_bsgs Steps 2-3). */
+typedef struct {
+  uint32_t vector_dim, n1, num_slots, block_n, blocks_m, groups_per_ct;
+  uint64_t num_vectors, num_groups, num_aggregates;
+  int32_t giant_min, giant_max;  /* giantSteps J (R6) */
+  uint32_t agg_begin, agg_end;   /* aggregates held by this database handle */
+} hd_layout;
+
+/* ---- context ------------------------------------------------------------ */
+/* Creates the context: moduli (R5), primitive roots (R13), NTT/FFT tables.
+ * cuda_stream: cudaStream_t of the caller (NULL = default stream).            */
+hd_status hd_context_create(const hd_params *params, int cuda_device, void *cuda_stream,
+                            hd_context **out);
+void hd_context_destroy(hd_context *ctx);
+hd_status hd_context_set_stream(hd_context *ctx, void *cuda_stream);
+/* moduli[0..L-1] = q_i, moduli[L] = P; psi likewise (host arrays, L+1 each). */
+hd_status hd_context_moduli(const hd_context *ctx, uint64_t *moduli, uint64_t *psi, size_t cap);
+
+/* ---- client -------------------------------------------------------------- */
+/* Rotation-key set of the fold schedule (R2): baby {1..n1-1}, giant
+ * {preRot(j) != 0}, fold {numSlots - N}; sorted ascending, unique.
+ * Writes min(count, cap) steps; *count = total.  cap too small -> HD_E_INVALID_ARG. */
+hd_status hd_rotation_steps(const hd_context *ctx, uint32_t vector_dim, uint32_t n1,
+                            int32_t *steps, size_t cap, size_t *count);
+/* Secret key (ternary, R14) and hybrid key-switching keys for every step
+ * (R11), generated on the device. */
+hd_status hd_keygen(hd_context *ctx, const int32_t *steps, size_t count, hd_secret_key **sk,
+                    hd_eval_keys **evk);
+/* L2-normalise q (R16), replicate with period N over all slots (R8), encode at
+ * Delta = 2^scale_bits over all L limbs (R15), encrypt symmetrically with the
+ * Philox stream keyed by enc_seed (R14).  q: host float32[vector_dim]. */
+hd_status hd_encrypt_query(hd_context *ctx, const hd_secret_key *sk, const float *q,
+                           uint32_t vector_dim, uint64_t enc_seed, hd_ciphertext **out);
+/* Decrypt + decode the n_ct output ciphertexts of aggregates
+ * [layout->agg_begin, layout->agg_begin + n_ct) and write the score of every
+ * database vector they hold, in vector order (R4): scores[v - v_first] for
+ * v in [agg_begin*(M/2)*N, min(num_vectors, agg_end*(M/2)*N)).
+ * *written (optional) = number of scores.  Decode is floating point: scores match
+ * the cosine within the CKKS error, not bit-exactly. */
+hd_status hd_decrypt_scores(hd_context *ctx, const hd_secret_key *sk, const hd_layout *layout,
+                            const hd_ciphertext *const *cts, size_t n_ct, double *scores,
+                            size_t capacity, size_t *written);
+/* Decrypt one ciphertext to its plaintext residues (host u64 [limbs][n]); test use. */
+hd_status hd_decrypt(hd_context *ctx, const hd_secret_key *sk, const hd_ciphertext *ct,
+                     uint64_t *pt_host, size_t cap);
+
+/* ---- enroller / server ----------------------------------------------------- */
+/* Enroll aggregates [agg_begin, agg_end) of a database of num_vectors vectors
+ * (host float32, row-major num_vectors x vector_dim): Steps 1-5 of Alg.
+ * enroller_bsgs with plaintext diagonals encoded at Delta = q_{L-1}
+ * (R1, R15), stored device-resident.  Only rows of the requested aggregates are
+ * read, so `vectors` may point at row 0 of the whole database.
+ * agg_end = 0 means "all aggregates".  Device memory exhausted -> HD_E_CAPACITY. */
+hd_status hd_enroll(hd_context *ctx, const float *vectors, uint64_t num_vectors,
+                    uint32_t vector_dim, uint32_t n1, uint32_t agg_begin, uint32_t agg_end,
+                    hd_database **out);
+hd_status hd_database_layout(const hd_database *db, hd_layout *out);
+/* The online scan (Alg. sender-bsgs; fold schedule R2): baby steps
+ * (hoisted), MAC over all local aggregates, rescale, giant rotations, fold.
+ * out[i] receives the score ciphertext (L-1 limbs) of aggregate agg_begin + i;
+ * n_out must equal agg_end - agg_begin.  A non-NULL out[i] from a previous call
+ * on the same context is overwritten in place (no allocation). */
+hd_status hd_query(hd_context *ctx, const hd_eval_keys *evk, const hd_database *db,
+                   const hd_ciphertext *query, hd_ciphertext **out, size_t n_out);
+/* Cumulative number of CUDA kernels this context has launched (all entry points). */
+hd_status hd_launch_count(const hd_context *ctx, uint64_t *count);
+/* Per-phase device times (ms), averaged over the hd_query calls issued since the
+ * previous hd_query_stats call (up to 64; synchronises), CUDA events on the context
+ * stream: [0] baby steps, [1] MAC, [2] rescale, [3] giant rotations, [4] fold. */
+hd_status hd_query_stats(const hd_context *ctx, double *phase_ms, size_t n_phases);
+
+/* ---- serialisation (canonical: 64-byte header + u64 residues) --------------- */
+/* dst/src on the host (on_device = 0) or on the context's device (on_device = 1);
+ * dst = NULL queries the size in *written. */
+hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, size_t cap, int dst_on_device,
+                               size_t *written);
+hd_status hd_ciphertext_import(hd_context *ctx, const void *src, size_t bytes, int src_on_device,
+                               hd_ciphertext **out);
+/* In-place import into an existing ciphertext of the same shape (no allocation). */
+hd_status hd_ciphertext_import_into(hd_ciphertext *ct, const void *src, size_t bytes,
+                                    int src_on_device);
+hd_status hd_ciphertext_limbs(const hd_ciphertext *ct, uint32_t *limbs);
+hd_status hd_eval_keys_export(const hd_eval_keys *evk, void *dst, size_t cap, int dst_on_device,
+                              size_t *written);
+hd_status hd_eval_keys_import(hd_context *ctx, const void *src, size_t bytes, int src_on_device,
+                              hd_eval_keys **out);
+/* Secret key in NTT form, host u64 [(L+1)][n]; test use. */
+hd_status hd_secret_key_export(const hd_secret_key *sk, uint64_t *dst, size_t cap);
+
+void hd_ciphertext_destroy(hd_ciphertext *ct);
+void hd_eval_keys_destroy(hd_eval_keys *evk);
+void hd_secret_key_destroy(hd_secret_key *sk);
+void hd_database_destroy(hd_database *db);
+
+/* ---- test-only stage entry points (host buffers, canonical layouts) --------- */
+/* Batched NTT (inverse != 0: INTT) of n_rows rows of n u64, row r over modulus
+ * index modulus_idx[r] (0..L).  data: host, in place. */
+hd_status hd_test_ntt(hd_context *ctx, uint64_t *data, uint32_t n_rows,
+                      const uint32_t *modulus_idx, int inverse);
+/* Stage buffers left by the last hd_query on `db` (host copy):
+ *   which 0: baby step r[index]            (ct, L limbs)
+ *         1: giant sum S_{agg,j}           (ct, L limbs),   index = j
+ *         2: rescaled S'_{agg,j}           (ct, L-1 limbs), index = j
+ *         3: y_agg = sum_j Rot(S'_j)       (ct, L-1 limbs)
+ *         4: diagonal plaintext D[agg][k]  (pt, L limbs),   index = k
+ * agg is the global aggregate index.  cap in u64 elements. */
+hd_status hd_test_stage(const hd_database *db, int which, uint32_t agg, int32_t index,
+                        uint64_t *host_dst, size_t cap);
+/* Rotation of one ciphertext by `step` with the key in evk (test use): ModUp,
+ * key inner product, ModDown (R11).  out is allocated. */
+hd_status hd_test_rotate(hd_context *ctx, const hd_eval_keys *evk, const hd_ciphertext *ct,
+                         int32_t step, hd_ciphertext **out);
+hd_status hd_test_rescale(hd_context *ctx, const hd_ciphertext *ct, hd_ciphertext **out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HD_H */

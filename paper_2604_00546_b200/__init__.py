@@ -1,0 +1,368 @@
+"""paper_2604_00546_b200 -- B200-native encrypted BSGS similarity scan (arXiv 2604.00546).
+
+Thin ctypes binding of ``libhd.so`` (include/hd.h).  Every function named
+``hd_*`` here marshals arguments to the C ABI function of the same name; all
+arithmetic runs in the CUDA kernels of ``csrc/``.  There is no CPU fallback:
+if ``libhd.so`` cannot be built/loaded, or no CUDA device is present, calls
+raise :class:`HDError`.
+
+The small classes (:class:`Context`, :class:`Database`, ...) only own handles
+and call the ``hd_*`` functions.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+
+from ._build import LIB as _LIB_PATH
+from ._build import build as _build_lib
+
+__all__ = ["HDError", "Params", "Layout", "Context", "Database", "load", "lib_path"]
+
+HD_OK, HD_E_INVALID_ARG, HD_E_PARAMS, HD_E_LAYOUT, HD_E_ZERO_VECTOR, HD_E_MISSING_KEY = 0, -1, -2, -3, -4, -5
+HD_E_LEVEL, HD_E_CAPACITY, HD_E_CUDA, HD_E_STATE, HD_E_FORMAT = -6, -7, -8, -9, -10
+
+ABI_FUNCTIONS = [
+    "hd_status_string", "hd_last_error", "hd_context_create", "hd_context_destroy", "hd_context_set_stream",
+    "hd_context_moduli", "hd_rotation_steps", "hd_keygen", "hd_encrypt_query", "hd_decrypt_scores", "hd_decrypt",
+    "hd_enroll", "hd_database_layout", "hd_query", "hd_query_stats", "hd_launch_count", "hd_ciphertext_export",
+    "hd_ciphertext_import", "hd_ciphertext_import_into", "hd_ciphertext_limbs", "hd_eval_keys_export",
+    "hd_eval_keys_import", "hd_secret_key_export", "hd_ciphertext_destroy", "hd_eval_keys_destroy",
+    "hd_secret_key_destroy", "hd_database_destroy", "hd_test_ntt", "hd_test_stage", "hd_test_rotate",
+    "hd_test_rescale",
+]
+
+
+class HDError(RuntimeError):
+    def __init__(self, fn, code, detail=""):
+        self.code = code
+        super().__init__(f"{fn}: status {code} ({_status_string(code)}){': ' + detail if detail else ''}")
+
+
+class Params(C.Structure):
+    _fields_ = [("log_n", C.c_uint32), ("num_limbs", C.c_uint32), ("q0_bits", C.c_uint32),
+                ("scale_bits", C.c_uint32), ("special_bits", C.c_uint32), ("num_special", C.c_uint32),
+                ("digit_limbs", C.c_uint32), ("reserved", C.c_uint32), ("seed", C.c_uint64)]
+
+
+class Layout(C.Structure):
+    _fields_ = [("vector_dim", C.c_uint32), ("n1", C.c_uint32), ("num_slots", C.c_uint32),
+                ("block_n", C.c_uint32), ("blocks_m", C.c_uint32), ("groups_per_ct", C.c_uint32),
+                ("num_vectors", C.c_uint64), ("num_groups", C.c_uint64), ("num_aggregates", C.c_uint64),
+                ("giant_min", C.c_int32), ("giant_max", C.c_int32), ("agg_begin", C.c_uint32),
+                ("agg_end", C.c_uint32)]
+
+
+_lib = None
+_lock = threading.Lock()
+VP = C.c_void_p
+
+
+def lib_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load libhd.so (building it with nvcc if it is missing or stale)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            path = _build_lib()
+            L = C.CDLL(path)
+            L.hd_status_string.restype = C.c_char_p
+            L.hd_status_string.argtypes = [C.c_int]
+            L.hd_last_error.restype = C.c_char_p
+            for name in ABI_FUNCTIONS:
+                f = getattr(L, name)
+                if name not in ("hd_status_string", "hd_last_error"):
+                    f.restype = C.c_int
+            for name in ("hd_context_destroy", "hd_ciphertext_destroy", "hd_eval_keys_destroy",
+                         "hd_secret_key_destroy", "hd_database_destroy"):
+                getattr(L, name).restype = None
+                getattr(L, name).argtypes = [VP]
+            L.hd_context_create.argtypes = [C.POINTER(Params), C.c_int, VP, C.POINTER(VP)]
+            L.hd_context_set_stream.argtypes = [VP, VP]
+            L.hd_context_moduli.argtypes = [VP, VP, VP, C.c_size_t]
+            L.hd_rotation_steps.argtypes = [VP, C.c_uint32, C.c_uint32, VP, C.c_size_t, C.POINTER(C.c_size_t)]
+            L.hd_keygen.argtypes = [VP, VP, C.c_size_t, C.POINTER(VP), C.POINTER(VP)]
+            L.hd_encrypt_query.argtypes = [VP, VP, VP, C.c_uint32, C.c_uint64, C.POINTER(VP)]
+            L.hd_decrypt_scores.argtypes = [VP, VP, C.POINTER(Layout), VP, C.c_size_t, VP, C.c_size_t,
+                                            C.POINTER(C.c_size_t)]
+            L.hd_decrypt.argtypes = [VP, VP, VP, VP, C.c_size_t]
+            L.hd_enroll.argtypes = [VP, VP, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                    C.POINTER(VP)]
+            L.hd_database_layout.argtypes = [VP, C.POINTER(Layout)]
+            L.hd_query.argtypes = [VP, VP, VP, VP, VP, C.c_size_t]
+            L.hd_query_stats.argtypes = [VP, VP, C.c_size_t]
+            L.hd_launch_count.argtypes = [VP, C.POINTER(C.c_uint64)]
+            L.hd_ciphertext_export.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(C.c_size_t)]
+            L.hd_ciphertext_import.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(VP)]
+            L.hd_ciphertext_import_into.argtypes = [VP, VP, C.c_size_t, C.c_int]
+            L.hd_ciphertext_limbs.argtypes = [VP, C.POINTER(C.c_uint32)]
+            L.hd_eval_keys_export.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(C.c_size_t)]
+            L.hd_eval_keys_import.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(VP)]
+            L.hd_secret_key_export.argtypes = [VP, VP, C.c_size_t]
+            L.hd_test_ntt.argtypes = [VP, VP, C.c_uint32, VP, C.c_int]
+            L.hd_test_stage.argtypes = [VP, C.c_int, C.c_uint32, C.c_int32, VP, C.c_size_t]
+            L.hd_test_rotate.argtypes = [VP, VP, VP, C.c_int32, C.POINTER(VP)]
+            L.hd_test_rescale.argtypes = [VP, VP, C.POINTER(VP)]
+            _lib = L
+        return _lib
+
+
+def _status_string(code):
+    try:
+        return load().hd_status_string(code).decode()
+    except Exception:  # noqa: BLE001
+        return "?"
+
+
+def _check(fn, rc):
+    if rc != HD_OK:
+        raise HDError(fn, rc, load().hd_last_error().decode())
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(VP)
+
+
+class _Handle:
+    _destroy = None
+
+    def __init__(self, h, owner=None):
+        self.h = h
+        self.owner = owner  # keeps the context alive
+
+    def close(self):
+        if self.h:
+            getattr(load(), self._destroy)(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
+class SecretKey(_Handle):
+    _destroy = "hd_secret_key_destroy"
+
+
+class EvalKeys(_Handle):
+    _destroy = "hd_eval_keys_destroy"
+
+
+class Ciphertext(_Handle):
+    _destroy = "hd_ciphertext_destroy"
+
+    @property
+    def limbs(self):
+        v = C.c_uint32()
+        _check("hd_ciphertext_limbs", load().hd_ciphertext_limbs(self.h, C.byref(v)))
+        return v.value
+
+
+class Database(_Handle):
+    _destroy = "hd_database_destroy"
+
+    @property
+    def layout(self) -> Layout:
+        lay = Layout()
+        _check("hd_database_layout", load().hd_database_layout(self.h, C.byref(lay)))
+        return lay
+
+    @property
+    def num_local(self):
+        lay = self.layout
+        return lay.agg_end - lay.agg_begin
+
+
+class Context(_Handle):
+    """One CUDA device + one stream (``stream``: a torch.cuda.Stream, an int handle or None)."""
+
+    _destroy = "hd_context_destroy"
+
+    def __init__(self, log_n, limbs=3, seed=1, device=0, stream=None, scale_bits=45, q0_bits=60):
+        p = Params(log_n=log_n, num_limbs=limbs, q0_bits=q0_bits, scale_bits=scale_bits,
+                   special_bits=q0_bits, num_special=1, digit_limbs=1, reserved=0, seed=seed)
+        h = VP()
+        _check("hd_context_create", load().hd_context_create(C.byref(p), device, _stream_handle(stream),
+                                                             C.byref(h)))
+        super().__init__(h.value)
+        self.log_n, self.L, self.n, self.ns = log_n, limbs, 1 << log_n, 1 << (log_n - 1)
+
+    def set_stream(self, stream):
+        _check("hd_context_set_stream", load().hd_context_set_stream(self.h, _stream_handle(stream)))
+
+    def moduli(self):
+        m = np.zeros(self.L + 1, np.uint64)
+        p = np.zeros(self.L + 1, np.uint64)
+        _check("hd_context_moduli", load().hd_context_moduli(self.h, _ptr(m), _ptr(p), self.L + 1))
+        return [int(x) for x in m], [int(x) for x in p]
+
+    # -- client -------------------------------------------------------------------------------------
+    def rotation_steps(self, vector_dim, n1):
+        cnt = C.c_size_t()
+        _check("hd_rotation_steps", load().hd_rotation_steps(self.h, vector_dim, n1, None, 0, C.byref(cnt)))
+        steps = np.zeros(cnt.value, np.int32)
+        _check("hd_rotation_steps", load().hd_rotation_steps(self.h, vector_dim, n1, _ptr(steps), cnt.value,
+                                                             C.byref(cnt)))
+        return steps
+
+    def keygen(self, steps):
+        steps = np.ascontiguousarray(steps, dtype=np.int32)
+        sk, evk = VP(), VP()
+        _check("hd_keygen", load().hd_keygen(self.h, _ptr(steps), len(steps), C.byref(sk), C.byref(evk)))
+        return SecretKey(sk.value, self), EvalKeys(evk.value, self)
+
+    def encrypt_query(self, sk, q, enc_seed):
+        q = np.ascontiguousarray(q, dtype=np.float32)
+        out = VP()
+        _check("hd_encrypt_query", load().hd_encrypt_query(self.h, sk.h, _ptr(q), len(q), C.c_uint64(enc_seed),
+                                                           C.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def decrypt_scores(self, sk, layout, cts):
+        arr = (VP * len(cts))(*[c.h for c in cts])
+        per = (layout.blocks_m // 2) * layout.block_n
+        v0 = layout.agg_begin * per
+        v1 = min(layout.num_vectors, (layout.agg_begin + len(cts)) * per)
+        scores = np.zeros(v1 - v0, np.float64)
+        w = C.c_size_t()
+        _check("hd_decrypt_scores", load().hd_decrypt_scores(self.h, sk.h, C.byref(layout), arr, len(cts),
+                                                             _ptr(scores), len(scores), C.byref(w)))
+        return scores
+
+    def decrypt(self, sk, ct):
+        out = np.zeros((ct.limbs, self.n), np.uint64)
+        _check("hd_decrypt", load().hd_decrypt(self.h, sk.h, ct.h, _ptr(out), out.size))
+        return out
+
+    # -- enroller / server ---------------------------------------------------------------------------
+    def enroll(self, vectors, n1, agg_begin=0, agg_end=0):
+        vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+        out = VP()
+        _check("hd_enroll", load().hd_enroll(self.h, _ptr(vectors), vectors.shape[0], vectors.shape[1], n1,
+                                             agg_begin, agg_end, C.byref(out)))
+        return Database(out.value, self)
+
+    def query(self, evk, db, query, outs=None):
+        nloc = db.num_local
+        if outs is None:
+            outs = [None] * nloc
+        arr = (VP * nloc)(*[(o.h if o is not None else None) for o in outs])
+        _check("hd_query", load().hd_query(self.h, evk.h, db.h, query.h, arr, nloc))
+        return [o if o is not None else Ciphertext(arr[i], self) for i, o in enumerate(outs)]
+
+    def query_stats(self):
+        ms = np.zeros(5, np.float64)
+        _check("hd_query_stats", load().hd_query_stats(self.h, _ptr(ms), 5))
+        return ms
+
+    def launch_count(self):
+        v = C.c_uint64()
+        _check("hd_launch_count", load().hd_launch_count(self.h, C.byref(v)))
+        return v.value
+
+    # -- serialisation -----------------------------------------------------------------------------
+    def ciphertext_export(self, ct, dst=None, on_device=False):
+        """Export to a new numpy uint8 array (host) or into ``dst`` (pointer int + capacity) on device."""
+        w = C.c_size_t()
+        _check("hd_ciphertext_export", load().hd_ciphertext_export(ct.h, None, 0, 0, C.byref(w)))
+        if dst is None:
+            buf = np.zeros(w.value, np.uint8)
+            _check("hd_ciphertext_export", load().hd_ciphertext_export(ct.h, _ptr(buf), w.value, 0, C.byref(w)))
+            return buf
+        ptr, cap = dst
+        _check("hd_ciphertext_export", load().hd_ciphertext_export(ct.h, VP(ptr), cap, 1 if on_device else 0,
+                                                                   C.byref(w)))
+        return w.value
+
+    def ciphertext_export_size(self, ct):
+        w = C.c_size_t()
+        _check("hd_ciphertext_export", load().hd_ciphertext_export(ct.h, None, 0, 0, C.byref(w)))
+        return w.value
+
+    def ciphertext_import(self, src, nbytes=None, on_device=False):
+        out = VP()
+        if isinstance(src, np.ndarray):
+            _check("hd_ciphertext_import", load().hd_ciphertext_import(self.h, _ptr(src), src.nbytes, 0,
+                                                                       C.byref(out)))
+        else:
+            _check("hd_ciphertext_import", load().hd_ciphertext_import(self.h, VP(src), nbytes,
+                                                                       1 if on_device else 0, C.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def ciphertext_import_into(self, ct, src, nbytes=None, on_device=False):
+        if isinstance(src, np.ndarray):
+            _check("hd_ciphertext_import_into", load().hd_ciphertext_import_into(ct.h, _ptr(src), src.nbytes, 0))
+        else:
+            _check("hd_ciphertext_import_into", load().hd_ciphertext_import_into(ct.h, VP(src), nbytes,
+                                                                                 1 if on_device else 0))
+
+    def ciphertext_residues(self, ct):
+        """Residues [2][limbs][n] (host copy, via the canonical export)."""
+        buf = self.ciphertext_export(ct)
+        return buf[64:].view(np.uint64).reshape(2, -1, self.n).copy()
+
+    def eval_keys_export(self, evk):
+        w = C.c_size_t()
+        _check("hd_eval_keys_export", load().hd_eval_keys_export(evk.h, None, 0, 0, C.byref(w)))
+        buf = np.zeros(w.value, np.uint8)
+        _check("hd_eval_keys_export", load().hd_eval_keys_export(evk.h, _ptr(buf), w.value, 0, C.byref(w)))
+        return buf
+
+    def eval_keys_import(self, buf):
+        out = VP()
+        _check("hd_eval_keys_import", load().hd_eval_keys_import(self.h, _ptr(buf), buf.nbytes, 0, C.byref(out)))
+        return EvalKeys(out.value, self)
+
+    def secret_key_export(self, sk):
+        out = np.zeros((self.L + 1, self.n), np.uint64)
+        _check("hd_secret_key_export", load().hd_secret_key_export(sk.h, _ptr(out), out.size))
+        return out
+
+    # -- test-only stage entry points ----------------------------------------------------------------
+    def test_ntt(self, rows, modulus_idx, inverse=False):
+        rows = np.ascontiguousarray(rows, dtype=np.uint64).copy()
+        mi = np.ascontiguousarray(modulus_idx, dtype=np.uint32)
+        _check("hd_test_ntt", load().hd_test_ntt(self.h, _ptr(rows), rows.shape[0], _ptr(mi), 1 if inverse else 0))
+        return rows
+
+    def test_stage(self, db, which, agg, index):
+        ell = self.L if which in (0, 1) else (self.L - 1 if which in (2, 3) else self.L)
+        shape = (self.L, self.n) if which == 4 else (2, ell, self.n)
+        out = np.zeros(shape, np.uint64)
+        _check("hd_test_stage", load().hd_test_stage(db.h, which, agg, index, _ptr(out), out.size))
+        return out
+
+    def test_rotate(self, evk, ct, step):
+        out = VP()
+        _check("hd_test_rotate", load().hd_test_rotate(self.h, evk.h, ct.h, step, C.byref(out)))
+        return Ciphertext(out.value, self)
+
+    def test_rescale(self, ct):
+        out = VP()
+        _check("hd_test_rescale", load().hd_test_rescale(self.h, ct.h, C.byref(out)))
+        return Ciphertext(out.value, self)
+
+
+def _stream_handle(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return VP(stream)
+    return VP(stream.cuda_stream)  # torch.cuda.Stream
+
+
+def eval_key_residues(ctx: Context, buf: np.ndarray):
+    """Split an exported eval-key buffer into (steps, keys[count][L][2][L+1][n])."""
+    count = int(buf[20:24].view(np.uint32)[0])
+    steps_bytes = ((count * 4 + 63) // 64) * 64
+    steps = buf[64:64 + count * 4].view(np.int32).copy()
+    keys = buf[64 + steps_bytes:].view(np.uint64).reshape(count, ctx.L, 2, ctx.L + 1, ctx.n)
+    return steps, keys

@@ -1,0 +1,433 @@
+// client.cu -- secret key, rotation keys, query encryption, decryption and decoding
+// (P:L302-310), all on the device.
+//
+// Randomness (R14): Philox4x32-10 keyed by (seed_lo, seed_hi) with
+// counter (coef j, modulus index l, object, tag<<16 | sub).
+#include <cmath>
+
+#include "common.cuh"
+#include "ks.cuh"
+
+hd_status normalize_on_device(hd_context *c, const float *dv, int rows, int dim, double *U);
+hd_status check_flag(hd_context *c);
+
+namespace {
+constexpr int TPB = 256;
+enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5 };
+
+__device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                              uint32_t k1, uint64_t &w0, uint64_t &w1) {
+#pragma unroll
+  for (int r = 0; r < 10; r++) {
+    if (r) {
+      k0 += 0x9E3779B9u;
+      k1 += 0xBB67AE85u;
+    }
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  w0 = (uint64_t)c0 | ((uint64_t)c1 << 32);
+  w1 = (uint64_t)c2 | ((uint64_t)c3 << 32);
+}
+__device__ __forceinline__ void draw(uint64_t seed, uint32_t j, uint32_t l, uint32_t obj, uint32_t tag, uint32_t sub,
+                                     uint64_t &w0, uint64_t &w1) {
+  philox4x32_10(j, l, obj, (tag << 16) | sub, (uint32_t)seed, (uint32_t)(seed >> 32), w0, w1);
+}
+__device__ __forceinline__ int64_t cbd21(uint64_t w0) {
+  return (int64_t)__popcll(w0 & 0x1FFFFFull) - (int64_t)__popcll((w0 >> 21) & 0x1FFFFFull);
+}
+__device__ __forceinline__ uint64_t smod_dev(int64_t x, uint64_t q, uint64_t bar) {
+  if (x >= 0) return reduce64((uint64_t)x, q, bar);
+  uint64_t r = reduce64((uint64_t)(-x), q, bar);
+  return r ? q - r : 0;
+}
+
+// s (ternary) into every modulus row [(L+1)][n] (coefficient form).
+__global__ void secret_kernel(uint64_t seed, int n, int nm, uint64_t *__restrict__ s, ModTab mt) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  uint64_t w0, w1;
+  draw(seed, j, 0, 0, TAG_SECRET, 0, w0, w1);
+  const int64_t v = (int64_t)(w0 % 3) - 1;
+  for (int l = 0; l < nm; l++) s[(size_t)l * n + j] = smod_dev(v, mt.q[l], mt.bar[l]);
+}
+
+// error rows of a key: key[d][0][l][j] = CBD draw of (j, step, d) mod q_l (coefficient form).
+__global__ void key_error_kernel(uint64_t seed, uint32_t step, int n, int L, uint64_t *__restrict__ key, ModTab mt) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int d = blockIdx.y;
+  if (j >= n) return;
+  uint64_t w0, w1;
+  draw(seed, j, 0, step, TAG_KEY_E, d, w0, w1);
+  const int64_t e = cbd21(w0);
+  for (int l = 0; l <= L; l++) key[((size_t)(d * 2) * (L + 1) + l) * n + j] = smod_dev(e, mt.q[l], mt.bar[l]);
+}
+
+// b_d = e_d - a_d s + [l == d] (P mod q_d) sigma_g(s);  a_d uniform in NTT form (R11, R14).
+__global__ void key_combine_kernel(uint64_t seed, uint32_t step, uint32_t g, int logn, int L,
+                                   const uint64_t *__restrict__ s_ntt, uint64_t *__restrict__ key, ModTab mt,
+                                   InvTab2 pmod) {
+  const int n = 1 << logn;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int dl = blockIdx.y;
+  const int d = dl / (L + 1), l = dl % (L + 1);
+  if (j >= n) return;
+  const uint64_t q = mt.q[l];
+  uint64_t w0, w1;
+  draw(seed, j, l, step, TAG_KEY_A, d, w0, w1);
+  const uint64_t a = reduce128(w0, w1, q, mt.bar[l], mt.r64[l], mt.r64s[l]);
+  uint64_t *kb = key + ((size_t)(d * 2 + 0) * (L + 1) + l) * n;
+  uint64_t *ka = key + ((size_t)(d * 2 + 1) * (L + 1) + l) * n;
+  uint64_t b = submod(kb[j], mulmod(a, s_ntt[(size_t)l * n + j], mt, l), q);
+  if (l == d) {
+    const uint64_t sp = s_ntt[(size_t)l * n + galois_src(j, g, logn)];  // sigma_g(s) in the NTT domain
+    b = addmod(b, mulmod(pmod.w[l], sp, mt, l), q);
+  }
+  kb[j] = b;
+  ka[j] = a;
+}
+
+// encryption: ct c0 holds pt, c1 holds e (NTT form): c0 = e - a s + pt, c1 = a.
+__global__ void enc_error_kernel(uint64_t seed, int n, int nl, uint64_t *__restrict__ c1, ModTab mt) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  uint64_t w0, w1;
+  draw(seed, j, 0, 0, TAG_ENC_E, 0, w0, w1);
+  const int64_t e = cbd21(w0);
+  for (int l = 0; l < nl; l++) c1[(size_t)l * n + j] = smod_dev(e, mt.q[l], mt.bar[l]);
+}
+__global__ void enc_combine_kernel(uint64_t seed, int n, int nl, const uint64_t *__restrict__ s_ntt,
+                                   uint64_t *__restrict__ ct, ModTab mt) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = blockIdx.y;
+  if (j >= n) return;
+  const uint64_t q = mt.q[l];
+  uint64_t w0, w1;
+  draw(seed, j, l, 0, TAG_ENC_A, 0, w0, w1);
+  const uint64_t a = reduce128(w0, w1, q, mt.bar[l], mt.r64[l], mt.r64s[l]);
+  uint64_t *c0 = ct + (size_t)l * n, *c1 = ct + ((size_t)nl + l) * n;
+  uint64_t v = submod(c1[j], mulmod(a, s_ntt[(size_t)l * n + j], mt, l), q);
+  c0[j] = addmod(v, c0[j], q);
+  c1[j] = a;
+}
+
+// query slots: z_s = u_{s mod N} (R8)
+__global__ void query_slots_kernel(const double *__restrict__ u, int N, int ns, double *__restrict__ re,
+                                   double *__restrict__ im) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= ns) return;
+  re[s] = u[s % N];
+  im[s] = 0.0;
+}
+
+// m = c0 + c1 s (NTT form)
+__global__ void decrypt_kernel(const uint64_t *__restrict__ ct, const uint64_t *__restrict__ s_ntt, int n, int nl,
+                               uint64_t *__restrict__ m, ModTab mt) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = blockIdx.y;
+  if (j >= n) return;
+  const uint64_t q = mt.q[l];
+  m[(size_t)l * n + j] = addmod(ct[(size_t)l * n + j], mulmod(ct[((size_t)nl + l) * n + j], s_ntt[(size_t)l * n + j], mt, l), q);
+}
+
+struct CrtTab {
+  uint64_t inv[HD_MAXMOD][HD_MAXMOD];  // inv[i][k] = q_k^{-1} mod q_i
+  uint64_t Q[HD_MAXMOD + 1];           // prod_{k<nl} q_k, little-endian words
+  uint64_t W[HD_MAXMOD][HD_MAXMOD + 1]; // W[i] = prod_{k<i} q_k
+};
+
+// centred CRT (Garner) of coefficient-form limbs -> double / delta; complex slots
+// w_k = (m_k, m_{k+ns}) / delta written bit-reversed (input of the forward special FFT).
+__global__ void crt_decode_kernel(const uint64_t *__restrict__ m, int n, int nl, double delta, int logns,
+                                  double *__restrict__ re, double *__restrict__ im, ModTab mt, CrtTab ct) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const int ns = n / 2;
+  uint64_t v[HD_MAXMOD];
+  for (int i = 0; i < nl; i++) {
+    const uint64_t qi = mt.q[i];
+    uint64_t t = m[(size_t)i * n + c];
+    for (int k = 0; k < i; k++) t = mulmod(submod(t, reduce64(v[k], qi, mt.bar[i]), qi), ct.inv[i][k], mt, i);
+    v[i] = t;
+  }
+  // X = sum_i v_i W_i
+  uint64_t X[HD_MAXMOD + 1];
+  for (int w = 0; w <= nl; w++) X[w] = 0;
+  for (int i = 0; i < nl; i++) {
+    unsigned __int128 carry = 0;
+    for (int w = 0; w <= nl; w++) {
+      unsigned __int128 s = (unsigned __int128)v[i] * ct.W[i][w] + X[w] + carry;
+      X[w] = (uint64_t)s;
+      carry = s >> 64;
+    }
+  }
+  // negative iff 2X > Q
+  bool gt = false;
+  {
+    uint64_t c2 = 0;
+    uint64_t X2[HD_MAXMOD + 1];
+    for (int w = 0; w <= nl; w++) {
+      X2[w] = (X[w] << 1) | c2;
+      c2 = X[w] >> 63;
+    }
+    for (int w = nl; w >= 0; w--)
+      if (X2[w] != ct.Q[w]) {
+        gt = X2[w] > ct.Q[w];
+        break;
+      }
+  }
+  if (gt) {
+    unsigned __int128 borrow = 0;
+    for (int w = 0; w <= nl; w++) {
+      unsigned __int128 d = (unsigned __int128)ct.Q[w] - X[w] - borrow;
+      X[w] = (uint64_t)d;
+      borrow = (d >> 64) ? 1 : 0;
+    }
+  }
+  double r = 0.0;
+  for (int w = nl; w >= 0; w--) r = r * 18446744073709551616.0 + (double)X[w];
+  if (gt) r = -r;
+  r = r / delta;
+  const int k = c < ns ? c : c - ns;
+  const int pos = __brev((uint32_t)k) >> (32 - logns);
+  if (c < ns) re[pos] = r;
+  else im[pos] = r;
+}
+
+__global__ void fft_fwd_stage_kernel(double *__restrict__ re, double *__restrict__ im, int ns, int len,
+                                     const uint32_t *__restrict__ rotg, const double *__restrict__ xr,
+                                     const double *__restrict__ xim, uint32_t two_n) {
+  const int bf = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bf >= ns / 2) return;
+  const int lenh = len >> 1;
+  const uint32_t lenq = (uint32_t)len << 2;
+  const int blk = bf / lenh, j = bf % lenh;
+  const int i0 = blk * len + j, i1 = i0 + lenh;
+  const uint32_t idx = (rotg[j] % lenq) * (two_n / lenq);
+  const double wr = xr[idx], wi = xim[idx];
+  const double xr1 = re[i1], xi1 = im[i1];
+  const double vr = __dsub_rn(__dmul_rn(xr1, wr), __dmul_rn(xi1, wi));
+  const double vi = __dadd_rn(__dmul_rn(xr1, wi), __dmul_rn(xi1, wr));
+  const double ur = re[i0], ui = im[i0];
+  re[i0] = __dadd_rn(ur, vr);
+  im[i0] = __dadd_rn(ui, vi);
+  re[i1] = __dsub_rn(ur, vr);
+  im[i1] = __dsub_rn(ui, vi);
+}
+
+// scores of aggregate agg: v = (agg M/2 + b) N + t -> slot b 2N + t (R4)
+__global__ void scores_kernel(const double *__restrict__ z, int N, int M, long long agg, long long v_first,
+                              long long v_end, double *__restrict__ scores) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (M / 2) * N) return;
+  const int b = i / N, t = i % N;
+  const long long v = (agg * (M / 2) + b) * N + t;
+  if (v >= v_first && v < v_end) scores[v - v_first] = z[b * 2 * N + t];
+}
+}  // namespace
+
+static uint64_t inv_host(uint64_t a, uint64_t q) { return host_powmod(a % q, q - 2, q); }
+
+extern "C" hd_status hd_keygen(hd_context *c, const int32_t *steps, size_t count, hd_secret_key **sk_out,
+                               hd_eval_keys **evk_out) {
+  if (!c || !sk_out || !evk_out || (count && !steps)) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *sk_out = nullptr;
+  *evk_out = nullptr;
+  for (size_t i = 0; i < count; i++)
+    if (steps[i] <= 0 || steps[i] >= c->ns) return hd_fail(HD_E_INVALID_ARG, "rotation step outside (0, numSlots)");
+  HD_CUDA(cudaSetDevice(c->device));
+  const int n = c->n, L = c->L;
+  hd_secret_key *sk = new hd_secret_key{c, nullptr};
+  hd_eval_keys *evk = new hd_eval_keys();
+  evk->ctx = c;
+  evk->steps.assign(steps, steps + count);
+  evk->key_elems = (size_t)L * 2 * (L + 1) * n;
+  auto fail = [&](hd_status s) {
+    hd_secret_key_destroy(sk);
+    hd_eval_keys_destroy(evk);
+    return s;
+  };
+  cudaError_t e = cudaMalloc(&sk->s_ntt, (size_t)(L + 1) * n * 8);
+  if (!e && count) e = cudaMalloc(&evk->keys, evk->key_elems * count * 8);
+  if (e) return fail(hd_fail(HD_E_CAPACITY, cudaGetErrorString(e)));
+  const uint64_t seed = c->params.seed;
+  secret_kernel<<<(n + TPB - 1) / TPB, TPB, 0, c->stream>>>(seed, n, L + 1, sk->s_ntt, c->mt); ++c->launches;
+  RowMap rm{};
+  rm.gsize = 1u << 30;
+  rm.mdiv = 1;
+  rm.mlen = L + 1;
+  for (int l = 0; l <= L; l++) rm.midx[l] = l;
+  hd_status s = ntt_rows(c, sk->s_ntt, L + 1, rm, false);
+  if (s) return fail(s);
+  InvTab2 pmod{};
+  for (int l = 0; l < L; l++) pmod.w[l] = c->mod[L] % c->mod[l];
+  for (size_t i = 0; i < count; i++) {
+    uint64_t *key = evk->keys + evk->key_elems * i;
+    const uint32_t step = (uint32_t)steps[i];
+    const uint32_t g = (uint32_t)host_powmod(5, step, 2ull * n);
+    key_error_kernel<<<dim3((n + TPB - 1) / TPB, L), TPB, 0, c->stream>>>(seed, step, n, L, key, c->mt); ++c->launches;
+    RowMap rk{};  // rows (d, l) at key + (d 2 (L+1) + l) n
+    rk.gsize = L + 1;
+    rk.gstride = (uint64_t)2 * (L + 1) * n;
+    rk.mdiv = 1;
+    rk.mlen = L + 1;
+    for (int l = 0; l <= L; l++) rk.midx[l] = l;
+    if ((s = ntt_rows(c, key, L * (L + 1), rk, false))) return fail(s);
+    key_combine_kernel<<<dim3((n + TPB - 1) / TPB, L * (L + 1)), TPB, 0, c->stream>>>(seed, step, g, c->logn, L,
+                                                                                      sk->s_ntt, key, c->mt, pmod); ++c->launches;
+  }
+  e = cudaStreamSynchronize(c->stream);
+  if (e) return fail(hd_fail(HD_E_CUDA, cudaGetErrorString(e)));
+  *sk_out = sk;
+  *evk_out = evk;
+  return HD_OK;
+}
+
+extern "C" hd_status hd_encrypt_query(hd_context *c, const hd_secret_key *sk, const float *q, uint32_t vector_dim,
+                                      uint64_t enc_seed, hd_ciphertext **out) {
+  if (!c || !sk || !q || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (vector_dim < 2 || (vector_dim & (vector_dim - 1)) || (uint32_t)c->ns % (2 * vector_dim))
+    return hd_fail(HD_E_LAYOUT, "vector_dim must be a power of two with numSlots % (2 vector_dim) == 0");
+  HD_CUDA(cudaSetDevice(c->device));
+  const int n = c->n, ns = c->ns, L = c->L, N = (int)vector_dim;
+  float *dq = nullptr;
+  double *U = nullptr, *re = nullptr, *im = nullptr;
+  hd_ciphertext *ct = nullptr;
+  hd_status s = alloc_ct(c, L, &ct);
+  if (s) return s;
+  cudaError_t e = cudaMalloc(&dq, N * 4);
+  if (!e) e = cudaMalloc(&U, N * 8);
+  if (!e) e = cudaMalloc(&re, (size_t)ns * 8);
+  if (!e) e = cudaMalloc(&im, (size_t)ns * 8);
+  if (!e) e = cudaMemcpyAsync(dq, q, N * 4, cudaMemcpyHostToDevice, c->stream);
+  if (e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  if (!s) s = normalize_on_device(c, dq, 1, N, U);
+  if (!s) s = check_flag(c);
+  if (!s) {
+    query_slots_kernel<<<(ns + TPB - 1) / TPB, TPB, 0, c->stream>>>(U, N, ns, re, im); ++c->launches;
+    s = encode_batch(c, re, im, 1, std::ldexp(1.0, (int)c->params.scale_bits), L, ct->data, (size_t)2 * L * n);
+  }
+  if (!s) {
+    enc_error_kernel<<<(n + TPB - 1) / TPB, TPB, 0, c->stream>>>(enc_seed, n, L, ct->data + (size_t)L * n, c->mt); ++c->launches;
+    RowMap rm{};
+    rm.gsize = 1u << 30;
+    rm.mdiv = 1;
+    rm.mlen = L;
+    for (int l = 0; l < L; l++) rm.midx[l] = l;
+    s = ntt_rows(c, ct->data + (size_t)L * n, L, rm, false);
+  }
+  if (!s) {
+    enc_combine_kernel<<<dim3((n + TPB - 1) / TPB, L), TPB, 0, c->stream>>>(enc_seed, n, L, sk->s_ntt, ct->data, c->mt); ++c->launches;
+    s = check_flag(c);
+  }
+  cudaFree(dq);
+  cudaFree(U);
+  cudaFree(re);
+  cudaFree(im);
+  if (s) {
+    hd_ciphertext_destroy(ct);
+    return s;
+  }
+  *out = ct;
+  return HD_OK;
+}
+
+static hd_status decrypt_to(hd_context *c, const hd_secret_key *sk, const hd_ciphertext *ct, uint64_t *m) {
+  const int n = c->n;
+  decrypt_kernel<<<dim3((n + TPB - 1) / TPB, ct->limbs), TPB, 0, c->stream>>>(ct->data, sk->s_ntt, n, ct->limbs, m,
+                                                                             c->mt); ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  return HD_OK;
+}
+
+extern "C" hd_status hd_decrypt(hd_context *c, const hd_secret_key *sk, const hd_ciphertext *ct, uint64_t *pt_host,
+                                size_t cap) {
+  if (!c || !sk || !ct || !pt_host) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  const size_t need = (size_t)ct->limbs * c->n;
+  if (cap < need) return hd_fail(HD_E_INVALID_ARG, "capacity too small");
+  uint64_t *m;
+  HD_CUDA(cudaMalloc(&m, need * 8));
+  hd_status s = decrypt_to(c, sk, ct, m);
+  cudaError_t e = cudaMemcpyAsync(pt_host, m, need * 8, cudaMemcpyDeviceToHost, c->stream);
+  if (!e) e = cudaStreamSynchronize(c->stream);
+  cudaFree(m);
+  if (!s && e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  return s;
+}
+
+extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, const hd_layout *lay,
+                                       const hd_ciphertext *const *cts, size_t n_ct, double *scores, size_t capacity,
+                                       size_t *written) {
+  if (!c || !sk || !lay || !cts || !scores) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  const int n = c->n, ns = c->ns, N = (int)lay->block_n, M = (int)lay->blocks_m;
+  const long long per = (long long)(M / 2) * N;
+  const long long v_first = (long long)lay->agg_begin * per;
+  const long long v_end = std::min<long long>((long long)lay->num_vectors, (long long)(lay->agg_begin + n_ct) * per);
+  if (v_end <= v_first) return hd_fail(HD_E_INVALID_ARG, "no vectors in the given aggregates");
+  if (capacity < (size_t)(v_end - v_first)) return hd_fail(HD_E_INVALID_ARG, "scores capacity too small");
+  uint32_t nl = 0;
+  for (size_t i = 0; i < n_ct; i++) {
+    if (!cts[i]) return hd_fail(HD_E_INVALID_ARG, "null ciphertext");
+    if (i == 0) nl = cts[i]->limbs;
+    if (cts[i]->limbs != nl) return hd_fail(HD_E_LEVEL, "mixed ciphertext levels");
+  }
+  CrtTab ctab{};
+  for (uint32_t i = 0; i < nl; i++)
+    for (uint32_t k = 0; k < i; k++) ctab.inv[i][k] = inv_host(c->mod[k], c->mod[i]);
+  {
+    std::vector<uint64_t> W(nl + 1, 0);
+    W[0] = 1;
+    for (uint32_t i = 0; i < nl; i++) {
+      for (uint32_t w = 0; w <= nl; w++) ctab.W[i][w] = W[w];
+      unsigned __int128 carry = 0;
+      for (uint32_t w = 0; w <= nl; w++) {
+        unsigned __int128 s2 = (unsigned __int128)W[w] * c->mod[i] + carry;
+        W[w] = (uint64_t)s2;
+        carry = s2 >> 64;
+      }
+    }
+    for (uint32_t w = 0; w <= nl; w++) ctab.Q[w] = W[w];
+  }
+  uint64_t *m = nullptr;
+  double *re = nullptr, *im = nullptr, *dsc = nullptr;
+  const size_t nsc = (size_t)(v_end - v_first);
+  cudaError_t e = cudaMalloc(&m, (size_t)nl * n * 8);
+  if (!e) e = cudaMalloc(&re, (size_t)ns * 8);
+  if (!e) e = cudaMalloc(&im, (size_t)ns * 8);
+  if (!e) e = cudaMalloc(&dsc, nsc * 8);
+  hd_status s = e ? hd_fail(HD_E_CUDA, cudaGetErrorString(e)) : HD_OK;
+  const double delta = std::ldexp(1.0, (int)c->params.scale_bits);
+  RowMap rm{};
+  rm.gsize = 1u << 30;
+  rm.mdiv = 1;
+  rm.mlen = nl;
+  for (uint32_t l = 0; l < nl; l++) rm.midx[l] = l;
+  for (size_t i = 0; i < n_ct && !s; i++) {
+    if ((s = decrypt_to(c, sk, cts[i], m))) break;
+    if ((s = ntt_rows(c, m, nl, rm, true))) break;
+    crt_decode_kernel<<<(n + TPB - 1) / TPB, TPB, 0, c->stream>>>(m, n, nl, delta, c->logn - 1, re, im, c->mt, ctab); ++c->launches;
+    for (int len = 2; len <= ns; len <<= 1)
+      fft_fwd_stage_kernel<<<(ns / 2 + TPB - 1) / TPB, TPB, 0, c->stream>>>(re, im, ns, len, c->rotg, c->xi_re,
+                                                                            c->xi_im, 2u * n);
+    c->launches += c->logn - 1;
+    scores_kernel<<<((M / 2) * N + TPB - 1) / TPB, TPB, 0, c->stream>>>(re, N, M, (long long)(lay->agg_begin + i),
+                                                                       v_first, v_end, dsc); ++c->launches;
+  }
+  if (!s) {
+    e = cudaMemcpyAsync(scores, dsc, nsc * 8, cudaMemcpyDeviceToHost, c->stream);
+    if (!e) e = cudaStreamSynchronize(c->stream);
+    if (e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  }
+  cudaFree(m);
+  cudaFree(re);
+  cudaFree(im);
+  cudaFree(dsc);
+  if (!s && written) *written = nsc;
+  return s;
+}

@@ -1,0 +1,203 @@
+// common.cuh -- shared device arithmetic and host plumbing of libhd (sm_100a).
+//
+// Moduli are < 2^61 (q0, P ~ 2^60; q1, q2 ~ 2^45; R5), so lazy sums of
+// up to 4 reduced values fit in 64 bits.  Multiplication by a fixed operand uses
+// Shoup's precomputed quotient; products of two variable operands are
+// accumulated exactly in 128 bits and reduced once (reduce128).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hd.h"
+
+#define HD_MAXMOD 8
+
+// ---------------------------------------------------------------------------
+// Per-modulus constants, passed to kernels by value.
+// ---------------------------------------------------------------------------
+struct ModTab {
+  uint64_t q[HD_MAXMOD];
+  uint64_t bar[HD_MAXMOD];   // floor(2^64 / q)
+  uint64_t r64[HD_MAXMOD];   // 2^64 mod q
+  uint64_t r64s[HD_MAXMOD];  // Shoup companion of r64
+};
+
+struct InvTab2 {
+  uint64_t w[HD_MAXMOD];
+};
+
+// Row addressing for batched kernels: row r lives at
+//   base + (r / gsize) * gstride + (r % gsize) * n
+// and is reduced modulo q[midx[(r / mdiv) % mlen]].
+struct RowMap {
+  uint32_t gsize;
+  uint32_t mdiv, mlen;
+  uint32_t pad;
+  uint64_t gstride;
+  uint8_t midx[32];
+};
+
+// ---------------------------------------------------------------------------
+// Device arithmetic
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t mulhi64(uint64_t a, uint64_t b) { return __umul64hi(a, b); }
+
+// a * w mod q with Shoup companion ws = floor(w 2^64 / q); result in [0, 2q).
+__device__ __forceinline__ uint64_t shoup_lazy(uint64_t a, uint64_t w, uint64_t ws, uint64_t q) {
+  uint64_t qh = __umul64hi(a, ws);
+  return a * w - qh * q;
+}
+__device__ __forceinline__ uint64_t shoup(uint64_t a, uint64_t w, uint64_t ws, uint64_t q) {
+  uint64_t r = shoup_lazy(a, w, ws, q);
+  return r >= q ? r - q : r;
+}
+// x mod q for any 64-bit x; bar = floor(2^64/q).
+__device__ __forceinline__ uint64_t reduce64(uint64_t x, uint64_t q, uint64_t bar) {
+  uint64_t r = x - __umul64hi(x, bar) * q;  // [0, 2q)
+  return r >= q ? r - q : r;
+}
+// (hi 2^64 + lo) mod q.
+__device__ __forceinline__ uint64_t reduce128(uint64_t hi, uint64_t lo, uint64_t q, uint64_t bar,
+                                              uint64_t r64, uint64_t r64s) {
+  uint64_t t = shoup_lazy(hi, r64, r64s, q);     // [0, 2q)
+  uint64_t u = lo - __umul64hi(lo, bar) * q;     // [0, 2q)
+  uint64_t s = t + u;                            // < 4q < 2^63
+  if (s >= 2 * q) s -= 2 * q;
+  if (s >= q) s -= q;
+  return s;
+}
+__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, const ModTab &M, int m) {
+  return reduce128(__umul64hi(a, b), a * b, M.q[m], M.bar[m], M.r64[m], M.r64s[m]);
+}
+__device__ __forceinline__ uint64_t addmod(uint64_t a, uint64_t b, uint64_t q) {
+  uint64_t s = a + b;
+  return s >= q ? s - q : s;
+}
+__device__ __forceinline__ uint64_t submod(uint64_t a, uint64_t b, uint64_t q) {
+  return a >= b ? a - b : a + q - b;
+}
+// 128-bit accumulate acc += a*b (exact).
+__device__ __forceinline__ void mac128(uint64_t &lo, uint64_t &hi, uint64_t a, uint64_t b) {
+  uint64_t plo = a * b, phi = __umul64hi(a, b);
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(plo), "l"(phi));
+}
+// centred lift (R12) of x in [0, qs) into modulus m (bar_m = floor(2^64/m)).
+__device__ __forceinline__ uint64_t lift_centred(uint64_t x, uint64_t qs, uint64_t m, uint64_t bar_m) {
+  if (x > (qs >> 1)) {
+    uint64_t r = reduce64(qs - x, m, bar_m);
+    return r ? m - r : 0;
+  }
+  return reduce64(x, m, bar_m);
+}
+// Galois index map in the NTT domain (R11): out[t] = in[pi_g(t)],
+// pi_g(t) = br(((g (2 br(t) + 1)) mod 2n - 1) / 2).
+__device__ __forceinline__ uint32_t galois_src(uint32_t t, uint32_t g, int logn) {
+  uint32_t bt = __brev(t) >> (32 - logn);
+  uint32_t mask = (2u << logn) - 1u;  // mod 2n
+  uint32_t e = (uint32_t)(((uint64_t)g * (2u * bt + 1u)) & mask);
+  return __brev((e - 1u) >> 1) >> (32 - logn);
+}
+
+__device__ __forceinline__ uint64_t *row_ptr(uint64_t *base, const RowMap &rm, uint32_t r, uint32_t n) {
+  return base + (uint64_t)(r / rm.gsize) * rm.gstride + (uint64_t)(r % rm.gsize) * n;
+}
+__device__ __forceinline__ int row_mod(const RowMap &rm, uint32_t r) {
+  return rm.midx[(r / rm.mdiv) % rm.mlen];
+}
+
+// ---------------------------------------------------------------------------
+// Host-side context (C++ only).
+// ---------------------------------------------------------------------------
+struct hd_context {
+  hd_params params;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int logn = 0, n = 0, ns = 0, L = 0;
+  uint64_t mod[HD_MAXMOD] = {0};  // q_0..q_{L-1}, P at index L
+  uint64_t psi[HD_MAXMOD] = {0};
+  ModTab mt;
+  // device tables
+  uint64_t *tw = nullptr, *tws = nullptr, *itw = nullptr, *itws = nullptr;  // [L+1][n]
+  uint64_t ninv[HD_MAXMOD], ninvs[HD_MAXMOD];
+  double *xi_re = nullptr, *xi_im = nullptr;  // [2n]: xi^t, R15
+  uint32_t *rotg = nullptr;                   // [ns]: 5^j mod 2n
+  // scratch (grown on demand at setup time only)
+  void *scratch = nullptr;
+  size_t scratch_bytes = 0;
+  int *d_flag = nullptr;  // device error flag
+  cudaEvent_t ev[64][8];  // per-query phase events (ring of 64 queries)
+  int ev_next = 0, ev_pending = 0;
+  double last_phase_ms[5] = {0, 0, 0, 0, 0};
+  uint64_t launches = 0;  // kernels launched on this context (hd_launch_count)
+};
+
+struct hd_secret_key {
+  hd_context *ctx;
+  uint64_t *s_ntt;  // [(L+1)][n]
+};
+
+struct hd_eval_keys {
+  hd_context *ctx;
+  std::vector<int32_t> steps;
+  uint64_t *keys = nullptr;  // [count][L][2][L+1][n]
+  size_t key_elems = 0;      // per key
+  const uint64_t *find(int32_t step) const {
+    for (size_t i = 0; i < steps.size(); i++)
+      if (steps[i] == step) return keys + key_elems * i;
+    return nullptr;
+  }
+};
+
+struct hd_ciphertext {
+  hd_context *ctx;
+  uint32_t limbs;
+  uint64_t *data;  // [2][limbs][n]
+};
+
+struct hd_database {
+  hd_context *ctx;
+  hd_layout lay;
+  uint32_t N, M, n1, A_loc;
+  std::vector<int32_t> js;       // giant steps j (contiguous, non-empty ranges)
+  std::vector<int32_t> pre;      // preRot(j) per j
+  uint64_t *D = nullptr;         // [A_loc][N][L][n] diagonal plaintexts
+  // query workspaces (allocated at enrollment; reused by every hd_query)
+  uint64_t *r = nullptr;         // [n1][2][L][n] baby steps
+  uint64_t *S = nullptr;         // [A_loc][nj][2][L][n] giant-step sums
+  uint64_t *Sp = nullptr;        // [A_loc][nj][2][L-1][n] rescaled
+  uint64_t *y = nullptr;         // [A_loc][2][L-1][n]
+  uint64_t *outbuf = nullptr;    // [A_loc][2][L-1][n] folded outputs
+  uint64_t *dig = nullptr;       // ModUp digits
+  uint64_t *u = nullptr;         // KIP output
+  uint64_t *tmp = nullptr;       // INTT / lift scratch
+  uint64_t *tmp2 = nullptr;      // rescale scratch
+  uint32_t rescale_chunk = 1;
+  // rotation-key tables for the (db, evk) pair last used: [0, n1-1) baby i = 1..n1-1,
+  // [n1-1, n1-1+nj) giant j (NULL key when preRot = 0), [n1-1+nj] fold
+  const hd_eval_keys *keyed_for = nullptr;
+  const uint64_t **kptr = nullptr;
+  uint32_t *gal = nullptr;
+  size_t bytes = 0;
+  bool has_run = false;
+};
+
+// error plumbing
+hd_status hd_fail(hd_status s, const std::string &msg);
+#define HD_CUDA(call)                                                                     \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) return hd_fail(HD_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// kernels / host drivers (defined in the .cu files)
+hd_status ntt_rows(hd_context *c, uint64_t *base, uint32_t rows, const RowMap &rm, bool inverse);
+RowMap rowmap_simple(uint32_t mdiv, std::initializer_list<int> mods, uint32_t gsize = 1u << 30,
+                     uint64_t gstride = 0);
+uint64_t host_mulmod(uint64_t a, uint64_t b, uint64_t m);
+uint64_t host_powmod(uint64_t b, uint64_t e, uint64_t m);
+uint64_t host_shoup(uint64_t w, uint64_t q);

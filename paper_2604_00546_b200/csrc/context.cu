@@ -1,0 +1,478 @@
+// context.cu -- parameters, tables, object lifetimes and serialisation of libhd.
+//
+// Moduli (R5): q0 = largest prime < 2^q0_bits, P = largest below q0,
+// q1 > q2 > ... = largest primes < 2^scale_bits, all = 1 (mod 2n).
+// psi (R13) = the smallest primitive 2n-th root of unity mod each modulus.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+typedef unsigned __int128 u128;
+
+static thread_local std::string g_last_error;
+
+hd_status hd_fail(hd_status s, const std::string &msg) {
+  g_last_error = msg;
+  return s;
+}
+
+extern "C" const char *hd_last_error(void) { return g_last_error.c_str(); }
+
+extern "C" const char *hd_status_string(hd_status s) {
+  switch (s) {
+    case HD_OK: return "ok";
+    case HD_E_INVALID_ARG: return "invalid argument";
+    case HD_E_PARAMS: return "unsupported parameters";
+    case HD_E_LAYOUT: return "layout error (vector_dim must be a power of two with numSlots % 2N == 0)";
+    case HD_E_ZERO_VECTOR: return "zero vector cannot be L2-normalised";
+    case HD_E_MISSING_KEY: return "missing rotation key";
+    case HD_E_LEVEL: return "ciphertext level mismatch";
+    case HD_E_CAPACITY: return "device capacity exceeded";
+    case HD_E_CUDA: return "CUDA error";
+    case HD_E_STATE: return "object state / context mismatch";
+    case HD_E_FORMAT: return "bad serialised format";
+  }
+  return "unknown status";
+}
+
+// ---------------------------------------------------------------------------
+// host number theory (independent of oracle/)
+// ---------------------------------------------------------------------------
+uint64_t host_mulmod(uint64_t a, uint64_t b, uint64_t m) { return (uint64_t)((u128)a * b % m); }
+uint64_t host_powmod(uint64_t b, uint64_t e, uint64_t m) {
+  uint64_t r = 1;
+  b %= m;
+  for (; e; e >>= 1, b = host_mulmod(b, b, m))
+    if (e & 1) r = host_mulmod(r, b, m);
+  return r;
+}
+uint64_t host_shoup(uint64_t w, uint64_t q) { return (uint64_t)(((u128)w << 64) / q); }
+
+static bool miller_rabin(uint64_t n) {
+  if (n < 4) return n == 2 || n == 3;
+  if (n % 2 == 0) return false;
+  uint64_t d = n - 1;
+  int r = 0;
+  while (!(d & 1)) d >>= 1, ++r;
+  const uint64_t witnesses[] = {2, 325, 9375, 28178, 450775, 9780504, 1795265022};  // deterministic < 2^64
+  for (uint64_t a : witnesses) {
+    a %= n;
+    if (a == 0) continue;
+    uint64_t x = host_powmod(a, d, n);
+    if (x == 1 || x == n - 1) continue;
+    bool ok = false;
+    for (int i = 1; i < r && !ok; i++) {
+      x = host_mulmod(x, x, n);
+      ok = (x == n - 1);
+    }
+    if (!ok) return false;
+  }
+  return true;
+}
+
+// largest prime p < bound with p = 1 mod 2n
+static uint64_t ntt_prime_below(uint64_t bound, uint64_t two_n) {
+  uint64_t c = ((bound - 1) / two_n) * two_n + 1;
+  if (c >= bound) c -= two_n;
+  for (; c > two_n; c -= two_n)
+    if (miller_rabin(c)) return c;
+  return 0;
+}
+
+static uint64_t smallest_primitive_root(uint64_t q, uint64_t n) {
+  const uint64_t two_n = 2 * n;
+  uint64_t y = 0;
+  for (uint64_t x = 2;; x++) {
+    y = host_powmod(x, (q - 1) / two_n, q);
+    if (host_powmod(y, n, q) == q - 1) break;
+  }
+  uint64_t best = y, cur = y, y2 = host_mulmod(y, y, q);
+  for (uint64_t k = 1; k < n; k++) {
+    cur = host_mulmod(cur, y2, q);
+    if (cur < best) best = cur;
+  }
+  return best;
+}
+
+static uint32_t bitrev_host(uint32_t x, int bits) {
+  uint32_t r = 0;
+  for (int i = 0; i < bits; i++) r = (r << 1) | ((x >> i) & 1);
+  return r;
+}
+
+extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device, void *cuda_stream,
+                                       hd_context **out) {
+  if (!params || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  hd_params p = *params;
+  if (!p.num_limbs) p.num_limbs = 3;
+  if (!p.q0_bits) p.q0_bits = 60;
+  if (!p.scale_bits) p.scale_bits = 45;
+  if (!p.special_bits) p.special_bits = 60;
+  if (!p.num_special) p.num_special = 1;
+  if (!p.digit_limbs) p.digit_limbs = 1;
+  if (p.log_n < 4 || p.log_n > 16 || p.num_limbs < 2 || p.num_limbs + 1 > HD_MAXMOD ||
+      p.num_special != 1 || p.digit_limbs != 1 || p.q0_bits > 60 || p.special_bits != p.q0_bits ||
+      p.scale_bits > 60 || p.scale_bits < 20)
+    return hd_fail(HD_E_PARAMS, "supported: log_n in [4,16], num_special = digit_limbs = 1, moduli <= 60 bits");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+    return hd_fail(HD_E_CUDA, "no CUDA device (libhd has no CPU fallback)");
+  if (cuda_device < 0 || cuda_device >= ndev) return hd_fail(HD_E_INVALID_ARG, "bad device index");
+  HD_CUDA(cudaSetDevice(cuda_device));
+  hd_context *c = new hd_context();
+  c->params = p;
+  c->device = cuda_device;
+  c->stream = (cudaStream_t)cuda_stream;
+  c->logn = (int)p.log_n;
+  c->n = 1 << c->logn;
+  c->ns = c->n / 2;
+  c->L = (int)p.num_limbs;
+  const uint64_t two_n = 2 * (uint64_t)c->n;
+  c->mod[0] = ntt_prime_below(1ull << p.q0_bits, two_n);
+  c->mod[c->L] = ntt_prime_below(c->mod[0], two_n);
+  uint64_t bound = 1ull << p.scale_bits;
+  for (int i = 1; i < c->L; i++) bound = c->mod[i] = ntt_prime_below(bound, two_n);
+  for (int i = 0; i <= c->L; i++) {
+    if (!c->mod[i]) { delete c; return hd_fail(HD_E_PARAMS, "no NTT prime"); }
+    c->psi[i] = smallest_primitive_root(c->mod[i], c->n);
+    uint64_t q = c->mod[i];
+    c->mt.q[i] = q;
+    c->mt.bar[i] = (uint64_t)(((u128)1 << 64) / q);
+    c->mt.r64[i] = (uint64_t)(((u128)1 << 64) % q);
+    c->mt.r64s[i] = host_shoup(c->mt.r64[i], q);
+  }
+  // NTT twiddles psi^{br(k)} and inverse, Shoup companions, n^{-1}
+  const int n = c->n, M = c->L + 1;
+  std::vector<uint64_t> tw((size_t)M * n), tws((size_t)M * n), itw((size_t)M * n + 2 * HD_MAXMOD),
+      itws((size_t)M * n);
+  for (int l = 0; l < M; l++) {
+    uint64_t q = c->mod[l], g = c->psi[l], gi = host_powmod(g, q - 2, q);
+    std::vector<uint64_t> pw(n), ipw(n);
+    pw[0] = ipw[0] = 1;
+    for (int k = 1; k < n; k++) {
+      pw[k] = host_mulmod(pw[k - 1], g, q);
+      ipw[k] = host_mulmod(ipw[k - 1], gi, q);
+    }
+    for (int k = 0; k < n; k++) {
+      uint32_t b = bitrev_host(k, c->logn);
+      tw[(size_t)l * n + k] = pw[b];
+      tws[(size_t)l * n + k] = host_shoup(pw[b], q);
+      itw[(size_t)l * n + k] = ipw[b];
+      itws[(size_t)l * n + k] = host_shoup(ipw[b], q);
+    }
+    c->ninv[l] = host_powmod((uint64_t)n, q - 2, q);
+    c->ninvs[l] = host_shoup(c->ninv[l], q);
+    itw[(size_t)M * n + l] = c->ninv[l];
+    itw[(size_t)M * n + HD_MAXMOD + l] = c->ninvs[l];
+  }
+  // FFT tables for the special (I)FFT (R15): xi^t = exp(2 pi i t / 2n)
+  std::vector<double> xr(two_n), xim(two_n);
+  for (uint64_t t = 0; t < two_n; t++) {
+    double ang = (2.0 * 3.141592653589793 * (double)t) / (double)two_n;
+    xr[t] = std::cos(ang);
+    xim[t] = std::sin(ang);
+  }
+  std::vector<uint32_t> rg(c->ns);
+  uint64_t r = 1;
+  for (int j = 0; j < c->ns; j++) {
+    rg[j] = (uint32_t)r;
+    r = r * 5 % two_n;
+  }
+  auto fail = [&](cudaError_t e) {
+    hd_context_destroy(c);
+    return hd_fail(HD_E_CUDA, std::string("context tables: ") + cudaGetErrorString(e));
+  };
+  cudaError_t e;
+  if ((e = cudaMalloc(&c->tw, tw.size() * 8)) || (e = cudaMalloc(&c->tws, tws.size() * 8)) ||
+      (e = cudaMalloc(&c->itw, itw.size() * 8)) || (e = cudaMalloc(&c->itws, itws.size() * 8)) ||
+      (e = cudaMalloc(&c->xi_re, two_n * 8)) || (e = cudaMalloc(&c->xi_im, two_n * 8)) ||
+      (e = cudaMalloc(&c->rotg, c->ns * 4)) || (e = cudaMalloc(&c->d_flag, 64)))
+    return fail(e);
+  if ((e = cudaMemcpy(c->tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(c->tws, tws.data(), tws.size() * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(c->itw, itw.data(), itw.size() * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(c->itws, itws.data(), itws.size() * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(c->xi_re, xr.data(), two_n * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(c->xi_im, xim.data(), two_n * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(c->rotg, rg.data(), c->ns * 4, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemset(c->d_flag, 0, 64)))
+    return fail(e);
+  for (int i = 0; i < 8; i++)
+    for (int k = 0; k < 64; k++)
+      if ((e = cudaEventCreate(&c->ev[k][i]))) return fail(e);
+  *out = c;
+  return HD_OK;
+}
+
+extern "C" void hd_context_destroy(hd_context *c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaFree(c->tw);
+  cudaFree(c->tws);
+  cudaFree(c->itw);
+  cudaFree(c->itws);
+  cudaFree(c->xi_re);
+  cudaFree(c->xi_im);
+  cudaFree(c->rotg);
+  cudaFree(c->d_flag);
+  cudaFree(c->scratch);
+  for (int i = 0; i < 8; i++)
+    for (int k = 0; k < 64; k++)
+      if (c->ev[k][i]) cudaEventDestroy(c->ev[k][i]);
+  delete c;
+}
+
+extern "C" hd_status hd_launch_count(const hd_context *c, uint64_t *count) {
+  if (!c || !count) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *count = c->launches;
+  return HD_OK;
+}
+
+extern "C" hd_status hd_context_set_stream(hd_context *c, void *s) {
+  if (!c) return hd_fail(HD_E_INVALID_ARG, "null context");
+  c->stream = (cudaStream_t)s;
+  return HD_OK;
+}
+
+extern "C" hd_status hd_context_moduli(const hd_context *c, uint64_t *moduli, uint64_t *psi, size_t cap) {
+  if (!c || cap < (size_t)c->L + 1) return hd_fail(HD_E_INVALID_ARG, "capacity < L+1");
+  for (int i = 0; i <= c->L; i++) {
+    if (moduli) moduli[i] = c->mod[i];
+    if (psi) psi[i] = c->psi[i];
+  }
+  return HD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// serialisation: 64-byte header + payload
+// ---------------------------------------------------------------------------
+namespace {
+struct Header {
+  char magic[8];     // "HDBSGS01"
+  uint32_t kind;     // 1 ciphertext, 2 eval keys
+  uint32_t log_n;
+  uint32_t limbs;    // ciphertext limbs / L for keys
+  uint32_t count;    // number of keys
+  uint64_t mod_fp;   // fingerprint of the modulus chain
+  uint64_t payload;  // bytes after the header
+  uint8_t pad[24];
+};
+static_assert(sizeof(Header) == 64, "header");
+
+uint64_t mod_fingerprint(const hd_context *c) {
+  uint64_t h = 1469598103934665603ull;
+  for (int i = 0; i <= c->L; i++) h = (h ^ c->mod[i]) * 1099511628211ull;
+  return h;
+}
+cudaMemcpyKind kind_of(int dst_dev, int src_dev) {
+  if (dst_dev && src_dev) return cudaMemcpyDeviceToDevice;
+  if (dst_dev) return cudaMemcpyHostToDevice;
+  if (src_dev) return cudaMemcpyDeviceToHost;
+  return cudaMemcpyHostToHost;
+}
+}  // namespace
+
+hd_status alloc_ct(hd_context *c, uint32_t limbs, hd_ciphertext **out) {
+  hd_ciphertext *ct = new hd_ciphertext{c, limbs, nullptr};
+  cudaError_t e = cudaMalloc(&ct->data, sizeof(uint64_t) * 2 * limbs * c->n);
+  if (e != cudaSuccess) {
+    delete ct;
+    return hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, "ciphertext alloc");
+  }
+  *out = ct;
+  return HD_OK;
+}
+
+extern "C" hd_status hd_ciphertext_limbs(const hd_ciphertext *ct, uint32_t *limbs) {
+  if (!ct || !limbs) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *limbs = ct->limbs;
+  return HD_OK;
+}
+
+extern "C" hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, size_t cap, int dst_on_device,
+                                          size_t *written) {
+  if (!ct) return hd_fail(HD_E_INVALID_ARG, "null ciphertext");
+  const hd_context *c = ct->ctx;
+  size_t payload = sizeof(uint64_t) * 2 * ct->limbs * c->n, total = sizeof(Header) + payload;
+  if (written) *written = total;
+  if (!dst) return HD_OK;
+  if (cap < total) return hd_fail(HD_E_INVALID_ARG, "export capacity too small");
+  Header h{};
+  memcpy(h.magic, "HDBSGS01", 8);
+  h.kind = 1;
+  h.log_n = c->logn;
+  h.limbs = ct->limbs;
+  h.mod_fp = mod_fingerprint(c);
+  h.payload = payload;
+  HD_CUDA(cudaMemcpyAsync(dst, &h, sizeof(h), kind_of(dst_on_device, 0), c->stream));
+  HD_CUDA(cudaMemcpyAsync((char *)dst + sizeof(h), ct->data, payload, kind_of(dst_on_device, 1), c->stream));
+  HD_CUDA(cudaStreamSynchronize(c->stream));
+  return HD_OK;
+}
+
+static hd_status read_header(hd_context *c, const void *src, size_t bytes, int src_dev, Header &h) {
+  if (!src || bytes < sizeof(Header)) return hd_fail(HD_E_FORMAT, "short buffer");
+  if (src_dev) {
+    HD_CUDA(cudaMemcpyAsync(&h, src, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    HD_CUDA(cudaStreamSynchronize(c->stream));
+  } else {
+    memcpy(&h, src, sizeof(h));
+  }
+  if (memcmp(h.magic, "HDBSGS01", 8) != 0) return hd_fail(HD_E_FORMAT, "bad magic");
+  if (h.log_n != (uint32_t)c->logn || h.mod_fp != mod_fingerprint(c))
+    return hd_fail(HD_E_FORMAT, "serialised object belongs to other parameters");
+  if (bytes < sizeof(Header) + h.payload) return hd_fail(HD_E_FORMAT, "truncated payload");
+  return HD_OK;
+}
+
+extern "C" hd_status hd_ciphertext_import(hd_context *c, const void *src, size_t bytes, int src_on_device,
+                                          hd_ciphertext **out) {
+  if (!c || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  Header h;
+  hd_status s = read_header(c, src, bytes, src_on_device, h);
+  if (s) return s;
+  if (h.kind != 1 || h.limbs < 1 || h.limbs > (uint32_t)c->L) return hd_fail(HD_E_FORMAT, "not a ciphertext");
+  hd_ciphertext *ct;
+  if ((s = alloc_ct(c, h.limbs, &ct))) return s;
+  cudaError_t e = cudaMemcpyAsync(ct->data, (const char *)src + sizeof(Header), h.payload,
+                                  kind_of(1, src_on_device), c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    hd_ciphertext_destroy(ct);
+    return hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  }
+  *out = ct;
+  return HD_OK;
+}
+
+extern "C" hd_status hd_ciphertext_import_into(hd_ciphertext *ct, const void *src, size_t bytes,
+                                               int src_on_device) {
+  if (!ct) return hd_fail(HD_E_INVALID_ARG, "null ciphertext");
+  hd_context *c = ct->ctx;
+  size_t payload = sizeof(uint64_t) * 2 * ct->limbs * c->n;
+  if (!src || bytes < sizeof(Header) + payload) return hd_fail(HD_E_FORMAT, "short buffer");
+  if (!src_on_device) {  // header check only for host sources (device: no sync in the hot path)
+    Header h;
+    hd_status s = read_header(c, src, bytes, 0, h);
+    if (s) return s;
+    if (h.kind != 1 || h.limbs != ct->limbs) return hd_fail(HD_E_LEVEL, "shape mismatch");
+  }
+  HD_CUDA(cudaMemcpyAsync(ct->data, (const char *)src + sizeof(Header), payload, kind_of(1, src_on_device),
+                          c->stream));
+  return HD_OK;
+}
+
+extern "C" void hd_ciphertext_destroy(hd_ciphertext *ct) {
+  if (!ct) return;
+  cudaFree(ct->data);
+  delete ct;
+}
+
+extern "C" hd_status hd_eval_keys_export(const hd_eval_keys *k, void *dst, size_t cap, int dst_on_device,
+                                         size_t *written) {
+  if (!k) return hd_fail(HD_E_INVALID_ARG, "null keys");
+  const hd_context *c = k->ctx;
+  size_t nk = k->steps.size();
+  size_t steps_bytes = ((nk * 4 + 63) / 64) * 64;
+  size_t payload = steps_bytes + sizeof(uint64_t) * k->key_elems * nk, total = sizeof(Header) + payload;
+  if (written) *written = total;
+  if (!dst) return HD_OK;
+  if (cap < total) return hd_fail(HD_E_INVALID_ARG, "export capacity too small");
+  Header h{};
+  memcpy(h.magic, "HDBSGS01", 8);
+  h.kind = 2;
+  h.log_n = c->logn;
+  h.limbs = c->L;
+  h.count = (uint32_t)nk;
+  h.mod_fp = mod_fingerprint(c);
+  h.payload = payload;
+  std::vector<char> head(sizeof(h) + steps_bytes, 0);
+  memcpy(head.data(), &h, sizeof(h));
+  memcpy(head.data() + sizeof(h), k->steps.data(), nk * 4);
+  HD_CUDA(cudaMemcpyAsync(dst, head.data(), head.size(), kind_of(dst_on_device, 0), c->stream));
+  HD_CUDA(cudaMemcpyAsync((char *)dst + head.size(), k->keys, sizeof(uint64_t) * k->key_elems * nk,
+                          kind_of(dst_on_device, 1), c->stream));
+  HD_CUDA(cudaStreamSynchronize(c->stream));
+  return HD_OK;
+}
+
+extern "C" hd_status hd_eval_keys_import(hd_context *c, const void *src, size_t bytes, int src_on_device,
+                                         hd_eval_keys **out) {
+  if (!c || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  Header h;
+  hd_status s = read_header(c, src, bytes, src_on_device, h);
+  if (s) return s;
+  if (h.kind != 2 || h.limbs != (uint32_t)c->L) return hd_fail(HD_E_FORMAT, "not an eval-key set");
+  size_t nk = h.count, steps_bytes = ((nk * 4 + 63) / 64) * 64;
+  hd_eval_keys *k = new hd_eval_keys();
+  k->ctx = c;
+  k->steps.resize(nk);
+  k->key_elems = (size_t)c->L * 2 * (c->L + 1) * c->n;
+  const char *p = (const char *)src + sizeof(Header);
+  cudaError_t e = cudaMemcpyAsync(k->steps.data(), p, nk * 4, kind_of(0, src_on_device), c->stream);
+  if (e == cudaSuccess) e = cudaMalloc(&k->keys, sizeof(uint64_t) * k->key_elems * nk);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(k->keys, p + steps_bytes, sizeof(uint64_t) * k->key_elems * nk, kind_of(1, src_on_device),
+                        c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    hd_eval_keys_destroy(k);
+    return hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, cudaGetErrorString(e));
+  }
+  *out = k;
+  return HD_OK;
+}
+
+extern "C" void hd_eval_keys_destroy(hd_eval_keys *k) {
+  if (!k) return;
+  cudaFree(k->keys);
+  delete k;
+}
+
+extern "C" hd_status hd_secret_key_export(const hd_secret_key *sk, uint64_t *dst, size_t cap) {
+  if (!sk || !dst) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  const hd_context *c = sk->ctx;
+  size_t need = (size_t)(c->L + 1) * c->n;
+  if (cap < need) return hd_fail(HD_E_INVALID_ARG, "capacity too small");
+  HD_CUDA(cudaMemcpy(dst, sk->s_ntt, need * 8, cudaMemcpyDeviceToHost));
+  return HD_OK;
+}
+
+extern "C" void hd_secret_key_destroy(hd_secret_key *sk) {
+  if (!sk) return;
+  cudaFree(sk->s_ntt);
+  delete sk;
+}
+
+extern "C" hd_status hd_test_ntt(hd_context *c, uint64_t *data, uint32_t n_rows, const uint32_t *modulus_idx,
+                                 int inverse) {
+  if (!c || !data || !modulus_idx) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  for (uint32_t r = 0; r < n_rows; r++)
+    if (modulus_idx[r] > (uint32_t)c->L) return hd_fail(HD_E_INVALID_ARG, "modulus index > L");
+  uint64_t *d;
+  size_t bytes = (size_t)n_rows * c->n * 8;
+  HD_CUDA(cudaMalloc(&d, bytes));
+  HD_CUDA(cudaMemcpy(d, data, bytes, cudaMemcpyHostToDevice));
+  // rows may have arbitrary moduli: launch one row-group per run of equal index
+  hd_status s = HD_OK;
+  for (uint32_t r = 0; r < n_rows && !s;) {
+    uint32_t e = r;
+    while (e < n_rows && modulus_idx[e] == modulus_idx[r]) e++;
+    RowMap rm = rowmap_simple(1, {(int)modulus_idx[r]});
+    s = ntt_rows(c, d + (size_t)r * c->n, e - r, rm, inverse != 0);
+    r = e;
+  }
+  if (!s) {
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (e == cudaSuccess) e = cudaMemcpy(data, d, bytes, cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  }
+  cudaFree(d);
+  return s;
+}

@@ -1,0 +1,339 @@
+// enroll.cu -- enrollment (Alg. enroller_bsgs) and CKKS encoding on the GPU.
+//
+// Pipeline per aggregate (K16 of SURVEY 2.2): upload the aggregate's rows ->
+// normalise (Step 1, R16: sequential double sum, IEEE-rounded ops, no FMA) ->
+// pack the slot vectors of a batch of diagonals (Steps 2-5: diagonal, giant-step
+// right pre-shift shiftN, stride-2N placement) -> special inverse FFT (R15,
+// HEAAN order, __dmul_rn/__dadd_rn so nothing is contracted) -> bit-reverse,
+// / numSlots, x Delta, round-half-even -> residues mod q_l -> NTT, written
+// straight into the device-resident diagonal array D[a][k][l][t].
+#include <cmath>
+
+#include "common.cuh"
+#include "ks.cuh"
+
+namespace {
+constexpr int TPB = 256;
+
+__global__ void normalize_rows_kernel(const float *__restrict__ v, int rows, int dim, double *__restrict__ U,
+                                      int *flag) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const float *x = v + (size_t)r * dim;
+  double s = 0.0;
+  for (int i = 0; i < dim; i++) {
+    double xi = (double)x[i];
+    s = __dadd_rn(s, __dmul_rn(xi, xi));
+  }
+  if (s == 0.0) {
+    atomicExch(flag, 1);
+    return;
+  }
+  double nrm = __dsqrt_rn(s);
+  double *u = U + (size_t)r * dim;
+  for (int i = 0; i < dim; i++) u[i] = __ddiv_rn((double)x[i], nrm);
+}
+
+// Slot vectors of diagonals k0..k0+B-1 of aggregate `agg` (R4):
+// slot b*2N + t (t < N) = diagonal_g[k][(t - shiftN) mod N], g = agg*M/2 + b,
+// diagonal_g[k][s] = U[g N + s][(s + k) mod N] (0 beyond the database); gaps 0.
+__global__ void pack_kernel(const double *__restrict__ U, long long v_first, long long num_vectors, int N, int M,
+                            int n1, long long agg, int k0, int ns, double *__restrict__ re, double *__restrict__ im) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int kk = blockIdx.y;
+  if (s >= ns) return;
+  const int k = k0 + kk;
+  const int b = s / (2 * N), t = s % (2 * N);
+  double val = 0.0;
+  if (t < N) {
+    const int ks = k < N / 2 ? k : k - N;
+    const int j = ks >= 0 ? ks / n1 : -((-ks + n1 - 1) / n1);  // floor (R3)
+    const int shift = ((n1 * j) % N + N) % N;
+    const int src = (t - shift + N) % N;
+    const long long g = agg * (M / 2) + b;
+    const long long v = g * N + src;
+    if (v < num_vectors) val = U[(size_t)(v - v_first) * N + ((src + k) % N)];
+  }
+  re[(size_t)kk * ns + s] = val;
+  im[(size_t)kk * ns + s] = 0.0;
+}
+
+// One stage (len) of the special inverse FFT over B vectors of ns complex slots.
+__global__ void fft_inv_stage_kernel(double *__restrict__ re, double *__restrict__ im, int ns, int len,
+                                     const uint32_t *__restrict__ rotg, const double *__restrict__ xr,
+                                     const double *__restrict__ xim, uint32_t two_n) {
+  const int bf = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bf >= ns / 2) return;
+  const size_t base = (size_t)blockIdx.y * ns;
+  const int lenh = len >> 1;
+  const uint32_t lenq = (uint32_t)len << 2;
+  const int blk = bf / lenh, j = bf % lenh;
+  const int i0 = blk * len + j, i1 = i0 + lenh;
+  const uint32_t idx = (lenq - (rotg[j] % lenq)) * (two_n / lenq);
+  const double wr = xr[idx], wi = xim[idx];
+  const double ar = re[base + i0], ai = im[base + i0], br = re[base + i1], bi = im[base + i1];
+  const double ur = __dadd_rn(ar, br), ui = __dadd_rn(ai, bi);
+  const double vr = __dsub_rn(ar, br), vi = __dsub_rn(ai, bi);
+  re[base + i0] = ur;
+  im[base + i0] = ui;
+  re[base + i1] = __dsub_rn(__dmul_rn(vr, wr), __dmul_rn(vi, wi));
+  im[base + i1] = __dadd_rn(__dmul_rn(vr, wi), __dmul_rn(vi, wr));
+}
+
+// bit-reverse, / ns, x delta, llrint, residues: out[b][l][c] for c < n.
+__global__ void round_kernel(const double *__restrict__ re, const double *__restrict__ im, int ns, int logns,
+                             double delta, int nlimbs, uint64_t *__restrict__ out, size_t out_stride, ModTab mt,
+                             int *flag) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int n = 2 * ns;
+  if (c >= n) return;
+  const size_t b = blockIdx.y;
+  const int k = c < ns ? c : c - ns;
+  const uint32_t src = __brev((uint32_t)k) >> (32 - logns);
+  const double v = (c < ns ? re : im)[b * ns + src];
+  const double x = __dmul_rn(__ddiv_rn(v, (double)ns), delta);
+  if (!(fabs(x) < 4611686018427387904.0)) atomicExch(flag, 2);
+  const long long coef = __double2ll_rn(x);
+  uint64_t *o = out + b * out_stride + c;
+  for (int l = 0; l < nlimbs; l++) {
+    const uint64_t q = mt.q[l];
+    uint64_t r;
+    if (coef >= 0) {
+      r = reduce64((uint64_t)coef, q, mt.bar[l]);
+    } else {
+      r = reduce64((uint64_t)(-coef), q, mt.bar[l]);
+      r = r ? q - r : 0;
+    }
+    o[(size_t)l * n] = r;
+  }
+}
+}  // namespace
+
+hd_status encode_batch(hd_context *c, double *re, double *im, uint32_t B, double delta, int nlimbs, uint64_t *out,
+                       size_t out_stride) {
+  const int ns = c->ns;
+  int logns = c->logn - 1;
+  dim3 g((ns / 2 + TPB - 1) / TPB, B);
+  for (int len = ns; len >= 2; len >>= 1)
+    fft_inv_stage_kernel<<<g, TPB, 0, c->stream>>>(re, im, ns, len, c->rotg, c->xi_re, c->xi_im, 2u * c->n);
+  c->launches += c->logn - 1;
+  round_kernel<<<dim3((c->n + TPB - 1) / TPB, B), TPB, 0, c->stream>>>(re, im, ns, logns, delta, nlimbs, out,
+                                                                       out_stride, c->mt, c->d_flag); ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  RowMap rm{};
+  rm.gsize = nlimbs;
+  rm.gstride = out_stride;
+  rm.mdiv = 1;
+  rm.mlen = nlimbs;
+  for (int l = 0; l < nlimbs; l++) rm.midx[l] = l;
+  return ntt_rows(c, out, B * nlimbs, rm, false);
+}
+
+hd_status normalize_on_device(hd_context *c, const float *dv, int rows, int dim, double *U) {
+  normalize_rows_kernel<<<(rows + TPB - 1) / TPB, TPB, 0, c->stream>>>(dv, rows, dim, U, c->d_flag); ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  return HD_OK;
+}
+
+hd_status check_flag(hd_context *c) {
+  int f = 0;
+  HD_CUDA(cudaMemcpyAsync(&f, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  HD_CUDA(cudaStreamSynchronize(c->stream));
+  if (f) {
+    HD_CUDA(cudaMemset(c->d_flag, 0, sizeof(int)));
+    if (f == 1) return hd_fail(HD_E_ZERO_VECTOR, "an input vector is all zero (cannot L2-normalise)");
+    return hd_fail(HD_E_PARAMS, "encoded coefficient exceeds 2^62");
+  }
+  return HD_OK;
+}
+
+// ---------------------------------------------------------------------------
+// layout helpers
+// ---------------------------------------------------------------------------
+static int floordiv_i(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+hd_status layout_make(const hd_context *c, uint64_t K, uint32_t dim, uint32_t n1, hd_layout *lay) {
+  if (dim < 2 || n1 < 1 || K < 1) return hd_fail(HD_E_INVALID_ARG, "vector_dim >= 2, n1 >= 1, num_vectors >= 1");
+  if ((dim & (dim - 1)) != 0 || (uint32_t)c->ns % (2 * dim) != 0)
+    return hd_fail(HD_E_LAYOUT, "vector_dim must be a power of two with numSlots % (2 vector_dim) == 0");
+  memset(lay, 0, sizeof(*lay));
+  lay->vector_dim = dim;
+  lay->n1 = n1;
+  lay->num_slots = c->ns;
+  lay->block_n = dim;                 // N = min(VECTOR_DIM, numSlots) = VECTOR_DIM
+  lay->blocks_m = c->ns / dim;        // M
+  lay->groups_per_ct = lay->blocks_m / 2;
+  lay->num_vectors = K;
+  lay->num_groups = (K + dim - 1) / dim;                                      // G
+  lay->num_aggregates = (2 * lay->num_groups + lay->blocks_m - 1) / lay->blocks_m;  // A
+  lay->giant_min = floordiv_i(-(int)(dim / 2), (int)n1);                      // R6
+  lay->giant_max = floordiv_i((int)(dim / 2) - 1, (int)n1);
+  return HD_OK;
+}
+
+extern "C" hd_status hd_rotation_steps(const hd_context *c, uint32_t vector_dim, uint32_t n1, int32_t *steps,
+                                       size_t cap, size_t *count) {
+  if (!c || !count) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  hd_layout lay;
+  hd_status s = layout_make(c, 1, vector_dim, n1, &lay);
+  if (s) return s;
+  const int N = (int)vector_dim, ns = c->ns;
+  std::vector<char> used(ns, 0);
+  for (uint32_t i = 1; i < n1; i++) used[i % ns] = 1;
+  for (int j = lay.giant_min; j <= lay.giant_max; j++) {
+    int pr = (((int)n1 * j) % N + N) % N;
+    if (pr) used[pr] = 1;
+  }
+  used[ns - N] = 1;
+  size_t cnt = 0;
+  for (int st = 1; st < ns; st++)
+    if (used[st]) {
+      if (steps && cnt < cap) steps[cnt] = st;
+      cnt++;
+    }
+  *count = cnt;
+  if (steps && cnt > cap) return hd_fail(HD_E_INVALID_ARG, "steps capacity too small");
+  return HD_OK;
+}
+
+extern "C" hd_status hd_database_layout(const hd_database *db, hd_layout *out) {
+  if (!db || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *out = db->lay;
+  return HD_OK;
+}
+
+extern "C" void hd_database_destroy(hd_database *db) {
+  if (!db) return;
+  cudaFree(db->D);
+  cudaFree(db->r);
+  cudaFree(db->S);
+  cudaFree(db->Sp);
+  cudaFree(db->y);
+  cudaFree(db->dig);
+  cudaFree(db->u);
+  cudaFree(db->tmp);
+  cudaFree(db->tmp2);
+  cudaFree(db->outbuf);
+  cudaFree(db->kptr);
+  cudaFree(db->gal);
+  delete db;
+}
+
+extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num_vectors, uint32_t vector_dim,
+                               uint32_t n1, uint32_t agg_begin, uint32_t agg_end, hd_database **out) {
+  if (!c || !vectors || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  hd_layout lay;
+  hd_status s = layout_make(c, num_vectors, vector_dim, n1, &lay);
+  if (s) return s;
+  if (agg_end == 0) agg_end = (uint32_t)lay.num_aggregates;
+  if (agg_begin >= agg_end || agg_end > lay.num_aggregates) return hd_fail(HD_E_INVALID_ARG, "bad aggregate range");
+  lay.agg_begin = agg_begin;
+  lay.agg_end = agg_end;
+  HD_CUDA(cudaSetDevice(c->device));
+  hd_database *db = new hd_database();
+  db->ctx = c;
+  db->lay = lay;
+  db->N = vector_dim;
+  db->M = lay.blocks_m;
+  db->n1 = n1;
+  db->A_loc = agg_end - agg_begin;
+  const int N = (int)db->N, L = c->L, n = c->n, ns = c->ns;
+  for (int j = lay.giant_min; j <= lay.giant_max; j++) {
+    int lo = std::max(0, -j * (int)n1 - N / 2), hi = std::min((int)n1 - 1, N / 2 - 1 - j * (int)n1);
+    if (lo > hi) continue;
+    db->js.push_back(j);
+    db->pre.push_back((((int)n1 * j) % N + N) % N);
+  }
+  for (size_t i = 1; i < db->js.size(); i++)
+    if (db->js[i] != db->js[i - 1] + 1) {
+      delete db;
+      return hd_fail(HD_E_LAYOUT, "non-contiguous giant steps");
+    }
+  const size_t A = db->A_loc, nj = db->js.size(), ctL = (size_t)2 * L * n, ct1 = (size_t)2 * (L - 1) * n;
+  const size_t rescale_chunk = std::min<size_t>(A * nj, 256);
+  size_t dig_e = std::max((size_t)L * (L + 1) * n, A * (L - 1) * L * n);
+  size_t u_e = std::max((size_t)(n1 > 1 ? n1 - 1 : 1) * 2 * (L + 1) * n, A * 2 * L * n);
+  size_t tmp_e = std::max({(size_t)(n1 > 1 ? n1 - 1 : 1) * 2 * L * n, A * 2 * L * n, rescale_chunk * 2 * n,
+                           (size_t)L * n});
+  size_t tmp2_e = rescale_chunk * 2 * (L - 1) * n;
+  db->rescale_chunk = (uint32_t)rescale_chunk;
+  struct Req {
+    void **p;
+    size_t bytes;
+  } reqs[] = {{(void **)&db->D, A * N * (size_t)L * n * 8},
+              {(void **)&db->r, (size_t)n1 * ctL * 8},
+              {(void **)&db->S, A * nj * ctL * 8},
+              {(void **)&db->Sp, A * nj * ct1 * 8},
+              {(void **)&db->y, A * ct1 * 8},
+              {(void **)&db->outbuf, A * ct1 * 8},
+              {(void **)&db->dig, dig_e * 8},
+              {(void **)&db->u, u_e * 8},
+              {(void **)&db->tmp, tmp_e * 8},
+              {(void **)&db->tmp2, tmp2_e * 8}};
+  size_t total = 0;
+  for (auto &q : reqs) total += q.bytes;
+  size_t fr = 0, tot = 0;
+  HD_CUDA(cudaMemGetInfo(&fr, &tot));
+  if (total + (256ull << 20) > fr) {
+    delete db;
+    return hd_fail(HD_E_CAPACITY, "database of " + std::to_string(total >> 20) + " MiB exceeds free device memory (" +
+                                      std::to_string(fr >> 20) + " MiB); shard the aggregates over more GPUs");
+  }
+  for (auto &q : reqs) {
+    cudaError_t e = cudaMalloc(q.p, q.bytes);
+    if (e != cudaSuccess) {
+      hd_database_destroy(db);
+      return hd_fail(HD_E_CAPACITY, std::string("device allocation: ") + cudaGetErrorString(e));
+    }
+  }
+  db->bytes = total;
+  // enrollment scratch: rows of one aggregate (float + double), FFT buffers for a batch of diagonals
+  const size_t rows_per_agg = (size_t)(db->M / 2) * N;
+  const int KB = std::min(N, std::max(1, (int)((256ull << 20) / ((size_t)ns * 16))));
+  float *dv = nullptr;
+  double *U = nullptr, *re = nullptr, *im = nullptr;
+  cudaError_t e = cudaMalloc(&dv, rows_per_agg * N * 4);
+  if (!e) e = cudaMalloc(&U, rows_per_agg * N * 8);
+  if (!e) e = cudaMalloc(&re, (size_t)KB * ns * 8);
+  if (!e) e = cudaMalloc(&im, (size_t)KB * ns * 8);
+  auto cleanup = [&]() {
+    cudaFree(dv);
+    cudaFree(U);
+    cudaFree(re);
+    cudaFree(im);
+  };
+  if (e) {
+    cleanup();
+    hd_database_destroy(db);
+    return hd_fail(HD_E_CAPACITY, "enrollment scratch");
+  }
+  const double delta = (double)c->mod[L - 1];  // Delta_D = q_{L-1} (R15)
+  for (uint32_t a = agg_begin; a < agg_end && !s; a++) {
+    const uint64_t v0 = (uint64_t)a * rows_per_agg;
+    const uint64_t v1 = std::min<uint64_t>(num_vectors, v0 + rows_per_agg);
+    const int rows = (int)(v1 - v0);
+    e = cudaMemcpyAsync(dv, vectors + v0 * N, (size_t)rows * N * 4, cudaMemcpyHostToDevice, c->stream);
+    if (e) {
+      s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    if ((s = normalize_on_device(c, dv, rows, N, U))) break;
+    if ((s = check_flag(c))) break;
+    uint64_t *Da = db->D + (size_t)(a - agg_begin) * N * L * n;
+    for (int k0 = 0; k0 < N && !s; k0 += KB) {
+      int kb = std::min(KB, N - k0);
+      pack_kernel<<<dim3((ns + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(U, (long long)v0, (long long)num_vectors, N,
+                                                                         db->M, n1, a, k0, ns, re, im); ++c->launches;
+      s = encode_batch(c, re, im, kb, delta, L, Da + (size_t)k0 * L * n, (size_t)L * n);
+    }
+    if (!s) s = check_flag(c);
+  }
+  cleanup();
+  if (s) {
+    hd_database_destroy(db);
+    return s;
+  }
+  *out = db;
+  return HD_OK;
+}

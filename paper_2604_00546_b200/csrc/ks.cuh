@@ -1,0 +1,34 @@
+// ks.cuh -- host drivers of the key-switching / rescale / MAC / encode kernels.
+#pragma once
+#include "common.cuh"
+
+// ModUp (R11) of B c1 polynomials at ell limbs (c1 of ciphertext b at c1 + b*c1_stride).
+// dig: [B][ell][ell+1][n] (slot layout: see ks.cu).  tmp: B*ell*n scratch.
+hd_status ks_modup(hd_context *c, const uint64_t *c1, size_t c1_stride, uint32_t B, int ell, uint64_t *dig,
+                   uint64_t *tmp);
+// Key inner product for X = B*K (b, k) pairs -> u [X][2][ell+1][n].
+hd_status ks_kip(hd_context *c, const uint64_t *dig, uint32_t B, uint32_t K, int ell,
+                 const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u);
+// ModDown of u [X][2][ell+1][n] (P limb INTT'd in place) -> dst_x (+ pi_{g_k}(c0_b)).
+hd_status ks_moddown(hd_context *c, uint64_t *u, uint32_t X, uint32_t K, int ell, const uint32_t *gal_dev,
+                     const uint64_t *c0, size_t c0_stride, uint64_t *dst, size_t dst_stride, bool accumulate,
+                     uint64_t *tmp);
+// Rescale B ciphertexts at ell limbs (S_b at S + b*s_stride) -> out_b (ell-1 limbs).
+hd_status ks_rescale(hd_context *c, const uint64_t *S, size_t s_stride, uint32_t B, int ell, uint64_t *out,
+                     size_t out_stride, uint64_t *tmp1, uint64_t *tmp2);
+hd_status ct_add(hd_context *c, uint64_t *dst, size_t dst_stride, const uint64_t *src, size_t src_stride,
+                 uint32_t B, int ell);
+
+// MAC (mac.cu)
+struct MacPlan {
+  int n1, N, L, logn;
+  int jmin, nj;        // valid giant steps j = js[0..nj)
+  const int32_t *js;   // host
+};
+hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
+                  const std::vector<int32_t> &js);
+
+// encode (enroll.cu)
+hd_status encode_batch(hd_context *c, double *re, double *im, uint32_t B, double delta, int nlimbs,
+                       uint64_t *out, size_t out_stride);
+hd_status alloc_ct(hd_context *c, uint32_t limbs, hd_ciphertext **out);

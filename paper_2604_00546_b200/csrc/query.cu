@@ -1,0 +1,267 @@
+// query.cu -- the online scan (Alg. sender-bsgs) with the fold
+// schedule of DESIGN.md R2, orchestrated on the context stream:
+//   a2/a3  hoisted ModUp of q.c1, batched KIP over the n1-1 baby keys, batched ModDown
+//   a5     MAC over every local aggregate and giant step (one launch)
+//   a6     rescale of every giant-step sum (batched)
+//   a7     per giant step j with preRot(j) != 0: ModUp of the c1 of S'_{a,j} for all
+//          local aggregates a, KIP with key preRot(j) (read once for all a), ModDown
+//          accumulated into y_a; S'_{a,j} with preRot = 0 added directly
+//   a8     fold: out_a = y_a + Rot_{numSlots-N}(y_a), batched over a
+#include <cstring>
+
+#include "common.cuh"
+#include "ks.cuh"
+
+static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
+  hd_context *c = db->ctx;
+  if (db->keyed_for == evk && db->kptr) return HD_OK;
+  const int n1 = (int)db->n1, nj = (int)db->js.size();
+  const size_t cnt = (size_t)(n1 - 1) + nj + 1;
+  std::vector<const uint64_t *> kp(cnt, nullptr);
+  std::vector<uint32_t> gl(cnt, 1);
+  auto need = [&](int32_t step, size_t slot) -> hd_status {
+    const uint64_t *k = evk->find(step);
+    if (!k) return hd_fail(HD_E_MISSING_KEY, "missing rotation key for step " + std::to_string(step));
+    kp[slot] = k;
+    gl[slot] = (uint32_t)host_powmod(5, (uint64_t)step, 2ull * c->n);
+    return HD_OK;
+  };
+  hd_status s;
+  for (int i = 1; i < n1; i++)
+    if ((s = need(i, i - 1))) return s;
+  for (int jj = 0; jj < nj; jj++)
+    if (db->pre[jj] && (s = need(db->pre[jj], n1 - 1 + jj))) return s;
+  if ((s = need(c->ns - (int)db->N, cnt - 1))) return s;
+  if (!db->kptr) {
+    HD_CUDA(cudaMalloc(&db->kptr, cnt * sizeof(uint64_t *)));
+    HD_CUDA(cudaMalloc(&db->gal, cnt * sizeof(uint32_t)));
+  }
+  HD_CUDA(cudaMemcpyAsync(db->kptr, kp.data(), cnt * sizeof(uint64_t *), cudaMemcpyHostToDevice, c->stream));
+  HD_CUDA(cudaMemcpyAsync(db->gal, gl.data(), cnt * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+  HD_CUDA(cudaStreamSynchronize(c->stream));
+  db->keyed_for = evk;
+  return HD_OK;
+}
+
+static hd_status run_scan(hd_database *db, const hd_ciphertext *query) {
+  hd_context *c = db->ctx;
+  const int n = c->n, L = c->L, n1 = (int)db->n1, nj = (int)db->js.size();
+  const uint32_t A = db->A_loc;
+  const size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * (L - 1) * n;
+  hd_status s;
+  cudaEvent_t *E = c->ev[c->ev_next % 64];
+  c->ev_next++;
+  c->ev_pending = std::min(c->ev_pending + 1, 64);
+  cudaEventRecord(E[0], c->stream);
+  // ---- baby steps: r[0] = q; r[i] = Rot_i(q), hoisted ----
+  HD_CUDA(cudaMemcpyAsync(db->r, query->data, ctL * 8, cudaMemcpyDeviceToDevice, c->stream));
+  if (n1 > 1) {
+    if ((s = ks_modup(c, query->data + (size_t)L * n, 0, 1, L, db->dig, db->tmp))) return s;
+    if ((s = ks_kip(c, db->dig, 1, n1 - 1, L, db->kptr, db->gal, db->u))) return s;
+    if ((s = ks_moddown(c, db->u, n1 - 1, n1 - 1, L, db->gal, query->data, 0, db->r + ctL, ctL, false, db->tmp)))
+      return s;
+  }
+  cudaEventRecord(E[1], c->stream);
+  // ---- MAC ----
+  if ((s = mac_run(c, db->D, db->r, db->S, A, n1, (int)db->N, db->js))) return s;
+  cudaEventRecord(E[2], c->stream);
+  // ---- rescale every S_{a,j} ----
+  const uint32_t total = A * nj;
+  for (uint32_t b0 = 0; b0 < total; b0 += db->rescale_chunk) {
+    uint32_t B = std::min(db->rescale_chunk, total - b0);
+    if ((s = ks_rescale(c, db->S + (size_t)b0 * ctL, ctL, B, L, db->Sp + (size_t)b0 * ct1, ct1, db->tmp, db->tmp2)))
+      return s;
+  }
+  cudaEventRecord(E[3], c->stream);
+  // ---- giant rotations and sum (R2) ----
+  HD_CUDA(cudaMemsetAsync(db->y, 0, (size_t)A * ct1 * 8, c->stream));
+  const size_t sp_stride = (size_t)nj * ct1;  // between aggregates for fixed j
+  for (int jj = 0; jj < nj; jj++) {
+    const uint64_t *Sj = db->Sp + (size_t)jj * ct1;
+    if (db->pre[jj] == 0) {
+      if ((s = ct_add(c, db->y, ct1, Sj, sp_stride, A, L - 1))) return s;
+      continue;
+    }
+    const size_t slot = (size_t)(n1 - 1) + jj;
+    if ((s = ks_modup(c, Sj + (size_t)(L - 1) * n, sp_stride, A, L - 1, db->dig, db->tmp))) return s;
+    if ((s = ks_kip(c, db->dig, A, 1, L - 1, db->kptr + slot, db->gal + slot, db->u))) return s;
+    if ((s = ks_moddown(c, db->u, A, 1, L - 1, db->gal + slot, Sj, sp_stride, db->y, ct1, true, db->tmp))) return s;
+  }
+  cudaEventRecord(E[4], c->stream);
+  // ---- fold: out = y + Rot_{numSlots - N}(y) ----
+  {
+    const size_t slot = (size_t)(n1 - 1) + nj;
+    HD_CUDA(cudaMemcpyAsync(db->outbuf, db->y, (size_t)A * ct1 * 8, cudaMemcpyDeviceToDevice, c->stream));
+    if ((s = ks_modup(c, db->y + (size_t)(L - 1) * n, ct1, A, L - 1, db->dig, db->tmp))) return s;
+    if ((s = ks_kip(c, db->dig, A, 1, L - 1, db->kptr + slot, db->gal + slot, db->u))) return s;
+    if ((s = ks_moddown(c, db->u, A, 1, L - 1, db->gal + slot, db->y, ct1, db->outbuf, ct1, true, db->tmp))) return s;
+  }
+  cudaEventRecord(E[5], c->stream);
+  return HD_OK;
+}
+
+extern "C" hd_status hd_query(hd_context *c, const hd_eval_keys *evk, const hd_database *dbc,
+                              const hd_ciphertext *query, hd_ciphertext **out, size_t n_out) {
+  if (!c || !evk || !dbc || !query || (!out && n_out)) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  hd_database *db = const_cast<hd_database *>(dbc);
+  if (db->ctx != c || evk->ctx != c || query->ctx != c) return hd_fail(HD_E_STATE, "objects from another context");
+  if (query->limbs != (uint32_t)c->L) return hd_fail(HD_E_LEVEL, "query must be at L limbs");
+  if (n_out != db->A_loc) return hd_fail(HD_E_INVALID_ARG, "n_out must equal agg_end - agg_begin");
+  const int L = c->L, n = c->n;
+  const size_t ct1 = (size_t)2 * (L - 1) * n;
+  hd_status s = bind_keys(db, evk);
+  if (s) return s;
+  for (size_t i = 0; i < n_out; i++) {
+    if (out[i] && (out[i]->ctx != c || out[i]->limbs != (uint32_t)(L - 1)))
+      return hd_fail(HD_E_LEVEL, "reused output ciphertext has the wrong shape");
+  }
+  std::vector<hd_ciphertext *> fresh;
+  for (size_t i = 0; i < n_out; i++)
+    if (!out[i]) {
+      hd_ciphertext *ct;
+      if ((s = alloc_ct(c, L - 1, &ct))) {
+        for (auto *f : fresh) hd_ciphertext_destroy(f);
+        return s;
+      }
+      fresh.push_back(ct);
+    }
+  if ((s = run_scan(db, query))) {
+    for (auto *f : fresh) hd_ciphertext_destroy(f);
+    return s;
+  }
+  size_t fi = 0;
+  for (size_t i = 0; i < n_out; i++) {
+    if (!out[i]) out[i] = fresh[fi++];
+    HD_CUDA(cudaMemcpyAsync(out[i]->data, db->outbuf + i * ct1, ct1 * 8, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  HD_CUDA(cudaGetLastError());
+  db->has_run = true;
+  // per-phase times are read lazily by hd_query_stats (no sync here)
+
+  return HD_OK;
+}
+
+extern "C" hd_status hd_query_stats(const hd_context *cc, double *phase_ms, size_t n_phases) {
+  if (!cc || !phase_ms) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  hd_context *c = const_cast<hd_context *>(cc);
+  // average over the queries issued since the previous call (up to the last 64)
+  if (c->ev_pending > 0) {
+    double acc[5] = {0, 0, 0, 0, 0};
+    const int last = (c->ev_next - 1) % 64;
+    HD_CUDA(cudaEventSynchronize(c->ev[last][5]));
+    for (int q = 0; q < c->ev_pending; q++) {
+      const int idx = ((c->ev_next - 1 - q) % 64 + 64) % 64;
+      for (int i = 0; i < 5; i++) {
+        float ms = 0;
+        HD_CUDA(cudaEventElapsedTime(&ms, c->ev[idx][i], c->ev[idx][i + 1]));
+        acc[i] += ms;
+      }
+    }
+    for (int i = 0; i < 5; i++) c->last_phase_ms[i] = acc[i] / c->ev_pending;
+    c->ev_pending = 0;
+  }
+  for (size_t i = 0; i < n_phases && i < 5; i++) phase_ms[i] = c->last_phase_ms[i];
+  return HD_OK;
+}
+
+extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t agg, int32_t index, uint64_t *host_dst,
+                                   size_t cap) {
+  if (!db || !host_dst) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  const hd_context *c = db->ctx;
+  const int n = c->n, L = c->L, nj = (int)db->js.size();
+  const size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * (L - 1) * n, ptL = (size_t)L * n;
+  if (agg < db->lay.agg_begin || agg >= db->lay.agg_end) return hd_fail(HD_E_INVALID_ARG, "aggregate not in database");
+  const size_t a = agg - db->lay.agg_begin;
+  const uint64_t *src = nullptr;
+  size_t len = 0;
+  int jj = index - (db->js.empty() ? 0 : db->js.front());
+  switch (which) {
+    case 0:
+      if (index < 0 || index >= (int)db->n1) return hd_fail(HD_E_INVALID_ARG, "baby index");
+      src = db->r + (size_t)index * ctL, len = ctL;
+      break;
+    case 1:
+      if (jj < 0 || jj >= nj) return hd_fail(HD_E_INVALID_ARG, "giant index");
+      src = db->S + (a * nj + jj) * ctL, len = ctL;
+      break;
+    case 2:
+      if (jj < 0 || jj >= nj) return hd_fail(HD_E_INVALID_ARG, "giant index");
+      src = db->Sp + (a * nj + jj) * ct1, len = ct1;
+      break;
+    case 3:
+      src = db->y + a * ct1, len = ct1;
+      break;
+    case 4:
+      if (index < 0 || index >= (int)db->N) return hd_fail(HD_E_INVALID_ARG, "diagonal index");
+      src = db->D + (a * db->N + index) * ptL, len = ptL;
+      break;
+    default:
+      return hd_fail(HD_E_INVALID_ARG, "stage");
+  }
+  if (which < 4 && !db->has_run) return hd_fail(HD_E_STATE, "no query has run on this database");
+  if (cap < len) return hd_fail(HD_E_INVALID_ARG, "capacity too small");
+  HD_CUDA(cudaStreamSynchronize(c->stream));
+  HD_CUDA(cudaMemcpy(host_dst, src, len * 8, cudaMemcpyDeviceToHost));
+  return HD_OK;
+}
+
+extern "C" hd_status hd_test_rotate(hd_context *c, const hd_eval_keys *evk, const hd_ciphertext *ct, int32_t step,
+                                    hd_ciphertext **out) {
+  if (!c || !evk || !ct || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  const uint64_t *k = evk->find(step);
+  if (!k) return hd_fail(HD_E_MISSING_KEY, "missing rotation key for step " + std::to_string(step));
+  const int n = c->n, L = c->L, ell = (int)ct->limbs;
+  uint64_t *dig, *u, *tmp, **kp;
+  uint32_t *g;
+  uint32_t gh = (uint32_t)host_powmod(5, (uint64_t)step, 2ull * n);
+  HD_CUDA(cudaMalloc(&dig, (size_t)ell * (ell + 1) * n * 8));
+  HD_CUDA(cudaMalloc(&u, (size_t)2 * (ell + 1) * n * 8));
+  HD_CUDA(cudaMalloc(&tmp, (size_t)2 * (ell + 1) * n * 8));
+  HD_CUDA(cudaMalloc(&kp, sizeof(uint64_t *)));
+  HD_CUDA(cudaMalloc(&g, 4));
+  HD_CUDA(cudaMemcpy(kp, &k, sizeof(uint64_t *), cudaMemcpyHostToDevice));
+  HD_CUDA(cudaMemcpy(g, &gh, 4, cudaMemcpyHostToDevice));
+  hd_ciphertext *o;
+  hd_status s = alloc_ct(c, ell, &o);
+  if (!s) s = ks_modup(c, ct->data + (size_t)ell * n, 0, 1, ell, dig, tmp);
+  if (!s) s = ks_kip(c, dig, 1, 1, ell, (const uint64_t *const *)kp, g, u);
+  if (!s) s = ks_moddown(c, u, 1, 1, ell, g, ct->data, 0, o->data, 0, false, tmp);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (!s && e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  cudaFree(dig);
+  cudaFree(u);
+  cudaFree(tmp);
+  cudaFree(kp);
+  cudaFree(g);
+  (void)L;
+  if (s) {
+    hd_ciphertext_destroy(o);
+    return s;
+  }
+  *out = o;
+  return HD_OK;
+}
+
+extern "C" hd_status hd_test_rescale(hd_context *c, const hd_ciphertext *ct, hd_ciphertext **out) {
+  if (!c || !ct || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  if (ct->limbs < 2) return hd_fail(HD_E_LEVEL, "cannot rescale a 1-limb ciphertext");
+  const int n = c->n, ell = (int)ct->limbs;
+  uint64_t *t1, *t2;
+  HD_CUDA(cudaMalloc(&t1, (size_t)2 * n * 8));
+  HD_CUDA(cudaMalloc(&t2, (size_t)2 * ell * n * 8));
+  hd_ciphertext *o;
+  hd_status s = alloc_ct(c, ell - 1, &o);
+  if (!s) s = ks_rescale(c, ct->data, 0, 1, ell, o->data, 0, t1, t2);
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (!s && e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  cudaFree(t1);
+  cudaFree(t2);
+  if (s) {
+    hd_ciphertext_destroy(o);
+    return s;
+  }
+  *out = o;
+  return HD_OK;
+}

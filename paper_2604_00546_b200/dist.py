@@ -1,0 +1,57 @@
+"""Multi-GPU plumbing: one process per GPU, torch.distributed (NCCL) for the two
+real exchanges of the serving path:
+
+  * broadcast of the query ciphertext bytes from rank 0 (a1), and of the
+    exported evaluation keys once at setup;
+  * gather of the per-rank score ciphertexts to rank 0 (a9).
+
+The database is sharded by aggregate: rank r owns aggregates
+[floor(r A / P), floor((r + 1) A / P)) and enrolls only their rows; no
+collective touches the diagonals.  These helpers move opaque byte tensors
+(device tensors under NCCL, CPU tensors under gloo) and hold no arithmetic.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+def shard_range(num_aggregates: int, rank: int, world: int):
+    """Contiguous aggregate range of `rank` (sizes differ by at most one)."""
+    return (num_aggregates * rank) // world, (num_aggregates * (rank + 1)) // world
+
+
+def rows_of_aggregates(agg_begin: int, agg_end: int, per_aggregate: int, num_vectors: int):
+    return min(agg_begin * per_aggregate, num_vectors), min(agg_end * per_aggregate, num_vectors)
+
+
+def broadcast_bytes(buf: torch.Tensor | None, nbytes: int, device, src: int = 0) -> torch.Tensor:
+    """Broadcast a uint8 tensor of known size from `src`; returns the tensor on every rank."""
+    if dist.get_rank() != src or buf is None:
+        buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+    dist.broadcast(buf, src=src)
+    return buf
+
+
+def gather_bytes(local: torch.Tensor, max_bytes: int, dst: int = 0):
+    """Gather variable-size uint8 tensors (padded to max_bytes) to `dst`.
+
+    Returns the list of per-rank tensors (trimmed) on dst, None elsewhere."""
+    world = dist.get_world_size()
+    n = torch.tensor([local.numel()], dtype=torch.int64, device=local.device)
+    sizes = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(sizes, n)
+    padded = torch.zeros(max_bytes, dtype=torch.uint8, device=local.device)
+    padded[: local.numel()] = local
+    if dist.get_rank() == dst:
+        bufs = [torch.empty(max_bytes, dtype=torch.uint8, device=local.device) for _ in range(world)]
+        dist.gather(padded, gather_list=bufs, dst=dst)
+        return [b[: int(s.item())] for b, s in zip(bufs, sizes)]
+    dist.gather(padded, dst=dst)
+    return None
+
+
+def max_over_ranks(x: float, device) -> float:
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())

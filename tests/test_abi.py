@@ -1,0 +1,56 @@
+"""The C-ABI library loads and exports every symbol include/hd.h declares (not gpu).
+
+No compute call is made here; on a box without a GPU the context constructor
+must refuse (no CPU fallback)."""
+import ctypes as C
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    src = open(os.path.join(ROOT, "include", "hd.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(hd_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_declares_the_north_star_calls():
+    names = _declared()
+    for call in ("hd_keygen", "hd_enroll", "hd_query", "hd_decrypt_scores", "hd_encrypt_query",
+                 "hd_rotation_steps", "hd_context_create"):
+        assert call in names
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_2604_00546_b200 as hd
+    lib = hd.load()
+    path = hd.lib_path()
+    assert os.path.exists(path)
+    missing = [n for n in _declared() if not hasattr(lib, n)]
+    assert not missing, missing
+    assert set(_declared()) == set(hd.ABI_FUNCTIONS)
+    # every symbol is a plain C symbol (extern "C": unmangled)
+    raw = C.CDLL(path)
+    for n in _declared():
+        getattr(raw, n)
+
+
+def test_library_is_sm100a():
+    import subprocess
+    import paper_2604_00546_b200 as hd
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", hd.lib_path()],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_no_cpu_fallback_without_device():
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    import paper_2604_00546_b200 as hd
+    with pytest.raises(hd.HDError) as e:
+        hd.Context(12)
+    assert e.value.code == hd.HD_E_CUDA

@@ -1,0 +1,75 @@
+"""Multi-process host logic of the N > 1 path on CPU (gloo, world size 2 and 3).
+
+The NCCL path moves the same opaque byte tensors: the exported query ciphertext is
+broadcast from rank 0 and the per-rank score ciphertexts are gathered to rank 0.
+Here the bytes are the oracle's own ciphertext residues, so a bit flip anywhere in
+the plumbing fails the comparison."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2604_00546_b200 import dist as hdd
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, payload, results):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = 7
+        a0, a1 = hdd.shard_range(A, rank, world)
+        # query broadcast: only rank 0 holds the bytes
+        src = torch.from_numpy(payload.copy()) if rank == 0 else None
+        got = hdd.broadcast_bytes(src, payload.nbytes, "cpu")
+        ok_bcast = bool((got.numpy() == payload).all())
+        # each rank "produces" one score ciphertext per local aggregate: tagged copies
+        local = torch.from_numpy(np.concatenate([np.roll(payload, a) for a in range(a0, a1)]) if a1 > a0
+                                 else np.zeros(0, np.uint8))
+        per = payload.nbytes
+        gathered = hdd.gather_bytes(local, ((A + world - 1) // world) * per, 0)
+        mx = hdd.max_over_ranks(float(rank + 1), "cpu")
+        if rank == 0:
+            flat = torch.cat(gathered).numpy()
+            want = np.concatenate([np.roll(payload, a) for a in range(A)])
+            results.put(("gather", bool((flat == want).all())))
+        results.put(("bcast", ok_bcast))
+        results.put(("range", (a0, a1)))
+        results.put(("max", mx))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_broadcast_gather_and_sharding(world, oracle_mod):
+    o = oracle_mod.Oracle(6, 3)
+    s, s_ntt = o.secret_key()
+    z = np.linspace(-1, 1, o.ns)
+    ct = o.encrypt(s_ntt, o.encode(z, 2.0 ** 45, 3), 1000)
+    payload = ct.view(np.uint8).ravel()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, payload, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = [q.get() for _ in range(3 * world + 1)]
+    assert all(v for k, v in res if k in ("gather", "bcast"))
+    ranges = sorted(v for k, v in res if k == "range")
+    assert ranges[0][0] == 0 and ranges[-1][1] == 7
+    assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
+    assert all(v == world for k, v in res if k == "max")

@@ -1,0 +1,259 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle, bit-exact on
+every RNS residue; decrypted scores vs brute-force cosine within 1e-3 (north star).
+
+Sizes: the toy config C1 (every stage, every aggregate), C2 (2^15 ring, all
+aggregates), and the bench configuration C4 (2^16 ring, 2^20 x 512, n1 = 64) on
+a sampled aggregate the oracle computes one by one.
+"""
+import numpy as np
+import pytest
+
+from synth_inputs import CONFIGS, ENC_SEED_BASE, dataset_rows, make_dataset
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2604_00546_b200 as hd  # noqa: E402
+
+
+def _cos(db, q):
+    d = db.astype(np.float64)
+    qq = q.astype(np.float64)
+    return d @ qq / (np.linalg.norm(d, axis=1) * np.linalg.norm(qq))
+
+
+class Run:
+    """One config: GPU objects + oracle objects on identical seeded inputs."""
+
+    def __init__(self, cfg, full_db=True, agg_range=(0, 0)):
+        self.cfg = cfg
+        self.ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
+        self.o = oracle.Oracle(cfg.log_n, cfg.limbs, seed=1)
+        self.db_vecs, self.q, self.pos = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+        self.steps = self.ctx.rotation_steps(cfg.dim, cfg.n1)
+        self.sk, self.evk = self.ctx.keygen(self.steps)
+        self.qct = self.ctx.encrypt_query(self.sk, self.q, ENC_SEED_BASE)
+        self.db = self.ctx.enroll(self.db_vecs, cfg.n1, *agg_range)
+        self.outs = self.ctx.query(self.evk, self.db, self.qct)
+        torch.cuda.synchronize()
+        self._okeys = None
+
+    # oracle side -----------------------------------------------------------------------------
+    def oracle_keys(self):
+        if self._okeys is None:
+            s, s_ntt = self.o.secret_key()
+            steps, keys = self.o.keyset(s_ntt, [int(x) for x in self.steps])
+            self._okeys = (s_ntt, steps, keys)
+        return self._okeys
+
+    def oracle_query_ct(self):
+        s_ntt, _, _ = self.oracle_keys()
+        z = self.o.query_slots(self.q)
+        return self.o.encrypt(s_ntt, self.o.encode(z, 2.0 ** 45, self.cfg.limbs), ENC_SEED_BASE)
+
+    def oracle_D(self, agg):
+        cfg = self.cfg
+        per = (self.o.ns // cfg.dim // 2) * cfg.dim
+        pair = agg - agg % 2   # Alg. enroller_bsgs builds the (ctA, ctB) pair from one temporary
+        v0, v1 = pair * per, min(cfg.num_vectors, (pair + 2) * per)
+        U = self.o.normalize_rows(self.db_vecs[v0:v1])
+        return self.o.enroll_aggregate(U, v0, cfg.num_vectors, cfg.n1, agg)
+
+
+@pytest.fixture(scope="module")
+def toy():
+    return Run(CONFIGS["C1"])
+
+
+def test_moduli_and_roots_match_oracle(toy):
+    mods, psi = toy.ctx.moduli()
+    assert mods == toy.o.p.moduli
+    assert psi == [int(toy.o.p.psi[i]) for i in range(toy.cfg.limbs + 1)]
+
+
+@pytest.mark.parametrize("log_n", [12, 15, 16])
+def test_ntt_bit_exact(log_n):
+    ctx = hd.Context(log_n, 3)
+    o = oracle.Oracle(log_n, 3)
+    rng = np.random.default_rng(log_n)
+    rows, mi = [], []
+    for l, m in enumerate(o.p.moduli):
+        for _ in range(3):
+            rows.append(rng.integers(0, m, o.n, dtype=np.uint64))
+            mi.append(l)
+    rows = np.stack(rows)
+    fwd = ctx.test_ntt(rows, mi)
+    inv = ctx.test_ntt(rows, mi, inverse=True)
+    for r in range(len(rows)):
+        assert (fwd[r] == o.ntt(rows[r], mi[r])).all()
+        assert (inv[r] == o.ntt(rows[r], mi[r], inverse=True)).all()
+    # edge values: 0 and q-1 everywhere
+    for l, m in enumerate(o.p.moduli):
+        for v in (0, m - 1):
+            row = np.full((1, o.n), v, np.uint64)
+            assert (ctx.test_ntt(row, [l])[0] == o.ntt(row[0], l)).all()
+
+
+def test_keys_bit_exact(toy):
+    s_ntt, steps, keys = toy.oracle_keys()
+    assert (toy.ctx.secret_key_export(toy.sk) == s_ntt).all()
+    gsteps, gkeys = hd.eval_key_residues(toy.ctx, toy.ctx.eval_keys_export(toy.evk))
+    assert list(gsteps) == list(steps)
+    assert (gkeys == keys).all()
+
+
+def test_query_encryption_bit_exact(toy):
+    assert (toy.ctx.ciphertext_residues(toy.qct) == toy.oracle_query_ct()).all()
+
+
+def test_rotate_and_rescale_bit_exact(toy):
+    s_ntt, steps, keys = toy.oracle_keys()
+    qo = toy.oracle_query_ct()
+    for st in (1, 5, int(steps[-1])):
+        k = keys[list(steps).index(st)]
+        got = toy.ctx.ciphertext_residues(toy.ctx.test_rotate(toy.evk, toy.qct, st))
+        assert (got == toy.o.rotate(qo, k, st)).all()
+    got = toy.ctx.ciphertext_residues(toy.ctx.test_rescale(toy.qct))
+    assert (got == toy.o.rescale(qo)).all()
+
+
+def test_enrollment_bit_exact(toy):
+    D = toy.oracle_D(0)
+    for k in range(toy.cfg.dim):
+        assert (toy.ctx.test_stage(toy.db, 4, 0, k) == D[k]).all(), k
+
+
+def test_toy_every_stage_bit_exact(toy):
+    o, cfg = toy.o, toy.cfg
+    s_ntt, steps, keys = toy.oracle_keys()
+    r = o.baby_steps(toy.oracle_query_ct(), cfg.n1, steps, keys)
+    for i in range(cfg.n1):
+        assert (toy.ctx.test_stage(toy.db, 0, 0, i) == r[i]).all(), f"r[{i}]"
+    D = toy.oracle_D(0)
+    jmin, jmax = o.giant_range(cfg.dim, cfg.n1)
+    for j in range(jmin, jmax + 1):
+        S = o.giant_sum(r, cfg.n1, cfg.dim, D, j)
+        assert (toy.ctx.test_stage(toy.db, 1, 0, j) == S).all(), f"S_{j}"
+        assert (toy.ctx.test_stage(toy.db, 2, 0, j) == o.rescale(S)).all(), f"S'_{j}"
+    out, y = o.scan_aggregate(r, cfg.n1, cfg.dim, D, steps, keys, want_y=True)
+    assert (toy.ctx.test_stage(toy.db, 3, 0, 0) == y).all()
+    assert (toy.ctx.ciphertext_residues(toy.outs[0]) == out).all()
+
+
+def test_toy_scores(toy):
+    sc = toy.ctx.decrypt_scores(toy.sk, toy.db.layout, toy.outs)
+    cos = _cos(toy.db_vecs, toy.q)
+    assert len(sc) == toy.cfg.num_vectors
+    assert np.abs(sc - cos).max() < 1e-3
+    assert np.abs(sc - cos).max() < 1e-6   # noise budget: a larger error is a bug
+    assert sorted(np.argsort(-sc)[:3]) == sorted(toy.pos.tolist())
+    # the oracle's decode of the GPU ciphertext agrees
+    s_ntt, _, _ = toy.oracle_keys()
+    osc = toy.o.decrypt_scores(s_ntt, toy.ctx.ciphertext_residues(toy.outs[0]), toy.cfg.dim, 0,
+                               toy.cfg.num_vectors)
+    assert np.abs(osc[:len(sc)] - sc).max() < 1e-9
+
+
+def test_c2_all_aggregates_bit_exact():
+    run = Run(CONFIGS["C2"])
+    o, cfg = run.o, run.cfg
+    s_ntt, steps, keys = run.oracle_keys()
+    assert (run.ctx.ciphertext_residues(run.qct) == run.oracle_query_ct()).all()
+    r = o.baby_steps(run.oracle_query_ct(), cfg.n1, steps, keys)
+    for i in (0, 1, cfg.n1 - 1):
+        assert (run.ctx.test_stage(run.db, 0, 0, i) == r[i]).all()
+    for a in range(cfg.aggregates):
+        D = run.oracle_D(a)
+        for k in (0, 1, 255, 256, 511):
+            assert (run.ctx.test_stage(run.db, 4, a, k) == D[k]).all()
+        out = o.scan_aggregate(r, cfg.n1, cfg.dim, D, steps, keys)
+        assert (run.ctx.ciphertext_residues(run.outs[a]) == out).all(), a
+    sc = run.ctx.decrypt_scores(run.sk, run.db.layout, run.outs)
+    assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-6
+    assert sorted(np.argsort(-sc)[:3]) == sorted(run.pos.tolist())
+
+
+@pytest.mark.slow
+def test_c4_bench_config_sampled_aggregate():
+    """The bench launch configuration (2^16 ring, 2^20 x 512, n1 = 64, all 64 aggregates
+    on one GPU): bit-exact on a sampled aggregate, scores everywhere vs cosine."""
+    cfg = CONFIGS["C4"]
+    run = Run(cfg)
+    o = run.o
+    s_ntt, steps, keys = run.oracle_keys()
+    r = o.baby_steps(run.oracle_query_ct(), cfg.n1, steps, keys)
+    assert (run.ctx.test_stage(run.db, 0, 0, cfg.n1 - 1) == r[-1]).all()
+    a = 37
+    D = run.oracle_D(a)
+    out = o.scan_aggregate(r, cfg.n1, cfg.dim, D, steps, keys)
+    assert (run.ctx.ciphertext_residues(run.outs[a]) == out).all()
+    sc = run.ctx.decrypt_scores(run.sk, run.db.layout, run.outs)
+    assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-3
+    assert sorted(np.argsort(-sc)[:3]) == sorted(run.pos.tolist())
+
+
+def test_sharding_invariance_and_partial_aggregates():
+    """out_a is bit-identical whatever aggregate range a rank enrolls (P = 1, 2, 3 shards),
+    including an odd A with a partial last aggregate (K not a multiple of N)."""
+    from synth_inputs import Config
+    cfg = Config("shard", 11, 16, 1500, 4, index=9)   # ns = 1024, N = 16, M = 64, G = 94, A = 3
+    full = Run(cfg)
+    assert cfg.aggregates == 3
+    for rng_ in ((0, 1), (1, 3), (2, 3)):
+        db = full.ctx.enroll(full.db_vecs, cfg.n1, *rng_)
+        outs = full.ctx.query(full.evk, db, full.qct)
+        for i, a in enumerate(range(*rng_)):
+            assert (full.ctx.ciphertext_residues(outs[i]) == full.ctx.ciphertext_residues(full.outs[a])).all()
+    s_ntt, steps, keys = full.oracle_keys()
+    r = full.o.baby_steps(full.oracle_query_ct(), cfg.n1, steps, keys)
+    D = full.oracle_D(2)
+    assert (full.ctx.ciphertext_residues(full.outs[2]) ==
+            full.o.scan_aggregate(r, cfg.n1, cfg.dim, D, steps, keys)).all()
+    sc = full.ctx.decrypt_scores(full.sk, full.db.layout, full.outs)
+    assert len(sc) == cfg.num_vectors
+    assert np.abs(sc - _cos(full.db_vecs, full.q)).max() < 1e-6
+
+
+def test_n1_equals_N_and_reused_outputs():
+    from synth_inputs import Config
+    cfg = Config("diag", 12, 64, 300, 64, index=10)   # n1 = N: plain diagonal method, no giant rotation
+    run = Run(cfg)
+    s_ntt, steps, keys = run.oracle_keys()
+    r = run.o.baby_steps(run.oracle_query_ct(), cfg.n1, steps, keys)
+    out = run.o.scan_aggregate(r, cfg.n1, cfg.dim, run.oracle_D(0), steps, keys)
+    assert (run.ctx.ciphertext_residues(run.outs[0]) == out).all()
+    # a second query into the same output handles (in place) gives the same bits
+    again = run.ctx.query(run.evk, run.db, run.qct, outs=run.outs)
+    assert again[0] is run.outs[0]
+    assert (run.ctx.ciphertext_residues(again[0]) == out).all()
+
+
+def test_errors():
+    ctx = hd.Context(12, 3)
+    v = np.ones((100, 64), np.float32)
+    v[17] = 0
+    with pytest.raises(hd.HDError) as e:
+        ctx.enroll(v, 8)
+    assert e.value.code == hd.HD_E_ZERO_VECTOR
+    with pytest.raises(hd.HDError) as e:
+        ctx.enroll(np.ones((10, 48), np.float32), 8)         # not a power of two
+    assert e.value.code == hd.HD_E_LAYOUT
+    with pytest.raises(hd.HDError) as e:
+        ctx.enroll(np.ones((10, 2048), np.float32), 8)       # numSlots % 2N != 0
+    assert e.value.code == hd.HD_E_LAYOUT
+    sk, evk = ctx.keygen(ctx.rotation_steps(64, 8)[:-1])    # drop the fold key
+    db = ctx.enroll(np.ones((100, 64), np.float32), 8)
+    qct = ctx.encrypt_query(sk, np.ones(64, np.float32), 5)
+    with pytest.raises(hd.HDError) as e:
+        ctx.query(evk, db, qct)
+    assert e.value.code == hd.HD_E_MISSING_KEY and "1984" in str(e.value)
+    import ctypes as C
+    big = hd.Context(16, 3)
+    out = C.c_void_p()
+    few = np.ones((4, 512), np.float32)   # the capacity check precedes any read of the rows
+    rc = hd.load().hd_enroll(big.h, few.ctypes.data_as(C.c_void_p), 1 << 26, 512, 64, 0, 0, C.byref(out))
+    assert rc == hd.HD_E_CAPACITY and not out.value          # 2^26 vectors: ~3.3 TB of diagonals
