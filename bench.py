@@ -154,7 +154,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -165,7 +165,14 @@ class ClockSampler:
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) == 6:
-                self.samples.append(parts)
+                self.samples.append((time.perf_counter(), parts))
+
+    def window(self, t0, t1):
+        """keep the samples taken inside [t0, t1] (else the 3 nearest to the window)"""
+        inside = [s for s in self.samples if t0 <= s[0] <= t1]
+        if not inside:
+            inside = sorted(self.samples, key=lambda s: min(abs(s[0] - t0), abs(s[0] - t1)))[:3]
+        self.samples = inside
 
     def stop(self):
         if self.proc:
@@ -176,6 +183,7 @@ class ClockSampler:
                 self.proc.kill()
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        self.samples = [s[1] for s in self.samples]
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -265,24 +273,29 @@ def main():
                 ctx.ciphertext_export(o, (gbuf.data_ptr() + i * out_ct_bytes, out_ct_bytes), on_device=True)
             hdd.gather_bytes(gbuf, ((A + world - 1) // world) * out_ct_bytes, 0)
 
+    clk = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
+    clk.start()  # nvidia-smi sampler (100 ms); only samples inside the timed window are kept
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     launches0 = ctx.launch_count()
-    clk = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     ctx.query_stats()  # resets the per-query phase-event ring before the timed region
-    clk.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.nvtx.range_push("timed")
+    t_w0 = time.perf_counter()
     ev0.record(stream)
     for _ in range(args.steps):
         step()
     ev1.record(stream)
     torch.cuda.synchronize()
+    t_w1 = time.perf_counter()
+    torch.cuda.nvtx.range_pop()
     if world > 1:
         dist.barrier()
+    clk.window(t_w0, t_w1)
     clocks = clk.stop()
     # per-phase CUDA-event times recorded on the context stream during the timed steps (avg)
     phase = ctx.query_stats() * args.steps
@@ -295,7 +308,7 @@ def main():
     value = args.steps / (t_ms / 1e3)
     # ---- e2e through the public API with host buffers: H2D query, scan, D2H of every output ----
     e2e = None
-    if world == 1:
+    if world == 1 and args.e2e_steps > 0:
         host_q = torch.from_numpy(ctx.ciphertext_export(qct)).pin_memory()
         ob = ctx.ciphertext_export_size(outs[0])
         host_out = torch.empty(nloc * ob, dtype=torch.uint8).pin_memory()

@@ -32,14 +32,15 @@ struct InvTab2 {
 };
 
 // Row addressing for batched kernels: row r lives at
-//   base + (r / gsize) * gstride + (r % gsize) * n
-// and is reduced modulo q[midx[(r / mdiv) % mlen]].
+//   base + (r / gsize) * gstride + ((r % gsize) / g2) * s2 + (r % g2) * s3   (s3 == 0 means n)
+// and is reduced modulo q[midx[(r / mdiv) % mlen]].  Defaults (g2 = gsize, s3 = 0)
+// give base + (r / gsize) * gstride + (r % gsize) * n.
 struct RowMap {
-  uint32_t gsize;
-  uint32_t mdiv, mlen;
-  uint32_t pad;
-  uint64_t gstride;
-  uint8_t midx[32];
+  uint32_t gsize = 1u << 30;
+  uint32_t mdiv = 1, mlen = 1;
+  uint32_t g2 = 1u << 30;
+  uint64_t gstride = 0, s2 = 0, s3 = 0;
+  uint8_t midx[32] = {0};
 };
 
 // ---------------------------------------------------------------------------
@@ -103,8 +104,13 @@ __device__ __forceinline__ uint32_t galois_src(uint32_t t, uint32_t g, int logn)
   return __brev((e - 1u) >> 1) >> (32 - logn);
 }
 
+__host__ __device__ __forceinline__ uint64_t row_off(const RowMap &rm, uint32_t r, uint32_t n) {
+  const uint32_t in = r % rm.gsize;
+  const uint32_t g2 = rm.g2 < rm.gsize ? rm.g2 : rm.gsize;
+  return (uint64_t)(r / rm.gsize) * rm.gstride + (uint64_t)(in / g2) * rm.s2 + (uint64_t)(in % g2) * (rm.s3 ? rm.s3 : n);
+}
 __device__ __forceinline__ uint64_t *row_ptr(uint64_t *base, const RowMap &rm, uint32_t r, uint32_t n) {
-  return base + (uint64_t)(r / rm.gsize) * rm.gstride + (uint64_t)(r % rm.gsize) * n;
+  return base + row_off(rm, r, n);
 }
 __device__ __forceinline__ int row_mod(const RowMap &rm, uint32_t r) {
   return rm.midx[(r / rm.mdiv) % rm.mlen];
@@ -122,7 +128,9 @@ struct hd_context {
   uint64_t psi[HD_MAXMOD] = {0};
   ModTab mt;
   // device tables
-  uint64_t *tw = nullptr, *tws = nullptr, *itw = nullptr, *itws = nullptr;  // [L+1][n]
+  uint64_t *tw2 = nullptr, *itw2 = nullptr;  // [L+1][n] x {w, shoup(w)}: psi^{br(k)}, psi^{-br(k)}
+  uint64_t *ninv_dev = nullptr;              // [2 HD_MAXMOD]: n^{-1} mod q_l, then Shoup companions
+  bool ntt_attr_set = false;
   uint64_t ninv[HD_MAXMOD], ninvs[HD_MAXMOD];
   double *xi_re = nullptr, *xi_im = nullptr;  // [2n]: xi^t, R15
   uint32_t *rotg = nullptr;                   // [ns]: 5^j mod 2n
@@ -130,7 +138,7 @@ struct hd_context {
   void *scratch = nullptr;
   size_t scratch_bytes = 0;
   int *d_flag = nullptr;  // device error flag
-  cudaEvent_t ev[64][8];  // per-query phase events (ring of 64 queries)
+  cudaEvent_t ev[64][8] = {};  // per-query phase events (ring of 64 queries)
   int ev_next = 0, ev_pending = 0;
   double last_phase_ms[5] = {0, 0, 0, 0, 0};
   uint64_t launches = 0;  // kernels launched on this context (hd_launch_count)
@@ -196,6 +204,32 @@ hd_status hd_fail(hd_status s, const std::string &msg);
 
 // kernels / host drivers (defined in the .cu files)
 hd_status ntt_rows(hd_context *c, uint64_t *base, uint32_t rows, const RowMap &rm, bool inverse);
+
+// Fused NTT jobs (ntt.cu).  The first kernel of the transform may read its input from
+// another row map (out-of-place), optionally lifting the centred representative of a
+// coefficient-form residue mod q[row_mod(src.map, r)] into the row's modulus (R12); the
+// final forward store may combine: out[r] (=|+=) (A[r] - v) * w[l] (+ c0 permuted by the
+// Galois map, for p == 0), rows r = (x 2 + p) ell + l.
+struct NttSrc {
+  const uint64_t *base = nullptr;
+  RowMap map;
+  bool lift = false;
+};
+struct NttEpi {
+  int mode = 0;  // 0: none, 1: (A - v) w, 2: (A - v) w + pi_g(c0) on p == 0
+  bool acc = false;
+  int ell = 1, K = 1;
+  const uint64_t *A = nullptr;
+  RowMap amap;
+  uint64_t *out = nullptr;
+  RowMap omap;
+  const uint64_t *c0 = nullptr;
+  uint64_t c0_stride = 0;
+  const uint32_t *gal = nullptr;
+  uint64_t w[HD_MAXMOD] = {0}, ws[HD_MAXMOD] = {0};
+};
+hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &map, bool inverse, const NttSrc *src,
+                  const NttEpi *epi);
 RowMap rowmap_simple(uint32_t mdiv, std::initializer_list<int> mods, uint32_t gsize = 1u << 30,
                      uint64_t gstride = 0);
 uint64_t host_mulmod(uint64_t a, uint64_t b, uint64_t m);

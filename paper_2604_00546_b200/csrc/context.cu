@@ -147,8 +147,8 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
   }
   // NTT twiddles psi^{br(k)} and inverse, Shoup companions, n^{-1}
   const int n = c->n, M = c->L + 1;
-  std::vector<uint64_t> tw((size_t)M * n), tws((size_t)M * n), itw((size_t)M * n + 2 * HD_MAXMOD),
-      itws((size_t)M * n);
+  // interleaved {w, shoup(w)} per index (one 128-bit load per butterfly group)
+  std::vector<uint64_t> tw((size_t)2 * M * n), itw((size_t)2 * M * n), nv(2 * HD_MAXMOD, 0);
   for (int l = 0; l < M; l++) {
     uint64_t q = c->mod[l], g = c->psi[l], gi = host_powmod(g, q - 2, q);
     std::vector<uint64_t> pw(n), ipw(n);
@@ -159,15 +159,15 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
     }
     for (int k = 0; k < n; k++) {
       uint32_t b = bitrev_host(k, c->logn);
-      tw[(size_t)l * n + k] = pw[b];
-      tws[(size_t)l * n + k] = host_shoup(pw[b], q);
-      itw[(size_t)l * n + k] = ipw[b];
-      itws[(size_t)l * n + k] = host_shoup(ipw[b], q);
+      tw[2 * ((size_t)l * n + k)] = pw[b];
+      tw[2 * ((size_t)l * n + k) + 1] = host_shoup(pw[b], q);
+      itw[2 * ((size_t)l * n + k)] = ipw[b];
+      itw[2 * ((size_t)l * n + k) + 1] = host_shoup(ipw[b], q);
     }
     c->ninv[l] = host_powmod((uint64_t)n, q - 2, q);
     c->ninvs[l] = host_shoup(c->ninv[l], q);
-    itw[(size_t)M * n + l] = c->ninv[l];
-    itw[(size_t)M * n + HD_MAXMOD + l] = c->ninvs[l];
+    nv[l] = c->ninv[l];
+    nv[HD_MAXMOD + l] = c->ninvs[l];
   }
   // FFT tables for the special (I)FFT (R15): xi^t = exp(2 pi i t / 2n)
   std::vector<double> xr(two_n), xim(two_n);
@@ -187,15 +187,14 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
     return hd_fail(HD_E_CUDA, std::string("context tables: ") + cudaGetErrorString(e));
   };
   cudaError_t e;
-  if ((e = cudaMalloc(&c->tw, tw.size() * 8)) || (e = cudaMalloc(&c->tws, tws.size() * 8)) ||
-      (e = cudaMalloc(&c->itw, itw.size() * 8)) || (e = cudaMalloc(&c->itws, itws.size() * 8)) ||
+  if ((e = cudaMalloc(&c->tw2, tw.size() * 8)) || (e = cudaMalloc(&c->itw2, itw.size() * 8)) ||
+      (e = cudaMalloc(&c->ninv_dev, nv.size() * 8)) ||
       (e = cudaMalloc(&c->xi_re, two_n * 8)) || (e = cudaMalloc(&c->xi_im, two_n * 8)) ||
       (e = cudaMalloc(&c->rotg, c->ns * 4)) || (e = cudaMalloc(&c->d_flag, 64)))
     return fail(e);
-  if ((e = cudaMemcpy(c->tw, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(c->tws, tws.data(), tws.size() * 8, cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(c->itw, itw.data(), itw.size() * 8, cudaMemcpyHostToDevice)) ||
-      (e = cudaMemcpy(c->itws, itws.data(), itws.size() * 8, cudaMemcpyHostToDevice)) ||
+  if ((e = cudaMemcpy(c->tw2, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(c->itw2, itw.data(), itw.size() * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(c->ninv_dev, nv.data(), nv.size() * 8, cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(c->xi_re, xr.data(), two_n * 8, cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(c->xi_im, xim.data(), two_n * 8, cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(c->rotg, rg.data(), c->ns * 4, cudaMemcpyHostToDevice)) ||
@@ -211,10 +210,9 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
 extern "C" void hd_context_destroy(hd_context *c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  cudaFree(c->tw);
-  cudaFree(c->tws);
-  cudaFree(c->itw);
-  cudaFree(c->itws);
+  cudaFree(c->tw2);
+  cudaFree(c->itw2);
+  cudaFree(c->ninv_dev);
   cudaFree(c->xi_re);
   cudaFree(c->xi_im);
   cudaFree(c->rotg);

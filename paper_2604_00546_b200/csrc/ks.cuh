@@ -3,12 +3,13 @@
 #include "common.cuh"
 
 // ModUp (R11) of B c1 polynomials at ell limbs (c1 of ciphertext b at c1 + b*c1_stride).
-// dig: [B][ell][ell+1][n] (slot layout: see ks.cu).  tmp: B*ell*n scratch.
+// dig: [B][ell][ell][n] (lifted digits; slot layout: see ks.cu).  tmp: B*ell*n scratch.
 hd_status ks_modup(hd_context *c, const uint64_t *c1, size_t c1_stride, uint32_t B, int ell, uint64_t *dig,
                    uint64_t *tmp);
 // Key inner product for X = B*K (b, k) pairs -> u [X][2][ell+1][n].
-hd_status ks_kip(hd_context *c, const uint64_t *dig, uint32_t B, uint32_t K, int ell,
-                 const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u);
+// (the own-modulus digit of c1 is read from c1 itself: c1 of ciphertext b at c1 + b*c1_stride)
+hd_status ks_kip(hd_context *c, const uint64_t *dig, const uint64_t *c1, size_t c1_stride, uint32_t B, uint32_t K,
+                 int ell, const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u);
 // ModDown of u [X][2][ell+1][n] (P limb INTT'd in place) -> dst_x (+ pi_{g_k}(c0_b)).
 hd_status ks_moddown(hd_context *c, uint64_t *u, uint32_t X, uint32_t K, int ell, const uint32_t *gal_dev,
                      const uint64_t *c0, size_t c0_stride, uint64_t *dst, size_t dst_stride, bool accumulate,

@@ -13,6 +13,8 @@
 #include "common.cuh"
 #include "ks.cuh"
 
+#include <cstdlib>
+
 namespace {
 constexpr int MAC_TPB = 128;
 
@@ -57,14 +59,598 @@ __global__ void __launch_bounds__(MAC_TPB) mac_kernel(const uint64_t *__restrict
     Sa[(size_t)(jj * 2 + 1) * limb_stride] = s1;
   }
 }
+// Full-range variant (n1 | N/2, so every giant step uses all n1 baby steps): baby
+// step i outer, JT giant steps inner with their 128-bit accumulators in registers.
+// Each i issues JT independent coalesced D loads (memory-level parallelism) and
+// reuses the two r[i] words JT times.  blockIdx.x = aggregate (fastest), so the
+// CTAs resident at any time share few (limb, tile) r tiles -> r stays in L2 and
+// the D stream is the only HBM traffic.
+template <int JT>
+__global__ void __launch_bounds__(MAC_TPB) mac_full_kernel(const uint64_t *__restrict__ D,
+                                                           const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
+                                                           int n1, int N, int L, int logn, int jmin, int nj,
+                                                           ModTab mt) {
+  const int n = 1 << logn;
+  const uint32_t a = blockIdx.x;
+  const uint32_t t = blockIdx.y * MAC_TPB + threadIdx.x;
+  const int ngrp = nj / JT;
+  const int m = blockIdx.z / ngrp, jg = blockIdx.z % ngrp;
+  const size_t ls = (size_t)L * n;
+  const uint64_t *Da = D + (size_t)a * N * ls + (size_t)m * n + t;
+  const uint64_t *rr = r + (size_t)m * n + t;
+  int kb[JT];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) kb[jj] = (jmin + jg * JT + jj) * n1;
+  uint64_t acc[JT][4];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) acc[jj][0] = acc[jj][1] = acc[jj][2] = acc[jj][3] = 0;
+  for (int i = 0; i < n1; i++) {
+    const uint64_t r0 = __ldg(rr + (size_t)(2 * i) * ls);
+    const uint64_t r1 = __ldg(rr + (size_t)(2 * i + 1) * ls);
+    uint64_t d[JT];
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) d[jj] = __ldcs(Da + (size_t)((kb[jj] + i) & (N - 1)) * ls);
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      mac128(acc[jj][0], acc[jj][1], r0, d[jj]);
+      mac128(acc[jj][2], acc[jj][3], r1, d[jj]);
+    }
+  }
+  const uint64_t q = mt.q[m], bar = mt.bar[m], r64 = mt.r64[m], r64s = mt.r64s[m];
+  uint64_t *Sa = S + (size_t)a * nj * 2 * ls + (size_t)m * n + t;
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) {
+    const size_t jx = (size_t)(jg * JT + jj);
+    Sa[(jx * 2 + 0) * ls] = reduce128(acc[jj][1], acc[jj][0], q, bar, r64, r64s);
+    Sa[(jx * 2 + 1) * ls] = reduce128(acc[jj][3], acc[jj][2], q, bar, r64, r64s);
+  }
+}
+// ---- carry-save variant (q < 2^60, n1 <= 128) ----------------------------------------
+// a = a1 2^32 + a0, b = b1 2^32 + b0 (a1, b1 < 2^28).  Per product:
+//   lo  += a0 b0          (64-bit add, carry counted in cnt)
+//   mid += a0 b1 + a1 b0  (mad.wide into 64 bits: each term < 2^60, folded every 8 i)
+//   hi  += a1 b1          (< 2^56 per term)
+// i.e. 4 IMAD.WIDE + 3 IADD per product instead of a full 64x64->128 multiply and a
+// 128-bit add.  value = lo + mid 2^32 + (hi + cnt) 2^64, reduced once per (a, j).
+struct CsAcc {
+  uint64_t lo, mid, hi;
+  uint32_t cnt;
+};
+__device__ __forceinline__ void cs_mac(CsAcc &A, uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
+  asm("{\n\t.reg .u64 t;\n\t"
+      "mul.wide.u32 t, %4, %6;\n\t"
+      "add.cc.u64 %0, %0, t;\n\t"
+      "addc.u32 %3, %3, 0;\n\t"
+      "mad.wide.u32 %1, %4, %7, %1;\n\t"
+      "mad.wide.u32 %1, %5, %6, %1;\n\t"
+      "mad.wide.u32 %2, %5, %7, %2;\n\t"
+      "}"
+      : "+l"(A.lo), "+l"(A.mid), "+l"(A.hi), "+r"(A.cnt)
+      : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void cs_fold(CsAcc &A) {
+  const uint64_t ml = A.mid << 32, mh = A.mid >> 32;
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+l"(A.lo), "+r"(A.cnt) : "l"(ml));
+  A.hi += mh;
+  A.mid = 0;
+}
+__device__ __forceinline__ uint64_t ld_stream(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.global.cs.u64 %0, [%1];" : "=l"(v) : "l"(p));
+  return v;
+}
+
+template <int JT>
+__global__ void __launch_bounds__(MAC_TPB) mac_cs_kernel(const uint64_t *__restrict__ D,
+                                                         const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
+                                                         int n1, int N, int L, int logn, int jmin, int nj, ModTab mt) {
+  const int n = 1 << logn;
+  const uint32_t a = blockIdx.x;
+  const uint32_t t = blockIdx.y * MAC_TPB + threadIdx.x;
+  const int ngrp = nj / JT;
+  const int m = blockIdx.z / ngrp, jg = blockIdx.z % ngrp;
+  const size_t ls = (size_t)L * n;
+  const uint64_t *Da = D + (size_t)a * N * ls + (size_t)m * n + t;
+  const uint64_t *rr = r + (size_t)m * n + t;
+  const uint64_t *p[JT];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) p[jj] = Da + (size_t)(((jmin + jg * JT + jj) * n1) & (N - 1)) * ls;
+  CsAcc acc[JT][2];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++)
+#pragma unroll
+    for (int q2 = 0; q2 < 2; q2++) acc[jj][q2] = CsAcc{0, 0, 0, 0};
+  for (int i0 = 0; i0 < n1; i0 += 8) {
+#pragma unroll 2
+    for (int i = i0; i < i0 + 8 && i < n1; i++) {
+      uint64_t d[JT];
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++) d[jj] = ld_stream(p[jj] + (size_t)i * ls);
+      const uint64_t r0 = __ldg(rr + (size_t)(2 * i) * ls);
+      const uint64_t r1 = __ldg(rr + (size_t)(2 * i + 1) * ls);
+      const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1, r11 = (uint32_t)(r1 >> 32);
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++) {
+        const uint32_t b0 = (uint32_t)d[jj], b1 = (uint32_t)(d[jj] >> 32);
+        cs_mac(acc[jj][0], r00, r01, b0, b1);
+        cs_mac(acc[jj][1], r10, r11, b0, b1);
+      }
+    }
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      cs_fold(acc[jj][0]);
+      cs_fold(acc[jj][1]);
+    }
+  }
+  const uint64_t q = mt.q[m], bar = mt.bar[m], r64 = mt.r64[m], r64s = mt.r64s[m];
+  uint64_t *Sa = S + (size_t)a * nj * 2 * ls + (size_t)m * n + t;
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) {
+    const size_t jx = (size_t)(jg * JT + jj);
+#pragma unroll
+    for (int q2 = 0; q2 < 2; q2++) {
+      const CsAcc &A = acc[jj][q2];
+      Sa[(jx * 2 + q2) * ls] = reduce128(A.hi + A.cnt, A.lo, q, bar, r64, r64s);
+    }
+  }
+}
+// ---- carry-save, software-pipelined loads: the JT loads of baby step i+1 are issued
+// before the arithmetic of step i (2 JT loads in flight per thread), running pointers. --
+template <int JT>
+__global__ void __launch_bounds__(MAC_TPB) mac_cs2_kernel(const uint64_t *__restrict__ D,
+                                                          const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
+                                                          int n1, int N, int L, int logn, int jmin, int nj,
+                                                          ModTab mt) {
+  const int n = 1 << logn;
+  const uint32_t a = blockIdx.x;
+  const uint32_t t = blockIdx.y * MAC_TPB + threadIdx.x;
+  const int ngrp = nj / JT;
+  const int m = blockIdx.z / ngrp, jg = blockIdx.z % ngrp;
+  const size_t ls = (size_t)L * n;
+  const uint64_t *Da = D + (size_t)a * N * ls + (size_t)m * n + t;
+  const uint64_t *rr = r + (size_t)m * n + t;
+  const uint64_t *p[JT];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) p[jj] = Da + (size_t)(((jmin + jg * JT + jj) * n1) & (N - 1)) * ls;
+  CsAcc acc[JT][2];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) acc[jj][0] = acc[jj][1] = CsAcc{0, 0, 0, 0};
+  uint64_t d[JT], dn[JT];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) {
+    d[jj] = ld_stream(p[jj]);
+    p[jj] += ls;
+  }
+  uint64_t r0 = __ldg(rr), r1 = __ldg(rr + ls);
+  for (int i = 0; i < n1; i++) {
+    const bool more = i + 1 < n1;
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      dn[jj] = more ? ld_stream(p[jj]) : 0;
+      p[jj] += ls;
+    }
+    const uint64_t rn0 = more ? __ldg(rr + (size_t)(2 * i + 2) * ls) : 0;
+    const uint64_t rn1 = more ? __ldg(rr + (size_t)(2 * i + 3) * ls) : 0;
+    const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1, r11 = (uint32_t)(r1 >> 32);
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      const uint32_t b0 = (uint32_t)d[jj], b1 = (uint32_t)(d[jj] >> 32);
+      cs_mac(acc[jj][0], r00, r01, b0, b1);
+      cs_mac(acc[jj][1], r10, r11, b0, b1);
+      d[jj] = dn[jj];
+    }
+    r0 = rn0;
+    r1 = rn1;
+    if ((i & 7) == 7) {
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++) {
+        cs_fold(acc[jj][0]);
+        cs_fold(acc[jj][1]);
+      }
+    }
+  }
+  const uint64_t q = mt.q[m], bar = mt.bar[m], r64 = mt.r64[m], r64s = mt.r64s[m];
+  uint64_t *Sa = S + (size_t)a * nj * 2 * ls + (size_t)m * n + t;
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) {
+    const size_t jx = (size_t)(jg * JT + jj);
+#pragma unroll
+    for (int q2 = 0; q2 < 2; q2++) {
+      CsAcc &A = acc[jj][q2];
+      cs_fold(A);
+      Sa[(jx * 2 + q2) * ls] = reduce128(A.hi + A.cnt, A.lo, q, bar, r64, r64s);
+    }
+  }
+}
+
+// ---- bulk-copy pipelined variant: TMA (cp.async.bulk) ring + carry-save MAC -----------
+// The CTA owns (aggregate a, tile of MT = 128 coefficients of limb m, JT giant steps).
+// Stage i of the ring holds the JT diagonal rows D[a][k(j,i)][m][tile] (JT x 1 KiB,
+// contiguous in HBM) and the two baby-step rows r[i][0/1][m][tile]; one elected thread
+// issues the bulk copies, completion is tracked by one mbarrier per slot (expect_tx),
+// and NS stages (NS (JT+2) KiB per CTA) are in flight: HBM latency is hidden by
+// bytes in flight, not by warps.
+constexpr int MT = MAC_TPB;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+      "@!P bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <int JT, int NS>
+__global__ void __launch_bounds__(MT) mac_tma_kernel(const uint64_t *__restrict__ D, const uint64_t *__restrict__ r,
+                                                     uint64_t *__restrict__ S, int n1, int N, int L, int logn, int jmin,
+                                                     int nj, ModTab mt) {
+  extern __shared__ __align__(128) uint64_t ring[];  // [NS][JT + 2][MT]
+  __shared__ __align__(8) uint64_t full_bar[NS];
+  constexpr int ROWS = JT + 2;
+  constexpr uint32_t STAGE_BYTES = ROWS * MT * 8;
+  const int n = 1 << logn;
+  const uint32_t a = blockIdx.x;
+  const uint32_t t0 = blockIdx.y * MT;
+  const int ngrp = nj / JT;
+  const int m = blockIdx.z / ngrp, jg = blockIdx.z % ngrp;
+  const size_t ls = (size_t)L * n;
+  const uint64_t *Dt = D + (size_t)a * N * ls + (size_t)m * n + t0;
+  const uint64_t *rt = r + (size_t)m * n + t0;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; s++) mbar_init(&full_bar[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int i, int slot) {
+    uint64_t *dst = ring + (size_t)slot * ROWS * MT;
+    mbar_expect_tx(&full_bar[slot], STAGE_BYTES);
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      const int k = (((jmin + jg * JT + jj) * n1) & (N - 1)) + i;  // no wrap: n1 | N/2
+      bulk_g2s(dst + jj * MT, Dt + (size_t)k * ls, MT * 8, &full_bar[slot]);
+    }
+    bulk_g2s(dst + JT * MT, rt + (size_t)(2 * i) * ls, MT * 8, &full_bar[slot]);
+    bulk_g2s(dst + (JT + 1) * MT, rt + (size_t)(2 * i + 1) * ls, MT * 8, &full_bar[slot]);
+  };
+  if (threadIdx.x == 0)
+    for (int s = 0; s < NS && s < n1; s++) issue(s, s);
+  CsAcc acc[JT][2];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) acc[jj][0] = acc[jj][1] = CsAcc{0, 0, 0, 0};
+  for (int i = 0; i < n1; i++) {
+    const int slot = i % NS;
+    mbar_wait(&full_bar[slot], (uint32_t)((i / NS) & 1));
+    const uint64_t *st = ring + (size_t)slot * ROWS * MT + threadIdx.x;
+    uint64_t d[JT];
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) d[jj] = st[jj * MT];
+    const uint64_t r0 = st[JT * MT], r1 = st[(JT + 1) * MT];
+    __syncthreads();  // every thread has its words of this slot: refill it
+    if (threadIdx.x == 0 && i + NS < n1) issue(i + NS, slot);
+    const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1, r11 = (uint32_t)(r1 >> 32);
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      const uint32_t b0 = (uint32_t)d[jj], b1 = (uint32_t)(d[jj] >> 32);
+      cs_mac(acc[jj][0], r00, r01, b0, b1);
+      cs_mac(acc[jj][1], r10, r11, b0, b1);
+    }
+    if ((i & 7) == 7) {
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++) {
+        cs_fold(acc[jj][0]);
+        cs_fold(acc[jj][1]);
+      }
+    }
+  }
+  const uint64_t q = mt.q[m], bar = mt.bar[m], r64 = mt.r64[m], r64s = mt.r64s[m];
+  uint64_t *Sa = S + (size_t)a * nj * 2 * ls + (size_t)m * n + t0 + threadIdx.x;
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) {
+    const size_t jx = (size_t)(jg * JT + jj);
+#pragma unroll
+    for (int q2 = 0; q2 < 2; q2++) {
+      CsAcc &A = acc[jj][q2];
+      cs_fold(A);
+      Sa[(jx * 2 + q2) * ls] = reduce128(A.hi + A.cnt, A.lo, q, bar, r64, r64s);
+    }
+  }
+}
+// ---- warp-specialised variant: 4 compute warps + 1 producer warp ---------------------
+// Same stage contents as mac_tma_kernel, but the producer warp refills a slot as soon as
+// the four compute warps have released it (per-slot "empty" mbarrier, one arrival per
+// warp), so compute warps never meet at a CTA-wide barrier inside the i loop.
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int JT, int NS>
+__global__ void __launch_bounds__(MT + 32) mac_ws_kernel(const uint64_t *__restrict__ D,
+                                                         const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
+                                                         int n1, int N, int L, int logn, int jmin, int nj, ModTab mt) {
+  extern __shared__ __align__(128) uint64_t ring[];  // [NS][JT + 2][MT]
+  __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS];
+  constexpr int ROWS = JT + 2;
+  constexpr uint32_t STAGE_BYTES = ROWS * MT * 8;
+  constexpr int NCW = MT / 32;  // compute warps
+  const int n = 1 << logn;
+  const uint32_t a = blockIdx.x;
+  const uint32_t t0 = blockIdx.y * MT;
+  const int ngrp = nj / JT;
+  const int m = blockIdx.z / ngrp, jg = blockIdx.z % ngrp;
+  const size_t ls = (size_t)L * n;
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; s++) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == NCW) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t *Dt = D + (size_t)a * N * ls + (size_t)m * n + t0;
+      const uint64_t *rt = r + (size_t)m * n + t0;
+      int kb[JT];
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++) kb[jj] = ((jmin + jg * JT + jj) * n1) & (N - 1);  // no wrap: n1 | N/2
+      for (int i = 0; i < n1; i++) {
+        const int slot = i % NS;
+        if (i >= NS) mbar_wait(&empty_bar[slot], (uint32_t)(((i / NS) - 1) & 1));
+        uint64_t *dst = ring + (size_t)slot * ROWS * MT;
+        mbar_expect_tx(&full_bar[slot], STAGE_BYTES);
+#pragma unroll
+        for (int jj = 0; jj < JT; jj++) bulk_g2s(dst + jj * MT, Dt + (size_t)(kb[jj] + i) * ls, MT * 8, &full_bar[slot]);
+        bulk_g2s(dst + JT * MT, rt + (size_t)(2 * i) * ls, MT * 8, &full_bar[slot]);
+        bulk_g2s(dst + (JT + 1) * MT, rt + (size_t)(2 * i + 1) * ls, MT * 8, &full_bar[slot]);
+      }
+    }
+    return;
+  }
+  // ---------------- compute warps ----------------
+  CsAcc acc[JT][2];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) acc[jj][0] = acc[jj][1] = CsAcc{0, 0, 0, 0};
+  for (int i = 0; i < n1; i++) {
+    const int slot = i % NS;
+    mbar_wait(&full_bar[slot], (uint32_t)((i / NS) & 1));
+    const uint64_t *st = ring + (size_t)slot * ROWS * MT + threadIdx.x;
+    uint64_t d[JT];
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) d[jj] = st[jj * MT];
+    const uint64_t r0 = st[JT * MT], r1 = st[(JT + 1) * MT];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty_bar[slot]);
+    const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1, r11 = (uint32_t)(r1 >> 32);
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      const uint32_t b0 = (uint32_t)d[jj], b1 = (uint32_t)(d[jj] >> 32);
+      cs_mac(acc[jj][0], r00, r01, b0, b1);
+      cs_mac(acc[jj][1], r10, r11, b0, b1);
+    }
+    if ((i & 7) == 7) {
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++) {
+        cs_fold(acc[jj][0]);
+        cs_fold(acc[jj][1]);
+      }
+    }
+  }
+  const uint64_t q = mt.q[m], bar = mt.bar[m], r64 = mt.r64[m], r64s = mt.r64s[m];
+  uint64_t *Sa = S + (size_t)a * nj * 2 * ls + (size_t)m * n + t0 + threadIdx.x;
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) {
+    const size_t jx = (size_t)(jg * JT + jj);
+#pragma unroll
+    for (int q2 = 0; q2 < 2; q2++) {
+      CsAcc &A = acc[jj][q2];
+      cs_fold(A);
+      Sa[(jx * 2 + q2) * ls] = reduce128(A.hi + A.cnt, A.lo, q, bar, r64, r64s);
+    }
+  }
+}
+// ---- persistent warp-specialised variant ------------------------------------------------
+// gridDim.x CTAs (a few per SM) walk the flattened work list w = (a, tile, m, jg) with
+// the aggregate fastest (consecutive CTAs share the same r tile -> r stays in L2).  The
+// producer warp streams stage after stage across work items, so the ring never drains
+// between tiles and the per-CTA prologue is paid once.
+template <int JT, int NS>
+__global__ void __launch_bounds__(MT + 32) mac_pers_kernel(const uint64_t *__restrict__ D,
+                                                           const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
+                                                           int n1, int N, int L, int logn, int jmin, int nj,
+                                                           uint32_t A_loc, ModTab mt) {
+  extern __shared__ __align__(128) uint64_t ring[];  // [NS][JT + 2][MT]
+  __shared__ __align__(8) uint64_t full_bar[NS], empty_bar[NS];
+  constexpr int ROWS = JT + 2;
+  constexpr uint32_t STAGE_BYTES = ROWS * MT * 8;
+  constexpr int NCW = MT / 32;
+  const int n = 1 << logn;
+  const size_t ls = (size_t)L * n;
+  const int ngrp = nj / JT;
+  const uint32_t tiles = n / MT;
+  const uint32_t nwork = A_loc * tiles * L * ngrp;
+  const uint32_t warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NS; s++) {
+      mbar_init(&full_bar[s], 1);
+      mbar_init(&empty_bar[s], NCW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto decode = [&](uint32_t w, uint32_t &a, uint32_t &t0, int &m, int &jg) {
+    a = w % A_loc;
+    uint32_t rest = w / A_loc;
+    t0 = (rest % tiles) * MT;
+    rest /= tiles;
+    m = (int)(rest % L);
+    jg = (int)(rest / L);
+  };
+  if (warp == NCW) {  // ---------------- producer ----------------
+    if (lane == 0) {
+      uint32_t it = 0;  // global stage counter
+      for (uint32_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+        uint32_t a, t0;
+        int m, jg;
+        decode(w, a, t0, m, jg);
+        const uint64_t *Dt = D + (size_t)a * N * ls + (size_t)m * n + t0;
+        const uint64_t *rt = r + (size_t)m * n + t0;
+        for (int i = 0; i < n1; i++, it++) {
+          const uint32_t slot = it % NS;
+          if (it >= NS) mbar_wait(&empty_bar[slot], ((it / NS) - 1) & 1);
+          uint64_t *dst = ring + (size_t)slot * ROWS * MT;
+          mbar_expect_tx(&full_bar[slot], STAGE_BYTES);
+#pragma unroll
+          for (int jj = 0; jj < JT; jj++) {
+            const int k = (((jmin + jg * JT + jj) * n1) & (N - 1)) + i;  // no wrap: n1 | N/2
+            bulk_g2s(dst + jj * MT, Dt + (size_t)k * ls, MT * 8, &full_bar[slot]);
+          }
+          bulk_g2s(dst + JT * MT, rt + (size_t)(2 * i) * ls, MT * 8, &full_bar[slot]);
+          bulk_g2s(dst + (JT + 1) * MT, rt + (size_t)(2 * i + 1) * ls, MT * 8, &full_bar[slot]);
+        }
+      }
+    }
+    return;
+  }
+  // ---------------- compute warps ----------------
+  uint32_t it = 0;
+  for (uint32_t w = blockIdx.x; w < nwork; w += gridDim.x) {
+    uint32_t a, t0;
+    int m, jg;
+    decode(w, a, t0, m, jg);
+    CsAcc acc[JT][2];
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) acc[jj][0] = acc[jj][1] = CsAcc{0, 0, 0, 0};
+    for (int i = 0; i < n1; i++, it++) {
+      const uint32_t slot = it % NS;
+      mbar_wait(&full_bar[slot], (it / NS) & 1);
+      const uint64_t *st = ring + (size_t)slot * ROWS * MT + threadIdx.x;
+      uint64_t d[JT];
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++) d[jj] = st[jj * MT];
+      const uint64_t r0 = st[JT * MT], r1 = st[(JT + 1) * MT];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty_bar[slot]);
+      const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1, r11 = (uint32_t)(r1 >> 32);
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++) {
+        const uint32_t b0 = (uint32_t)d[jj], b1 = (uint32_t)(d[jj] >> 32);
+        cs_mac(acc[jj][0], r00, r01, b0, b1);
+        cs_mac(acc[jj][1], r10, r11, b0, b1);
+      }
+      if ((i & 7) == 7) {
+#pragma unroll
+        for (int jj = 0; jj < JT; jj++) {
+          cs_fold(acc[jj][0]);
+          cs_fold(acc[jj][1]);
+        }
+      }
+    }
+    const uint64_t q = mt.q[m], bar = mt.bar[m], r64 = mt.r64[m], r64s = mt.r64s[m];
+    uint64_t *Sa = S + (size_t)a * nj * 2 * ls + (size_t)m * n + t0 + threadIdx.x;
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      const size_t jx = (size_t)(jg * JT + jj);
+#pragma unroll
+      for (int q2 = 0; q2 < 2; q2++) {
+        CsAcc &Ac = acc[jj][q2];
+        cs_fold(Ac);
+        Sa[(jx * 2 + q2) * ls] = reduce128(Ac.hi + Ac.cnt, Ac.lo, q, bar, r64, r64s);
+      }
+    }
+  }
+}
 }  // namespace
 
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
                   const std::vector<int32_t> &js) {
   if (js.empty() || A_loc == 0) return HD_OK;
   const int jmin = js.front(), nj = (int)js.size();
-  dim3 grid((c->n + MAC_TPB - 1) / MAC_TPB, c->L, A_loc);
-  mac_kernel<<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt); ++c->launches;
+  const bool full = (N / 2) % n1 == 0 && n1 <= 256 && c->n % MAC_TPB == 0;
+  bool small_q = true;
+  for (int l = 0; l < c->L; l++) small_q = small_q && c->mod[l] < (1ull << 60);
+  const char *force = getenv("HD_MAC_VARIANT");
+  const bool use_cs = full && small_q && n1 <= 128 && nj % 4 == 0 && !(force && force[0] == 'f');
+  // variants: 3 (default) carry-save, JT = 2, software-pipelined loads; 2 same with JT = 4;
+  // c carry-save JT = 4; w / p / q / t bulk-copy (TMA) rings; f 128-bit accumulators
+  const char v = force ? force[0] : '3';
+  const bool use_tma = use_cs && (v == 't' || v == 'w');
+  const bool use_ws = use_cs && v == 'w';
+  const bool use_pers = use_cs && (v == 'p' || v == 'q');
+  if (use_cs && (v == '2' || v == '3')) {
+    dim3 grid(A_loc, c->n / MAC_TPB, c->L * (nj / 4));
+    if (v == '2') mac_cs2_kernel<4><<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+    else {
+      dim3 g2(A_loc, c->n / MAC_TPB, c->L * (nj / 2));
+      if (nj % 2) return hd_fail(HD_E_PARAMS, "variant 3 needs an even giant-step count");
+      mac_cs2_kernel<2><<<g2, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+    }
+  } else if (use_pers) {
+    constexpr int JT = 4, NS = 12;
+    const size_t smem = (size_t)NS * (JT + 2) * MT * 8;
+    static bool attr_p = false;
+    if (!attr_p) {
+      cudaFuncSetAttribute(mac_pers_kernel<JT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_p = true;
+    }
+    int dev_sms = 148;
+    cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device);
+    const int per_sm = v == 'q' ? 2 : 3;
+    mac_pers_kernel<JT, NS><<<dev_sms * per_sm, MAC_TPB + 32, smem, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin,
+                                                                                  nj, A_loc, c->mt);
+  } else if (use_ws) {
+    constexpr int JT = 4, NS = 12;
+    const size_t smem = (size_t)NS * (JT + 2) * MT * 8;
+    static bool attr_ws = false;
+    if (!attr_ws) {
+      cudaFuncSetAttribute(mac_ws_kernel<JT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr_ws = true;
+    }
+    dim3 grid(A_loc, c->n / MAC_TPB, c->L * (nj / JT));
+    mac_ws_kernel<JT, NS><<<grid, MAC_TPB + 32, smem, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+  } else if (use_tma) {
+    constexpr int JT = 4, NS = 8;
+    const size_t smem = (size_t)NS * (JT + 2) * MT * 8;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(mac_tma_kernel<JT, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    dim3 grid(A_loc, c->n / MAC_TPB, c->L * (nj / JT));
+    mac_tma_kernel<JT, NS><<<grid, MAC_TPB, smem, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+  } else if (use_cs) {
+    dim3 grid(A_loc, c->n / MAC_TPB, c->L * (nj / 4));
+    mac_cs_kernel<4><<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+  } else if (full && nj % 8 == 0) {
+    dim3 grid(A_loc, c->n / MAC_TPB, c->L * (nj / 8));
+    mac_full_kernel<8><<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+  } else if (full && nj % 4 == 0) {
+    dim3 grid(A_loc, c->n / MAC_TPB, c->L * (nj / 4));
+    mac_full_kernel<4><<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+  } else {
+    dim3 grid((c->n + MAC_TPB - 1) / MAC_TPB, c->L, A_loc);
+    mac_kernel<<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+  }
+  ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;
 }

@@ -1,119 +1,309 @@
 // ntt.cu -- batched 64-bit negacyclic NTT / INTT for sm_100a (K9 of SURVEY 2.2).
 //
 // Forward: Cooley-Tukey, natural order in, bit-reversed evaluation order out
-// (R13); inverse: Gentleman-Sande, then x n^{-1}.  Twiddles are
-// psi^{br(k)} with Shoup companions, per modulus.
+// (R13); inverse: Gentleman-Sande, then x n^{-1}.  Twiddles psi^{br(k)}
+// are stored interleaved with their Shoup companions ({w, floor(w 2^64 / q)}: one
+// 128-bit load per butterfly group).
 //
-// log n = s1 + s2.  The s1 "high" stages act on columns {hi 2^s2 + lo : hi} (one
-// CTA holds CH columns of 2^s1 elements, loaded with coalesced row segments);
-// the s2 "low" stages act on contiguous chunks of 2^s2 elements.  Each phase is
-// one kernel with the data staged in shared memory; every butterfly keeps its
-// operands fully reduced in [0, q).
+// Decomposition: log n = s1 + s2.  Kernel "cols" runs the s1 high stages on
+// columns {x 2^s2 + c : x < 2^s1} (a CTA owns TPC consecutive columns; global
+// loads/stores are coalesced across columns); kernel "chunks" runs the s2 low
+// stages on contiguous chunks of 2^s2 elements (staged through shared memory
+// with flat 128-bit coalesced copies).  Inside a kernel every thread holds 16
+// elements and performs up to 4 butterfly stages in registers per pass
+// (radix-16); passes exchange through padded shared memory.  Every index is a
+// compile-time function of (S, pass, slot) plus the thread id.  Harvey lazy
+// reduction: forward values live in [0, 4q), inverse values in [0, 2q); the last
+// kernel reduces to [0, q).  Moduli are < 2^60, so 4q < 2^62.
+//
+// Fusion (ntt_run): the first kernel may load its rows from another row map (out
+// of place) and lift centred residues from the source modulus (ModUp / ModDown /
+// rescale lifts, R12); the final forward store may apply the ModDown / rescale
+// combine (A - v) w (+ pi_g(c0)), written or accumulated into a third row map.
 #include "common.cuh"
 
 namespace {
 
-constexpr int NTT_THREADS = 256;
-constexpr int LO_BITS_MAX = 11;  // 2^11 u64 = 16 KiB per chunk
+constexpr int E = 16;  // elements per thread
 
-__device__ __forceinline__ void ct_bfly(uint64_t &a, uint64_t &b, uint64_t w, uint64_t ws, uint64_t q) {
-  uint64_t V = shoup(b, w, ws, q);
-  uint64_t U = a;
-  a = addmod(U, V, q);
-  b = submod(U, V, q);
-}
-__device__ __forceinline__ void gs_bfly(uint64_t &a, uint64_t &b, uint64_t w, uint64_t ws, uint64_t q) {
-  uint64_t U = a, V = b;
-  a = addmod(U, V, q);
-  b = shoup(submod(U, V, q), w, ws, q);
+__device__ __forceinline__ uint32_t pad_idx(uint32_t x) { return x + (x >> 4); }
+
+template <bool INV, int S, int P>
+struct Pass {
+  static constexpr int NP = (S + 3) / 4;
+  static constexpr int LAST = S - 4 * (NP - 1);
+  static constexpr int KP = INV ? (P == 0 ? LAST : 4) : (P == NP - 1 ? LAST : 4);
+  static constexpr int REM = INV ? (LAST + 4 * P) : (S - 4 * P);
+};
+
+// Thread element of slot = g 2^KP + e:  x = (y >> DL) 2^REM + e 2^DL + (y & (2^DL - 1)),
+// y = g 2^(S-4) + tid, DL = REM - KP.
+template <int KP, int REM, int S>
+__device__ __forceinline__ uint32_t elem_of(int slot, uint32_t tid) {
+  constexpr int DL = REM - KP;
+  const int g = slot >> KP, e = slot & ((1 << KP) - 1);
+  const uint32_t y = ((uint32_t)g << (S - 4)) + tid;
+  return ((y >> DL) << REM) + ((uint32_t)e << DL) + (y & ((1u << DL) - 1));
 }
 
-// High stages (mm = 1 .. 2^(s1-1)) forward / (2^(s1-1) .. 1) inverse.
-template <bool INV>
-__global__ void __launch_bounds__(NTT_THREADS) ntt_hi_kernel(uint64_t *base, RowMap rm, ModTab mt,
-                                                             const uint64_t *__restrict__ tw,
-                                                             const uint64_t *__restrict__ tws, int logn,
-                                                             int s1, int ch, const uint64_t *ninv,
-                                                             const uint64_t *ninvs, uint32_t r0) {
+// KP <= 4 butterfly stages in registers.  The butterfly at distance d = 2^(u + DL)
+// uses twiddle T[base 2^(S-1-u-DL) + (y >> DL) 2^(KP-u-1) + (e >> (u+1))].
+template <bool INV, int KP, int REM, int S>
+__device__ __forceinline__ void radix_pass(uint64_t (&v)[E], uint32_t tid, uint32_t base,
+                                           const ulonglong2 *__restrict__ T, uint64_t q) {
+  constexpr int NG = 1 << (4 - KP);
+  constexpr int DL = REM - KP;
+  const uint64_t two_q = 2 * q;
+#pragma unroll
+  for (int uu = 0; uu < KP; uu++) {
+    const int u = INV ? uu : (KP - 1 - uu);
+#pragma unroll
+    for (int g = 0; g < NG; g++) {
+      const uint32_t y = ((uint32_t)g << (S - 4)) + tid;
+      const uint32_t tbase = (base << (S - 1 - u - DL)) + ((y >> DL) << (KP - u - 1));
+#pragma unroll
+      for (int e = 0; e < (1 << KP); e++) {
+        if (!(e & (1 << u))) {
+          const int i0 = g * (1 << KP) + e, i1 = i0 + (1 << u);
+          const ulonglong2 w = __ldg(&T[tbase + (e >> (u + 1))]);
+          const uint64_t X = v[i0], Y = v[i1];
+          if (!INV) {
+            const uint64_t Xr = X >= two_q ? X - two_q : X;
+            const uint64_t t = shoup_lazy(Y, w.x, w.y, q);
+            v[i0] = Xr + t;
+            v[i1] = Xr - t + two_q;
+          } else {
+            const uint64_t a = X + Y;
+            v[i0] = a >= two_q ? a - two_q : a;
+            v[i1] = shoup_lazy(X - Y + two_q, w.x, w.y, q);
+          }
+        }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ uint64_t final_reduce(uint64_t x, uint64_t q) {  // [0, 4q) -> [0, q)
+  if (x >= 2 * q) x -= 2 * q;
+  if (x >= q) x -= q;
+  return x;
+}
+
+// input element of the first kernel: in-place row, or source row (+ centred lift)
+struct InRow {
+  const uint64_t *p;
+  bool lift;
+  uint64_t qs, q, bar;
+  __device__ __forceinline__ uint64_t ld(size_t i) const {
+    const uint64_t v = p[i];
+    return lift ? lift_centred(v, qs, q, bar) : v;
+  }
+};
+
+__device__ __forceinline__ InRow in_row(uint64_t *data, const RowMap &map, const NttSrc &src, uint32_t row, uint32_t n,
+                                        int m, const ModTab &mt) {
+  InRow I;
+  if (src.base) {
+    I.p = src.base + row_off(src.map, row, n);
+    I.lift = src.lift;
+    I.qs = mt.q[row_mod(src.map, row)];
+  } else {
+    I.p = data + row_off(map, row, n);
+    I.lift = false;
+    I.qs = 0;
+  }
+  I.q = mt.q[m];
+  I.bar = mt.bar[m];
+  return I;
+}
+
+struct ColArgs {
+  uint32_t s2, tid, c;
+  uint64_t *a, *smt;
+  InRow in;
+  const ulonglong2 *T;
+  uint64_t q;
+  const uint64_t *ninv;
+  int m;
+  bool final_out;
+};
+
+template <bool INV, int S, int P>
+__device__ __forceinline__ void cols_rec(uint64_t (&v)[E], const ColArgs &A) {
+  using PP = Pass<INV, S, P>;
+#pragma unroll
+  for (int i = 0; i < E; i++) {
+    const uint32_t x = elem_of<PP::KP, PP::REM, S>(i, A.tid);
+    v[i] = P == 0 ? A.in.ld(((size_t)x << A.s2) + A.c) : A.smt[pad_idx(x)];
+  }
+  radix_pass<INV, PP::KP, PP::REM, S>(v, A.tid, 1u, A.T, A.q);
+  if constexpr (P == PP::NP - 1) {
+#pragma unroll
+    for (int i = 0; i < E; i++) {
+      uint64_t o = v[i];
+      if (INV) o = shoup(o, A.ninv[A.m], A.ninv[HD_MAXMOD + A.m], A.q);
+      else if (A.final_out) o = final_reduce(o, A.q);
+      A.a[((size_t)elem_of<PP::KP, PP::REM, S>(i, A.tid) << A.s2) + A.c] = o;
+    }
+  } else {
+    if (P > 0) __syncthreads();
+#pragma unroll
+    for (int i = 0; i < E; i++) A.smt[pad_idx(elem_of<PP::KP, PP::REM, S>(i, A.tid))] = v[i];
+    __syncthreads();
+    cols_rec<INV, S, P + 1>(v, A);
+  }
+}
+
+// ---- columns kernel: the S high stages; tpc columns per CTA, 2^(S-4) threads per column ----
+template <bool INV, int S>
+__global__ void __launch_bounds__(256) ntt_cols_kernel(uint64_t *base, RowMap rm, ModTab mt,
+                                                       const ulonglong2 *__restrict__ tw, int logn, int tpc,
+                                                       const uint64_t *__restrict__ ninv, uint32_t r0, bool final_out,
+                                                       NttSrc src) {
   extern __shared__ uint64_t sm[];
-  const uint32_t n = 1u << logn, s2 = logn - s1;
+  const uint32_t n = 1u << logn;
+  const uint32_t row = blockIdx.y + r0;
+  const int m = row_mod(rm, row);
+  ColArgs A;
+  A.s2 = logn - S;
+  A.q = mt.q[m];
+  A.a = row_ptr(base, rm, row, n);
+  A.in = in_row(base, rm, src, row, n, m, mt);
+  A.T = tw + (size_t)m * n;
+  const uint32_t tr = threadIdx.x % tpc;
+  A.tid = threadIdx.x / tpc;
+  A.c = blockIdx.x * tpc + tr;
+  A.smt = sm + tr * (pad_idx(1u << S) + 1);  // odd column stride: conflict-free across columns
+  A.ninv = ninv;
+  A.m = m;
+  A.final_out = final_out;
+  uint64_t v[E];
+  cols_rec<INV, S, 0>(v, A);
+}
+
+template <bool INV, int S, int P>
+__device__ __forceinline__ void chunks_rec(uint64_t (&v)[E], uint32_t tid, uint32_t bidx, uint64_t *smt,
+                                           const ulonglong2 *T, uint64_t q) {
+  using PP = Pass<INV, S, P>;
+#pragma unroll
+  for (int i = 0; i < E; i++) v[i] = smt[pad_idx(elem_of<PP::KP, PP::REM, S>(i, tid))];
+  radix_pass<INV, PP::KP, PP::REM, S>(v, tid, bidx, T, q);
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < E; i++) smt[pad_idx(elem_of<PP::KP, PP::REM, S>(i, tid))] = v[i];
+  __syncthreads();
+  if constexpr (P < PP::NP - 1) chunks_rec<INV, S, P + 1>(v, tid, bidx, smt, T, q);
+}
+
+// ---- chunks kernel: the S low stages on contiguous chunks of 2^S; tpc chunks per CTA ----
+template <bool INV, int S>
+__global__ void __launch_bounds__(256) ntt_chunks_kernel(uint64_t *base, RowMap rm, ModTab mt,
+                                                         const ulonglong2 *__restrict__ tw, int logn, int tpc,
+                                                         const uint64_t *__restrict__ ninv, uint32_t r0, bool final_out,
+                                                         NttSrc src, NttEpi epi) {
+  extern __shared__ uint64_t sm[];
+  constexpr uint32_t SZ = 1u << S, TPT = SZ / E, PS = SZ + (SZ >> 4);
+  const uint32_t n = 1u << logn, s1 = logn - S;
   const uint32_t row = blockIdx.y + r0;
   const int m = row_mod(rm, row);
   const uint64_t q = mt.q[m];
-  uint64_t *a = row_ptr(base, rm, row, n);
-  const uint64_t *T = tw + (size_t)m * n, *TS = tws + (size_t)m * n;
-  const uint32_t col0 = blockIdx.x * ch;
-  const uint32_t H = 1u << s1, tot = H * ch;
-  for (uint32_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-    uint32_t hi = idx / ch, c = idx % ch;
-    sm[idx] = a[((size_t)hi << s2) + col0 + c];
+  const uint32_t chunk0 = blockIdx.x * tpc;
+  const size_t off0 = (size_t)chunk0 * SZ;
+  uint64_t *a = row_ptr(base, rm, row, n) + off0;
+  const InRow in = in_row(base, rm, src, row, n, m, mt);
+  const ulonglong2 *T = tw + (size_t)m * n;
+  const uint32_t tr = threadIdx.x / TPT, tid = threadIdx.x % TPT;
+  const uint32_t total = tpc * SZ;
+  for (uint32_t i = threadIdx.x * 2; i < total; i += blockDim.x * 2) {
+    uint64_t w0, w1;
+    if (!in.lift) {
+      const ulonglong2 w = *reinterpret_cast<const ulonglong2 *>(in.p + off0 + i);
+      w0 = w.x;
+      w1 = w.y;
+    } else {
+      w0 = in.ld(off0 + i);
+      w1 = in.ld(off0 + i + 1);
+    }
+    const uint32_t t0 = i >> S, x0 = i & (SZ - 1);
+    sm[t0 * PS + pad_idx(x0)] = w0;
+    sm[t0 * PS + pad_idx(x0 + 1)] = w1;
   }
   __syncthreads();
-  const uint32_t nb = (H / 2) * ch;
-  for (int k = 0; k < s1; k++) {
-    int st = INV ? (s1 - 1 - k) : k;
-    uint32_t mm = 1u << st, th = 1u << (s1 - 1 - st);
-    for (uint32_t b = threadIdx.x; b < nb; b += blockDim.x) {
-      uint32_t c = b % ch, bi = b / ch;
-      uint32_t grp = bi >> (s1 - 1 - st);
-      uint32_t h0 = grp * 2 * th + (bi & (th - 1));
-      uint64_t &x0 = sm[h0 * ch + c], &x1 = sm[(h0 + th) * ch + c];
-      uint64_t w = T[mm + grp], ws = TS[mm + grp];
-      uint64_t u = x0, v = x1;
-      if (INV) gs_bfly(u, v, w, ws, q);
-      else ct_bfly(u, v, w, ws, q);
-      x0 = u;
-      x1 = v;
+  uint64_t v[E];
+  chunks_rec<INV, S, 0>(v, tid, (1u << s1) + chunk0 + tr, sm + tr * PS, T, q);
+  const bool scale = INV && s1 == 0;
+  const bool fin = !INV && final_out;
+  // epilogue rows: r = (x 2 + p) ell + l
+  const uint32_t l = row % epi.ell, p = (row / epi.ell) & 1, x = row / (2 * epi.ell);
+  uint64_t *dst = a;
+  const uint64_t *Arow = nullptr, *c0row = nullptr;
+  uint32_t g = 1;
+  if (fin && epi.mode) {
+    dst = row_ptr(epi.out, epi.omap, row, n) + off0;
+    Arow = epi.A + row_off(epi.amap, row, n) + off0;
+    if (epi.mode == 2 && p == 0) {
+      c0row = epi.c0 + (size_t)(x / epi.K) * epi.c0_stride + (size_t)l * n;
+      g = epi.gal[x % epi.K];
     }
-    __syncthreads();
   }
-  for (uint32_t idx = threadIdx.x; idx < tot; idx += blockDim.x) {
-    uint32_t hi = idx / ch, c = idx % ch;
-    uint64_t v = sm[idx];
-    if (INV) v = shoup(v, ninv[m], ninvs[m], q);
-    a[((size_t)hi << s2) + col0 + c] = v;
+  for (uint32_t i = threadIdx.x * 2; i < total; i += blockDim.x * 2) {
+    const uint32_t t0 = i >> S, x0 = i & (SZ - 1);
+    uint64_t o0 = sm[t0 * PS + pad_idx(x0)], o1 = sm[t0 * PS + pad_idx(x0 + 1)];
+    if (scale) {
+      o0 = shoup(o0, ninv[m], ninv[HD_MAXMOD + m], q);
+      o1 = shoup(o1, ninv[m], ninv[HD_MAXMOD + m], q);
+    } else if (fin) {
+      o0 = final_reduce(o0, q);
+      o1 = final_reduce(o1, q);
+      if (epi.mode) {
+        const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(Arow + i);
+        o0 = shoup(submod(av.x, o0, q), epi.w[m], epi.ws[m], q);
+        o1 = shoup(submod(av.y, o1, q), epi.w[m], epi.ws[m], q);
+        if (c0row) {
+          const uint32_t gi = (uint32_t)(off0 + i);
+          o0 = addmod(o0, c0row[galois_src(gi, g, logn)], q);
+          o1 = addmod(o1, c0row[galois_src(gi + 1, g, logn)], q);
+        }
+        if (epi.acc) {
+          const ulonglong2 dv = *reinterpret_cast<const ulonglong2 *>(dst + i);
+          o0 = addmod(o0, dv.x, q);
+          o1 = addmod(o1, dv.y, q);
+        }
+      }
+    }
+    *reinterpret_cast<ulonglong2 *>(dst + i) = make_ulonglong2(o0, o1);
   }
 }
 
-// Low stages on contiguous chunks of 2^s2 elements.
+typedef void (*cols_kernel_t)(uint64_t *, RowMap, ModTab, const ulonglong2 *, int, int, const uint64_t *, uint32_t,
+                              bool, NttSrc);
+typedef void (*chunks_kernel_t)(uint64_t *, RowMap, ModTab, const ulonglong2 *, int, int, const uint64_t *, uint32_t,
+                                bool, NttSrc, NttEpi);
+
 template <bool INV>
-__global__ void __launch_bounds__(NTT_THREADS) ntt_lo_kernel(uint64_t *base, RowMap rm, ModTab mt,
-                                                             const uint64_t *__restrict__ tw,
-                                                             const uint64_t *__restrict__ tws, int logn,
-                                                             int s1, const uint64_t *ninv,
-                                                             const uint64_t *ninvs, uint32_t r0) {
-  extern __shared__ uint64_t sm[];
-  const uint32_t n = 1u << logn, s2 = logn - s1, C = 1u << s2;
-  const uint32_t row = blockIdx.y + r0, hi = blockIdx.x;
-  const int m = row_mod(rm, row);
-  const uint64_t q = mt.q[m];
-  uint64_t *a = row_ptr(base, rm, row, n) + ((size_t)hi << s2);
-  const uint64_t *T = tw + (size_t)m * n, *TS = tws + (size_t)m * n;
-  for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) sm[i] = a[i];
-  __syncthreads();
-  for (int k = 0; k < (int)s2; k++) {
-    int st = INV ? ((int)s2 - 1 - k) : k;  // stage within the low part
-    uint32_t mm = 1u << (s1 + st);
-    uint32_t t = 1u << (s2 - 1 - st);
-    for (uint32_t b = threadIdx.x; b < C / 2; b += blockDim.x) {
-      uint32_t grp_l = b / t, off = b % t;  // group inside the chunk
-      uint32_t j0 = grp_l * 2 * t + off;
-      uint32_t grp = (hi << st) + grp_l;
-      uint64_t w = T[mm + grp], ws = TS[mm + grp];
-      uint64_t u = sm[j0], v = sm[j0 + t];
-      if (INV) gs_bfly(u, v, w, ws, q);
-      else ct_bfly(u, v, w, ws, q);
-      sm[j0] = u;
-      sm[j0 + t] = v;
-    }
-    __syncthreads();
+cols_kernel_t cols_for(int s) {
+  switch (s) {
+    case 5: return ntt_cols_kernel<INV, 5>;
+    case 6: return ntt_cols_kernel<INV, 6>;
+    case 7: return ntt_cols_kernel<INV, 7>;
+    case 8: return ntt_cols_kernel<INV, 8>;
   }
-  const bool scale = INV && s1 == 0;
-  for (uint32_t i = threadIdx.x; i < C; i += blockDim.x) {
-    uint64_t v = sm[i];
-    if (scale) v = shoup(v, ninv[m], ninvs[m], q);
-    a[i] = v;
+  return nullptr;
+}
+template <bool INV>
+chunks_kernel_t chunks_for(int s) {
+  switch (s) {
+    case 4: return ntt_chunks_kernel<INV, 4>;
+    case 5: return ntt_chunks_kernel<INV, 5>;
+    case 6: return ntt_chunks_kernel<INV, 6>;
+    case 7: return ntt_chunks_kernel<INV, 7>;
+    case 8: return ntt_chunks_kernel<INV, 8>;
+    case 9: return ntt_chunks_kernel<INV, 9>;
+    case 10: return ntt_chunks_kernel<INV, 10>;
+    case 11: return ntt_chunks_kernel<INV, 11>;
+    case 12: return ntt_chunks_kernel<INV, 12>;
   }
+  return nullptr;
 }
 
 }  // namespace
@@ -129,32 +319,64 @@ RowMap rowmap_simple(uint32_t mdiv, std::initializer_list<int> mods, uint32_t gs
   return rm;
 }
 
-// Constants n^{-1} per modulus live in a small device array inside the context's
-// twiddle allocation (see context.cu): ninv_dev = itw + (L+1) n, shoup after it.
-hd_status ntt_rows(hd_context *c, uint64_t *base, uint32_t rows, const RowMap &rm, bool inverse) {
+hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &map, bool inverse, const NttSrc *srcp,
+                  const NttEpi *epip) {
   if (rows == 0) return HD_OK;
   const int logn = c->logn;
-  const int s2 = logn <= 12 ? logn : LO_BITS_MAX;
-  const int s1 = logn - s2;
-  const uint64_t *ninv = c->itw + (size_t)(c->L + 1) * c->n;
-  const uint64_t *ninvs = ninv + HD_MAXMOD;
-  const size_t lo_smem = sizeof(uint64_t) << s2;
-  int ch = s1 ? (2048 >> s1) : 0;
-  if (ch < 16) ch = 16;
-  const size_t hi_smem = sizeof(uint64_t) * ((size_t)ch << s1);
-  dim3 glo(1u << s1, rows), ghi((1u << s2) / ch, rows);
+  const int s2 = logn <= 12 ? logn : 8;  // chunk stages
+  const int s1 = logn - s2;              // column stages (0, or 5..8)
+  const ulonglong2 *tw = reinterpret_cast<const ulonglong2 *>(inverse ? c->itw2 : c->tw2);
+  const uint64_t *ninv = c->ninv_dev;
+  const NttSrc none_src{};
+  const NttEpi none_epi{};
+  const NttSrc src = srcp ? *srcp : none_src;
+  const NttEpi epi = epip ? *epip : none_epi;
+  if (inverse && epi.mode) return hd_fail(HD_E_INVALID_ARG, "epilogue only on forward transforms");
+  const int tpt_b = 1 << (s2 - 4);
+  const int tpc_b = std::max(1, std::min(256 / tpt_b, 1 << s1));
+  const size_t smem_b = sizeof(uint64_t) * tpc_b * (size_t)((1 << s2) + ((1 << s2) >> 4));
+  const int tpt_a = s1 >= 4 ? 1 << (s1 - 4) : 1;
+  const int tpc_a = std::max(1, std::min(256 / tpt_a, 1 << s2));
+  const size_t smem_a = sizeof(uint64_t) * tpc_a * (size_t)((1 << s1) + ((1 << s1) >> 4) + 1);
+  chunks_kernel_t kb = inverse ? chunks_for<true>(s2) : chunks_for<false>(s2);
+  cols_kernel_t ka = s1 ? (inverse ? cols_for<true>(s1) : cols_for<false>(s1)) : nullptr;
+  if (!kb || (s1 && !ka)) return hd_fail(HD_E_PARAMS, "unsupported NTT size");
+  if (!c->ntt_attr_set) {
+    for (int s = 4; s <= 12; s++) {
+      cudaFuncSetAttribute(chunks_for<false>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      cudaFuncSetAttribute(chunks_for<true>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    }
+    for (int s = 5; s <= 8; s++) {
+      cudaFuncSetAttribute(cols_for<false>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      cudaFuncSetAttribute(cols_for<true>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    }
+    c->ntt_attr_set = true;
+  }
   for (uint32_t r0 = 0; r0 < rows; r0 += 65535) {
-    uint32_t rr = rows - r0 < 65535 ? rows - r0 : 65535;
-    glo.y = rr;
-    ghi.y = rr;
+    const uint32_t rr = rows - r0 < 65535 ? rows - r0 : 65535;
+    const dim3 ga(s1 ? (1u << s2) / tpc_a : 1, rr), gb((1u << s1) / tpc_b, rr);
     if (!inverse) {
-      if (s1) { ntt_hi_kernel<false><<<ghi, NTT_THREADS, hi_smem, c->stream>>>(base, rm, c->mt, c->tw, c->tws, logn, s1, ch, ninv, ninvs, r0); ++c->launches; }
-      ntt_lo_kernel<false><<<glo, NTT_THREADS, lo_smem, c->stream>>>(base, rm, c->mt, c->tw, c->tws, logn, s1, ninv, ninvs, r0); ++c->launches;
+      if (s1) {
+        ka<<<ga, tpc_a * tpt_a, smem_a, c->stream>>>(data, map, c->mt, tw, logn, tpc_a, ninv, r0, false, src);
+        ++c->launches;
+      }
+      kb<<<gb, tpc_b * tpt_b, smem_b, c->stream>>>(data, map, c->mt, tw, logn, tpc_b, ninv, r0, true,
+                                                   s1 ? none_src : src, epi);
+      ++c->launches;
     } else {
-      ntt_lo_kernel<true><<<glo, NTT_THREADS, lo_smem, c->stream>>>(base, rm, c->mt, c->itw, c->itws, logn, s1, ninv, ninvs, r0); ++c->launches;
-      if (s1) { ntt_hi_kernel<true><<<ghi, NTT_THREADS, hi_smem, c->stream>>>(base, rm, c->mt, c->itw, c->itws, logn, s1, ch, ninv, ninvs, r0); ++c->launches; }
+      kb<<<gb, tpc_b * tpt_b, smem_b, c->stream>>>(data, map, c->mt, tw, logn, tpc_b, ninv, r0, false, src,
+                                                   none_epi);
+      ++c->launches;
+      if (s1) {
+        ka<<<ga, tpc_a * tpt_a, smem_a, c->stream>>>(data, map, c->mt, tw, logn, tpc_a, ninv, r0, true, none_src);
+        ++c->launches;
+      }
     }
   }
   HD_CUDA(cudaGetLastError());
   return HD_OK;
+}
+
+hd_status ntt_rows(hd_context *c, uint64_t *base, uint32_t rows, const RowMap &rm, bool inverse) {
+  return ntt_run(c, base, rows, rm, inverse, nullptr, nullptr);
 }

@@ -57,7 +57,7 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query) {
   HD_CUDA(cudaMemcpyAsync(db->r, query->data, ctL * 8, cudaMemcpyDeviceToDevice, c->stream));
   if (n1 > 1) {
     if ((s = ks_modup(c, query->data + (size_t)L * n, 0, 1, L, db->dig, db->tmp))) return s;
-    if ((s = ks_kip(c, db->dig, 1, n1 - 1, L, db->kptr, db->gal, db->u))) return s;
+    if ((s = ks_kip(c, db->dig, query->data + (size_t)L * n, 0, 1, n1 - 1, L, db->kptr, db->gal, db->u))) return s;
     if ((s = ks_moddown(c, db->u, n1 - 1, n1 - 1, L, db->gal, query->data, 0, db->r + ctL, ctL, false, db->tmp)))
       return s;
   }
@@ -84,7 +84,9 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query) {
     }
     const size_t slot = (size_t)(n1 - 1) + jj;
     if ((s = ks_modup(c, Sj + (size_t)(L - 1) * n, sp_stride, A, L - 1, db->dig, db->tmp))) return s;
-    if ((s = ks_kip(c, db->dig, A, 1, L - 1, db->kptr + slot, db->gal + slot, db->u))) return s;
+    if ((s = ks_kip(c, db->dig, Sj + (size_t)(L - 1) * n, sp_stride, A, 1, L - 1, db->kptr + slot, db->gal + slot,
+                    db->u)))
+      return s;
     if ((s = ks_moddown(c, db->u, A, 1, L - 1, db->gal + slot, Sj, sp_stride, db->y, ct1, true, db->tmp))) return s;
   }
   cudaEventRecord(E[4], c->stream);
@@ -93,7 +95,9 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query) {
     const size_t slot = (size_t)(n1 - 1) + nj;
     HD_CUDA(cudaMemcpyAsync(db->outbuf, db->y, (size_t)A * ct1 * 8, cudaMemcpyDeviceToDevice, c->stream));
     if ((s = ks_modup(c, db->y + (size_t)(L - 1) * n, ct1, A, L - 1, db->dig, db->tmp))) return s;
-    if ((s = ks_kip(c, db->dig, A, 1, L - 1, db->kptr + slot, db->gal + slot, db->u))) return s;
+    if ((s = ks_kip(c, db->dig, db->y + (size_t)(L - 1) * n, ct1, A, 1, L - 1, db->kptr + slot, db->gal + slot,
+                    db->u)))
+      return s;
     if ((s = ks_moddown(c, db->u, A, 1, L - 1, db->gal + slot, db->y, ct1, db->outbuf, ct1, true, db->tmp))) return s;
   }
   cudaEventRecord(E[5], c->stream);
@@ -225,7 +229,7 @@ extern "C" hd_status hd_test_rotate(hd_context *c, const hd_eval_keys *evk, cons
   hd_ciphertext *o;
   hd_status s = alloc_ct(c, ell, &o);
   if (!s) s = ks_modup(c, ct->data + (size_t)ell * n, 0, 1, ell, dig, tmp);
-  if (!s) s = ks_kip(c, dig, 1, 1, ell, (const uint64_t *const *)kp, g, u);
+  if (!s) s = ks_kip(c, dig, ct->data + (size_t)ell * n, 0, 1, 1, ell, (const uint64_t *const *)kp, g, u);
   if (!s) s = ks_moddown(c, u, 1, 1, ell, g, ct->data, 0, o->data, 0, false, tmp);
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (!s && e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
