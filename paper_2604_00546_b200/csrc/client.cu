@@ -334,12 +334,14 @@ extern "C" hd_status hd_encrypt_query(hd_context *c, const hd_secret_key *sk, co
     hd_ciphertext_destroy(ct);
     return s;
   }
+  HD_CUDA(cudaEventRecord(ct->ready, c->stream));
   *out = ct;
   return HD_OK;
 }
 
 static hd_status decrypt_to(hd_context *c, const hd_secret_key *sk, const hd_ciphertext *ct, uint64_t *m) {
   const int n = c->n;
+  HD_CUDA(cudaStreamWaitEvent(c->stream, ct->ready, 0));
   decrypt_kernel<<<dim3((n + TPB - 1) / TPB, ct->limbs), TPB, 0, c->stream>>>(ct->data, sk->s_ntt, n, ct->limbs, m,
                                                                              c->mt); ++c->launches;
   HD_CUDA(cudaGetLastError());

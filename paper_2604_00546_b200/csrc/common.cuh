@@ -142,6 +142,7 @@ struct hd_context {
   int ev_next = 0, ev_pending = 0;
   double last_phase_ms[5] = {0, 0, 0, 0, 0};
   uint64_t launches = 0;  // kernels launched on this context (hd_launch_count)
+  cudaStream_t sA = nullptr, sB = nullptr;  // internal streams of the query pipeline
 };
 
 struct hd_secret_key {
@@ -164,7 +165,8 @@ struct hd_eval_keys {
 struct hd_ciphertext {
   hd_context *ctx;
   uint32_t limbs;
-  uint64_t *data;  // [2][limbs][n]
+  uint64_t *data;                 // [2][limbs][n]
+  cudaEvent_t ready = nullptr;    // recorded by the last writer (any stream); readers wait on it
 };
 
 struct hd_database {
@@ -173,7 +175,11 @@ struct hd_database {
   uint32_t N, M, n1, A_loc;
   std::vector<int32_t> js;       // giant steps j (contiguous, non-empty ranges)
   std::vector<int32_t> pre;      // preRot(j) per j
-  uint64_t *D = nullptr;         // [A_loc][N][L][n] diagonal plaintexts
+  uint64_t *D = nullptr;         // [A_loc][N][L][n] diagonal plaintexts (or MAC-tiled, below)
+  // tiled: per aggregate [limb][tile of 128 coefs][giant group][baby i][jj < tile_jt][128]
+  // so every MAC CTA streams one contiguous n1 * tile_jt KiB block (mac.cu)
+  bool tiled = false;
+  uint32_t tile_jt = 2;
   // query workspaces (allocated at enrollment; reused by every hd_query)
   uint64_t *r = nullptr;         // [n1][2][L][n] baby steps
   uint64_t *S = nullptr;         // [A_loc][nj][2][L][n] giant-step sums
@@ -185,6 +191,12 @@ struct hd_database {
   uint64_t *tmp = nullptr;       // INTT / lift scratch
   uint64_t *tmp2 = nullptr;      // rescale scratch
   uint32_t rescale_chunk = 1;
+  // two-stream pipeline (query.cu): baby steps + MAC of query q+1 on stream A overlap the
+  // rescale / giant / fold of query q on stream B; S is double-buffered.
+  uint64_t *S2 = nullptr;                                  // second giant-sum buffer
+  uint64_t *dig_b = nullptr, *u_b = nullptr, *tmp_b = nullptr;  // baby-step scratch (stream A)
+  uint64_t qcount = 0;
+  cudaEvent_t ev_in = nullptr, ev_mac = nullptr, ev_done = nullptr, ev_sfree[2] = {nullptr, nullptr};
   // rotation-key tables for the (db, evk) pair last used: [0, n1-1) baby i = 1..n1-1,
   // [n1-1, n1-1+nj) giant j (NULL key when preRot = 0), [n1-1+nj] fold
   const hd_eval_keys *keyed_for = nullptr;

@@ -218,6 +218,8 @@ extern "C" void hd_context_destroy(hd_context *c) {
   cudaFree(c->rotg);
   cudaFree(c->d_flag);
   cudaFree(c->scratch);
+  if (c->sA) cudaStreamDestroy(c->sA);
+  if (c->sB) cudaStreamDestroy(c->sB);
   for (int i = 0; i < 8; i++)
     for (int k = 0; k < 64; k++)
       if (c->ev[k][i]) cudaEventDestroy(c->ev[k][i]);
@@ -277,7 +279,9 @@ cudaMemcpyKind kind_of(int dst_dev, int src_dev) {
 hd_status alloc_ct(hd_context *c, uint32_t limbs, hd_ciphertext **out) {
   hd_ciphertext *ct = new hd_ciphertext{c, limbs, nullptr};
   cudaError_t e = cudaMalloc(&ct->data, sizeof(uint64_t) * 2 * limbs * c->n);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ct->ready, cudaEventDisableTiming);
   if (e != cudaSuccess) {
+    cudaFree(ct->data);
     delete ct;
     return hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, "ciphertext alloc");
   }
@@ -306,9 +310,10 @@ extern "C" hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, si
   h.limbs = ct->limbs;
   h.mod_fp = mod_fingerprint(c);
   h.payload = payload;
+  HD_CUDA(cudaStreamWaitEvent(c->stream, ct->ready, 0));  // last writer (e.g. hd_query's stream B)
   HD_CUDA(cudaMemcpyAsync(dst, &h, sizeof(h), kind_of(dst_on_device, 0), c->stream));
   HD_CUDA(cudaMemcpyAsync((char *)dst + sizeof(h), ct->data, payload, kind_of(dst_on_device, 1), c->stream));
-  HD_CUDA(cudaStreamSynchronize(c->stream));
+  if (!dst_on_device) HD_CUDA(cudaStreamSynchronize(c->stream));  // host copy complete on return
   return HD_OK;
 }
 
@@ -339,6 +344,7 @@ extern "C" hd_status hd_ciphertext_import(hd_context *c, const void *src, size_t
   if ((s = alloc_ct(c, h.limbs, &ct))) return s;
   cudaError_t e = cudaMemcpyAsync(ct->data, (const char *)src + sizeof(Header), h.payload,
                                   kind_of(1, src_on_device), c->stream);
+  if (e == cudaSuccess) e = cudaEventRecord(ct->ready, c->stream);
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
     hd_ciphertext_destroy(ct);
@@ -362,11 +368,16 @@ extern "C" hd_status hd_ciphertext_import_into(hd_ciphertext *ct, const void *sr
   }
   HD_CUDA(cudaMemcpyAsync(ct->data, (const char *)src + sizeof(Header), payload, kind_of(1, src_on_device),
                           c->stream));
+  HD_CUDA(cudaEventRecord(ct->ready, c->stream));
   return HD_OK;
 }
 
 extern "C" void hd_ciphertext_destroy(hd_ciphertext *ct) {
   if (!ct) return;
+  if (ct->ready) {
+    cudaEventSynchronize(ct->ready);
+    cudaEventDestroy(ct->ready);
+  }
   cudaFree(ct->data);
   delete ct;
 }

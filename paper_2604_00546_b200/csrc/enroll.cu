@@ -216,6 +216,12 @@ extern "C" void hd_database_destroy(hd_database *db) {
   cudaFree(db->outbuf);
   cudaFree(db->kptr);
   cudaFree(db->gal);
+  cudaFree(db->S2);
+  cudaFree(db->dig_b);
+  cudaFree(db->u_b);
+  cudaFree(db->tmp_b);
+  for (cudaEvent_t e : {db->ev_in, db->ev_mac, db->ev_done, db->ev_sfree[0], db->ev_sfree[1]})
+    if (e) cudaEventDestroy(e);
   delete db;
 }
 
@@ -252,11 +258,13 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
     }
   const size_t A = db->A_loc, nj = db->js.size(), ctL = (size_t)2 * L * n, ct1 = (size_t)2 * (L - 1) * n;
   const size_t rescale_chunk = std::min<size_t>(A * nj, 256);
-  size_t dig_e = std::max((size_t)L * (L + 1) * n, A * (L - 1) * L * n);
-  size_t u_e = std::max((size_t)(n1 > 1 ? n1 - 1 : 1) * 2 * (L + 1) * n, A * 2 * L * n);
-  size_t tmp_e = std::max({(size_t)(n1 > 1 ? n1 - 1 : 1) * 2 * L * n, A * 2 * L * n, rescale_chunk * 2 * n,
-                           (size_t)L * n});
-  size_t tmp2_e = rescale_chunk * 2 * (L - 1) * n;
+  const size_t nb = n1 > 1 ? n1 - 1 : 1;
+  // giant / fold / rescale scratch (stream B) and baby-step scratch (stream A)
+  size_t dig_e = A * (L - 1) * (L - 1) * n;
+  size_t u_e = A * 2 * L * n;
+  size_t tmp_e = std::max({A * 2 * (L - 1) * n, rescale_chunk * 2 * n, (size_t)L * n});
+  size_t tmp2_e = 1;
+  size_t digb_e = (size_t)L * L * n, ub_e = nb * 2 * (L + 1) * n, tmpb_e = std::max(nb * 2 * L * n, (size_t)L * n);
   db->rescale_chunk = (uint32_t)rescale_chunk;
   struct Req {
     void **p;
@@ -270,7 +278,11 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
               {(void **)&db->dig, dig_e * 8},
               {(void **)&db->u, u_e * 8},
               {(void **)&db->tmp, tmp_e * 8},
-              {(void **)&db->tmp2, tmp2_e * 8}};
+              {(void **)&db->tmp2, tmp2_e * 8},
+              {(void **)&db->S2, A * nj * ctL * 8},
+              {(void **)&db->dig_b, digb_e * 8},
+              {(void **)&db->u_b, ub_e * 8},
+              {(void **)&db->tmp_b, tmpb_e * 8}};
   size_t total = 0;
   for (auto &q : reqs) total += q.bytes;
   size_t fr = 0, tot = 0;
@@ -288,6 +300,11 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
     }
   }
   db->bytes = total;
+  for (cudaEvent_t *e : {&db->ev_in, &db->ev_mac, &db->ev_done, &db->ev_sfree[0], &db->ev_sfree[1]})
+    if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) {
+      hd_database_destroy(db);
+      return hd_fail(HD_E_CUDA, "event creation");
+    }
   // enrollment scratch: rows of one aggregate (float + double), FFT buffers for a batch of diagonals
   const size_t rows_per_agg = (size_t)(db->M / 2) * N;
   const int KB = std::min(N, std::max(1, (int)((256ull << 20) / ((size_t)ns * 16))));
@@ -303,8 +320,16 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
     cudaFree(re);
     cudaFree(im);
   };
+  // MAC-tiled diagonal layout (mac.cu): needs every giant step to use all n1 baby steps
+  const int nj_ = (int)db->js.size();
+  db->tile_jt = nj_ % 2 == 0 ? 2 : 1;
+  const char *no_tile = getenv("HD_NO_TILE");
+  db->tiled = (N / 2) % (int)n1 == 0 && n % 128 == 0 && !(no_tile && no_tile[0] == '1');
+  uint64_t *Dtmp = nullptr;
+  if (!e && db->tiled) e = cudaMalloc(&Dtmp, (size_t)N * L * n * 8);
   if (e) {
     cleanup();
+    cudaFree(Dtmp);
     hd_database_destroy(db);
     return hd_fail(HD_E_CAPACITY, "enrollment scratch");
   }
@@ -320,15 +345,19 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
     }
     if ((s = normalize_on_device(c, dv, rows, N, U))) break;
     if ((s = check_flag(c))) break;
-    uint64_t *Da = db->D + (size_t)(a - agg_begin) * N * L * n;
+    uint64_t *Dfinal = db->D + (size_t)(a - agg_begin) * N * L * n;
+    uint64_t *Da = db->tiled ? Dtmp : Dfinal;
     for (int k0 = 0; k0 < N && !s; k0 += KB) {
       int kb = std::min(KB, N - k0);
       pack_kernel<<<dim3((ns + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(U, (long long)v0, (long long)num_vectors, N,
                                                                          db->M, n1, a, k0, ns, re, im); ++c->launches;
       s = encode_batch(c, re, im, kb, delta, L, Da + (size_t)k0 * L * n, (size_t)L * n);
     }
+    if (!s && db->tiled) s = mac_tile_aggregate(c, Dtmp, Dfinal, N, (int)n1, db->js.front(), (int)db->js.size(),
+                                                (int)db->tile_jt);
     if (!s) s = check_flag(c);
   }
+  cudaFree(Dtmp);
   cleanup();
   if (s) {
     hd_database_destroy(db);

@@ -46,11 +46,41 @@ __device__ __forceinline__ uint32_t elem_of(int slot, uint32_t tid) {
   return ((y >> DL) << REM) + ((uint32_t)e << DL) + (y & ((1u << DL) - 1));
 }
 
+// Twiddles of a kernel, staged in shared memory at kernel start: for every level k
+// (2^k butterfly groups per transform) the tpc transforms of the CTA use the contiguous
+// table range T[(b0 + tr) 2^k + local], b0 = first transform's block index; level k is
+// stored at tpc (2^k - 1) + tr 2^k + local.
+struct TwShared {
+  const ulonglong2 *sm;
+  uint32_t tr, tpc;
+  __device__ __forceinline__ ulonglong2 get(int k, uint32_t local) const {
+    return sm[tpc * ((1u << k) - 1) + (tr << k) + local];
+  }
+};
+// Twiddles read straight from the global table (L1/L2): T[(b0 + tr) 2^k + local].
+struct TwGlobal {
+  const ulonglong2 *T;
+  uint32_t blk;  // b0 + tr
+  __device__ __forceinline__ ulonglong2 get(int k, uint32_t local) const {
+    return __ldg(&T[((size_t)blk << k) + local]);
+  }
+};
+template <int S>
+__device__ __forceinline__ void stage_twiddles(ulonglong2 *dst, const ulonglong2 *__restrict__ T, uint32_t b0,
+                                               uint32_t tpc) {
+#pragma unroll 1
+  for (int k = 0; k < S; k++) {
+    const uint32_t cnt = tpc << k;
+    const ulonglong2 *src = T + ((size_t)b0 << k);
+    ulonglong2 *d = dst + tpc * ((1u << k) - 1);
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) d[i] = __ldg(src + i);
+  }
+}
+
 // KP <= 4 butterfly stages in registers.  The butterfly at distance d = 2^(u + DL)
-// uses twiddle T[base 2^(S-1-u-DL) + (y >> DL) 2^(KP-u-1) + (e >> (u+1))].
-template <bool INV, int KP, int REM, int S>
-__device__ __forceinline__ void radix_pass(uint64_t (&v)[E], uint32_t tid, uint32_t base,
-                                           const ulonglong2 *__restrict__ T, uint64_t q) {
+// uses the twiddle of level k = S-1-u-DL, local index (y >> DL) 2^(KP-u-1) + (e >> (u+1)).
+template <bool INV, int KP, int REM, int S, class TW>
+__device__ __forceinline__ void radix_pass(uint64_t (&v)[E], uint32_t tid, const TW &tw, uint64_t q) {
   constexpr int NG = 1 << (4 - KP);
   constexpr int DL = REM - KP;
   const uint64_t two_q = 2 * q;
@@ -60,12 +90,12 @@ __device__ __forceinline__ void radix_pass(uint64_t (&v)[E], uint32_t tid, uint3
 #pragma unroll
     for (int g = 0; g < NG; g++) {
       const uint32_t y = ((uint32_t)g << (S - 4)) + tid;
-      const uint32_t tbase = (base << (S - 1 - u - DL)) + ((y >> DL) << (KP - u - 1));
+      const uint32_t tloc = (y >> DL) << (KP - u - 1);
 #pragma unroll
       for (int e = 0; e < (1 << KP); e++) {
         if (!(e & (1 << u))) {
           const int i0 = g * (1 << KP) + e, i1 = i0 + (1 << u);
-          const ulonglong2 w = __ldg(&T[tbase + (e >> (u + 1))]);
+          const ulonglong2 w = tw.get(S - 1 - u - DL, tloc + (e >> (u + 1)));
           const uint64_t X = v[i0], Y = v[i1];
           if (!INV) {
             const uint64_t Xr = X >= two_q ? X - two_q : X;
@@ -121,7 +151,7 @@ struct ColArgs {
   uint32_t s2, tid, c;
   uint64_t *a, *smt;
   InRow in;
-  const ulonglong2 *T;
+  TwShared tw;
   uint64_t q;
   const uint64_t *ninv;
   int m;
@@ -136,7 +166,7 @@ __device__ __forceinline__ void cols_rec(uint64_t (&v)[E], const ColArgs &A) {
     const uint32_t x = elem_of<PP::KP, PP::REM, S>(i, A.tid);
     v[i] = P == 0 ? A.in.ld(((size_t)x << A.s2) + A.c) : A.smt[pad_idx(x)];
   }
-  radix_pass<INV, PP::KP, PP::REM, S>(v, A.tid, 1u, A.T, A.q);
+  radix_pass<INV, PP::KP, PP::REM, S>(v, A.tid, A.tw, A.q);
   if constexpr (P == PP::NP - 1) {
 #pragma unroll
     for (int i = 0; i < E; i++) {
@@ -169,30 +199,37 @@ __global__ void __launch_bounds__(256) ntt_cols_kernel(uint64_t *base, RowMap rm
   A.q = mt.q[m];
   A.a = row_ptr(base, rm, row, n);
   A.in = in_row(base, rm, src, row, n, m, mt);
-  A.T = tw + (size_t)m * n;
   const uint32_t tr = threadIdx.x % tpc;
   A.tid = threadIdx.x / tpc;
   A.c = blockIdx.x * tpc + tr;
-  A.smt = sm + tr * (pad_idx(1u << S) + 1);  // odd column stride: conflict-free across columns
+  const uint32_t col_stride = pad_idx(1u << S) + 1;  // odd column stride: conflict-free across columns
+  A.smt = sm + tr * col_stride;
+  // every column of the row uses the same twiddles T[1 .. 2^S - 1]
+  ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(sm + ((tpc * col_stride + 1) & ~1u));
+  stage_twiddles<S>(tws, tw + (size_t)m * n, 1u, 1u);
+  A.tw.sm = tws;
+  A.tw.tr = 0;
+  A.tw.tpc = 1;
   A.ninv = ninv;
   A.m = m;
   A.final_out = final_out;
+  __syncthreads();
   uint64_t v[E];
   cols_rec<INV, S, 0>(v, A);
 }
 
 template <bool INV, int S, int P>
-__device__ __forceinline__ void chunks_rec(uint64_t (&v)[E], uint32_t tid, uint32_t bidx, uint64_t *smt,
-                                           const ulonglong2 *T, uint64_t q) {
+__device__ __forceinline__ void chunks_rec(uint64_t (&v)[E], uint32_t tid, uint64_t *smt, const TwGlobal &tw,
+                                           uint64_t q) {
   using PP = Pass<INV, S, P>;
 #pragma unroll
   for (int i = 0; i < E; i++) v[i] = smt[pad_idx(elem_of<PP::KP, PP::REM, S>(i, tid))];
-  radix_pass<INV, PP::KP, PP::REM, S>(v, tid, bidx, T, q);
+  radix_pass<INV, PP::KP, PP::REM, S>(v, tid, tw, q);
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < E; i++) smt[pad_idx(elem_of<PP::KP, PP::REM, S>(i, tid))] = v[i];
   __syncthreads();
-  if constexpr (P < PP::NP - 1) chunks_rec<INV, S, P + 1>(v, tid, bidx, smt, T, q);
+  if constexpr (P < PP::NP - 1) chunks_rec<INV, S, P + 1>(v, tid, smt, tw, q);
 }
 
 // ---- chunks kernel: the S low stages on contiguous chunks of 2^S; tpc chunks per CTA ----
@@ -211,9 +248,13 @@ __global__ void __launch_bounds__(256) ntt_chunks_kernel(uint64_t *base, RowMap 
   const size_t off0 = (size_t)chunk0 * SZ;
   uint64_t *a = row_ptr(base, rm, row, n) + off0;
   const InRow in = in_row(base, rm, src, row, n, m, mt);
-  const ulonglong2 *T = tw + (size_t)m * n;
   const uint32_t tr = threadIdx.x / TPT, tid = threadIdx.x % TPT;
   const uint32_t total = tpc * SZ;
+  // twiddles of this chunk: transform block index 2^s1 + chunk0 + tr at every level
+  // (each chunk uses its own 2^S - 1 entries: read from L1/L2, not staged)
+  TwGlobal twv;
+  twv.T = tw + (size_t)m * n;
+  twv.blk = (1u << s1) + chunk0 + tr;
   for (uint32_t i = threadIdx.x * 2; i < total; i += blockDim.x * 2) {
     uint64_t w0, w1;
     if (!in.lift) {
@@ -230,7 +271,7 @@ __global__ void __launch_bounds__(256) ntt_chunks_kernel(uint64_t *base, RowMap 
   }
   __syncthreads();
   uint64_t v[E];
-  chunks_rec<INV, S, 0>(v, tid, (1u << s1) + chunk0 + tr, sm + tr * PS, T, q);
+  chunks_rec<INV, S, 0>(v, tid, sm + tr * PS, twv, q);
   const bool scale = INV && s1 == 0;
   const bool fin = !INV && final_out;
   // epilogue rows: r = (x 2 + p) ell + l
@@ -337,18 +378,19 @@ hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &ma
   const size_t smem_b = sizeof(uint64_t) * tpc_b * (size_t)((1 << s2) + ((1 << s2) >> 4));
   const int tpt_a = s1 >= 4 ? 1 << (s1 - 4) : 1;
   const int tpc_a = std::max(1, std::min(256 / tpt_a, 1 << s2));
-  const size_t smem_a = sizeof(uint64_t) * tpc_a * (size_t)((1 << s1) + ((1 << s1) >> 4) + 1);
+  const size_t smem_a = sizeof(uint64_t) * (tpc_a * (size_t)((1 << s1) + ((1 << s1) >> 4) + 1) + 2) +
+                        16 * (size_t)((1 << s1) - 1);
   chunks_kernel_t kb = inverse ? chunks_for<true>(s2) : chunks_for<false>(s2);
   cols_kernel_t ka = s1 ? (inverse ? cols_for<true>(s1) : cols_for<false>(s1)) : nullptr;
   if (!kb || (s1 && !ka)) return hd_fail(HD_E_PARAMS, "unsupported NTT size");
   if (!c->ntt_attr_set) {
     for (int s = 4; s <= 12; s++) {
-      cudaFuncSetAttribute(chunks_for<false>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      cudaFuncSetAttribute(chunks_for<true>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      cudaFuncSetAttribute(chunks_for<false>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(chunks_for<true>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     }
     for (int s = 5; s <= 8; s++) {
-      cudaFuncSetAttribute(cols_for<false>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-      cudaFuncSetAttribute(cols_for<true>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+      cudaFuncSetAttribute(cols_for<false>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(cols_for<true>(s), cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     }
     c->ntt_attr_set = true;
   }

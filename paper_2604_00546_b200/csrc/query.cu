@@ -7,10 +7,13 @@
 //          local aggregates a, KIP with key preRot(j) (read once for all a), ModDown
 //          accumulated into y_a; S'_{a,j} with preRot = 0 added directly
 //   a8     fold: out_a = y_a + Rot_{numSlots-N}(y_a), batched over a
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
 #include "ks.cuh"
+
+static hd_status giant_and_fold(hd_database *db, cudaEvent_t *E);
 
 static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
   hd_context *c = db->ctx;
@@ -43,36 +46,81 @@ static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
   return HD_OK;
 }
 
-static hd_status run_scan(hd_database *db, const hd_ciphertext *query) {
+// Stream A: baby steps + MAC of this query (into the S buffer of its parity).
+// Stream B: rescale / giant rotations / fold (+ output copies).  A query's B work
+// overlaps the next query's A work; S is double-buffered (A waits until B's rescale
+// of the query two back has consumed the buffer).  With HD_SERIAL=1 both run on the
+// caller's stream.
+static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStream_t sa, cudaStream_t sb,
+                          hd_ciphertext **out, size_t n_out) {
   hd_context *c = db->ctx;
   const int n = c->n, L = c->L, n1 = (int)db->n1, nj = (int)db->js.size();
   const uint32_t A = db->A_loc;
   const size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * (L - 1) * n;
+  const int par = (int)(db->qcount & 1);
+  uint64_t *Sbuf = par ? db->S2 : db->S;
+  cudaStream_t caller = c->stream;
   hd_status s;
   cudaEvent_t *E = c->ev[c->ev_next % 64];
   c->ev_next++;
   c->ev_pending = std::min(c->ev_pending + 1, 64);
-  cudaEventRecord(E[0], c->stream);
+  // ---------------- stream A ----------------
+  // A depends only on the query's last writer (not on the caller's stream position), so
+  // the baby steps + MAC of this query can run while B still finishes the previous one.
+  HD_CUDA(cudaEventRecord(db->ev_in, caller));
+  HD_CUDA(cudaStreamWaitEvent(sa, query->ready, 0));
+  if (db->qcount >= 2) HD_CUDA(cudaStreamWaitEvent(sa, db->ev_sfree[par], 0));
+  c->stream = sa;
+  cudaEventRecord(E[0], sa);
   // ---- baby steps: r[0] = q; r[i] = Rot_i(q), hoisted ----
-  HD_CUDA(cudaMemcpyAsync(db->r, query->data, ctL * 8, cudaMemcpyDeviceToDevice, c->stream));
+  HD_CUDA(cudaMemcpyAsync(db->r, query->data, ctL * 8, cudaMemcpyDeviceToDevice, sa));
   if (n1 > 1) {
-    if ((s = ks_modup(c, query->data + (size_t)L * n, 0, 1, L, db->dig, db->tmp))) return s;
-    if ((s = ks_kip(c, db->dig, query->data + (size_t)L * n, 0, 1, n1 - 1, L, db->kptr, db->gal, db->u))) return s;
-    if ((s = ks_moddown(c, db->u, n1 - 1, n1 - 1, L, db->gal, query->data, 0, db->r + ctL, ctL, false, db->tmp)))
+    if ((s = ks_modup(c, query->data + (size_t)L * n, 0, 1, L, db->dig_b, db->tmp_b))) return s;
+    if ((s = ks_kip(c, db->dig_b, query->data + (size_t)L * n, 0, 1, n1 - 1, L, db->kptr, db->gal, db->u_b)))
+      return s;
+    if ((s = ks_moddown(c, db->u_b, n1 - 1, n1 - 1, L, db->gal, query->data, 0, db->r + ctL, ctL, false,
+                        db->tmp_b)))
       return s;
   }
-  cudaEventRecord(E[1], c->stream);
+  cudaEventRecord(E[1], sa);
   // ---- MAC ----
-  if ((s = mac_run(c, db->D, db->r, db->S, A, n1, (int)db->N, db->js))) return s;
-  cudaEventRecord(E[2], c->stream);
-  // ---- rescale every S_{a,j} ----
-  const uint32_t total = A * nj;
-  for (uint32_t b0 = 0; b0 < total; b0 += db->rescale_chunk) {
-    uint32_t B = std::min(db->rescale_chunk, total - b0);
-    if ((s = ks_rescale(c, db->S + (size_t)b0 * ctL, ctL, B, L, db->Sp + (size_t)b0 * ct1, ct1, db->tmp, db->tmp2)))
-      return s;
+  if ((s = mac_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js, db->tiled, (int)db->tile_jt))) return s;
+  cudaEventRecord(E[2], sa);
+  HD_CUDA(cudaEventRecord(db->ev_mac, sa));
+  // ---------------- stream B ----------------
+  HD_CUDA(cudaStreamWaitEvent(sb, db->ev_mac, 0));
+  c->stream = sb;
+  cudaEventRecord(E[3], sb);
+  {
+    // ---- rescale every S_{a,j} ----
+    const uint32_t total = A * nj;
+    for (uint32_t b0 = 0; b0 < total; b0 += db->rescale_chunk) {
+      uint32_t B = std::min(db->rescale_chunk, total - b0);
+      if ((s = ks_rescale(c, Sbuf + (size_t)b0 * ctL, ctL, B, L, db->Sp + (size_t)b0 * ct1, ct1, db->tmp, db->tmp2)))
+        return s;
+    }
   }
-  cudaEventRecord(E[3], c->stream);
+  HD_CUDA(cudaEventRecord(db->ev_sfree[par], sb));
+  cudaEventRecord(E[4], sb);
+  if ((s = giant_and_fold(db, E))) return s;
+  // outputs may still be read by caller-stream work enqueued before this call
+  HD_CUDA(cudaStreamWaitEvent(sb, db->ev_in, 0));
+  for (size_t i = 0; i < n_out; i++) {
+    HD_CUDA(cudaMemcpyAsync(out[i]->data, db->outbuf + i * ct1, ct1 * 8, cudaMemcpyDeviceToDevice, sb));
+    HD_CUDA(cudaEventRecord(out[i]->ready, sb));
+  }
+  HD_CUDA(cudaEventRecord(db->ev_done, sb));
+  HD_CUDA(cudaStreamWaitEvent(caller, db->ev_done, 0));
+  db->qcount++;
+  return HD_OK;
+}
+
+static hd_status giant_and_fold(hd_database *db, cudaEvent_t *E) {
+  hd_context *c = db->ctx;
+  const int n = c->n, L = c->L, n1 = (int)db->n1, nj = (int)db->js.size();
+  const uint32_t A = db->A_loc;
+  const size_t ct1 = (size_t)2 * (L - 1) * n;
+  hd_status s;
   // ---- giant rotations and sum (R2) ----
   HD_CUDA(cudaMemsetAsync(db->y, 0, (size_t)A * ct1 * 8, c->stream));
   const size_t sp_stride = (size_t)nj * ct1;  // between aggregates for fixed j
@@ -89,7 +137,7 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query) {
       return s;
     if ((s = ks_moddown(c, db->u, A, 1, L - 1, db->gal + slot, Sj, sp_stride, db->y, ct1, true, db->tmp))) return s;
   }
-  cudaEventRecord(E[4], c->stream);
+  cudaEventRecord(E[5], c->stream);
   // ---- fold: out = y + Rot_{numSlots - N}(y) ----
   {
     const size_t slot = (size_t)(n1 - 1) + nj;
@@ -100,7 +148,19 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query) {
       return s;
     if ((s = ks_moddown(c, db->u, A, 1, L - 1, db->gal + slot, db->y, ct1, db->outbuf, ct1, true, db->tmp))) return s;
   }
-  cudaEventRecord(E[5], c->stream);
+  cudaEventRecord(E[6], c->stream);
+  return HD_OK;
+}
+
+static hd_status ensure_streams(hd_context *c) {
+  // B (key switching, ALU-bound) gets the higher priority: its CTAs are dispatched ahead
+  // of the remaining CTAs of the HBM-bound MAC grid running on A.
+  int lo = 0, hi = 0;
+  HD_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  const char *pr = getenv("HD_PRIO");
+  const bool prio = !(pr && pr[0] == '0');
+  if (!c->sA) HD_CUDA(cudaStreamCreateWithPriority(&c->sA, cudaStreamNonBlocking, lo));
+  if (!c->sB) HD_CUDA(cudaStreamCreateWithPriority(&c->sB, cudaStreamNonBlocking, prio ? hi : lo));
   return HD_OK;
 }
 
@@ -119,7 +179,9 @@ extern "C" hd_status hd_query(hd_context *c, const hd_eval_keys *evk, const hd_d
     if (out[i] && (out[i]->ctx != c || out[i]->limbs != (uint32_t)(L - 1)))
       return hd_fail(HD_E_LEVEL, "reused output ciphertext has the wrong shape");
   }
+  (void)ct1;
   std::vector<hd_ciphertext *> fresh;
+  std::vector<hd_ciphertext *> outs(out, out + n_out);
   for (size_t i = 0; i < n_out; i++)
     if (!out[i]) {
       hd_ciphertext *ct;
@@ -128,20 +190,26 @@ extern "C" hd_status hd_query(hd_context *c, const hd_eval_keys *evk, const hd_d
         return s;
       }
       fresh.push_back(ct);
+      outs[i] = ct;
     }
-  if ((s = run_scan(db, query))) {
+  const char *serial = getenv("HD_SERIAL");
+  cudaStream_t sa = c->stream, sb = c->stream;
+  if (!(serial && serial[0] == '1')) {
+    if ((s = ensure_streams(c))) return s;
+    sa = c->sA;
+    sb = c->sB;
+  }
+  cudaStream_t caller = c->stream;
+  s = run_scan(db, query, sa, sb, outs.data(), n_out);
+  c->stream = caller;
+  if (s) {
     for (auto *f : fresh) hd_ciphertext_destroy(f);
     return s;
   }
-  size_t fi = 0;
-  for (size_t i = 0; i < n_out; i++) {
-    if (!out[i]) out[i] = fresh[fi++];
-    HD_CUDA(cudaMemcpyAsync(out[i]->data, db->outbuf + i * ct1, ct1 * 8, cudaMemcpyDeviceToDevice, c->stream));
-  }
+  for (size_t i = 0; i < n_out; i++) out[i] = outs[i];
   HD_CUDA(cudaGetLastError());
   db->has_run = true;
   // per-phase times are read lazily by hd_query_stats (no sync here)
-
   return HD_OK;
 }
 
@@ -150,14 +218,16 @@ extern "C" hd_status hd_query_stats(const hd_context *cc, double *phase_ms, size
   hd_context *c = const_cast<hd_context *>(cc);
   // average over the queries issued since the previous call (up to the last 64)
   if (c->ev_pending > 0) {
+    // events: 0 A start, 1 baby done, 2 MAC done (A), 3 B start, 4 rescale, 5 giant, 6 fold (B)
+    static const int from[5] = {0, 1, 3, 4, 5}, to[5] = {1, 2, 4, 5, 6};
     double acc[5] = {0, 0, 0, 0, 0};
     const int last = (c->ev_next - 1) % 64;
-    HD_CUDA(cudaEventSynchronize(c->ev[last][5]));
+    HD_CUDA(cudaEventSynchronize(c->ev[last][6]));
     for (int q = 0; q < c->ev_pending; q++) {
       const int idx = ((c->ev_next - 1 - q) % 64 + 64) % 64;
       for (int i = 0; i < 5; i++) {
         float ms = 0;
-        HD_CUDA(cudaEventElapsedTime(&ms, c->ev[idx][i], c->ev[idx][i + 1]));
+        HD_CUDA(cudaEventElapsedTime(&ms, c->ev[idx][from[i]], c->ev[idx][to[i]]));
         acc[i] += ms;
       }
     }
@@ -186,7 +256,7 @@ extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t ag
       break;
     case 1:
       if (jj < 0 || jj >= nj) return hd_fail(HD_E_INVALID_ARG, "giant index");
-      src = db->S + (a * nj + jj) * ctL, len = ctL;
+      src = (((db->qcount - 1) & 1) ? db->S2 : db->S) + (a * nj + jj) * ctL, len = ctL;
       break;
     case 2:
       if (jj < 0 || jj >= nj) return hd_fail(HD_E_INVALID_ARG, "giant index");
@@ -205,6 +275,19 @@ extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t ag
   if (which < 4 && !db->has_run) return hd_fail(HD_E_STATE, "no query has run on this database");
   if (cap < len) return hd_fail(HD_E_INVALID_ARG, "capacity too small");
   HD_CUDA(cudaStreamSynchronize(c->stream));
+  if (which == 4 && db->tiled) {  // undo the MAC tiling of this aggregate for the export
+    uint64_t *tmp = nullptr;
+    HD_CUDA(cudaMalloc(&tmp, len * 8));
+    hd_context *cc = const_cast<hd_context *>(c);
+    hd_status s = mac_untile_diagonal(cc, db->D + a * db->N * ptL, tmp, (int)db->N, (int)db->n1, db->js.front(),
+                                      (int)db->js.size(), (int)db->tile_jt, index);
+    cudaError_t e = cudaStreamSynchronize(c->stream);
+    if (!s && e == cudaSuccess) e = cudaMemcpy(host_dst, tmp, len * 8, cudaMemcpyDeviceToHost);
+    cudaFree(tmp);
+    if (s) return s;
+    HD_CUDA(e);
+    return HD_OK;
+  }
   HD_CUDA(cudaMemcpy(host_dst, src, len * 8, cudaMemcpyDeviceToHost));
   return HD_OK;
 }
@@ -243,6 +326,7 @@ extern "C" hd_status hd_test_rotate(hd_context *c, const hd_eval_keys *evk, cons
     hd_ciphertext_destroy(o);
     return s;
   }
+  cudaEventRecord(o->ready, c->stream);
   *out = o;
   return HD_OK;
 }
@@ -266,6 +350,7 @@ extern "C" hd_status hd_test_rescale(hd_context *c, const hd_ciphertext *ct, hd_
     hd_ciphertext_destroy(o);
     return s;
   }
+  cudaEventRecord(o->ready, c->stream);
   *out = o;
   return HD_OK;
 }

@@ -51,14 +51,19 @@ class Config:
         return DATA_SEED_BASE + self.index
 
 
-# BASELINE.json "configs" (C1..C5); n1 for C4 chosen from the C5 sweep (R22).
+# BASELINE.json "configs" (C1..C5); n1 = 128 for C4 chosen from the n1 sweep at 2^20 (R22).
 CONFIGS = {
     "C1": Config("C1-toy", 12, 64, 256, 8, index=1),
     "C2": Config("C2", 15, 512, 1 << 14, 16, index=2),
     "C3": Config("C3", 15, 512, 1 << 17, 16, index=3),
-    "C4": Config("C4", 16, 512, 1 << 20, 64, index=4),
+    "C4": Config("C4", 16, 512, 1 << 20, 128, index=4),
+    "C4n64": Config("C4-n64", 16, 512, 1 << 20, 64, index=4),
     "C4n16": Config("C4-n16", 16, 512, 1 << 20, 16, index=4),
     "C4n32": Config("C4-n32", 16, 512, 1 << 20, 32, index=4),
+    "C4n128": Config("C4-n128", 16, 512, 1 << 20, 128, index=4),
+    "C2n128": Config("C2-n128", 15, 512, 1 << 14, 128, index=2),
+    "C4n256": Config("C4-n256", 16, 512, 1 << 20, 256, index=4),
+    "C2n256": Config("C2-n256", 15, 512, 1 << 14, 256, index=2),
 }
 for _n1 in (4, 8, 16, 32, 64):
     CONFIGS[f"C5n{_n1}"] = Config(f"C5-n1={_n1}", 15, 512, 1 << 17, _n1, index=5)

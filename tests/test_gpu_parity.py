@@ -177,6 +177,22 @@ def test_c2_all_aggregates_bit_exact():
     assert sorted(np.argsort(-sc)[:3]) == sorted(run.pos.tolist())
 
 
+@pytest.mark.parametrize("name", ["C2n128", "C2n256"])
+def test_large_n1_bit_exact(name):
+    """n1 = 128 / 256 (4 / 2 giant steps): the MAC's carry-save accumulators run at their
+    maximum depth and are banked every 128 terms; every output bit-exact vs the oracle."""
+    run = Run(CONFIGS[name])
+    o, cfg = run.o, run.cfg
+    s_ntt, steps, keys = run.oracle_keys()
+    r = o.baby_steps(run.oracle_query_ct(), cfg.n1, steps, keys)
+    for a in range(cfg.aggregates):
+        D = run.oracle_D(a)
+        out = o.scan_aggregate(r, cfg.n1, cfg.dim, D, steps, keys)
+        assert (run.ctx.ciphertext_residues(run.outs[a]) == out).all(), a
+    sc = run.ctx.decrypt_scores(run.sk, run.db.layout, run.outs)
+    assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-6
+
+
 @pytest.mark.slow
 def test_c4_bench_config_sampled_aggregate():
     """The bench launch configuration (2^16 ring, 2^20 x 512, n1 = 64, all 64 aggregates
