@@ -323,8 +323,10 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
   // MAC-tiled diagonal layout (mac.cu): needs every giant step to use all n1 baby steps
   const int nj_ = (int)db->js.size();
   db->tile_jt = nj_ % 2 == 0 ? 2 : 1;
-  const char *no_tile = getenv("HD_NO_TILE");
-  db->tiled = (N / 2) % (int)n1 == 0 && n % 128 == 0 && !(no_tile && no_tile[0] == '1');
+  // opt-in (HD_TILE=1): on B200 the plain [k][limb][coef] layout with the carry-save
+  // kernel streams faster (tools/mac_sweep.py: 11.1 ms vs 12.5 ms at 2^20 x 512)
+  const char *tile = getenv("HD_TILE");
+  db->tiled = (N / 2) % (int)n1 == 0 && n % 128 == 0 && (tile && tile[0] == '1');
   uint64_t *Dtmp = nullptr;
   if (!e && db->tiled) e = cudaMalloc(&Dtmp, (size_t)N * L * n * 8);
   if (e) {

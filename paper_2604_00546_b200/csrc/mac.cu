@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(MAC_TPB) mac_cs_kernel(const uint64_t *__restr
 }
 // ---- carry-save, software-pipelined loads: the JT loads of baby step i+1 are issued
 // before the arithmetic of step i (2 JT loads in flight per thread), running pointers. --
-template <int JT>
+template <int JT, bool FLUSH = false>
 __global__ void __launch_bounds__(MAC_TPB) mac_cs2_kernel(const uint64_t *__restrict__ D,
                                                           const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
                                                           int n1, int N, int L, int logn, int jmin, int nj,
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(MAC_TPB) mac_cs2_kernel(const uint64_t *__rest
         cs_fold(acc[jj][1]);
       }
     }
-    if ((i & 127) == 127 && more) {  // n1 > 128: bank the carry-save sums every 128 terms
+    if (FLUSH && (i & 127) == 127 && more) {  // n1 > 128: bank the carry-save sums every 128 terms
 #pragma unroll
       for (int jj = 0; jj < JT; jj++)
 #pragma unroll
@@ -895,7 +895,7 @@ __device__ __forceinline__ void mac_step(CsAcc (&acc)[JT][2], const uint64_t (&d
   }
 }
 
-template <int JT>
+template <int JT, bool FLUSH = false>
 __global__ void __launch_bounds__(TILE) mac_tiled2_kernel(const uint64_t *__restrict__ D,
                                                           const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
                                                           int n1, int N, int L, int logn, int nj, ModTab mt) {
@@ -943,7 +943,7 @@ __global__ void __launch_bounds__(TILE) mac_tiled2_kernel(const uint64_t *__rest
         cs_fold(acc[jj][1]);
       }
     }
-    if ((i & 127) == 126 && i + 2 < n1) {
+    if (FLUSH && (i & 127) == 126 && i + 2 < n1) {
 #pragma unroll
       for (int jj = 0; jj < JT; jj++)
 #pragma unroll
@@ -1033,10 +1033,15 @@ hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t 
     const int PD = pd ? atoi(pd) : 0;
     dim3 grid(A_loc, c->n / TILE, c->L * (nj / tile_jt));
     if (n1 % 2 == 0 && PD == 0) {  // default: ping-pong pairs
-      if (tile_jt == 2)
-        mac_tiled2_kernel<2><<<grid, TILE, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, nj, c->mt);
+      const bool fl = n1 > 128;
+      if (tile_jt == 2 && !fl)
+        mac_tiled2_kernel<2, false><<<grid, TILE, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, nj, c->mt);
+      else if (tile_jt == 2)
+        mac_tiled2_kernel<2, true><<<grid, TILE, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, nj, c->mt);
+      else if (!fl)
+        mac_tiled2_kernel<1, false><<<grid, TILE, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, nj, c->mt);
       else
-        mac_tiled2_kernel<1><<<grid, TILE, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, nj, c->mt);
+        mac_tiled2_kernel<1, true><<<grid, TILE, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, nj, c->mt);
     } else if (tile_jt == 2) {
       if (PD >= 4) mac_tiled_kernel<2, 4><<<grid, TILE, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, nj, c->mt);
       else if (PD >= 2) mac_tiled_kernel<2, 2><<<grid, TILE, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, nj, c->mt);
@@ -1071,7 +1076,10 @@ hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t 
     else mac_cs4_kernel<1><<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
   } else if (full && small_q && v == '3' && nj % 2 == 0) {  // default (any n1: banked every 128 terms)
     dim3 g2(A_loc, c->n / MAC_TPB, c->L * (nj / 2));
-    mac_cs2_kernel<2><<<g2, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+    if (n1 > 128)
+      mac_cs2_kernel<2, true><<<g2, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+    else
+      mac_cs2_kernel<2, false><<<g2, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
   } else if (use_cs && (v == '2' || v == '3')) {
     dim3 grid(A_loc, c->n / MAC_TPB, c->L * (nj / 4));
     if (v == '2') mac_cs2_kernel<4><<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);

@@ -186,7 +186,7 @@ __device__ __forceinline__ void cols_rec(uint64_t (&v)[E], const ColArgs &A) {
 
 // ---- columns kernel: the S high stages; tpc columns per CTA, 2^(S-4) threads per column ----
 template <bool INV, int S>
-__global__ void __launch_bounds__(256) ntt_cols_kernel(uint64_t *base, RowMap rm, ModTab mt,
+__global__ void __launch_bounds__(256, 3) ntt_cols_kernel(uint64_t *base, RowMap rm, ModTab mt,
                                                        const ulonglong2 *__restrict__ tw, int logn, int tpc,
                                                        const uint64_t *__restrict__ ninv, uint32_t r0, bool final_out,
                                                        NttSrc src) {
@@ -234,7 +234,7 @@ __device__ __forceinline__ void chunks_rec(uint64_t (&v)[E], uint32_t tid, uint6
 
 // ---- chunks kernel: the S low stages on contiguous chunks of 2^S; tpc chunks per CTA ----
 template <bool INV, int S>
-__global__ void __launch_bounds__(256) ntt_chunks_kernel(uint64_t *base, RowMap rm, ModTab mt,
+__global__ void __launch_bounds__(256, 3) ntt_chunks_kernel(uint64_t *base, RowMap rm, ModTab mt,
                                                          const ulonglong2 *__restrict__ tw, int logn, int tpc,
                                                          const uint64_t *__restrict__ ninv, uint32_t r0, bool final_out,
                                                          NttSrc src, NttEpi epi) {

@@ -193,6 +193,46 @@ def test_large_n1_bit_exact(name):
     assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-6
 
 
+@pytest.mark.parametrize("name", ["C1", "C2n256"])
+def test_tiled_layout_bit_exact(name, monkeypatch):
+    """The optional MAC-tiled diagonal layout (HD_TILE=1) gives the same bits: the
+    exported diagonals are un-tiled on the device and the outputs equal the oracle's."""
+    monkeypatch.setenv("HD_TILE", "1")
+    run = Run(CONFIGS[name])
+    o, cfg = run.o, run.cfg
+    s_ntt, steps, keys = run.oracle_keys()
+    r = o.baby_steps(run.oracle_query_ct(), cfg.n1, steps, keys)
+    a = cfg.aggregates - 1
+    D = run.oracle_D(a)
+    for k in (0, 1, cfg.dim // 2, cfg.dim - 1):
+        assert (run.ctx.test_stage(run.db, 4, a, k) == D[k]).all(), k
+    out = o.scan_aggregate(r, cfg.n1, cfg.dim, D, steps, keys)
+    assert (run.ctx.ciphertext_residues(run.outs[a]) == out).all()
+
+
+def test_pipelined_queries_match_serial(monkeypatch):
+    """Back-to-back queries on the two-stream pipeline (S double-buffered, outputs reused
+    in place) give exactly the serial results, for alternating query ciphertexts."""
+    cfg = CONFIGS["C1"]
+    run = Run(cfg)
+    q2 = run.ctx.encrypt_query(run.sk, run.q[::-1].copy(), ENC_SEED_BASE + 1)
+    monkeypatch.setenv("HD_SERIAL", "1")
+    ref1 = [run.ctx.ciphertext_residues(o) for o in run.ctx.query(run.evk, run.db, run.qct)]
+    ref2 = [run.ctx.ciphertext_residues(o) for o in run.ctx.query(run.evk, run.db, q2)]
+    monkeypatch.setenv("HD_SERIAL", "0")
+    # six queries enqueued back to back (no host sync in between), fresh outputs each
+    results = [run.ctx.query(run.evk, run.db, run.qct if it % 2 == 0 else q2) for it in range(6)]
+    for it, outs in enumerate(results):
+        want = ref1 if it % 2 == 0 else ref2
+        got = [run.ctx.ciphertext_residues(o) for o in outs]
+        assert all((g == w).all() for g, w in zip(got, want)), it
+    # and in place: the same output handles reused by consecutive queries
+    outs = None
+    for it in range(4):
+        outs = run.ctx.query(run.evk, run.db, run.qct if it % 2 == 0 else q2, outs)
+    assert all((run.ctx.ciphertext_residues(o) == w).all() for o, w in zip(outs, ref2))
+
+
 @pytest.mark.slow
 def test_c4_bench_config_sampled_aggregate():
     """The bench launch configuration (2^16 ring, 2^20 x 512, n1 = 64, all 64 aggregates
