@@ -65,15 +65,23 @@ struct TwGlobal {
     return __ldg(&T[((size_t)blk << k) + local]);
   }
 };
+// Column twiddles (b0 = 1, one transform per table): level k lives at (2^k - 1) + local
+// and comes from T[2^k + local], i.e. the staged table is T[1 .. 2^S - 1] copied flat
+// (all loads issued before any store: one global latency, not S).
 template <int S>
-__device__ __forceinline__ void stage_twiddles(ulonglong2 *dst, const ulonglong2 *__restrict__ T, uint32_t b0,
-                                               uint32_t tpc) {
-#pragma unroll 1
-  for (int k = 0; k < S; k++) {
-    const uint32_t cnt = tpc << k;
-    const ulonglong2 *src = T + ((size_t)b0 << k);
-    ulonglong2 *d = dst + tpc * ((1u << k) - 1);
-    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) d[i] = __ldg(src + i);
+__device__ __forceinline__ void stage_twiddles(ulonglong2 *dst, const ulonglong2 *__restrict__ T) {
+  constexpr uint32_t CNT = (1u << S) - 1;
+  constexpr int PER = (CNT + 127) / 128;  // blockDim.x >= 128 for S <= 8
+  ulonglong2 t[PER];
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    const uint32_t i = threadIdx.x + k * blockDim.x;
+    if (i < CNT) t[k] = __ldg(T + 1 + i);
+  }
+#pragma unroll
+  for (int k = 0; k < PER; k++) {
+    const uint32_t i = threadIdx.x + k * blockDim.x;
+    if (i < CNT) dst[i] = t[k];
   }
 }
 
@@ -206,7 +214,7 @@ __global__ void __launch_bounds__(256, 3) ntt_cols_kernel(uint64_t *base, RowMap
   A.smt = sm + tr * col_stride;
   // every column of the row uses the same twiddles T[1 .. 2^S - 1]
   ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(sm + ((tpc * col_stride + 1) & ~1u));
-  stage_twiddles<S>(tws, tw + (size_t)m * n, 1u, 1u);
+  stage_twiddles<S>(tws, tw + (size_t)m * n);
   A.tw.sm = tws;
   A.tw.tr = 0;
   A.tw.tpc = 1;
@@ -249,28 +257,33 @@ __global__ void __launch_bounds__(256, 3) ntt_chunks_kernel(uint64_t *base, RowM
   uint64_t *a = row_ptr(base, rm, row, n) + off0;
   const InRow in = in_row(base, rm, src, row, n, m, mt);
   const uint32_t tr = threadIdx.x / TPT, tid = threadIdx.x % TPT;
-  const uint32_t total = tpc * SZ;
   // twiddles of this chunk: transform block index 2^s1 + chunk0 + tr at every level
   // (each chunk uses its own 2^S - 1 entries: read from L1/L2, not staged)
   TwGlobal twv;
   twv.T = tw + (size_t)m * n;
   twv.blk = (1u << s1) + chunk0 + tr;
-  for (uint32_t i = threadIdx.x * 2; i < total; i += blockDim.x * 2) {
-    uint64_t w0, w1;
-    if (!in.lift) {
-      const ulonglong2 w = *reinterpret_cast<const ulonglong2 *>(in.p + off0 + i);
-      w0 = w.x;
-      w1 = w.y;
-    } else {
-      w0 = in.ld(off0 + i);
-      w1 = in.ld(off0 + i + 1);
+  // blockDim.x * E == total: every thread moves exactly E elements (E/2 128-bit words);
+  // all loads are issued before the first shared-memory store.
+  uint64_t v[E];
+  {
+    ulonglong2 w[E / 2];
+#pragma unroll
+    for (int k = 0; k < E / 2; k++)
+      w[k] = *reinterpret_cast<const ulonglong2 *>(in.p + off0 + 2 * (threadIdx.x + k * blockDim.x));
+#pragma unroll
+    for (int k = 0; k < E / 2; k++) {
+      const uint32_t i = 2 * (threadIdx.x + k * blockDim.x);
+      uint64_t w0 = w[k].x, w1 = w[k].y;
+      if (in.lift) {
+        w0 = lift_centred(w0, in.qs, in.q, in.bar);
+        w1 = lift_centred(w1, in.qs, in.q, in.bar);
+      }
+      const uint32_t t0 = i >> S, x0 = i & (SZ - 1);
+      sm[t0 * PS + pad_idx(x0)] = w0;
+      sm[t0 * PS + pad_idx(x0 + 1)] = w1;
     }
-    const uint32_t t0 = i >> S, x0 = i & (SZ - 1);
-    sm[t0 * PS + pad_idx(x0)] = w0;
-    sm[t0 * PS + pad_idx(x0 + 1)] = w1;
   }
   __syncthreads();
-  uint64_t v[E];
   chunks_rec<INV, S, 0>(v, tid, sm + tr * PS, twv, q);
   const bool scale = INV && s1 == 0;
   const bool fin = !INV && final_out;
@@ -287,7 +300,49 @@ __global__ void __launch_bounds__(256, 3) ntt_chunks_kernel(uint64_t *base, RowM
       g = epi.gal[x % epi.K];
     }
   }
-  for (uint32_t i = threadIdx.x * 2; i < total; i += blockDim.x * 2) {
+  if (fin && epi.mode) {
+    // combine epilogue, in batches of H 128-bit words: the batch's global operands
+    // (A, the Galois-gathered c0, the accumulator) are all loaded before use.
+    constexpr int H = E / 4;
+    const uint64_t w = epi.w[m], ws = epi.ws[m];
+#pragma unroll
+    for (int b = 0; b < E / 2; b += H) {
+      ulonglong2 av[H], cv[H], dv[H];
+#pragma unroll
+      for (int k = 0; k < H; k++) {
+        const uint32_t i = 2 * (threadIdx.x + (b + k) * blockDim.x);
+        av[k] = *reinterpret_cast<const ulonglong2 *>(Arow + i);
+        if (c0row) {
+          const uint32_t gi = (uint32_t)(off0 + i);
+          cv[k].x = c0row[galois_src(gi, g, logn)];
+          cv[k].y = c0row[galois_src(gi + 1, g, logn)];
+        }
+        if (epi.acc) dv[k] = *reinterpret_cast<const ulonglong2 *>(dst + i);
+      }
+#pragma unroll
+      for (int k = 0; k < H; k++) {
+        const uint32_t i = 2 * (threadIdx.x + (b + k) * blockDim.x);
+        const uint32_t t0 = i >> S, x0 = i & (SZ - 1);
+        uint64_t o0 = final_reduce(sm[t0 * PS + pad_idx(x0)], q);
+        uint64_t o1 = final_reduce(sm[t0 * PS + pad_idx(x0 + 1)], q);
+        o0 = shoup(submod(av[k].x, o0, q), w, ws, q);
+        o1 = shoup(submod(av[k].y, o1, q), w, ws, q);
+        if (c0row) {
+          o0 = addmod(o0, cv[k].x, q);
+          o1 = addmod(o1, cv[k].y, q);
+        }
+        if (epi.acc) {
+          o0 = addmod(o0, dv[k].x, q);
+          o1 = addmod(o1, dv[k].y, q);
+        }
+        *reinterpret_cast<ulonglong2 *>(dst + i) = make_ulonglong2(o0, o1);
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < E / 2; k++) {
+    const uint32_t i = 2 * (threadIdx.x + k * blockDim.x);
     const uint32_t t0 = i >> S, x0 = i & (SZ - 1);
     uint64_t o0 = sm[t0 * PS + pad_idx(x0)], o1 = sm[t0 * PS + pad_idx(x0 + 1)];
     if (scale) {
@@ -296,21 +351,6 @@ __global__ void __launch_bounds__(256, 3) ntt_chunks_kernel(uint64_t *base, RowM
     } else if (fin) {
       o0 = final_reduce(o0, q);
       o1 = final_reduce(o1, q);
-      if (epi.mode) {
-        const ulonglong2 av = *reinterpret_cast<const ulonglong2 *>(Arow + i);
-        o0 = shoup(submod(av.x, o0, q), epi.w[m], epi.ws[m], q);
-        o1 = shoup(submod(av.y, o1, q), epi.w[m], epi.ws[m], q);
-        if (c0row) {
-          const uint32_t gi = (uint32_t)(off0 + i);
-          o0 = addmod(o0, c0row[galois_src(gi, g, logn)], q);
-          o1 = addmod(o1, c0row[galois_src(gi + 1, g, logn)], q);
-        }
-        if (epi.acc) {
-          const ulonglong2 dv = *reinterpret_cast<const ulonglong2 *>(dst + i);
-          o0 = addmod(o0, dv.x, q);
-          o1 = addmod(o1, dv.y, q);
-        }
-      }
     }
     *reinterpret_cast<ulonglong2 *>(dst + i) = make_ulonglong2(o0, o1);
   }
