@@ -175,11 +175,7 @@ struct hd_database {
   uint32_t N, M, n1, A_loc;
   std::vector<int32_t> js;       // giant steps j (contiguous, non-empty ranges)
   std::vector<int32_t> pre;      // preRot(j) per j
-  uint64_t *D = nullptr;         // [A_loc][N][L][n] diagonal plaintexts (or MAC-tiled, below)
-  // tiled: per aggregate [limb][tile of 128 coefs][giant group][baby i][jj < tile_jt][128]
-  // so every MAC CTA streams one contiguous n1 * tile_jt KiB block (mac.cu)
-  bool tiled = false;
-  uint32_t tile_jt = 2;
+  uint64_t *D = nullptr;         // [A_loc][N][L][n] diagonal plaintexts
   // query workspaces (allocated at enrollment; reused by every hd_query)
   uint64_t *r = nullptr;         // [n1][2][L][n] baby steps
   uint64_t *S = nullptr;         // [A_loc][nj][2][L][n] giant-step sums

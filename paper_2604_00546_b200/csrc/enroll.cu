@@ -320,18 +320,8 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
     cudaFree(re);
     cudaFree(im);
   };
-  // MAC-tiled diagonal layout (mac.cu): needs every giant step to use all n1 baby steps
-  const int nj_ = (int)db->js.size();
-  db->tile_jt = nj_ % 2 == 0 ? 2 : 1;
-  // opt-in (HD_TILE=1): on B200 the plain [k][limb][coef] layout with the carry-save
-  // kernel streams faster (tools/mac_sweep.py: 11.1 ms vs 12.5 ms at 2^20 x 512)
-  const char *tile = getenv("HD_TILE");
-  db->tiled = (N / 2) % (int)n1 == 0 && n % 128 == 0 && (tile && tile[0] == '1');
-  uint64_t *Dtmp = nullptr;
-  if (!e && db->tiled) e = cudaMalloc(&Dtmp, (size_t)N * L * n * 8);
   if (e) {
     cleanup();
-    cudaFree(Dtmp);
     hd_database_destroy(db);
     return hd_fail(HD_E_CAPACITY, "enrollment scratch");
   }
@@ -347,19 +337,15 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
     }
     if ((s = normalize_on_device(c, dv, rows, N, U))) break;
     if ((s = check_flag(c))) break;
-    uint64_t *Dfinal = db->D + (size_t)(a - agg_begin) * N * L * n;
-    uint64_t *Da = db->tiled ? Dtmp : Dfinal;
+    uint64_t *Da = db->D + (size_t)(a - agg_begin) * N * L * n;
     for (int k0 = 0; k0 < N && !s; k0 += KB) {
       int kb = std::min(KB, N - k0);
       pack_kernel<<<dim3((ns + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(U, (long long)v0, (long long)num_vectors, N,
                                                                          db->M, n1, a, k0, ns, re, im); ++c->launches;
       s = encode_batch(c, re, im, kb, delta, L, Da + (size_t)k0 * L * n, (size_t)L * n);
     }
-    if (!s && db->tiled) s = mac_tile_aggregate(c, Dtmp, Dfinal, N, (int)n1, db->js.front(), (int)db->js.size(),
-                                                (int)db->tile_jt);
     if (!s) s = check_flag(c);
   }
-  cudaFree(Dtmp);
   cleanup();
   if (s) {
     hd_database_destroy(db);

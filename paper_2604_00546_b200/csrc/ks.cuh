@@ -27,12 +27,7 @@ struct MacPlan {
   const int32_t *js;   // host
 };
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
-                  const std::vector<int32_t> &js, bool tiled, int tile_jt);
-// Reorder one aggregate's diagonals [k][limb][coef] into the MAC-tiled layout.
-hd_status mac_tile_aggregate(hd_context *c, const uint64_t *src, uint64_t *dst, int N, int n1, int jmin, int nj, int JT);
-// Inverse of the tiling for one diagonal k (test export): dst = [limb][coef].
-hd_status mac_untile_diagonal(hd_context *c, const uint64_t *src, uint64_t *dst, int N, int n1, int jmin, int nj, int JT,
-                              int k);
+                  const std::vector<int32_t> &js);
 
 // encode (enroll.cu)
 hd_status encode_batch(hd_context *c, double *re, double *im, uint32_t B, double delta, int nlimbs,

@@ -84,7 +84,7 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
   }
   cudaEventRecord(E[1], sa);
   // ---- MAC ----
-  if ((s = mac_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js, db->tiled, (int)db->tile_jt))) return s;
+  if ((s = mac_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js))) return s;
   cudaEventRecord(E[2], sa);
   HD_CUDA(cudaEventRecord(db->ev_mac, sa));
   // ---------------- stream B ----------------
@@ -275,19 +275,6 @@ extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t ag
   if (which < 4 && !db->has_run) return hd_fail(HD_E_STATE, "no query has run on this database");
   if (cap < len) return hd_fail(HD_E_INVALID_ARG, "capacity too small");
   HD_CUDA(cudaStreamSynchronize(c->stream));
-  if (which == 4 && db->tiled) {  // undo the MAC tiling of this aggregate for the export
-    uint64_t *tmp = nullptr;
-    HD_CUDA(cudaMalloc(&tmp, len * 8));
-    hd_context *cc = const_cast<hd_context *>(c);
-    hd_status s = mac_untile_diagonal(cc, db->D + a * db->N * ptL, tmp, (int)db->N, (int)db->n1, db->js.front(),
-                                      (int)db->js.size(), (int)db->tile_jt, index);
-    cudaError_t e = cudaStreamSynchronize(c->stream);
-    if (!s && e == cudaSuccess) e = cudaMemcpy(host_dst, tmp, len * 8, cudaMemcpyDeviceToHost);
-    cudaFree(tmp);
-    if (s) return s;
-    HD_CUDA(e);
-    return HD_OK;
-  }
   HD_CUDA(cudaMemcpy(host_dst, src, len * 8, cudaMemcpyDeviceToHost));
   return HD_OK;
 }
