@@ -259,10 +259,14 @@ class Oracle:
         _check("giant_sum", rc)
         return S
 
-    def scan_aggregate(self, r, n1, N, Dagg, steps, keys, want_y=False):
+    def scan_aggregate(self, r, n1, N, Dagg, steps, keys, want_y=False, hoisted=True):
+        """One aggregate's output ciphertext.  hoisted=True (the CUDA path's schedule,
+        R23): giant-step rotations accumulated in Q u {P}, one ModDown; False: one
+        ModDown per rotation (the textbook rotation of Alg. sender-bsgs)."""
         out = u64((2, self.L - 1, self.n))
         y = u64((2, self.L - 1, self.n))
-        _check("scan_aggregate", lib().or_scan_aggregate(
+        fn = lib().or_scan_aggregate_hoisted if hoisted else lib().or_scan_aggregate
+        _check("scan_aggregate", fn(
             C.byref(self.p), _p(np.ascontiguousarray(r)), n1, N, _p(np.ascontiguousarray(Dagg)),
             _p(steps), len(steps), _p(keys), _p(out), _p(y)))
         return (out, y) if want_y else out

@@ -627,12 +627,11 @@ static void moddown(const or_params *p, uint64_t *u /* (ell+1) x n */, int ell, 
 
 /* "EvalFastRotation": permute digits by pi_g in the NTT domain, key
  * inner product over Q_ell u {P}, ModDown, add pi_g(c0). */
-int or_rotate_hoisted(const or_params *p, const uint64_t *ct, const uint64_t *dig, int32_t ell,
-                      const uint64_t *key, int64_t step, uint64_t *out) {
+/* Key inner product in the extended basis: u[pp][e] += sum_d pi_g(dig_d)[e] * key[d][pp][e]
+ * (u: 2 x (ell+1) x n, accumulated, so several rotations can share one ModDown). */
+static void kip_accumulate(const or_params *p, const uint64_t *dig, int32_t ell, const uint64_t *key,
+                           uint64_t g, uint64_t *u) {
   int n = p->n, L = p->L;
-  if (ell < 1 || ell > L) return OR_E_ARG;
-  uint64_t g = or_galois_elt(p, step);
-  uint64_t *u = calloc((size_t)2 * (ell + 1) * n, sizeof(uint64_t));
   uint64_t *perm = malloc(sizeof(uint64_t) * n);
   for (int d = 0; d < ell; d++) {
     for (int e = 0; e <= ell; e++) {
@@ -646,6 +645,17 @@ int or_rotate_hoisted(const or_params *p, const uint64_t *ct, const uint64_t *di
       }
     }
   }
+  free(perm);
+}
+
+int or_rotate_hoisted(const or_params *p, const uint64_t *ct, const uint64_t *dig, int32_t ell,
+                      const uint64_t *key, int64_t step, uint64_t *out) {
+  int n = p->n, L = p->L;
+  if (ell < 1 || ell > L) return OR_E_ARG;
+  uint64_t g = or_galois_elt(p, step);
+  uint64_t *u = calloc((size_t)2 * (ell + 1) * n, sizeof(uint64_t));
+  uint64_t *perm = malloc(sizeof(uint64_t) * n);
+  kip_accumulate(p, dig, ell, key, g, u);
   uint64_t *u0 = malloc(sizeof(uint64_t) * (size_t)ell * n), *u1 = malloc(sizeof(uint64_t) * (size_t)ell * n);
   moddown(p, u, ell, u0);
   moddown(p, u + (size_t)(ell + 1) * n, ell, u1);
@@ -946,6 +956,78 @@ int or_scan_aggregate(const or_params *p, const uint64_t *r, int32_t n1, int32_t
     }
   }
   free(S); free(Sp); free(T); free(y);
+  return rc;
+}
+
+/* One aggregate with the giant-step rotations accumulated in the extended basis
+ * Q_ell u {P} and ONE ModDown per aggregate (R23; "double hoisting",
+ * P:L498-506): with T_j = Rescale(S_j) and s_j = preRot(j),
+ *   y_ext = sum_{s_j = 0} P T_j  +  sum_{s_j != 0} ( KIP_{s_j}(pi_{s_j}(ModUp(T_j.c1)))
+ *                                                    + (P pi_{s_j}(T_j.c0), 0) ),
+ *   y = ModDown(y_ext),  out = y + Rot_{numSlots-N}(y)          (fold as in R2).
+ * Each term ModDown'ed alone is exactly the eager rotation (ModDown(P x + a) =
+ * x + ModDown(a)), so the sum differs from or_scan_aggregate only by the rounding of
+ * the single ModDown. */
+int or_scan_aggregate_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
+                              const uint64_t *Dagg, const int32_t *steps, int32_t nkeys,
+                              const uint64_t *keys, uint64_t *out, uint64_t *y_out) {
+  int n = p->n, L = p->L, ell = L - 1;
+  size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * ell * n, ext = (size_t)(ell + 1) * n;
+  uint64_t P = p->mod[L];
+  uint64_t *S = malloc(sizeof(uint64_t) * ctL), *Sp = malloc(sizeof(uint64_t) * ct1);
+  uint64_t *T = malloc(sizeof(uint64_t) * ct1), *y = malloc(sizeof(uint64_t) * ct1);
+  uint64_t *yx = calloc(2 * ext, sizeof(uint64_t)); /* [pp][e][t], e == ell: P */
+  uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)ell * (ell + 1) * n);
+  uint64_t *perm = malloc(sizeof(uint64_t) * n);
+  int jmin, jmax, rc = OR_OK;
+  or_giant_range(N, n1, &jmin, &jmax);
+  for (int j = jmin; j <= jmax && rc == OR_OK; j++) {
+    if (or_giant_sum(p, r, n1, N, Dagg, j, S) != OR_OK) continue; /* empty range */
+    or_rescale(p, S, L, Sp);                                      /* Step 2c */
+    int s = or_pre_rot(N, n1, j);                                 /* Step 2d */
+    if (s == 0) { /* y_ext += P T_j (P limb += 0) */
+      for (int pp = 0; pp < 2; pp++)
+        for (int l = 0; l < ell; l++) {
+          uint64_t q = p->mod[l];
+          for (int t = 0; t < n; t++) {
+            size_t o = (size_t)pp * ext + (size_t)l * n + t;
+            yx[o] = addmod(yx[o], mulmod(P % q, Sp[((size_t)pp * ell + l) * n + t], q), q);
+          }
+        }
+      continue;
+    }
+    const uint64_t *key = find_key(p, steps, nkeys, keys, s);
+    if (!key) { rc = OR_E_MISSING_KEY; break; }
+    uint64_t g = or_galois_elt(p, s);
+    or_modup(p, Sp + (size_t)ell * n, ell, dig);
+    kip_accumulate(p, dig, ell, key, g, yx);
+    for (int l = 0; l < ell; l++) { /* + (P pi_g(T_j.c0), 0) */
+      uint64_t q = p->mod[l];
+      or_automorph_ntt(p, g, Sp + (size_t)l * n, perm);
+      for (int t = 0; t < n; t++) {
+        size_t o = (size_t)l * n + t;
+        yx[o] = addmod(yx[o], mulmod(P % q, perm[t], q), q);
+      }
+    }
+  }
+  if (rc == OR_OK) {
+    moddown(p, yx, ell, y);                      /* c0 */
+    moddown(p, yx + ext, ell, y + (size_t)ell * n); /* c1 */
+    int fold = p->num_slots - N;
+    const uint64_t *key = find_key(p, steps, nkeys, keys, fold);
+    if (!key) rc = OR_E_MISSING_KEY;
+    else {
+      or_rotate(p, y, ell, key, fold, T);
+      for (int pp = 0; pp < 2; pp++)
+        for (int l = 0; l < ell; l++)
+          for (int t = 0; t < n; t++) {
+            size_t o = ((size_t)pp * ell + l) * n + t;
+            out[o] = addmod(y[o], T[o], p->mod[l]);
+          }
+      if (y_out) memcpy(y_out, y, sizeof(uint64_t) * ct1);
+    }
+  }
+  free(S); free(Sp); free(T); free(y); free(yx); free(dig); free(perm);
   return rc;
 }
 

@@ -122,6 +122,12 @@ int or_scan_aggregate(const or_params *p, const uint64_t *r, int32_t n1, int32_t
                       const uint64_t *Dagg, const int32_t *steps, int32_t nkeys,
                       const uint64_t *keys, uint64_t *out /* ct(L-1) */,
                       uint64_t *y_out /* optional ct(L-1): sum before the fold */);
+/* Same result with the giant-step sum accumulated in Q u {P} and one ModDown (R23,
+ * P:L498-506); bits differ from or_scan_aggregate only by that ModDown's rounding.
+ * This is the schedule the CUDA path implements. */
+int or_scan_aggregate_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
+                              const uint64_t *Dagg, const int32_t *steps, int32_t nkeys,
+                              const uint64_t *keys, uint64_t *out, uint64_t *y_out);
 
 /* Decrypt + decode one output ciphertext and read the scores of its vectors (R4). */
 int or_decrypt_scores(const or_params *p, const uint64_t *s_ntt, const uint64_t *out_ct,

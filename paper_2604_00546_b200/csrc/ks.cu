@@ -18,10 +18,17 @@ constexpr int TPB = 256;
 // Key inner product; x = b * K + k.  Output u[x][p][e][t], e <= ell (e == ell: P).
 // Digit d in extended modulus e: e == d -> c1[b][d] itself (NTT form), else the
 // lifted digit dig[b][d][slot], slot = e < d ? e : e - 1.  Two coefficients per thread.
+// Extended-basis accumulation (R23): with acc.c0 set, u[x][p][e] += sum + (p == 0 &&
+// e < ell ? P pi_g(c0_b)[e] : 0), i.e. the rotation before its ModDown, added onto u.
+struct KipAcc {
+  const uint64_t *c0 = nullptr;  // c0 of ciphertext b at c0 + b * c0_stride ([ell][n])
+  size_t c0_stride = 0;
+  uint64_t pw[HD_MAXMOD] = {}, pws[HD_MAXMOD] = {};  // P mod q_e and its Shoup companion
+};
 __global__ void __launch_bounds__(TPB) kip_kernel(const uint64_t *__restrict__ dig, const uint64_t *__restrict__ c1,
                                                   size_t c1_stride, uint64_t *__restrict__ u, int ell, int K, int L,
                                                   int logn, const uint64_t *const *__restrict__ kptr,
-                                                  const uint32_t *__restrict__ gal, ModTab mt) {
+                                                  const uint32_t *__restrict__ gal, ModTab mt, KipAcc ka) {
   const int n = 1 << logn;
   const uint32_t t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
   const uint32_t xe = blockIdx.y;
@@ -47,10 +54,50 @@ __global__ void __launch_bounds__(TPB) kip_kernel(const uint64_t *__restrict__ d
     mac128(b1l, b1h, v1, k1.y);
   }
   const uint64_t q = mt.q[gm], bar = mt.bar[gm], r64 = mt.r64[gm], r64s = mt.r64s[gm];
-  *reinterpret_cast<ulonglong2 *>(u + ((size_t)(x * 2 + 0) * (ell + 1) + e) * n + t) =
-      make_ulonglong2(reduce128(a0h, a0l, q, bar, r64, r64s), reduce128(b0h, b0l, q, bar, r64, r64s));
-  *reinterpret_cast<ulonglong2 *>(u + ((size_t)(x * 2 + 1) * (ell + 1) + e) * n + t) =
-      make_ulonglong2(reduce128(a1h, a1l, q, bar, r64, r64s), reduce128(b1h, b1l, q, bar, r64, r64s));
+  ulonglong2 *o0 = reinterpret_cast<ulonglong2 *>(u + ((size_t)(x * 2 + 0) * (ell + 1) + e) * n + t);
+  ulonglong2 *o1 = reinterpret_cast<ulonglong2 *>(u + ((size_t)(x * 2 + 1) * (ell + 1) + e) * n + t);
+  ulonglong2 v0 = make_ulonglong2(reduce128(a0h, a0l, q, bar, r64, r64s), reduce128(b0h, b0l, q, bar, r64, r64s));
+  ulonglong2 v1 = make_ulonglong2(reduce128(a1h, a1l, q, bar, r64, r64s), reduce128(b1h, b1l, q, bar, r64, r64s));
+  if (ka.c0) {
+    const ulonglong2 p0 = *o0, p1 = *o1;
+    v0 = make_ulonglong2(addmod(v0.x, p0.x, q), addmod(v0.y, p0.y, q));
+    v1 = make_ulonglong2(addmod(v1.x, p1.x, q), addmod(v1.y, p1.y, q));
+    if ((int)e < ell) {
+      const uint64_t *c0r = ka.c0 + (size_t)b * ka.c0_stride + (size_t)e * n;
+      v0.x = addmod(v0.x, shoup(c0r[s0], ka.pw[e], ka.pws[e], q), q);
+      v0.y = addmod(v0.y, shoup(c0r[s1], ka.pw[e], ka.pws[e], q), q);
+    }
+  }
+  *o0 = v0;
+  *o1 = v1;
+}
+
+// dst[b][p][e] += P src[b][p][e] for e < ell (the P limb of P src is 0): a giant step
+// without rotation, in the extended basis (R23).  dst rows [b][p][ell+1][n], src [b][p][ell][n].
+__global__ void add_pscaled_kernel(uint64_t *__restrict__ dst, size_t dst_stride, const uint64_t *__restrict__ src,
+                                   size_t src_stride, int ell, int n, ModTab mt, KipAcc ka) {
+  const uint32_t t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const uint32_t bpl = blockIdx.y;
+  const uint32_t l = bpl % ell, bp = bpl / ell, b = bp / 2, p = bp % 2;
+  if (t >= (uint32_t)n) return;
+  const uint64_t q = mt.q[l];
+  ulonglong2 *o = reinterpret_cast<ulonglong2 *>(dst + (size_t)b * dst_stride + ((size_t)p * (ell + 1) + l) * n + t);
+  const ulonglong2 sv =
+      *reinterpret_cast<const ulonglong2 *>(src + (size_t)b * src_stride + ((size_t)p * ell + l) * n + t);
+  const ulonglong2 dv = *o;
+  *o = make_ulonglong2(addmod(dv.x, shoup(sv.x, ka.pw[l], ka.pws[l], q), q),
+                       addmod(dv.y, shoup(sv.y, ka.pw[l], ka.pws[l], q), q));
+}
+
+KipAcc kip_acc(const hd_context *c, int ell, const uint64_t *c0, size_t c0_stride) {
+  KipAcc ka;
+  ka.c0 = c0;
+  ka.c0_stride = c0_stride;
+  for (int l = 0; l < ell; l++) {
+    ka.pw[l] = c->mod[c->L] % c->mod[l];
+    ka.pws[l] = host_shoup(ka.pw[l], c->mod[l]);
+  }
+  return ka;
 }
 
 __global__ void add_ct_kernel(uint64_t *__restrict__ dst, size_t dst_stride, const uint64_t *__restrict__ src,
@@ -112,7 +159,25 @@ hd_status ks_modup(hd_context *c, const uint64_t *c1, size_t c1_stride, uint32_t
 hd_status ks_kip(hd_context *c, const uint64_t *dig, const uint64_t *c1, size_t c1_stride, uint32_t B, uint32_t K,
                  int ell, const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u) {
   kip_kernel<<<grid_pairs(c->n, B * K * (ell + 1)), TPB, 0, c->stream>>>(dig, c1, c1_stride, u, ell, K, c->L, c->logn,
-                                                                        kptr_dev, gal_dev, c->mt);
+                                                                        kptr_dev, gal_dev, c->mt, KipAcc{});
+  ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  return HD_OK;
+}
+
+hd_status ks_kip_accumulate(hd_context *c, const uint64_t *dig, const uint64_t *ct, size_t ct_stride, uint32_t B,
+                            int ell, const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u) {
+  kip_kernel<<<grid_pairs(c->n, B * (ell + 1)), TPB, 0, c->stream>>>(
+      dig, ct + (size_t)ell * c->n, ct_stride, u, ell, 1, c->L, c->logn, kptr_dev, gal_dev, c->mt,
+      kip_acc(c, ell, ct, ct_stride));
+  ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  return HD_OK;
+}
+
+hd_status ks_add_pscaled(hd_context *c, uint64_t *u, const uint64_t *ct, size_t ct_stride, uint32_t B, int ell) {
+  add_pscaled_kernel<<<grid_pairs(c->n, B * 2 * ell), TPB, 0, c->stream>>>(
+      u, (size_t)2 * (ell + 1) * c->n, ct, ct_stride, ell, c->n, c->mt, kip_acc(c, ell, nullptr, 0));
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;

@@ -10,6 +10,13 @@ hd_status ks_modup(hd_context *c, const uint64_t *c1, size_t c1_stride, uint32_t
 // (the own-modulus digit of c1 is read from c1 itself: c1 of ciphertext b at c1 + b*c1_stride)
 hd_status ks_kip(hd_context *c, const uint64_t *dig, const uint64_t *c1, size_t c1_stride, uint32_t B, uint32_t K,
                  int ell, const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u);
+// Extended-basis giant-step accumulation (R23), B ciphertexts ct_b = ct + b*ct_stride
+// ([2][ell][n]), one key, u [B][2][ell+1][n] accumulated:
+//   u_b += KIP(pi_g(dig_b)) + (P pi_g(ct_b.c0), 0)   (a rotation before its ModDown)
+hd_status ks_kip_accumulate(hd_context *c, const uint64_t *dig, const uint64_t *ct, size_t ct_stride, uint32_t B,
+                            int ell, const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u);
+//   u_b += (P ct_b, with P limb 0)                    (a giant step without rotation)
+hd_status ks_add_pscaled(hd_context *c, uint64_t *u, const uint64_t *ct, size_t ct_stride, uint32_t B, int ell);
 // ModDown of u [X][2][ell+1][n] (P limb INTT'd in place) -> dst_x (+ pi_{g_k}(c0_b)).
 hd_status ks_moddown(hd_context *c, uint64_t *u, uint32_t X, uint32_t K, int ell, const uint32_t *gal_dev,
                      const uint64_t *c0, size_t c0_stride, uint64_t *dst, size_t dst_stride, bool accumulate,

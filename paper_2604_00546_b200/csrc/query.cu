@@ -121,22 +121,23 @@ static hd_status giant_and_fold(hd_database *db, cudaEvent_t *E) {
   const uint32_t A = db->A_loc;
   const size_t ct1 = (size_t)2 * (L - 1) * n;
   hd_status s;
-  // ---- giant rotations and sum (R2) ----
-  HD_CUDA(cudaMemsetAsync(db->y, 0, (size_t)A * ct1 * 8, c->stream));
+  // ---- giant rotations and sum (R2), accumulated in Q u {P} with one
+  //      ModDown per aggregate (R23) ----
+  const int ell = L - 1;
+  const size_t ext = (size_t)2 * (ell + 1) * n;  // u: [A][2][ell+1][n]
+  HD_CUDA(cudaMemsetAsync(db->u, 0, (size_t)A * ext * 8, c->stream));
   const size_t sp_stride = (size_t)nj * ct1;  // between aggregates for fixed j
   for (int jj = 0; jj < nj; jj++) {
     const uint64_t *Sj = db->Sp + (size_t)jj * ct1;
     if (db->pre[jj] == 0) {
-      if ((s = ct_add(c, db->y, ct1, Sj, sp_stride, A, L - 1))) return s;
+      if ((s = ks_add_pscaled(c, db->u, Sj, sp_stride, A, ell))) return s;
       continue;
     }
     const size_t slot = (size_t)(n1 - 1) + jj;
-    if ((s = ks_modup(c, Sj + (size_t)(L - 1) * n, sp_stride, A, L - 1, db->dig, db->tmp))) return s;
-    if ((s = ks_kip(c, db->dig, Sj + (size_t)(L - 1) * n, sp_stride, A, 1, L - 1, db->kptr + slot, db->gal + slot,
-                    db->u)))
-      return s;
-    if ((s = ks_moddown(c, db->u, A, 1, L - 1, db->gal + slot, Sj, sp_stride, db->y, ct1, true, db->tmp))) return s;
+    if ((s = ks_modup(c, Sj + (size_t)ell * n, sp_stride, A, ell, db->dig, db->tmp))) return s;
+    if ((s = ks_kip_accumulate(c, db->dig, Sj, sp_stride, A, ell, db->kptr + slot, db->gal + slot, db->u))) return s;
   }
+  if ((s = ks_moddown(c, db->u, A, 1, ell, db->gal, nullptr, 0, db->y, ct1, false, db->tmp))) return s;
   cudaEventRecord(E[5], c->stream);
   // ---- fold: out = y + Rot_{numSlots - N}(y) ----
   {

@@ -91,3 +91,53 @@ def test_multi_aggregate_partial_and_n1_equals_N(oracle_mod):
             assert all(o.pre_rot(N, n1, j) == 0 for j in range(jmin, jmax + 1))
         sc = _run_encrypted(o, db, q, N, n1, enc_seed=7)
         assert np.abs(sc - _cos(db, q)).max() < 1e-6
+
+
+def _centred_coeffs(o, pt):
+    """CRT-centred integer coefficients of an NTT-domain plaintext at len(pt) limbs."""
+    qs = o.p.moduli[: pt.shape[0]]
+    rows = [[int(v) for v in o.ntt(pt[l].copy(), l, inverse=True)] for l in range(len(qs))]
+    Q = 1
+    for q in qs:
+        Q *= q
+    out = []
+    for t in range(o.n):
+        x = 0
+        for l, q in enumerate(qs):
+            Ql = Q // q
+            x += rows[l][t] * Ql * pow(Ql, -1, q)
+        x %= Q
+        out.append(x - Q if x > Q // 2 else x)
+    return out
+
+
+@pytest.mark.parametrize("N,n1,K", [(16, 8, 60), (16, 4, 60), (16, 2, 40)])
+def test_hoisted_giant_sum_matches_eager(oracle_mod, N, n1, K):
+    """R23: accumulating the giant-step rotations in Q u {P} with one ModDown
+    gives exactly the per-rotation ModDown result when a single rotation is nonzero
+    (ModDown(P x + a) = x + ModDown(a)), and otherwise differs only by the ModDown
+    rounding: |dec_h - dec_e| <= (rotations + 1) (1 + ||s||_1) / 2 per coefficient."""
+    o = oracle_mod.Oracle(9, 3, seed=5)
+    rng = np.random.default_rng(N * n1)
+    db = rng.integers(-99, 100, size=(K, N)).astype(np.float32)
+    q = rng.integers(-99, 100, size=N).astype(np.float32)
+    s, s_ntt = o.secret_key()
+    steps, keys = o.keyset(s_ntt, o.rotation_steps(N, n1))
+    qct = o.encrypt(s_ntt, o.encode(o.query_slots(q), D45, o.L), 11)
+    r = o.baby_steps(qct, n1, steps, keys)
+    D = o.enroll_aggregate(o.normalize_rows(db), 0, K, n1, 0)
+    jmin, jmax = o.giant_range(N, n1)
+    rots = sum(1 for j in range(jmin, jmax + 1) if o.pre_rot(N, n1, j) != 0)
+    out_h, y_h = o.scan_aggregate(r, n1, N, D, steps, keys, want_y=True, hoisted=True)
+    out_e, y_e = o.scan_aggregate(r, n1, N, D, steps, keys, want_y=True, hoisted=False)
+    if rots == 1:
+        assert (y_h == y_e).all() and (out_h == out_e).all()
+    else:
+        assert not (y_h == y_e).all()  # the rounding really differs: the test sees both paths
+    bound = (rots + 1) * (1 + int(np.abs(s).sum())) / 2
+    dh, de = _centred_coeffs(o, o.decrypt(s_ntt, y_h)), _centred_coeffs(o, o.decrypt(s_ntt, y_e))
+    assert max(abs(a - b) for a, b in zip(dh, de)) <= bound
+    sc_h = o.decrypt_scores(s_ntt, out_h, N, 0, K)[:K]
+    sc_e = o.decrypt_scores(s_ntt, out_e, N, 0, K)[:K]
+    assert np.abs(sc_h - sc_e).max() < 1e-9
+    assert np.abs(sc_h - _cos(db, q)).max() < 1e-6
