@@ -159,6 +159,20 @@ hd_status hd_ciphertext_import(hd_context *ctx, const void *src, size_t bytes, i
 hd_status hd_ciphertext_import_into(hd_ciphertext *ct, const void *src, size_t bytes,
                                     int src_on_device);
 hd_status hd_ciphertext_limbs(const hd_ciphertext *ct, uint32_t *limbs);
+/* Asynchronous, level-reduced export (result download).  Writes the header and the
+ * limbs 0..nlimbs-1 of c0 and c1 (nlimbs = 0: all limbs) on an internal copy stream
+ * ordered after the ciphertext's last writer, and returns without waiting.  Dropping
+ * the top limbs is exact modular reduction to the smaller modulus Q' = q_0..q_{k-1}:
+ * decryption is unchanged while the plaintext stays below Q'/2 (R24: scores
+ * are < 2^46 against q_0 ~ 2^60), and the bytes halve at nlimbs = 1.  dst: pinned
+ * host memory (pageable also works but copies synchronously) or device memory.
+ * The data is in dst after hd_context_synchronize(); a later writer of ct (hd_query
+ * output, import_into) waits for the copy.  Errors: HD_E_LEVEL if nlimbs > limbs,
+ * HD_E_INVALID_ARG if cap is too small (dst = NULL queries the size in *written). */
+hd_status hd_ciphertext_export_async(hd_ciphertext *ct, uint32_t nlimbs, void *dst, size_t cap,
+                                     int dst_on_device, size_t *written);
+/* Waits for all work of the context: its stream, the query pipeline and the copies. */
+hd_status hd_context_synchronize(hd_context *ctx);
 hd_status hd_eval_keys_export(const hd_eval_keys *evk, void *dst, size_t cap, int dst_on_device,
                               size_t *written);
 hd_status hd_eval_keys_import(hd_context *ctx, const void *src, size_t bytes, int src_on_device,

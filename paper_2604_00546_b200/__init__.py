@@ -32,7 +32,7 @@ ABI_FUNCTIONS = [
     "hd_ciphertext_import", "hd_ciphertext_import_into", "hd_ciphertext_limbs", "hd_eval_keys_export",
     "hd_eval_keys_import", "hd_secret_key_export", "hd_ciphertext_destroy", "hd_eval_keys_destroy",
     "hd_secret_key_destroy", "hd_database_destroy", "hd_test_ntt", "hd_test_stage", "hd_test_rotate",
-    "hd_test_rescale",
+    "hd_test_rescale", "hd_ciphertext_export_async", "hd_context_synchronize",
 ]
 
 
@@ -101,6 +101,8 @@ def load():
             L.hd_ciphertext_export.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(C.c_size_t)]
             L.hd_ciphertext_import.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(VP)]
             L.hd_ciphertext_import_into.argtypes = [VP, VP, C.c_size_t, C.c_int]
+            L.hd_ciphertext_export_async.argtypes = [VP, C.c_uint32, VP, C.c_size_t, C.c_int, C.POINTER(C.c_size_t)]
+            L.hd_context_synchronize.argtypes = [VP]
             L.hd_ciphertext_limbs.argtypes = [VP, C.POINTER(C.c_uint32)]
             L.hd_eval_keys_export.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(C.c_size_t)]
             L.hd_eval_keys_import.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(VP)]
@@ -281,6 +283,22 @@ class Context(_Handle):
         _check("hd_ciphertext_export", load().hd_ciphertext_export(ct.h, VP(ptr), cap, 1 if on_device else 0,
                                                                    C.byref(w)))
         return w.value
+
+    def ciphertext_export_async(self, ct, dst, nlimbs=0, on_device=False):
+        """Level-reduced asynchronous export (hd_ciphertext_export_async): ``dst`` is
+        (pointer int, capacity) or None to query the size; data valid after synchronize()."""
+        w = C.c_size_t()
+        if dst is None:
+            _check("hd_ciphertext_export_async",
+                   load().hd_ciphertext_export_async(ct.h, nlimbs, None, 0, 0, C.byref(w)))
+            return w.value
+        ptr, cap = dst
+        _check("hd_ciphertext_export_async", load().hd_ciphertext_export_async(
+            ct.h, nlimbs, VP(ptr), cap, 1 if on_device else 0, C.byref(w)))
+        return w.value
+
+    def synchronize(self):
+        _check("hd_context_synchronize", load().hd_context_synchronize(self.h))
 
     def ciphertext_export_size(self, ct):
         w = C.c_size_t()

@@ -143,6 +143,7 @@ struct hd_context {
   double last_phase_ms[5] = {0, 0, 0, 0, 0};
   uint64_t launches = 0;  // kernels launched on this context (hd_launch_count)
   cudaStream_t sA = nullptr, sB = nullptr;  // internal streams of the query pipeline
+  cudaStream_t sIO = nullptr;               // device->host result downloads (export_async)
 };
 
 struct hd_secret_key {
@@ -167,6 +168,8 @@ struct hd_ciphertext {
   uint32_t limbs;
   uint64_t *data;                 // [2][limbs][n]
   cudaEvent_t ready = nullptr;    // recorded by the last writer (any stream); readers wait on it
+  cudaEvent_t used = nullptr;     // recorded by the last asynchronous reader (export_async);
+                                  // writers wait on it before overwriting data
 };
 
 struct hd_database {

@@ -220,6 +220,7 @@ extern "C" void hd_context_destroy(hd_context *c) {
   cudaFree(c->scratch);
   if (c->sA) cudaStreamDestroy(c->sA);
   if (c->sB) cudaStreamDestroy(c->sB);
+  if (c->sIO) cudaStreamDestroy(c->sIO);
   for (int i = 0; i < 8; i++)
     for (int k = 0; k < 64; k++)
       if (c->ev[k][i]) cudaEventDestroy(c->ev[k][i]);
@@ -366,9 +367,52 @@ extern "C" hd_status hd_ciphertext_import_into(hd_ciphertext *ct, const void *sr
     if (s) return s;
     if (h.kind != 1 || h.limbs != ct->limbs) return hd_fail(HD_E_LEVEL, "shape mismatch");
   }
+  if (ct->used) HD_CUDA(cudaStreamWaitEvent(c->stream, ct->used, 0));  // pending async export
   HD_CUDA(cudaMemcpyAsync(ct->data, (const char *)src + sizeof(Header), payload, kind_of(1, src_on_device),
                           c->stream));
   HD_CUDA(cudaEventRecord(ct->ready, c->stream));
+  return HD_OK;
+}
+
+extern "C" hd_status hd_ciphertext_export_async(hd_ciphertext *ct, uint32_t nlimbs, void *dst, size_t cap,
+                                                int dst_on_device, size_t *written) {
+  if (!ct) return hd_fail(HD_E_INVALID_ARG, "null ciphertext");
+  hd_context *c = ct->ctx;
+  if (nlimbs == 0) nlimbs = ct->limbs;
+  if (nlimbs > ct->limbs) return hd_fail(HD_E_LEVEL, "cannot export more limbs than the ciphertext has");
+  const size_t limb_bytes = sizeof(uint64_t) * c->n;
+  const size_t payload = 2 * nlimbs * limb_bytes, total = sizeof(Header) + payload;
+  if (written) *written = total;
+  if (!dst) return HD_OK;
+  if (cap < total) return hd_fail(HD_E_INVALID_ARG, "export capacity too small");
+  if (!c->sIO) HD_CUDA(cudaStreamCreateWithFlags(&c->sIO, cudaStreamNonBlocking));
+  if (!ct->used) HD_CUDA(cudaEventCreateWithFlags(&ct->used, cudaEventDisableTiming));
+  Header h{};
+  memcpy(h.magic, "HDBSGS01", 8);
+  h.kind = 1;
+  h.log_n = c->logn;
+  h.limbs = nlimbs;
+  h.mod_fp = mod_fingerprint(c);
+  h.payload = payload;
+  if (dst_on_device)  // pageable source: staged by the runtime before this call returns
+    HD_CUDA(cudaMemcpyAsync(dst, &h, sizeof(h), cudaMemcpyHostToDevice, c->sIO));
+  else
+    memcpy(dst, &h, sizeof(h));
+  HD_CUDA(cudaStreamWaitEvent(c->sIO, ct->ready, 0));
+  char *p = (char *)dst + sizeof(h);
+  const cudaMemcpyKind kind = kind_of(dst_on_device, 1);
+  // c0 limbs 0..nlimbs-1, then c1 limbs 0..nlimbs-1 (dropping the top limbs: R24)
+  HD_CUDA(cudaMemcpyAsync(p, ct->data, nlimbs * limb_bytes, kind, c->sIO));
+  HD_CUDA(cudaMemcpyAsync(p + nlimbs * limb_bytes, ct->data + (size_t)ct->limbs * c->n, nlimbs * limb_bytes, kind,
+                          c->sIO));
+  HD_CUDA(cudaEventRecord(ct->used, c->sIO));
+  return HD_OK;
+}
+
+extern "C" hd_status hd_context_synchronize(hd_context *c) {
+  if (!c) return hd_fail(HD_E_INVALID_ARG, "null context");
+  for (cudaStream_t s : {c->stream, c->sA, c->sB, c->sIO})
+    if (s || s == c->stream) HD_CUDA(cudaStreamSynchronize(s));
   return HD_OK;
 }
 
@@ -377,6 +421,10 @@ extern "C" void hd_ciphertext_destroy(hd_ciphertext *ct) {
   if (ct->ready) {
     cudaEventSynchronize(ct->ready);
     cudaEventDestroy(ct->ready);
+  }
+  if (ct->used) {
+    cudaEventSynchronize(ct->used);
+    cudaEventDestroy(ct->used);
   }
   cudaFree(ct->data);
   delete ct;

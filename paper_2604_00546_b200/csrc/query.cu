@@ -106,6 +106,7 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
   // outputs may still be read by caller-stream work enqueued before this call
   HD_CUDA(cudaStreamWaitEvent(sb, db->ev_in, 0));
   for (size_t i = 0; i < n_out; i++) {
+    if (out[i]->used) HD_CUDA(cudaStreamWaitEvent(sb, out[i]->used, 0));  // pending async export
     HD_CUDA(cudaMemcpyAsync(out[i]->data, db->outbuf + i * ct1, ct1 * 8, cudaMemcpyDeviceToDevice, sb));
     HD_CUDA(cudaEventRecord(out[i]->ready, sb));
   }

@@ -311,3 +311,32 @@ def test_errors():
     few = np.ones((4, 512), np.float32)   # the capacity check precedes any read of the rows
     rc = hd.load().hd_enroll(big.h, few.ctypes.data_as(C.c_void_p), 1 << 26, 512, 64, 0, 0, C.byref(out))
     assert rc == hd.HD_E_CAPACITY and not out.value          # 2^26 vectors: ~3.3 TB of diagonals
+
+
+def test_level_reduced_async_export():
+    """hd_ciphertext_export_async at 1 limb (R24): the exported residues are limb 0 of
+    the outputs bit for bit, they decrypt to the cosine scores, and a query issued right
+    after the export (no host sync) does not overwrite the outputs before the copies ran."""
+    run = Run(CONFIGS["C1"])
+    ctx, cfg = run.ctx, run.cfg
+    full = [ctx.ciphertext_residues(o) for o in run.outs]
+    sz = ctx.ciphertext_export_async(run.outs[0], None, nlimbs=1)
+    assert sz == 64 + 2 * ctx.n * 8
+    host = torch.empty(len(run.outs) * sz, dtype=torch.uint8, pin_memory=True)
+    for i, o in enumerate(run.outs):
+        ctx.ciphertext_export_async(o, (host.data_ptr() + i * sz, sz), nlimbs=1)
+    rng = np.random.default_rng(5)
+    q2 = rng.standard_normal(cfg.dim).astype(np.float32)
+    ctx.query(run.evk, run.db, ctx.encrypt_query(run.sk, q2, ENC_SEED_BASE + 1), run.outs)  # overwrites outs
+    ctx.synchronize()
+    buf = host.numpy()
+    cts = []
+    for i in range(len(run.outs)):
+        blob = buf[i * sz:(i + 1) * sz].copy()
+        got = blob[64:].view(np.uint64).reshape(2, 1, ctx.n)
+        assert (got[:, 0] == full[i][:, 0]).all(), i
+        cts.append(ctx.ciphertext_import(blob))
+    sc = ctx.decrypt_scores(run.sk, run.db.layout, cts)
+    assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-6
+    with pytest.raises(hd.HDError):
+        ctx.ciphertext_export_async(run.outs[0], None, nlimbs=cfg.limbs)  # outputs have L-1 limbs
