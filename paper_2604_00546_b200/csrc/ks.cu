@@ -100,19 +100,6 @@ KipAcc kip_acc(const hd_context *c, int ell, const uint64_t *c0, size_t c0_strid
   return ka;
 }
 
-__global__ void add_ct_kernel(uint64_t *__restrict__ dst, size_t dst_stride, const uint64_t *__restrict__ src,
-                              size_t src_stride, int ell, int n, ModTab mt) {
-  const uint32_t t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
-  const uint32_t bpl = blockIdx.y;
-  const uint32_t l = bpl % ell, bp = bpl / ell, b = bp / 2, p = bp % 2;
-  if (t >= (uint32_t)n) return;
-  const size_t off = ((size_t)p * ell + l) * n + t;
-  ulonglong2 *o = reinterpret_cast<ulonglong2 *>(dst + (size_t)b * dst_stride + off);
-  const ulonglong2 s = *reinterpret_cast<const ulonglong2 *>(src + (size_t)b * src_stride + off);
-  const ulonglong2 dv = *o;
-  *o = make_ulonglong2(addmod(dv.x, s.x, mt.q[l]), addmod(dv.y, s.y, mt.q[l]));
-}
-
 inline dim3 grid_pairs(int n, uint32_t rows) { return dim3((n / 2 + TPB - 1) / TPB, rows); }
 
 RowMap mods_seq(RowMap rm, uint32_t mdiv, int count, int first = 0) {
@@ -263,13 +250,4 @@ hd_status ks_rescale(hd_context *c, const uint64_t *S, size_t s_stride, uint32_t
     epi.ws[l] = host_shoup(epi.w[l], c->mod[l]);
   }
   return ntt_run(c, out, 2 * B * lo, ro, false, &lift, &epi);
-}
-
-hd_status ct_add(hd_context *c, uint64_t *dst, size_t dst_stride, const uint64_t *src, size_t src_stride,
-                 uint32_t B, int ell) {
-  add_ct_kernel<<<grid_pairs(c->n, B * 2 * ell), TPB, 0, c->stream>>>(dst, dst_stride, src, src_stride, ell, c->n,
-                                                                      c->mt);
-  ++c->launches;
-  HD_CUDA(cudaGetLastError());
-  return HD_OK;
 }

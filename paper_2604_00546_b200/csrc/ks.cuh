@@ -24,8 +24,6 @@ hd_status ks_moddown(hd_context *c, uint64_t *u, uint32_t X, uint32_t K, int ell
 // Rescale B ciphertexts at ell limbs (S_b at S + b*s_stride) -> out_b (ell-1 limbs).
 hd_status ks_rescale(hd_context *c, const uint64_t *S, size_t s_stride, uint32_t B, int ell, uint64_t *out,
                      size_t out_stride, uint64_t *tmp1, uint64_t *tmp2);
-hd_status ct_add(hd_context *c, uint64_t *dst, size_t dst_stride, const uint64_t *src, size_t src_stride,
-                 uint32_t B, int ell);
 
 // MAC (mac.cu)
 struct MacPlan {
