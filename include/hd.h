@@ -144,8 +144,10 @@ hd_status hd_query(hd_context *ctx, const hd_eval_keys *evk, const hd_database *
 /* Cumulative number of CUDA kernels this context has launched (all entry points). */
 hd_status hd_launch_count(const hd_context *ctx, uint64_t *count);
 /* Per-phase device times (ms), averaged over the hd_query calls issued since the
- * previous hd_query_stats call (up to 64; synchronises), CUDA events on the context
- * stream: [0] baby steps, [1] MAC, [2] rescale, [3] giant rotations, [4] fold. */
+ * previous hd_query_stats call (up to 64; synchronises), CUDA events on the streams
+ * that run them: [0] baby steps, [1] MAC, [2] rescale, [3] giant rotations, [4] fold,
+ * [5] the baby-step key inner product alone (part of [0]; the key-switch HBM stream).
+ * n_phases <= 6 values are written. */
 hd_status hd_query_stats(const hd_context *ctx, double *phase_ms, size_t n_phases);
 
 /* ---- serialisation (canonical: 64-byte header + u64 residues) --------------- */

@@ -261,8 +261,9 @@ class Context(_Handle):
         return [o if o is not None else Ciphertext(arr[i], self) for i, o in enumerate(outs)]
 
     def query_stats(self):
-        ms = np.zeros(5, np.float64)
-        _check("hd_query_stats", load().hd_query_stats(self.h, _ptr(ms), 5))
+        """[baby, mac, rescale, giant, fold, baby_kip] ms averaged over the queries since the last call."""
+        ms = np.zeros(6, np.float64)
+        _check("hd_query_stats", load().hd_query_stats(self.h, _ptr(ms), 6))
         return ms
 
     def launch_count(self):

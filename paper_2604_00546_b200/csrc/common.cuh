@@ -138,9 +138,10 @@ struct hd_context {
   void *scratch = nullptr;
   size_t scratch_bytes = 0;
   int *d_flag = nullptr;  // device error flag
-  cudaEvent_t ev[64][8] = {};  // per-query phase events (ring of 64 queries)
+constexpr static int kPhaseEvents = 9;
+  cudaEvent_t ev[64][kPhaseEvents] = {};  // per-query phase events (ring of 64 queries)
   int ev_next = 0, ev_pending = 0;
-  double last_phase_ms[5] = {0, 0, 0, 0, 0};
+  double last_phase_ms[6] = {0, 0, 0, 0, 0, 0};
   uint64_t launches = 0;  // kernels launched on this context (hd_launch_count)
   cudaStream_t sA = nullptr, sB = nullptr;  // internal streams of the query pipeline
   cudaStream_t sIO = nullptr;               // device->host result downloads (export_async)

@@ -200,7 +200,7 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
       (e = cudaMemcpy(c->rotg, rg.data(), c->ns * 4, cudaMemcpyHostToDevice)) ||
       (e = cudaMemset(c->d_flag, 0, 64)))
     return fail(e);
-  for (int i = 0; i < 8; i++)
+  for (int i = 0; i < hd_context::kPhaseEvents; i++)
     for (int k = 0; k < 64; k++)
       if ((e = cudaEventCreate(&c->ev[k][i]))) return fail(e);
   *out = c;
@@ -221,7 +221,7 @@ extern "C" void hd_context_destroy(hd_context *c) {
   if (c->sA) cudaStreamDestroy(c->sA);
   if (c->sB) cudaStreamDestroy(c->sB);
   if (c->sIO) cudaStreamDestroy(c->sIO);
-  for (int i = 0; i < 8; i++)
+  for (int i = 0; i < hd_context::kPhaseEvents; i++)
     for (int k = 0; k < 64; k++)
       if (c->ev[k][i]) cudaEventDestroy(c->ev[k][i]);
   delete c;

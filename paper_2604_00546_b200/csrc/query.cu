@@ -72,12 +72,18 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
   if (db->qcount >= 2) HD_CUDA(cudaStreamWaitEvent(sa, db->ev_sfree[par], 0));
   c->stream = sa;
   cudaEventRecord(E[0], sa);
+  if (n1 <= 1) {  // no baby-step key inner product: an empty KIP phase
+    cudaEventRecord(E[7], sa);
+    cudaEventRecord(E[8], sa);
+  }
   // ---- baby steps: r[0] = q; r[i] = Rot_i(q), hoisted ----
   HD_CUDA(cudaMemcpyAsync(db->r, query->data, ctL * 8, cudaMemcpyDeviceToDevice, sa));
   if (n1 > 1) {
     if ((s = ks_modup(c, query->data + (size_t)L * n, 0, 1, L, db->dig_b, db->tmp_b))) return s;
+    cudaEventRecord(E[7], sa);
     if ((s = ks_kip(c, db->dig_b, query->data + (size_t)L * n, 0, 1, n1 - 1, L, db->kptr, db->gal, db->u_b)))
       return s;
+    cudaEventRecord(E[8], sa);
     if ((s = ks_moddown(c, db->u_b, n1 - 1, n1 - 1, L, db->gal, query->data, 0, db->r + ctL, ctL, false,
                         db->tmp_b)))
       return s;
@@ -220,23 +226,24 @@ extern "C" hd_status hd_query_stats(const hd_context *cc, double *phase_ms, size
   hd_context *c = const_cast<hd_context *>(cc);
   // average over the queries issued since the previous call (up to the last 64)
   if (c->ev_pending > 0) {
-    // events: 0 A start, 1 baby done, 2 MAC done (A), 3 B start, 4 rescale, 5 giant, 6 fold (B)
-    static const int from[5] = {0, 1, 3, 4, 5}, to[5] = {1, 2, 4, 5, 6};
-    double acc[5] = {0, 0, 0, 0, 0};
+    // events: 0 A start, 1 baby done, 2 MAC done (A), 3 B start, 4 rescale, 5 giant, 6 fold (B),
+    // 7 / 8 around the baby-step key inner product (A; == 0 when n1 == 1)
+    static const int from[6] = {0, 1, 3, 4, 5, 7}, to[6] = {1, 2, 4, 5, 6, 8};
+    double acc[6] = {0, 0, 0, 0, 0, 0};
     const int last = (c->ev_next - 1) % 64;
     HD_CUDA(cudaEventSynchronize(c->ev[last][6]));
     for (int q = 0; q < c->ev_pending; q++) {
       const int idx = ((c->ev_next - 1 - q) % 64 + 64) % 64;
-      for (int i = 0; i < 5; i++) {
+      for (int i = 0; i < 6; i++) {
         float ms = 0;
         HD_CUDA(cudaEventElapsedTime(&ms, c->ev[idx][from[i]], c->ev[idx][to[i]]));
         acc[i] += ms;
       }
     }
-    for (int i = 0; i < 5; i++) c->last_phase_ms[i] = acc[i] / c->ev_pending;
+    for (int i = 0; i < 6; i++) c->last_phase_ms[i] = acc[i] / c->ev_pending;
     c->ev_pending = 0;
   }
-  for (size_t i = 0; i < n_phases && i < 5; i++) phase_ms[i] = c->last_phase_ms[i];
+  for (size_t i = 0; i < n_phases && i < 6; i++) phase_ms[i] = c->last_phase_ms[i];
   return HD_OK;
 }
 
