@@ -271,6 +271,58 @@ class Oracle:
             _p(steps), len(steps), _p(keys), _p(out), _p(y)))
         return (out, y) if want_y else out
 
+    # -- encrypted-database mode (NEXT-1, R26) ------------------------------------
+    def public_key(self, s_ntt):
+        pk = u64((2, self.L, self.n))
+        _check("public_key", lib().or_public_key(C.byref(self.p), _p(s_ntt), _p(pk)))
+        return pk
+
+    def encrypt_pk(self, pk, pt, enc_seed, obj):
+        nl = pt.shape[0]
+        ct = u64((2, nl, self.n))
+        _check("encrypt_pk", lib().or_encrypt_pk(C.byref(self.p), _p(pk), _p(np.ascontiguousarray(pt)), nl,
+                                                 C.c_uint64(enc_seed), C.c_uint32(obj), _p(ct)))
+        return ct
+
+    def relin_key(self, s_ntt):
+        key = u64((self.L, 2, self.L + 1, self.n))
+        _check("relin_key", lib().or_relin_key(C.byref(self.p), _p(s_ntt), _p(key)))
+        return key
+
+    def enroll_aggregate_encrypted(self, U, u_first, num_vectors, n1, agg, pk, enc_seed):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        dim = U.shape[1]
+        N = min(dim, self.ns)
+        D = u64((N, 2, self.L, self.n))
+        _check("enroll_aggregate_encrypted", lib().or_enroll_aggregate_encrypted(
+            C.byref(self.p), _p(U), C.c_int64(u_first), C.c_int64(U.shape[0]),
+            C.c_int64(num_vectors), dim, n1, C.c_int64(agg), _p(pk), C.c_uint64(enc_seed), _p(D)))
+        return D
+
+    def giant_sum_ct(self, r, n1, N, Dct, j):
+        S = u64((3, self.L, self.n))
+        rc = lib().or_giant_sum_ct(C.byref(self.p), _p(np.ascontiguousarray(r)), n1, N,
+                                   _p(np.ascontiguousarray(Dct)), j, _p(S))
+        if rc == OR_E_RANGE:
+            return None
+        _check("giant_sum_ct", rc)
+        return S
+
+    def relinearize(self, S3, rlk):
+        ell = S3.shape[1]
+        out = u64((2, ell, self.n))
+        _check("relinearize", lib().or_relinearize(C.byref(self.p), _p(np.ascontiguousarray(S3)), ell, _p(rlk),
+                                                   _p(out)))
+        return out
+
+    def scan_aggregate_ct(self, r, n1, N, Dct, steps, keys, rlk, want_y=False):
+        out = u64((2, self.L - 1, self.n))
+        y = u64((2, self.L - 1, self.n))
+        _check("scan_aggregate_ct", lib().or_scan_aggregate_ct(
+            C.byref(self.p), _p(np.ascontiguousarray(r)), n1, N, _p(np.ascontiguousarray(Dct)), _p(rlk),
+            _p(steps), len(steps), _p(keys), _p(out), _p(y)))
+        return (out, y) if want_y else out
+
     def decrypt_scores(self, s_ntt, out_ct, N, agg, num_vectors):
         M = self.ns // N
         sc = np.zeros((M // 2) * N, dtype=np.float64)

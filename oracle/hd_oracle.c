@@ -242,7 +242,9 @@ void or_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out
   out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
 }
 
-enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5 };
+enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5,
+       /* encrypted-database mode (NEXT-1, R26) */
+       TAG_PK_A = 6, TAG_PK_E = 7, TAG_PKE_V = 8, TAG_PKE_E = 9, TAG_RLK_A = 10, TAG_RLK_E = 11 };
 
 static void draw(uint64_t seed, uint32_t j, uint32_t l, uint32_t obj, uint32_t tag, uint32_t sub,
                  uint64_t *w0, uint64_t *w1) {
@@ -508,38 +510,110 @@ int or_secret_key(const or_params *p, int64_t *s_coeff, uint64_t *s_ntt) {
 
 /* Hybrid key-switching key for sigma_g(s) -> s, alpha = 1 limb per digit,
  * one special prime P (R11):  b_d = -a_d s + e_d + [l == d] (P mod q_d) s'. */
+/* Switching key from s' to s (s' given in NTT form over all L+1 moduli):
+ * b_d = -a_d s + e_d + [l == d] (P mod q_d) s', draws keyed by (obj, tag_a, tag_e). */
+static void switch_key(const or_params *p, const uint64_t *s_ntt, const uint64_t *sp_ntt, uint32_t obj,
+                       uint32_t tag_a, uint32_t tag_e, uint64_t *key) {
+  int n = p->n, L = p->L;
+  uint64_t *e_ntt = malloc(sizeof(uint64_t) * n);
+  for (int d = 0; d < L; d++) {
+    for (int l = 0; l <= L; l++) {
+      uint64_t m = p->mod[l];
+      for (int j = 0; j < n; j++)
+        e_ntt[j] = smod(draw_cbd21(p->seed, (uint32_t)j, obj, tag_e, (uint32_t)d), m);
+      or_ntt_forward(p, l, e_ntt);
+      uint64_t *kb = key + (((size_t)d * 2 + 0) * (L + 1) + l) * n;
+      uint64_t *ka = key + (((size_t)d * 2 + 1) * (L + 1) + l) * n;
+      uint64_t gad = (l == d) ? p->mod[L] % m : 0; /* (P mod q_d) on limb d only */
+      for (int j = 0; j < n; j++) {
+        uint64_t a = draw_uniform(p->seed, (uint32_t)j, (uint32_t)l, obj, tag_a, (uint32_t)d, m);
+        uint64_t b = submod(e_ntt[j], mulmod(a, s_ntt[(size_t)l * n + j], m), m);
+        b = addmod(b, mulmod(gad, sp_ntt[(size_t)l * n + j], m), m);
+        ka[j] = a;
+        kb[j] = b;
+      }
+    }
+  }
+  free(e_ntt);
+}
+
 int or_rotation_key(const or_params *p, const uint64_t *s_ntt, int64_t step, uint64_t *key) {
   int n = p->n, L = p->L;
   if (step <= 0 || step >= p->num_slots) return OR_E_ARG;
   uint64_t g = or_galois_elt(p, step);
   /* s' = sigma_g(s) from the coefficient-domain definition */
   int64_t *s = malloc(sizeof(int64_t) * n), *sp = malloc(sizeof(int64_t) * n);
-  uint64_t *sp_ntt = malloc(sizeof(uint64_t) * n);
-  uint64_t *e_ntt = malloc(sizeof(uint64_t) * n);
+  uint64_t *sp_ntt = malloc(sizeof(uint64_t) * (size_t)(L + 1) * n);
   for (int j = 0; j < n; j++) s[j] = draw_ternary(p->seed, (uint32_t)j, 0, TAG_SECRET);
   or_automorph_coeff(p, g, s, sp);
-  for (int d = 0; d < L; d++) {
-    for (int l = 0; l <= L; l++) {
-      uint64_t m = p->mod[l];
-      for (int j = 0; j < n; j++) sp_ntt[j] = smod(sp[j], m);
-      or_ntt_forward(p, l, sp_ntt);
-      for (int j = 0; j < n; j++)
-        e_ntt[j] = smod(draw_cbd21(p->seed, (uint32_t)j, (uint32_t)step, TAG_KEY_E, (uint32_t)d), m);
-      or_ntt_forward(p, l, e_ntt);
-      uint64_t *kb = key + (((size_t)d * 2 + 0) * (L + 1) + l) * n;
-      uint64_t *ka = key + (((size_t)d * 2 + 1) * (L + 1) + l) * n;
-      uint64_t gad = (l == d) ? p->mod[L] % m : 0; /* (P mod q_d) on limb d only */
-      for (int j = 0; j < n; j++) {
-        uint64_t a = draw_uniform(p->seed, (uint32_t)j, (uint32_t)l, (uint32_t)step, TAG_KEY_A,
-                                  (uint32_t)d, m);
-        uint64_t b = submod(e_ntt[j], mulmod(a, s_ntt[(size_t)l * n + j], m), m);
-        b = addmod(b, mulmod(gad, sp_ntt[j], m), m);
-        ka[j] = a;
-        kb[j] = b;
-      }
+  for (int l = 0; l <= L; l++) {
+    uint64_t *row = sp_ntt + (size_t)l * n;
+    for (int j = 0; j < n; j++) row[j] = smod(sp[j], p->mod[l]);
+    or_ntt_forward(p, l, row);
+  }
+  switch_key(p, s_ntt, sp_ntt, (uint32_t)step, TAG_KEY_A, TAG_KEY_E, key);
+  free(s); free(sp); free(sp_ntt);
+  return OR_OK;
+}
+
+/* Relinearisation key (encrypted-database mode): switching key from s^2 to s;
+ * s^2 in NTT form is the pointwise square of s_ntt (the negacyclic product). */
+int or_relin_key(const or_params *p, const uint64_t *s_ntt, uint64_t *key) {
+  int n = p->n, L = p->L;
+  uint64_t *s2 = malloc(sizeof(uint64_t) * (size_t)(L + 1) * n);
+  for (int l = 0; l <= L; l++)
+    for (int j = 0; j < n; j++) {
+      size_t o = (size_t)l * n + j;
+      s2[o] = mulmod(s_ntt[o], s_ntt[o], p->mod[l]);
+    }
+  switch_key(p, s_ntt, s2, 0, TAG_RLK_A, TAG_RLK_E, key);
+  free(s2);
+  return OR_OK;
+}
+
+/* Public key (R26): pk = (b, a) over the L ciphertext moduli, b = -a s + e. */
+int or_public_key(const or_params *p, const uint64_t *s_ntt, uint64_t *pk /* [2][L][n] */) {
+  int n = p->n, L = p->L;
+  uint64_t *e_ntt = malloc(sizeof(uint64_t) * n);
+  for (int l = 0; l < L; l++) {
+    uint64_t m = p->mod[l];
+    for (int j = 0; j < n; j++) e_ntt[j] = smod(draw_cbd21(p->seed, (uint32_t)j, 0, TAG_PK_E, 0), m);
+    or_ntt_forward(p, l, e_ntt);
+    uint64_t *b = pk + (size_t)l * n, *a = pk + ((size_t)L + l) * n;
+    for (int j = 0; j < n; j++) {
+      a[j] = draw_uniform(p->seed, (uint32_t)j, (uint32_t)l, 0, TAG_PK_A, 0, m);
+      b[j] = submod(e_ntt[j], mulmod(a[j], s_ntt[(size_t)l * n + j], m), m);
     }
   }
-  free(s); free(sp); free(sp_ntt); free(e_ntt);
+  free(e_ntt);
+  return OR_OK;
+}
+
+/* Public-key encryption (R26): c = (v b + e0 + pt, v a + e1), v ternary, e0/e1 CBD(21),
+ * drawn in the coefficient domain with Philox key enc_seed and object id obj. */
+int or_encrypt_pk(const or_params *p, const uint64_t *pk, const uint64_t *pt, int32_t nlimbs, uint64_t enc_seed,
+                  uint32_t obj, uint64_t *ct) {
+  int n = p->n, L = p->L;
+  if (nlimbs < 1 || nlimbs > L) return OR_E_ARG;
+  uint64_t *v = malloc(sizeof(uint64_t) * n), *e0 = malloc(sizeof(uint64_t) * n), *e1 = malloc(sizeof(uint64_t) * n);
+  for (int l = 0; l < nlimbs; l++) {
+    uint64_t m = p->mod[l];
+    for (int j = 0; j < n; j++) {
+      v[j] = smod(draw_ternary(enc_seed, (uint32_t)j, obj, TAG_PKE_V), m);
+      e0[j] = smod(draw_cbd21(enc_seed, (uint32_t)j, obj, TAG_PKE_E, 0), m);
+      e1[j] = smod(draw_cbd21(enc_seed, (uint32_t)j, obj, TAG_PKE_E, 1), m);
+    }
+    or_ntt_forward(p, l, v);
+    or_ntt_forward(p, l, e0);
+    or_ntt_forward(p, l, e1);
+    const uint64_t *b = pk + (size_t)l * n, *a = pk + ((size_t)L + l) * n;
+    uint64_t *c0 = ct + (size_t)l * n, *c1 = ct + ((size_t)nlimbs + l) * n;
+    for (int j = 0; j < n; j++) {
+      c0[j] = addmod(addmod(mulmod(v[j], b[j], m), e0[j], m), pt[(size_t)l * n + j], m);
+      c1[j] = addmod(mulmod(v[j], a[j], m), e1[j], m);
+    }
+  }
+  free(v); free(e0); free(e1);
   return OR_OK;
 }
 
@@ -821,6 +895,23 @@ int or_enroll_aggregate(const or_params *p, const double *U, int64_t u_first, in
   return rc;
 }
 
+/* Encrypted-database enrollment (NEXT-1, R26): the diagonal plaintexts of
+ * or_enroll_aggregate, each encrypted under the public key with object id
+ * agg * N + k (the enroller ships encrypted diagonals). */
+int or_enroll_aggregate_encrypted(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                                  int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg,
+                                  const uint64_t *pk, uint64_t enc_seed, uint64_t *Dct /* N x ct(L) */) {
+  int ns = p->num_slots, L = p->L, n = p->n;
+  int N = dim < ns ? dim : ns;
+  uint64_t *Dagg = malloc(sizeof(uint64_t) * (size_t)N * L * n);
+  int rc = or_enroll_aggregate(p, U, u_first, u_count, num_vectors, dim, n1, agg, Dagg);
+  for (int k = 0; k < N && rc == OR_OK; k++)
+    rc = or_encrypt_pk(p, pk, Dagg + (size_t)k * L * n, L, enc_seed, (uint32_t)(agg * N + k),
+                       Dct + (size_t)k * 2 * L * n);
+  free(Dagg);
+  return rc;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Scan (Alg. sender-bsgs).                                      */
 /* ------------------------------------------------------------------------ */
@@ -911,6 +1002,60 @@ int or_giant_sum(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
   return OR_OK;
 }
 
+/* Encrypted diagonals (NEXT-1): S_j = sum_i EvalMultNoRelin(r[i], Dct_k),
+ * the degree-2 tensor (r0 + r1 s)(D0 + D1 s) = d0 + d1 s + d2 s^2 accumulated as
+ * d0 += r0 D0, d1 += r0 D1 + r1 D0, d2 += r1 D1.  S: [3][L][n]. */
+int or_giant_sum_ct(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
+                    int32_t j, uint64_t *S) {
+  int n = p->n, L = p->L;
+  size_t ctsz = (size_t)2 * L * n;
+  int i_lo = 0 > -j * n1 - N / 2 ? 0 : -j * n1 - N / 2;
+  int i_hi = n1 - 1 < N / 2 - 1 - j * n1 ? n1 - 1 : N / 2 - 1 - j * n1;
+  memset(S, 0, sizeof(uint64_t) * 3 * L * n);
+  if (i_lo > i_hi) return OR_E_RANGE;
+  for (int i = i_lo; i <= i_hi; i++) {
+    int k = (((j * n1 + i) % N) + N) % N;
+    const uint64_t *D = Dct + ctsz * k, *ri = r + ctsz * i;
+    for (int l = 0; l < L; l++) {
+      uint64_t q = p->mod[l];
+      const uint64_t *r0 = ri + (size_t)l * n, *r1 = ri + ((size_t)L + l) * n;
+      const uint64_t *D0 = D + (size_t)l * n, *D1 = D + ((size_t)L + l) * n;
+      uint64_t *d0 = S + (size_t)l * n, *d1 = S + ((size_t)L + l) * n, *d2 = S + ((size_t)2 * L + l) * n;
+      for (int t = 0; t < n; t++) {
+        d0[t] = addmod(d0[t], mulmod(r0[t], D0[t], q), q);
+        d1[t] = addmod(d1[t], addmod(mulmod(r0[t], D1[t], q), mulmod(r1[t], D0[t], q), q), q);
+        d2[t] = addmod(d2[t], mulmod(r1[t], D1[t], q), q);
+      }
+    }
+  }
+  return OR_OK;
+}
+
+/* Relinearize: (d0, d1, d2) -> (d0, d1) + KeySwitch_{s^2 -> s}(d2): ModUp of
+ * d2, key inner product with the relinearisation key (no automorphism), ModDown. */
+int or_relinearize(const or_params *p, const uint64_t *S3, int32_t ell, const uint64_t *rlk, uint64_t *out) {
+  int n = p->n;
+  if (ell < 1 || ell > p->L) return OR_E_ARG;
+  size_t ext = (size_t)(ell + 1) * n;
+  uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)ell * (ell + 1) * n);
+  uint64_t *u = calloc(2 * ext, sizeof(uint64_t));
+  uint64_t *u0 = malloc(sizeof(uint64_t) * (size_t)ell * n), *u1 = malloc(sizeof(uint64_t) * (size_t)ell * n);
+  or_modup(p, S3 + (size_t)2 * ell * n, ell, dig);
+  kip_accumulate(p, dig, ell, rlk, 1, u);
+  moddown(p, u, ell, u0);
+  moddown(p, u + ext, ell, u1);
+  for (int l = 0; l < ell; l++) {
+    uint64_t q = p->mod[l];
+    for (int t = 0; t < n; t++) {
+      size_t o = (size_t)l * n + t;
+      out[o] = addmod(S3[o], u0[o], q);
+      out[(size_t)ell * n + o] = addmod(S3[(size_t)ell * n + o], u1[o], q);
+    }
+  }
+  free(dig); free(u); free(u0); free(u1);
+  return OR_OK;
+}
+
 /* One aggregate: steps 2a-2f with the fold reading (R2):
  * y = sum_j Rot_{preRot(j)}(Rescale(S_j)); out = y + Rot_{numSlots-N}(y). */
 int or_scan_aggregate(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
@@ -968,9 +1113,28 @@ int or_scan_aggregate(const or_params *p, const uint64_t *r, int32_t n1, int32_t
  * Each term ModDown'ed alone is exactly the eager rotation (ModDown(P x + a) =
  * x + ModDown(a)), so the sum differs from or_scan_aggregate only by the rounding of
  * the single ModDown. */
+static int scan_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dagg,
+                        const uint64_t *Dct, const uint64_t *rlk, const int32_t *steps, int32_t nkeys,
+                        const uint64_t *keys, uint64_t *out, uint64_t *y_out);
+
 int or_scan_aggregate_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
                               const uint64_t *Dagg, const int32_t *steps, int32_t nkeys,
                               const uint64_t *keys, uint64_t *out, uint64_t *y_out) {
+  return scan_hoisted(p, r, n1, N, Dagg, NULL, NULL, steps, nkeys, keys, out, y_out);
+}
+
+/* Encrypted-database scan (NEXT-1): Alg. sender-bsgs as written, S_j = Relinearize(
+ * sum_i EvalMultNoRelin(r[i], Dct_k)), then the schedule of
+ * or_scan_aggregate_hoisted (rescale, giant rotations in Q u {P}, fold). */
+int or_scan_aggregate_ct(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
+                         const uint64_t *rlk, const int32_t *steps, int32_t nkeys, const uint64_t *keys,
+                         uint64_t *out, uint64_t *y_out) {
+  return scan_hoisted(p, r, n1, N, NULL, Dct, rlk, steps, nkeys, keys, out, y_out);
+}
+
+static int scan_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dagg,
+                        const uint64_t *Dct, const uint64_t *rlk, const int32_t *steps, int32_t nkeys,
+                        const uint64_t *keys, uint64_t *out, uint64_t *y_out) {
   int n = p->n, L = p->L, ell = L - 1;
   size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * ell * n, ext = (size_t)(ell + 1) * n;
   uint64_t P = p->mod[L];
@@ -979,10 +1143,16 @@ int or_scan_aggregate_hoisted(const or_params *p, const uint64_t *r, int32_t n1,
   uint64_t *yx = calloc(2 * ext, sizeof(uint64_t)); /* [pp][e][t], e == ell: P */
   uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)ell * (ell + 1) * n);
   uint64_t *perm = malloc(sizeof(uint64_t) * n);
+  uint64_t *S3 = Dct ? malloc(sizeof(uint64_t) * (size_t)3 * L * n) : NULL;
   int jmin, jmax, rc = OR_OK;
   or_giant_range(N, n1, &jmin, &jmax);
   for (int j = jmin; j <= jmax && rc == OR_OK; j++) {
-    if (or_giant_sum(p, r, n1, N, Dagg, j, S) != OR_OK) continue; /* empty range */
+    if (Dct) {
+      if (or_giant_sum_ct(p, r, n1, N, Dct, j, S3) != OR_OK) continue; /* empty range */
+      or_relinearize(p, S3, L, rlk, S);                                  /* Step 2c */
+    } else if (or_giant_sum(p, r, n1, N, Dagg, j, S) != OR_OK) {
+      continue; /* empty range */
+    }
     or_rescale(p, S, L, Sp);                                      /* Step 2c */
     int s = or_pre_rot(N, n1, j);                                 /* Step 2d */
     if (s == 0) { /* y_ext += P T_j (P limb += 0) */
@@ -1027,7 +1197,7 @@ int or_scan_aggregate_hoisted(const or_params *p, const uint64_t *r, int32_t n1,
       if (y_out) memcpy(y_out, y, sizeof(uint64_t) * ct1);
     }
   }
-  free(S); free(Sp); free(T); free(y); free(yx); free(dig); free(perm);
+  free(S); free(Sp); free(T); free(y); free(yx); free(dig); free(perm); free(S3);
   return rc;
 }
 

@@ -88,6 +88,13 @@ int or_encrypt(const or_params *p, const uint64_t *s_ntt, const uint64_t *pt, in
 int or_decrypt(const or_params *p, const uint64_t *s_ntt, const uint64_t *ct, int32_t nlimbs,
                uint64_t *pt);
 
+/* Encrypted-database mode (NEXT-1, R26): public key [2][L][n] (b, a); public-key
+ * encryption with object id obj; relinearisation key (layout of a rotation key). */
+int or_public_key(const or_params *p, const uint64_t *s_ntt, uint64_t *pk);
+int or_encrypt_pk(const or_params *p, const uint64_t *pk, const uint64_t *pt, int32_t nlimbs,
+                  uint64_t enc_seed, uint32_t obj, uint64_t *ct);
+int or_relin_key(const or_params *p, const uint64_t *s_ntt, uint64_t *key);
+
 /* Key switching pieces (R11, R12) at ciphertext level `ell` (limbs q_0..q_{ell-1}). */
 int or_modup(const or_params *p, const uint64_t *c1, int32_t ell, uint64_t *dig);
 int or_rotate_hoisted(const or_params *p, const uint64_t *ct, const uint64_t *dig, int32_t ell,
@@ -95,6 +102,8 @@ int or_rotate_hoisted(const or_params *p, const uint64_t *ct, const uint64_t *di
 int or_rotate(const or_params *p, const uint64_t *ct, int32_t ell, const uint64_t *key,
               int64_t step, uint64_t *out);
 int or_rescale(const or_params *p, const uint64_t *ct, int32_t ell, uint64_t *out);
+/* (d0, d1, d2) [3][ell][n] -> (d0, d1) + KeySwitch_{s^2->s}(d2) [2][ell][n]. */
+int or_relinearize(const or_params *p, const uint64_t *S3, int32_t ell, const uint64_t *rlk, uint64_t *out);
 
 /* Enrollment (Alg. enroller_bsgs) and query slot layout (R8). */
 int or_normalize(const float *v, int32_t dim, double *u);
@@ -106,6 +115,10 @@ int or_enroll_slots(const or_params *p, const double *U, int64_t u_first, int64_
 int or_enroll_aggregate(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
                         int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg,
                         uint64_t *Dagg /* N x pt(L) */);
+
+int or_enroll_aggregate_encrypted(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                                  int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg,
+                                  const uint64_t *pk, uint64_t enc_seed, uint64_t *Dct /* N x ct(L) */);
 
 /* Scan layout helpers (R6) */
 int or_giant_range(int32_t N, int32_t n1, int32_t *j_min, int32_t *j_max);
@@ -128,6 +141,14 @@ int or_scan_aggregate(const or_params *p, const uint64_t *r, int32_t n1, int32_t
 int or_scan_aggregate_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
                               const uint64_t *Dagg, const int32_t *steps, int32_t nkeys,
                               const uint64_t *keys, uint64_t *out, uint64_t *y_out);
+
+/* Encrypted diagonals (NEXT-1): degree-2 giant-step sum [3][L][n], and the scan with
+ * Relinearize before the rescale, then the R23 schedule. */
+int or_giant_sum_ct(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
+                    int32_t j, uint64_t *S /* [3][L][n] */);
+int or_scan_aggregate_ct(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
+                         const uint64_t *rlk, const int32_t *steps, int32_t nkeys, const uint64_t *keys,
+                         uint64_t *out, uint64_t *y_out);
 
 /* Decrypt + decode one output ciphertext and read the scores of its vectors (R4). */
 int or_decrypt_scores(const or_params *p, const uint64_t *s_ntt, const uint64_t *out_ct,
