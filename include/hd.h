@@ -66,6 +66,7 @@ typedef struct hd_secret_key hd_secret_key; /* client only                      
 typedef struct hd_eval_keys hd_eval_keys;   /* rotation keys, device-resident   */
 typedef struct hd_database hd_database;     /* diagonal plaintexts of [agg_begin, agg_end) */
 typedef struct hd_ciphertext hd_ciphertext; /* device-resident ciphertext       */
+typedef struct hd_public_key hd_public_key; /* encrypted-database mode (R26)     */
 
 /* CKKS parameters (R5, R11).  Defaults (when a field is 0): num_limbs 3,
  * q0_bits 60, scale_bits 45, special_bits 60, num_special 1, digit_limbs 1.
@@ -133,6 +134,17 @@ hd_status hd_decrypt(hd_context *ctx, const hd_secret_key *sk, const hd_cipherte
 hd_status hd_enroll(hd_context *ctx, const float *vectors, uint64_t num_vectors,
                     uint32_t vector_dim, uint32_t n1, uint32_t agg_begin, uint32_t agg_end,
                     hd_database **out);
+/* Encrypted-database mode (NEXT-1; the paper's threat model):
+ * as hd_enroll, then every diagonal plaintext is encrypted under the public key
+ * (R26: c = (v b + e0 + pt, v a + e1), v ternary, e0/e1 CBD(21), Philox key enc_seed,
+ * object id agg * vector_dim + k), so the server never sees the database.  hd_query
+ * on such a database computes S_j = Relinearize(sum_i r[i] (x) Dct_k)
+ * and needs the relinearisation key in evk (hd_relin_keygen; else HD_E_MISSING_KEY).
+ * Diagonal bytes double (2 polynomials). */
+hd_status hd_enroll_encrypted(hd_context *ctx, const hd_public_key *pk, const float *vectors,
+                              uint64_t num_vectors, uint32_t vector_dim, uint32_t n1,
+                              uint32_t agg_begin, uint32_t agg_end, uint64_t enc_seed,
+                              hd_database **out);
 hd_status hd_database_layout(const hd_database *db, hd_layout *out);
 /* The online scan (Alg. sender-bsgs; fold schedule R2): baby steps
  * (hoisted), MAC over all local aggregates, rescale, giant rotations, fold.
@@ -182,6 +194,18 @@ hd_status hd_eval_keys_import(hd_context *ctx, const void *src, size_t bytes, in
 /* Secret key in NTT form, host u64 [(L+1)][n]; test use. */
 hd_status hd_secret_key_export(const hd_secret_key *sk, uint64_t *dst, size_t cap);
 
+/* Public key pk = (b, a) = (-a s + e, a) over the L ciphertext moduli (R26; Philox
+ * tags 6/7 under the context seed), for the enroller's encryption. */
+hd_status hd_public_keygen(hd_context *ctx, const hd_secret_key *sk, hd_public_key **out);
+/* Host u64 [2][L][n] (b then a), NTT form. */
+hd_status hd_public_key_export(const hd_public_key *pk, uint64_t *dst, size_t cap);
+hd_status hd_public_key_import(hd_context *ctx, const uint64_t *src, size_t count, hd_public_key **out);
+/* Adds the relinearisation key (key switching s^2 -> s, layout of a rotation key,
+ * Philox tags 10/11, object 0) to an evaluation-key set; exported/imported with it
+ * under the reserved step 0.  No-op if present. */
+hd_status hd_relin_keygen(hd_context *ctx, const hd_secret_key *sk, hd_eval_keys *evk);
+void hd_public_key_destroy(hd_public_key *pk);
+
 void hd_ciphertext_destroy(hd_ciphertext *ct);
 void hd_eval_keys_destroy(hd_eval_keys *evk);
 void hd_secret_key_destroy(hd_secret_key *sk);
@@ -194,10 +218,11 @@ hd_status hd_test_ntt(hd_context *ctx, uint64_t *data, uint32_t n_rows,
                       const uint32_t *modulus_idx, int inverse);
 /* Stage buffers left by the last hd_query on `db` (host copy):
  *   which 0: baby step r[index]            (ct, L limbs)
- *         1: giant sum S_{agg,j}           (ct, L limbs),   index = j
+ *         1: giant sum S_{agg,j}           (ct, L limbs),   index = j; encrypted
+ *            database: 3 polynomials, (d0, d1) relinearised and d2 as accumulated
  *         2: rescaled S'_{agg,j}           (ct, L-1 limbs), index = j
  *         3: y_agg = sum_j Rot(S'_j)       (ct, L-1 limbs)
- *         4: diagonal plaintext D[agg][k]  (pt, L limbs),   index = k
+ *         4: diagonal D[agg][k]            (pt, L limbs; encrypted: ct, L limbs), index = k
  * agg is the global aggregate index.  cap in u64 elements. */
 hd_status hd_test_stage(const hd_database *db, int which, uint32_t agg, int32_t index,
                         uint64_t *host_dst, size_t cap);

@@ -32,7 +32,8 @@ ABI_FUNCTIONS = [
     "hd_ciphertext_import", "hd_ciphertext_import_into", "hd_ciphertext_limbs", "hd_eval_keys_export",
     "hd_eval_keys_import", "hd_secret_key_export", "hd_ciphertext_destroy", "hd_eval_keys_destroy",
     "hd_secret_key_destroy", "hd_database_destroy", "hd_test_ntt", "hd_test_stage", "hd_test_rotate",
-    "hd_test_rescale", "hd_ciphertext_export_async", "hd_context_synchronize",
+    "hd_test_rescale", "hd_ciphertext_export_async", "hd_context_synchronize", "hd_enroll_encrypted",
+    "hd_public_keygen", "hd_public_key_export", "hd_public_key_import", "hd_relin_keygen", "hd_public_key_destroy",
 ]
 
 
@@ -80,7 +81,7 @@ def load():
                 if name not in ("hd_status_string", "hd_last_error"):
                     f.restype = C.c_int
             for name in ("hd_context_destroy", "hd_ciphertext_destroy", "hd_eval_keys_destroy",
-                         "hd_secret_key_destroy", "hd_database_destroy"):
+                         "hd_secret_key_destroy", "hd_database_destroy", "hd_public_key_destroy"):
                 getattr(L, name).restype = None
                 getattr(L, name).argtypes = [VP]
             L.hd_context_create.argtypes = [C.POINTER(Params), C.c_int, VP, C.POINTER(VP)]
@@ -103,6 +104,12 @@ def load():
             L.hd_ciphertext_import_into.argtypes = [VP, VP, C.c_size_t, C.c_int]
             L.hd_ciphertext_export_async.argtypes = [VP, C.c_uint32, VP, C.c_size_t, C.c_int, C.POINTER(C.c_size_t)]
             L.hd_context_synchronize.argtypes = [VP]
+            L.hd_enroll_encrypted.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                              C.c_uint64, C.POINTER(VP)]
+            L.hd_public_keygen.argtypes = [VP, VP, C.POINTER(VP)]
+            L.hd_public_key_export.argtypes = [VP, VP, C.c_size_t]
+            L.hd_public_key_import.argtypes = [VP, VP, C.c_size_t, C.POINTER(VP)]
+            L.hd_relin_keygen.argtypes = [VP, VP, VP]
             L.hd_ciphertext_limbs.argtypes = [VP, C.POINTER(C.c_uint32)]
             L.hd_eval_keys_export.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(C.c_size_t)]
             L.hd_eval_keys_import.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(VP)]
@@ -156,6 +163,10 @@ class SecretKey(_Handle):
 
 class EvalKeys(_Handle):
     _destroy = "hd_eval_keys_destroy"
+
+
+class PublicKey(_Handle):
+    _destroy = "hd_public_key_destroy"
 
 
 class Ciphertext(_Handle):
@@ -251,6 +262,36 @@ class Context(_Handle):
         _check("hd_enroll", load().hd_enroll(self.h, _ptr(vectors), vectors.shape[0], vectors.shape[1], n1,
                                              agg_begin, agg_end, C.byref(out)))
         return Database(out.value, self)
+
+    # -- encrypted-database mode (NEXT-1, R26) ------------------------------------------------
+    def public_keygen(self, sk):
+        out = VP()
+        _check("hd_public_keygen", load().hd_public_keygen(self.h, sk.h, C.byref(out)))
+        return PublicKey(out.value, self)
+
+    def public_key_export(self, pk):
+        buf = np.zeros((2, self.L, self.n), np.uint64)
+        _check("hd_public_key_export", load().hd_public_key_export(pk.h, _ptr(buf), buf.size))
+        return buf
+
+    def public_key_import(self, arr):
+        arr = np.ascontiguousarray(arr, dtype=np.uint64)
+        out = VP()
+        _check("hd_public_key_import", load().hd_public_key_import(self.h, _ptr(arr), arr.size, C.byref(out)))
+        return PublicKey(out.value, self)
+
+    def relin_keygen(self, sk, evk):
+        _check("hd_relin_keygen", load().hd_relin_keygen(self.h, sk.h, evk.h))
+
+    def enroll_encrypted(self, pk, vectors, n1, enc_seed, agg_begin=0, agg_end=0):
+        vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+        out = VP()
+        _check("hd_enroll_encrypted", load().hd_enroll_encrypted(
+            self.h, pk.h, _ptr(vectors), vectors.shape[0], vectors.shape[1], n1, agg_begin, agg_end,
+            C.c_uint64(enc_seed), C.byref(out)))
+        db = Database(out.value, self)
+        db.encrypted = True
+        return db
 
     def query(self, evk, db, query, outs=None):
         nloc = db.num_local
@@ -353,8 +394,10 @@ class Context(_Handle):
         return rows
 
     def test_stage(self, db, which, agg, index):
+        enc = getattr(db, "encrypted", False)
         ell = self.L if which in (0, 1) else (self.L - 1 if which in (2, 3) else self.L)
-        shape = (self.L, self.n) if which == 4 else (2, ell, self.n)
+        shape = ((2, self.L, self.n) if enc else (self.L, self.n)) if which == 4 else \
+            (3 if which == 1 and enc else 2, ell, self.n)
         out = np.zeros(shape, np.uint64)
         _check("hd_test_stage", load().hd_test_stage(db.h, which, agg, index, _ptr(out), out.size))
         return out

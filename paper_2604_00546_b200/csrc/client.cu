@@ -7,45 +7,13 @@
 
 #include "common.cuh"
 #include "ks.cuh"
+#include "rng.cuh"
 
 hd_status normalize_on_device(hd_context *c, const float *dv, int rows, int dim, double *U);
 hd_status check_flag(hd_context *c);
 
 namespace {
 constexpr int TPB = 256;
-enum { TAG_SECRET = 1, TAG_KEY_A = 2, TAG_KEY_E = 3, TAG_ENC_A = 4, TAG_ENC_E = 5 };
-
-__device__ __forceinline__ void philox4x32_10(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
-                                              uint32_t k1, uint64_t &w0, uint64_t &w1) {
-#pragma unroll
-  for (int r = 0; r < 10; r++) {
-    if (r) {
-      k0 += 0x9E3779B9u;
-      k1 += 0xBB67AE85u;
-    }
-    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
-    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
-    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
-    c0 = n0;
-    c1 = lo1;
-    c2 = n2;
-    c3 = lo0;
-  }
-  w0 = (uint64_t)c0 | ((uint64_t)c1 << 32);
-  w1 = (uint64_t)c2 | ((uint64_t)c3 << 32);
-}
-__device__ __forceinline__ void draw(uint64_t seed, uint32_t j, uint32_t l, uint32_t obj, uint32_t tag, uint32_t sub,
-                                     uint64_t &w0, uint64_t &w1) {
-  philox4x32_10(j, l, obj, (tag << 16) | sub, (uint32_t)seed, (uint32_t)(seed >> 32), w0, w1);
-}
-__device__ __forceinline__ int64_t cbd21(uint64_t w0) {
-  return (int64_t)__popcll(w0 & 0x1FFFFFull) - (int64_t)__popcll((w0 >> 21) & 0x1FFFFFull);
-}
-__device__ __forceinline__ uint64_t smod_dev(int64_t x, uint64_t q, uint64_t bar) {
-  if (x >= 0) return reduce64((uint64_t)x, q, bar);
-  uint64_t r = reduce64((uint64_t)(-x), q, bar);
-  return r ? q - r : 0;
-}
 
 // s (ternary) into every modulus row [(L+1)][n] (coefficient form).
 __global__ void secret_kernel(uint64_t seed, int n, int nm, uint64_t *__restrict__ s, ModTab mt) {
@@ -57,19 +25,21 @@ __global__ void secret_kernel(uint64_t seed, int n, int nm, uint64_t *__restrict
   for (int l = 0; l < nm; l++) s[(size_t)l * n + j] = smod_dev(v, mt.q[l], mt.bar[l]);
 }
 
-// error rows of a key: key[d][0][l][j] = CBD draw of (j, step, d) mod q_l (coefficient form).
-__global__ void key_error_kernel(uint64_t seed, uint32_t step, int n, int L, uint64_t *__restrict__ key, ModTab mt) {
+// error rows of a key: key[d][0][l][j] = CBD draw of (j, obj, d) mod q_l (coefficient form).
+__global__ void key_error_kernel(uint64_t seed, uint32_t step, uint32_t tag, int n, int L, uint64_t *__restrict__ key,
+                                 ModTab mt) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int d = blockIdx.y;
   if (j >= n) return;
   uint64_t w0, w1;
-  draw(seed, j, 0, step, TAG_KEY_E, d, w0, w1);
+  draw(seed, j, 0, step, tag, d, w0, w1);
   const int64_t e = cbd21(w0);
   for (int l = 0; l <= L; l++) key[((size_t)(d * 2) * (L + 1) + l) * n + j] = smod_dev(e, mt.q[l], mt.bar[l]);
 }
 
-// b_d = e_d - a_d s + [l == d] (P mod q_d) sigma_g(s);  a_d uniform in NTT form (R11, R14).
-__global__ void key_combine_kernel(uint64_t seed, uint32_t step, uint32_t g, int logn, int L,
+// b_d = e_d - a_d s + [l == d] (P mod q_d) s';  a_d uniform in NTT form (R11, R14).
+// s' = sigma_g(s) (rotation key, g = Galois element) or s^2 (g = 0: relinearisation key, R26).
+__global__ void key_combine_kernel(uint64_t seed, uint32_t step, uint32_t tag_a, uint32_t g, int logn, int L,
                                    const uint64_t *__restrict__ s_ntt, uint64_t *__restrict__ key, ModTab mt,
                                    InvTab2 pmod) {
   const int n = 1 << logn;
@@ -79,13 +49,15 @@ __global__ void key_combine_kernel(uint64_t seed, uint32_t step, uint32_t g, int
   if (j >= n) return;
   const uint64_t q = mt.q[l];
   uint64_t w0, w1;
-  draw(seed, j, l, step, TAG_KEY_A, d, w0, w1);
+  draw(seed, j, l, step, tag_a, d, w0, w1);
   const uint64_t a = reduce128(w0, w1, q, mt.bar[l], mt.r64[l], mt.r64s[l]);
   uint64_t *kb = key + ((size_t)(d * 2 + 0) * (L + 1) + l) * n;
   uint64_t *ka = key + ((size_t)(d * 2 + 1) * (L + 1) + l) * n;
   uint64_t b = submod(kb[j], mulmod(a, s_ntt[(size_t)l * n + j], mt, l), q);
   if (l == d) {
-    const uint64_t sp = s_ntt[(size_t)l * n + galois_src(j, g, logn)];  // sigma_g(s) in the NTT domain
+    const uint64_t sj = s_ntt[(size_t)l * n + j];
+    const uint64_t sp = g ? s_ntt[(size_t)l * n + galois_src(j, g, logn)]  // sigma_g(s) in the NTT domain
+                          : mulmod(sj, sj, mt, l);                          // s^2
     b = addmod(b, mulmod(pmod.w[l], sp, mt, l), q);
   }
   kb[j] = b;
@@ -229,6 +201,66 @@ __global__ void scores_kernel(const double *__restrict__ z, int N, int M, long l
   const long long v = (agg * (M / 2) + b) * N + t;
   if (v >= v_first && v < v_end) scores[v - v_first] = z[b * 2 * N + t];
 }
+// ---- encrypted-database mode (NEXT-1, R26) -------------------------------------------
+// public key: b rows hold e (coefficient form) before the NTT; then b = e - a s, a uniform.
+__global__ void pk_error_kernel(uint64_t seed, int n, int L, uint64_t *__restrict__ b, ModTab mt) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  uint64_t w0, w1;
+  draw(seed, j, 0, 0, TAG_PK_E, 0, w0, w1);
+  const int64_t e = cbd21(w0);
+  for (int l = 0; l < L; l++) b[(size_t)l * n + j] = smod_dev(e, mt.q[l], mt.bar[l]);
+}
+__global__ void pk_combine_kernel(uint64_t seed, int n, int L, const uint64_t *__restrict__ s_ntt,
+                                  uint64_t *__restrict__ pk, ModTab mt) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int l = blockIdx.y;
+  if (j >= n) return;
+  const uint64_t q = mt.q[l];
+  uint64_t w0, w1;
+  draw(seed, j, l, 0, TAG_PK_A, 0, w0, w1);
+  const uint64_t a = reduce128(w0, w1, q, mt.bar[l], mt.r64[l], mt.r64s[l]);
+  uint64_t *b = pk + (size_t)l * n;
+  b[j] = submod(b[j], mulmod(a, s_ntt[(size_t)l * n + j], mt, l), q);
+  pk[((size_t)L + l) * n + j] = a;
+}
+// public-key encryption of B ciphertexts (ct_x at ct + x*ct_stride, c0 holding the plaintext):
+// v (ternary) and e0 into scratch rows [x][l], e1 into the c1 rows, coefficient form.
+__global__ void pke_draw_kernel(uint64_t seed, uint32_t obj0, int n, int L, uint64_t *__restrict__ ct,
+                                size_t ct_stride, uint64_t *__restrict__ V, uint64_t *__restrict__ E0, ModTab mt) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t x = blockIdx.y;
+  if (j >= n) return;
+  const uint32_t obj = obj0 + x;
+  uint64_t w0, w1;
+  draw(seed, j, 0, obj, TAG_PKE_V, 0, w0, w1);
+  const int64_t v = (int64_t)(w0 % 3) - 1;
+  draw(seed, j, 0, obj, TAG_PKE_E, 0, w0, w1);
+  const int64_t e0 = cbd21(w0);
+  draw(seed, j, 0, obj, TAG_PKE_E, 1, w0, w1);
+  const int64_t e1 = cbd21(w0);
+  uint64_t *c1 = ct + (size_t)x * ct_stride + (size_t)L * n;
+  for (int l = 0; l < L; l++) {
+    const size_t o = ((size_t)x * L + l) * n + j;
+    V[o] = smod_dev(v, mt.q[l], mt.bar[l]);
+    E0[o] = smod_dev(e0, mt.q[l], mt.bar[l]);
+    c1[(size_t)l * n + j] = smod_dev(e1, mt.q[l], mt.bar[l]);
+  }
+}
+// c0 = v b + e0 + pt, c1 = v a + e1 (all NTT form)
+__global__ void pke_combine_kernel(int n, int L, const uint64_t *__restrict__ pk, uint64_t *__restrict__ ct,
+                                   size_t ct_stride, const uint64_t *__restrict__ V, const uint64_t *__restrict__ E0,
+                                   ModTab mt) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t xl = blockIdx.y, x = xl / L, l = xl % L;
+  if (j >= n) return;
+  const uint64_t q = mt.q[l];
+  const size_t o = ((size_t)x * L + l) * n + j;
+  const uint64_t v = V[o];
+  uint64_t *c0 = ct + (size_t)x * ct_stride + (size_t)l * n, *c1 = c0 + (size_t)L * n;
+  c0[j] = addmod(addmod(mulmod(v, pk[(size_t)l * n + j], mt, l), E0[o], q), c0[j], q);
+  c1[j] = addmod(mulmod(v, pk[((size_t)L + l) * n + j], mt, l), c1[j], q);
+}
 }  // namespace
 
 static uint64_t inv_host(uint64_t a, uint64_t q) { return host_powmod(a % q, q - 2, q); }
@@ -270,7 +302,7 @@ extern "C" hd_status hd_keygen(hd_context *c, const int32_t *steps, size_t count
     uint64_t *key = evk->keys + evk->key_elems * i;
     const uint32_t step = (uint32_t)steps[i];
     const uint32_t g = (uint32_t)host_powmod(5, step, 2ull * n);
-    key_error_kernel<<<dim3((n + TPB - 1) / TPB, L), TPB, 0, c->stream>>>(seed, step, n, L, key, c->mt); ++c->launches;
+    key_error_kernel<<<dim3((n + TPB - 1) / TPB, L), TPB, 0, c->stream>>>(seed, step, TAG_KEY_E, n, L, key, c->mt); ++c->launches;
     RowMap rk{};  // rows (d, l) at key + (d 2 (L+1) + l) n
     rk.gsize = L + 1;
     rk.gstride = (uint64_t)2 * (L + 1) * n;
@@ -278,8 +310,8 @@ extern "C" hd_status hd_keygen(hd_context *c, const int32_t *steps, size_t count
     rk.mlen = L + 1;
     for (int l = 0; l <= L; l++) rk.midx[l] = l;
     if ((s = ntt_rows(c, key, L * (L + 1), rk, false))) return fail(s);
-    key_combine_kernel<<<dim3((n + TPB - 1) / TPB, L * (L + 1)), TPB, 0, c->stream>>>(seed, step, g, c->logn, L,
-                                                                                      sk->s_ntt, key, c->mt, pmod); ++c->launches;
+    key_combine_kernel<<<dim3((n + TPB - 1) / TPB, L * (L + 1)), TPB, 0, c->stream>>>(
+        seed, step, TAG_KEY_A, g, c->logn, L, sk->s_ntt, key, c->mt, pmod); ++c->launches;
   }
   e = cudaStreamSynchronize(c->stream);
   if (e) return fail(hd_fail(HD_E_CUDA, cudaGetErrorString(e)));
@@ -432,4 +464,127 @@ extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, c
   cudaFree(dsc);
   if (!s && written) *written = nsc;
   return s;
+}
+
+// ---------------------------------------------------------------------------
+// Encrypted-database mode (NEXT-1, R26): public key, relinearisation key, public-key
+// encryption of batches of plaintext rows (the enroller's diagonals).
+// ---------------------------------------------------------------------------
+static RowMap limb_rows(int L, uint32_t gsize, uint64_t gstride) {
+  RowMap rm{};
+  rm.gsize = gsize;
+  rm.gstride = gstride;
+  rm.mdiv = 1;
+  rm.mlen = L;
+  for (int l = 0; l < L; l++) rm.midx[l] = (uint8_t)l;
+  return rm;
+}
+
+extern "C" hd_status hd_public_keygen(hd_context *c, const hd_secret_key *sk, hd_public_key **out) {
+  if (!c || !sk || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  HD_CUDA(cudaSetDevice(c->device));
+  const int n = c->n, L = c->L;
+  hd_public_key *pk = new hd_public_key{c, nullptr};
+  if (cudaMalloc(&pk->pk, (size_t)2 * L * n * 8) != cudaSuccess) {
+    delete pk;
+    return hd_fail(HD_E_CAPACITY, "public key alloc");
+  }
+  const uint64_t seed = c->params.seed;
+  pk_error_kernel<<<(n + TPB - 1) / TPB, TPB, 0, c->stream>>>(seed, n, L, pk->pk, c->mt); ++c->launches;
+  hd_status s = ntt_rows(c, pk->pk, L, limb_rows(L, 1u << 30, 0), false);
+  if (!s) {
+    pk_combine_kernel<<<dim3((n + TPB - 1) / TPB, L), TPB, 0, c->stream>>>(seed, n, L, sk->s_ntt, pk->pk, c->mt); ++c->launches;
+    if (cudaStreamSynchronize(c->stream) != cudaSuccess) s = hd_fail(HD_E_CUDA, "public keygen");
+  }
+  if (s) {
+    hd_public_key_destroy(pk);
+    return s;
+  }
+  *out = pk;
+  return HD_OK;
+}
+
+extern "C" void hd_public_key_destroy(hd_public_key *pk) {
+  if (!pk) return;
+  cudaFree(pk->pk);
+  delete pk;
+}
+
+extern "C" hd_status hd_public_key_export(const hd_public_key *pk, uint64_t *dst, size_t cap) {
+  if (!pk || !dst) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  const size_t need = (size_t)2 * pk->ctx->L * pk->ctx->n;
+  if (cap < need) return hd_fail(HD_E_INVALID_ARG, "capacity too small");
+  HD_CUDA(cudaMemcpy(dst, pk->pk, need * 8, cudaMemcpyDeviceToHost));
+  return HD_OK;
+}
+
+extern "C" hd_status hd_public_key_import(hd_context *c, const uint64_t *src, size_t count, hd_public_key **out) {
+  if (!c || !src || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  *out = nullptr;
+  const size_t need = (size_t)2 * c->L * c->n;
+  if (count != need) return hd_fail(HD_E_FORMAT, "public key must hold 2 L n residues");
+  for (size_t i = 0; i < need; i++)
+    if (src[i] >= c->mod[(i / c->n) % c->L]) return hd_fail(HD_E_FORMAT, "public key residue out of range");
+  hd_public_key *pk = new hd_public_key{c, nullptr};
+  if (cudaMalloc(&pk->pk, need * 8) != cudaSuccess) {
+    delete pk;
+    return hd_fail(HD_E_CAPACITY, "public key alloc");
+  }
+  if (cudaMemcpy(pk->pk, src, need * 8, cudaMemcpyHostToDevice) != cudaSuccess) {
+    hd_public_key_destroy(pk);
+    return hd_fail(HD_E_CUDA, "public key copy");
+  }
+  *out = pk;
+  return HD_OK;
+}
+
+extern "C" hd_status hd_relin_keygen(hd_context *c, const hd_secret_key *sk, hd_eval_keys *evk) {
+  if (!c || !sk || !evk) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  if (evk->ctx != c || sk->ctx != c) return hd_fail(HD_E_STATE, "objects from another context");
+  if (evk->find(HD_RELIN_STEP)) return HD_OK;  // already present
+  HD_CUDA(cudaSetDevice(c->device));
+  const int n = c->n, L = c->L;
+  const size_t cnt = evk->steps.size(), ke = (size_t)L * 2 * (L + 1) * n;
+  uint64_t *keys = nullptr;
+  if (cudaMalloc(&keys, ke * (cnt + 1) * 8) != cudaSuccess) return hd_fail(HD_E_CAPACITY, "relinearisation key alloc");
+  if (cnt) HD_CUDA(cudaMemcpyAsync(keys, evk->keys, ke * cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
+  uint64_t *key = keys + ke * cnt;
+  const uint64_t seed = c->params.seed;
+  key_error_kernel<<<dim3((n + TPB - 1) / TPB, L), TPB, 0, c->stream>>>(seed, 0, TAG_RLK_E, n, L, key, c->mt); ++c->launches;
+  RowMap rk = limb_rows(L + 1, L + 1, (uint64_t)2 * (L + 1) * n);  // rows (d, l) of the b halves
+  hd_status s = ntt_rows(c, key, L * (L + 1), rk, false);
+  if (s) {
+    cudaFree(keys);
+    return s;
+  }
+  InvTab2 pmod{};
+  for (int l = 0; l < L; l++) pmod.w[l] = c->mod[L] % c->mod[l];
+  key_combine_kernel<<<dim3((n + TPB - 1) / TPB, L * (L + 1)), TPB, 0, c->stream>>>(
+      seed, 0, TAG_RLK_A, 0, c->logn, L, sk->s_ntt, key, c->mt, pmod); ++c->launches;
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
+    cudaFree(keys);
+    return hd_fail(HD_E_CUDA, "relinearisation keygen");
+  }
+  cudaFree(evk->keys);
+  evk->keys = keys;
+  evk->key_elems = ke;
+  evk->steps.push_back(HD_RELIN_STEP);
+  return HD_OK;
+}
+
+hd_status pk_encrypt_rows(hd_context *c, const hd_public_key *pk, uint64_t *ct, size_t ct_stride, uint32_t count,
+                          uint64_t enc_seed, uint32_t obj0, uint64_t *V, uint64_t *E0) {
+  if (count == 0) return HD_OK;
+  const int n = c->n, L = c->L;
+  pke_draw_kernel<<<dim3((n + TPB - 1) / TPB, count), TPB, 0, c->stream>>>(enc_seed, obj0, n, L, ct, ct_stride, V, E0,
+                                                                           c->mt); ++c->launches;
+  hd_status s = ntt_rows(c, V, count * L, limb_rows(L, 1u << 30, 0), false);
+  if (!s) s = ntt_rows(c, E0, count * L, limb_rows(L, 1u << 30, 0), false);
+  if (!s) s = ntt_rows(c, ct + (size_t)L * n, count * L, limb_rows(L, L, ct_stride), false);
+  if (s) return s;
+  pke_combine_kernel<<<dim3((n + TPB - 1) / TPB, count * L), TPB, 0, c->stream>>>(n, L, pk->pk, ct, ct_stride, V, E0,
+                                                                                 c->mt); ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  return HD_OK;
 }

@@ -164,6 +164,15 @@ struct hd_eval_keys {
   }
 };
 
+// Public key (encrypted-database mode, R26): pk = (b, a) over the L ciphertext moduli.
+struct hd_public_key {
+  hd_context *ctx;
+  uint64_t *pk;  // [2][L][n], NTT form
+};
+
+// Relinearisation key (s^2 -> s) stored in hd_eval_keys under this reserved step.
+constexpr int32_t HD_RELIN_STEP = 0;
+
 struct hd_ciphertext {
   hd_context *ctx;
   uint32_t limbs;
@@ -179,10 +188,13 @@ struct hd_database {
   uint32_t N, M, n1, A_loc;
   std::vector<int32_t> js;       // giant steps j (contiguous, non-empty ranges)
   std::vector<int32_t> pre;      // preRot(j) per j
-  uint64_t *D = nullptr;         // [A_loc][N][L][n] diagonal plaintexts
+  uint64_t *D = nullptr;         // [A_loc][N][L][n] diagonal plaintexts, or
+                                 // [A_loc][N][2][L][n] diagonal ciphertexts (encrypted)
+  bool encrypted = false;        // encrypted-database mode (NEXT-1, R26)
+  uint32_t spoly = 2;            // polynomials per giant-step sum: 2, or 3 (degree 2) encrypted
   // query workspaces (allocated at enrollment; reused by every hd_query)
   uint64_t *r = nullptr;         // [n1][2][L][n] baby steps
-  uint64_t *S = nullptr;         // [A_loc][nj][2][L][n] giant-step sums
+  uint64_t *S = nullptr;         // [A_loc][nj][spoly][L][n] giant-step sums
   uint64_t *Sp = nullptr;        // [A_loc][nj][2][L-1][n] rescaled
   uint64_t *y = nullptr;         // [A_loc][2][L-1][n]
   uint64_t *outbuf = nullptr;    // [A_loc][2][L-1][n] folded outputs
@@ -199,9 +211,11 @@ struct hd_database {
   cudaEvent_t ev_in = nullptr, ev_mac = nullptr, ev_done = nullptr, ev_sfree[2] = {nullptr, nullptr};
   // rotation-key tables for the (db, evk) pair last used: [0, n1-1) baby i = 1..n1-1,
   // [n1-1, n1-1+nj) giant j (NULL key when preRot = 0), [n1-1+nj] fold
+  // [n1+nj] relinearisation key (encrypted mode), gal 1 (identity permutation)
   const hd_eval_keys *keyed_for = nullptr;
   const uint64_t **kptr = nullptr;
   uint32_t *gal = nullptr;
+  uint32_t relin_chunk = 1;      // giant-step sums relinearised per batch (encrypted mode)
   size_t bytes = 0;
   bool has_run = false;
 };

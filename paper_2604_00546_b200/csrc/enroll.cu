@@ -225,9 +225,13 @@ extern "C" void hd_database_destroy(hd_database *db) {
   delete db;
 }
 
-extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num_vectors, uint32_t vector_dim,
-                               uint32_t n1, uint32_t agg_begin, uint32_t agg_end, hd_database **out) {
+// pk == NULL: plaintext diagonals (the north-star pt x ct scan); else every diagonal
+// plaintext is encrypted under pk (encrypted-database mode, NEXT-1, R26).
+static hd_status enroll_impl(hd_context *c, const hd_public_key *pk, uint64_t enc_seed, const float *vectors,
+                             uint64_t num_vectors, uint32_t vector_dim, uint32_t n1, uint32_t agg_begin,
+                             uint32_t agg_end, hd_database **out) {
   if (!c || !vectors || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  if (pk && pk->ctx != c) return hd_fail(HD_E_STATE, "public key from another context");
   *out = nullptr;
   hd_layout lay;
   hd_status s = layout_make(c, num_vectors, vector_dim, n1, &lay);
@@ -244,6 +248,8 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
   db->M = lay.blocks_m;
   db->n1 = n1;
   db->A_loc = agg_end - agg_begin;
+  db->encrypted = pk != nullptr;
+  db->spoly = pk ? 3 : 2;
   const int N = (int)db->N, L = c->L, n = c->n, ns = c->ns;
   for (int j = lay.giant_min; j <= lay.giant_max; j++) {
     int lo = std::max(0, -j * (int)n1 - N / 2), hi = std::min((int)n1 - 1, N / 2 - 1 - j * (int)n1);
@@ -263,15 +269,23 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
   size_t dig_e = A * (L - 1) * (L - 1) * n;
   size_t u_e = A * 2 * L * n;
   size_t tmp_e = std::max({A * 2 * (L - 1) * n, rescale_chunk * 2 * n, (size_t)L * n});
+  const size_t sL = (size_t)db->spoly * L * n;  // one giant-step sum
+  if (pk) {  // relinearisation of A sums at a time at L limbs (ModUp digits, KIP, ModDown)
+    db->relin_chunk = (uint32_t)A;
+    dig_e = std::max(dig_e, A * L * L * n);
+    u_e = std::max(u_e, A * 2 * (L + 1) * n);
+    tmp_e = std::max(tmp_e, A * 2 * L * n);
+  }
+  const size_t dstride = (pk ? 2 : 1) * (size_t)L * n;  // one diagonal (pt, or ct)
   size_t tmp2_e = 1;
   size_t digb_e = (size_t)L * L * n, ub_e = nb * 2 * (L + 1) * n, tmpb_e = std::max(nb * 2 * L * n, (size_t)L * n);
   db->rescale_chunk = (uint32_t)rescale_chunk;
   struct Req {
     void **p;
     size_t bytes;
-  } reqs[] = {{(void **)&db->D, A * N * (size_t)L * n * 8},
+  } reqs[] = {{(void **)&db->D, A * N * dstride * 8},
               {(void **)&db->r, (size_t)n1 * ctL * 8},
-              {(void **)&db->S, A * nj * ctL * 8},
+              {(void **)&db->S, A * nj * sL * 8},
               {(void **)&db->Sp, A * nj * ct1 * 8},
               {(void **)&db->y, A * ct1 * 8},
               {(void **)&db->outbuf, A * ct1 * 8},
@@ -279,7 +293,7 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
               {(void **)&db->u, u_e * 8},
               {(void **)&db->tmp, tmp_e * 8},
               {(void **)&db->tmp2, tmp2_e * 8},
-              {(void **)&db->S2, A * nj * ctL * 8},
+              {(void **)&db->S2, A * nj * sL * 8},
               {(void **)&db->dig_b, digb_e * 8},
               {(void **)&db->u_b, ub_e * 8},
               {(void **)&db->tmp_b, tmpb_e * 8}};
@@ -314,11 +328,16 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
   if (!e) e = cudaMalloc(&U, rows_per_agg * N * 8);
   if (!e) e = cudaMalloc(&re, (size_t)KB * ns * 8);
   if (!e) e = cudaMalloc(&im, (size_t)KB * ns * 8);
+  uint64_t *V = nullptr, *E0 = nullptr;  // public-key encryption scratch (v, e0 of a batch)
+  if (!e && pk) e = cudaMalloc(&V, (size_t)KB * L * n * 8);
+  if (!e && pk) e = cudaMalloc(&E0, (size_t)KB * L * n * 8);
   auto cleanup = [&]() {
     cudaFree(dv);
     cudaFree(U);
     cudaFree(re);
     cudaFree(im);
+    cudaFree(V);
+    cudaFree(E0);
   };
   if (e) {
     cleanup();
@@ -337,12 +356,16 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
     }
     if ((s = normalize_on_device(c, dv, rows, N, U))) break;
     if ((s = check_flag(c))) break;
-    uint64_t *Da = db->D + (size_t)(a - agg_begin) * N * L * n;
+    uint64_t *Da = db->D + (size_t)(a - agg_begin) * N * dstride;
     for (int k0 = 0; k0 < N && !s; k0 += KB) {
       int kb = std::min(KB, N - k0);
       pack_kernel<<<dim3((ns + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(U, (long long)v0, (long long)num_vectors, N,
                                                                          db->M, n1, a, k0, ns, re, im); ++c->launches;
-      s = encode_batch(c, re, im, kb, delta, L, Da + (size_t)k0 * L * n, (size_t)L * n);
+      // plaintext rows (into c0 of each diagonal ciphertext in encrypted mode)
+      s = encode_batch(c, re, im, kb, delta, L, Da + (size_t)k0 * dstride, dstride);
+      if (!s && pk)  // Enc_pk with object id a N + k (R26), the oracle's or_enroll_aggregate_encrypted
+        s = pk_encrypt_rows(c, pk, Da + (size_t)k0 * dstride, dstride, (uint32_t)kb, enc_seed,
+                            (uint32_t)((uint64_t)a * N + k0), V, E0);
     }
     if (!s) s = check_flag(c);
   }
@@ -353,4 +376,16 @@ extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num
   }
   *out = db;
   return HD_OK;
+}
+
+extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num_vectors, uint32_t vector_dim,
+                               uint32_t n1, uint32_t agg_begin, uint32_t agg_end, hd_database **out) {
+  return enroll_impl(c, nullptr, 0, vectors, num_vectors, vector_dim, n1, agg_begin, agg_end, out);
+}
+
+extern "C" hd_status hd_enroll_encrypted(hd_context *c, const hd_public_key *pk, const float *vectors,
+                                         uint64_t num_vectors, uint32_t vector_dim, uint32_t n1, uint32_t agg_begin,
+                                         uint32_t agg_end, uint64_t enc_seed, hd_database **out) {
+  if (!pk) return hd_fail(HD_E_INVALID_ARG, "null public key");
+  return enroll_impl(c, pk, enc_seed, vectors, num_vectors, vector_dim, n1, agg_begin, agg_end, out);
 }

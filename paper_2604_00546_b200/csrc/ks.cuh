@@ -31,8 +31,16 @@ struct MacPlan {
   int jmin, nj;        // valid giant steps j = js[0..nj)
   const int32_t *js;   // host
 };
+// Encrypted diagonals (NEXT-1): degree-2 sums S3 [a][j][3][L][n] of Dct [a][k][2][L][n].
+hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint64_t *S3, uint32_t A_loc, int n1,
+                     int N, const std::vector<int32_t> &js);
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
                   const std::vector<int32_t> &js);
+
+// Public-key encryption of count ciphertexts in place (c0 of ct_x = ct + x*ct_stride holds
+// the plaintext on entry); object ids obj0 + x; V, E0: count*L*n scratch each (client.cu).
+hd_status pk_encrypt_rows(hd_context *c, const hd_public_key *pk, uint64_t *ct, size_t ct_stride, uint32_t count,
+                          uint64_t enc_seed, uint32_t obj0, uint64_t *V, uint64_t *E0);
 
 // encode (enroll.cu)
 hd_status encode_batch(hd_context *c, double *re, double *im, uint32_t B, double delta, int nlimbs,

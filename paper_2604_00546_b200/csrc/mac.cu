@@ -185,7 +185,73 @@ __global__ void __launch_bounds__(MAC_TPB) mac_cs_kernel(const uint64_t *__restr
     }
   }
 }
+
+// ---- encrypted diagonals (NEXT-1, R26): degree-2 MAC ---------------------------------
+// S_{a,j} = sum_i r[i] (x) Dct[a][k(j,i)], the tensor of (r0, r1) and
+// (D0, D1): d0 += r0 D0, d1 += r0 D1 + r1 D0, d2 += r1 D1, each in a carry-save
+// accumulator (folded every 4 steps: d1 takes 4 mid terms per step), banked into a
+// reduced partial sum every 64 steps so any n1 and partial giant-step ranges are safe.
+// One (a, j, limb, 128-coefficient tile) per CTA; S: [a][j][3][L][n].
+__global__ void __launch_bounds__(MAC_TPB) mac_ct_kernel(const uint64_t *__restrict__ D,
+                                                          const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
+                                                          int n1, int N, int L, int logn, int jmin, int nj,
+                                                          ModTab mt) {
+  const int n = 1 << logn;
+  const uint32_t a = blockIdx.x;
+  const uint32_t t = blockIdx.y * MAC_TPB + threadIdx.x;
+  const int m = blockIdx.z / nj, jj = blockIdx.z % nj;
+  const int j = jmin + jj;
+  const size_t ls = (size_t)L * n, ds = 2 * ls;
+  const uint64_t *Da = D + (size_t)a * N * ds + (size_t)m * n + t;
+  const uint64_t *rr = r + (size_t)m * n + t;
+  const int i_lo = max(0, -j * n1 - N / 2), i_hi = min(n1 - 1, N / 2 - 1 - j * n1);
+  const uint64_t q = mt.q[m], bar = mt.bar[m], r64 = mt.r64[m], r64s = mt.r64s[m];
+  CsAcc acc[3] = {CsAcc{0, 0, 0, 0}, CsAcc{0, 0, 0, 0}, CsAcc{0, 0, 0, 0}};
+  uint64_t part[3] = {0, 0, 0};
+  auto bank = [&]() {
+#pragma unroll
+    for (int e = 0; e < 3; e++) {
+      cs_fold(acc[e]);
+      part[e] = addmod(part[e], reduce128(acc[e].hi + acc[e].cnt, acc[e].lo, q, bar, r64, r64s), q);
+      acc[e] = CsAcc{0, 0, 0, 0};
+    }
+  };
+  for (int i = i_lo, c = 0; i <= i_hi; i++, c++) {
+    const int k = (j * n1 + i) & (N - 1);
+    const uint64_t *dk = Da + (size_t)k * ds;
+    const uint64_t d0 = ld_stream(dk), d1 = ld_stream(dk + ls);
+    const uint64_t r0 = __ldg(rr + (size_t)(2 * i) * ls), r1 = __ldg(rr + (size_t)(2 * i + 1) * ls);
+    const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1, r11 = (uint32_t)(r1 >> 32);
+    const uint32_t a00 = (uint32_t)d0, a01 = (uint32_t)(d0 >> 32), a10 = (uint32_t)d1, a11 = (uint32_t)(d1 >> 32);
+    cs_mac(acc[0], r00, r01, a00, a01);
+    cs_mac(acc[1], r00, r01, a10, a11);
+    cs_mac(acc[1], r10, r11, a00, a01);
+    cs_mac(acc[2], r10, r11, a10, a11);
+    if ((c & 3) == 3) {
+      cs_fold(acc[0]);
+      cs_fold(acc[1]);
+      cs_fold(acc[2]);
+    }
+    if ((c & 63) == 63) bank();
+  }
+  bank();
+  uint64_t *Sa = S + ((size_t)a * nj + jj) * 3 * ls + (size_t)m * n + t;
+#pragma unroll
+  for (int e = 0; e < 3; e++) Sa[(size_t)e * ls] = part[e];
+}
 }  // namespace
+
+hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint64_t *S3, uint32_t A_loc, int n1,
+                     int N, const std::vector<int32_t> &js) {
+  if (js.empty() || A_loc == 0) return HD_OK;
+  if (c->n % MAC_TPB) return hd_fail(HD_E_PARAMS, "ring too small for the encrypted MAC");
+  const int jmin = js.front(), nj = (int)js.size();
+  const dim3 grid(A_loc, c->n / MAC_TPB, c->L * nj);
+  mac_ct_kernel<<<grid, MAC_TPB, 0, c->stream>>>(Dct, r, S3, n1, N, c->L, c->logn, jmin, nj, c->mt);
+  ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  return HD_OK;
+}
 
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
                   const std::vector<int32_t> &js) {

@@ -19,7 +19,7 @@ static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
   hd_context *c = db->ctx;
   if (db->keyed_for == evk && db->kptr) return HD_OK;
   const int n1 = (int)db->n1, nj = (int)db->js.size();
-  const size_t cnt = (size_t)(n1 - 1) + nj + 1;
+  const size_t cnt = (size_t)(n1 - 1) + nj + 1 + (db->encrypted ? 1 : 0);
   std::vector<const uint64_t *> kp(cnt, nullptr);
   std::vector<uint32_t> gl(cnt, 1);
   auto need = [&](int32_t step, size_t slot) -> hd_status {
@@ -34,7 +34,13 @@ static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
     if ((s = need(i, i - 1))) return s;
   for (int jj = 0; jj < nj; jj++)
     if (db->pre[jj] && (s = need(db->pre[jj], n1 - 1 + jj))) return s;
-  if ((s = need(c->ns - (int)db->N, cnt - 1))) return s;
+  const size_t fold_slot = (size_t)(n1 - 1) + nj;
+  if ((s = need(c->ns - (int)db->N, fold_slot))) return s;
+  if (db->encrypted) {  // relinearisation key: identity permutation (g = 1)
+    kp[fold_slot + 1] = evk->find(HD_RELIN_STEP);
+    if (!kp[fold_slot + 1])
+      return hd_fail(HD_E_MISSING_KEY, "missing relinearisation key (hd_relin_keygen) for an encrypted database");
+  }
   if (!db->kptr) {
     HD_CUDA(cudaMalloc(&db->kptr, cnt * sizeof(uint64_t *)));
     HD_CUDA(cudaMalloc(&db->gal, cnt * sizeof(uint32_t)));
@@ -90,19 +96,37 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
   }
   cudaEventRecord(E[1], sa);
   // ---- MAC ----
-  if ((s = mac_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js))) return s;
+  if (db->encrypted) {
+    if ((s = mac_ct_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js))) return s;
+  } else if ((s = mac_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js))) {
+    return s;
+  }
   cudaEventRecord(E[2], sa);
   HD_CUDA(cudaEventRecord(db->ev_mac, sa));
   // ---------------- stream B ----------------
   HD_CUDA(cudaStreamWaitEvent(sb, db->ev_mac, 0));
   c->stream = sb;
   cudaEventRecord(E[3], sb);
+  const size_t sL = (size_t)db->spoly * L * n;  // one giant-step sum
+  if (db->encrypted) {
+    // ---- Relinearize every degree-2 S_{a,j}: (d0, d1) += KeySwitch_{s^2->s}(d2) ----
+    const uint32_t total = A * nj;
+    const size_t rslot = (size_t)(n1 - 1) + nj + 1;
+    for (uint32_t b0 = 0; b0 < total; b0 += db->relin_chunk) {
+      const uint32_t B = std::min(db->relin_chunk, total - b0);
+      uint64_t *S3 = Sbuf + (size_t)b0 * sL;
+      if ((s = ks_modup(c, S3 + (size_t)2 * L * n, sL, B, L, db->dig, db->tmp))) return s;
+      if ((s = ks_kip(c, db->dig, S3 + (size_t)2 * L * n, sL, B, 1, L, db->kptr + rslot, db->gal + rslot, db->u)))
+        return s;
+      if ((s = ks_moddown(c, db->u, B, 1, L, db->gal + rslot, nullptr, 0, S3, sL, true, db->tmp))) return s;
+    }
+  }
   {
     // ---- rescale every S_{a,j} ----
     const uint32_t total = A * nj;
     for (uint32_t b0 = 0; b0 < total; b0 += db->rescale_chunk) {
       uint32_t B = std::min(db->rescale_chunk, total - b0);
-      if ((s = ks_rescale(c, Sbuf + (size_t)b0 * ctL, ctL, B, L, db->Sp + (size_t)b0 * ct1, ct1, db->tmp, db->tmp2)))
+      if ((s = ks_rescale(c, Sbuf + (size_t)b0 * sL, sL, B, L, db->Sp + (size_t)b0 * ct1, ct1, db->tmp, db->tmp2)))
         return s;
     }
   }
@@ -265,7 +289,8 @@ extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t ag
       break;
     case 1:
       if (jj < 0 || jj >= nj) return hd_fail(HD_E_INVALID_ARG, "giant index");
-      src = (((db->qcount - 1) & 1) ? db->S2 : db->S) + (a * nj + jj) * ctL, len = ctL;
+      len = (size_t)db->spoly * L * n;  // encrypted: (d0, d1) relinearised, d2 as accumulated
+      src = (((db->qcount - 1) & 1) ? db->S2 : db->S) + (a * nj + jj) * len;
       break;
     case 2:
       if (jj < 0 || jj >= nj) return hd_fail(HD_E_INVALID_ARG, "giant index");
@@ -276,7 +301,8 @@ extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t ag
       break;
     case 4:
       if (index < 0 || index >= (int)db->N) return hd_fail(HD_E_INVALID_ARG, "diagonal index");
-      src = db->D + (a * db->N + index) * ptL, len = ptL;
+      len = (db->encrypted ? 2 : 1) * ptL;  // plaintext, or the diagonal ciphertext
+      src = db->D + (a * db->N + index) * len;
       break;
     default:
       return hd_fail(HD_E_INVALID_ARG, "stage");
