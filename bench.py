@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--db", default="plain", choices=["plain", "encrypted"],
+                    help="plaintext diagonals (the north-star scan) or the encrypted-database mode (NEXT-1)")
     return ap.parse_args()
 
 
@@ -221,8 +223,18 @@ def main():
     # ---- setup (untimed): keys on rank 0 -> NCCL broadcast; local enrollment of this shard ----
     _, q, _ = make_dataset(16, cfg.dim, cfg.data_seed)  # query only (rows drawn per shard below)
     steps = ctx.rotation_steps(cfg.dim, cfg.n1)
+    enc_db = args.db == "encrypted"
     if rank == 0:
         sk, evk = ctx.keygen(steps)
+        if enc_db:  # relinearisation key travels with the eval keys (reserved step 0)
+            ctx.relin_keygen(sk, evk)
+    pk = None
+    if enc_db:  # public key from rank 0 to every enroller
+        pkt = torch.from_numpy(ctx.public_key_export(ctx.public_keygen(sk)).view(np.uint8).ravel()).to(dev) \
+            if rank == 0 else torch.empty(2 * cfg.limbs * (1 << cfg.log_n) * 8, dtype=torch.uint8, device=dev)
+        if world > 1:
+            dist.broadcast(pkt, 0)
+        pk = ctx.public_key_import(pkt.cpu().numpy().view(np.uint64))
     if world > 1:
         kb = torch.from_numpy(ctx.eval_keys_export(evk)).to(dev) if rank == 0 else None
         nbytes = torch.tensor([kb.numel() if rank == 0 else 0], device=dev)
@@ -233,7 +245,7 @@ def main():
         del kb
     v0, v1 = hdd.rows_of_aggregates(a0, a1, per, cfg.num_vectors)
     rows = dataset_rows(cfg.num_vectors, cfg.dim, cfg.data_seed, v0, v1)
-    db = enroll_rows(hd, ctx, rows, v0, cfg, a0, a1)
+    db = enroll_rows(hd, ctx, rows, v0, cfg, a0, a1, pk)
     del rows
     # ---- the query: encrypted on rank 0, exported into a device buffer (NCCL-broadcast each step) ----
     ct_bytes = 0
@@ -333,13 +345,14 @@ def main():
     # ---- roofline of the dominant kernel (MAC, HBM-bound) ----
     L, n, N = cfg.limbs, 1 << cfg.log_n, cfg.dim
     nj = len(db_js(cfg))
-    mac_bytes = nloc * N * L * n * 8 + cfg.n1 * 2 * L * n * 8 + nloc * nj * 2 * L * n * 8
+    dpoly, spoly = (2, 3) if enc_db else (1, 2)  # diagonal / giant-sum polynomials
+    mac_bytes = nloc * N * dpoly * L * n * 8 + cfg.n1 * 2 * L * n * 8 + nloc * nj * spoly * L * n * 8
     mac_avg_ms = statistics.mean(mac_ms)
     peak, peak_src = peaks()
     achieved = mac_bytes / (mac_avg_ms / 1e3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "mac_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and not enc_db:
         try:
             traffic = json.load(open(tf)).get(cfg.name)
         except Exception:  # noqa: BLE001
@@ -368,8 +381,8 @@ def main():
                      "avg_launch_ms": kip_ms, "timing": "CUDA events around the launch, serial pass after the timed region"}
     # ---- whole-query compulsory bytes against the step time ----
     nnz = sum(1 for j in db_js(cfg) if ((cfg.n1 * j) % N + N) % N != 0)
-    q_bytes = (nloc * N * L * n * 8 + (cfg.n1 - 1) * key_bytes + (nnz + 1) * (L - 1) * 2 * L * n * 8
-               + 2 * L * n * 8 + nloc * 2 * (L - 1) * n * 8)
+    q_bytes = (nloc * N * dpoly * L * n * 8 + (cfg.n1 - 1) * key_bytes + (nnz + 1) * (L - 1) * 2 * L * n * 8
+               + 2 * L * n * 8 + nloc * 2 * (L - 1) * n * 8 + (nj * key_bytes if enc_db else 0))
     query_roofline = {"bytes": q_bytes, "achieved": q_bytes / (ms_per_step / 1e3) / 1e9, "peak": peak,
                       "unit": "GB/s", "frac": q_bytes / (ms_per_step / 1e3) / 1e9 / peak,
                       "roofline_queries_per_s": peak * 1e9 / q_bytes}  # every rank serves every query
@@ -377,7 +390,9 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64 (RNS residues, 64-bit modular integer arithmetic)",
             "data": "synthetic (P:L2175-2179 generator, seeded)",
-            "config": cfg_dict(cfg, world, "fixed 2^20 database sharded by aggregate"),
+            "config": dict(cfg_dict(cfg, world, "fixed 2^20 database sharded by aggregate"),
+                           database="encrypted diagonals (NEXT-1: degree-2 MAC + relinearisation)" if enc_db
+                           else "plaintext diagonals (north-star pt x ct scan)"),
             "phase_ms": {"baby": phase[0] / args.steps, "mac": phase[1] / args.steps,
                          "rescale": phase[2] / args.steps, "giant": phase[3] / args.steps,
                          "fold": phase[4] / args.steps, "baby_kip": phase[5] / args.steps,
@@ -416,15 +431,25 @@ def db_js(cfg):
     return list(range((-(N // 2)) // n1, (N // 2 - 1) // n1 + 1))
 
 
-def enroll_rows(hd, ctx, rows, v0, cfg, a0, a1):
+DB_ENC_SEED = 4242  # encrypted-database mode: Philox key of the enroller's encryption
+
+
+def enroll_rows(hd, ctx, rows, v0, cfg, a0, a1, pk=None):
     """hd_enroll reads rows [a0*per, a1*per) of the array it is given (indexed from vector 0):
     pass a pointer shifted back by v0 rows so this rank only materialises its own shard."""
     import ctypes as C
     out = C.c_void_p()
     ptr = rows.ctypes.data - v0 * cfg.dim * 4
-    hd._check("hd_enroll", hd.load().hd_enroll(ctx.h, C.c_void_p(ptr), cfg.num_vectors, cfg.dim, cfg.n1, a0, a1,
-                                               C.byref(out)))
-    return hd.Database(out.value, ctx)
+    if pk is None:
+        hd._check("hd_enroll", hd.load().hd_enroll(ctx.h, C.c_void_p(ptr), cfg.num_vectors, cfg.dim, cfg.n1, a0, a1,
+                                                   C.byref(out)))
+        return hd.Database(out.value, ctx)
+    hd._check("hd_enroll_encrypted", hd.load().hd_enroll_encrypted(
+        ctx.h, pk.h, C.c_void_p(ptr), cfg.num_vectors, cfg.dim, cfg.n1, a0, a1, C.c_uint64(DB_ENC_SEED),
+        C.byref(out)))
+    db = hd.Database(out.value, ctx)
+    db.encrypted = True
+    return db
 
 
 if __name__ == "__main__":

@@ -118,3 +118,14 @@ def test_missing_relinearisation_key_and_public_key_roundtrip(toy):
     bad[0, 0, 0] = np.uint64(2 ** 63)
     with pytest.raises(hd.HDError):
         ctx.public_key_import(bad)
+
+
+def test_generic_degree2_mac_bit_exact(monkeypatch):
+    """The general degree-2 MAC (partial giant-step ranges, any n1; forced with
+    HD_MAC_VARIANT=g) gives the same bits as the streaming one and the oracle."""
+    monkeypatch.setenv("HD_MAC_VARIANT", "g")
+    run = EncRun(CONFIGS["C1"])
+    cfg, o = run.cfg, run.o
+    out = o.scan_aggregate_ct(run.oracle_r(), cfg.n1, cfg.dim, run.oracle_Dct(0), run.ok_steps, run.ok_keys,
+                              run.orlk)
+    assert (run.ctx.ciphertext_residues(run.outs[0]) == out).all()
