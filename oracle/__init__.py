@@ -271,6 +271,54 @@ class Oracle:
             _p(steps), len(steps), _p(keys), _p(out), _p(y)))
         return (out, y) if want_y else out
 
+    # -- flat pre-rotated layout (NEXT-2, R27) ------------------------------------
+    def enroll_slots_flat(self, U, u_first, num_vectors, n1, agg, k):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        z = np.zeros(self.ns, np.float64)
+        _check("enroll_slots_flat", lib().or_enroll_slots_flat(
+            C.byref(self.p), _p(U), C.c_int64(u_first), C.c_int64(U.shape[0]), C.c_int64(num_vectors),
+            U.shape[1], n1, C.c_int64(agg), k, _p(z)))
+        return z
+
+    def enroll_aggregate_flat(self, U, u_first, num_vectors, n1, agg):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        D = u64((U.shape[1], self.L, self.n))
+        _check("enroll_aggregate_flat", lib().or_enroll_aggregate_flat(
+            C.byref(self.p), _p(U), C.c_int64(u_first), C.c_int64(U.shape[0]), C.c_int64(num_vectors),
+            U.shape[1], n1, C.c_int64(agg), _p(D)))
+        return D
+
+    def rotation_steps_flat(self, N, n1):
+        cap = self.ns
+        steps = np.zeros(cap, np.int32)
+        cnt = C.c_int32()
+        _check("rotation_steps_flat", lib().or_rotation_steps_flat(C.byref(self.p), N, n1, _p(steps), cap,
+                                                                   C.byref(cnt)))
+        return [int(s) for s in steps[:cnt.value]]
+
+    def giant_sum_flat(self, r, n1, N, Dagg, j):
+        S = u64((2, self.L, self.n))
+        rc = lib().or_giant_sum_flat(C.byref(self.p), _p(np.ascontiguousarray(r)), n1, N,
+                                     _p(np.ascontiguousarray(Dagg)), j, _p(S))
+        if rc == OR_E_RANGE:
+            return None
+        _check("giant_sum_flat", rc)
+        return S
+
+    def scan_aggregate_flat(self, r, n1, N, Dagg, steps, keys):
+        out = u64((2, self.L - 1, self.n))
+        _check("scan_aggregate_flat", lib().or_scan_aggregate_flat(
+            C.byref(self.p), _p(np.ascontiguousarray(r)), n1, N, _p(np.ascontiguousarray(Dagg)), _p(steps),
+            len(steps), _p(keys), _p(out)))
+        return out
+
+    def decrypt_scores_flat(self, s_ntt, out_ct, N, agg, num_vectors):
+        sc = np.zeros((self.ns // N) * N, dtype=np.float64)
+        _check("decrypt_scores_flat", lib().or_decrypt_scores_flat(
+            C.byref(self.p), _p(s_ntt), _p(np.ascontiguousarray(out_ct)), N, C.c_int64(agg),
+            C.c_int64(num_vectors), _p(sc)))
+        return sc
+
     # -- encrypted-database mode (NEXT-1, R26) ------------------------------------
     def public_key(self, s_ntt):
         pk = u64((2, self.L, self.n))

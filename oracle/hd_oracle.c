@@ -913,6 +913,83 @@ int or_enroll_aggregate_encrypted(const or_params *p, const double *U, int64_t u
 }
 
 /* ------------------------------------------------------------------------ */
+/* Flat pre-rotated layout (NEXT-2, R27: BSGS-RTX-TBE). */
+/* ------------------------------------------------------------------------ */
+/* Slot vector of pre-rotated diagonal k of aggregate agg in the flat HyDia packing
+ * (Eq. equ:diag P:L332-336): M = numSlots/N groups per ciphertext, no gaps,
+ *   diag_k[b N + t] = group_{agg M + b}[t][(t + k) mod N]   (0 beyond the database),
+ * and the enroller's plaintext pre-rotation (Eq. eq:prerotation):
+ *   diag'_k = Rot_{-j n1}(diag_k),  j = floor(k / n1),  i.e. diag'_k[s] = diag_k[s - j n1]. */
+int or_enroll_slots_flat(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                         int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, int32_t k, double *z) {
+  int ns = p->num_slots;
+  if (dim < 2 || n1 < 1 || (dim & (dim - 1)) != 0 || ns % dim != 0) return OR_E_LAYOUT;
+  int N = dim, M = ns / N;
+  int64_t G = (num_vectors + N - 1) / N, A = (G + M - 1) / M;
+  if (agg < 0 || agg >= A || k < 0 || k >= N) return OR_E_ARG;
+  double *diag = calloc((size_t)ns, sizeof(double));
+  for (int b = 0; b < M; b++)
+    for (int t = 0; t < N; t++) {
+      int64_t v = (agg * M + b) * N + t;
+      if (v >= num_vectors) continue;
+      if (v < u_first || v >= u_first + u_count) { free(diag); return OR_E_ARG; }
+      diag[b * N + t] = U[(size_t)(v - u_first) * dim + (t + k) % N];
+    }
+  int sh = (k / n1) * n1; /* Rot_{-j n1} */
+  for (int s = 0; s < ns; s++) z[s] = diag[((s - sh) % ns + ns) % ns];
+  free(diag);
+  return OR_OK;
+}
+
+int or_enroll_aggregate_flat(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                             int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, uint64_t *Dagg) {
+  int ns = p->num_slots;
+  double *z = malloc(sizeof(double) * ns);
+  int rc = OR_OK;
+  for (int k = 0; k < dim && rc == OR_OK; k++) {
+    rc = or_enroll_slots_flat(p, U, u_first, u_count, num_vectors, dim, n1, agg, k, z);
+    if (rc == OR_OK) rc = or_encode(p, z, (double)p->mod[p->L - 1], p->L, Dagg + (size_t)k * p->L * p->n);
+  }
+  free(z);
+  return rc;
+}
+
+/* Keys of the flat schedule: baby {1..n1-1}, giant {j n1 : 1 <= j < ceil(N/n1)}. */
+int or_rotation_steps_flat(const or_params *p, int32_t N, int32_t n1, int32_t *steps, int32_t cap,
+                           int32_t *count) {
+  int ns = p->num_slots, c = 0;
+  char *used = calloc((size_t)ns, 1);
+  for (int i = 1; i < n1 && i < ns; i++) used[i] = 1;
+  for (int j = 1; j * n1 < N; j++) used[(j * n1) % ns] = 1;
+  for (int s = 1; s < ns; s++)
+    if (used[s]) {
+      if (c < cap) steps[c] = s;
+      c++;
+    }
+  free(used);
+  *count = c;
+  return c <= cap ? OR_OK : OR_E_ARG;
+}
+
+/* Decrypt + decode a flat-layout output: score(v) = slot (floor(v/N) mod M) N + (v mod N)
+ * of output floor(v / (M N)). */
+int or_decrypt_scores_flat(const or_params *p, const uint64_t *s_ntt, const uint64_t *out_ct, int32_t N,
+                           int64_t agg, int64_t num_vectors, double *scores /* M N */) {
+  int n = p->n, ell = p->L - 1, ns = p->num_slots, M = ns / N;
+  uint64_t *pt = malloc(sizeof(uint64_t) * (size_t)ell * n);
+  double *z = malloc(sizeof(double) * ns);
+  or_decrypt(p, s_ntt, out_ct, ell, pt);
+  or_decode(p, pt, ell, ldexp(1.0, p->scale_bits), z);
+  for (int b = 0; b < M; b++)
+    for (int t = 0; t < N; t++) {
+      int64_t v = (agg * M + b) * N + t;
+      scores[(size_t)b * N + t] = v < num_vectors ? z[b * N + t] : 0.0;
+    }
+  free(pt); free(z);
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Scan (Alg. sender-bsgs).                                      */
 /* ------------------------------------------------------------------------ */
 static int floordiv(int a, int b) { return (int)floor((double)a / (double)b); }
@@ -1114,13 +1191,13 @@ int or_scan_aggregate(const or_params *p, const uint64_t *r, int32_t n1, int32_t
  * x + ModDown(a)), so the sum differs from or_scan_aggregate only by the rounding of
  * the single ModDown. */
 static int scan_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dagg,
-                        const uint64_t *Dct, const uint64_t *rlk, const int32_t *steps, int32_t nkeys,
+                        const uint64_t *Dct, const uint64_t *rlk, int flat, const int32_t *steps, int32_t nkeys,
                         const uint64_t *keys, uint64_t *out, uint64_t *y_out);
 
 int or_scan_aggregate_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
                               const uint64_t *Dagg, const int32_t *steps, int32_t nkeys,
                               const uint64_t *keys, uint64_t *out, uint64_t *y_out) {
-  return scan_hoisted(p, r, n1, N, Dagg, NULL, NULL, steps, nkeys, keys, out, y_out);
+  return scan_hoisted(p, r, n1, N, Dagg, NULL, NULL, 0, steps, nkeys, keys, out, y_out);
 }
 
 /* Encrypted-database scan (NEXT-1): Alg. sender-bsgs as written, S_j = Relinearize(
@@ -1129,11 +1206,42 @@ int or_scan_aggregate_hoisted(const or_params *p, const uint64_t *r, int32_t n1,
 int or_scan_aggregate_ct(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
                          const uint64_t *rlk, const int32_t *steps, int32_t nkeys, const uint64_t *keys,
                          uint64_t *out, uint64_t *y_out) {
-  return scan_hoisted(p, r, n1, N, NULL, Dct, rlk, steps, nkeys, keys, out, y_out);
+  return scan_hoisted(p, r, n1, N, NULL, Dct, rlk, 0, steps, nkeys, keys, out, y_out);
+}
+
+/* Flat pre-rotated layout (NEXT-2, R27): for j = 0 .. ceil(N/n1)-1,
+ *   S_j = sum_{i < n1, j n1 + i < N} r[i] (.) diag'_{j n1 + i},
+ * rescale, y = sum_j Rot_{j n1}(S'_j) accumulated in Q u {P} as in R23 (the giant
+ * rotation re-aligns the baby component; Rot_{j n1} Rot_{-j n1} = id),
+ * and out = y: no fold (no gaps). */
+int or_scan_aggregate_flat(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dagg,
+                           const int32_t *steps, int32_t nkeys, const uint64_t *keys, uint64_t *out) {
+  return scan_hoisted(p, r, n1, N, Dagg, NULL, NULL, 1, steps, nkeys, keys, out, NULL);
+}
+
+/* S_j of the flat layout (diagonals j n1 + i, i < n1, below N); OR_E_RANGE if empty. */
+int or_giant_sum_flat(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dagg,
+                      int32_t j, uint64_t *S) {
+  int n = p->n, L = p->L;
+  size_t ctsz = (size_t)2 * L * n, ptsz = (size_t)L * n;
+  memset(S, 0, sizeof(uint64_t) * ctsz);
+  if (j < 0 || j * n1 >= N) return OR_E_RANGE;
+  for (int i = 0; i < n1 && j * n1 + i < N; i++) {
+    const uint64_t *diag = Dagg + ptsz * (size_t)(j * n1 + i);
+    for (int pp = 0; pp < 2; pp++)
+      for (int l = 0; l < L; l++) {
+        uint64_t q = p->mod[l];
+        const uint64_t *ri = r + ctsz * i + ((size_t)pp * L + l) * n;
+        uint64_t *acc = S + ((size_t)pp * L + l) * n;
+        const uint64_t *dl = diag + (size_t)l * n;
+        for (int t = 0; t < n; t++) acc[t] = addmod(acc[t], mulmod(ri[t], dl[t], q), q);
+      }
+  }
+  return OR_OK;
 }
 
 static int scan_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dagg,
-                        const uint64_t *Dct, const uint64_t *rlk, const int32_t *steps, int32_t nkeys,
+                        const uint64_t *Dct, const uint64_t *rlk, int flat, const int32_t *steps, int32_t nkeys,
                         const uint64_t *keys, uint64_t *out, uint64_t *y_out) {
   int n = p->n, L = p->L, ell = L - 1;
   size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * ell * n, ext = (size_t)(ell + 1) * n;
@@ -1145,16 +1253,23 @@ static int scan_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32
   uint64_t *perm = malloc(sizeof(uint64_t) * n);
   uint64_t *S3 = Dct ? malloc(sizeof(uint64_t) * (size_t)3 * L * n) : NULL;
   int jmin, jmax, rc = OR_OK;
-  or_giant_range(N, n1, &jmin, &jmax);
+  if (flat) {
+    jmin = 0;
+    jmax = (N + n1 - 1) / n1 - 1;
+  } else {
+    or_giant_range(N, n1, &jmin, &jmax);
+  }
   for (int j = jmin; j <= jmax && rc == OR_OK; j++) {
-    if (Dct) {
+    if (flat) {
+      if (or_giant_sum_flat(p, r, n1, N, Dagg, j, S) != OR_OK) continue;
+    } else if (Dct) {
       if (or_giant_sum_ct(p, r, n1, N, Dct, j, S3) != OR_OK) continue; /* empty range */
       or_relinearize(p, S3, L, rlk, S);                                  /* Step 2c */
     } else if (or_giant_sum(p, r, n1, N, Dagg, j, S) != OR_OK) {
       continue; /* empty range */
     }
     or_rescale(p, S, L, Sp);                                      /* Step 2c */
-    int s = or_pre_rot(N, n1, j);                                 /* Step 2d */
+    int s = flat ? (j * n1) % p->num_slots : or_pre_rot(N, n1, j); /* Step 2d */
     if (s == 0) { /* y_ext += P T_j (P limb += 0) */
       for (int pp = 0; pp < 2; pp++)
         for (int l = 0; l < ell; l++) {
@@ -1180,7 +1295,10 @@ static int scan_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32
       }
     }
   }
-  if (rc == OR_OK) {
+  if (rc == OR_OK && flat) { /* no fold: out = y */
+    moddown(p, yx, ell, out);
+    moddown(p, yx + ext, ell, out + (size_t)ell * n);
+  } else if (rc == OR_OK) {
     moddown(p, yx, ell, y);                      /* c0 */
     moddown(p, yx + ext, ell, y + (size_t)ell * n); /* c1 */
     int fold = p->num_slots - N;

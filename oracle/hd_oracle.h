@@ -150,6 +150,20 @@ int or_scan_aggregate_ct(const or_params *p, const uint64_t *r, int32_t n1, int3
                          const uint64_t *rlk, const int32_t *steps, int32_t nkeys, const uint64_t *keys,
                          uint64_t *out, uint64_t *y_out);
 
+/* Flat pre-rotated layout (NEXT-2, R27; BSGS-RTX-TBE). */
+int or_enroll_slots_flat(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                         int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, int32_t k, double *z);
+int or_enroll_aggregate_flat(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                             int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, uint64_t *Dagg);
+int or_rotation_steps_flat(const or_params *p, int32_t N, int32_t n1, int32_t *steps, int32_t cap,
+                           int32_t *count);
+int or_giant_sum_flat(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dagg,
+                      int32_t j, uint64_t *S);
+int or_scan_aggregate_flat(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dagg,
+                           const int32_t *steps, int32_t nkeys, const uint64_t *keys, uint64_t *out);
+int or_decrypt_scores_flat(const or_params *p, const uint64_t *s_ntt, const uint64_t *out_ct, int32_t N,
+                           int64_t agg, int64_t num_vectors, double *scores);
+
 /* Decrypt + decode one output ciphertext and read the scores of its vectors (R4). */
 int or_decrypt_scores(const or_params *p, const uint64_t *s_ntt, const uint64_t *out_ct,
                       int32_t N, int64_t agg, int64_t num_vectors, double *scores /* M/2*N */);
