@@ -82,9 +82,28 @@ typedef struct {
 typedef struct {
   uint32_t vector_dim, n1, num_slots, block_n, blocks_m, groups_per_ct;
   uint64_t num_vectors, num_groups, num_aggregates;
-  int32_t giant_min, giant_max;  /* giantSteps J (R6) */
+  int32_t giant_min, giant_max;  /* giantSteps J (R6; flat: 0 .. ceil(N/n1) - 1) */
   uint32_t agg_begin, agg_end;   /* aggregates held by this database handle */
+  uint32_t packing;              /* HD_PACKING_* */
+  uint32_t reserved;
 } hd_layout;
+
+/* Database packings.  REPLICATED: Alg. enroller_bsgs, M/2 groups per
+ * ciphertext at stride 2N, giant steps preshifted within blocks and one rotate-by-N
+ * fold (the north-star scan).  FLAT (NEXT-2, R27; BSGS-RTX-TBE, P:L846-865,
+ * P:L883-905): HyDia packing with M groups per ciphertext and no gaps, diagonals
+ * pre-rotated by the enroller (diag'_k = Rot_{-floor(k/n1) n1}(diag_k)), giant steps
+ * k = j n1 + i with j >= 0 rotated by j n1 online, no fold: half the diagonal bytes. */
+enum { HD_PACKING_REPLICATED = 0, HD_PACKING_FLAT = 1 };
+
+/* Options of hd_enroll_ex: packing, and for the encrypted-database mode (NEXT-1)
+ * the public key and the enroller's encryption seed (pk = NULL: plaintext diagonals). */
+typedef struct {
+  uint32_t packing;
+  uint32_t reserved;
+  const struct hd_public_key *pk;
+  uint64_t enc_seed;
+} hd_enroll_options;
 
 /* ---- context ------------------------------------------------------------ */
 /* Creates the context: moduli (R5), primitive roots (R13), NTT/FFT tables.
@@ -100,6 +119,10 @@ hd_status hd_context_moduli(const hd_context *ctx, uint64_t *moduli, uint64_t *p
 /* Rotation-key set of the fold schedule (R2): baby {1..n1-1}, giant
  * {preRot(j) != 0}, fold {numSlots - N}; sorted ascending, unique.
  * Writes min(count, cap) steps; *count = total.  cap too small -> HD_E_INVALID_ARG. */
+/* Rotation keys of a packing: REPLICATED as hd_rotation_steps; FLAT baby {1..n1-1} and
+ * giant {j n1 : 1 <= j < ceil(N/n1)} (the paper's S_baby u S_giant). */
+hd_status hd_rotation_steps_ex(const hd_context *ctx, uint32_t vector_dim, uint32_t n1, uint32_t packing,
+                               int32_t *steps, size_t cap, size_t *count);
 hd_status hd_rotation_steps(const hd_context *ctx, uint32_t vector_dim, uint32_t n1,
                             int32_t *steps, size_t cap, size_t *count);
 /* Secret key (ternary, R14) and hybrid key-switching keys for every step
@@ -145,6 +168,11 @@ hd_status hd_enroll_encrypted(hd_context *ctx, const hd_public_key *pk, const fl
                               uint64_t num_vectors, uint32_t vector_dim, uint32_t n1,
                               uint32_t agg_begin, uint32_t agg_end, uint64_t enc_seed,
                               hd_database **out);
+/* General enrollment: hd_enroll = { REPLICATED, pk = NULL }, hd_enroll_encrypted =
+ * { REPLICATED, pk, seed }.  opt = NULL: hd_enroll. */
+hd_status hd_enroll_ex(hd_context *ctx, const hd_enroll_options *opt, const float *vectors,
+                       uint64_t num_vectors, uint32_t vector_dim, uint32_t n1, uint32_t agg_begin,
+                       uint32_t agg_end, hd_database **out);
 hd_status hd_database_layout(const hd_database *db, hd_layout *out);
 /* The online scan (Alg. sender-bsgs; fold schedule R2): baby steps
  * (hoisted), MAC over all local aggregates, rescale, giant rotations, fold.

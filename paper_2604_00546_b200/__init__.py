@@ -34,6 +34,7 @@ ABI_FUNCTIONS = [
     "hd_secret_key_destroy", "hd_database_destroy", "hd_test_ntt", "hd_test_stage", "hd_test_rotate",
     "hd_test_rescale", "hd_ciphertext_export_async", "hd_context_synchronize", "hd_enroll_encrypted",
     "hd_public_keygen", "hd_public_key_export", "hd_public_key_import", "hd_relin_keygen", "hd_public_key_destroy",
+    "hd_enroll_ex", "hd_rotation_steps_ex",
 ]
 
 
@@ -54,7 +55,14 @@ class Layout(C.Structure):
                 ("block_n", C.c_uint32), ("blocks_m", C.c_uint32), ("groups_per_ct", C.c_uint32),
                 ("num_vectors", C.c_uint64), ("num_groups", C.c_uint64), ("num_aggregates", C.c_uint64),
                 ("giant_min", C.c_int32), ("giant_max", C.c_int32), ("agg_begin", C.c_uint32),
-                ("agg_end", C.c_uint32)]
+                ("agg_end", C.c_uint32), ("packing", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+PACKING = {"replicated": 0, "flat": 1}  # HD_PACKING_* (flat: NEXT-2, R27)
+
+
+class EnrollOptions(C.Structure):
+    _fields_ = [("packing", C.c_uint32), ("reserved", C.c_uint32), ("pk", C.c_void_p), ("enc_seed", C.c_uint64)]
 
 
 _lib = None
@@ -107,6 +115,10 @@ def load():
             L.hd_enroll_encrypted.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                               C.c_uint64, C.POINTER(VP)]
             L.hd_public_keygen.argtypes = [VP, VP, C.POINTER(VP)]
+            L.hd_enroll_ex.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                       C.POINTER(VP)]
+            L.hd_rotation_steps_ex.argtypes = [VP, C.c_uint32, C.c_uint32, C.c_uint32, VP, C.c_size_t,
+                                               C.POINTER(C.c_size_t)]
             L.hd_public_key_export.argtypes = [VP, VP, C.c_size_t]
             L.hd_public_key_import.argtypes = [VP, VP, C.c_size_t, C.POINTER(VP)]
             L.hd_relin_keygen.argtypes = [VP, VP, VP]
@@ -218,12 +230,14 @@ class Context(_Handle):
         return [int(x) for x in m], [int(x) for x in p]
 
     # -- client -------------------------------------------------------------------------------------
-    def rotation_steps(self, vector_dim, n1):
+    def rotation_steps(self, vector_dim, n1, packing="replicated"):
+        pk_ = PACKING[packing]
         cnt = C.c_size_t()
-        _check("hd_rotation_steps", load().hd_rotation_steps(self.h, vector_dim, n1, None, 0, C.byref(cnt)))
+        _check("hd_rotation_steps_ex", load().hd_rotation_steps_ex(self.h, vector_dim, n1, pk_, None, 0,
+                                                                   C.byref(cnt)))
         steps = np.zeros(cnt.value, np.int32)
-        _check("hd_rotation_steps", load().hd_rotation_steps(self.h, vector_dim, n1, _ptr(steps), cnt.value,
-                                                             C.byref(cnt)))
+        _check("hd_rotation_steps_ex", load().hd_rotation_steps_ex(self.h, vector_dim, n1, pk_, _ptr(steps),
+                                                                   cnt.value, C.byref(cnt)))
         return steps
 
     def keygen(self, steps):
@@ -241,7 +255,7 @@ class Context(_Handle):
 
     def decrypt_scores(self, sk, layout, cts):
         arr = (VP * len(cts))(*[c.h for c in cts])
-        per = (layout.blocks_m // 2) * layout.block_n
+        per = layout.groups_per_ct * layout.block_n
         v0 = layout.agg_begin * per
         v1 = min(layout.num_vectors, (layout.agg_begin + len(cts)) * per)
         scores = np.zeros(v1 - v0, np.float64)
@@ -256,12 +270,16 @@ class Context(_Handle):
         return out
 
     # -- enroller / server ---------------------------------------------------------------------------
-    def enroll(self, vectors, n1, agg_begin=0, agg_end=0):
+    def enroll(self, vectors, n1, agg_begin=0, agg_end=0, packing="replicated", pk=None, enc_seed=0):
+        """hd_enroll_ex: plaintext (pk None) or encrypted (NEXT-1) diagonals, replicated or flat (NEXT-2)."""
         vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+        opt = EnrollOptions(PACKING[packing], 0, pk.h if pk is not None else None, enc_seed)
         out = VP()
-        _check("hd_enroll", load().hd_enroll(self.h, _ptr(vectors), vectors.shape[0], vectors.shape[1], n1,
-                                             agg_begin, agg_end, C.byref(out)))
-        return Database(out.value, self)
+        _check("hd_enroll_ex", load().hd_enroll_ex(self.h, C.byref(opt), _ptr(vectors), vectors.shape[0],
+                                                   vectors.shape[1], n1, agg_begin, agg_end, C.byref(out)))
+        db = Database(out.value, self)
+        db.encrypted = pk is not None
+        return db
 
     # -- encrypted-database mode (NEXT-1, R26) ------------------------------------------------
     def public_keygen(self, sk):

@@ -192,14 +192,15 @@ __global__ void fft_fwd_stage_kernel(double *__restrict__ re, double *__restrict
   im[i1] = __dsub_rn(ui, vi);
 }
 
-// scores of aggregate agg: v = (agg M/2 + b) N + t -> slot b 2N + t (R4)
-__global__ void scores_kernel(const double *__restrict__ z, int N, int M, long long agg, long long v_first,
-                              long long v_end, double *__restrict__ scores) {
+// scores of aggregate agg: v = (agg G + b) N + t -> slot b stride + t, G groups per ciphertext
+// (replicated, R4: G = M/2, stride 2N; flat, R27: G = M, stride N)
+__global__ void scores_kernel(const double *__restrict__ z, int N, int G, int stride, long long agg,
+                              long long v_first, long long v_end, double *__restrict__ scores) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (M / 2) * N) return;
+  if (i >= G * N) return;
   const int b = i / N, t = i % N;
-  const long long v = (agg * (M / 2) + b) * N + t;
-  if (v >= v_first && v < v_end) scores[v - v_first] = z[b * 2 * N + t];
+  const long long v = (agg * G + b) * N + t;
+  if (v >= v_first && v < v_end) scores[v - v_first] = z[(size_t)b * stride + t];
 }
 // ---- encrypted-database mode (NEXT-1, R26) -------------------------------------------
 // public key: b rows hold e (coefficient form) before the NTT; then b = e - a s, a uniform.
@@ -400,7 +401,8 @@ extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, c
                                        size_t *written) {
   if (!c || !sk || !lay || !cts || !scores) return hd_fail(HD_E_INVALID_ARG, "null argument");
   const int n = c->n, ns = c->ns, N = (int)lay->block_n, M = (int)lay->blocks_m;
-  const long long per = (long long)(M / 2) * N;
+  const int G = (int)lay->groups_per_ct, stride = lay->packing == HD_PACKING_FLAT ? N : 2 * N;
+  const long long per = (long long)G * N;
   const long long v_first = (long long)lay->agg_begin * per;
   const long long v_end = std::min<long long>((long long)lay->num_vectors, (long long)(lay->agg_begin + n_ct) * per);
   if (v_end <= v_first) return hd_fail(HD_E_INVALID_ARG, "no vectors in the given aggregates");
@@ -450,8 +452,8 @@ extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, c
       fft_fwd_stage_kernel<<<(ns / 2 + TPB - 1) / TPB, TPB, 0, c->stream>>>(re, im, ns, len, c->rotg, c->xi_re,
                                                                             c->xi_im, 2u * n);
     c->launches += c->logn - 1;
-    scores_kernel<<<((M / 2) * N + TPB - 1) / TPB, TPB, 0, c->stream>>>(re, N, M, (long long)(lay->agg_begin + i),
-                                                                       v_first, v_end, dsc); ++c->launches;
+    scores_kernel<<<(G * N + TPB - 1) / TPB, TPB, 0, c->stream>>>(re, N, G, stride, (long long)(lay->agg_begin + i),
+                                                                 v_first, v_end, dsc); ++c->launches;
   }
   if (!s) {
     e = cudaMemcpyAsync(scores, dsc, nsc * 8, cudaMemcpyDeviceToHost, c->stream);

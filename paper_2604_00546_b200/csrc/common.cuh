@@ -191,6 +191,7 @@ struct hd_database {
   uint64_t *D = nullptr;         // [A_loc][N][L][n] diagonal plaintexts, or
                                  // [A_loc][N][2][L][n] diagonal ciphertexts (encrypted)
   bool encrypted = false;        // encrypted-database mode (NEXT-1, R26)
+  bool flat = false;             // flat pre-rotated packing (NEXT-2, R27): no fold
   uint32_t spoly = 2;            // polynomials per giant-step sum: 2, or 3 (degree 2) encrypted
   // query workspaces (allocated at enrollment; reused by every hd_query)
   uint64_t *r = nullptr;         // [n1][2][L][n] baby steps

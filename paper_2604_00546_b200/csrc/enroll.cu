@@ -58,6 +58,25 @@ __global__ void pack_kernel(const double *__restrict__ U, long long v_first, lon
   im[(size_t)kk * ns + s] = 0.0;
 }
 
+// Flat pre-rotated packing (NEXT-2, R27): slot s of diagonal k of aggregate agg is
+// diag_k[(s - j n1) mod ns], j = floor(k / n1), with diag_k[b N + t] =
+// U[(agg M + b) N + t][(t + k) mod N] (0 beyond the database), M = ns / N, no gaps.
+__global__ void pack_flat_kernel(const double *__restrict__ U, long long v_first, long long num_vectors, int N,
+                                 int M, int n1, long long agg, int k0, int ns, double *__restrict__ re,
+                                 double *__restrict__ im) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  const int kk = blockIdx.y;
+  if (s >= ns) return;
+  const int k = k0 + kk;
+  const int src = ((s - (k / n1) * n1) % ns + ns) % ns;  // Rot_{-j n1}
+  const int b = src / N, t = src % N;
+  const long long v = (agg * M + b) * N + t;
+  double val = 0.0;
+  if (v < num_vectors) val = U[(size_t)(v - v_first) * N + ((t + k) % N)];
+  re[(size_t)kk * ns + s] = val;
+  im[(size_t)kk * ns + s] = 0.0;
+}
+
 // One stage (len) of the special inverse FFT over B vectors of ns complex slots.
 __global__ void fft_inv_stage_kernel(double *__restrict__ re, double *__restrict__ im, int ns, int len,
                                      const uint32_t *__restrict__ rotg, const double *__restrict__ xr,
@@ -152,8 +171,10 @@ hd_status check_flag(hd_context *c) {
 // ---------------------------------------------------------------------------
 static int floordiv_i(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
-hd_status layout_make(const hd_context *c, uint64_t K, uint32_t dim, uint32_t n1, hd_layout *lay) {
+hd_status layout_make(const hd_context *c, uint64_t K, uint32_t dim, uint32_t n1, uint32_t packing,
+                      hd_layout *lay) {
   if (dim < 2 || n1 < 1 || K < 1) return hd_fail(HD_E_INVALID_ARG, "vector_dim >= 2, n1 >= 1, num_vectors >= 1");
+  if (packing != HD_PACKING_REPLICATED && packing != HD_PACKING_FLAT) return hd_fail(HD_E_INVALID_ARG, "packing");
   if ((dim & (dim - 1)) != 0 || (uint32_t)c->ns % (2 * dim) != 0)
     return hd_fail(HD_E_LAYOUT, "vector_dim must be a power of two with numSlots % (2 vector_dim) == 0");
   memset(lay, 0, sizeof(*lay));
@@ -168,23 +189,34 @@ hd_status layout_make(const hd_context *c, uint64_t K, uint32_t dim, uint32_t n1
   lay->num_aggregates = (2 * lay->num_groups + lay->blocks_m - 1) / lay->blocks_m;  // A
   lay->giant_min = floordiv_i(-(int)(dim / 2), (int)n1);                      // R6
   lay->giant_max = floordiv_i((int)(dim / 2) - 1, (int)n1);
+  lay->packing = packing;
+  if (packing == HD_PACKING_FLAT) {  // R27: M groups per ciphertext, j = 0 .. ceil(N/n1) - 1
+    lay->groups_per_ct = lay->blocks_m;
+    lay->num_aggregates = (lay->num_groups + lay->blocks_m - 1) / lay->blocks_m;
+    lay->giant_min = 0;
+    lay->giant_max = (int)((dim + n1 - 1) / n1) - 1;
+  }
   return HD_OK;
 }
 
-extern "C" hd_status hd_rotation_steps(const hd_context *c, uint32_t vector_dim, uint32_t n1, int32_t *steps,
-                                       size_t cap, size_t *count) {
+extern "C" hd_status hd_rotation_steps_ex(const hd_context *c, uint32_t vector_dim, uint32_t n1, uint32_t packing,
+                                          int32_t *steps, size_t cap, size_t *count) {
   if (!c || !count) return hd_fail(HD_E_INVALID_ARG, "null argument");
   hd_layout lay;
-  hd_status s = layout_make(c, 1, vector_dim, n1, &lay);
+  hd_status s = layout_make(c, 1, vector_dim, n1, packing, &lay);
   if (s) return s;
   const int N = (int)vector_dim, ns = c->ns;
   std::vector<char> used(ns, 0);
   for (uint32_t i = 1; i < n1; i++) used[i % ns] = 1;
-  for (int j = lay.giant_min; j <= lay.giant_max; j++) {
-    int pr = (((int)n1 * j) % N + N) % N;
-    if (pr) used[pr] = 1;
+  if (packing == HD_PACKING_FLAT) {  // giant j n1, no fold (R27)
+    for (int j = 1; j <= lay.giant_max; j++) used[((int)n1 * j) % ns] = 1;
+  } else {
+    for (int j = lay.giant_min; j <= lay.giant_max; j++) {
+      int pr = (((int)n1 * j) % N + N) % N;
+      if (pr) used[pr] = 1;
+    }
+    used[ns - N] = 1;
   }
-  used[ns - N] = 1;
   size_t cnt = 0;
   for (int st = 1; st < ns; st++)
     if (used[st]) {
@@ -194,6 +226,11 @@ extern "C" hd_status hd_rotation_steps(const hd_context *c, uint32_t vector_dim,
   *count = cnt;
   if (steps && cnt > cap) return hd_fail(HD_E_INVALID_ARG, "steps capacity too small");
   return HD_OK;
+}
+
+extern "C" hd_status hd_rotation_steps(const hd_context *c, uint32_t vector_dim, uint32_t n1, int32_t *steps,
+                                       size_t cap, size_t *count) {
+  return hd_rotation_steps_ex(c, vector_dim, n1, HD_PACKING_REPLICATED, steps, cap, count);
 }
 
 extern "C" hd_status hd_database_layout(const hd_database *db, hd_layout *out) {
@@ -227,14 +264,16 @@ extern "C" void hd_database_destroy(hd_database *db) {
 
 // pk == NULL: plaintext diagonals (the north-star pt x ct scan); else every diagonal
 // plaintext is encrypted under pk (encrypted-database mode, NEXT-1, R26).
-static hd_status enroll_impl(hd_context *c, const hd_public_key *pk, uint64_t enc_seed, const float *vectors,
-                             uint64_t num_vectors, uint32_t vector_dim, uint32_t n1, uint32_t agg_begin,
-                             uint32_t agg_end, hd_database **out) {
+static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_key *pk, uint64_t enc_seed,
+                             const float *vectors, uint64_t num_vectors, uint32_t vector_dim, uint32_t n1,
+                             uint32_t agg_begin, uint32_t agg_end, hd_database **out) {
   if (!c || !vectors || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
   if (pk && pk->ctx != c) return hd_fail(HD_E_STATE, "public key from another context");
+  if (pk && packing == HD_PACKING_FLAT)
+    return hd_fail(HD_E_INVALID_ARG, "encrypted diagonals are supported with the replicated packing only");
   *out = nullptr;
   hd_layout lay;
-  hd_status s = layout_make(c, num_vectors, vector_dim, n1, &lay);
+  hd_status s = layout_make(c, num_vectors, vector_dim, n1, packing, &lay);
   if (s) return s;
   if (agg_end == 0) agg_end = (uint32_t)lay.num_aggregates;
   if (agg_begin >= agg_end || agg_end > lay.num_aggregates) return hd_fail(HD_E_INVALID_ARG, "bad aggregate range");
@@ -251,7 +290,13 @@ static hd_status enroll_impl(hd_context *c, const hd_public_key *pk, uint64_t en
   db->encrypted = pk != nullptr;
   db->spoly = pk ? 3 : 2;
   const int N = (int)db->N, L = c->L, n = c->n, ns = c->ns;
+  db->flat = packing == HD_PACKING_FLAT;
   for (int j = lay.giant_min; j <= lay.giant_max; j++) {
+    if (db->flat) {  // R27: diagonals j n1 .. j n1 + n1 - 1 (< N), rotation j n1
+      db->js.push_back(j);
+      db->pre.push_back((int)((int64_t)n1 * j % ns));
+      continue;
+    }
     int lo = std::max(0, -j * (int)n1 - N / 2), hi = std::min((int)n1 - 1, N / 2 - 1 - j * (int)n1);
     if (lo > hi) continue;
     db->js.push_back(j);
@@ -320,7 +365,7 @@ static hd_status enroll_impl(hd_context *c, const hd_public_key *pk, uint64_t en
       return hd_fail(HD_E_CUDA, "event creation");
     }
   // enrollment scratch: rows of one aggregate (float + double), FFT buffers for a batch of diagonals
-  const size_t rows_per_agg = (size_t)(db->M / 2) * N;
+  const size_t rows_per_agg = (size_t)lay.groups_per_ct * N;
   const int KB = std::min(N, std::max(1, (int)((256ull << 20) / ((size_t)ns * 16))));
   float *dv = nullptr;
   double *U = nullptr, *re = nullptr, *im = nullptr;
@@ -359,8 +404,13 @@ static hd_status enroll_impl(hd_context *c, const hd_public_key *pk, uint64_t en
     uint64_t *Da = db->D + (size_t)(a - agg_begin) * N * dstride;
     for (int k0 = 0; k0 < N && !s; k0 += KB) {
       int kb = std::min(KB, N - k0);
-      pack_kernel<<<dim3((ns + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(U, (long long)v0, (long long)num_vectors, N,
-                                                                         db->M, n1, a, k0, ns, re, im); ++c->launches;
+      if (db->flat)
+        pack_flat_kernel<<<dim3((ns + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(
+            U, (long long)v0, (long long)num_vectors, N, db->M, n1, a, k0, ns, re, im);
+      else
+        pack_kernel<<<dim3((ns + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(U, (long long)v0, (long long)num_vectors,
+                                                                           N, db->M, n1, a, k0, ns, re, im);
+      ++c->launches;
       // plaintext rows (into c0 of each diagonal ciphertext in encrypted mode)
       s = encode_batch(c, re, im, kb, delta, L, Da + (size_t)k0 * dstride, dstride);
       if (!s && pk)  // Enc_pk with object id a N + k (R26), the oracle's or_enroll_aggregate_encrypted
@@ -380,12 +430,22 @@ static hd_status enroll_impl(hd_context *c, const hd_public_key *pk, uint64_t en
 
 extern "C" hd_status hd_enroll(hd_context *c, const float *vectors, uint64_t num_vectors, uint32_t vector_dim,
                                uint32_t n1, uint32_t agg_begin, uint32_t agg_end, hd_database **out) {
-  return enroll_impl(c, nullptr, 0, vectors, num_vectors, vector_dim, n1, agg_begin, agg_end, out);
+  return enroll_impl(c, HD_PACKING_REPLICATED, nullptr, 0, vectors, num_vectors, vector_dim, n1, agg_begin, agg_end,
+                     out);
+}
+
+extern "C" hd_status hd_enroll_ex(hd_context *c, const hd_enroll_options *opt, const float *vectors,
+                                  uint64_t num_vectors, uint32_t vector_dim, uint32_t n1, uint32_t agg_begin,
+                                  uint32_t agg_end, hd_database **out) {
+  if (!opt) return hd_enroll(c, vectors, num_vectors, vector_dim, n1, agg_begin, agg_end, out);
+  return enroll_impl(c, opt->packing, opt->pk, opt->enc_seed, vectors, num_vectors, vector_dim, n1, agg_begin,
+                     agg_end, out);
 }
 
 extern "C" hd_status hd_enroll_encrypted(hd_context *c, const hd_public_key *pk, const float *vectors,
                                          uint64_t num_vectors, uint32_t vector_dim, uint32_t n1, uint32_t agg_begin,
                                          uint32_t agg_end, uint64_t enc_seed, hd_database **out) {
   if (!pk) return hd_fail(HD_E_INVALID_ARG, "null public key");
-  return enroll_impl(c, pk, enc_seed, vectors, num_vectors, vector_dim, n1, agg_begin, agg_end, out);
+  return enroll_impl(c, HD_PACKING_REPLICATED, pk, enc_seed, vectors, num_vectors, vector_dim, n1, agg_begin,
+                     agg_end, out);
 }

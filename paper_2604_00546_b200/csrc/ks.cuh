@@ -33,9 +33,10 @@ struct MacPlan {
 };
 // Encrypted diagonals (NEXT-1): degree-2 sums S3 [a][j][3][L][n] of Dct [a][k][2][L][n].
 hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint64_t *S3, uint32_t A_loc, int n1,
-                     int N, const std::vector<int32_t> &js);
+                     int N, const std::vector<int32_t> &js, bool flat);
+// flat: the giant-step ranges of the flat packing (R27)
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
-                  const std::vector<int32_t> &js);
+                  const std::vector<int32_t> &js, bool flat);
 
 // Public-key encryption of count ciphertexts in place (c0 of ct_x = ct + x*ct_stride holds
 // the plaintext on entry); object ids obj0 + x; V, E0: count*L*n scratch each (client.cu).

@@ -20,7 +20,8 @@ constexpr int MAC_TPB = 128;
 
 __global__ void __launch_bounds__(MAC_TPB) mac_kernel(const uint64_t *__restrict__ D,
                                                       const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
-                                                      int n1, int N, int L, int logn, int jmin, int nj, ModTab mt) {
+                                                      int n1, int N, int L, int logn, int jmin, int nj, ModTab mt,
+                                                      int flat) {
   const int n = 1 << logn;
   const uint32_t t = blockIdx.x * MAC_TPB + threadIdx.x;
   const int m = blockIdx.y;
@@ -33,9 +34,10 @@ __global__ void __launch_bounds__(MAC_TPB) mac_kernel(const uint64_t *__restrict
   const uint64_t q = mt.q[m], bar = mt.bar[m], r64 = mt.r64[m], r64s = mt.r64s[m];
   for (int jj = 0; jj < nj; jj++) {
     const int j = jmin + jj;
-    int i_lo = -j * n1 - N / 2;
+    // replicated: P:L206-207; flat (R27): diagonals j n1 + i < N
+    int i_lo = flat ? 0 : -j * n1 - N / 2;
     if (i_lo < 0) i_lo = 0;
-    int i_hi = N / 2 - 1 - j * n1;
+    int i_hi = flat ? N - 1 - j * n1 : N / 2 - 1 - j * n1;
     if (i_hi > n1 - 1) i_hi = n1 - 1;
     uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
     int cnt = 0;
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(MAC_TPB) mac_cs_kernel(const uint64_t *__restr
 __global__ void __launch_bounds__(MAC_TPB) mac_ct_kernel(const uint64_t *__restrict__ D,
                                                           const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
                                                           int n1, int N, int L, int logn, int jmin, int nj,
-                                                          ModTab mt) {
+                                                          ModTab mt, int flat) {
   const int n = 1 << logn;
   const uint32_t a = blockIdx.x;
   const uint32_t t = blockIdx.y * MAC_TPB + threadIdx.x;
@@ -204,7 +206,8 @@ __global__ void __launch_bounds__(MAC_TPB) mac_ct_kernel(const uint64_t *__restr
   const size_t ls = (size_t)L * n, ds = 2 * ls;
   const uint64_t *Da = D + (size_t)a * N * ds + (size_t)m * n + t;
   const uint64_t *rr = r + (size_t)m * n + t;
-  const int i_lo = max(0, -j * n1 - N / 2), i_hi = min(n1 - 1, N / 2 - 1 - j * n1);
+  const int i_lo = flat ? 0 : max(0, -j * n1 - N / 2);
+  const int i_hi = flat ? min(n1 - 1, N - 1 - j * n1) : min(n1 - 1, N / 2 - 1 - j * n1);
   const uint64_t q = mt.q[m], bar = mt.bar[m], r64 = mt.r64[m], r64s = mt.r64s[m];
   CsAcc acc[3] = {CsAcc{0, 0, 0, 0}, CsAcc{0, 0, 0, 0}, CsAcc{0, 0, 0, 0}};
   uint64_t part[3] = {0, 0, 0};
@@ -300,26 +303,27 @@ __global__ void __launch_bounds__(MAC_TPB) mac_ct_stream_kernel(const uint64_t *
 }  // namespace
 
 hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint64_t *S3, uint32_t A_loc, int n1,
-                     int N, const std::vector<int32_t> &js) {
+                     int N, const std::vector<int32_t> &js, bool flat) {
   if (js.empty() || A_loc == 0) return HD_OK;
   if (c->n % MAC_TPB) return hd_fail(HD_E_PARAMS, "ring too small for the encrypted MAC");
   const int jmin = js.front(), nj = (int)js.size();
   const dim3 grid(A_loc, c->n / MAC_TPB, c->L * nj);
   const char *force = getenv("HD_MAC_VARIANT");  // 'g': the generic kernel (tests)
-  if ((N / 2) % n1 == 0 && !(force && force[0] == 'g'))
+  if ((flat ? N % n1 : (N / 2) % n1) == 0 && !(force && force[0] == 'g'))
     mac_ct_stream_kernel<<<grid, MAC_TPB, 0, c->stream>>>(Dct, r, S3, n1, N, c->L, c->logn, jmin, nj, c->mt);
   else
-    mac_ct_kernel<<<grid, MAC_TPB, 0, c->stream>>>(Dct, r, S3, n1, N, c->L, c->logn, jmin, nj, c->mt);
+    mac_ct_kernel<<<grid, MAC_TPB, 0, c->stream>>>(Dct, r, S3, n1, N, c->L, c->logn, jmin, nj, c->mt, flat ? 1 : 0);
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;
 }
 
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
-                  const std::vector<int32_t> &js) {
+                  const std::vector<int32_t> &js, bool flat) {
   if (js.empty() || A_loc == 0) return HD_OK;
   const int jmin = js.front(), nj = (int)js.size();
-  const bool full = (N / 2) % n1 == 0 && n1 <= 256 && c->n % MAC_TPB == 0;
+  // every giant step uses all n1 baby steps (replicated: n1 | N/2; flat: n1 | N)
+  const bool full = (flat ? N % n1 : (N / 2) % n1) == 0 && n1 <= 256 && c->n % MAC_TPB == 0;
   bool small_q = true;
   for (int l = 0; l < c->L; l++) small_q = small_q && c->mod[l] < (1ull << 60);
   const char *force = getenv("HD_MAC_VARIANT");  // 'g': force the generic kernel (tests)
@@ -337,7 +341,7 @@ hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t 
       mac_cs_kernel<1, true><<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
   } else {
     const dim3 grid((c->n + MAC_TPB - 1) / MAC_TPB, c->L, A_loc);
-    mac_kernel<<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt);
+    mac_kernel<<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, c->mt, flat ? 1 : 0);
   }
   ++c->launches;
   HD_CUDA(cudaGetLastError());

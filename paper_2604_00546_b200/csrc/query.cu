@@ -35,7 +35,7 @@ static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
   for (int jj = 0; jj < nj; jj++)
     if (db->pre[jj] && (s = need(db->pre[jj], n1 - 1 + jj))) return s;
   const size_t fold_slot = (size_t)(n1 - 1) + nj;
-  if ((s = need(c->ns - (int)db->N, fold_slot))) return s;
+  if (!db->flat && (s = need(c->ns - (int)db->N, fold_slot))) return s;  // flat packing: no fold (R27)
   if (db->encrypted) {  // relinearisation key: identity permutation (g = 1)
     kp[fold_slot + 1] = evk->find(HD_RELIN_STEP);
     if (!kp[fold_slot + 1])
@@ -97,8 +97,8 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
   cudaEventRecord(E[1], sa);
   // ---- MAC ----
   if (db->encrypted) {
-    if ((s = mac_ct_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js))) return s;
-  } else if ((s = mac_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js))) {
+    if ((s = mac_ct_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js, db->flat))) return s;
+  } else if ((s = mac_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js, db->flat))) {
     return s;
   }
   cudaEventRecord(E[2], sa);
@@ -170,6 +170,11 @@ static hd_status giant_and_fold(hd_database *db, cudaEvent_t *E) {
   }
   if ((s = ks_moddown(c, db->u, A, 1, ell, db->gal, nullptr, 0, db->y, ct1, false, db->tmp))) return s;
   cudaEventRecord(E[5], c->stream);
+  if (db->flat) {  // flat packing (R27): no gaps, no fold -- out = y
+    HD_CUDA(cudaMemcpyAsync(db->outbuf, db->y, (size_t)A * ct1 * 8, cudaMemcpyDeviceToDevice, c->stream));
+    cudaEventRecord(E[6], c->stream);
+    return HD_OK;
+  }
   // ---- fold: out = y + Rot_{numSlots - N}(y) ----
   {
     const size_t slot = (size_t)(n1 - 1) + nj;
