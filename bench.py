@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--packing", default="replicated", choices=["replicated", "flat"],
+                    help="stride-2N replicated blocks + fold (the north-star scan) or the flat pre-rotated "
+                         "layout (NEXT-2, BSGS-RTX-TBE)")
     ap.add_argument("--db", default="plain", choices=["plain", "encrypted"],
                     help="plaintext diagonals (the north-star scan) or the encrypted-database mode (NEXT-1)")
     return ap.parse_args()
@@ -217,12 +220,13 @@ def main():
     cfg = CONFIGS[args.config]
     stream = torch.cuda.current_stream()
     ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1, device=local, stream=stream)
-    A = cfg.aggregates
+    flat = args.packing == "flat"
+    per = cfg.num_slots if flat else (cfg.num_slots // cfg.dim // 2) * cfg.dim  # vectors per aggregate
+    A = -(-cfg.num_vectors // per)
     a0, a1 = hdd.shard_range(A, rank, world)
-    per = (cfg.num_slots // cfg.dim // 2) * cfg.dim
     # ---- setup (untimed): keys on rank 0 -> NCCL broadcast; local enrollment of this shard ----
     _, q, _ = make_dataset(16, cfg.dim, cfg.data_seed)  # query only (rows drawn per shard below)
-    steps = ctx.rotation_steps(cfg.dim, cfg.n1)
+    steps = ctx.rotation_steps(cfg.dim, cfg.n1, packing=args.packing)
     enc_db = args.db == "encrypted"
     if rank == 0:
         sk, evk = ctx.keygen(steps)
@@ -245,7 +249,7 @@ def main():
         del kb
     v0, v1 = hdd.rows_of_aggregates(a0, a1, per, cfg.num_vectors)
     rows = dataset_rows(cfg.num_vectors, cfg.dim, cfg.data_seed, v0, v1)
-    db = enroll_rows(hd, ctx, rows, v0, cfg, a0, a1, pk)
+    db = enroll_rows(hd, ctx, rows, v0, cfg, a0, a1, pk, args.packing)
     del rows
     # ---- the query: encrypted on rank 0, exported into a device buffer (NCCL-broadcast each step) ----
     ct_bytes = 0
@@ -344,7 +348,7 @@ def main():
                       " -> hd_context_synchronize"}
     # ---- roofline of the dominant kernel (MAC, HBM-bound) ----
     L, n, N = cfg.limbs, 1 << cfg.log_n, cfg.dim
-    nj = len(db_js(cfg))
+    nj = len(db_js(cfg, flat))
     dpoly, spoly = (2, 3) if enc_db else (1, 2)  # diagonal / giant-sum polynomials
     mac_bytes = nloc * N * dpoly * L * n * 8 + cfg.n1 * 2 * L * n * 8 + nloc * nj * spoly * L * n * 8
     mac_avg_ms = statistics.mean(mac_ms)
@@ -352,7 +356,7 @@ def main():
     achieved = mac_bytes / (mac_avg_ms / 1e3) / 1e9
     traffic = None
     tf = os.path.join(ROOT, "profiles", "mac_traffic.json")
-    if os.path.exists(tf) and not enc_db:
+    if os.path.exists(tf) and not enc_db and not flat:
         try:
             traffic = json.load(open(tf)).get(cfg.name)
         except Exception:  # noqa: BLE001
@@ -380,8 +384,9 @@ def main():
                      "frac": kip_bytes / (kip_ms / 1e3) / 1e9 / peak, "algorithmic_bytes": kip_bytes,
                      "avg_launch_ms": kip_ms, "timing": "CUDA events around the launch, serial pass after the timed region"}
     # ---- whole-query compulsory bytes against the step time ----
-    nnz = sum(1 for j in db_js(cfg) if ((cfg.n1 * j) % N + N) % N != 0)
-    q_bytes = (nloc * N * dpoly * L * n * 8 + (cfg.n1 - 1) * key_bytes + (nnz + 1) * (L - 1) * 2 * L * n * 8
+    # giant keys (+ the fold key for the replicated packing)
+    n_gkeys = (nj - 1) if flat else sum(1 for j in db_js(cfg) if ((cfg.n1 * j) % N + N) % N != 0) + 1
+    q_bytes = (nloc * N * dpoly * L * n * 8 + (cfg.n1 - 1) * key_bytes + n_gkeys * (L - 1) * 2 * L * n * 8
                + 2 * L * n * 8 + nloc * 2 * (L - 1) * n * 8 + (nj * key_bytes if enc_db else 0))
     query_roofline = {"bytes": q_bytes, "achieved": q_bytes / (ms_per_step / 1e3) / 1e9, "peak": peak,
                       "unit": "GB/s", "frac": q_bytes / (ms_per_step / 1e3) / 1e9 / peak,
@@ -392,7 +397,10 @@ def main():
             "data": "synthetic (P:L2175-2179 generator, seeded)",
             "config": dict(cfg_dict(cfg, world, "fixed 2^20 database sharded by aggregate"),
                            database="encrypted diagonals (NEXT-1: degree-2 MAC + relinearisation)" if enc_db
-                           else "plaintext diagonals (north-star pt x ct scan)"),
+                           else "plaintext diagonals (north-star pt x ct scan)",
+                           packing="flat pre-rotated (NEXT-2, BSGS-RTX-TBE; no fold, M groups per ciphertext)"
+                           if flat else "stride-2N replicated blocks + rotate-by-N fold (Alg. enroller_bsgs)",
+                           aggregates=A),
             "phase_ms": {"baby": phase[0] / args.steps, "mac": phase[1] / args.steps,
                          "rescale": phase[2] / args.steps, "giant": phase[3] / args.steps,
                          "fold": phase[4] / args.steps, "baby_kip": phase[5] / args.steps,
@@ -426,29 +434,28 @@ def main():
         dist.destroy_process_group()
 
 
-def db_js(cfg):
+def db_js(cfg, flat=False):
     N, n1 = cfg.dim, cfg.n1
+    if flat:  # R27: j = 0 .. ceil(N / n1) - 1
+        return list(range(-(-N // n1)))
     return list(range((-(N // 2)) // n1, (N // 2 - 1) // n1 + 1))
 
 
 DB_ENC_SEED = 4242  # encrypted-database mode: Philox key of the enroller's encryption
 
 
-def enroll_rows(hd, ctx, rows, v0, cfg, a0, a1, pk=None):
-    """hd_enroll reads rows [a0*per, a1*per) of the array it is given (indexed from vector 0):
+def enroll_rows(hd, ctx, rows, v0, cfg, a0, a1, pk=None, packing="replicated"):
+    """hd_enroll_ex reads rows [a0*per, a1*per) of the array it is given (indexed from vector 0):
     pass a pointer shifted back by v0 rows so this rank only materialises its own shard."""
     import ctypes as C
     out = C.c_void_p()
     ptr = rows.ctypes.data - v0 * cfg.dim * 4
-    if pk is None:
-        hd._check("hd_enroll", hd.load().hd_enroll(ctx.h, C.c_void_p(ptr), cfg.num_vectors, cfg.dim, cfg.n1, a0, a1,
-                                                   C.byref(out)))
-        return hd.Database(out.value, ctx)
-    hd._check("hd_enroll_encrypted", hd.load().hd_enroll_encrypted(
-        ctx.h, pk.h, C.c_void_p(ptr), cfg.num_vectors, cfg.dim, cfg.n1, a0, a1, C.c_uint64(DB_ENC_SEED),
-        C.byref(out)))
+    opt = hd.EnrollOptions(hd.PACKING[packing], 0, pk.h if pk is not None else None,
+                           DB_ENC_SEED if pk is not None else 0)
+    hd._check("hd_enroll_ex", hd.load().hd_enroll_ex(ctx.h, C.byref(opt), C.c_void_p(ptr), cfg.num_vectors,
+                                                     cfg.dim, cfg.n1, a0, a1, C.byref(out)))
     db = hd.Database(out.value, ctx)
-    db.encrypted = True
+    db.encrypted = pk is not None
     return db
 
 
