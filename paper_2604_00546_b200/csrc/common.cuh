@@ -31,6 +31,36 @@ struct InvTab2 {
   uint64_t w[HD_MAXMOD];
 };
 
+// Division by a runtime divisor d without the ~25-instruction integer division: a shift
+// when d is a power of two, else floor(r / d) = floor(r m / 2^48) with m = floor(2^48/d)+1,
+// exact for r < 2^31 and d < 2^17 (error < r / 2^48 < 1/d); other d divide plainly.
+struct FDiv {
+  uint64_t m = 0;
+  uint32_t d = 1;
+  int32_t sh = 0;  // >= 0: shift; -1: multiply-high; -2: plain division
+};
+inline FDiv fdiv_make(uint32_t d) {
+  FDiv f;
+  f.d = d ? d : 1;
+  if ((f.d & (f.d - 1)) == 0) {
+    f.sh = 0;
+    while ((1u << f.sh) < f.d) f.sh++;
+  } else if (f.d < (1u << 17)) {
+    f.sh = -1;
+    f.m = (uint64_t)((((unsigned __int128)1) << 48) / f.d) + 1;
+  } else {
+    f.sh = -2;
+  }
+  return f;
+}
+__host__ __device__ __forceinline__ uint32_t fdiv_q(uint32_t r, const FDiv &f) {
+#ifdef __CUDA_ARCH__
+  if (f.sh >= 0) return r >> f.sh;
+  if (f.sh == -1) return (uint32_t)__umul64hi((uint64_t)r << 16, f.m);
+#endif
+  return r / f.d;
+}
+
 // Row addressing for batched kernels: row r lives at
 //   base + (r / gsize) * gstride + ((r % gsize) / g2) * s2 + (r % g2) * s3   (s3 == 0 means n)
 // and is reduced modulo q[midx[(r / mdiv) % mlen]].  Defaults (g2 = gsize, s3 = 0)
@@ -41,7 +71,17 @@ struct RowMap {
   uint32_t g2 = 1u << 30;
   uint64_t gstride = 0, s2 = 0, s3 = 0;
   uint8_t midx[32] = {0};
+  // fast divisors for gsize, min(g2, gsize), mdiv, mlen (rowmap_finalize; device use only)
+  bool fast = false;
+  FDiv fg, fg2, fmd, fml;
 };
+inline void rowmap_finalize(RowMap &rm) {
+  rm.fg = fdiv_make(rm.gsize);
+  rm.fg2 = fdiv_make(rm.g2 < rm.gsize ? rm.g2 : rm.gsize);
+  rm.fmd = fdiv_make(rm.mdiv);
+  rm.fml = fdiv_make(rm.mlen);
+  rm.fast = true;
+}
 
 // ---------------------------------------------------------------------------
 // Device arithmetic
@@ -89,11 +129,10 @@ __device__ __forceinline__ void mac128(uint64_t &lo, uint64_t &hi, uint64_t a, u
 }
 // centred lift (R12) of x in [0, qs) into modulus m (bar_m = floor(2^64/m)).
 __device__ __forceinline__ uint64_t lift_centred(uint64_t x, uint64_t qs, uint64_t m, uint64_t bar_m) {
-  if (x > (qs >> 1)) {
-    uint64_t r = reduce64(qs - x, m, bar_m);
-    return r ? m - r : 0;
-  }
-  return reduce64(x, m, bar_m);
+  // branch-free (no divergence): reduce |centred x|, negate when x > qs/2
+  const bool neg = x > (qs >> 1);
+  const uint64_t r = reduce64(neg ? qs - x : x, m, bar_m);
+  return neg ? (r ? m - r : 0) : r;
 }
 // Galois index map in the NTT domain (R11): out[t] = in[pi_g(t)],
 // pi_g(t) = br(((g (2 br(t) + 1)) mod 2n - 1) / 2).
@@ -105,14 +144,23 @@ __device__ __forceinline__ uint32_t galois_src(uint32_t t, uint32_t g, int logn)
 }
 
 __host__ __device__ __forceinline__ uint64_t row_off(const RowMap &rm, uint32_t r, uint32_t n) {
-  const uint32_t in = r % rm.gsize;
   const uint32_t g2 = rm.g2 < rm.gsize ? rm.g2 : rm.gsize;
+  if (rm.fast) {
+    const uint32_t gq = fdiv_q(r, rm.fg), in = r - gq * rm.gsize;
+    const uint32_t q2 = fdiv_q(in, rm.fg2), i2 = in - q2 * g2;
+    return (uint64_t)gq * rm.gstride + (uint64_t)q2 * rm.s2 + (uint64_t)i2 * (rm.s3 ? rm.s3 : n);
+  }
+  const uint32_t in = r % rm.gsize;
   return (uint64_t)(r / rm.gsize) * rm.gstride + (uint64_t)(in / g2) * rm.s2 + (uint64_t)(in % g2) * (rm.s3 ? rm.s3 : n);
 }
 __device__ __forceinline__ uint64_t *row_ptr(uint64_t *base, const RowMap &rm, uint32_t r, uint32_t n) {
   return base + row_off(rm, r, n);
 }
 __device__ __forceinline__ int row_mod(const RowMap &rm, uint32_t r) {
+  if (rm.fast) {
+    const uint32_t a = fdiv_q(r, rm.fmd);
+    return rm.midx[a - fdiv_q(a, rm.fml) * rm.mlen];
+  }
   return rm.midx[(r / rm.mdiv) % rm.mlen];
 }
 
@@ -254,6 +302,7 @@ struct NttEpi {
   uint64_t c0_stride = 0;
   const uint32_t *gal = nullptr;
   uint64_t w[HD_MAXMOD] = {0}, ws[HD_MAXMOD] = {0};
+  FDiv fell, f2ell, fK;  // ell, 2 ell, K (set by ntt_run)
 };
 hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &map, bool inverse, const NttSrc *src,
                   const NttEpi *epi);

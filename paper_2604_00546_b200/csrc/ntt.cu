@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(256, 3) ntt_chunks_kernel(uint64_t *base, RowM
   const bool scale = INV && s1 == 0;
   const bool fin = !INV && final_out;
   // epilogue rows: r = (x 2 + p) ell + l
-  const uint32_t l = row % epi.ell, p = (row / epi.ell) & 1, x = row / (2 * epi.ell);
+  const uint32_t rq = fdiv_q(row, epi.fell), l = row - rq * epi.ell, p = rq & 1, x = fdiv_q(row, epi.f2ell);
   uint64_t *dst = a;
   const uint64_t *Arow = nullptr, *c0row = nullptr;
   uint32_t g = 1;
@@ -296,8 +296,9 @@ __global__ void __launch_bounds__(256, 3) ntt_chunks_kernel(uint64_t *base, RowM
     dst = row_ptr(epi.out, epi.omap, row, n) + off0;
     Arow = epi.A + row_off(epi.amap, row, n) + off0;
     if (epi.mode == 2 && p == 0) {
-      c0row = epi.c0 + (size_t)(x / epi.K) * epi.c0_stride + (size_t)l * n;
-      g = epi.gal[x % epi.K];
+      const uint32_t xk = fdiv_q(x, epi.fK);
+      c0row = epi.c0 + (size_t)xk * epi.c0_stride + (size_t)l * n;
+      g = epi.gal[x - xk * epi.K];
     }
   }
   if (fin && epi.mode) {
@@ -400,18 +401,28 @@ RowMap rowmap_simple(uint32_t mdiv, std::initializer_list<int> mods, uint32_t gs
   return rm;
 }
 
-hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &map, bool inverse, const NttSrc *srcp,
-                  const NttEpi *epip) {
+hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &map_in, bool inverse,
+                  const NttSrc *srcp, const NttEpi *epip) {
   if (rows == 0) return HD_OK;
   const int logn = c->logn;
   const int s2 = logn <= 12 ? logn : 8;  // chunk stages
   const int s1 = logn - s2;              // column stages (0, or 5..8)
   const ulonglong2 *tw = reinterpret_cast<const ulonglong2 *>(inverse ? c->itw2 : c->tw2);
   const uint64_t *ninv = c->ninv_dev;
-  const NttSrc none_src{};
-  const NttEpi none_epi{};
-  const NttSrc src = srcp ? *srcp : none_src;
-  const NttEpi epi = epip ? *epip : none_epi;
+  NttSrc none_src{};
+  NttEpi none_epi{};
+  NttSrc src = srcp ? *srcp : none_src;
+  NttEpi epi = epip ? *epip : none_epi;
+  RowMap map = map_in;  // fast row divisions for the device
+  rowmap_finalize(map);
+  rowmap_finalize(src.map);
+  rowmap_finalize(none_src.map);
+  rowmap_finalize(epi.amap);
+  rowmap_finalize(epi.omap);
+  epi.fell = fdiv_make((uint32_t)epi.ell);
+  epi.f2ell = fdiv_make(2u * (uint32_t)epi.ell);
+  epi.fK = fdiv_make((uint32_t)epi.K);
+  none_epi.fell = none_epi.f2ell = none_epi.fK = fdiv_make(1);
   if (inverse && epi.mode) return hd_fail(HD_E_INVALID_ARG, "epilogue only on forward transforms");
   const int tpt_b = 1 << (s2 - 4);
   const int tpc_b = std::max(1, std::min(256 / tpt_b, 1 << s1));
