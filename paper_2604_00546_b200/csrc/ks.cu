@@ -28,12 +28,13 @@ struct KipAcc {
 __global__ void __launch_bounds__(TPB) kip_kernel(const uint64_t *__restrict__ dig, const uint64_t *__restrict__ c1,
                                                   size_t c1_stride, uint64_t *__restrict__ u, int ell, int K, int L,
                                                   int logn, const uint64_t *const *__restrict__ kptr,
-                                                  const uint32_t *__restrict__ gal, ModTab mt, KipAcc ka) {
+                                                  const uint32_t *__restrict__ gal, ModTab mt, KipAcc ka,
+                                                  FDiv f_ell1, FDiv f_K) {
   const int n = 1 << logn;
   const uint32_t t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
   const uint32_t xe = blockIdx.y;
-  const uint32_t x = xe / (ell + 1), e = xe % (ell + 1);
-  const uint32_t b = x / K, k = x % K;
+  const uint32_t x = fdiv_q(xe, f_ell1), e = xe - x * (ell + 1);
+  const uint32_t b = fdiv_q(x, f_K), k = x - b * K;
   if (t >= (uint32_t)n) return;
   const int gm = (int)e < ell ? (int)e : L;
   const uint32_t g = gal[k];
@@ -146,7 +147,8 @@ hd_status ks_modup(hd_context *c, const uint64_t *c1, size_t c1_stride, uint32_t
 hd_status ks_kip(hd_context *c, const uint64_t *dig, const uint64_t *c1, size_t c1_stride, uint32_t B, uint32_t K,
                  int ell, const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u) {
   kip_kernel<<<grid_pairs(c->n, B * K * (ell + 1)), TPB, 0, c->stream>>>(dig, c1, c1_stride, u, ell, K, c->L, c->logn,
-                                                                        kptr_dev, gal_dev, c->mt, KipAcc{});
+                                                                        kptr_dev, gal_dev, c->mt, KipAcc{},
+                                                                        fdiv_make(ell + 1), fdiv_make(K));
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;
@@ -156,7 +158,7 @@ hd_status ks_kip_accumulate(hd_context *c, const uint64_t *dig, const uint64_t *
                             int ell, const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u) {
   kip_kernel<<<grid_pairs(c->n, B * (ell + 1)), TPB, 0, c->stream>>>(
       dig, ct + (size_t)ell * c->n, ct_stride, u, ell, 1, c->L, c->logn, kptr_dev, gal_dev, c->mt,
-      kip_acc(c, ell, ct, ct_stride));
+      kip_acc(c, ell, ct, ct_stride), fdiv_make(ell + 1), fdiv_make(1));
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;

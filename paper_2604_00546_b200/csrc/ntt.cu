@@ -207,8 +207,8 @@ __global__ void __launch_bounds__(256, 3) ntt_cols_kernel(uint64_t *base, RowMap
   A.q = mt.q[m];
   A.a = row_ptr(base, rm, row, n);
   A.in = in_row(base, rm, src, row, n, m, mt);
-  const uint32_t tr = threadIdx.x % tpc;
-  A.tid = threadIdx.x / tpc;
+  const uint32_t tr = threadIdx.x & (tpc - 1);  // tpc is a power of two (ntt_run)
+  A.tid = threadIdx.x >> (__ffs(tpc) - 1);
   A.c = blockIdx.x * tpc + tr;
   const uint32_t col_stride = pad_idx(1u << S) + 1;  // odd column stride: conflict-free across columns
   A.smt = sm + tr * col_stride;
