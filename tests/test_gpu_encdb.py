@@ -129,3 +129,18 @@ def test_generic_degree2_mac_bit_exact(monkeypatch):
     out = o.scan_aggregate_ct(run.oracle_r(), cfg.n1, cfg.dim, run.oracle_Dct(0), run.ok_steps, run.ok_keys,
                               run.orlk)
     assert (run.ctx.ciphertext_residues(run.outs[0]) == out).all()
+
+
+@pytest.mark.slow
+def test_encrypted_c4_bench_config_sampled_aggregate():
+    """`bench.py --db encrypted` configuration (2^16 ring, 2^20 x 512 encrypted diagonals,
+    103 GB on one GPU): bit-exact on a sampled aggregate, scores everywhere vs cosine."""
+    run = EncRun(CONFIGS["C4"])
+    cfg, o = run.cfg, run.o
+    a = 50
+    out = o.scan_aggregate_ct(run.oracle_r(), cfg.n1, cfg.dim, run.oracle_Dct(a), run.ok_steps, run.ok_keys,
+                              run.orlk)
+    assert (run.ctx.ciphertext_residues(run.outs[a]) == out).all()
+    sc = run.ctx.decrypt_scores(run.sk, run.db.layout, run.outs)
+    assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-3
+    assert sorted(np.argsort(-sc)[:3]) == sorted(run.pos.tolist())

@@ -102,3 +102,18 @@ def test_flat_rejects_encrypted(toy):
     pk = toy.ctx.public_keygen(toy.sk)
     with pytest.raises(hd.HDError):
         toy.ctx.enroll(toy.db_vecs, toy.n1, packing="flat", pk=pk, enc_seed=1)
+
+
+@pytest.mark.slow
+def test_flat_c4_bench_config_sampled_aggregate():
+    """`bench.py --packing flat` configuration (2^16 ring, 2^20 x 512, n1 = 128, all 32
+    aggregates on one GPU): bit-exact on a sampled aggregate, scores everywhere vs cosine."""
+    run = FlatRun(CONFIGS["C4"])
+    o, cfg = run.o, run.cfg
+    r = run.oracle_r()
+    a = 21
+    out = o.scan_aggregate_flat(r, run.n1, cfg.dim, run.oracle_D(a), run.ok_steps, run.ok_keys)
+    assert (run.ctx.ciphertext_residues(run.outs[a]) == out).all()
+    sc = run.ctx.decrypt_scores(run.sk, run.db.layout, run.outs)
+    assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-3
+    assert sorted(np.argsort(-sc)[:3]) == sorted(run.pos.tolist())

@@ -233,7 +233,7 @@ def test_pipelined_queries_match_serial(monkeypatch):
 
 @pytest.mark.slow
 def test_c4_bench_config_sampled_aggregate():
-    """The bench launch configuration (2^16 ring, 2^20 x 512, n1 = 64, all 64 aggregates
+    """The bench launch configuration (2^16 ring, 2^20 x 512, n1 = 128, all 64 aggregates
     on one GPU): bit-exact on a sampled aggregate, scores everywhere vs cosine."""
     cfg = CONFIGS["C4"]
     run = Run(cfg)
