@@ -312,6 +312,30 @@ class Oracle:
             len(steps), _p(keys), _p(out)))
         return out
 
+    def enroll_aggregate_flat_encrypted(self, U, u_first, num_vectors, n1, agg, pk, enc_seed):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        D = u64((U.shape[1], 2, self.L, self.n))
+        _check("enroll_aggregate_flat_encrypted", lib().or_enroll_aggregate_flat_encrypted(
+            C.byref(self.p), _p(U), C.c_int64(u_first), C.c_int64(U.shape[0]), C.c_int64(num_vectors),
+            U.shape[1], n1, C.c_int64(agg), _p(pk), C.c_uint64(enc_seed), _p(D)))
+        return D
+
+    def giant_sum_ct_flat(self, r, n1, N, Dct, j):
+        S = u64((3, self.L, self.n))
+        rc = lib().or_giant_sum_ct_flat(C.byref(self.p), _p(np.ascontiguousarray(r)), n1, N,
+                                        _p(np.ascontiguousarray(Dct)), j, _p(S))
+        if rc == OR_E_RANGE:
+            return None
+        _check("giant_sum_ct_flat", rc)
+        return S
+
+    def scan_aggregate_flat_ct(self, r, n1, N, Dct, steps, keys, rlk):
+        out = u64((2, self.L - 1, self.n))
+        _check("scan_aggregate_flat_ct", lib().or_scan_aggregate_flat_ct(
+            C.byref(self.p), _p(np.ascontiguousarray(r)), n1, N, _p(np.ascontiguousarray(Dct)), _p(rlk), _p(steps),
+            len(steps), _p(keys), _p(out)))
+        return out
+
     def decrypt_scores_flat(self, s_ntt, out_ct, N, agg, num_vectors):
         sc = np.zeros((self.ns // N) * N, dtype=np.float64)
         _check("decrypt_scores_flat", lib().or_decrypt_scores_flat(

@@ -954,6 +954,21 @@ int or_enroll_aggregate_flat(const or_params *p, const double *U, int64_t u_firs
   return rc;
 }
 
+/* BSGS-RTX-TBE as in the paper: the enroller pre-rotates each flat diagonal
+ * plaintext and then encrypts it under the public key (object id agg N + k, R26). */
+int or_enroll_aggregate_flat_encrypted(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                                       int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg,
+                                       const uint64_t *pk, uint64_t enc_seed, uint64_t *Dct) {
+  int L = p->L, n = p->n;
+  uint64_t *Dagg = malloc(sizeof(uint64_t) * (size_t)dim * L * n);
+  int rc = or_enroll_aggregate_flat(p, U, u_first, u_count, num_vectors, dim, n1, agg, Dagg);
+  for (int k = 0; k < dim && rc == OR_OK; k++)
+    rc = or_encrypt_pk(p, pk, Dagg + (size_t)k * L * n, L, enc_seed, (uint32_t)(agg * dim + k),
+                       Dct + (size_t)k * 2 * L * n);
+  free(Dagg);
+  return rc;
+}
+
 /* Keys of the flat schedule: baby {1..n1-1}, giant {j n1 : 1 <= j < ceil(N/n1)}. */
 int or_rotation_steps_flat(const or_params *p, int32_t N, int32_t n1, int32_t *steps, int32_t cap,
                            int32_t *count) {
@@ -1082,12 +1097,28 @@ int or_giant_sum(const or_params *p, const uint64_t *r, int32_t n1, int32_t N,
 /* Encrypted diagonals (NEXT-1): S_j = sum_i EvalMultNoRelin(r[i], Dct_k),
  * the degree-2 tensor (r0 + r1 s)(D0 + D1 s) = d0 + d1 s + d2 s^2 accumulated as
  * d0 += r0 D0, d1 += r0 D1 + r1 D0, d2 += r1 D1.  S: [3][L][n]. */
+static int giant_sum_ct_range(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
+                              int32_t j, int32_t i_lo, int32_t i_hi, uint64_t *S);
 int or_giant_sum_ct(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
                     int32_t j, uint64_t *S) {
-  int n = p->n, L = p->L;
-  size_t ctsz = (size_t)2 * L * n;
   int i_lo = 0 > -j * n1 - N / 2 ? 0 : -j * n1 - N / 2;
   int i_hi = n1 - 1 < N / 2 - 1 - j * n1 ? n1 - 1 : N / 2 - 1 - j * n1;
+  return giant_sum_ct_range(p, r, n1, N, Dct, j, i_lo, i_hi, S);
+}
+/* Flat layout (R27): diagonals j n1 + i, i < n1, below N. */
+int or_giant_sum_ct_flat(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
+                         int32_t j, uint64_t *S) {
+  if (j < 0 || j * n1 >= N) {
+    memset(S, 0, sizeof(uint64_t) * 3 * p->L * p->n);
+    return OR_E_RANGE;
+  }
+  int i_hi = n1 - 1 < N - 1 - j * n1 ? n1 - 1 : N - 1 - j * n1;
+  return giant_sum_ct_range(p, r, n1, N, Dct, j, 0, i_hi, S);
+}
+static int giant_sum_ct_range(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
+                              int32_t j, int32_t i_lo, int32_t i_hi, uint64_t *S) {
+  int n = p->n, L = p->L;
+  size_t ctsz = (size_t)2 * L * n;
   memset(S, 0, sizeof(uint64_t) * 3 * L * n);
   if (i_lo > i_hi) return OR_E_RANGE;
   for (int i = i_lo; i <= i_hi; i++) {
@@ -1219,6 +1250,14 @@ int or_scan_aggregate_flat(const or_params *p, const uint64_t *r, int32_t n1, in
   return scan_hoisted(p, r, n1, N, Dagg, NULL, NULL, 1, steps, nkeys, keys, out, NULL);
 }
 
+/* Encrypted flat scan (BSGS-RTX-TBE with encrypted diagonals, the paper's GPU setting):
+ * S_j = Relinearize(sum_i r[i] (x) Dct'_{j n1 + i}), then as or_scan_aggregate_flat. */
+int or_scan_aggregate_flat_ct(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
+                              const uint64_t *rlk, const int32_t *steps, int32_t nkeys, const uint64_t *keys,
+                              uint64_t *out) {
+  return scan_hoisted(p, r, n1, N, NULL, Dct, rlk, 1, steps, nkeys, keys, out, NULL);
+}
+
 /* S_j of the flat layout (diagonals j n1 + i, i < n1, below N); OR_E_RANGE if empty. */
 int or_giant_sum_flat(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dagg,
                       int32_t j, uint64_t *S) {
@@ -1260,7 +1299,10 @@ static int scan_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32
     or_giant_range(N, n1, &jmin, &jmax);
   }
   for (int j = jmin; j <= jmax && rc == OR_OK; j++) {
-    if (flat) {
+    if (flat && Dct) {
+      if (or_giant_sum_ct_flat(p, r, n1, N, Dct, j, S3) != OR_OK) continue;
+      or_relinearize(p, S3, L, rlk, S);
+    } else if (flat) {
       if (or_giant_sum_flat(p, r, n1, N, Dagg, j, S) != OR_OK) continue;
     } else if (Dct) {
       if (or_giant_sum_ct(p, r, n1, N, Dct, j, S3) != OR_OK) continue; /* empty range */

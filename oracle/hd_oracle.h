@@ -161,6 +161,14 @@ int or_giant_sum_flat(const or_params *p, const uint64_t *r, int32_t n1, int32_t
                       int32_t j, uint64_t *S);
 int or_scan_aggregate_flat(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dagg,
                            const int32_t *steps, int32_t nkeys, const uint64_t *keys, uint64_t *out);
+int or_enroll_aggregate_flat_encrypted(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                                       int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg,
+                                       const uint64_t *pk, uint64_t enc_seed, uint64_t *Dct);
+int or_giant_sum_ct_flat(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
+                         int32_t j, uint64_t *S);
+int or_scan_aggregate_flat_ct(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
+                              const uint64_t *rlk, const int32_t *steps, int32_t nkeys, const uint64_t *keys,
+                              uint64_t *out);
 int or_decrypt_scores_flat(const or_params *p, const uint64_t *s_ntt, const uint64_t *out_ct, int32_t N,
                            int64_t agg, int64_t num_vectors, double *scores);
 

@@ -269,8 +269,6 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
                              uint32_t agg_begin, uint32_t agg_end, hd_database **out) {
   if (!c || !vectors || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
   if (pk && pk->ctx != c) return hd_fail(HD_E_STATE, "public key from another context");
-  if (pk && packing == HD_PACKING_FLAT)
-    return hd_fail(HD_E_INVALID_ARG, "encrypted diagonals are supported with the replicated packing only");
   *out = nullptr;
   hd_layout lay;
   hd_status s = layout_make(c, num_vectors, vector_dim, n1, packing, &lay);

@@ -98,10 +98,34 @@ def test_flat_c2_bit_exact(name, n1):
     assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-6
 
 
-def test_flat_rejects_encrypted(toy):
-    pk = toy.ctx.public_keygen(toy.sk)
-    with pytest.raises(hd.HDError):
-        toy.ctx.enroll(toy.db_vecs, toy.n1, packing="flat", pk=pk, enc_seed=1)
+def test_flat_encrypted_database_bit_exact():
+    """BSGS-RTX-TBE with encrypted diagonals (the paper's GPU setting): pre-rotated flat
+    diagonals encrypted under the public key, degree-2 MAC with the flat ranges,
+    relinearisation, no fold; every residue equals the oracle's."""
+    cfg = CONFIGS["C2"]
+    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
+    o = oracle.Oracle(cfg.log_n, cfg.limbs, seed=1)
+    db_vecs, q, _ = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    steps = ctx.rotation_steps(cfg.dim, cfg.n1, packing="flat")
+    sk, evk = ctx.keygen(steps)
+    ctx.relin_keygen(sk, evk)
+    pk = ctx.public_keygen(sk)
+    db = ctx.enroll(db_vecs, cfg.n1, packing="flat", pk=pk, enc_seed=99)
+    outs = ctx.query(evk, db, ctx.encrypt_query(sk, q, ENC_SEED_BASE))
+    s, s_ntt = o.secret_key()
+    ok_steps, ok_keys = o.keyset(s_ntt, [int(x) for x in steps])
+    opk, orlk = o.public_key(s_ntt), o.relin_key(s_ntt)
+    qct = o.encrypt(s_ntt, o.encode(o.query_slots(q), 2.0 ** 45, cfg.limbs), ENC_SEED_BASE)
+    r = o.baby_steps(qct, cfg.n1, ok_steps, ok_keys)
+    for a in range(db.layout.num_aggregates):
+        v0, v1 = a * o.ns, min(cfg.num_vectors, (a + 1) * o.ns)
+        Dct = o.enroll_aggregate_flat_encrypted(o.normalize_rows(db_vecs[v0:v1]), v0, cfg.num_vectors, cfg.n1, a,
+                                                opk, 99)
+        assert (ctx.test_stage(db, 4, a, cfg.dim - 1) == Dct[-1]).all(), a
+        out = o.scan_aggregate_flat_ct(r, cfg.n1, cfg.dim, Dct, ok_steps, ok_keys, orlk)
+        assert (ctx.ciphertext_residues(outs[a]) == out).all(), a
+    sc = ctx.decrypt_scores(sk, db.layout, outs)
+    assert np.abs(sc - _cos(db_vecs, q)).max() < 1e-6
 
 
 @pytest.mark.slow

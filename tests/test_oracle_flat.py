@@ -99,3 +99,28 @@ def test_flat_encrypted_scan_scores(oracle_mod):
     sc = o.decrypt_scores_flat(s_ntt, out, cfg.dim, 0, cfg.num_vectors)[:cfg.num_vectors]
     assert np.abs(sc - _cos(db, q)).max() < 1e-6
     assert sorted(np.argsort(-sc)[:len(pos)]) == sorted(pos.tolist())
+
+
+def test_flat_encrypted_database_scan(oracle_mod):
+    """BSGS-RTX-TBE with encrypted diagonals (the paper's GPU setting, P:L883-905 with
+    P:L119): the degree-2 flat giant sum is the exact tensor product of the decrypted
+    operands, and the scan decodes to cosine within 1e-6 with the planted matches on top."""
+    from tests.test_oracle_encdb import _dec_poly
+    cfg = CONFIGS["C1"]
+    o = oracle_mod.Oracle(cfg.log_n, cfg.limbs, seed=1)
+    db, q, pos = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    s, s_ntt = o.secret_key()
+    pk, rlk = o.public_key(s_ntt), o.relin_key(s_ntt)
+    steps, keys = o.keyset(s_ntt, o.rotation_steps_flat(cfg.dim, cfg.n1))
+    qct = o.encrypt(s_ntt, o.encode(o.query_slots(q), D45, o.L), 1000)
+    r = o.baby_steps(qct, cfg.n1, steps, keys)
+    Dct = o.enroll_aggregate_flat_encrypted(o.normalize_rows(db), 0, cfg.num_vectors, cfg.n1, 0, pk, 77)
+    j = 1
+    S3 = o.giant_sum_ct_flat(r, cfg.n1, cfg.dim, Dct, j)
+    rhs = sum(_dec_poly(o, s_ntt, r[i]) * _dec_poly(o, s_ntt, Dct[j * cfg.n1 + i]) for i in range(cfg.n1))
+    rhs = rhs % np.array(o.p.moduli[:o.L], dtype=object)[:, None]
+    assert (_dec_poly(o, s_ntt, S3) == rhs).all()
+    out = o.scan_aggregate_flat_ct(r, cfg.n1, cfg.dim, Dct, steps, keys, rlk)
+    sc = o.decrypt_scores_flat(s_ntt, out, cfg.dim, 0, cfg.num_vectors)[:cfg.num_vectors]
+    assert np.abs(sc - _cos(db, q)).max() < 1e-6
+    assert sorted(np.argsort(-sc)[:len(pos)]) == sorted(pos.tolist())
