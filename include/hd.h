@@ -8,6 +8,11 @@
  *     query                -> hd_keygen, hd_encrypt_query
  *   - the enroller normalises, diagonalises, packs and encodes the database
  *     (Alg. enroller_bsgs)                -> hd_enroll
+ *     optionally encrypting the diagonals under the client's public key (the
+ *     paper's threat model; NEXT-1)          -> hd_public_keygen,
+ *                                                        hd_relin_keygen, hd_enroll_encrypted
+ *     and/or in the flat pre-rotated layout (BSGS-RTX-TBE; NEXT-2)
+ *                                                     -> hd_enroll_ex, hd_rotation_steps_ex
  *   - the server evaluates the BSGS scan (Alg. sender-bsgs)
  *                                                     -> hd_query
  *   - the client decrypts and reads the scores (reading R4 of DESIGN.md)
@@ -64,7 +69,7 @@ const char *hd_last_error(void);
 typedef struct hd_context hd_context;       /* params + tables, one device      */
 typedef struct hd_secret_key hd_secret_key; /* client only                      */
 typedef struct hd_eval_keys hd_eval_keys;   /* rotation keys, device-resident   */
-typedef struct hd_database hd_database;     /* diagonal plaintexts of [agg_begin, agg_end) */
+typedef struct hd_database hd_database;     /* diagonals of aggregates [agg_begin, agg_end) */
 typedef struct hd_ciphertext hd_ciphertext; /* device-resident ciphertext       */
 typedef struct hd_public_key hd_public_key; /* encrypted-database mode (R26)     */
 
@@ -175,10 +180,14 @@ hd_status hd_enroll_ex(hd_context *ctx, const hd_enroll_options *opt, const floa
                        uint32_t agg_end, hd_database **out);
 hd_status hd_database_layout(const hd_database *db, hd_layout *out);
 /* The online scan (Alg. sender-bsgs; fold schedule R2): baby steps
- * (hoisted), MAC over all local aggregates, rescale, giant rotations, fold.
- * out[i] receives the score ciphertext (L-1 limbs) of aggregate agg_begin + i;
- * n_out must equal agg_end - agg_begin.  A non-NULL out[i] from a previous call
- * on the same context is overwritten in place (no allocation). */
+ * (hoisted), MAC over all local aggregates, rescale, giant rotations accumulated in
+ * the extended basis with one ModDown per aggregate (R23), fold.  Encrypted databases
+ * relinearise each giant-step sum before its rescale (R26); flat databases have no
+ * fold (R27).  out[i] receives the score ciphertext (L-1 limbs) of aggregate
+ * agg_begin + i; n_out must equal agg_end - agg_begin.  A non-NULL out[i] from a
+ * previous call on the same context is overwritten in place (no allocation), after
+ * any pending hd_ciphertext_export_async of it.  The call is asynchronous with
+ * respect to the host; outputs carry events that later readers wait on. */
 hd_status hd_query(hd_context *ctx, const hd_eval_keys *evk, const hd_database *db,
                    const hd_ciphertext *query, hd_ciphertext **out, size_t n_out);
 /* Cumulative number of CUDA kernels this context has launched (all entry points). */
