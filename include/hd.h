@@ -206,7 +206,11 @@ hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, size_t cap, i
                                size_t *written);
 hd_status hd_ciphertext_import(hd_context *ctx, const void *src, size_t bytes, int src_on_device,
                                hd_ciphertext **out);
-/* In-place import into an existing ciphertext of the same shape (no allocation). */
+/* In-place import into an existing ciphertext of the same shape (no allocation).
+ * Host sources are uploaded asynchronously on the context's upload stream, after the
+ * ciphertext's last reader (the baby steps of an hd_query on it) and last writer; pinned
+ * host memory keeps the copy asynchronous and must stay valid until the ciphertext is
+ * next read or hd_context_synchronize().  Device sources are copied on the context stream. */
 hd_status hd_ciphertext_import_into(hd_ciphertext *ct, const void *src, size_t bytes,
                                     int src_on_device);
 hd_status hd_ciphertext_limbs(const hd_ciphertext *ct, uint32_t *limbs);

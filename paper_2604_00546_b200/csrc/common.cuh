@@ -193,6 +193,7 @@ constexpr static int kPhaseEvents = 9;
   uint64_t launches = 0;  // kernels launched on this context (hd_launch_count)
   cudaStream_t sA = nullptr, sB = nullptr;  // internal streams of the query pipeline
   cudaStream_t sIO = nullptr;               // device->host result downloads (export_async)
+  cudaStream_t sUp = nullptr;               // host->device uploads (import_into from host)
 };
 
 struct hd_secret_key {

@@ -221,6 +221,7 @@ extern "C" void hd_context_destroy(hd_context *c) {
   if (c->sA) cudaStreamDestroy(c->sA);
   if (c->sB) cudaStreamDestroy(c->sB);
   if (c->sIO) cudaStreamDestroy(c->sIO);
+  if (c->sUp) cudaStreamDestroy(c->sUp);
   for (int i = 0; i < hd_context::kPhaseEvents; i++)
     for (int k = 0; k < 64; k++)
       if (c->ev[k][i]) cudaEventDestroy(c->ev[k][i]);
@@ -367,10 +368,19 @@ extern "C" hd_status hd_ciphertext_import_into(hd_ciphertext *ct, const void *sr
     if (s) return s;
     if (h.kind != 1 || h.limbs != ct->limbs) return hd_fail(HD_E_LEVEL, "shape mismatch");
   }
-  if (ct->used) HD_CUDA(cudaStreamWaitEvent(c->stream, ct->used, 0));  // pending async export
-  HD_CUDA(cudaMemcpyAsync(ct->data, (const char *)src + sizeof(Header), payload, kind_of(1, src_on_device),
-                          c->stream));
-  HD_CUDA(cudaEventRecord(ct->ready, c->stream));
+  // Host sources are uploaded on the context's upload stream, ordered only after the
+  // ciphertext's last reader (e.g. the baby steps of the previous hd_query on it) and last
+  // writer, so the upload of the next query overlaps the current scan.  Device sources
+  // (e.g. an NCCL broadcast buffer) are ordered on the caller's stream that produced them.
+  cudaStream_t s = c->stream;
+  if (!src_on_device) {
+    if (!c->sUp) HD_CUDA(cudaStreamCreateWithFlags(&c->sUp, cudaStreamNonBlocking));
+    s = c->sUp;  // not behind the result downloads on sIO
+    HD_CUDA(cudaStreamWaitEvent(s, ct->ready, 0));
+  }
+  if (ct->used) HD_CUDA(cudaStreamWaitEvent(s, ct->used, 0));  // pending readers
+  HD_CUDA(cudaMemcpyAsync(ct->data, (const char *)src + sizeof(Header), payload, kind_of(1, src_on_device), s));
+  HD_CUDA(cudaEventRecord(ct->ready, s));
   return HD_OK;
 }
 
@@ -386,7 +396,10 @@ extern "C" hd_status hd_ciphertext_export_async(hd_ciphertext *ct, uint32_t nlim
   if (!dst) return HD_OK;
   if (cap < total) return hd_fail(HD_E_INVALID_ARG, "export capacity too small");
   if (!c->sIO) HD_CUDA(cudaStreamCreateWithFlags(&c->sIO, cudaStreamNonBlocking));
-  if (!ct->used) HD_CUDA(cudaEventCreateWithFlags(&ct->used, cudaEventDisableTiming));
+  if (!ct->used) {
+    HD_CUDA(cudaEventCreateWithFlags(&ct->used, cudaEventDisableTiming));
+    HD_CUDA(cudaEventRecord(ct->used, c->sIO));
+  }
   Header h{};
   memcpy(h.magic, "HDBSGS01", 8);
   h.kind = 1;
@@ -399,6 +412,7 @@ extern "C" hd_status hd_ciphertext_export_async(hd_ciphertext *ct, uint32_t nlim
   else
     memcpy(dst, &h, sizeof(h));
   HD_CUDA(cudaStreamWaitEvent(c->sIO, ct->ready, 0));
+  HD_CUDA(cudaStreamWaitEvent(c->sIO, ct->used, 0));  // the new `used` covers earlier readers too
   char *p = (char *)dst + sizeof(h);
   const cudaMemcpyKind kind = kind_of(dst_on_device, 1);
   // c0 limbs 0..nlimbs-1, then c1 limbs 0..nlimbs-1 (dropping the top limbs: R24)
@@ -411,7 +425,7 @@ extern "C" hd_status hd_ciphertext_export_async(hd_ciphertext *ct, uint32_t nlim
 
 extern "C" hd_status hd_context_synchronize(hd_context *c) {
   if (!c) return hd_fail(HD_E_INVALID_ARG, "null context");
-  for (cudaStream_t s : {c->stream, c->sA, c->sB, c->sIO})
+  for (cudaStream_t s : {c->stream, c->sA, c->sB, c->sIO, c->sUp})
     if (s || s == c->stream) HD_CUDA(cudaStreamSynchronize(s));
   return HD_OK;
 }

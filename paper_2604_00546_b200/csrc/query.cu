@@ -75,6 +75,12 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
   // the baby steps + MAC of this query can run while B still finishes the previous one.
   HD_CUDA(cudaEventRecord(db->ev_in, caller));
   HD_CUDA(cudaStreamWaitEvent(sa, query->ready, 0));
+  hd_ciphertext *qmut = const_cast<hd_ciphertext *>(query);  // reader bookkeeping only
+  if (!qmut->used) {
+    HD_CUDA(cudaEventCreateWithFlags(&qmut->used, cudaEventDisableTiming));
+  } else {
+    HD_CUDA(cudaStreamWaitEvent(sa, qmut->used, 0));  // the new `used` covers earlier readers too
+  }
   if (db->qcount >= 2) HD_CUDA(cudaStreamWaitEvent(sa, db->ev_sfree[par], 0));
   c->stream = sa;
   cudaEventRecord(E[0], sa);
@@ -95,6 +101,7 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
       return s;
   }
   cudaEventRecord(E[1], sa);
+  HD_CUDA(cudaEventRecord(qmut->used, sa));  // the query is not read after the baby steps
   // ---- MAC ----
   if (db->encrypted) {
     if ((s = mac_ct_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js, db->flat))) return s;
