@@ -231,6 +231,38 @@ def test_pipelined_queries_match_serial(monkeypatch):
     assert all((run.ctx.ciphertext_residues(o) == w).all() for o, w in zip(outs, ref2))
 
 
+def test_streamed_host_queries_match_serial(monkeypatch):
+    """The end-to-end pattern of bench.py: host query bytes imported in place into two
+    alternating ciphertexts (upload stream, ordered after the previous query's baby steps),
+    outputs reused in place and downloaded asynchronously -- every downloaded result equals
+    the serial one, although nothing synchronises the host between steps."""
+    cfg = CONFIGS["C1"]
+    run = Run(cfg)
+    ctx = run.ctx
+    qs = [run.qct, ctx.encrypt_query(run.sk, run.q[::-1].copy(), ENC_SEED_BASE + 1)]
+    monkeypatch.setenv("HD_SERIAL", "1")
+    refs = [[ctx.ciphertext_residues(o) for o in ctx.query(run.evk, run.db, qq)] for qq in qs]
+    monkeypatch.setenv("HD_SERIAL", "0")
+    blobs = [torch.from_numpy(ctx.ciphertext_export(qq)).pin_memory() for qq in qs]
+    qin = [ctx.ciphertext_import(blobs[0].numpy()), ctx.ciphertext_import(blobs[0].numpy())]
+    sz = ctx.ciphertext_export_async(run.outs[0], None)
+    steps = 6
+    host = torch.empty(steps * len(run.outs) * sz, dtype=torch.uint8, pin_memory=True)
+    outs = None
+    for k in range(steps):
+        ctx.ciphertext_import_into(qin[k % 2], blobs[k % 2].data_ptr(), blobs[k % 2].numel(), on_device=False)
+        outs = ctx.query(run.evk, run.db, qin[k % 2], outs)
+        for i, o in enumerate(outs):
+            ctx.ciphertext_export_async(o, (host.data_ptr() + (k * len(outs) + i) * sz, sz))
+    ctx.synchronize()
+    buf = host.numpy()
+    for k in range(steps):
+        for i in range(len(outs)):
+            off = (k * len(outs) + i) * sz
+            got = buf[off + 64:off + sz].view(np.uint64).reshape(2, -1, ctx.n)
+            assert (got == refs[k % 2][i]).all(), (k, i)
+
+
 @pytest.mark.slow
 def test_c4_bench_config_sampled_aggregate():
     """The bench launch configuration (2^16 ring, 2^20 x 512, n1 = 128, all 64 aggregates
