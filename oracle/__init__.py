@@ -320,6 +320,20 @@ class Oracle:
             U.shape[1], n1, C.c_int64(agg), _p(pk), C.c_uint64(enc_seed), _p(D)))
         return D
 
+    def enroll_aggregate_flat_tbs(self, U, u_first, num_vectors, n1, agg, pk, enc_seed):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        D = u64((U.shape[1], 2, self.L, self.n))
+        _check("enroll_aggregate_flat_tbs", lib().or_enroll_aggregate_flat_tbs(
+            C.byref(self.p), _p(U), C.c_int64(u_first), C.c_int64(U.shape[0]), C.c_int64(num_vectors),
+            U.shape[1], n1, C.c_int64(agg), _p(pk), C.c_uint64(enc_seed), _p(D)))
+        return D
+
+    def prerotate_tbs(self, Dct, n1, steps, keys):
+        D = np.ascontiguousarray(Dct).copy()
+        _check("prerotate_tbs", lib().or_prerotate_tbs(C.byref(self.p), _p(D), D.shape[0], n1, _p(steps), len(steps),
+                                                       _p(keys)))
+        return D
+
     def giant_sum_ct_flat(self, r, n1, N, Dct, j):
         S = u64((3, self.L, self.n))
         rc = lib().or_giant_sum_ct_flat(C.byref(self.p), _p(np.ascontiguousarray(r)), n1, N,

@@ -920,8 +920,16 @@ int or_enroll_aggregate_encrypted(const or_params *p, const double *U, int64_t u
  *   diag_k[b N + t] = group_{agg M + b}[t][(t + k) mod N]   (0 beyond the database),
  * and the enroller's plaintext pre-rotation (Eq. eq:prerotation):
  *   diag'_k = Rot_{-j n1}(diag_k),  j = floor(k / n1),  i.e. diag'_k[s] = diag_k[s - j n1]. */
+static int flat_slots(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                      int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, int32_t k, int prerotate,
+                      double *z);
 int or_enroll_slots_flat(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
                          int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, int32_t k, double *z) {
+  return flat_slots(p, U, u_first, u_count, num_vectors, dim, n1, agg, k, 1, z);
+}
+static int flat_slots(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                      int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, int32_t k, int prerotate,
+                      double *z) {
   int ns = p->num_slots;
   if (dim < 2 || n1 < 1 || (dim & (dim - 1)) != 0 || ns % dim != 0) return OR_E_LAYOUT;
   int N = dim, M = ns / N;
@@ -935,7 +943,7 @@ int or_enroll_slots_flat(const or_params *p, const double *U, int64_t u_first, i
       if (v < u_first || v >= u_first + u_count) { free(diag); return OR_E_ARG; }
       diag[b * N + t] = U[(size_t)(v - u_first) * dim + (t + k) % N];
     }
-  int sh = (k / n1) * n1; /* Rot_{-j n1} */
+  int sh = prerotate ? (k / n1) * n1 : 0; /* Rot_{-j n1} */
   for (int s = 0; s < ns; s++) z[s] = diag[((s - sh) % ns + ns) % ns];
   free(diag);
   return OR_OK;
@@ -951,6 +959,45 @@ int or_enroll_aggregate_flat(const or_params *p, const double *U, int64_t u_firs
     if (rc == OR_OK) rc = or_encode(p, z, (double)p->mod[p->L - 1], p->L, Dagg + (size_t)k * p->L * p->n);
   }
   free(z);
+  return rc;
+}
+
+/* BSGS-RTX-TBS: the enroller encrypts the plain flat (HyDia) diagonals; the
+ * server pre-rotates them homomorphically, diag'_k = Rot_{-j n1}(Dct_k) for j = floor(k/n1)
+ * >= 1, with the negative giant-step keys numSlots - j n1 (or_prerotate_tbs). */
+int or_enroll_aggregate_flat_tbs(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                                 int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, const uint64_t *pk,
+                                 uint64_t enc_seed, uint64_t *Dct) {
+  int ns = p->num_slots, L = p->L, n = p->n;
+  double *z = malloc(sizeof(double) * ns);
+  uint64_t *pt = malloc(sizeof(uint64_t) * (size_t)L * n);
+  int rc = OR_OK;
+  for (int k = 0; k < dim && rc == OR_OK; k++) {
+    rc = flat_slots(p, U, u_first, u_count, num_vectors, dim, n1, agg, k, 0, z);
+    if (rc == OR_OK) rc = or_encode(p, z, (double)p->mod[L - 1], L, pt);
+    if (rc == OR_OK)
+      rc = or_encrypt_pk(p, pk, pt, L, enc_seed, (uint32_t)(agg * dim + k), Dct + (size_t)k * 2 * L * n);
+  }
+  free(z); free(pt);
+  return rc;
+}
+
+static const uint64_t *find_key(const or_params *p, const int32_t *steps, int32_t nkeys,
+                                const uint64_t *keys, int64_t step);
+int or_prerotate_tbs(const or_params *p, uint64_t *Dct, int32_t dim, int32_t n1, const int32_t *steps,
+                     int32_t nkeys, const uint64_t *keys) {
+  int ns = p->num_slots, L = p->L, n = p->n;
+  size_t ct = (size_t)2 * L * n;
+  uint64_t *tmp = malloc(sizeof(uint64_t) * ct);
+  int rc = OR_OK;
+  for (int k = n1; k < dim && rc == OR_OK; k++) {
+    int step = ns - (k / n1) * n1;
+    const uint64_t *key = find_key(p, steps, nkeys, keys, step);
+    if (!key) { rc = OR_E_MISSING_KEY; break; }
+    rc = or_rotate(p, Dct + (size_t)k * ct, L, key, step, tmp);
+    if (rc == OR_OK) memcpy(Dct + (size_t)k * ct, tmp, sizeof(uint64_t) * ct);
+  }
+  free(tmp);
   return rc;
 }
 

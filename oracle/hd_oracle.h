@@ -164,6 +164,13 @@ int or_scan_aggregate_flat(const or_params *p, const uint64_t *r, int32_t n1, in
 int or_enroll_aggregate_flat_encrypted(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
                                        int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg,
                                        const uint64_t *pk, uint64_t enc_seed, uint64_t *Dct);
+/* BSGS-RTX-TBS: plain flat diagonals encrypted by the enroller, pre-rotated by
+ * the server with the negative giant-step keys numSlots - j n1 (in place, eager ModDown). */
+int or_enroll_aggregate_flat_tbs(const or_params *p, const double *U, int64_t u_first, int64_t u_count,
+                                 int64_t num_vectors, int32_t dim, int32_t n1, int64_t agg, const uint64_t *pk,
+                                 uint64_t enc_seed, uint64_t *Dct);
+int or_prerotate_tbs(const or_params *p, uint64_t *Dct, int32_t dim, int32_t n1, const int32_t *steps,
+                     int32_t nkeys, const uint64_t *keys);
 int or_giant_sum_ct_flat(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,
                          int32_t j, uint64_t *S);
 int or_scan_aggregate_flat_ct(const or_params *p, const uint64_t *r, int32_t n1, int32_t N, const uint64_t *Dct,

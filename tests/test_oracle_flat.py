@@ -124,3 +124,33 @@ def test_flat_encrypted_database_scan(oracle_mod):
     sc = o.decrypt_scores_flat(s_ntt, out, cfg.dim, 0, cfg.num_vectors)[:cfg.num_vectors]
     assert np.abs(sc - _cos(db, q)).max() < 1e-6
     assert sorted(np.argsort(-sc)[:len(pos)]) == sorted(pos.tolist())
+
+
+def test_flat_tbs_server_prerotation(oracle_mod):
+    """BSGS-RTX-TBS: plain flat diagonals encrypted by the enroller, pre-rotated
+    homomorphically by the server with the negative giant-step keys.  Each pre-rotated
+    ciphertext decrypts to the enroller-side pre-rotated (TBE) plaintext within the
+    key-switching noise, and the scan decodes to cosine like TBE."""
+    from tests.test_oracle_scan import _centred_coeffs
+    cfg = CONFIGS["C1"]
+    o = oracle_mod.Oracle(cfg.log_n, cfg.limbs, seed=1)
+    db, q, pos = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    N, n1 = cfg.dim, cfg.n1
+    s, s_ntt = o.secret_key()
+    pk, rlk = o.public_key(s_ntt), o.relin_key(s_ntt)
+    neg = [o.ns - j * n1 for j in range(1, -(-N // n1))]
+    steps, keys = o.keyset(s_ntt, sorted(set(o.rotation_steps_flat(N, n1)) | set(neg)))
+    U = o.normalize_rows(db)
+    Dtbs = o.prerotate_tbs(o.enroll_aggregate_flat_tbs(U, 0, cfg.num_vectors, n1, 0, pk, 5), n1, steps, keys)
+    Dtbe = o.enroll_aggregate_flat(U, 0, cfg.num_vectors, n1, 0)   # plaintext pre-rotated by the enroller
+    mods = np.array(o.p.moduli[:o.L], dtype=object)[:, None]
+    for k in (0, n1, N - 1):
+        diff = _centred_coeffs(o, ((o.decrypt(s_ntt, Dtbs[k]).astype(object) - Dtbe[k].astype(object)) % mods)
+                               .astype(np.uint64))
+        assert max(abs(d) for d in diff) < 2 ** 20, k
+    qct = o.encrypt(s_ntt, o.encode(o.query_slots(q), D45, o.L), 1000)
+    r = o.baby_steps(qct, n1, steps, keys)
+    out = o.scan_aggregate_flat_ct(r, n1, N, Dtbs, steps, keys, rlk)
+    sc = o.decrypt_scores_flat(s_ntt, out, N, 0, cfg.num_vectors)[:cfg.num_vectors]
+    assert np.abs(sc - _cos(db, q)).max() < 1e-6
+    assert sorted(np.argsort(-sc)[:len(pos)]) == sorted(pos.tolist())
