@@ -99,7 +99,11 @@ typedef struct {
  * P:L883-905): HyDia packing with M groups per ciphertext and no gaps, diagonals
  * pre-rotated by the enroller (diag'_k = Rot_{-floor(k/n1) n1}(diag_k)), giant steps
  * k = j n1 + i with j >= 0 rotated by j n1 online, no fold: half the diagonal bytes. */
-enum { HD_PACKING_REPLICATED = 0, HD_PACKING_FLAT = 1 };
+enum { HD_PACKING_REPLICATED = 0, HD_PACKING_FLAT = 1, HD_PACKING_FLAT_TBS = 2 };
+/* FLAT_TBS (BSGS-RTX-TBS): encrypted flat diagonals enrolled WITHOUT the
+ * enroller's pre-rotation; the server pre-rotates them homomorphically once with
+ * hd_database_prerotate (negative giant-step keys numSlots - j n1, hd_prerotation_steps)
+ * before the first hd_query (HD_E_STATE otherwise).  Requires a public key. */
 
 /* Options of hd_enroll_ex: packing, and for the encrypted-database mode (NEXT-1)
  * the public key and the enroller's encryption seed (pk = NULL: plaintext diagonals). */
@@ -179,6 +183,13 @@ hd_status hd_enroll_ex(hd_context *ctx, const hd_enroll_options *opt, const floa
                        uint64_t num_vectors, uint32_t vector_dim, uint32_t n1, uint32_t agg_begin,
                        uint32_t agg_end, hd_database **out);
 hd_status hd_database_layout(const hd_database *db, hd_layout *out);
+/* Keys of the TBS pre-rotation: {numSlots - j n1 : 1 <= j < ceil(N/n1)} (ascending). */
+hd_status hd_prerotation_steps(const hd_context *ctx, uint32_t vector_dim, uint32_t n1, int32_t *steps,
+                               size_t cap, size_t *count);
+/* Server-side pre-rotation of a FLAT_TBS database, in place: Dct_k <- Rot_{-j n1}(Dct_k)
+ * for every diagonal k with j = floor(k / n1) >= 1 (full key switch per diagonal, batched
+ * per (aggregate, j)).  evk must hold the pre-rotation keys (HD_E_MISSING_KEY). */
+hd_status hd_database_prerotate(hd_context *ctx, const hd_eval_keys *evk, hd_database *db);
 /* The online scan (Alg. sender-bsgs; fold schedule R2): baby steps
  * (hoisted), MAC over all local aggregates, rescale, giant rotations accumulated in
  * the extended basis with one ModDown per aggregate (R23), fold.  Encrypted databases

@@ -34,7 +34,7 @@ ABI_FUNCTIONS = [
     "hd_secret_key_destroy", "hd_database_destroy", "hd_test_ntt", "hd_test_stage", "hd_test_rotate",
     "hd_test_rescale", "hd_ciphertext_export_async", "hd_context_synchronize", "hd_enroll_encrypted",
     "hd_public_keygen", "hd_public_key_export", "hd_public_key_import", "hd_relin_keygen", "hd_public_key_destroy",
-    "hd_enroll_ex", "hd_rotation_steps_ex",
+    "hd_enroll_ex", "hd_rotation_steps_ex", "hd_prerotation_steps", "hd_database_prerotate",
 ]
 
 
@@ -58,7 +58,7 @@ class Layout(C.Structure):
                 ("agg_end", C.c_uint32), ("packing", C.c_uint32), ("reserved", C.c_uint32)]
 
 
-PACKING = {"replicated": 0, "flat": 1}  # HD_PACKING_* (flat: NEXT-2, R27)
+PACKING = {"replicated": 0, "flat": 1, "flat_tbs": 2}  # HD_PACKING_* (flat: NEXT-2, R27; flat_tbs: TBS)
 
 
 class EnrollOptions(C.Structure):
@@ -119,6 +119,8 @@ def load():
                                        C.POINTER(VP)]
             L.hd_rotation_steps_ex.argtypes = [VP, C.c_uint32, C.c_uint32, C.c_uint32, VP, C.c_size_t,
                                                C.POINTER(C.c_size_t)]
+            L.hd_prerotation_steps.argtypes = [VP, C.c_uint32, C.c_uint32, VP, C.c_size_t, C.POINTER(C.c_size_t)]
+            L.hd_database_prerotate.argtypes = [VP, VP, VP]
             L.hd_public_key_export.argtypes = [VP, VP, C.c_size_t]
             L.hd_public_key_import.argtypes = [VP, VP, C.c_size_t, C.POINTER(VP)]
             L.hd_relin_keygen.argtypes = [VP, VP, VP]
@@ -297,6 +299,18 @@ class Context(_Handle):
         out = VP()
         _check("hd_public_key_import", load().hd_public_key_import(self.h, _ptr(arr), arr.size, C.byref(out)))
         return PublicKey(out.value, self)
+
+    def prerotation_steps(self, vector_dim, n1):
+        """Negative giant-step keys of the TBS server-side pre-rotation."""
+        cnt = C.c_size_t()
+        _check("hd_prerotation_steps", load().hd_prerotation_steps(self.h, vector_dim, n1, None, 0, C.byref(cnt)))
+        steps = np.zeros(cnt.value, np.int32)
+        _check("hd_prerotation_steps", load().hd_prerotation_steps(self.h, vector_dim, n1, _ptr(steps), cnt.value,
+                                                                   C.byref(cnt)))
+        return steps
+
+    def database_prerotate(self, evk, db):
+        _check("hd_database_prerotate", load().hd_database_prerotate(self.h, evk.h, db.h))
 
     def relin_keygen(self, sk, evk):
         _check("hd_relin_keygen", load().hd_relin_keygen(self.h, sk.h, evk.h))

@@ -401,7 +401,7 @@ extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, c
                                        size_t *written) {
   if (!c || !sk || !lay || !cts || !scores) return hd_fail(HD_E_INVALID_ARG, "null argument");
   const int n = c->n, ns = c->ns, N = (int)lay->block_n, M = (int)lay->blocks_m;
-  const int G = (int)lay->groups_per_ct, stride = lay->packing == HD_PACKING_FLAT ? N : 2 * N;
+  const int G = (int)lay->groups_per_ct, stride = lay->packing == HD_PACKING_REPLICATED ? 2 * N : N;
   const long long per = (long long)G * N;
   const long long v_first = (long long)lay->agg_begin * per;
   const long long v_end = std::min<long long>((long long)lay->num_vectors, (long long)(lay->agg_begin + n_ct) * per);

@@ -241,6 +241,7 @@ struct hd_database {
                                  // [A_loc][N][2][L][n] diagonal ciphertexts (encrypted)
   bool encrypted = false;        // encrypted-database mode (NEXT-1, R26)
   bool flat = false;             // flat pre-rotated packing (NEXT-2, R27): no fold
+  bool needs_prerotation = false;  // FLAT_TBS before hd_database_prerotate
   uint32_t spoly = 2;            // polynomials per giant-step sum: 2, or 3 (degree 2) encrypted
   // query workspaces (allocated at enrollment; reused by every hd_query)
   uint64_t *r = nullptr;         // [n1][2][L][n] baby steps

@@ -62,13 +62,13 @@ __global__ void pack_kernel(const double *__restrict__ U, long long v_first, lon
 // diag_k[(s - j n1) mod ns], j = floor(k / n1), with diag_k[b N + t] =
 // U[(agg M + b) N + t][(t + k) mod N] (0 beyond the database), M = ns / N, no gaps.
 __global__ void pack_flat_kernel(const double *__restrict__ U, long long v_first, long long num_vectors, int N,
-                                 int M, int n1, long long agg, int k0, int ns, double *__restrict__ re,
+                                 int M, int n1, long long agg, int k0, int ns, int prerotate, double *__restrict__ re,
                                  double *__restrict__ im) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   const int kk = blockIdx.y;
   if (s >= ns) return;
   const int k = k0 + kk;
-  const int src = ((s - (k / n1) * n1) % ns + ns) % ns;  // Rot_{-j n1}
+  const int src = prerotate ? ((s - (k / n1) * n1) % ns + ns) % ns : s;  // Rot_{-j n1} (TBE) or none (TBS)
   const int b = src / N, t = src % N;
   const long long v = (agg * M + b) * N + t;
   double val = 0.0;
@@ -174,7 +174,8 @@ static int floordiv_i(int a, int b) { return a >= 0 ? a / b : -((-a + b - 1) / b
 hd_status layout_make(const hd_context *c, uint64_t K, uint32_t dim, uint32_t n1, uint32_t packing,
                       hd_layout *lay) {
   if (dim < 2 || n1 < 1 || K < 1) return hd_fail(HD_E_INVALID_ARG, "vector_dim >= 2, n1 >= 1, num_vectors >= 1");
-  if (packing != HD_PACKING_REPLICATED && packing != HD_PACKING_FLAT) return hd_fail(HD_E_INVALID_ARG, "packing");
+  if (packing != HD_PACKING_REPLICATED && packing != HD_PACKING_FLAT && packing != HD_PACKING_FLAT_TBS)
+    return hd_fail(HD_E_INVALID_ARG, "packing");
   if ((dim & (dim - 1)) != 0 || (uint32_t)c->ns % (2 * dim) != 0)
     return hd_fail(HD_E_LAYOUT, "vector_dim must be a power of two with numSlots % (2 vector_dim) == 0");
   memset(lay, 0, sizeof(*lay));
@@ -190,7 +191,7 @@ hd_status layout_make(const hd_context *c, uint64_t K, uint32_t dim, uint32_t n1
   lay->giant_min = floordiv_i(-(int)(dim / 2), (int)n1);                      // R6
   lay->giant_max = floordiv_i((int)(dim / 2) - 1, (int)n1);
   lay->packing = packing;
-  if (packing == HD_PACKING_FLAT) {  // R27: M groups per ciphertext, j = 0 .. ceil(N/n1) - 1
+  if (packing != HD_PACKING_REPLICATED) {  // R27: M groups per ciphertext, j = 0 .. ceil(N/n1) - 1
     lay->groups_per_ct = lay->blocks_m;
     lay->num_aggregates = (lay->num_groups + lay->blocks_m - 1) / lay->blocks_m;
     lay->giant_min = 0;
@@ -208,7 +209,7 @@ extern "C" hd_status hd_rotation_steps_ex(const hd_context *c, uint32_t vector_d
   const int N = (int)vector_dim, ns = c->ns;
   std::vector<char> used(ns, 0);
   for (uint32_t i = 1; i < n1; i++) used[i % ns] = 1;
-  if (packing == HD_PACKING_FLAT) {  // giant j n1, no fold (R27)
+  if (packing != HD_PACKING_REPLICATED) {  // giant j n1, no fold (R27)
     for (int j = 1; j <= lay.giant_max; j++) used[((int)n1 * j) % ns] = 1;
   } else {
     for (int j = lay.giant_min; j <= lay.giant_max; j++) {
@@ -269,6 +270,8 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
                              uint32_t agg_begin, uint32_t agg_end, hd_database **out) {
   if (!c || !vectors || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
   if (pk && pk->ctx != c) return hd_fail(HD_E_STATE, "public key from another context");
+  if (packing == HD_PACKING_FLAT_TBS && !pk)
+    return hd_fail(HD_E_INVALID_ARG, "FLAT_TBS packing needs a public key (encrypted diagonals)");
   *out = nullptr;
   hd_layout lay;
   hd_status s = layout_make(c, num_vectors, vector_dim, n1, packing, &lay);
@@ -288,7 +291,8 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
   db->encrypted = pk != nullptr;
   db->spoly = pk ? 3 : 2;
   const int N = (int)db->N, L = c->L, n = c->n, ns = c->ns;
-  db->flat = packing == HD_PACKING_FLAT;
+  db->flat = packing != HD_PACKING_REPLICATED;
+  db->needs_prerotation = packing == HD_PACKING_FLAT_TBS;
   for (int j = lay.giant_min; j <= lay.giant_max; j++) {
     if (db->flat) {  // R27: diagonals j n1 .. j n1 + n1 - 1 (< N), rotation j n1
       db->js.push_back(j);
@@ -404,7 +408,8 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
       int kb = std::min(KB, N - k0);
       if (db->flat)
         pack_flat_kernel<<<dim3((ns + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(
-            U, (long long)v0, (long long)num_vectors, N, db->M, n1, a, k0, ns, re, im);
+            U, (long long)v0, (long long)num_vectors, N, db->M, n1, a, k0, ns, packing == HD_PACKING_FLAT ? 1 : 0, re,
+            im);
       else
         pack_kernel<<<dim3((ns + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(U, (long long)v0, (long long)num_vectors,
                                                                            N, db->M, n1, a, k0, ns, re, im);

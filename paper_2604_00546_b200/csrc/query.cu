@@ -215,6 +215,7 @@ extern "C" hd_status hd_query(hd_context *c, const hd_eval_keys *evk, const hd_d
   if (db->ctx != c || evk->ctx != c || query->ctx != c) return hd_fail(HD_E_STATE, "objects from another context");
   if (query->limbs != (uint32_t)c->L) return hd_fail(HD_E_LEVEL, "query must be at L limbs");
   if (n_out != db->A_loc) return hd_fail(HD_E_INVALID_ARG, "n_out must equal agg_end - agg_begin");
+  if (db->needs_prerotation) return hd_fail(HD_E_STATE, "FLAT_TBS database: call hd_database_prerotate first");
   const int L = c->L, n = c->n;
   const size_t ct1 = (size_t)2 * (L - 1) * n;
   hd_status s = bind_keys(db, evk);
@@ -388,3 +389,74 @@ extern "C" hd_status hd_test_rescale(hd_context *c, const hd_ciphertext *ct, hd_
   *out = o;
   return HD_OK;
 }
+
+// ---------------------------------------------------------------------------
+// BSGS-RTX-TBS server-side pre-rotation: Dct_k <- Rot_{-j n1}(Dct_k).
+// ---------------------------------------------------------------------------
+extern "C" hd_status hd_prerotation_steps(const hd_context *c, uint32_t vector_dim, uint32_t n1, int32_t *steps,
+                                          size_t cap, size_t *count) {
+  if (!c || !count || n1 < 1 || vector_dim < 2) return hd_fail(HD_E_INVALID_ARG, "bad argument");
+  std::vector<int32_t> v;
+  for (uint32_t j = 1; j * n1 < vector_dim; j++) v.push_back(c->ns - (int32_t)(j * n1 % (uint32_t)c->ns));
+  std::sort(v.begin(), v.end());
+  *count = v.size();
+  if (steps) {
+    if (cap < v.size()) return hd_fail(HD_E_INVALID_ARG, "steps capacity too small");
+    for (size_t i = 0; i < v.size(); i++) steps[i] = v[i];
+  }
+  return HD_OK;
+}
+
+extern "C" hd_status hd_database_prerotate(hd_context *c, const hd_eval_keys *evk, hd_database *db) {
+  if (!c || !evk || !db) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  if (db->ctx != c || evk->ctx != c) return hd_fail(HD_E_STATE, "objects from another context");
+  if (!db->needs_prerotation) return hd_fail(HD_E_STATE, "not a FLAT_TBS database awaiting pre-rotation");
+  HD_CUDA(cudaSetDevice(c->device));
+  const int n = c->n, L = c->L, N = (int)db->N, n1 = (int)db->n1;
+  const size_t ct = (size_t)2 * L * n;
+  const uint32_t Bmax = (uint32_t)std::min(n1, N);
+  uint64_t *dig = nullptr, *tmp = nullptr, *u = nullptr, *out = nullptr, **kp = nullptr;
+  uint32_t *gal = nullptr;
+  cudaError_t e = cudaMalloc(&dig, (size_t)Bmax * L * L * n * 8);
+  if (!e) e = cudaMalloc(&tmp, (size_t)Bmax * 2 * L * n * 8);
+  if (!e) e = cudaMalloc(&u, (size_t)Bmax * 2 * (L + 1) * n * 8);
+  if (!e) e = cudaMalloc(&out, (size_t)Bmax * ct * 8);
+  if (!e) e = cudaMalloc(&kp, sizeof(uint64_t *));
+  if (!e) e = cudaMalloc(&gal, sizeof(uint32_t));
+  hd_status s = e ? hd_fail(HD_E_CAPACITY, "pre-rotation scratch") : HD_OK;
+  for (int j = 1; !s && j * n1 < N; j++) {
+    const int32_t step = c->ns - (j * n1) % c->ns;
+    const uint64_t *key = evk->find(step);
+    if (!key) {
+      s = hd_fail(HD_E_MISSING_KEY, "missing rotation key for step " + std::to_string(step));
+      break;
+    }
+    const uint32_t g = (uint32_t)host_powmod(5, (uint64_t)step, 2ull * n);
+    if ((e = cudaMemcpyAsync(kp, &key, sizeof(key), cudaMemcpyHostToDevice, c->stream)) ||
+        (e = cudaMemcpyAsync(gal, &g, sizeof(g), cudaMemcpyHostToDevice, c->stream))) {
+      s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+      break;
+    }
+    const uint32_t B = (uint32_t)std::min(n1, N - j * n1);
+    for (uint32_t a = 0; a < db->A_loc && !s; a++) {
+      uint64_t *base = db->D + ((size_t)a * N + (size_t)j * n1) * ct;  // diagonals j n1 .. j n1 + B - 1
+      if ((s = ks_modup(c, base + (size_t)L * n, ct, B, L, dig, tmp))) break;
+      if ((s = ks_kip(c, dig, base + (size_t)L * n, ct, B, 1, L, kp, gal, u))) break;
+      if ((s = ks_moddown(c, u, B, 1, L, gal, base, ct, out, ct, false, tmp))) break;
+      if ((e = cudaMemcpyAsync(base, out, (size_t)B * ct * 8, cudaMemcpyDeviceToDevice, c->stream)))
+        s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+    }
+    // the host-side key / Galois values must stay valid until their copies ran
+    if (!s && (e = cudaStreamSynchronize(c->stream))) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  }
+  if (!s && (e = cudaStreamSynchronize(c->stream))) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  cudaFree(dig);
+  cudaFree(tmp);
+  cudaFree(u);
+  cudaFree(out);
+  cudaFree(kp);
+  cudaFree(gal);
+  if (!s) db->needs_prerotation = false;
+  return s;
+}
+

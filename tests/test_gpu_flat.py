@@ -141,3 +141,43 @@ def test_flat_c4_bench_config_sampled_aggregate():
     sc = run.ctx.decrypt_scores(run.sk, run.db.layout, run.outs)
     assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-3
     assert sorted(np.argsort(-sc)[:3]) == sorted(run.pos.tolist())
+
+
+def test_flat_tbs_server_prerotation_bit_exact():
+    """BSGS-RTX-TBS: plain flat diagonals encrypted by the enroller, pre-rotated
+    on the GPU with the negative giant-step keys (hd_database_prerotate) -- the stored
+    ciphertexts before and after the pre-rotation and the scan outputs equal the oracle's."""
+    cfg = CONFIGS["C1"]
+    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
+    o = oracle.Oracle(cfg.log_n, cfg.limbs, seed=1)
+    db_vecs, q, pos = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    N, n1 = cfg.dim, cfg.n1
+    neg = ctx.prerotation_steps(N, n1)
+    assert [int(x) for x in neg] == sorted(ctx.ns - j * n1 for j in range(1, -(-N // n1)))
+    steps = np.array(sorted(set(int(x) for x in ctx.rotation_steps(N, n1, packing="flat")) | set(int(x) for x in neg)),
+                     np.int32)
+    sk, evk = ctx.keygen(steps)
+    ctx.relin_keygen(sk, evk)
+    pk = ctx.public_keygen(sk)
+    db = ctx.enroll(db_vecs, n1, packing="flat_tbs", pk=pk, enc_seed=5)
+    qct = ctx.encrypt_query(sk, q, ENC_SEED_BASE)
+    with pytest.raises(hd.HDError):
+        ctx.query(evk, db, qct)  # not yet pre-rotated
+    s, s_ntt = o.secret_key()
+    ok_steps, ok_keys = o.keyset(s_ntt, [int(x) for x in steps])
+    opk, orlk = o.public_key(s_ntt), o.relin_key(s_ntt)
+    D0 = o.enroll_aggregate_flat_tbs(o.normalize_rows(db_vecs), 0, cfg.num_vectors, n1, 0, opk, 5)
+    for k in (0, n1, N - 1):
+        assert (ctx.test_stage(db, 4, 0, k) == D0[k]).all(), k
+    ctx.database_prerotate(evk, db)
+    D1 = o.prerotate_tbs(D0, n1, ok_steps, ok_keys)
+    for k in (0, n1, 2 * n1 + 3, N - 1):
+        assert (ctx.test_stage(db, 4, 0, k) == D1[k]).all(), k
+    outs = ctx.query(evk, db, qct)
+    r = o.baby_steps(o.encrypt(s_ntt, o.encode(o.query_slots(q), 2.0 ** 45, cfg.limbs), ENC_SEED_BASE), n1, ok_steps,
+                     ok_keys)
+    out = o.scan_aggregate_flat_ct(r, n1, N, D1, ok_steps, ok_keys, orlk)
+    assert (ctx.ciphertext_residues(outs[0]) == out).all()
+    sc = ctx.decrypt_scores(sk, db.layout, outs)
+    assert np.abs(sc - _cos(db_vecs, q)).max() < 1e-6
+    assert sorted(np.argsort(-sc)[:len(pos)]) == sorted(pos.tolist())
