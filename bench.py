@@ -46,7 +46,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
-    ap.add_argument("--packing", default="replicated", choices=["replicated", "flat"],
+    ap.add_argument("--packing", default="replicated", choices=["replicated", "flat", "flat_tbs"],
                     help="stride-2N replicated blocks + fold (the north-star scan) or the flat pre-rotated "
                          "layout (NEXT-2, BSGS-RTX-TBE)")
     ap.add_argument("--db", default="plain", choices=["plain", "encrypted"],
@@ -220,13 +220,18 @@ def main():
     cfg = CONFIGS[args.config]
     stream = torch.cuda.current_stream()
     ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1, device=local, stream=stream)
-    flat = args.packing == "flat"
+    flat = args.packing in ("flat", "flat_tbs")
+    if args.packing == "flat_tbs" and args.db != "encrypted":
+        raise SystemExit("--packing flat_tbs needs --db encrypted (BSGS-RTX-TBS pre-rotates encrypted diagonals)")
     per = cfg.num_slots if flat else (cfg.num_slots // cfg.dim // 2) * cfg.dim  # vectors per aggregate
     A = -(-cfg.num_vectors // per)
     a0, a1 = hdd.shard_range(A, rank, world)
     # ---- setup (untimed): keys on rank 0 -> NCCL broadcast; local enrollment of this shard ----
     _, q, _ = make_dataset(16, cfg.dim, cfg.data_seed)  # query only (rows drawn per shard below)
     steps = ctx.rotation_steps(cfg.dim, cfg.n1, packing=args.packing)
+    if args.packing == "flat_tbs":  # + the negative giant-step keys of the server-side pre-rotation
+        steps = np.array(sorted(set(int(s) for s in steps) | set(int(s) for s in ctx.prerotation_steps(cfg.dim, cfg.n1))),
+                         np.int32)
     enc_db = args.db == "encrypted"
     if rank == 0:
         sk, evk = ctx.keygen(steps)
@@ -251,6 +256,12 @@ def main():
     rows = dataset_rows(cfg.num_vectors, cfg.dim, cfg.data_seed, v0, v1)
     db = enroll_rows(hd, ctx, rows, v0, cfg, a0, a1, pk, args.packing)
     del rows
+    prerot_s = None
+    if args.packing == "flat_tbs":  # setup (untimed): BSGS-RTX-TBS homomorphic pre-rotation
+        torch.cuda.synchronize()
+        t_p = time.perf_counter()
+        ctx.database_prerotate(evk, db)
+        prerot_s = time.perf_counter() - t_p
     # ---- the query: encrypted on rank 0, exported into a device buffer (NCCL-broadcast each step) ----
     ct_bytes = 0
     if rank == 0:
@@ -399,7 +410,9 @@ def main():
             "config": dict(cfg_dict(cfg, world, "fixed 2^20 database sharded by aggregate"),
                            database="encrypted diagonals (NEXT-1: degree-2 MAC + relinearisation)" if enc_db
                            else "plaintext diagonals (north-star pt x ct scan)",
-                           packing="flat pre-rotated (NEXT-2, BSGS-RTX-TBE; no fold, M groups per ciphertext)"
+                           packing=("flat, server-side homomorphic pre-rotation (BSGS-RTX-TBS; setup "
+                                    f"{prerot_s:.2f} s)" if args.packing == "flat_tbs" else
+                                    "flat pre-rotated (NEXT-2, BSGS-RTX-TBE; no fold, M groups per ciphertext)")
                            if flat else "stride-2N replicated blocks + rotate-by-N fold (Alg. enroller_bsgs)",
                            aggregates=A),
             "phase_ms": {"baby": phase[0] / args.steps, "mac": phase[1] / args.steps,
