@@ -417,6 +417,45 @@ class Oracle:
                                                          C.c_int64(agg), C.c_int64(num_vectors), _p(sc)))
         return sc
 
+    # -- encrypted comparison and scenario tail (NEXT-3, R29) ---------------------
+    def cheb_compare(self, ct, scale, coeffs, rlk):
+        """ChebyshevCompare (Alg. gpu-chebyshev, P:L734-789): returns (ct_out, scale_out)."""
+        ell = ct.shape[1]
+        c = np.ascontiguousarray(coeffs, dtype=np.float64)
+        out = u64((2, ell, self.n))
+        eo = C.c_int32(0)
+        so = C.c_double(0.0)
+        _check("cheb_compare", lib().or_cheb_compare(
+            C.byref(self.p), _p(np.ascontiguousarray(ct)), ell, C.c_double(scale), _p(c), len(c) - 1,
+            _p(np.ascontiguousarray(rlk)), _p(out), C.byref(eo), C.byref(so)))
+        return np.ascontiguousarray(out.reshape(-1)[: 2 * eo.value * self.n].reshape(2, eo.value, self.n)), so.value
+
+    def membership(self, cts, steps, keys):
+        """EvalAddMany + RotateAndSum over numSlots (Alg. membership)."""
+        cts = np.ascontiguousarray(cts, dtype=np.uint64)
+        count, _, ell, _ = cts.shape
+        out = u64((2, ell, self.n))
+        _check("membership", lib().or_membership(C.byref(self.p), _p(cts), count, ell, _p(steps), len(steps),
+                                                 _p(keys), _p(out)))
+        return out
+
+
+def cheb_degree(kappa: int) -> int:
+    lib().or_cheb_degree.restype = C.c_int32
+    return int(lib().or_cheb_degree(kappa))
+
+
+def ps_split(n: int):
+    d1, d2 = C.c_int32(0), C.c_int32(0)
+    _check("ps_split", lib().or_ps_split(n, C.byref(d1), C.byref(d2)))
+    return d1.value, d2.value
+
+
+def cheb_coeffs(delta: float, n: int) -> np.ndarray:
+    c = np.zeros(n + 1, dtype=np.float64)
+    _check("cheb_coeffs", lib().or_cheb_coeffs(C.c_double(delta), n, _p(c)))
+    return c
+
 
 def philox4x32_10(ctr, key):
     c = (C.c_uint32 * 4)(*ctr)

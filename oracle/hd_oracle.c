@@ -1425,3 +1425,352 @@ int or_decrypt_scores(const or_params *p, const uint64_t *s_ntt, const uint64_t 
   free(pt); free(z);
   return OR_OK;
 }
+
+/* ======================================================================== */
+/* Encrypted comparison and scenario tail (NEXT-3; reading R29 of DESIGN.md) */
+/* ======================================================================== */
+/* Degree of the Chebyshev series from the comparison depth budget kappa: the
+ * paper's Paterson-Stockmeyer-aware lookup table: 7 -> 5, 8 -> 13,
+ * 9 -> 27, 10 -> 59.  Other kappa: 0 (unsupported). */
+int32_t or_cheb_degree(int32_t kappa) {
+  switch (kappa) {
+    case 7: return 5;
+    case 8: return 13;
+    case 9: return 27;
+    case 10: return 59;
+    default: return 0;
+  }
+}
+
+/* PS split: d1, d2 minimising d1 + d2 subject to d1 * 2^(d2-1) >= n;
+ * ties go to the smallest d2 (R29: n = 13 -> (2, 4) as the paper states). */
+int or_ps_split(int32_t n, int32_t *d1, int32_t *d2) {
+  if (n < 1) return OR_E_ARG;
+  int best = 1 << 30, b1 = 0, b2 = 0;
+  for (int g = 1; g <= 31; g++)
+    for (int b = 1; b <= n; b++) {
+      if ((long long)b << (g - 1) < n) continue;
+      if (b + g < best || (b + g == best && g < b2)) { best = b + g; b1 = b; b2 = g; }
+      break; /* larger b only grows b + g */
+    }
+  *d1 = b1; *d2 = b2;
+  return OR_OK;
+}
+
+/* Chebyshev coefficients ("computed offline via DCT-based interpolation";
+ * R29): the degree-n interpolant of f(x) = 1/2 (sign(x - delta) + 1) (Eq. eq:cheb-sign,
+ * sign(0) = +1 so f = 1 for x >= delta) at the n + 1 Chebyshev nodes of the first kind
+ * x_k = cos(pi (k + 1/2) / (n + 1)):
+ *   c_i = 2/(n+1) sum_k f(x_k) cos(pi i (k + 1/2) / (n + 1)),   c_0 halved.
+ * Interpolating f directly folds the 1/2 and the Alg.'s final "+1" into the series. */
+int or_cheb_coeffs(double delta, int32_t n, double *c) {
+  if (n < 1) return OR_E_ARG;
+  const double pi = 3.14159265358979323846;
+  for (int i = 0; i <= n; i++) {
+    double s = 0.0;
+    for (int k = 0; k <= n; k++) {
+      double xk = cos(pi * ((double)k + 0.5) / (double)(n + 1));
+      double fk = xk >= delta ? 1.0 : 0.0;
+      s = s + fk * cos(pi * (double)i * ((double)k + 0.5) / (double)(n + 1));
+    }
+    c[i] = 2.0 * s / (double)(n + 1);
+  }
+  c[0] = c[0] / 2.0;
+  return OR_OK;
+}
+
+/* Set when a product or a scalar multiplication is asked for at one limb (no level left). */
+static int g_cheb_range_err;
+
+/* A ciphertext in the comparison: [2][ell][n] residues plus its scale (R29). */
+typedef struct {
+  uint64_t *d;
+  int ell;
+  double scale;
+} or_cct;
+
+static or_cct cct_new(const or_params *p, int ell, double scale) {
+  or_cct r;
+  r.d = calloc((size_t)2 * ell * p->n, sizeof(uint64_t));
+  r.ell = ell;
+  r.scale = scale;
+  return r;
+}
+static void cct_free(or_cct *a) { free(a->d); a->d = NULL; }
+
+/* MatchLevel: keep limbs q_0..q_{ell-1} of both polynomials (exact
+ * modular reduction; the scale is unchanged). */
+static or_cct cct_drop(const or_params *p, const or_cct *a, int ell) {
+  or_cct r = cct_new(p, ell, a->scale);
+  int n = p->n;
+  for (int pp = 0; pp < 2; pp++)
+    memcpy(r.d + (size_t)pp * ell * n, a->d + (size_t)pp * a->ell * n, sizeof(uint64_t) * (size_t)ell * n);
+  return r;
+}
+
+/* Ciphertext product: MatchLevel, tensor (d0, d1, d2) = (a0 b0, a0 b1 + a1 b0, a1 b1),
+ * Relinearize, Rescale (invariant (i) of P:L792-793: every product is
+ * rescaled at once).  scale = s_a s_b / q_{ell-1}. */
+static or_cct cct_mul(const or_params *p, const or_cct *a0, const or_cct *b0, const uint64_t *rlk) {
+  int ell = a0->ell < b0->ell ? a0->ell : b0->ell, n = p->n;
+  if (ell < 2) { g_cheb_range_err = 1; return cct_new(p, 1, a0->scale); }
+  or_cct a = cct_drop(p, a0, ell), b = cct_drop(p, b0, ell);
+  uint64_t *S3 = malloc(sizeof(uint64_t) * (size_t)3 * ell * n);
+  uint64_t *R = malloc(sizeof(uint64_t) * (size_t)2 * ell * n);
+  for (int l = 0; l < ell; l++) {
+    uint64_t q = p->mod[l];
+    for (int t = 0; t < n; t++) {
+      size_t o = (size_t)l * n + t, o1 = (size_t)ell * n + o;
+      S3[o] = mulmod(a.d[o], b.d[o], q);
+      S3[o1] = addmod(mulmod(a.d[o], b.d[o1], q), mulmod(a.d[o1], b.d[o], q), q);
+      S3[(size_t)2 * ell * n + o] = mulmod(a.d[o1], b.d[o1], q);
+    }
+  }
+  or_relinearize(p, S3, ell, rlk, R);
+  or_cct r = cct_new(p, ell - 1, a.scale * b.scale / (double)p->mod[ell - 1]);
+  or_rescale(p, R, ell, r.d);
+  free(S3); free(R); cct_free(&a); cct_free(&b);
+  return r;
+}
+
+/* k * a for a small integer k (exact; scale unchanged). */
+static or_cct cct_mul_int(const or_params *p, const or_cct *a, int64_t k) {
+  or_cct r = cct_new(p, a->ell, a->scale);
+  int n = p->n;
+  for (int pp = 0; pp < 2; pp++)
+    for (int l = 0; l < a->ell; l++) {
+      uint64_t q = p->mod[l], kq = smod(k, q);
+      for (int t = 0; t < n; t++) {
+        size_t o = ((size_t)pp * a->ell + l) * n + t;
+        r.d[o] = mulmod(a->d[o], kq, q);
+      }
+    }
+  return r;
+}
+
+/* a + c for a real constant c: the constant polynomial round(c * scale) (R15
+ * rounding, half-even) is constant in every NTT slot; added to c0. */
+static or_cct cct_add_const(const or_params *p, const or_cct *a, double c) {
+  or_cct r = cct_new(p, a->ell, a->scale);
+  int n = p->n;
+  int64_t v = llrint(c * a->scale);
+  memcpy(r.d, a->d, sizeof(uint64_t) * (size_t)2 * a->ell * n);
+  for (int l = 0; l < a->ell; l++) {
+    uint64_t q = p->mod[l], vq = smod(v, q);
+    for (int t = 0; t < n; t++) r.d[(size_t)l * n + t] = addmod(r.d[(size_t)l * n + t], vq, q);
+  }
+  return r;
+}
+
+/* c * a for a real constant c: multiply by C = round(c * q_{ell-1}) and rescale by
+ * q_{ell-1}; the message becomes m C / q_{ell-1} ~ c m, the scale is kept (R29). */
+static or_cct cct_mul_const(const or_params *p, const or_cct *a, double c) {
+  int ell = a->ell, n = p->n;
+  if (ell < 2) { g_cheb_range_err = 1; return cct_new(p, 1, a->scale); }
+  int64_t C = llrint(c * (double)p->mod[ell - 1]);
+  uint64_t *X = malloc(sizeof(uint64_t) * (size_t)2 * ell * n);
+  for (int pp = 0; pp < 2; pp++)
+    for (int l = 0; l < ell; l++) {
+      uint64_t q = p->mod[l], Cq = smod(C, q);
+      for (int t = 0; t < n; t++) {
+        size_t o = ((size_t)pp * ell + l) * n + t;
+        X[o] = mulmod(a->d[o], Cq, q);
+      }
+    }
+  or_cct r = cct_new(p, ell - 1, a->scale);
+  or_rescale(p, X, ell, r.d);
+  free(X);
+  return r;
+}
+
+/* a + sgn * b after MatchLevel; the result keeps a's scale (R29). */
+static or_cct cct_add(const or_params *p, const or_cct *a0, const or_cct *b0, int sgn) {
+  int ell = a0->ell < b0->ell ? a0->ell : b0->ell, n = p->n;
+  or_cct a = cct_drop(p, a0, ell), b = cct_drop(p, b0, ell);
+  for (int pp = 0; pp < 2; pp++)
+    for (int l = 0; l < ell; l++) {
+      uint64_t q = p->mod[l];
+      for (int t = 0; t < n; t++) {
+        size_t o = ((size_t)pp * ell + l) * n + t;
+        a.d[o] = sgn > 0 ? addmod(a.d[o], b.d[o], q) : submod(a.d[o], b.d[o], q);
+      }
+    }
+  cct_free(&b);
+  return a;
+}
+
+/* An intermediate value of the evaluation: a ciphertext, or a plain constant. */
+typedef struct {
+  int is_ct;
+  or_cct ct;
+  double k;
+} or_val;
+
+typedef struct {
+  const or_params *p;
+  const uint64_t *rlk;
+  int d1, d2;
+  or_cct T[64];     /* baby powers T[1..d1] (Step 1) */
+  or_cct G[32];     /* giant powers G[j] = T_{d1 2^j} (Step 2) */
+  int nG;
+} or_ps;
+
+/* 2 a b - c, every product rescaled. */
+static or_cct cct_two_ab_minus(const or_params *p, const or_cct *a, const or_cct *b, const or_cct *c_ct,
+                               double c_const, const uint64_t *rlk) {
+  or_cct ab = cct_mul(p, a, b, rlk);
+  or_cct t2 = cct_mul_int(p, &ab, 2);
+  cct_free(&ab);
+  or_cct r;
+  if (c_ct) r = cct_add(p, &t2, c_ct, -1);
+  else r = cct_add_const(p, &t2, -c_const);
+  cct_free(&t2);
+  return r;
+}
+
+static or_val val_const(double k) { or_val v; memset(&v, 0, sizeof v); v.k = k; return v; }
+static or_val val_ct(or_cct c) { or_val v; memset(&v, 0, sizeof v); v.is_ct = 1; v.ct = c; return v; }
+
+/* Chunk polynomial (Alg. gpu-chebyshev Step 3): Q = c_0 + sum_{i>=1, c_i != 0}
+ * c_i T[i], deg < d1. */
+static or_val ps_chunk(or_ps *S, const double *c, int m) {
+  or_val acc = val_const(0.0);
+  for (int i = 1; i <= m; i++) {
+    if (c[i] == 0.0) continue;
+    or_cct t = cct_mul_const(S->p, &S->T[i], c[i]);
+    if (!acc.is_ct) {
+      acc = val_ct(t);
+    } else {
+      or_cct s = cct_add(S->p, &acc.ct, &t, 1);
+      cct_free(&acc.ct); cct_free(&t);
+      acc.ct = s;
+    }
+  }
+  if (!acc.is_ct) return val_const(c[0]);
+  if (c[0] != 0.0) {
+    or_cct s = cct_add_const(S->p, &acc.ct, c[0]);
+    cct_free(&acc.ct);
+    acc.ct = s;
+  }
+  return acc;
+}
+
+/* Evaluates sum_{i<=m} c_i T_i by Chebyshev-basis division (R29): with k = d1 2^j the
+ * largest giant degree <= m, p = q T_k + r where q_0 = c_k, q_i = 2 c_{k+i} and
+ * r_{k-i} = c_{k-i} - c_{k+i} (T_k T_i = (T_{k+i} + T_{k-i}) / 2; m < 2k). */
+static or_val ps_eval(or_ps *S, const double *c0, int m) {
+  while (m > 0 && c0[m] == 0.0) m--;
+  if (m < S->d1) return ps_chunk(S, c0, m);
+  int j = 0;
+  while (j + 1 < S->nG && (S->d1 << (j + 1)) <= m) j++;
+  int k = S->d1 << j;
+  double *q = malloc(sizeof(double) * (size_t)(m - k + 1)), *r = malloc(sizeof(double) * (size_t)k);
+  q[0] = c0[k];
+  for (int i = 1; i <= m - k; i++) q[i] = 2.0 * c0[k + i];
+  for (int i = 0; i < k; i++) r[i] = c0[i];
+  for (int i = 1; i <= m - k; i++) r[k - i] = r[k - i] - c0[k + i];
+  or_val Q = ps_eval(S, q, m - k), R = ps_eval(S, r, k - 1);
+  free(q); free(r);
+  or_val P;
+  if (Q.is_ct) {
+    P = val_ct(cct_mul(S->p, &Q.ct, &S->G[j], S->rlk));
+    cct_free(&Q.ct);
+  } else if (Q.k != 0.0) {
+    P = val_ct(cct_mul_const(S->p, &S->G[j], Q.k));
+  } else {
+    P = val_const(0.0);
+  }
+  if (!P.is_ct) return R;
+  if (R.is_ct) {
+    or_cct s = cct_add(S->p, &P.ct, &R.ct, 1);
+    cct_free(&P.ct); cct_free(&R.ct);
+    P.ct = s;
+  } else if (R.k != 0.0) {
+    or_cct s = cct_add_const(S->p, &P.ct, R.k);
+    cct_free(&P.ct);
+    P.ct = s;
+  }
+  return P;
+}
+
+/* ChebyshevCompare (Alg. gpu-chebyshev; R29).  in: [2][ell][n] at scale
+ * `scale` (slots in [-1, 1]); c[0..degree]; rlk: relinearisation key.  out: [2][*ell_out][n]
+ * (capacity 2 ell n), *scale_out its scale.  OR_E_RANGE if the levels run out. */
+int or_cheb_compare(const or_params *p, const uint64_t *in, int32_t ell, double scale, const double *c,
+                    int32_t degree, const uint64_t *rlk, uint64_t *out, int32_t *ell_out, double *scale_out) {
+  if (ell < 1 || ell > p->L || degree < 1) return OR_E_ARG;
+  or_ps S;
+  memset(&S, 0, sizeof S);
+  S.p = p;
+  S.rlk = rlk;
+  g_cheb_range_err = 0;
+  or_ps_split(degree, &S.d1, &S.d2);
+  if (S.d1 >= 64) return OR_E_ARG;
+  /* Step 1: baby powers */
+  S.T[1] = cct_new(p, ell, scale);
+  memcpy(S.T[1].d, in, sizeof(uint64_t) * (size_t)2 * ell * p->n);
+  for (int i = 2; i <= S.d1; i++) {
+    if ((i & (i - 1)) == 0)
+      S.T[i] = cct_two_ab_minus(p, &S.T[i / 2], &S.T[i / 2], NULL, 1.0, rlk);
+    else
+      S.T[i] = cct_two_ab_minus(p, &S.T[i / 2], &S.T[(i + 1) / 2], &S.T[1], 0.0, rlk);
+  }
+  /* Step 2: giant powers T_{d1 2^j} by doubling, up to the degree */
+  S.G[0] = cct_drop(p, &S.T[S.d1], S.T[S.d1].ell);
+  S.nG = 1;
+  while ((S.d1 << S.nG) <= degree) {
+    S.G[S.nG] = cct_two_ab_minus(p, &S.G[S.nG - 1], &S.G[S.nG - 1], NULL, 1.0, rlk);
+    S.nG++;
+  }
+  /* Step 3: chunks and combination */
+  int rc = OR_OK;
+  or_val V = ps_eval(&S, c, degree);
+  if (!V.is_ct) {
+    rc = OR_E_ARG; /* constant polynomial: nothing encrypted to return */
+  } else if (g_cheb_range_err) {
+    rc = OR_E_RANGE;
+    cct_free(&V.ct);
+  } else {
+    *ell_out = V.ct.ell;
+    *scale_out = V.ct.scale;
+    memcpy(out, V.ct.d, sizeof(uint64_t) * (size_t)2 * V.ct.ell * p->n);
+    cct_free(&V.ct);
+  }
+  for (int i = 1; i <= S.d1; i++) cct_free(&S.T[i]);
+  for (int j = 0; j < S.nG; j++) cct_free(&S.G[j]);
+  return rc;
+}
+
+/* Membership tail (Alg. membership, Alg. gpu-bsgs-membership):
+ * EvalAddMany of the count comparison ciphertexts ([count][2][ell][n]), then
+ * RotateAndSum over numSlots: x <- x + Rot_k(x) for k = 1, 2, 4, ..., numSlots/2
+ * (power-of-two keys).  Every slot of out = the sum over all slots. */
+int or_membership(const or_params *p, const uint64_t *cts, int32_t count, int32_t ell, const int32_t *steps,
+                  int32_t nkeys, const uint64_t *keys, uint64_t *out) {
+  int n = p->n;
+  size_t ct = (size_t)2 * ell * n;
+  if (count < 1 || ell < 1) return OR_E_ARG;
+  memcpy(out, cts, sizeof(uint64_t) * ct);
+  for (int i = 1; i < count; i++)
+    for (int pp = 0; pp < 2; pp++)
+      for (int l = 0; l < ell; l++)
+        for (int t = 0; t < n; t++) {
+          size_t o = ((size_t)pp * ell + l) * n + t;
+          out[o] = addmod(out[o], cts[(size_t)i * ct + o], p->mod[l]);
+        }
+  uint64_t *R = malloc(sizeof(uint64_t) * ct);
+  int rc = OR_OK;
+  for (int k = 1; k < p->num_slots; k <<= 1) {
+    const uint64_t *key = find_key(p, steps, nkeys, keys, k);
+    if (!key) { rc = OR_E_MISSING_KEY; break; }
+    or_rotate(p, out, ell, key, k, R);
+    for (int pp = 0; pp < 2; pp++)
+      for (int l = 0; l < ell; l++)
+        for (int t = 0; t < n; t++) {
+          size_t o = ((size_t)pp * ell + l) * n + t;
+          out[o] = addmod(out[o], R[o], p->mod[l]);
+        }
+  }
+  free(R);
+  return rc;
+}

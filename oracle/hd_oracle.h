@@ -183,6 +183,16 @@ int or_decrypt_scores_flat(const or_params *p, const uint64_t *s_ntt, const uint
 int or_decrypt_scores(const or_params *p, const uint64_t *s_ntt, const uint64_t *out_ct,
                       int32_t N, int64_t agg, int64_t num_vectors, double *scores /* M/2*N */);
 
+/* Encrypted comparison and scenario tail (NEXT-3, R29; Alg. gpu-chebyshev P:L734-789,
+ * Alg. membership). */
+int32_t or_cheb_degree(int32_t kappa);
+int or_ps_split(int32_t n, int32_t *d1, int32_t *d2);
+int or_cheb_coeffs(double delta, int32_t n, double *c /* n + 1 */);
+int or_cheb_compare(const or_params *p, const uint64_t *in, int32_t ell, double scale, const double *c,
+                    int32_t degree, const uint64_t *rlk, uint64_t *out, int32_t *ell_out, double *scale_out);
+int or_membership(const or_params *p, const uint64_t *cts, int32_t count, int32_t ell, const int32_t *steps,
+                  int32_t nkeys, const uint64_t *keys, uint64_t *out);
+
 #ifdef __cplusplus
 }
 #endif

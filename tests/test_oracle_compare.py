@@ -1,0 +1,123 @@
+"""Pins of the oracle's encrypted comparison and scenario tail (NEXT-3, R29; not gpu).
+
+(1) the paper's degree table kappa -> n and its PS split n = 13 -> (d1, d2) = (2, 4)
+    (P:L727); the split is minimal by brute force over all (d1, d2);
+(2) Chebyshev coefficients = numpy's chebinterpolate of f(x) = 1/2 (sign(x - delta) + 1)
+    (library routine, first-kind points) and interpolate f at the n + 1 nodes (closed form);
+(3) ChebyshevCompare decrypts to the plain series sum_i c_i T_i(x) (numpy chebval) on every
+    slot, at the minimum multiplicative depth ceil(log2(n + 1)) (4 for n = 13), for the
+    paper's degree (d1 = 2) and for n = 5 (d1 = 3: the odd baby power T3 = 2 T1 T2 - T1);
+(4) membership: every slot of RotateAndSum(sum of the inputs) decrypts to the sum of all
+    decrypted input slots (a linear identity, independent of the evaluation);
+(5) end to end on the flat scan (C1 database): compare(scan) decodes to chebval(cosine).
+"""
+import math
+
+import numpy as np
+import pytest
+from numpy.polynomial import chebyshev as npcheb
+
+from synth_inputs import CONFIGS, make_dataset
+
+D45 = 2.0 ** 45
+
+
+def _f(delta):
+    return lambda x: np.where(np.asarray(x) >= delta, 1.0, 0.0)
+
+
+def test_degree_table_and_ps_split(oracle_mod):
+    assert [oracle_mod.cheb_degree(k) for k in (7, 8, 9, 10)] == [5, 13, 27, 59]
+    assert oracle_mod.cheb_degree(6) == 0
+    assert oracle_mod.ps_split(13) == (2, 4)
+    for n in (2, 3, 5, 13, 27, 59, 100):
+        d1, d2 = oracle_mod.ps_split(n)
+        assert d1 * 2 ** (d2 - 1) >= n
+        best = min(a + b for a in range(1, n + 1) for b in range(1, 12) if a * 2 ** (b - 1) >= n)
+        assert d1 + d2 == best
+
+
+@pytest.mark.parametrize("delta,n", [(0.5, 13), (0.0, 13), (-0.3, 5), (0.8, 27)])
+def test_coefficients(oracle_mod, delta, n):
+    c = oracle_mod.cheb_coeffs(delta, n)
+    ref = npcheb.chebinterpolate(_f(delta), n)
+    assert np.abs(c - ref).max() < 1e-13
+    xk = np.cos(np.pi * (np.arange(n + 1) + 0.5) / (n + 1))
+    assert np.abs(npcheb.chebval(xk, c) - _f(delta)(xk)).max() < 1e-12
+
+
+@pytest.fixture(scope="module")
+def ring6(oracle_mod):
+    o = oracle_mod.Oracle(10, 6, seed=5)
+    s, s_ntt = o.secret_key()
+    return o, s_ntt, o.relin_key(s_ntt)
+
+
+def _encrypt_slots(o, s_ntt, z, ell, seed):
+    return o.encrypt(s_ntt, o.encode(z, D45, ell), seed)
+
+
+@pytest.mark.parametrize("n,delta", [(13, 0.5), (5, -0.2)])
+def test_compare_evaluates_the_series(oracle_mod, ring6, n, delta):
+    o, s_ntt, rlk = ring6
+    rng = np.random.default_rng(n)
+    z = rng.uniform(-1, 1, o.ns)
+    z[:4] = [-1.0, 1.0, delta, 0.0]
+    ell = 5                                   # the scan's output level at L = 6
+    ct = _encrypt_slots(o, s_ntt, z, ell, 9)
+    c = oracle_mod.cheb_coeffs(delta, n)
+    out, scale = o.cheb_compare(ct, D45, c, rlk)
+    assert out.shape[1] == ell - math.ceil(math.log2(n + 1))   # minimum depth of a degree-n polynomial
+    got = o.decode(o.decrypt(s_ntt, out), scale)
+    want = npcheb.chebval(z, c)
+    assert np.abs(got - want).max() < 1e-5
+    # the approximation itself separates the far sides of the threshold
+    far = np.abs(z - delta) > 0.4
+    assert np.abs(got[far] - _f(delta)(z[far])).max() < 0.2
+
+
+def test_compare_runs_out_of_levels(oracle_mod, ring6):
+    o, s_ntt, rlk = ring6
+    ct = _encrypt_slots(o, s_ntt, np.zeros(o.ns), 3, 4)
+    with pytest.raises(oracle_mod.OracleError) as e:
+        o.cheb_compare(ct, D45, oracle_mod.cheb_coeffs(0.5, 13), rlk)
+    assert e.value.code == oracle_mod.OR_E_RANGE
+
+
+def test_membership_sums_every_slot(oracle_mod, ring6):
+    o, s_ntt, rlk = ring6
+    rng = np.random.default_rng(3)
+    zs = [rng.uniform(0, 1, o.ns) * 1e-3 for _ in range(3)]
+    cts = np.stack([_encrypt_slots(o, s_ntt, z, 2, 40 + i) for i, z in enumerate(zs)])
+    steps = [1 << k for k in range(o.log_n - 1)]
+    st, keys = o.keyset(s_ntt, steps)
+    out = o.membership(cts, st, keys)
+    got = o.decode(o.decrypt(s_ntt, out), D45)
+    dec = sum(o.decode(o.decrypt(s_ntt, cts[i]), D45) for i in range(3))
+    assert np.abs(got - dec.sum()).max() < 1e-6
+    with pytest.raises(oracle_mod.OracleError):
+        o.membership(cts, st[:-1], keys[:-1])
+
+
+def test_identification_end_to_end(oracle_mod):
+    """Flat scan at L = 6, then ChebyshevCompare: decodes to chebval(cosine) per vector."""
+    cfg = CONFIGS["C1"]
+    o = oracle_mod.Oracle(cfg.log_n, 6, seed=1)
+    s, s_ntt = o.secret_key()
+    rlk = o.relin_key(s_ntt)
+    db, q, pos = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    st, keys = o.keyset(s_ntt, o.rotation_steps_flat(cfg.dim, cfg.n1))
+    qct = o.encrypt(s_ntt, o.encode(o.query_slots(q), D45, o.L), 1000)
+    r = o.baby_steps(qct, cfg.n1, st, keys)
+    D = o.enroll_aggregate_flat(o.normalize_rows(db), 0, cfg.num_vectors, cfg.n1, 0)
+    out = o.scan_aggregate_flat(r, cfg.n1, cfg.dim, D, st, keys)
+    delta = 0.5
+    c = oracle_mod.cheb_coeffs(delta, 13)
+    cmp_ct, scale = o.cheb_compare(out, D45, c, rlk)
+    assert cmp_ct.shape[1] == 1
+    z = o.decode(o.decrypt(s_ntt, cmp_ct), scale)
+    d = db.astype(np.float64)
+    cos = d @ q.astype(np.float64) / (np.linalg.norm(d, axis=1) * np.linalg.norm(q.astype(np.float64)))
+    got = z[: cfg.num_vectors]          # flat packing, one aggregate: slot v = vector v (R27)
+    assert np.abs(got - npcheb.chebval(cos, c)).max() < 1e-5
+    assert (got[pos] > 0.8).all() and np.delete(got, pos).max() < 0.3
