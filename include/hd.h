@@ -17,6 +17,10 @@
  *                                                     -> hd_query
  *   - the client decrypts and reads the scores (reading R4 of DESIGN.md)
  *                                                     -> hd_decrypt_scores
+ *   - or the server thresholds them first (encrypted comparison, identification and
+ *     membership tails; NEXT-3)
+ *                                                     -> hd_chebyshev_coefficients,
+ *                                                        hd_compare, hd_membership
  *
  * Conventions
  *   - Every function returns hd_status (HD_OK = 0).  No C++ exception crosses the
@@ -257,6 +261,44 @@ hd_status hd_public_key_import(hd_context *ctx, const uint64_t *src, size_t coun
  * under the reserved step 0.  No-op if present. */
 hd_status hd_relin_keygen(hd_context *ctx, const hd_secret_key *sk, hd_eval_keys *evk);
 void hd_public_key_destroy(hd_public_key *pk);
+
+/* ---- encrypted comparison and scenario tail (NEXT-3, R29) ------------ */
+/* Degree n of the Chebyshev sign approximation for the comparison depth budget kappa,
+ * the paper's lookup table: 7 -> 5, 8 -> 13, 9 -> 27, 10 -> 59; other kappa ->
+ * HD_E_INVALID_ARG. */
+hd_status hd_chebyshev_degree(uint32_t kappa, uint32_t *degree);
+/* Client side (host, no device): the coefficients c_0..c_degree of the degree-n Chebyshev
+ * interpolant of f(x) = 1/2 (sign(x - delta) + 1) (Eq. eq:cheb-sign) at the
+ * first-kind Chebyshev nodes (DCT-II; R29), so sum_i c_i T_i(x) ~ 1 for x >= delta and ~ 0
+ * below, on [-1, 1].  coeffs: host double[cap], cap >= degree + 1. */
+hd_status hd_chebyshev_coefficients(double delta, uint32_t degree, double *coeffs, size_t cap);
+/* ChebyshevCompare (Alg. gpu-chebyshev; R29): out[i] = sum_k coeffs[k] T_k(in[i])
+ * slot-wise, by Paterson-Stockmeyer in the Chebyshev basis ((d1, d2) of P:L725-727) at depth
+ * ceil(log2(degree + 1)); every product is relinearised (evk must hold the relinearisation
+ * key, hd_relin_keygen; else HD_E_MISSING_KEY) and rescaled at once.  All inputs must share
+ * one level and scale (e.g. hd_query outputs); slots are expected in [-1, 1].  The count
+ * inputs are evaluated together in batches (one launch per step for the whole batch).
+ * out[i]: NULL -> allocated; else overwritten in place (same context and level).  The
+ * result level is the input's minus the depth (HD_E_LEVEL if the limbs run out: the scan
+ * plus degree 13 needs num_limbs >= 6); its scale is in hd_ciphertext_scale.  Identification
+ * (Alg. index) = hd_compare over the hd_query outputs. */
+hd_status hd_compare(hd_context *ctx, const hd_eval_keys *evk, const hd_ciphertext *const *in, size_t count,
+                     const double *coeffs, uint32_t degree, hd_ciphertext **out);
+/* Rotation steps of the membership RotateAndSum: 1, 2, 4, ..., numSlots / 2. */
+hd_status hd_membership_steps(const hd_context *ctx, int32_t *steps, size_t cap, size_t *count);
+/* Membership (Alg. membership, Alg. gpu-bsgs-membership): the sum
+ * of the count comparison ciphertexts (EvalAddMany), then RotateAndSum over numSlots with the
+ * power-of-two keys (HD_E_MISSING_KEY if one is absent): every slot of *out holds the sum of
+ * all slots of all inputs (the approximate match count).  Meaningful on the FLAT packing
+ * (every slot a vector or zero padding, R29).  *out: NULL -> allocated. */
+hd_status hd_membership(hd_context *ctx, const hd_eval_keys *evk, const hd_ciphertext *const *in, size_t count,
+                        hd_ciphertext **out);
+/* Scale of a ciphertext's message (2^scale_bits for queries and scan outputs). */
+hd_status hd_ciphertext_scale(const hd_ciphertext *ct, double *scale);
+/* Decrypt + decode one ciphertext at its own scale: slots[0..numSlots) = real parts
+ * (host double[cap], cap >= numSlots).  Floating point (CKKS error), not bit-exact. */
+hd_status hd_decrypt_slots(hd_context *ctx, const hd_secret_key *sk, const hd_ciphertext *ct, double *slots,
+                           size_t cap);
 
 void hd_ciphertext_destroy(hd_ciphertext *ct);
 void hd_eval_keys_destroy(hd_eval_keys *evk);

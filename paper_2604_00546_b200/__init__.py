@@ -35,6 +35,8 @@ ABI_FUNCTIONS = [
     "hd_test_rescale", "hd_ciphertext_export_async", "hd_context_synchronize", "hd_enroll_encrypted",
     "hd_public_keygen", "hd_public_key_export", "hd_public_key_import", "hd_relin_keygen", "hd_public_key_destroy",
     "hd_enroll_ex", "hd_rotation_steps_ex", "hd_prerotation_steps", "hd_database_prerotate",
+    "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
+    "hd_ciphertext_scale", "hd_decrypt_slots",
 ]
 
 
@@ -132,6 +134,13 @@ def load():
             L.hd_test_stage.argtypes = [VP, C.c_int, C.c_uint32, C.c_int32, VP, C.c_size_t]
             L.hd_test_rotate.argtypes = [VP, VP, VP, C.c_int32, C.POINTER(VP)]
             L.hd_test_rescale.argtypes = [VP, VP, C.POINTER(VP)]
+            L.hd_chebyshev_degree.argtypes = [C.c_uint32, C.POINTER(C.c_uint32)]
+            L.hd_chebyshev_coefficients.argtypes = [C.c_double, C.c_uint32, VP, C.c_size_t]
+            L.hd_compare.argtypes = [VP, VP, VP, C.c_size_t, VP, C.c_uint32, VP]
+            L.hd_membership_steps.argtypes = [VP, VP, C.c_size_t, C.POINTER(C.c_size_t)]
+            L.hd_membership.argtypes = [VP, VP, VP, C.c_size_t, C.POINTER(VP)]
+            L.hd_ciphertext_scale.argtypes = [VP, C.POINTER(C.c_double)]
+            L.hd_decrypt_slots.argtypes = [VP, VP, VP, VP, C.c_size_t]
             _lib = L
         return _lib
 
@@ -325,6 +334,40 @@ class Context(_Handle):
         db.encrypted = True
         return db
 
+    # -- encrypted comparison and scenario tail (NEXT-3, R29) ---------------------------------
+    def compare(self, evk, cts, coeffs, outs=None):
+        """hd_compare: ChebyshevCompare of every ciphertext (identification, Alg. index)."""
+        coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
+        if outs is None:
+            outs = [None] * len(cts)
+        src = (VP * len(cts))(*[c.h for c in cts])
+        arr = (VP * len(cts))(*[(o.h if o is not None else None) for o in outs])
+        _check("hd_compare", load().hd_compare(self.h, evk.h, src, len(cts), _ptr(coeffs), len(coeffs) - 1, arr))
+        return [o if o is not None else Ciphertext(arr[i], self) for i, o in enumerate(outs)]
+
+    def membership_steps(self):
+        cnt = C.c_size_t()
+        _check("hd_membership_steps", load().hd_membership_steps(self.h, None, 0, C.byref(cnt)))
+        steps = np.zeros(cnt.value, np.int32)
+        _check("hd_membership_steps", load().hd_membership_steps(self.h, _ptr(steps), cnt.value, C.byref(cnt)))
+        return steps
+
+    def membership(self, evk, cts, out=None):
+        src = (VP * len(cts))(*[c.h for c in cts])
+        o = VP(out.h if out is not None else None)
+        _check("hd_membership", load().hd_membership(self.h, evk.h, src, len(cts), C.byref(o)))
+        return out if out is not None else Ciphertext(o.value, self)
+
+    def ciphertext_scale(self, ct):
+        v = C.c_double()
+        _check("hd_ciphertext_scale", load().hd_ciphertext_scale(ct.h, C.byref(v)))
+        return v.value
+
+    def decrypt_slots(self, sk, ct):
+        z = np.zeros(self.n // 2, np.float64)
+        _check("hd_decrypt_slots", load().hd_decrypt_slots(self.h, sk.h, ct.h, _ptr(z), z.size))
+        return z
+
     def query(self, evk, db, query, outs=None):
         nloc = db.num_local
         if outs is None:
@@ -443,6 +486,20 @@ class Context(_Handle):
         out = VP()
         _check("hd_test_rescale", load().hd_test_rescale(self.h, ct.h, C.byref(out)))
         return Ciphertext(out.value, self)
+
+
+def chebyshev_degree(kappa):
+    d = C.c_uint32()
+    _check("hd_chebyshev_degree", load().hd_chebyshev_degree(kappa, C.byref(d)))
+    return d.value
+
+
+def chebyshev_coefficients(delta, degree):
+    """Client side (host): coefficients of the Chebyshev sign approximation (R29)."""
+    c = np.zeros(degree + 1, np.float64)
+    _check("hd_chebyshev_coefficients", load().hd_chebyshev_coefficients(C.c_double(delta), degree, _ptr(c),
+                                                                         c.size))
+    return c
 
 
 def _stream_handle(stream):

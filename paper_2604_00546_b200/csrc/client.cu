@@ -396,23 +396,7 @@ extern "C" hd_status hd_decrypt(hd_context *c, const hd_secret_key *sk, const hd
   return s;
 }
 
-extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, const hd_layout *lay,
-                                       const hd_ciphertext *const *cts, size_t n_ct, double *scores, size_t capacity,
-                                       size_t *written) {
-  if (!c || !sk || !lay || !cts || !scores) return hd_fail(HD_E_INVALID_ARG, "null argument");
-  const int n = c->n, ns = c->ns, N = (int)lay->block_n, M = (int)lay->blocks_m;
-  const int G = (int)lay->groups_per_ct, stride = lay->packing == HD_PACKING_REPLICATED ? 2 * N : N;
-  const long long per = (long long)G * N;
-  const long long v_first = (long long)lay->agg_begin * per;
-  const long long v_end = std::min<long long>((long long)lay->num_vectors, (long long)(lay->agg_begin + n_ct) * per);
-  if (v_end <= v_first) return hd_fail(HD_E_INVALID_ARG, "no vectors in the given aggregates");
-  if (capacity < (size_t)(v_end - v_first)) return hd_fail(HD_E_INVALID_ARG, "scores capacity too small");
-  uint32_t nl = 0;
-  for (size_t i = 0; i < n_ct; i++) {
-    if (!cts[i]) return hd_fail(HD_E_INVALID_ARG, "null ciphertext");
-    if (i == 0) nl = cts[i]->limbs;
-    if (cts[i]->limbs != nl) return hd_fail(HD_E_LEVEL, "mixed ciphertext levels");
-  }
+static CrtTab crt_table(const hd_context *c, uint32_t nl) {
   CrtTab ctab{};
   for (uint32_t i = 0; i < nl; i++)
     for (uint32_t k = 0; k < i; k++) ctab.inv[i][k] = inv_host(c->mod[k], c->mod[i]);
@@ -430,6 +414,27 @@ extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, c
     }
     for (uint32_t w = 0; w <= nl; w++) ctab.Q[w] = W[w];
   }
+  return ctab;
+}
+
+extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, const hd_layout *lay,
+                                       const hd_ciphertext *const *cts, size_t n_ct, double *scores, size_t capacity,
+                                       size_t *written) {
+  if (!c || !sk || !lay || !cts || !scores) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  const int n = c->n, ns = c->ns, N = (int)lay->block_n, M = (int)lay->blocks_m;
+  const int G = (int)lay->groups_per_ct, stride = lay->packing == HD_PACKING_REPLICATED ? 2 * N : N;
+  const long long per = (long long)G * N;
+  const long long v_first = (long long)lay->agg_begin * per;
+  const long long v_end = std::min<long long>((long long)lay->num_vectors, (long long)(lay->agg_begin + n_ct) * per);
+  if (v_end <= v_first) return hd_fail(HD_E_INVALID_ARG, "no vectors in the given aggregates");
+  if (capacity < (size_t)(v_end - v_first)) return hd_fail(HD_E_INVALID_ARG, "scores capacity too small");
+  uint32_t nl = 0;
+  for (size_t i = 0; i < n_ct; i++) {
+    if (!cts[i]) return hd_fail(HD_E_INVALID_ARG, "null ciphertext");
+    if (i == 0) nl = cts[i]->limbs;
+    if (cts[i]->limbs != nl) return hd_fail(HD_E_LEVEL, "mixed ciphertext levels");
+  }
+  const CrtTab ctab = crt_table(c, nl);
   uint64_t *m = nullptr;
   double *re = nullptr, *im = nullptr, *dsc = nullptr;
   const size_t nsc = (size_t)(v_end - v_first);
@@ -465,6 +470,44 @@ extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, c
   cudaFree(im);
   cudaFree(dsc);
   if (!s && written) *written = nsc;
+  return s;
+}
+
+// Decrypt + decode one ciphertext at its own scale (R29): the real parts of all numSlots slots.
+extern "C" hd_status hd_decrypt_slots(hd_context *c, const hd_secret_key *sk, const hd_ciphertext *ct, double *slots,
+                                      size_t cap) {
+  if (!c || !sk || !ct || !slots) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  if (cap < (size_t)c->ns) return hd_fail(HD_E_INVALID_ARG, "slots capacity too small");
+  const int n = c->n, ns = c->ns;
+  const uint32_t nl = ct->limbs;
+  const CrtTab ctab = crt_table(c, nl);
+  uint64_t *m = nullptr;
+  double *re = nullptr, *im = nullptr;
+  cudaError_t e = cudaMalloc(&m, (size_t)nl * n * 8);
+  if (!e) e = cudaMalloc(&re, (size_t)ns * 8);
+  if (!e) e = cudaMalloc(&im, (size_t)ns * 8);
+  hd_status s = e ? hd_fail(HD_E_CUDA, cudaGetErrorString(e)) : HD_OK;
+  RowMap rm{};
+  rm.gsize = 1u << 30;
+  rm.mdiv = 1;
+  rm.mlen = nl;
+  for (uint32_t l = 0; l < nl; l++) rm.midx[l] = l;
+  if (!s) s = decrypt_to(c, sk, ct, m);
+  if (!s) s = ntt_rows(c, m, nl, rm, true);
+  if (!s) {
+    crt_decode_kernel<<<(n + TPB - 1) / TPB, TPB, 0, c->stream>>>(m, n, nl, ct->scale, c->logn - 1, re, im, c->mt, ctab);
+    ++c->launches;
+    for (int len = 2; len <= ns; len <<= 1)
+      fft_fwd_stage_kernel<<<(ns / 2 + TPB - 1) / TPB, TPB, 0, c->stream>>>(re, im, ns, len, c->rotg, c->xi_re,
+                                                                            c->xi_im, 2u * n);
+    c->launches += c->logn - 1;
+    e = cudaMemcpyAsync(slots, re, (size_t)ns * 8, cudaMemcpyDeviceToHost, c->stream);
+    if (!e) e = cudaStreamSynchronize(c->stream);
+    if (e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  }
+  cudaFree(m);
+  cudaFree(re);
+  cudaFree(im);
   return s;
 }
 

@@ -70,7 +70,7 @@ struct RowMap {
   uint32_t mdiv = 1, mlen = 1;
   uint32_t g2 = 1u << 30;
   uint64_t gstride = 0, s2 = 0, s3 = 0;
-  uint8_t midx[32] = {0};
+  uint8_t midx[64] = {0};  // ell*ell ModUp rows up to ell = 7 (L = 7, HD_MAXMOD 8)
   // fast divisors for gsize, min(g2, gsize), mdiv, mlen (rowmap_finalize; device use only)
   bool fast = false;
   FDiv fg, fg2, fmd, fml;
@@ -226,6 +226,8 @@ struct hd_ciphertext {
   hd_context *ctx;
   uint32_t limbs;
   uint64_t *data;                 // [2][limbs][n]
+  double scale = 0.0;             // CKKS scale of the message (2^scale_bits unless an
+                                  // evaluation changed it, R29)
   cudaEvent_t ready = nullptr;    // recorded by the last writer (any stream); readers wait on it
   cudaEvent_t used = nullptr;     // recorded by the last asynchronous reader (export_async);
                                   // writers wait on it before overwriting data

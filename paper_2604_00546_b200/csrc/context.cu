@@ -261,7 +261,8 @@ struct Header {
   uint32_t count;    // number of keys
   uint64_t mod_fp;   // fingerprint of the modulus chain
   uint64_t payload;  // bytes after the header
-  uint8_t pad[24];
+  double scale;      // ciphertext scale (0 in files of older writers: 2^scale_bits)
+  uint8_t pad[16];
 };
 static_assert(sizeof(Header) == 64, "header");
 
@@ -280,6 +281,7 @@ cudaMemcpyKind kind_of(int dst_dev, int src_dev) {
 
 hd_status alloc_ct(hd_context *c, uint32_t limbs, hd_ciphertext **out) {
   hd_ciphertext *ct = new hd_ciphertext{c, limbs, nullptr};
+  ct->scale = std::ldexp(1.0, (int)c->params.scale_bits);
   cudaError_t e = cudaMalloc(&ct->data, sizeof(uint64_t) * 2 * limbs * c->n);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ct->ready, cudaEventDisableTiming);
   if (e != cudaSuccess) {
@@ -312,6 +314,7 @@ extern "C" hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, si
   h.limbs = ct->limbs;
   h.mod_fp = mod_fingerprint(c);
   h.payload = payload;
+  h.scale = ct->scale;
   HD_CUDA(cudaStreamWaitEvent(c->stream, ct->ready, 0));  // last writer (e.g. hd_query's stream B)
   HD_CUDA(cudaMemcpyAsync(dst, &h, sizeof(h), kind_of(dst_on_device, 0), c->stream));
   HD_CUDA(cudaMemcpyAsync((char *)dst + sizeof(h), ct->data, payload, kind_of(dst_on_device, 1), c->stream));
@@ -344,6 +347,7 @@ extern "C" hd_status hd_ciphertext_import(hd_context *c, const void *src, size_t
   if (h.kind != 1 || h.limbs < 1 || h.limbs > (uint32_t)c->L) return hd_fail(HD_E_FORMAT, "not a ciphertext");
   hd_ciphertext *ct;
   if ((s = alloc_ct(c, h.limbs, &ct))) return s;
+  if (h.scale > 0.0) ct->scale = h.scale;
   cudaError_t e = cudaMemcpyAsync(ct->data, (const char *)src + sizeof(Header), h.payload,
                                   kind_of(1, src_on_device), c->stream);
   if (e == cudaSuccess) e = cudaEventRecord(ct->ready, c->stream);
@@ -367,6 +371,7 @@ extern "C" hd_status hd_ciphertext_import_into(hd_ciphertext *ct, const void *sr
     hd_status s = read_header(c, src, bytes, 0, h);
     if (s) return s;
     if (h.kind != 1 || h.limbs != ct->limbs) return hd_fail(HD_E_LEVEL, "shape mismatch");
+    ct->scale = h.scale > 0.0 ? h.scale : std::ldexp(1.0, (int)c->params.scale_bits);
   }
   // Host sources are uploaded on the context's upload stream, ordered only after the
   // ciphertext's last reader (e.g. the baby steps of the previous hd_query on it) and last
@@ -407,6 +412,7 @@ extern "C" hd_status hd_ciphertext_export_async(hd_ciphertext *ct, uint32_t nlim
   h.limbs = nlimbs;
   h.mod_fp = mod_fingerprint(c);
   h.payload = payload;
+  h.scale = ct->scale;
   if (dst_on_device)  // pageable source: staged by the runtime before this call returns
     HD_CUDA(cudaMemcpyAsync(dst, &h, sizeof(h), cudaMemcpyHostToDevice, c->sIO));
   else

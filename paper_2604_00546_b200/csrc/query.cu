@@ -145,6 +145,7 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
   for (size_t i = 0; i < n_out; i++) {
     if (out[i]->used) HD_CUDA(cudaStreamWaitEvent(sb, out[i]->used, 0));  // pending async export
     HD_CUDA(cudaMemcpyAsync(out[i]->data, db->outbuf + i * ct1, ct1 * 8, cudaMemcpyDeviceToDevice, sb));
+    out[i]->scale = std::ldexp(1.0, (int)c->params.scale_bits);  // R15: the scan's output scale
     HD_CUDA(cudaEventRecord(out[i]->ready, sb));
   }
   HD_CUDA(cudaEventRecord(db->ev_done, sb));

@@ -54,3 +54,15 @@ def test_no_cpu_fallback_without_device():
     with pytest.raises(hd.HDError) as e:
         hd.Context(12)
     assert e.value.code == hd.HD_E_CUDA
+
+
+def test_host_chebyshev_coefficients_match_the_oracle(oracle_mod):
+    """Client-side host functions (no device): the kappa table of P:L721 and coefficients
+    identical to the oracle's, bit for bit (both sides must encode the same constants)."""
+    import numpy as np
+    import paper_2604_00546_b200 as hd
+    assert [hd.chebyshev_degree(k) for k in (7, 8, 9, 10)] == [5, 13, 27, 59]
+    with pytest.raises(hd.HDError):
+        hd.chebyshev_degree(6)
+    for delta, n in ((0.5, 13), (-0.2, 5), (0.0, 27), (0.75, 59)):
+        assert (hd.chebyshev_coefficients(delta, n) == oracle_mod.cheb_coeffs(delta, n)).all()

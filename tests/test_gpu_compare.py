@@ -1,0 +1,131 @@
+"""GPU parity of the encrypted comparison and the scenario tails (NEXT-3, R29): the CUDA path
+through the C ABI vs the CPU oracle, bit-exact on every residue (scan outputs at six limbs,
+ChebyshevCompare of a batch of aggregates incl. a ragged tail, membership), equal scales, and
+decrypted comparisons vs the plain Chebyshev series of the brute-force cosine."""
+import dataclasses
+
+import numpy as np
+import pytest
+from numpy.polynomial import chebyshev as npcheb
+
+from synth_inputs import CONFIGS, ENC_SEED_BASE, make_dataset
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import oracle  # noqa: E402
+import paper_2604_00546_b200 as hd  # noqa: E402
+
+D45 = 2.0 ** 45
+
+
+def _cos(db, q):
+    d = db.astype(np.float64)
+    qq = q.astype(np.float64)
+    return d @ qq / (np.linalg.norm(d, axis=1) * np.linalg.norm(qq))
+
+
+class CmpRun:
+    """C1 ring (2^12) at L = 6 limbs, flat packing, 5000 vectors -> 3 aggregates (last ragged)."""
+
+    def __init__(self):
+        cfg = dataclasses.replace(CONFIGS["C1"], limbs=6, num_vectors=5000)
+        self.cfg = cfg
+        self.ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
+        self.o = oracle.Oracle(cfg.log_n, cfg.limbs, seed=1)
+        self.db_vecs, self.q, self.pos = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+        scan_steps = [int(s) for s in self.ctx.rotation_steps(cfg.dim, cfg.n1, packing="flat")]
+        self.mem_steps = [int(s) for s in self.ctx.membership_steps()]
+        self.steps = sorted(set(scan_steps) | set(self.mem_steps))
+        self.sk, self.evk = self.ctx.keygen(np.array(self.steps, np.int32))
+        self.ctx.relin_keygen(self.sk, self.evk)
+        self.qct = self.ctx.encrypt_query(self.sk, self.q, ENC_SEED_BASE)
+        self.db = self.ctx.enroll(self.db_vecs, cfg.n1, packing="flat")
+        self.outs = self.ctx.query(self.evk, self.db, self.qct)
+        torch.cuda.synchronize()
+        _, self.s_ntt = self.o.secret_key()
+        self.ok_steps, self.ok_keys = self.o.keyset(self.s_ntt, self.steps)
+        self.rlk = self.o.relin_key(self.s_ntt)
+        z = self.o.query_slots(self.q)
+        qct = self.o.encrypt(self.s_ntt, self.o.encode(z, D45, cfg.limbs), ENC_SEED_BASE)
+        r = self.o.baby_steps(qct, cfg.n1, self.ok_steps, self.ok_keys)
+        self.ref_outs = []
+        per = self.o.ns
+        for agg in range(len(self.outs)):
+            v0, v1 = agg * per, min(cfg.num_vectors, (agg + 1) * per)
+            D = self.o.enroll_aggregate_flat(self.o.normalize_rows(self.db_vecs[v0:v1]), v0, cfg.num_vectors,
+                                             cfg.n1, agg)
+            self.ref_outs.append(self.o.scan_aggregate_flat(r, cfg.n1, cfg.dim, D, self.ok_steps, self.ok_keys))
+        self.cos = _cos(self.db_vecs, self.q)
+
+
+@pytest.fixture(scope="module")
+def run():
+    return CmpRun()
+
+
+def test_scan_bit_exact_at_six_limbs(run):
+    assert len(run.outs) == 3
+    for got, ref in zip(run.outs, run.ref_outs):
+        assert got.limbs == 5 and (run.ctx.ciphertext_residues(got) == ref).all()
+        assert run.ctx.ciphertext_scale(got) == D45
+
+
+@pytest.mark.parametrize("delta,kappa", [(0.5, 8), (-0.2, 7)])
+def test_compare_bit_exact(run, delta, kappa):
+    n = hd.chebyshev_degree(kappa)
+    c = hd.chebyshev_coefficients(delta, n)
+    assert (c == oracle.cheb_coeffs(delta, n)).all()
+    cmp = run.ctx.compare(run.evk, run.outs, c)
+    torch.cuda.synchronize()
+    for agg, (got, ref) in enumerate(zip(cmp, run.ref_outs)):
+        want, scale = run.o.cheb_compare(ref, D45, c, run.rlk)
+        assert got.limbs == want.shape[1] == 5 - int(np.ceil(np.log2(n + 1)))
+        assert (run.ctx.ciphertext_residues(got) == want).all(), agg
+        assert run.ctx.ciphertext_scale(got) == scale
+
+
+def test_identification_decodes_to_the_series(run):
+    c = hd.chebyshev_coefficients(0.5, 13)
+    cmp = run.ctx.compare(run.evk, run.outs, c)
+    per = run.ctx.ns
+    got = np.concatenate([run.ctx.decrypt_slots(run.sk, ct) for ct in cmp])[: run.cfg.num_vectors]
+    assert np.abs(got - npcheb.chebval(run.cos, c)).max() < 1e-5
+    assert (got[run.pos] > 0.8).all() and np.delete(got, run.pos).max() < 0.3
+    assert per * len(cmp) >= run.cfg.num_vectors
+    # in-place reuse of the outputs gives the same bits
+    again = run.ctx.compare(run.evk, run.outs, c, outs=cmp)
+    assert again[0] is cmp[0]
+    ref = run.o.cheb_compare(run.ref_outs[1], D45, c, run.rlk)[0]
+    assert (run.ctx.ciphertext_residues(again[1]) == ref).all()
+
+
+def test_membership_bit_exact(run):
+    c = hd.chebyshev_coefficients(0.5, 13)
+    cmp = run.ctx.compare(run.evk, run.outs, c)
+    mem = run.ctx.membership(run.evk, cmp)
+    torch.cuda.synchronize()
+    refs = np.stack([run.o.cheb_compare(r, D45, c, run.rlk)[0] for r in run.ref_outs])
+    want = run.o.membership(refs, np.array(run.mem_steps, np.int32),
+                            run.ok_keys[[run.steps.index(s) for s in run.mem_steps]])
+    assert (run.ctx.ciphertext_residues(mem) == want).all()
+    z = run.ctx.decrypt_slots(run.sk, mem)
+    total = npcheb.chebval(run.cos, c).sum() + (len(cmp) * run.ctx.ns - run.cfg.num_vectors) * npcheb.chebval(0.0, c)
+    assert np.abs(z - total).max() < 1e-3 * max(1.0, abs(total))
+
+
+def test_compare_errors(run):
+    c = hd.chebyshev_coefficients(0.5, 27)   # depth 5 > the 4 levels left
+    with pytest.raises(hd.HDError) as e:
+        run.ctx.compare(run.evk, run.outs, c)
+    assert e.value.code == -6  # HD_E_LEVEL
+    sk2, evk2 = run.ctx.keygen(np.array([1], np.int32))   # no relinearisation key
+    with pytest.raises(hd.HDError) as e:
+        run.ctx.compare(evk2, run.outs[:1], hd.chebyshev_coefficients(0.5, 13))
+    assert e.value.code == -5  # HD_E_MISSING_KEY
+    with pytest.raises(hd.HDError) as e:
+        run.ctx.membership(evk2, run.outs[:1])
+    assert e.value.code == -5
