@@ -49,6 +49,12 @@ def parse():
     ap.add_argument("--packing", default="replicated", choices=["replicated", "flat", "flat_tbs"],
                     help="stride-2N replicated blocks + fold (the north-star scan) or the flat pre-rotated "
                          "layout (NEXT-2, BSGS-RTX-TBE)")
+    ap.add_argument("--scenario", default="scan", choices=["scan", "identification", "membership"],
+                    help="scan only (the north-star hot path), or + the encrypted Chebyshev comparison of every "
+                         "score ciphertext (identification), + EvalAddMany / RotateAndSum (membership) (NEXT-3)")
+    ap.add_argument("--kappa", type=int, default=8, help="comparison depth budget (P:L721: 8 -> degree 13)")
+    ap.add_argument("--delta", type=float, default=0.5, help="comparison threshold")
+    ap.add_argument("--limbs", type=int, default=0, help="RNS limbs (default 3; 6 for the comparison scenarios)")
     ap.add_argument("--db", default="plain", choices=["plain", "encrypted"],
                     help="plaintext diagonals (the north-star scan) or the encrypted-database mode (NEXT-1)")
     return ap.parse_args()
@@ -75,7 +81,7 @@ def cfg_dict(cfg, world, scaling_note):
 # --------------------------------------------------------------------------------------------
 # CPU oracle timing (cpu_baseline and --impl reference): bounded sample, extrapolated
 # --------------------------------------------------------------------------------------------
-def oracle_sample(cfg, rng_seed=0):
+def oracle_sample(cfg, rng_seed=0, scenario="scan"):
     """Time one sample of the oracle on uniform random residues of the C4 shapes:
     one hoisted baby rotation, one giant-step MAC sum, one rescale, one giant rotation.
     Per-query time = ModUp + (n1-1) t_baby + A (n_g (t_mac + t_rs) + (nnz+1) t_rot)."""
@@ -115,31 +121,66 @@ def oracle_sample(cfg, rng_seed=0):
     t_rot = time.perf_counter() - t0
     per_query = t_modup + (n1 - 1) * t_baby + cfg.aggregates * (nj * (t_mac + t_rs) + (nnz + 1) * t_rot)
     sample_s = t_modup + t_baby + t_mac + t_rs + t_rot
+    if scenario != "scan":  # + one oracle ChebyshevCompare per aggregate (NEXT-3)
+        import oracle as _o
+        c = _o.cheb_coeffs(0.5, _o.cheb_degree(8))
+        t0 = time.perf_counter()
+        o.cheb_compare(np.ascontiguousarray(q[:, : L - 1]), 2.0 ** 45, c, key)
+        t_cmp = time.perf_counter() - t0
+        per_query += cfg.aggregates * t_cmp
+        sample_s += t_cmp
+        if scenario == "membership":  # + log2(numSlots) rotations at one limb
+            t0 = time.perf_counter()
+            o.rotate(np.ascontiguousarray(q[:, :1]), key, 1)
+            t_r1 = time.perf_counter() - t0
+            per_query += (cfg.log_n - 1) * t_r1
+            sample_s += t_r1
     return per_query, sample_s
+
+
+def workload_cfg(args):
+    """BASELINE config, with 6 RNS limbs when the comparison follows the scan (R29)."""
+    cfg = CONFIGS[args.config]
+    limbs = args.limbs or (6 if args.scenario != "scan" else cfg.limbs)
+    if limbs != cfg.limbs:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, limbs=limbs)
+    return cfg
+
+
+def metric_name(args):
+    if args.scenario == "scan":
+        return METRIC
+    return (f"encrypted queries/sec (2^20 x 512 {args.scenario}: scan + Chebyshev comparison"
+            + (" + EvalAddMany/RotateAndSum)" if args.scenario == "membership" else " of every score ciphertext)"))
+
+
+SAMPLE_TAIL = {"scan": "", "identification": " + 1 ChebyshevCompare (kappa 8) per aggregate",
+               "membership": " + 1 ChebyshevCompare per aggregate + log2(numSlots) one-limb rotations"}
 
 
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
+    cfg = workload_cfg(args)
     times, samples = [], []
     for i in range(args.warmup + args.steps):
-        pq, ss = oracle_sample(cfg, i)
+        pq, ss = oracle_sample(cfg, i, args.scenario)
         if i >= args.warmup:
             times.append(pq)
             samples.append(ss)
     pq = statistics.mean(times)
     v = 1.0 / pq
-    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+    line = {"impl": "reference", "metric": metric_name(args), "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": pq * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64 (RNS residues)", "data": "synthetic",
             "config": cfg_dict(cfg, 1, "CPU oracle, single thread"),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": "per step: oracle ModUp + 1 hoisted baby rotation + 1 giant-step MAC sum + "
-                                       "1 rescale + 1 giant rotation at the workload's shapes on uniform random "
+                                       "1 rescale + 1 giant rotation%s at the workload's shapes on uniform random "
                                        "residues (~%.1f s of CPU), extrapolated to the whole query" %
-                                       statistics.mean(samples)},
+                                       (SAMPLE_TAIL[args.scenario], statistics.mean(samples))},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -217,7 +258,10 @@ def main():
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    cfg = CONFIGS[args.config]
+    cfg = workload_cfg(args)
+    tail = args.scenario != "scan"
+    if args.scenario == "membership" and args.packing == "replicated":
+        raise SystemExit("--scenario membership needs a flat packing (every slot a vector; DESIGN.md R29)")
     stream = torch.cuda.current_stream()
     ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1, device=local, stream=stream)
     flat = args.packing in ("flat", "flat_tbs")
@@ -233,9 +277,12 @@ def main():
         steps = np.array(sorted(set(int(s) for s in steps) | set(int(s) for s in ctx.prerotation_steps(cfg.dim, cfg.n1))),
                          np.int32)
     enc_db = args.db == "encrypted"
+    if args.scenario == "membership":  # + the power-of-two keys of RotateAndSum
+        steps = np.array(sorted(set(int(s) for s in steps) | set(int(s) for s in ctx.membership_steps())), np.int32)
+    coeffs = hd.chebyshev_coefficients(args.delta, hd.chebyshev_degree(args.kappa)) if tail else None
     if rank == 0:
         sk, evk = ctx.keygen(steps)
-        if enc_db:  # relinearisation key travels with the eval keys (reserved step 0)
+        if enc_db or tail:  # relinearisation key travels with the eval keys (reserved step 0)
             ctx.relin_keygen(sk, evk)
     pk = None
     if enc_db:  # public key from rank 0 to every enroller
@@ -282,23 +329,37 @@ def main():
     torch.cuda.synchronize()
     nloc = a1 - a0
     outs = None
+    cmps = None
+    mem = None
     out_ct_bytes = None
     gbuf = None
 
+    def results():
+        """the step's result ciphertexts: scores, comparisons, or the (per-rank) membership sum"""
+        if args.scenario == "membership":
+            return [mem]
+        return cmps if tail else outs
+
     def step():
-        nonlocal outs, out_ct_bytes, gbuf
+        nonlocal outs, cmps, mem, out_ct_bytes, gbuf
         if world > 1:  # a1: query broadcast over NCCL, imported in place (no allocation)
             dist.broadcast(qbuf, 0)
             if rank != 0:
                 ctx.ciphertext_import_into(qct, qbuf.data_ptr(), ct_bytes, on_device=True)
         outs = ctx.query(evk, db, qct, outs)
-        if world > 1:  # a9: score ciphertexts gathered to rank 0 over NCCL
+        if tail:  # NEXT-3: ChebyshevCompare of every score ciphertext (+ membership sum)
+            cmps = ctx.compare(evk, outs, coeffs, cmps)
+            if args.scenario == "membership":
+                mem = ctx.membership(evk, cmps, mem)
+        if world > 1:  # a9: result ciphertexts gathered to rank 0 over NCCL
+            res = results()
             if out_ct_bytes is None:
-                out_ct_bytes = ctx.ciphertext_export_size(outs[0])
-                gbuf = torch.empty(nloc * out_ct_bytes, dtype=torch.uint8, device=dev)
-            for i, o in enumerate(outs):
+                out_ct_bytes = ctx.ciphertext_export_size(res[0])
+                gbuf = torch.empty(len(res) * out_ct_bytes, dtype=torch.uint8, device=dev)
+            for i, o in enumerate(res):
                 ctx.ciphertext_export(o, (gbuf.data_ptr() + i * out_ct_bytes, out_ct_bytes), on_device=True)
-            hdd.gather_bytes(gbuf, ((A + world - 1) // world) * out_ct_bytes, 0)
+            per_rank = 1 if args.scenario == "membership" else (A + world - 1) // world
+            hdd.gather_bytes(gbuf, per_rank * out_ct_bytes, 0)
 
     clk = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
     clk.start()  # nvidia-smi sampler (100 ms); only samples inside the timed window are kept
@@ -340,8 +401,8 @@ def main():
         # the asynchronous export, so step k's download overlaps step k+1's scan; every
         # step's scores are in pinned host memory when the timed region closes
         host_q = torch.from_numpy(ctx.ciphertext_export(qct)).pin_memory()
-        ob = ctx.ciphertext_export_async(outs[0], None, nlimbs=1)
-        host_out = torch.empty(nloc * ob, dtype=torch.uint8).pin_memory()
+        ob = ctx.ciphertext_export_async(results()[0], None, nlimbs=1)
+        host_out = torch.empty(len(results()) * ob, dtype=torch.uint8).pin_memory()
         # two query ciphertexts: step k+1's upload (context copy stream) overlaps step k's scan
         qin = [ctx.ciphertext_import(host_q.numpy()), ctx.ciphertext_import(host_q.numpy())]
         torch.cuda.synchronize()
@@ -349,13 +410,17 @@ def main():
         for k in range(args.e2e_steps):
             ctx.ciphertext_import_into(qin[k % 2], host_q.data_ptr(), host_q.numel(), on_device=False)
             outs = ctx.query(evk, db, qin[k % 2], outs)
-            for i, o in enumerate(outs):
+            if tail:
+                cmps = ctx.compare(evk, outs, coeffs, cmps)
+                if args.scenario == "membership":
+                    mem = ctx.membership(evk, cmps, mem)
+            for i, o in enumerate(results()):
                 ctx.ciphertext_export_async(o, (host_out.data_ptr() + i * ob, ob), nlimbs=1)
         ctx.synchronize()
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - t0
         e2e = {"value": args.e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(host_q.numel()),
-               "d2h_bytes_per_step": int(nloc * ob), "steps": args.e2e_steps,
+               "d2h_bytes_per_step": int(len(results()) * ob), "steps": args.e2e_steps,
                "api": "hd_ciphertext_import_into(host) -> hd_query -> hd_ciphertext_export_async(host, 1 limb) x A"
                       " -> hd_context_synchronize"}
     # ---- roofline of the dominant kernel (MAC, HBM-bound) ----
@@ -403,7 +468,26 @@ def main():
     query_roofline = {"bytes": q_bytes, "achieved": q_bytes / (ms_per_step / 1e3) / 1e9, "peak": peak,
                       "unit": "GB/s", "frac": q_bytes / (ms_per_step / 1e3) / 1e9 / peak,
                       "roofline_queries_per_s": peak * 1e9 / q_bytes}  # every rank serves every query
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+    tail_ms = None
+    if tail:  # CUDA events around the comparison (and membership) of the last scan's outputs
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        reps = 3
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(reps):
+            cmps = ctx.compare(evk, outs, coeffs, cmps)
+        e1.record(stream)
+        if args.scenario == "membership":
+            for _ in range(reps):
+                mem = ctx.membership(evk, cmps, mem)
+        e2.record(stream)
+        torch.cuda.synchronize()
+        tail_ms = {"compare": e0.elapsed_time(e1) / reps, "compare_per_ciphertext": e0.elapsed_time(e1) / reps / nloc,
+                   "membership": e1.elapsed_time(e2) / reps if args.scenario == "membership" else None,
+                   "kappa": args.kappa, "degree": len(coeffs) - 1, "delta": args.delta,
+                   "result_limbs": results()[0].limbs}
+    metric = metric_name(args)
+    line = {"metric": metric, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64 (RNS residues, 64-bit modular integer arithmetic)",
             "data": "synthetic (P:L2175-2179 generator, seeded)",
@@ -425,13 +509,14 @@ def main():
             "roofline": {"bound": "hbm", "kernel": "mac_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": mac_bytes, "avg_launch_ms": mac_avg_ms},
-            "keyswitch": keyswitch, "query_roofline": query_roofline,
+            "keyswitch": keyswitch, "query_roofline": query_roofline, "tail_ms": tail_ms,
+            "scenario": args.scenario,
             "clocks": clocks, "e2e": e2e}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import multiprocessing
         pqs, total, reps = [], 0.0, 0
         while total < 10.0 and reps < 60:  # bounded sample: ~10 s of single-thread oracle work
-            pq, ss = oracle_sample(cfg, reps)
+            pq, ss = oracle_sample(cfg, reps, args.scenario)
             pqs.append(pq)
             total += ss
             reps += 1
@@ -439,7 +524,7 @@ def main():
         line["cpu_baseline"] = {"value": 1.0 / pq, "unit": UNIT, "cores": 1, "kind": "oracle",
                                 "host_cores_available": multiprocessing.cpu_count(),
                                 "sample": f"{reps} x (oracle ModUp + 1 hoisted baby rotation + 1 giant-step MAC sum + "
-                                          "1 rescale + 1 giant rotation at the workload's shapes on uniform random "
+                                          f"1 rescale + 1 giant rotation{SAMPLE_TAIL[args.scenario]} at the workload's shapes on uniform random "
                                           f"residues), {total:.1f} s of CPU in total, extrapolated to one whole query "
                                           "(ModUp + (n1-1) baby + A (nj (MAC + rescale) + (nnz+1) rotations))"}
     if rank == 0:

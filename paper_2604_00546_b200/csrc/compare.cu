@@ -363,14 +363,17 @@ struct DevKeys {  // device arrays {key pointers}, {Galois elements}
 };
 hd_status upload_keys(hd_context *c, const std::vector<const uint64_t *> &kp, const std::vector<uint32_t> &gl,
                       DevKeys &dk) {
+  // stream-ordered: no device-wide synchronisation (the pageable source is staged by the
+  // runtime before cudaMemcpyAsync returns)
   const size_t cnt = kp.size(), bytes = cnt * sizeof(uint64_t *) + cnt * sizeof(uint32_t);
   std::vector<char> host(bytes);
   memcpy(host.data(), kp.data(), cnt * sizeof(uint64_t *));
   memcpy(host.data() + cnt * sizeof(uint64_t *), gl.data(), cnt * sizeof(uint32_t));
   void *p = nullptr;
-  HD_CUDA(cudaMalloc(&p, bytes));
-  dk.mem = std::shared_ptr<void>(p, [](void *q) { cudaFree(q); });
-  HD_CUDA(cudaMemcpy(p, host.data(), bytes, cudaMemcpyHostToDevice));
+  HD_CUDA(cudaMallocAsync(&p, bytes, c->stream));
+  cudaStream_t s = c->stream;
+  dk.mem = std::shared_ptr<void>(p, [s](void *q) { cudaFreeAsync(q, s); });
+  HD_CUDA(cudaMemcpyAsync(p, host.data(), bytes, cudaMemcpyHostToDevice, c->stream));
   dk.kp = (const uint64_t *const *)p;
   dk.gal = (const uint32_t *)((char *)p + cnt * sizeof(uint64_t *));
   return HD_OK;

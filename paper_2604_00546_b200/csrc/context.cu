@@ -123,6 +123,13 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
     return hd_fail(HD_E_CUDA, "no CUDA device (libhd has no CPU fallback)");
   if (cuda_device < 0 || cuda_device >= ndev) return hd_fail(HD_E_INVALID_ARG, "bad device index");
   HD_CUDA(cudaSetDevice(cuda_device));
+  {  // stream-ordered workspaces of the comparison (compare.cu) stay mapped between calls
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+  }
   hd_context *c = new hd_context();
   c->params = p;
   c->device = cuda_device;

@@ -94,7 +94,8 @@ def test_identification_decodes_to_the_series(run):
     per = run.ctx.ns
     got = np.concatenate([run.ctx.decrypt_slots(run.sk, ct) for ct in cmp])[: run.cfg.num_vectors]
     assert np.abs(got - npcheb.chebval(run.cos, c)).max() < 1e-5
-    assert (got[run.pos] > 0.8).all() and np.delete(got, run.pos).max() < 0.3
+    far = np.abs(run.cos - 0.5) > 0.4      # the degree-13 series separates values far from delta
+    assert (got[run.pos] > 0.8).all() and np.abs(got[far] - (run.cos[far] >= 0.5)).max() < 0.2
     assert per * len(cmp) >= run.cfg.num_vectors
     # in-place reuse of the outputs gives the same bits
     again = run.ctx.compare(run.evk, run.outs, c, outs=cmp)
