@@ -52,6 +52,9 @@ def parse():
     ap.add_argument("--scenario", default="scan", choices=["scan", "identification", "membership"],
                     help="scan only (the north-star hot path), or + the encrypted Chebyshev comparison of every "
                          "score ciphertext (identification), + EvalAddMany / RotateAndSum (membership) (NEXT-3)")
+    ap.add_argument("--batch", type=int, default=1,
+                    help="queries per step through hd_query_batch (NEXT-4: one diagonal stream serves up to 4 "
+                         "queries); 1 = hd_query")
     ap.add_argument("--kappa", type=int, default=8, help="comparison depth budget (P:L721: 8 -> degree 13)")
     ap.add_argument("--delta", type=float, default=0.5, help="comparison threshold")
     ap.add_argument("--limbs", type=int, default=0, help="RNS limbs (default 3; 6 for the comparison scenarios)")
@@ -310,25 +313,34 @@ def main():
         ctx.database_prerotate(evk, db)
         prerot_s = time.perf_counter() - t_p
     # ---- the query: encrypted on rank 0, exported into a device buffer (NCCL-broadcast each step) ----
+    # Q = --batch distinct queries (the first is the dataset's query with its planted matches)
+    Q = max(1, args.batch)
+    if Q > 1 and (enc_db or tail):
+        raise SystemExit("--batch > 1 needs plaintext diagonals and --scenario scan (hd_query_batch)")
     ct_bytes = 0
     if rank == 0:
-        qct = ctx.encrypt_query(sk, q, ENC_SEED_BASE)
-        ct_bytes = ctx.ciphertext_export_size(qct)
+        qrng = np.random.default_rng(99)
+        qvecs = [q] + [qrng.integers(-99, 100, cfg.dim).astype(np.float32) for _ in range(Q - 1)]
+        qcts = [ctx.encrypt_query(sk, v, ENC_SEED_BASE + i) for i, v in enumerate(qvecs)]
+        ct_bytes = ctx.ciphertext_export_size(qcts[0])
     nb = torch.tensor([ct_bytes], device=dev)
     if world > 1:
         dist.broadcast(nb, 0)
     ct_bytes = int(nb.item())
-    qbuf = torch.empty(ct_bytes, dtype=torch.uint8, device=dev)
+    qbuf = torch.empty(Q * ct_bytes, dtype=torch.uint8, device=dev)
     if rank == 0:
-        ctx.ciphertext_export(qct, (qbuf.data_ptr(), ct_bytes), on_device=True)
+        for i, qc in enumerate(qcts):
+            ctx.ciphertext_export(qc, (qbuf.data_ptr() + i * ct_bytes, ct_bytes), on_device=True)
     if world > 1:
         dist.broadcast(qbuf, 0)
         torch.cuda.synchronize()
-        if rank != 0:
-            qct = ctx.ciphertext_import(qbuf.data_ptr(), ct_bytes, on_device=True)  # setup-time allocation
+        if rank != 0:  # setup-time allocation
+            qcts = [ctx.ciphertext_import(qbuf.data_ptr() + i * ct_bytes, ct_bytes, on_device=True) for i in range(Q)]
+    qct = qcts[0]
     torch.cuda.synchronize()
     nloc = a1 - a0
     outs = None
+    outs_b = None  # hd_query_batch outputs [Q][nloc]
     cmps = None
     mem = None
     out_ct_bytes = None
@@ -341,12 +353,17 @@ def main():
         return cmps if tail else outs
 
     def step():
-        nonlocal outs, cmps, mem, out_ct_bytes, gbuf
+        nonlocal outs, outs_b, cmps, mem, out_ct_bytes, gbuf
         if world > 1:  # a1: query broadcast over NCCL, imported in place (no allocation)
             dist.broadcast(qbuf, 0)
             if rank != 0:
-                ctx.ciphertext_import_into(qct, qbuf.data_ptr(), ct_bytes, on_device=True)
-        outs = ctx.query(evk, db, qct, outs)
+                for i in range(Q):
+                    ctx.ciphertext_import_into(qcts[i], qbuf.data_ptr() + i * ct_bytes, ct_bytes, on_device=True)
+        if Q > 1:  # NEXT-4: Q queries per diagonal pass
+            outs_b = ctx.query_batch(evk, db, qcts, outs_b)
+            outs = [o for row in outs_b for o in row]
+        else:
+            outs = ctx.query(evk, db, qct, outs)
         if tail:  # NEXT-3: ChebyshevCompare of every score ciphertext (+ membership sum)
             cmps = ctx.compare(evk, outs, coeffs, cmps)
             if args.scenario == "membership":
@@ -358,7 +375,7 @@ def main():
                 gbuf = torch.empty(len(res) * out_ct_bytes, dtype=torch.uint8, device=dev)
             for i, o in enumerate(res):
                 ctx.ciphertext_export(o, (gbuf.data_ptr() + i * out_ct_bytes, out_ct_bytes), on_device=True)
-            per_rank = 1 if args.scenario == "membership" else (A + world - 1) // world
+            per_rank = 1 if args.scenario == "membership" else Q * ((A + world - 1) // world)
             hdd.gather_bytes(gbuf, per_rank * out_ct_bytes, 0)
 
     clk = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
@@ -393,23 +410,29 @@ def main():
     if world > 1:
         t_ms = hdd.max_over_ranks(t_ms, dev)
     ms_per_step = t_ms / args.steps
-    value = args.steps / (t_ms / 1e3)
+    value = Q * args.steps / (t_ms / 1e3)
     # ---- e2e through the public API with host buffers: H2D query, scan, D2H of every output ----
     e2e = None
     if world == 1 and args.e2e_steps > 0:
         # results leave the device level-reduced to 1 limb (R24: exact, half the bytes) through
         # the asynchronous export, so step k's download overlaps step k+1's scan; every
         # step's scores are in pinned host memory when the timed region closes
-        host_q = torch.from_numpy(ctx.ciphertext_export(qct)).pin_memory()
+        host_q = torch.from_numpy(np.concatenate([ctx.ciphertext_export(x) for x in qcts])).pin_memory()
+        qb = host_q.numel() // Q  # bytes of one exported query
         ob = ctx.ciphertext_export_async(results()[0], None, nlimbs=1)
         host_out = torch.empty(len(results()) * ob, dtype=torch.uint8).pin_memory()
-        # two query ciphertexts: step k+1's upload (context copy stream) overlaps step k's scan
-        qin = [ctx.ciphertext_import(host_q.numpy()), ctx.ciphertext_import(host_q.numpy())]
+        # two sets of query ciphertexts: step k+1's upload (context copy stream) overlaps step k's scan
+        qin = [[ctx.ciphertext_import(host_q.numpy()[i * qb:(i + 1) * qb]) for i in range(Q)] for _ in range(2)]
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for k in range(args.e2e_steps):
-            ctx.ciphertext_import_into(qin[k % 2], host_q.data_ptr(), host_q.numel(), on_device=False)
-            outs = ctx.query(evk, db, qin[k % 2], outs)
+            for i in range(Q):
+                ctx.ciphertext_import_into(qin[k % 2][i], host_q.data_ptr() + i * qb, qb, on_device=False)
+            if Q > 1:
+                outs_b = ctx.query_batch(evk, db, qin[k % 2], outs_b)
+                outs = [o for row in outs_b for o in row]
+            else:
+                outs = ctx.query(evk, db, qin[k % 2][0], outs)
             if tail:
                 cmps = ctx.compare(evk, outs, coeffs, cmps)
                 if args.scenario == "membership":
@@ -419,7 +442,7 @@ def main():
         ctx.synchronize()
         torch.cuda.synchronize()
         t_e2e = time.perf_counter() - t0
-        e2e = {"value": args.e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(host_q.numel()),
+        e2e = {"value": Q * args.e2e_steps / t_e2e, "unit": UNIT, "h2d_bytes_per_step": int(host_q.numel()),
                "d2h_bytes_per_step": int(len(results()) * ob), "steps": args.e2e_steps,
                "api": "hd_ciphertext_import_into(host) -> hd_query -> hd_ciphertext_export_async(host, 1 limb) x A"
                       " -> hd_context_synchronize"}
@@ -427,7 +450,9 @@ def main():
     L, n, N = cfg.limbs, 1 << cfg.log_n, cfg.dim
     nj = len(db_js(cfg, flat))
     dpoly, spoly = (2, 3) if enc_db else (1, 2)  # diagonal / giant-sum polynomials
-    mac_bytes = nloc * N * dpoly * L * n * 8 + cfg.n1 * 2 * L * n * 8 + nloc * nj * spoly * L * n * 8
+    d_passes = Q // 4 + (Q % 4) // 2 + (Q % 2)  # hd_query_batch: D streamed once per group of 4 / 2 / 1
+    mac_bytes = (d_passes * nloc * N * dpoly * L * n * 8
+                 + Q * (cfg.n1 * 2 * L * n * 8 + nloc * nj * spoly * L * n * 8))
     mac_avg_ms = statistics.mean(mac_ms)
     peak, peak_src = peaks()
     achieved = mac_bytes / (mac_avg_ms / 1e3) / 1e9
@@ -463,11 +488,12 @@ def main():
     # ---- whole-query compulsory bytes against the step time ----
     # giant keys (+ the fold key for the replicated packing)
     n_gkeys = (nj - 1) if flat else sum(1 for j in db_js(cfg) if ((cfg.n1 * j) % N + N) % N != 0) + 1
-    q_bytes = (nloc * N * dpoly * L * n * 8 + (cfg.n1 - 1) * key_bytes + n_gkeys * (L - 1) * 2 * L * n * 8
-               + 2 * L * n * 8 + nloc * 2 * (L - 1) * n * 8 + (nj * key_bytes if enc_db else 0))
+    q_bytes = (d_passes * nloc * N * dpoly * L * n * 8
+               + Q * ((cfg.n1 - 1) * key_bytes + n_gkeys * (L - 1) * 2 * L * n * 8
+                      + 2 * L * n * 8 + nloc * 2 * (L - 1) * n * 8 + (nj * key_bytes if enc_db else 0)))
     query_roofline = {"bytes": q_bytes, "achieved": q_bytes / (ms_per_step / 1e3) / 1e9, "peak": peak,
                       "unit": "GB/s", "frac": q_bytes / (ms_per_step / 1e3) / 1e9 / peak,
-                      "roofline_queries_per_s": peak * 1e9 / q_bytes}  # every rank serves every query
+                      "roofline_queries_per_s": Q * peak * 1e9 / q_bytes}  # every rank serves every query
     tail_ms = None
     if tail:  # CUDA events around the comparison (and membership) of the last scan's outputs
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
@@ -506,11 +532,11 @@ def main():
             "phase_ms_serial": dict(zip(["baby", "mac", "rescale", "giant", "fold", "baby_kip"],
                                         [float(x) for x in phase_serial])),
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "kernel": "mac_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "roofline": {"bound": "hbm", "kernel": "mac_cs_batch_kernel" if Q > 1 else "mac_cs_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": mac_bytes, "avg_launch_ms": mac_avg_ms},
             "keyswitch": keyswitch, "query_roofline": query_roofline, "tail_ms": tail_ms,
-            "scenario": args.scenario,
+            "scenario": args.scenario, "queries_per_step": Q,
             "clocks": clocks, "e2e": e2e}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import multiprocessing

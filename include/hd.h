@@ -205,6 +205,17 @@ hd_status hd_database_prerotate(hd_context *ctx, const hd_eval_keys *evk, hd_dat
  * respect to the host; outputs carry events that later readers wait on. */
 hd_status hd_query(hd_context *ctx, const hd_eval_keys *evk, const hd_database *db,
                    const hd_ciphertext *query, hd_ciphertext **out, size_t n_out);
+/* Query batching (NEXT-4): the scan of n_queries (1..64) independent query
+ * ciphertexts over the same database in one call.  The baby steps, rescale, giant steps and
+ * fold run per query as in hd_query; the diagonal MAC streams every diagonal word from HBM
+ * once for up to 4 queries (mac_cs_batch_kernel), so the dominant D bytes per query drop up
+ * to 4-fold.  out[q * n_local + i] receives the score ciphertext of aggregate agg_begin + i
+ * for query q, bit-identical to hd_query(queries[q]); n_out = n_queries * n_local.  Plaintext
+ * diagonals only (HD_E_INVALID_ARG for an encrypted database).  The batch workspace (baby
+ * steps and giant-step sums of n_queries queries, double-buffered) is allocated on the first
+ * call with a larger n_queries and kept; outputs as in hd_query. */
+hd_status hd_query_batch(hd_context *ctx, const hd_eval_keys *evk, const hd_database *db,
+                         const hd_ciphertext *const *queries, size_t n_queries, hd_ciphertext **out, size_t n_out);
 /* Cumulative number of CUDA kernels this context has launched (all entry points). */
 hd_status hd_launch_count(const hd_context *ctx, uint64_t *count);
 /* Per-phase device times (ms), averaged over the hd_query calls issued since the

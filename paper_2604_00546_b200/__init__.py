@@ -36,7 +36,7 @@ ABI_FUNCTIONS = [
     "hd_public_keygen", "hd_public_key_export", "hd_public_key_import", "hd_relin_keygen", "hd_public_key_destroy",
     "hd_enroll_ex", "hd_rotation_steps_ex", "hd_prerotation_steps", "hd_database_prerotate",
     "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
-    "hd_ciphertext_scale", "hd_decrypt_slots",
+    "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch",
 ]
 
 
@@ -141,6 +141,7 @@ def load():
             L.hd_membership.argtypes = [VP, VP, VP, C.c_size_t, C.POINTER(VP)]
             L.hd_ciphertext_scale.argtypes = [VP, C.POINTER(C.c_double)]
             L.hd_decrypt_slots.argtypes = [VP, VP, VP, VP, C.c_size_t]
+            L.hd_query_batch.argtypes = [VP, VP, VP, VP, C.c_size_t, VP, C.c_size_t]
             _lib = L
         return _lib
 
@@ -375,6 +376,16 @@ class Context(_Handle):
         arr = (VP * nloc)(*[(o.h if o is not None else None) for o in outs])
         _check("hd_query", load().hd_query(self.h, evk.h, db.h, query.h, arr, nloc))
         return [o if o is not None else Ciphertext(arr[i], self) for i, o in enumerate(outs)]
+
+    def query_batch(self, evk, db, queries, outs=None):
+        """hd_query_batch: outs[q][i] = score ciphertext of local aggregate i for queries[q] (NEXT-4)."""
+        nloc, Q = db.num_local, len(queries)
+        flat = [None] * (Q * nloc) if outs is None else [o for row in outs for o in row]
+        qs = (VP * Q)(*[x.h for x in queries])
+        arr = (VP * (Q * nloc))(*[(o.h if o is not None else None) for o in flat])
+        _check("hd_query_batch", load().hd_query_batch(self.h, evk.h, db.h, qs, Q, arr, Q * nloc))
+        res = [o if o is not None else Ciphertext(arr[i], self) for i, o in enumerate(flat)]
+        return [res[q * nloc:(q + 1) * nloc] for q in range(Q)]
 
     def query_stats(self):
         """[baby, mac, rescale, giant, fold, baby_kip] ms averaged over the queries since the last call."""

@@ -261,6 +261,10 @@ struct hd_database {
   uint64_t *S2 = nullptr;                                  // second giant-sum buffer
   uint64_t *dig_b = nullptr, *u_b = nullptr, *tmp_b = nullptr;  // baby-step scratch (stream A)
   uint64_t qcount = 0;
+  // query batching (NEXT-4, hd_query_batch): baby steps of Q queries and their giant-step
+  // sums (double-buffered), allocated on the first batch of a given size
+  uint64_t *rB = nullptr, *SB[2] = {nullptr, nullptr};
+  uint32_t qb_cap = 0;
   cudaEvent_t ev_in = nullptr, ev_mac = nullptr, ev_done = nullptr, ev_sfree[2] = {nullptr, nullptr};
   // rotation-key tables for the (db, evk) pair last used: [0, n1-1) baby i = 1..n1-1,
   // [n1-1, n1-1+nj) giant j (NULL key when preRot = 0), [n1-1+nj] fold

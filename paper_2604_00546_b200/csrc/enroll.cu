@@ -255,6 +255,9 @@ extern "C" void hd_database_destroy(hd_database *db) {
   cudaFree(db->kptr);
   cudaFree(db->gal);
   cudaFree(db->S2);
+  cudaFree(db->rB);
+  cudaFree(db->SB[0]);
+  cudaFree(db->SB[1]);
   cudaFree(db->dig_b);
   cudaFree(db->u_b);
   cudaFree(db->tmp_b);

@@ -38,6 +38,10 @@ hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
                   const std::vector<int32_t> &js, bool flat);
 
+// Query batching (NEXT-4): Q queries per D pass; r [Q][n1][2][L][n], S [Q][A][nj][2][L][n].
+hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1,
+                        int N, const std::vector<int32_t> &js, bool flat, uint32_t Q);
+
 // Public-key encryption of count ciphertexts in place (c0 of ct_x = ct + x*ct_stride holds
 // the plaintext on entry); object ids obj0 + x; V, E0: count*L*n scratch each (client.cu).
 hd_status pk_encrypt_rows(hd_context *c, const hd_public_key *pk, uint64_t *ct, size_t ct_stride, uint32_t count,

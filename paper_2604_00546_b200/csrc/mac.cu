@@ -334,6 +334,127 @@ __global__ void __launch_bounds__(MAC_TPB) mac_ct_stream_kernel(const uint64_t *
     }
   }
 }
+// ---- query batching (NEXT-4): one D stream serves QB queries ---------------------------
+// As mac_cs_kernel with one giant step per thread, but every diagonal word loaded from HBM
+// is multiplied into the baby steps of QB queries (r: [QB][n1][2][L][n], S: [QB][A][nj][2][L][n]):
+// the D bytes per query drop QB-fold and the kernel turns from HBM- to issue-bound.
+template <int QB, int JT, bool FLUSH>
+__global__ void __launch_bounds__(MAC_TPB) mac_cs_batch_kernel(const uint64_t *__restrict__ D,
+                                                               const uint64_t *__restrict__ r,
+                                                               uint64_t *__restrict__ S, int n1, int N, int L,
+                                                               int logn, int jmin, int nj, uint32_t A, ModTab mt) {
+  const int n = 1 << logn;
+  const uint32_t a = blockIdx.x;
+  const uint32_t t = blockIdx.y * MAC_TPB + threadIdx.x;
+  const int ngrp = nj / JT;
+  const int m = blockIdx.z / ngrp, jg = blockIdx.z % ngrp;
+  const size_t ls = (size_t)L * n, rq = (size_t)n1 * 2 * ls;  // r stride between queries
+  const uint64_t *Da = D + (size_t)a * N * ls + (size_t)m * n + t;
+  const uint64_t *p[JT];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) p[jj] = Da + (size_t)(((jmin + jg * JT + jj) * n1) & (N - 1)) * ls;
+  const uint64_t *rr = r + (size_t)m * n + t;
+  CsAcc acc[JT][QB][2];
+  uint64_t part[JT][QB][2];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++)
+#pragma unroll
+    for (int b = 0; b < QB; b++) {
+      acc[jj][b][0] = acc[jj][b][1] = CsAcc{0, 0, 0, 0};
+      part[jj][b][0] = part[jj][b][1] = 0;
+    }
+  const uint64_t q = mt.q[m], bar = mt.bar[m], r64 = mt.r64[m], r64s = mt.r64s[m];
+  // software pipeline: the D words and the QB r pairs of step i+1 are in flight while step i
+  // is multiplied (the r loads are L2 hits; without the prefetch the kernel is latency-bound)
+  uint64_t d[JT];
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++) {
+    d[jj] = ld_stream(p[jj]);
+    p[jj] += ls;
+  }
+  uint64_t rc[QB][2];
+#pragma unroll
+  for (int b = 0; b < QB; b++) {
+    rc[b][0] = __ldg(rr + b * rq);
+    rc[b][1] = __ldg(rr + b * rq + ls);
+  }
+  for (int i = 0; i < n1; i++) {
+    const bool more = i + 1 < n1;
+    uint64_t dn[JT];
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      dn[jj] = more ? ld_stream(p[jj]) : 0;
+      p[jj] += ls;
+    }
+    uint64_t rn[QB][2];
+#pragma unroll
+    for (int b = 0; b < QB; b++) {
+      const uint64_t *rb = rr + b * rq + (size_t)(2 * i + 2) * ls;
+      rn[b][0] = more ? __ldg(rb) : 0;
+      rn[b][1] = more ? __ldg(rb + ls) : 0;
+    }
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      const uint32_t b0 = (uint32_t)d[jj], b1 = (uint32_t)(d[jj] >> 32);
+#pragma unroll
+      for (int b = 0; b < QB; b++) {
+        cs_mac(acc[jj][b][0], (uint32_t)rc[b][0], (uint32_t)(rc[b][0] >> 32), b0, b1);
+        cs_mac(acc[jj][b][1], (uint32_t)rc[b][1], (uint32_t)(rc[b][1] >> 32), b0, b1);
+      }
+      d[jj] = dn[jj];
+    }
+#pragma unroll
+    for (int b = 0; b < QB; b++) {
+      rc[b][0] = rn[b][0];
+      rc[b][1] = rn[b][1];
+    }
+    if ((i & 7) == 7) {
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++)
+#pragma unroll
+        for (int b = 0; b < QB; b++) {
+          cs_fold(acc[jj][b][0]);
+          cs_fold(acc[jj][b][1]);
+        }
+    }
+    if (FLUSH && (i & 127) == 127 && more) {
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++)
+#pragma unroll
+        for (int b = 0; b < QB; b++)
+#pragma unroll
+          for (int q2 = 0; q2 < 2; q2++) {
+            CsAcc &X = acc[jj][b][q2];
+            part[jj][b][q2] = addmod(part[jj][b][q2], reduce128(X.hi + X.cnt, X.lo, q, bar, r64, r64s), q);
+            X = CsAcc{0, 0, 0, 0};
+          }
+    }
+  }
+#pragma unroll
+  for (int jj = 0; jj < JT; jj++)
+#pragma unroll
+    for (int b = 0; b < QB; b++) {
+      uint64_t *Sb = S + (((size_t)b * A + a) * nj + jg * JT + jj) * 2 * ls + (size_t)m * n + t;
+#pragma unroll
+      for (int q2 = 0; q2 < 2; q2++) {
+        CsAcc &X = acc[jj][b][q2];
+        cs_fold(X);
+        Sb[(size_t)q2 * ls] = addmod(part[jj][b][q2], reduce128(X.hi + X.cnt, X.lo, q, bar, r64, r64s), q);
+      }
+    }
+}
+
+template <int QB, int JT>
+void launch_batch(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A, int n1, int N,
+                  int jmin, int nj) {
+  const dim3 grid(A, c->n / MAC_TPB, c->L * (nj / JT));
+  if (n1 > 128)
+    mac_cs_batch_kernel<QB, JT, true><<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, A,
+                                                                       c->mt);
+  else
+    mac_cs_batch_kernel<QB, JT, false><<<grid, MAC_TPB, 0, c->stream>>>(D, r, S, n1, N, c->L, c->logn, jmin, nj, A,
+                                                                        c->mt);
+}
 }  // namespace
 
 hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint64_t *S3, uint32_t A_loc, int n1,
@@ -381,5 +502,42 @@ hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t 
   }
   ++c->launches;
   HD_CUDA(cudaGetLastError());
+  return HD_OK;
+}
+
+hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1,
+                        int N, const std::vector<int32_t> &js, bool flat, uint32_t Q) {
+  if (js.empty() || A_loc == 0 || Q == 0) return HD_OK;
+  const int jmin = js.front(), nj = (int)js.size();
+  const size_t ls = (size_t)c->L * c->n, rq = (size_t)n1 * 2 * ls, sq = (size_t)A_loc * nj * 2 * ls;
+  const bool full = (flat ? N % n1 : (N / 2) % n1) == 0 && n1 <= 256 && c->n % MAC_TPB == 0;
+  bool small_q = true;
+  for (int l = 0; l < c->L; l++) small_q = small_q && c->mod[l] < (1ull << 60);
+  if (!(full && small_q)) {  // partial giant-step ranges / wide moduli: the per-query kernels
+    for (uint32_t b = 0; b < Q; b++) {
+      hd_status s = mac_run(c, D, r + b * rq, S + b * sq, A_loc, n1, N, js, flat);
+      if (s) return s;
+    }
+    return HD_OK;
+  }
+  // groups of up to G queries per D pass (HD_MAC_BATCH = max group 1, 2 or 4; default 4);
+  // two giant steps per thread (JT = 2) for groups of 1 and 2 (HD_MAC_BATCH_JT=1 disables)
+  const char *g_env = getenv("HD_MAC_BATCH"), *jt_env = getenv("HD_MAC_BATCH_JT");
+  const uint32_t gmax = g_env ? (uint32_t)atoi(g_env) : 4u;
+  for (uint32_t b0 = 0; b0 < Q;) {
+    const uint32_t left = Q - b0;
+    const uint32_t g = (left >= 4 && gmax >= 4) ? 4 : ((left >= 2 && gmax >= 2) ? 2 : 1);
+    const uint64_t *rb = r + b0 * rq;
+    uint64_t *Sb = S + b0 * sq;
+    const bool jt2 = nj % 2 == 0 && !(jt_env && jt_env[0] == '1');
+    if (g == 4) launch_batch<4, 1>(c, D, rb, Sb, A_loc, n1, N, jmin, nj);
+    else if (g == 2 && jt2) launch_batch<2, 2>(c, D, rb, Sb, A_loc, n1, N, jmin, nj);
+    else if (g == 2) launch_batch<2, 1>(c, D, rb, Sb, A_loc, n1, N, jmin, nj);
+    else if (jt2) launch_batch<1, 2>(c, D, rb, Sb, A_loc, n1, N, jmin, nj);
+    else launch_batch<1, 1>(c, D, rb, Sb, A_loc, n1, N, jmin, nj);
+    ++c->launches;
+    HD_CUDA(cudaGetLastError());
+    b0 += g;
+  }
   return HD_OK;
 }

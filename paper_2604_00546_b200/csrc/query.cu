@@ -14,6 +14,7 @@
 #include "ks.cuh"
 
 static hd_status giant_and_fold(hd_database *db, cudaEvent_t *E);
+static hd_status scan_tail(hd_database *db, uint64_t *Sbuf, cudaEvent_t *E, bool last, int par, hd_ciphertext **out);
 
 static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
   hd_context *c = db->ctx;
@@ -57,14 +58,17 @@ static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
 // overlaps the next query's A work; S is double-buffered (A waits until B's rescale
 // of the query two back has consumed the buffer).  With HD_SERIAL=1 both run on the
 // caller's stream.
-static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStream_t sa, cudaStream_t sb,
-                          hd_ciphertext **out, size_t n_out) {
+static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, uint32_t Q, cudaStream_t sa,
+                          cudaStream_t sb, hd_ciphertext **out, size_t n_out) {
   hd_context *c = db->ctx;
   const int n = c->n, L = c->L, n1 = (int)db->n1, nj = (int)db->js.size();
   const uint32_t A = db->A_loc;
   const size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * (L - 1) * n;
   const int par = (int)(db->qcount & 1);
-  uint64_t *Sbuf = par ? db->S2 : db->S;
+  uint64_t *Sbuf = Q > 1 ? db->SB[par] : (par ? db->S2 : db->S);
+  uint64_t *rbase = Q > 1 ? db->rB : db->r;
+  const size_t sL = (size_t)db->spoly * L * n;  // one giant-step sum
+  const size_t sq = (size_t)A * nj * sL;         // the sums of one query
   cudaStream_t caller = c->stream;
   hd_status s;
   cudaEvent_t *E = c->ev[c->ev_next % 64];
@@ -74,12 +78,14 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
   // A depends only on the query's last writer (not on the caller's stream position), so
   // the baby steps + MAC of this query can run while B still finishes the previous one.
   HD_CUDA(cudaEventRecord(db->ev_in, caller));
-  HD_CUDA(cudaStreamWaitEvent(sa, query->ready, 0));
-  hd_ciphertext *qmut = const_cast<hd_ciphertext *>(query);  // reader bookkeeping only
-  if (!qmut->used) {
-    HD_CUDA(cudaEventCreateWithFlags(&qmut->used, cudaEventDisableTiming));
-  } else {
-    HD_CUDA(cudaStreamWaitEvent(sa, qmut->used, 0));  // the new `used` covers earlier readers too
+  for (uint32_t qi = 0; qi < Q; qi++) {
+    HD_CUDA(cudaStreamWaitEvent(sa, queries[qi]->ready, 0));
+    hd_ciphertext *qmut = const_cast<hd_ciphertext *>(queries[qi]);  // reader bookkeeping only
+    if (!qmut->used) {
+      HD_CUDA(cudaEventCreateWithFlags(&qmut->used, cudaEventDisableTiming));
+    } else {
+      HD_CUDA(cudaStreamWaitEvent(sa, qmut->used, 0));  // the new `used` covers earlier readers too
+    }
   }
   if (db->qcount >= 2) HD_CUDA(cudaStreamWaitEvent(sa, db->ev_sfree[par], 0));
   c->stream = sa;
@@ -88,22 +94,28 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
     cudaEventRecord(E[7], sa);
     cudaEventRecord(E[8], sa);
   }
-  // ---- baby steps: r[0] = q; r[i] = Rot_i(q), hoisted ----
-  HD_CUDA(cudaMemcpyAsync(db->r, query->data, ctL * 8, cudaMemcpyDeviceToDevice, sa));
-  if (n1 > 1) {
-    if ((s = ks_modup(c, query->data + (size_t)L * n, 0, 1, L, db->dig_b, db->tmp_b))) return s;
-    cudaEventRecord(E[7], sa);
-    if ((s = ks_kip(c, db->dig_b, query->data + (size_t)L * n, 0, 1, n1 - 1, L, db->kptr, db->gal, db->u_b)))
-      return s;
-    cudaEventRecord(E[8], sa);
-    if ((s = ks_moddown(c, db->u_b, n1 - 1, n1 - 1, L, db->gal, query->data, 0, db->r + ctL, ctL, false,
-                        db->tmp_b)))
-      return s;
+  // ---- baby steps: r[0] = q; r[i] = Rot_i(q), hoisted (per query) ----
+  for (uint32_t qi = 0; qi < Q; qi++) {
+    const hd_ciphertext *query = queries[qi];
+    uint64_t *rq = rbase + (size_t)qi * n1 * ctL;
+    HD_CUDA(cudaMemcpyAsync(rq, query->data, ctL * 8, cudaMemcpyDeviceToDevice, sa));
+    if (n1 > 1) {
+      if ((s = ks_modup(c, query->data + (size_t)L * n, 0, 1, L, db->dig_b, db->tmp_b))) return s;
+      cudaEventRecord(E[7], sa);
+      if ((s = ks_kip(c, db->dig_b, query->data + (size_t)L * n, 0, 1, n1 - 1, L, db->kptr, db->gal, db->u_b)))
+        return s;
+      cudaEventRecord(E[8], sa);
+      if ((s = ks_moddown(c, db->u_b, n1 - 1, n1 - 1, L, db->gal, query->data, 0, rq + ctL, ctL, false,
+                          db->tmp_b)))
+        return s;
+    }
+    HD_CUDA(cudaEventRecord(const_cast<hd_ciphertext *>(query)->used, sa));  // not read after the baby steps
   }
   cudaEventRecord(E[1], sa);
-  HD_CUDA(cudaEventRecord(qmut->used, sa));  // the query is not read after the baby steps
-  // ---- MAC ----
-  if (db->encrypted) {
+  // ---- MAC; a batch streams D once for all its queries (NEXT-4) ----
+  if (Q > 1) {
+    if ((s = mac_batch_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat, Q))) return s;
+  } else if (db->encrypted) {
     if ((s = mac_ct_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js, db->flat))) return s;
   } else if ((s = mac_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js, db->flat))) {
     return s;
@@ -114,7 +126,26 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
   HD_CUDA(cudaStreamWaitEvent(sb, db->ev_mac, 0));
   c->stream = sb;
   cudaEventRecord(E[3], sb);
+  // outputs may still be read by caller-stream work enqueued before this call
+  HD_CUDA(cudaStreamWaitEvent(sb, db->ev_in, 0));
+  for (uint32_t qi = 0; qi < Q; qi++) {
+    if ((s = scan_tail(db, Sbuf + qi * sq, E, qi + 1 == Q, par, out + (size_t)qi * A))) return s;
+  }
+  HD_CUDA(cudaEventRecord(db->ev_done, sb));
+  HD_CUDA(cudaStreamWaitEvent(caller, db->ev_done, 0));
+  db->qcount++;
+  return HD_OK;
+}
+
+// Stream B of one query: relinearisation (encrypted), rescale, giant steps, fold, output copies.
+static hd_status scan_tail(hd_database *db, uint64_t *Sbuf, cudaEvent_t *E, bool last, int par, hd_ciphertext **out) {
+  hd_context *c = db->ctx;
+  const int n = c->n, L = c->L, n1 = (int)db->n1, nj = (int)db->js.size();
+  const uint32_t A = db->A_loc;
+  const size_t ct1 = (size_t)2 * (L - 1) * n;
   const size_t sL = (size_t)db->spoly * L * n;  // one giant-step sum
+  cudaStream_t sb = c->stream;
+  hd_status s;
   if (db->encrypted) {
     // ---- Relinearize every degree-2 S_{a,j}: (d0, d1) += KeySwitch_{s^2->s}(d2) ----
     const uint32_t total = A * nj;
@@ -137,20 +168,15 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *query, cudaStrea
         return s;
     }
   }
-  HD_CUDA(cudaEventRecord(db->ev_sfree[par], sb));
+  if (last) HD_CUDA(cudaEventRecord(db->ev_sfree[par], sb));
   cudaEventRecord(E[4], sb);
   if ((s = giant_and_fold(db, E))) return s;
-  // outputs may still be read by caller-stream work enqueued before this call
-  HD_CUDA(cudaStreamWaitEvent(sb, db->ev_in, 0));
-  for (size_t i = 0; i < n_out; i++) {
+  for (size_t i = 0; i < A; i++) {
     if (out[i]->used) HD_CUDA(cudaStreamWaitEvent(sb, out[i]->used, 0));  // pending async export
     HD_CUDA(cudaMemcpyAsync(out[i]->data, db->outbuf + i * ct1, ct1 * 8, cudaMemcpyDeviceToDevice, sb));
     out[i]->scale = std::ldexp(1.0, (int)c->params.scale_bits);  // R15: the scan's output scale
     HD_CUDA(cudaEventRecord(out[i]->ready, sb));
   }
-  HD_CUDA(cudaEventRecord(db->ev_done, sb));
-  HD_CUDA(cudaStreamWaitEvent(caller, db->ev_done, 0));
-  db->qcount++;
   return HD_OK;
 }
 
@@ -246,7 +272,7 @@ extern "C" hd_status hd_query(hd_context *c, const hd_eval_keys *evk, const hd_d
     sb = c->sB;
   }
   cudaStream_t caller = c->stream;
-  s = run_scan(db, query, sa, sb, outs.data(), n_out);
+  s = run_scan(db, &query, 1, sa, sb, outs.data(), n_out);
   c->stream = caller;
   if (s) {
     for (auto *f : fresh) hd_ciphertext_destroy(f);
@@ -256,6 +282,74 @@ extern "C" hd_status hd_query(hd_context *c, const hd_eval_keys *evk, const hd_d
   HD_CUDA(cudaGetLastError());
   db->has_run = true;
   // per-phase times are read lazily by hd_query_stats (no sync here)
+  return HD_OK;
+}
+
+extern "C" hd_status hd_query_batch(hd_context *c, const hd_eval_keys *evk, const hd_database *dbc,
+                                    const hd_ciphertext *const *queries, size_t n_queries, hd_ciphertext **out,
+                                    size_t n_out) {
+  if (!c || !evk || !dbc || !queries || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  if (n_queries == 0 || n_queries > 64) return hd_fail(HD_E_INVALID_ARG, "n_queries must be in [1, 64]");
+  hd_database *db = const_cast<hd_database *>(dbc);
+  if (db->ctx != c || evk->ctx != c) return hd_fail(HD_E_STATE, "objects from another context");
+  if (db->encrypted) return hd_fail(HD_E_INVALID_ARG, "query batching needs plaintext diagonals (hd_query per query)");
+  if (n_out != n_queries * db->A_loc) return hd_fail(HD_E_INVALID_ARG, "n_out must equal n_queries * local aggregates");
+  if (db->needs_prerotation) return hd_fail(HD_E_STATE, "FLAT_TBS database: call hd_database_prerotate first");
+  const int L = c->L, n = c->n, n1 = (int)db->n1, nj = (int)db->js.size();
+  const uint32_t Q = (uint32_t)n_queries;
+  for (size_t q = 0; q < n_queries; q++) {
+    if (!queries[q]) return hd_fail(HD_E_INVALID_ARG, "null query");
+    if (queries[q]->ctx != c) return hd_fail(HD_E_STATE, "query from another context");
+    if (queries[q]->limbs != (uint32_t)L) return hd_fail(HD_E_LEVEL, "query must be at L limbs");
+  }
+  for (size_t i = 0; i < n_out; i++)
+    if (out[i] && (out[i]->ctx != c || out[i]->limbs != (uint32_t)(L - 1)))
+      return hd_fail(HD_E_LEVEL, "reused output ciphertext has the wrong shape");
+  hd_status s = bind_keys(db, evk);
+  if (s) return s;
+  if (Q > 1 && Q > db->qb_cap) {  // setup-time allocation for this batch size (kept for later batches)
+    HD_CUDA(cudaDeviceSynchronize());
+    cudaFree(db->rB);
+    cudaFree(db->SB[0]);
+    cudaFree(db->SB[1]);
+    db->rB = db->SB[0] = db->SB[1] = nullptr;
+    db->qb_cap = 0;
+    const size_t ctL = (size_t)2 * L * n, sq = (size_t)db->A_loc * nj * 2 * L * n;
+    cudaError_t e = cudaMalloc(&db->rB, (size_t)Q * n1 * ctL * 8);
+    if (!e) e = cudaMalloc(&db->SB[0], (size_t)Q * sq * 8);
+    if (!e) e = cudaMalloc(&db->SB[1], (size_t)Q * sq * 8);
+    if (e) return hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, "query batch workspace");
+    db->qb_cap = Q;
+  }
+  std::vector<hd_ciphertext *> fresh;
+  std::vector<hd_ciphertext *> outs(out, out + n_out);
+  for (size_t i = 0; i < n_out; i++)
+    if (!out[i]) {
+      hd_ciphertext *ct;
+      if ((s = alloc_ct(c, L - 1, &ct))) {
+        for (auto *f : fresh) hd_ciphertext_destroy(f);
+        return s;
+      }
+      fresh.push_back(ct);
+      outs[i] = ct;
+    }
+  const char *serial = getenv("HD_SERIAL");
+  cudaStream_t sa = c->stream, sb = c->stream;
+  if (!(serial && serial[0] == '1')) {
+    if ((s = ensure_streams(c))) return s;
+    sa = c->sA;
+    sb = c->sB;
+  }
+  cudaStream_t caller = c->stream;
+  s = run_scan(db, queries, Q, sa, sb, outs.data(), n_out);
+  c->stream = caller;
+  if (s) {
+    for (auto *f : fresh) hd_ciphertext_destroy(f);
+    return s;
+  }
+  for (size_t i = 0; i < n_out; i++) out[i] = outs[i];
+  HD_CUDA(cudaGetLastError());
+  db->has_run = true;
   return HD_OK;
 }
 
