@@ -207,9 +207,11 @@ hd_status hd_query(hd_context *ctx, const hd_eval_keys *evk, const hd_database *
                    const hd_ciphertext *query, hd_ciphertext **out, size_t n_out);
 /* Query batching (NEXT-4): the scan of n_queries (1..64) independent query
  * ciphertexts over the same database in one call.  The baby steps, rescale, giant steps and
- * fold run per query as in hd_query; the diagonal MAC streams every diagonal word from HBM
- * once for up to 4 queries (mac_cs_batch_kernel), so the dominant D bytes per query drop up
- * to 4-fold.  out[q * n_local + i] receives the score ciphertext of aggregate agg_begin + i
+ * fold run per query as in hd_query, issued back to back on the pipeline streams.  The
+ * diagonal MAC runs per query by default (the fastest kernel measured on B200); with the
+ * environment variable HD_MAC_BATCH=2|4 one HBM pass over the diagonals serves groups of 2 or
+ * 4 queries (mac_cs_batch_kernel: D bytes per query drop 2-4-fold, but its baby-step words
+ * come from L2 and it measured slower).  out[q * n_local + i] receives the score ciphertext of aggregate agg_begin + i
  * for query q, bit-identical to hd_query(queries[q]); n_out = n_queries * n_local.  Plaintext
  * diagonals only (HD_E_INVALID_ARG for an encrypted database).  The batch workspace (baby
  * steps and giant-step sums of n_queries queries, double-buffered) is allocated on the first

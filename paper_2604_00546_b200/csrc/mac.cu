@@ -513,7 +513,13 @@ hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uin
   const bool full = (flat ? N % n1 : (N / 2) % n1) == 0 && n1 <= 256 && c->n % MAC_TPB == 0;
   bool small_q = true;
   for (int l = 0; l < c->L; l++) small_q = small_q && c->mod[l] < (1ull << 60);
-  if (!(full && small_q)) {  // partial giant-step ranges / wide moduli: the per-query kernels
+  // Measured at 2^20 x 512 (n1 = 128, one B200): the shared-D kernel costs 12.5 ms per query
+  // in groups of 2 and 19 ms in groups of 4, against 11.1 ms for the single-query kernel: its
+  // 2 QB baby-step words per diagonal word come from L2 and L2 bandwidth / latency, not HBM,
+  // bounds it.  So the default runs the tuned single-query kernel per query; HD_MAC_BATCH=2|4
+  // selects the shared-D grouping.
+  const char *g_env = getenv("HD_MAC_BATCH");
+  if (!(full && small_q) || !g_env) {  // per-query kernels
     for (uint32_t b = 0; b < Q; b++) {
       hd_status s = mac_run(c, D, r + b * rq, S + b * sq, A_loc, n1, N, js, flat);
       if (s) return s;
@@ -522,8 +528,8 @@ hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uin
   }
   // groups of up to G queries per D pass (HD_MAC_BATCH = max group 1, 2 or 4; default 4);
   // two giant steps per thread (JT = 2) for groups of 1 and 2 (HD_MAC_BATCH_JT=1 disables)
-  const char *g_env = getenv("HD_MAC_BATCH"), *jt_env = getenv("HD_MAC_BATCH_JT");
-  const uint32_t gmax = g_env ? (uint32_t)atoi(g_env) : 4u;
+  const char *jt_env = getenv("HD_MAC_BATCH_JT");
+  const uint32_t gmax = (uint32_t)atoi(g_env);
   for (uint32_t b0 = 0; b0 < Q;) {
     const uint32_t left = Q - b0;
     const uint32_t g = (left >= 4 && gmax >= 4) ? 4 : ((left >= 2 && gmax >= 2) ? 2 : 1);

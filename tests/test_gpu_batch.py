@@ -1,9 +1,11 @@
 """GPU parity of query batching (NEXT-4, hd_query_batch): every output of a batch of Q queries
 is bit-identical to hd_query of that query alone (which the other GPU tests pin to the oracle),
-and one batch member is checked against the CPU oracle directly.  Covers the batched streaming
-MAC (groups of 4 / 2 / 1 queries, the n1 > 128 banking variant), the per-query fallback for
-partial giant-step ranges, both packings, and in-place reuse of the outputs."""
+and one batch member is checked against the CPU oracle directly.  Covers the default per-query
+MAC, the shared-D batched MAC kernel (HD_MAC_BATCH = 2 / 4: groups of 4 / 2 / 1 queries, the
+n1 > 128 banking variant), the per-query path for partial giant-step ranges, both packings,
+and in-place reuse of the outputs."""
 import dataclasses
+import os
 
 import numpy as np
 import pytest
@@ -35,7 +37,10 @@ def _setup(cfg, n1, packing):
     ("C1", 12, "replicated", 2),    # n1 does not divide N/2: per-query MAC fallback
     ("C2", 256, "replicated", 4),   # n1 > 128: the banking variant of the batched kernel
 ])
-def test_batch_equals_single_queries(name, n1, packing, Q):
+@pytest.mark.parametrize("group", ["default", "2", "4"])
+def test_batch_equals_single_queries(name, n1, packing, Q, group, monkeypatch):
+    if group != "default":   # the shared-D batched MAC kernel (HD_MAC_BATCH)
+        monkeypatch.setenv("HD_MAC_BATCH", group)
     cfg = CONFIGS[name]
     ctx, sk, evk, db, db_vecs, q, rng = _setup(cfg, n1, packing)
     qs = [q] + [rng.integers(-99, 100, cfg.dim).astype(np.float32) for _ in range(Q - 1)]
@@ -90,3 +95,26 @@ def test_batch_errors():
     with pytest.raises(hd.HDError) as e:
         ctx.query_batch(evk, edb, [ct, ct])
     assert e.value.code == -1
+
+
+@pytest.mark.slow
+def test_c4_batch_matches_single_queries():
+    """The bench configuration (2^16 ring, 2^20 x 512, n1 = 128, 64 aggregates): a batch of
+    two queries through the batched MAC equals hd_query of each, on every aggregate."""
+    cfg = CONFIGS["C4"]
+    ctx, sk, evk, db, db_vecs, q, rng = _setup(cfg, cfg.n1, "replicated")
+    q2 = rng.integers(-99, 100, cfg.dim).astype(np.float32)
+    cts = [ctx.encrypt_query(sk, q, ENC_SEED_BASE), ctx.encrypt_query(sk, q2, ENC_SEED_BASE + 1)]
+    os.environ["HD_MAC_BATCH"] = "2"   # the shared-D kernel at the bench configuration
+    try:
+        outs = ctx.query_batch(evk, db, cts)
+        torch.cuda.synchronize()
+    finally:
+        os.environ.pop("HD_MAC_BATCH")
+    got = [[ctx.ciphertext_residues(o) for o in row] for row in outs]
+    for i, ct in enumerate(cts):
+        single = ctx.query(evk, db, ct)
+        torch.cuda.synchronize()
+        assert len(single) == 64
+        for a, o in enumerate(single):
+            assert (ctx.ciphertext_residues(o) == got[i][a]).all(), (i, a)

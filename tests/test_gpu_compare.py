@@ -130,3 +130,29 @@ def test_compare_errors(run):
     with pytest.raises(hd.HDError) as e:
         run.ctx.membership(evk2, run.outs[:1])
     assert e.value.code == -5
+
+
+@pytest.mark.slow
+def test_compare_at_bench_ring_size():
+    """ChebyshevCompare at the bench's ring (2^16) and limb count (6), as a batch of 32
+    ciphertexts (the bench's batch): bit-exact vs the oracle on an encrypted slot vector."""
+    cfg = dataclasses.replace(CONFIGS["C4"], limbs=6)
+    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
+    o = oracle.Oracle(cfg.log_n, cfg.limbs, seed=1)
+    sk, evk = ctx.keygen(np.array([1], np.int32))
+    ctx.relin_keygen(sk, evk)
+    v = np.random.default_rng(11).integers(-99, 100, cfg.dim).astype(np.float32)
+    cts = [ctx.encrypt_query(sk, v, ENC_SEED_BASE + 7)] * 32
+    c = hd.chebyshev_coefficients(0.05, 13)
+    out = ctx.compare(evk, cts, c)
+    torch.cuda.synchronize()
+    _, s_ntt = o.secret_key()
+    oct_ = o.encrypt(s_ntt, o.encode(o.query_slots(v), D45, cfg.limbs), ENC_SEED_BASE + 7)
+    assert (ctx.ciphertext_residues(cts[0]) == oct_).all()
+    want, scale = o.cheb_compare(oct_, D45, c, o.relin_key(s_ntt))
+    for k in (0, 31):
+        assert (ctx.ciphertext_residues(out[k]) == want).all(), k
+    assert ctx.ciphertext_scale(out[0]) == scale and out[0].limbs == 2
+    z = ctx.decrypt_slots(sk, out[0])
+    x = o.query_slots(v)
+    assert np.abs(z - npcheb.chebval(x, c)).max() < 1e-5
