@@ -343,6 +343,8 @@ def main():
     outs_b = None  # hd_query_batch outputs [Q][nloc]
     cmps = None
     mem = None
+    part = [None]   # membership under sharding: this rank's EvalAddMany
+    parts_in = []   # rank 0: the gathered partial sums
     out_ct_bytes = None
     gbuf = None
 
@@ -367,16 +369,26 @@ def main():
         if tail:  # NEXT-3: ChebyshevCompare of every score ciphertext (+ membership sum)
             cmps = ctx.compare(evk, outs, coeffs, cmps)
             if args.scenario == "membership":
-                mem = ctx.membership(evk, cmps, mem)
+                if world == 1:
+                    mem = ctx.membership(evk, cmps, mem)
+                else:  # local EvalAddMany; rank 0 adds the partial sums and runs RotateAndSum
+                    part[0] = ctx.eval_add_many(cmps, part[0])
         if world > 1:  # a9: result ciphertexts gathered to rank 0 over NCCL
-            res = results()
+            res = part if args.scenario == "membership" else results()
             if out_ct_bytes is None:
                 out_ct_bytes = ctx.ciphertext_export_size(res[0])
                 gbuf = torch.empty(len(res) * out_ct_bytes, dtype=torch.uint8, device=dev)
             for i, o in enumerate(res):
                 ctx.ciphertext_export(o, (gbuf.data_ptr() + i * out_ct_bytes, out_ct_bytes), on_device=True)
             per_rank = 1 if args.scenario == "membership" else Q * ((A + world - 1) // world)
-            hdd.gather_bytes(gbuf, per_rank * out_ct_bytes, 0)
+            got = hdd.gather_bytes(gbuf, per_rank * out_ct_bytes, 0)
+            if args.scenario == "membership" and rank == 0:
+                if not parts_in:  # setup on the first step: one ciphertext per rank
+                    parts_in.extend(ctx.ciphertext_import(g.data_ptr(), out_ct_bytes, on_device=True) for g in got)
+                else:
+                    for ct_, g in zip(parts_in, got):
+                        ctx.ciphertext_import_into(ct_, g.data_ptr(), out_ct_bytes, on_device=True)
+                mem = ctx.membership(evk, parts_in, mem)
 
     clk = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)
     clk.start()  # nvidia-smi sampler (100 ms); only samples inside the timed window are kept

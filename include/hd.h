@@ -306,6 +306,11 @@ hd_status hd_membership_steps(const hd_context *ctx, int32_t *steps, size_t cap,
  * (every slot a vector or zero padding, R29).  *out: NULL -> allocated. */
 hd_status hd_membership(hd_context *ctx, const hd_eval_keys *evk, const hd_ciphertext *const *in, size_t count,
                         hd_ciphertext **out);
+/* EvalAddMany (Alg. membership): *out = sum of the count ciphertexts (same level and
+ * scale).  With the database sharded over GPUs each rank sums its own comparison ciphertexts,
+ * rank 0 gathers the partial sums and runs hd_membership on them (the RotateAndSum is linear).
+ * *out: NULL -> allocated. */
+hd_status hd_eval_add_many(hd_context *ctx, const hd_ciphertext *const *in, size_t count, hd_ciphertext **out);
 /* Scale of a ciphertext's message (2^scale_bits for queries and scan outputs). */
 hd_status hd_ciphertext_scale(const hd_ciphertext *ct, double *scale);
 /* Decrypt + decode one ciphertext at its own scale: slots[0..numSlots) = real parts

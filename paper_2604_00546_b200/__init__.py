@@ -36,7 +36,7 @@ ABI_FUNCTIONS = [
     "hd_public_keygen", "hd_public_key_export", "hd_public_key_import", "hd_relin_keygen", "hd_public_key_destroy",
     "hd_enroll_ex", "hd_rotation_steps_ex", "hd_prerotation_steps", "hd_database_prerotate",
     "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
-    "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch",
+    "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch", "hd_eval_add_many",
 ]
 
 
@@ -142,6 +142,7 @@ def load():
             L.hd_ciphertext_scale.argtypes = [VP, C.POINTER(C.c_double)]
             L.hd_decrypt_slots.argtypes = [VP, VP, VP, VP, C.c_size_t]
             L.hd_query_batch.argtypes = [VP, VP, VP, VP, C.c_size_t, VP, C.c_size_t]
+            L.hd_eval_add_many.argtypes = [VP, VP, C.c_size_t, C.POINTER(VP)]
             _lib = L
         return _lib
 
@@ -357,6 +358,12 @@ class Context(_Handle):
         src = (VP * len(cts))(*[c.h for c in cts])
         o = VP(out.h if out is not None else None)
         _check("hd_membership", load().hd_membership(self.h, evk.h, src, len(cts), C.byref(o)))
+        return out if out is not None else Ciphertext(o.value, self)
+
+    def eval_add_many(self, cts, out=None):
+        src = (VP * len(cts))(*[c.h for c in cts])
+        o = VP(out.h if out is not None else None)
+        _check("hd_eval_add_many", load().hd_eval_add_many(self.h, src, len(cts), C.byref(o)))
         return out if out is not None else Ciphertext(o.value, self)
 
     def ciphertext_scale(self, ct):

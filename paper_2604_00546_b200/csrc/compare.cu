@@ -516,6 +516,27 @@ extern "C" hd_status hd_membership(hd_context *c, const hd_eval_keys *evk, const
   return scatter(c, acc, 0, 1, out);
 }
 
+extern "C" hd_status hd_eval_add_many(hd_context *c, const hd_ciphertext *const *in, size_t count,
+                                      hd_ciphertext **out) {
+  uint32_t ell = 0;
+  double scale = 0.0;
+  hd_status s = check_inputs(c, in, count, ell, scale);
+  if (s) return s;
+  if (!out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  Eval E{c, 1, nullptr, nullptr};
+  Batch acc;
+  if ((s = gather(E, in, 0, 1, ell, scale, acc))) return s;
+  if ((s = mark_read(c, in[0]))) return s;
+  for (size_t i = 1; i < count; i++) {
+    Batch x;
+    if ((s = gather(E, in, i, 1, ell, scale, x))) return s;
+    if ((s = mark_read(c, in[i]))) return s;
+    acc = E.add(acc, x, 1);
+    if (E.err) return E.err;
+  }
+  return scatter(c, acc, 0, 1, out);
+}
+
 extern "C" hd_status hd_ciphertext_scale(const hd_ciphertext *ct, double *scale) {
   if (!ct || !scale) return hd_fail(HD_E_INVALID_ARG, "null argument");
   *scale = ct->scale;

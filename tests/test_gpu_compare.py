@@ -156,3 +156,15 @@ def test_compare_at_bench_ring_size():
     z = ctx.decrypt_slots(sk, out[0])
     x = o.query_slots(v)
     assert np.abs(z - npcheb.chebval(x, c)).max() < 1e-5
+
+
+def test_sharded_membership_equals_single(run):
+    """Membership under sharding (bench.py, P > 1): each rank's EvalAddMany of its comparison
+    ciphertexts, then hd_membership of the partial sums on rank 0 = hd_membership of all."""
+    c = hd.chebyshev_coefficients(0.5, 13)
+    cmp = run.ctx.compare(run.evk, run.outs, c)
+    whole = run.ctx.membership(run.evk, cmp)
+    parts = [run.ctx.eval_add_many(cmp[:2]), run.ctx.eval_add_many(cmp[2:])]
+    sharded = run.ctx.membership(run.evk, parts)
+    torch.cuda.synchronize()
+    assert (run.ctx.ciphertext_residues(sharded) == run.ctx.ciphertext_residues(whole)).all()
