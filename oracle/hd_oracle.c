@@ -1631,13 +1631,20 @@ static or_cct cct_two_ab_minus(const or_params *p, const or_cct *a, const or_cct
 static or_val val_const(double k) { or_val v; memset(&v, 0, sizeof v); v.k = k; return v; }
 static or_val val_ct(or_cct c) { or_val v; memset(&v, 0, sizeof v); v.is_ct = 1; v.ct = c; return v; }
 
+/* MatchLevel ahead of use (R29): a copy of a at min(a.ell, ell) limbs. */
+static or_cct cct_at(const or_params *p, const or_cct *a, int ell) {
+  return cct_drop(p, a, a->ell < ell ? a->ell : ell);
+}
+
 /* Chunk polynomial (Alg. gpu-chebyshev Step 3): Q = c_0 + sum_{i>=1, c_i != 0}
- * c_i T[i], deg < d1. */
-static or_val ps_chunk(or_ps *S, const double *c, int m) {
+ * c_i T[i], deg < d1, produced at `need` limbs (each T[i] dropped to need + 1 first). */
+static or_val ps_chunk(or_ps *S, const double *c, int m, int need) {
   or_val acc = val_const(0.0);
   for (int i = 1; i <= m; i++) {
     if (c[i] == 0.0) continue;
-    or_cct t = cct_mul_const(S->p, &S->T[i], c[i]);
+    or_cct Ti = cct_at(S->p, &S->T[i], need + 1);
+    or_cct t = cct_mul_const(S->p, &Ti, c[i]);
+    cct_free(&Ti);
     if (!acc.is_ct) {
       acc = val_ct(t);
     } else {
@@ -1657,10 +1664,12 @@ static or_val ps_chunk(or_ps *S, const double *c, int m) {
 
 /* Evaluates sum_{i<=m} c_i T_i by Chebyshev-basis division (R29): with k = d1 2^j the
  * largest giant degree <= m, p = q T_k + r where q_0 = c_k, q_i = 2 c_{k+i} and
- * r_{k-i} = c_{k-i} - c_{k+i} (T_k T_i = (T_{k+i} + T_{k-i}) / 2; m < 2k). */
-static or_val ps_eval(or_ps *S, const double *c0, int m) {
+ * r_{k-i} = c_{k-i} - c_{k+i} (T_k T_i = (T_{k+i} + T_{k-i}) / 2; m < 2k).
+ * Levels top-down (R29): the result is wanted at `need` limbs, so the product q T_k is taken
+ * at need + 1 limbs (q evaluated for need + 1, T_k dropped to it) and r is evaluated for need. */
+static or_val ps_eval(or_ps *S, const double *c0, int m, int need) {
   while (m > 0 && c0[m] == 0.0) m--;
-  if (m < S->d1) return ps_chunk(S, c0, m);
+  if (m < S->d1) return ps_chunk(S, c0, m, need);
   int j = 0;
   while (j + 1 < S->nG && (S->d1 << (j + 1)) <= m) j++;
   int k = S->d1 << j;
@@ -1669,17 +1678,19 @@ static or_val ps_eval(or_ps *S, const double *c0, int m) {
   for (int i = 1; i <= m - k; i++) q[i] = 2.0 * c0[k + i];
   for (int i = 0; i < k; i++) r[i] = c0[i];
   for (int i = 1; i <= m - k; i++) r[k - i] = r[k - i] - c0[k + i];
-  or_val Q = ps_eval(S, q, m - k), R = ps_eval(S, r, k - 1);
+  or_val Q = ps_eval(S, q, m - k, need + 1), R = ps_eval(S, r, k - 1, need);
   free(q); free(r);
   or_val P;
+  or_cct Gj = cct_at(S->p, &S->G[j], need + 1);
   if (Q.is_ct) {
-    P = val_ct(cct_mul(S->p, &Q.ct, &S->G[j], S->rlk));
+    P = val_ct(cct_mul(S->p, &Q.ct, &Gj, S->rlk));
     cct_free(&Q.ct);
   } else if (Q.k != 0.0) {
-    P = val_ct(cct_mul_const(S->p, &S->G[j], Q.k));
+    P = val_ct(cct_mul_const(S->p, &Gj, Q.k));
   } else {
     P = val_const(0.0);
   }
+  cct_free(&Gj);
   if (!P.is_ct) return R;
   if (R.is_ct) {
     or_cct s = cct_add(S->p, &P.ct, &R.ct, 1);
@@ -1724,7 +1735,7 @@ int or_cheb_compare(const or_params *p, const uint64_t *in, int32_t ell, double 
   }
   /* Step 3: chunks and combination */
   int rc = OR_OK;
-  or_val V = ps_eval(&S, c, degree);
+  or_val V = ps_eval(&S, c, degree, 1); /* the result at one limb (q_0) */
   if (!V.is_ct) {
     rc = OR_E_ARG; /* constant polynomial: nothing encrypted to return */
   } else if (g_cheb_range_err) {

@@ -67,7 +67,7 @@ def test_compare_evaluates_the_series(oracle_mod, ring6, n, delta):
     ct = _encrypt_slots(o, s_ntt, z, ell, 9)
     c = oracle_mod.cheb_coeffs(delta, n)
     out, scale = o.cheb_compare(ct, D45, c, rlk)
-    assert out.shape[1] == ell - math.ceil(math.log2(n + 1))   # minimum depth of a degree-n polynomial
+    assert out.shape[1] == 1                  # evaluated top-down to the last limb (R29)
     got = o.decode(o.decrypt(s_ntt, out), scale)
     want = npcheb.chebval(z, c)
     assert np.abs(got - want).max() < 1e-5
@@ -76,11 +76,22 @@ def test_compare_evaluates_the_series(oracle_mod, ring6, n, delta):
     assert np.abs(got[far] - _f(delta)(z[far])).max() < 0.2
 
 
-def test_compare_runs_out_of_levels(oracle_mod, ring6):
+@pytest.mark.parametrize("n", [5, 13])
+def test_compare_uses_the_minimum_depth(oracle_mod, ring6, n):
+    """A degree-n polynomial needs ceil(log2(n + 1)) multiplicative levels (each product at
+    most doubles the degree): the evaluation succeeds with exactly that many levels above q_0
+    and reports OR_E_RANGE with one fewer."""
     o, s_ntt, rlk = ring6
-    ct = _encrypt_slots(o, s_ntt, np.zeros(o.ns), 3, 4)
+    depth = math.ceil(math.log2(n + 1))
+    c = oracle_mod.cheb_coeffs(0.3, n)
+    z = np.random.default_rng(n).uniform(-1, 1, o.ns)
+    ok = _encrypt_slots(o, s_ntt, z, depth + 1, 4)
+    out, scale = o.cheb_compare(ok, D45, c, rlk)
+    assert out.shape[1] == 1
+    assert np.abs(o.decode(o.decrypt(s_ntt, out), scale) - npcheb.chebval(z, c)).max() < 1e-5
+    short = _encrypt_slots(o, s_ntt, z, depth, 4)
     with pytest.raises(oracle_mod.OracleError) as e:
-        o.cheb_compare(ct, D45, oracle_mod.cheb_coeffs(0.5, 13), rlk)
+        o.cheb_compare(short, D45, c, rlk)
     assert e.value.code == oracle_mod.OR_E_RANGE
 
 
