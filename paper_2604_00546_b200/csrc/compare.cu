@@ -65,13 +65,19 @@ __global__ void __launch_bounds__(CTPB) tensor_kernel(const uint64_t *__restrict
   o[(size_t)2 * ell * n] = mulmod(a1, b1, mt, l);
 }
 
-// A batch of B ciphertexts [B][2][ell][n] with a common scale.
+// A batch of B ciphertexts [B][2][lay][n] with a common scale, of which the first ell limbs
+// are used (ell < lay: a MatchLevel view, no copy).
 struct Batch {
   std::shared_ptr<uint64_t> d;
-  int ell = 0;
+  int ell = 0, lay = 0;
   double scale = 0.0;
   uint64_t *ptr() const { return d.get(); }
 };
+Batch at_level(const Batch &a, int ell) {  // MatchLevel ahead of use (R29)
+  Batch v = a;
+  v.ell = std::min(a.ell, ell);
+  return v;
+}
 
 // A value of the evaluation: a ciphertext batch, or a plain constant (R29).
 struct Val {
@@ -95,7 +101,7 @@ struct Eval {
 
   Batch alloc(int ell, double scale) {
     Batch r;
-    r.ell = ell;
+    r.ell = r.lay = ell;
     r.scale = scale;
     uint64_t *p = nullptr;
     if (err) return r;
@@ -132,8 +138,8 @@ struct Eval {
     Batch r = alloc(ell, scale);
     if (err) return r;
     const uint32_t total = B * 2u * ell * c->n;
-    lincomb_kernel<<<(total + CTPB - 1) / CTPB, CTPB, 0, c->stream>>>(a.ptr(), a.ell, b ? b->ptr() : nullptr,
-                                                                      b ? b->ell : 0, r.ptr(), ell, c->logn, total, k,
+    lincomb_kernel<<<(total + CTPB - 1) / CTPB, CTPB, 0, c->stream>>>(a.ptr(), a.lay, b ? b->ptr() : nullptr,
+                                                                      b ? b->lay : 0, r.ptr(), ell, c->logn, total, k,
                                                                       c->mt);
     launch_check();
     return r;
@@ -195,7 +201,7 @@ struct Eval {
     uint64_t *tmp = scratch((size_t)2 * B * ell * n, kt);
     if (err) return Batch{};
     const uint32_t total = B * (uint32_t)ell * n;
-    tensor_kernel<<<(total + CTPB - 1) / CTPB, CTPB, 0, c->stream>>>(a.ptr(), a.ell, b.ptr(), b.ell, S3, ell,
+    tensor_kernel<<<(total + CTPB - 1) / CTPB, CTPB, 0, c->stream>>>(a.ptr(), a.lay, b.ptr(), b.lay, S3, ell,
                                                                      c->logn, total, c->mt);
     launch_check();
     hd_status s;
@@ -237,11 +243,12 @@ struct Ps {
   std::vector<Batch> T;  // T[1..d1]
   std::vector<Batch> G;  // G[j] = T_{d1 2^j}
 
-  Val chunk(const std::vector<double> &cf, int m) {
+  // chunk at `need` limbs: each T[i] dropped to need + 1 before its scalar product (R29)
+  Val chunk(const std::vector<double> &cf, int m, int need) {
     Val acc;
     for (int i = 1; i <= m; i++) {
       if (cf[i] == 0.0) continue;
-      Batch t = E.mul_const(T[i], cf[i]);
+      Batch t = E.mul_const(at_level(T[i], need + 1), cf[i]);
       if (E.err) return acc;
       if (!acc.is_ct) {
         acc.is_ct = true;
@@ -257,9 +264,10 @@ struct Ps {
     if (cf[0] != 0.0) acc.ct = E.add_const(acc.ct, cf[0]);
     return acc;
   }
-  Val eval(const std::vector<double> &cf0, int m) {
+  // result wanted at `need` limbs: q T_k taken at need + 1, r evaluated for need (R29)
+  Val eval(const std::vector<double> &cf0, int m, int need) {
     while (m > 0 && cf0[m] == 0.0) m--;
-    if (m < d1) return chunk(cf0, m);
+    if (m < d1) return chunk(cf0, m, need);
     int j = 0;
     while (j + 1 < (int)G.size() && (d1 << (j + 1)) <= m) j++;
     const int k = d1 << j;
@@ -268,17 +276,18 @@ struct Ps {
     for (int i = 1; i <= m - k; i++) q[i] = 2.0 * cf0[k + i];
     for (int i = 0; i < k; i++) r[i] = cf0[i];
     for (int i = 1; i <= m - k; i++) r[k - i] = r[k - i] - cf0[k + i];
-    Val Q = eval(q, m - k);
+    Val Q = eval(q, m - k, need + 1);
     if (E.err) return Val{};
-    Val R = eval(r, k - 1);
+    Val R = eval(r, k - 1, need);
     if (E.err) return Val{};
     Val P;
+    const Batch Gj = at_level(G[j], need + 1);
     if (Q.is_ct) {
       P.is_ct = true;
-      P.ct = E.mul(Q.ct, G[j]);
+      P.ct = E.mul(Q.ct, Gj);
     } else if (Q.k != 0.0) {
       P.is_ct = true;
-      P.ct = E.mul_const(G[j], Q.k);
+      P.ct = E.mul_const(Gj, Q.k);
     }
     if (E.err) return Val{};
     if (!P.is_ct) return R;
@@ -446,9 +455,15 @@ extern "C" hd_status hd_compare(hd_context *c, const hd_eval_keys *evk, const hd
     while (!E.err && (d1 << P.G.size()) <= (int)degree) P.G.push_back(E.two_ab_minus(P.G.back(), P.G.back(), nullptr, 1.0));
     // Step 3: chunks and the Chebyshev-basis combination (R29)
     Val V;
-    if (!E.err) V = P.eval(cf, (int)degree);
+    if (!E.err) V = P.eval(cf, (int)degree, 1);  // the result at one limb (q_0)
     if (E.err) return E.err;
     if (!V.is_ct) return hd_fail(HD_E_INVALID_ARG, "constant series: nothing to evaluate");
+    if (V.ct.lay != V.ct.ell) {  // a MatchLevel view: materialise before the copy-out
+      Lin id{};
+      for (int l = 0; l < c->L; l++) id.ka[l] = 1;
+      V.ct = E.lincomb(V.ct, nullptr, id, V.ct.scale);
+      if (E.err) return E.err;
+    }
     if ((s = scatter(c, V.ct, i0, B, out))) return s;
   }
   return HD_OK;
