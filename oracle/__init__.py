@@ -430,6 +430,14 @@ class Oracle:
             _p(np.ascontiguousarray(rlk)), _p(out), C.byref(eo), C.byref(so)))
         return np.ascontiguousarray(out.reshape(-1)[: 2 * eo.value * self.n].reshape(2, eo.value, self.n)), so.value
 
+    def relin_rescale(self, S3, rlk):
+        """Relinearize + Rescale with one rounding by P q_{ell-1} (R29)."""
+        ell = S3.shape[1]
+        out = u64((2, ell - 1, self.n))
+        _check("relin_rescale", lib().or_relin_rescale(C.byref(self.p), _p(np.ascontiguousarray(S3)), ell,
+                                                        _p(np.ascontiguousarray(rlk)), _p(out)))
+        return out
+
     def membership(self, cts, steps, keys):
         """EvalAddMany + RotateAndSum over numSlots (Alg. membership)."""
         cts = np.ascontiguousarray(cts, dtype=np.uint64)

@@ -1508,6 +1508,59 @@ static or_cct cct_drop(const or_params *p, const or_cct *a, int ell) {
   return r;
 }
 
+/* Relinearize + Rescale in one rounding (R29): X = P (d0, d1) + KIP(ModUp(d2), rlk) exactly over
+ * Q_ell u {P}; out = (X - [X mod P q_{ell-1}]) / (P q_{ell-1}) over q_0..q_{ell-2}, with the
+ * remainder from the CRT of X's P and q_{ell-1} residues in the coefficient domain, centred in
+ * (-P q/2, P q/2] (R12).  Identical to Rescale(Relinearize(.)) bit for bit: with r = [X]_P and
+ * s = [(X - r)/P]_q (the two centred lifts of the two-stage path), r + P s lies in
+ * [-(Pq-1)/2, (Pq-1)/2], so it IS [X]_{Pq} (mixed radix).  Not used by the oracle's own
+ * schedule; it pins the identity the CUDA path's fused relinearise-rescale relies on. */
+int or_relin_rescale(const or_params *p, const uint64_t *S3, int32_t ell, const uint64_t *rlk, uint64_t *out) {
+  int n = p->n, L = p->L;
+  if (ell < 2 || ell > L) return OR_E_ARG;
+  size_t ext = (size_t)(ell + 1) * n;
+  uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)ell * (ell + 1) * n);
+  uint64_t *u = calloc(2 * ext, sizeof(uint64_t));
+  or_modup(p, S3 + (size_t)2 * ell * n, ell, dig);
+  kip_accumulate(p, dig, ell, rlk, 1, u);
+  const uint64_t P = p->mod[L], qt = p->mod[ell - 1];
+  const u128 PQ = (u128)P * qt;
+  const uint64_t qinvP = invmod(qt % P, P);
+  uint64_t *X = malloc(sizeof(uint64_t) * (size_t)ell * n), *xq = malloc(sizeof(uint64_t) * n),
+           *xP = malloc(sizeof(uint64_t) * n), *V = malloc(sizeof(uint64_t) * (size_t)ell * n);
+  for (int pp = 0; pp < 2; pp++) {
+    const uint64_t *up = u + (size_t)pp * ext, *dp = S3 + (size_t)pp * ell * n;
+    for (int l = 0; l < ell; l++) {
+      uint64_t q = p->mod[l], Pq = P % q;
+      for (int j = 0; j < n; j++)
+        X[(size_t)l * n + j] = addmod(up[(size_t)l * n + j], mulmod(Pq, dp[(size_t)l * n + j], q), q);
+    }
+    memcpy(xq, X + (size_t)(ell - 1) * n, sizeof(uint64_t) * n);
+    or_ntt_inverse(p, ell - 1, xq);
+    memcpy(xP, up + (size_t)ell * n, sizeof(uint64_t) * n);
+    or_ntt_inverse(p, L, xP);
+    for (int j = 0; j < n; j++) {
+      uint64_t k = mulmod(submod(xP[j], xq[j] % P, P), qinvP, P);
+      u128 v = (u128)xq[j] + (u128)qt * k; /* [X mod P q] in [0, P q) */
+      int neg = v > PQ / 2;
+      u128 mag = neg ? PQ - v : v;
+      for (int l = 0; l < ell - 1; l++) {
+        uint64_t q = p->mod[l], r = (uint64_t)(mag % q);
+        V[(size_t)l * n + j] = neg ? (q - r) % q : r;
+      }
+    }
+    for (int l = 0; l < ell - 1; l++) {
+      uint64_t q = p->mod[l];
+      uint64_t w = invmod((uint64_t)(PQ % q), q);
+      or_ntt_forward(p, l, V + (size_t)l * n);
+      for (int j = 0; j < n; j++)
+        out[((size_t)pp * (ell - 1) + l) * n + j] = mulmod(submod(X[(size_t)l * n + j], V[(size_t)l * n + j], q), w, q);
+    }
+  }
+  free(dig); free(u); free(X); free(xq); free(xP); free(V);
+  return OR_OK;
+}
+
 /* Ciphertext product: MatchLevel, tensor (d0, d1, d2) = (a0 b0, a0 b1 + a1 b0, a1 b1),
  * Relinearize, Rescale (invariant (i) of P:L792-793: every product is
  * rescaled at once).  scale = s_a s_b / q_{ell-1}. */

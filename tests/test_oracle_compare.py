@@ -7,6 +7,9 @@
 (3) ChebyshevCompare decrypts to the plain series sum_i c_i T_i(x) (numpy chebval) on every
     slot, at the minimum multiplicative depth ceil(log2(n + 1)) (4 for n = 13), for the
     paper's degree (d1 = 2) and for n = 5 (d1 = 3: the odd baby power T3 = 2 T1 T2 - T1);
+(3b) the fused Relinearize + Rescale (one rounding by P q_{ell-1}, the CUDA path's form): with
+    d2 = 0 it is exactly the textbook Rescale of (d0, d1), and in general it equals Relinearize
+    then Rescale bit for bit (mixed-radix identity) and decodes to the product of the slots;
 (4) membership: every slot of RotateAndSum(sum of the inputs) decrypts to the sum of all
     decrypted input slots (a linear identity, independent of the evaluation);
 (5) end to end on the flat scan (C1 database): compare(scan) decodes to chebval(cosine).
@@ -93,6 +96,37 @@ def test_compare_uses_the_minimum_depth(oracle_mod, ring6, n):
     with pytest.raises(oracle_mod.OracleError) as e:
         o.cheb_compare(short, D45, c, rlk)
     assert e.value.code == oracle_mod.OR_E_RANGE
+
+
+def test_fused_relin_rescale(oracle_mod, ring6):
+    o, s_ntt, rlk = ring6
+    rng = np.random.default_rng(21)
+    ell = 4
+    za, zb = rng.uniform(-1, 1, o.ns), rng.uniform(-1, 1, o.ns)
+    a = _encrypt_slots(o, s_ntt, za, ell, 31)
+    b = _encrypt_slots(o, s_ntt, zb, ell, 32)
+    mods = [int(m) for m in o.p.moduli[:ell]]
+    S3 = np.zeros((3, ell, o.n), dtype=np.uint64)
+    for l, q in enumerate(mods):   # tensor in the NTT domain (pointwise), Python ints
+        a0, a1 = a[0, l].astype(object), a[1, l].astype(object)
+        b0, b1 = b[0, l].astype(object), b[1, l].astype(object)
+        S3[0, l] = (a0 * b0 % q).astype(np.uint64)
+        S3[1, l] = ((a0 * b1 + a1 * b0) % q).astype(np.uint64)
+        S3[2, l] = (a1 * b1 % q).astype(np.uint64)
+    # d2 = 0: exactly the textbook rescale of (d0, d1)
+    Z = S3.copy()
+    Z[2] = 0
+    assert (o.relin_rescale(Z, rlk) == o.rescale(np.ascontiguousarray(S3[:2]))).all()
+    # general: bit-identical to Relinearize then Rescale (mixed-radix identity of the two centred
+    # lifts, R29), at every level, on the product and on uniform random residues
+    assert (o.relin_rescale(S3, rlk) == o.rescale(o.relinearize(S3, rlk))).all()
+    fused = o.relin_rescale(S3, rlk)
+    scale = D45 * D45 / mods[ell - 1]
+    assert np.abs(o.decode(o.decrypt(s_ntt, fused), scale) - za * zb).max() < 1e-6
+    for e in (2, 3, 5):
+        R = np.stack([np.stack([rng.integers(0, m, o.n, dtype=np.uint64) for m in o.p.moduli[:e]])
+                      for _ in range(3)])
+        assert (o.relin_rescale(R, rlk) == o.rescale(o.relinearize(R, rlk))).all(), e
 
 
 def test_membership_sums_every_slot(oracle_mod, ring6):
