@@ -331,7 +331,8 @@ hd_status hd_test_ntt(hd_context *ctx, uint64_t *data, uint32_t n_rows,
 /* Stage buffers left by the last hd_query on `db` (host copy):
  *   which 0: baby step r[index]            (ct, L limbs)
  *         1: giant sum S_{agg,j}           (ct, L limbs),   index = j; encrypted
- *            database: 3 polynomials, (d0, d1) relinearised and d2 as accumulated
+ *            database: the 3 polynomials (d0, d1, d2) as accumulated (relinearised and
+ *            rescaled in one step into stage 2)
  *         2: rescaled S'_{agg,j}           (ct, L-1 limbs), index = j
  *         3: y_agg = sum_j Rot(S'_j)       (ct, L-1 limbs)
  *         4: diagonal D[agg][k]            (pt, L limbs; encrypted: ct, L limbs), index = k

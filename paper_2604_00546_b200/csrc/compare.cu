@@ -204,14 +204,18 @@ struct Eval {
     tensor_kernel<<<(total + CTPB - 1) / CTPB, CTPB, 0, c->stream>>>(a.ptr(), a.lay, b.ptr(), b.lay, S3, ell,
                                                                      c->logn, total, c->mt);
     launch_check();
-    hd_status s;
-    uint64_t *d2 = S3 + (size_t)2 * ell * n;
-    if ((s = ks_modup(c, d2, s3, B, ell, dig, tmp)) || (s = ks_kip(c, dig, d2, s3, B, 1, ell, rlk_ptr, rlk_gal, u)) ||
-        (s = ks_moddown(c, u, B, 1, ell, rlk_gal, nullptr, 0, S3, s3, true, tmp))) {
+    // Relinearize and Rescale in one rounding by P q_{ell-1}: bit-identical to the
+    // two-stage schedule (mixed-radix identity, R29), 2 ell NTT rows fewer per product
+    Batch r = alloc(ell - 1, a.scale * b.scale / (double)c->mod[ell - 1]);
+    std::shared_ptr<uint64_t> kV;
+    uint64_t *V = scratch((size_t)B * 2 * (ell - 1) * n, kV);
+    if (err) return Batch{};
+    hd_status s = ks_relin_rescale(c, S3, B, ell, rlk_ptr, rlk_gal, r.ptr(), dig, u, tmp, V);
+    if (s) {
       if (!err) err = s;
       return Batch{};
     }
-    return rescale(S3, s3, ell, a.scale * b.scale / (double)c->mod[ell - 1]);
+    return r;
   }
   // 2 a b - (c_ct or c_const)
   Batch two_ab_minus(const Batch &a, const Batch &b, const Batch *c_ct, double c_const) {

@@ -327,7 +327,7 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
     tmp_e = std::max(tmp_e, A * 2 * L * n);
   }
   const size_t dstride = (pk ? 2 : 1) * (size_t)L * n;  // one diagonal (pt, or ct)
-  size_t tmp2_e = 1;
+  size_t tmp2_e = pk ? A * 2 * (L - 1) * n : 1;  // CRT remainders of the fused relinearise-rescale
   size_t digb_e = (size_t)L * L * n, ub_e = nb * 2 * (L + 1) * n, tmpb_e = std::max(nb * 2 * L * n, (size_t)L * n);
   db->rescale_chunk = (uint32_t)rescale_chunk;
   struct Req {

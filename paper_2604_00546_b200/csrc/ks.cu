@@ -90,6 +90,37 @@ __global__ void add_pscaled_kernel(uint64_t *__restrict__ dst, size_t dst_stride
                        addmod(dv.y, shoup(sv.y, ka.pw[l], ka.pws[l], q), q));
 }
 
+// Fused relinearise-rescale (R29): from the coefficient forms of X's q_last and P rows
+// (x = u[b][p][ell-1], xP = u[b][p][ell]) the centred remainder v = [X mod P q_last] by CRT,
+// v = x + q_last ((xP - x) q_last^{-1} mod P) in [0, P q_last), centred; V[b][p][l] = v mod q_l.
+__global__ void crt2_kernel(const uint64_t *__restrict__ u, int ell, int logn, uint32_t total,
+                            uint64_t *__restrict__ V, ModTab mt, int Lp, uint64_t qt, uint64_t qinvP,
+                            uint64_t qinvPs, uint64_t pq_hi, uint64_t pq_lo) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const uint32_t n = 1u << logn, t = i & (n - 1), bp = i >> logn;  // bp = b * 2 + p
+  const uint64_t *row = u + ((size_t)bp * (ell + 1) + ell - 1) * n;
+  const uint64_t x = row[t], xP = row[n + t];
+  const uint64_t P = mt.q[Lp];
+  const uint64_t k = shoup(submod(xP, x, P), qinvP, qinvPs, P);  // x < q_last < P
+  uint64_t lo = qt * k, hi = __umul64hi(qt, k);
+  asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, 0;" : "+l"(lo), "+l"(hi) : "l"(x));
+  // centred: v > floor(P q / 2)  <=>  2 v > P q  (P q odd)
+  const uint64_t h2 = (hi << 1) | (lo >> 63), l2 = lo << 1;
+  const bool neg = h2 > pq_hi || (h2 == pq_hi && l2 > pq_lo);
+  if (neg) {  // magnitude P q - v
+    const uint64_t nl = pq_lo - lo, nh = pq_hi - hi - (pq_lo < lo ? 1 : 0);
+    lo = nl;
+    hi = nh;
+  }
+  uint64_t *out = V + (size_t)bp * (ell - 1) * n + t;
+  for (int l = 0; l < ell - 1; l++) {
+    const uint64_t q = mt.q[l];
+    const uint64_t r = reduce128(hi, lo, q, mt.bar[l], mt.r64[l], mt.r64s[l]);
+    out[(size_t)l * n] = neg ? (r ? q - r : 0) : r;
+  }
+}
+
 KipAcc kip_acc(const hd_context *c, int ell, const uint64_t *c0, size_t c0_stride) {
   KipAcc ka;
   ka.c0 = c0;
@@ -252,4 +283,53 @@ hd_status ks_rescale(hd_context *c, const uint64_t *S, size_t s_stride, uint32_t
     epi.ws[l] = host_shoup(epi.w[l], c->mod[l]);
   }
   return ntt_run(c, out, 2 * B * lo, ro, false, &lift, &epi);
+}
+
+hd_status ks_relin_rescale(hd_context *c, uint64_t *S3, uint32_t B, int ell, const uint64_t *const *rlk_dev,
+                           const uint32_t *gal_dev, uint64_t *out, uint64_t *dig, uint64_t *u, uint64_t *tmp,
+                           uint64_t *V) {
+  const int n = c->n, L = c->L, lo = ell - 1;
+  const size_t s3 = (size_t)3 * ell * n;
+  uint64_t *d2 = S3 + (size_t)2 * ell * n;
+  hd_status s;
+  // 1. X = P (d0, d1) + KIP(ModUp(d2)) over Q_ell u {P}: u [B][2][ell+1][n]
+  if ((s = ks_modup(c, d2, s3, B, ell, dig, tmp))) return s;
+  if ((s = ks_kip(c, dig, d2, s3, B, 1, ell, rlk_dev, gal_dev, u))) return s;
+  if ((s = ks_add_pscaled(c, u, S3, s3, B, ell))) return s;
+  // 2. coefficient form of the q_{ell-1} and P rows of X, in place
+  RowMap rt = rowmap_simple(1, {lo, L}, 2, (uint64_t)(ell + 1) * n);
+  if ((s = ntt_run(c, u + (size_t)lo * n, 4 * B, rt, true, nullptr, nullptr))) return s;
+  // 3. centred CRT remainder v = [X mod P q_{ell-1}] into q_0..q_{ell-2}
+  const uint64_t P = c->mod[L], qt = c->mod[lo];
+  const uint64_t qinvP = host_powmod(qt % P, P - 2, P);
+  const unsigned __int128 pq = (unsigned __int128)P * qt;
+  const uint32_t total = 2u * B * n;
+  crt2_kernel<<<(total + TPB - 1) / TPB, TPB, 0, c->stream>>>(u, ell, c->logn, total, V, c->mt, L, qt, qinvP,
+                                                              host_shoup(qinvP, P), (uint64_t)(pq >> 64),
+                                                              (uint64_t)pq);
+  ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  // 4. out[b][p][l] = (X[b][p][l] - NTT_l(v)) (P q_{ell-1})^{-1}
+  RowMap ro;
+  ro.gsize = 2 * lo;
+  ro.gstride = (uint64_t)2 * lo * n;
+  ro = mods_seq(ro, 1, lo);
+  NttSrc src;
+  src.base = V;
+  NttEpi epi;
+  epi.mode = 1;
+  epi.ell = lo;
+  epi.A = u;
+  epi.amap.gsize = 2 * lo;
+  epi.amap.gstride = (uint64_t)2 * (ell + 1) * n;
+  epi.amap.g2 = lo;
+  epi.amap.s2 = (uint64_t)(ell + 1) * n;
+  epi.out = out;
+  epi.omap = ro;
+  for (int l = 0; l < lo; l++) {
+    const uint64_t q = c->mod[l];
+    epi.w[l] = host_powmod((uint64_t)(pq % q), q - 2, q);
+    epi.ws[l] = host_shoup(epi.w[l], q);
+  }
+  return ntt_run(c, out, 2 * B * lo, ro, false, &src, &epi);
 }

@@ -25,6 +25,13 @@ hd_status ks_moddown(hd_context *c, uint64_t *u, uint32_t X, uint32_t K, int ell
 hd_status ks_rescale(hd_context *c, const uint64_t *S, size_t s_stride, uint32_t B, int ell, uint64_t *out,
                      size_t out_stride, uint64_t *tmp1, uint64_t *tmp2);
 
+// Relinearise + rescale with one rounding by P q_{ell-1} (bit-identical to ks_moddown-accumulate
+// then ks_rescale: mixed-radix identity, R29): S3 [B][3][ell][n] -> out [B][2][ell-1][n].
+// Scratch: dig B ell ell n, u B 2 (ell+1) n, tmp B ell n, V B 2 (ell-1) n.
+hd_status ks_relin_rescale(hd_context *c, uint64_t *S3, uint32_t B, int ell, const uint64_t *const *rlk_dev,
+                           const uint32_t *gal_dev, uint64_t *out, uint64_t *dig, uint64_t *u, uint64_t *tmp,
+                           uint64_t *V);
+
 // MAC (mac.cu)
 struct MacPlan {
   int n1, N, L, logn;

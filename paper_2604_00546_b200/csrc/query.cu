@@ -147,19 +147,18 @@ static hd_status scan_tail(hd_database *db, uint64_t *Sbuf, cudaEvent_t *E, bool
   cudaStream_t sb = c->stream;
   hd_status s;
   if (db->encrypted) {
-    // ---- Relinearize every degree-2 S_{a,j}: (d0, d1) += KeySwitch_{s^2->s}(d2) ----
+    // ---- Relinearize and Rescale every degree-2 S_{a,j} in one rounding by
+    //      P q_{L-1}: bit-identical to KeySwitch_{s^2->s}(d2) added to (d0, d1) then Rescale
+    //      (mixed-radix identity, R29), 2 L NTT rows fewer per sum ----
     const uint32_t total = A * nj;
     const size_t rslot = (size_t)(n1 - 1) + nj + 1;
     for (uint32_t b0 = 0; b0 < total; b0 += db->relin_chunk) {
       const uint32_t B = std::min(db->relin_chunk, total - b0);
-      uint64_t *S3 = Sbuf + (size_t)b0 * sL;
-      if ((s = ks_modup(c, S3 + (size_t)2 * L * n, sL, B, L, db->dig, db->tmp))) return s;
-      if ((s = ks_kip(c, db->dig, S3 + (size_t)2 * L * n, sL, B, 1, L, db->kptr + rslot, db->gal + rslot, db->u)))
+      if ((s = ks_relin_rescale(c, Sbuf + (size_t)b0 * sL, B, L, db->kptr + rslot, db->gal + rslot,
+                                db->Sp + (size_t)b0 * ct1, db->dig, db->u, db->tmp, db->tmp2)))
         return s;
-      if ((s = ks_moddown(c, db->u, B, 1, L, db->gal + rslot, nullptr, 0, S3, sL, true, db->tmp))) return s;
     }
-  }
-  {
+  } else {
     // ---- rescale every S_{a,j} ----
     const uint32_t total = A * nj;
     for (uint32_t b0 = 0; b0 < total; b0 += db->rescale_chunk) {
@@ -397,7 +396,7 @@ extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t ag
       break;
     case 1:
       if (jj < 0 || jj >= nj) return hd_fail(HD_E_INVALID_ARG, "giant index");
-      len = (size_t)db->spoly * L * n;  // encrypted: (d0, d1) relinearised, d2 as accumulated
+      len = (size_t)db->spoly * L * n;  // encrypted: the degree-2 sum as accumulated
       src = (((db->qcount - 1) & 1) ? db->S2 : db->S) + (a * nj + jj) * len;
       break;
     case 2:
