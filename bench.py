@@ -462,7 +462,10 @@ def main():
     L, n, N = cfg.limbs, 1 << cfg.log_n, cfg.dim
     nj = len(db_js(cfg, flat))
     dpoly, spoly = (2, 3) if enc_db else (1, 2)  # diagonal / giant-sum polynomials
-    d_passes = Q // 4 + (Q % 4) // 2 + (Q % 2)  # hd_query_batch: D streamed once per group of 4 / 2 / 1
+    # D passes per step: hd_query_batch runs the single-query MAC per query unless HD_MAC_BATCH=G
+    # selects the shared-D kernel (one pass per group of up to G queries)
+    g_env = int(os.environ.get("HD_MAC_BATCH", "1") or 1)
+    d_passes = Q if g_env <= 1 else (Q // 4 + (Q % 4) // 2 + Q % 2 if g_env >= 4 else Q // 2 + Q % 2)
     mac_bytes = (d_passes * nloc * N * dpoly * L * n * 8
                  + Q * (cfg.n1 * 2 * L * n * 8 + nloc * nj * spoly * L * n * 8))
     mac_avg_ms = statistics.mean(mac_ms)
