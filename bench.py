@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--kappa", type=int, default=8, help="comparison depth budget (P:L721: 8 -> degree 13)")
     ap.add_argument("--delta", type=float, default=0.5, help="comparison threshold")
     ap.add_argument("--limbs", type=int, default=0, help="RNS limbs (default 3; 6 for the comparison scenarios)")
+    ap.add_argument("--n1", type=int, default=0, help="baby-step count (default: the config's; the paper uses 23)")
     ap.add_argument("--db", default="plain", choices=["plain", "encrypted"],
                     help="plaintext diagonals (the north-star scan) or the encrypted-database mode (NEXT-1)")
     return ap.parse_args()
@@ -143,11 +144,13 @@ def oracle_sample(cfg, rng_seed=0, scenario="scan"):
 
 def workload_cfg(args):
     """BASELINE config, with 6 RNS limbs when the comparison follows the scan (R29)."""
+    import dataclasses
     cfg = CONFIGS[args.config]
     limbs = args.limbs or (6 if args.scenario != "scan" else cfg.limbs)
     if limbs != cfg.limbs:
-        import dataclasses
         cfg = dataclasses.replace(cfg, limbs=limbs)
+    if args.n1 and args.n1 != cfg.n1:
+        cfg = dataclasses.replace(cfg, n1=args.n1)
     return cfg
 
 
