@@ -571,10 +571,40 @@ def main():
                                           f"1 rescale + 1 giant rotation{SAMPLE_TAIL[args.scenario]} at the workload's shapes on uniform random "
                                           f"residues), {total:.1f} s of CPU in total, extrapolated to one whole query "
                                           "(ModUp + (n1-1) baby + A (nj (MAC + rescale) + (nnz+1) rotations))"}
+        # the same oracle sample on every host core at once (one process per core, the
+        # query's rotations and aggregates are independent): the all-core CPU rate
+        allc = all_core_oracle_rate(cfg, args.scenario)
+        if allc:
+            line["cpu_baseline"]["all_cores"] = allc
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _oracle_sample_worker(argv):
+    cfg, seed, scenario = argv
+    return oracle_sample(cfg, seed, scenario)
+
+
+def all_core_oracle_rate(cfg, scenario):
+    """One oracle sample per host core, concurrently; throughput = sum over processes of
+    1 / (per-query time extrapolated from that process's sample under full-host contention)."""
+    import multiprocessing as mp
+    try:
+        procs = max(1, len(os.sched_getaffinity(0)))
+    except Exception:  # noqa: BLE001
+        procs = mp.cpu_count()
+    try:
+        t0 = time.perf_counter()
+        with mp.get_context("fork").Pool(procs) as pool:
+            res = pool.map(_oracle_sample_worker, [(cfg, 1000 + i, scenario) for i in range(procs)])
+        wall = time.perf_counter() - t0
+    except Exception:  # noqa: BLE001
+        return None
+    return {"value": sum(1.0 / pq for pq, _ in res), "unit": UNIT, "cores": procs, "kind": "oracle",
+            "sample": f"{procs} concurrent processes x 1 oracle sample ({wall:.1f} s wall), each extrapolated "
+                      "to a whole query; the query's rotations and aggregates split across cores"}
 
 
 def db_js(cfg, flat=False):
