@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(MAC_TPB) mac_cs_kernel(const uint64_t *__restr
 __global__ void __launch_bounds__(MAC_TPB) mac_ct_kernel(const uint64_t *__restrict__ D,
                                                           const uint64_t *__restrict__ r, uint64_t *__restrict__ S,
                                                           int n1, int N, int L, int logn, int jmin, int nj,
-                                                          ModTab mt, int flat) {
+                                                          ModTab mt, int flat, int njs) {
   const int n = 1 << logn;
   const uint32_t a = blockIdx.x;
   const uint32_t t = blockIdx.y * MAC_TPB + threadIdx.x;
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(MAC_TPB) mac_ct_kernel(const uint64_t *__restr
     if ((c & 63) == 63) bank();
   }
   bank();
-  uint64_t *Sa = S + ((size_t)a * nj + jj) * 3 * ls + (size_t)m * n + t;
+  uint64_t *Sa = S + ((size_t)a * njs + jj) * 3 * ls + (size_t)m * n + t;  // njs: giant steps in S's layout
 #pragma unroll
   for (int e = 0; e < 3; e++) Sa[(size_t)e * ls] = part[e];
 }
@@ -250,7 +250,7 @@ template <int JT>
 __global__ void __launch_bounds__(MAC_TPB) mac_ct_stream_kernel(const uint64_t *__restrict__ D,
                                                                  const uint64_t *__restrict__ r,
                                                                  uint64_t *__restrict__ S, int n1, int N, int L,
-                                                                 int logn, int jmin, int nj, ModTab mt) {
+                                                                 int logn, int jmin, int nj, ModTab mt, int njs) {
   const int n = 1 << logn;
   const uint32_t a = blockIdx.x;
   const uint32_t t = blockIdx.y * MAC_TPB + threadIdx.x;
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(MAC_TPB) mac_ct_stream_kernel(const uint64_t *
   }
 #pragma unroll
   for (int jj = 0; jj < JT; jj++) {
-    uint64_t *Sa = S + ((size_t)a * nj + jg * JT + jj) * 3 * ls + (size_t)m * n + t;
+    uint64_t *Sa = S + ((size_t)a * njs + jg * JT + jj) * 3 * ls + (size_t)m * n + t;
 #pragma unroll
     for (int e = 0; e < 3; e++) {
       cs_fold(acc[jj][e]);
@@ -462,14 +462,29 @@ hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint
   if (js.empty() || A_loc == 0) return HD_OK;
   if (c->n % MAC_TPB) return hd_fail(HD_E_PARAMS, "ring too small for the encrypted MAC");
   const int jmin = js.front(), nj = (int)js.size();
-  const dim3 grid(A_loc, c->n / MAC_TPB, c->L * nj);
   const char *force = getenv("HD_MAC_VARIANT");  // 'g': the generic kernel (tests)
+  const bool generic = force && force[0] == 'g';
   // one giant step per thread (64 registers): two per thread (110 registers) measured
   // 34.5 ms vs 28.0 ms at 2^20 x 512
-  if ((flat ? N % n1 : (N / 2) % n1) == 0 && !(force && force[0] == 'g'))
-    mac_ct_stream_kernel<1><<<grid, MAC_TPB, 0, c->stream>>>(Dct, r, S3, n1, N, c->L, c->logn, jmin, nj, c->mt);
-  else
-    mac_ct_kernel<<<grid, MAC_TPB, 0, c->stream>>>(Dct, r, S3, n1, N, c->L, c->logn, jmin, nj, c->mt, flat ? 1 : 0);
+  if ((flat ? N % n1 : (N / 2) % n1) == 0 && !generic) {
+    const dim3 grid(A_loc, c->n / MAC_TPB, c->L * nj);
+    mac_ct_stream_kernel<1><<<grid, MAC_TPB, 0, c->stream>>>(Dct, r, S3, n1, N, c->L, c->logn, jmin, nj, c->mt, nj);
+  } else if (flat && nj > 1 && !generic) {
+    // flat packing with n1 not dividing N (e.g. the paper's n1 = 23): giant steps 0 .. nj-2
+    // use all n1 baby steps (streaming kernel), only the last one is partial (general kernel)
+    const dim3 g_full(A_loc, c->n / MAC_TPB, c->L * (nj - 1)), g_tail(A_loc, c->n / MAC_TPB, c->L);
+    mac_ct_stream_kernel<1><<<g_full, MAC_TPB, 0, c->stream>>>(Dct, r, S3, n1, N, c->L, c->logn, jmin, nj - 1,
+                                                                c->mt, nj);
+    ++c->launches;
+    HD_CUDA(cudaGetLastError());
+    const size_t ls = (size_t)c->L * c->n;
+    mac_ct_kernel<<<g_tail, MAC_TPB, 0, c->stream>>>(Dct, r, S3 + (size_t)(nj - 1) * 3 * ls, n1, N, c->L, c->logn,
+                                                     jmin + nj - 1, 1, c->mt, 1, nj);
+  } else {
+    const dim3 grid(A_loc, c->n / MAC_TPB, c->L * nj);
+    mac_ct_kernel<<<grid, MAC_TPB, 0, c->stream>>>(Dct, r, S3, n1, N, c->L, c->logn, jmin, nj, c->mt, flat ? 1 : 0,
+                                                   nj);
+  }
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;
