@@ -350,6 +350,11 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
   size_t total = 0;
   for (auto &q : reqs) total += q.bytes;
   size_t fr = 0, tot = 0;
+  {  // return the comparison's stream-ordered workspaces (kept mapped between calls, context.cu)
+    HD_CUDA(cudaDeviceSynchronize());
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
+  }
   HD_CUDA(cudaMemGetInfo(&fr, &tot));
   if (total + (256ull << 20) > fr) {
     delete db;

@@ -308,6 +308,8 @@ extern "C" hd_status hd_query_batch(hd_context *c, const hd_eval_keys *evk, cons
   if (s) return s;
   if (Q > 1 && Q > db->qb_cap) {  // setup-time allocation for this batch size (kept for later batches)
     HD_CUDA(cudaDeviceSynchronize());
+    cudaMemPool_t pool;  // return the comparison's stream-ordered workspaces first
+    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
     cudaFree(db->rB);
     cudaFree(db->SB[0]);
     cudaFree(db->SB[1]);
