@@ -168,3 +168,19 @@ def test_sharded_membership_equals_single(run):
     sharded = run.ctx.membership(run.evk, parts)
     torch.cuda.synchronize()
     assert (run.ctx.ciphertext_residues(sharded) == run.ctx.ciphertext_residues(whole)).all()
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_compare_low_degrees_bit_exact(run, n):
+    """Degenerate Paterson-Stockmeyer shapes (n = 1: d1 = 1, a single scalar product; n = 2, 3)
+    on the scan outputs: bit-exact vs the oracle; a constant series is rejected."""
+    c = np.array([0.25, -0.5, 0.75, 0.125][: n + 1])
+    cmp = run.ctx.compare(run.evk, run.outs, c)
+    torch.cuda.synchronize()
+    for got, ref in zip(cmp, run.ref_outs):
+        want, scale = run.o.cheb_compare(ref, D45, c, run.rlk)
+        assert (run.ctx.ciphertext_residues(got) == want).all()
+        assert run.ctx.ciphertext_scale(got) == scale
+    with pytest.raises(hd.HDError) as e:
+        run.ctx.compare(run.evk, run.outs, np.array([1.0, 0.0, 0.0]))
+    assert e.value.code == -1

@@ -166,3 +166,26 @@ def test_identification_end_to_end(oracle_mod):
     got = z[: cfg.num_vectors]          # flat packing, one aggregate: slot v = vector v (R27)
     assert np.abs(got - npcheb.chebval(cos, c)).max() < 1e-5
     assert (got[pos] > 0.8).all() and np.delete(got, pos).max() < 0.3
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_compare_low_degrees(oracle_mod, ring6, n):
+    """Degenerate Paterson-Stockmeyer shapes: n = 1 (d1 = 1: a single scalar product),
+    n = 2 (d1 = 2, one giant power), n = 3; each decodes to the series."""
+    o, s_ntt, rlk = ring6
+    z = np.random.default_rng(40 + n).uniform(-1, 1, o.ns)
+    c = np.array([0.25, -0.5, 0.75, 0.125][: n + 1])
+    out, scale = o.cheb_compare(_encrypt_slots(o, s_ntt, z, 4, 5), D45, c, rlk)
+    assert out.shape[1] == 1
+    assert np.abs(o.decode(o.decrypt(s_ntt, out), scale) - npcheb.chebval(z, c)).max() < 1e-5
+
+
+def test_compare_constant_series_is_rejected(oracle_mod, ring6):
+    """delta <= -1: f = 1 on the whole interval, the interpolant is the constant 1 and there is
+    nothing encrypted to evaluate (the CUDA path returns HD_E_INVALID_ARG alike)."""
+    o, s_ntt, rlk = ring6
+    c = oracle_mod.cheb_coeffs(-1.5, 13)
+    assert abs(c[0] - 1.0) < 1e-15 and np.abs(c[1:]).max() < 1e-15
+    with pytest.raises(oracle_mod.OracleError) as e:
+        o.cheb_compare(_encrypt_slots(o, s_ntt, np.zeros(o.ns), 5, 6), D45, np.array([1.0] + [0.0] * 13), rlk)
+    assert e.value.code == oracle_mod.OR_E_ARG
