@@ -27,31 +27,33 @@ struct Lin {
   uint64_t ka[HD_MAXMOD], kb[HD_MAXMOD], kc[HD_MAXMOD];
 };
 
+// Grid (n / CTPB, ell, 2 B): no runtime divisions; a unit multiplier skips its product.
 __global__ void __launch_bounds__(CTPB) lincomb_kernel(const uint64_t *__restrict__ a, int la,
                                                        const uint64_t *__restrict__ b, int lb,
-                                                       uint64_t *__restrict__ out, int ell, int logn, uint32_t total,
-                                                       Lin k, ModTab mt) {
-  const uint32_t i = blockIdx.x * CTPB + threadIdx.x;
-  if (i >= total) return;
-  const uint32_t n = 1u << logn, t = i & (n - 1), row = i >> logn;  // row = (bb * 2 + p) * ell + l
-  const uint32_t l = row % (uint32_t)ell, bp = row / (uint32_t)ell, p = bp & 1, bb = bp >> 1;
-  const uint64_t q = mt.q[l];
-  uint64_t v = mulmod(a[(((size_t)bb * 2 + p) * la + l) * n + t], k.ka[l], mt, l);
-  if (b) v = addmod(v, mulmod(b[(((size_t)bb * 2 + p) * lb + l) * n + t], k.kb[l], mt, l), q);
+                                                       uint64_t *__restrict__ out, int ell, int logn, Lin k,
+                                                       ModTab mt) {
+  const uint32_t n = 1u << logn, t = blockIdx.x * CTPB + threadIdx.x, l = blockIdx.y, bp = blockIdx.z;
+  if (t >= n) return;
+  const uint32_t p = bp & 1;
+  const uint64_t q = mt.q[l], ka = k.ka[l], kb = k.kb[l];
+  const uint64_t av = a[((size_t)bp * la + l) * n + t];
+  uint64_t v = ka == 1 ? av : mulmod(av, ka, mt, l);
+  if (b) {
+    const uint64_t bv = b[((size_t)bp * lb + l) * n + t];
+    v = addmod(v, kb == 1 ? bv : (kb == q - 1 ? (bv ? q - bv : 0) : mulmod(bv, kb, mt, l)), q);
+  }
   if (p == 0) v = addmod(v, k.kc[l], q);
-  out[i] = v;
+  out[((size_t)bp * ell + l) * n + t] = v;
 }
 
 // Tensor product of B ciphertext pairs at ell limbs: out [B][3][ell][n] =
 // (a0 b0, a0 b1 + a1 b0, a1 b1), operands read with layout limbs la / lb (MatchLevel).
+// Grid (n / CTPB, ell, B).
 __global__ void __launch_bounds__(CTPB) tensor_kernel(const uint64_t *__restrict__ a, int la,
                                                       const uint64_t *__restrict__ b, int lb,
-                                                      uint64_t *__restrict__ out, int ell, int logn, uint32_t total,
-                                                      ModTab mt) {
-  const uint32_t i = blockIdx.x * CTPB + threadIdx.x;
-  if (i >= total) return;
-  const uint32_t n = 1u << logn, t = i & (n - 1), row = i >> logn;  // row = bb * ell + l
-  const uint32_t l = row % (uint32_t)ell, bb = row / (uint32_t)ell;
+                                                      uint64_t *__restrict__ out, int ell, int logn, ModTab mt) {
+  const uint32_t n = 1u << logn, t = blockIdx.x * CTPB + threadIdx.x, l = blockIdx.y, bb = blockIdx.z;
+  if (t >= n) return;
   const uint64_t q = mt.q[l], bar = mt.bar[l];
   const uint64_t a0 = a[((size_t)bb * 2 * la + l) * n + t], a1 = a[((size_t)bb * 2 * la + la + l) * n + t];
   const uint64_t b0 = b[((size_t)bb * 2 * lb + l) * n + t], b1 = b[((size_t)bb * 2 * lb + lb + l) * n + t];
@@ -137,10 +139,9 @@ struct Eval {
     const int ell = b ? std::min(a.ell, b->ell) : a.ell;
     Batch r = alloc(ell, scale);
     if (err) return r;
-    const uint32_t total = B * 2u * ell * c->n;
-    lincomb_kernel<<<(total + CTPB - 1) / CTPB, CTPB, 0, c->stream>>>(a.ptr(), a.lay, b ? b->ptr() : nullptr,
-                                                                      b ? b->lay : 0, r.ptr(), ell, c->logn, total, k,
-                                                                      c->mt);
+    const dim3 grid((c->n + CTPB - 1) / CTPB, ell, 2 * B);
+    lincomb_kernel<<<grid, CTPB, 0, c->stream>>>(a.ptr(), a.lay, b ? b->ptr() : nullptr, b ? b->lay : 0, r.ptr(), ell,
+                                                 c->logn, k, c->mt);
     launch_check();
     return r;
   }
@@ -200,9 +201,8 @@ struct Eval {
     uint64_t *u = scratch((size_t)B * 2 * (ell + 1) * n, ku);
     uint64_t *tmp = scratch((size_t)2 * B * ell * n, kt);
     if (err) return Batch{};
-    const uint32_t total = B * (uint32_t)ell * n;
-    tensor_kernel<<<(total + CTPB - 1) / CTPB, CTPB, 0, c->stream>>>(a.ptr(), a.lay, b.ptr(), b.lay, S3, ell,
-                                                                     c->logn, total, c->mt);
+    const dim3 grid((n + CTPB - 1) / CTPB, ell, B);
+    tensor_kernel<<<grid, CTPB, 0, c->stream>>>(a.ptr(), a.lay, b.ptr(), b.lay, S3, ell, c->logn, c->mt);
     launch_check();
     // Relinearize and Rescale in one rounding by P q_{ell-1}: bit-identical to the
     // two-stage schedule (mixed-radix identity, R29), 2 ell NTT rows fewer per product
