@@ -218,6 +218,17 @@ hd_status hd_query(hd_context *ctx, const hd_eval_keys *evk, const hd_database *
  * call with a larger n_queries and kept; outputs as in hd_query. */
 hd_status hd_query_batch(hd_context *ctx, const hd_eval_keys *evk, const hd_database *db,
                          const hd_ciphertext *const *queries, size_t n_queries, hd_ciphertext **out, size_t n_out);
+/* Split baby steps (with the database sharded over P GPUs every rank would
+ * otherwise recompute all n1 - 1 baby rotations).  hd_baby_steps writes r[i] = Rot_i(query)
+ * for i in [i_begin, i_end) (r[0] = the query itself) into r_dev, a device buffer laid out
+ * [n1][2][L][n] u64 (the caller's, e.g. one slice per rank followed by an NCCL all-gather);
+ * hd_query_baby then runs the scan (MAC, rescale, giant steps, fold) from a complete r_dev,
+ * bit-identical to hd_query of that query.  Both run in order on the context stream; the
+ * baby-step keys of [i_begin, i_end) and the scan keys must be in evk. */
+hd_status hd_baby_steps(hd_context *ctx, const hd_eval_keys *evk, const hd_database *db,
+                        const hd_ciphertext *query, uint32_t i_begin, uint32_t i_end, void *r_dev);
+hd_status hd_query_baby(hd_context *ctx, const hd_eval_keys *evk, const hd_database *db, const void *r_dev,
+                        hd_ciphertext **out, size_t n_out);
 /* Cumulative number of CUDA kernels this context has launched (all entry points). */
 hd_status hd_launch_count(const hd_context *ctx, uint64_t *count);
 /* Per-phase device times (ms), averaged over the hd_query calls issued since the

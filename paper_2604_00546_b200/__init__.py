@@ -36,7 +36,8 @@ ABI_FUNCTIONS = [
     "hd_public_keygen", "hd_public_key_export", "hd_public_key_import", "hd_relin_keygen", "hd_public_key_destroy",
     "hd_enroll_ex", "hd_rotation_steps_ex", "hd_prerotation_steps", "hd_database_prerotate",
     "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
-    "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch", "hd_eval_add_many",
+    "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch", "hd_eval_add_many", "hd_baby_steps",
+    "hd_query_baby",
 ]
 
 
@@ -143,6 +144,8 @@ def load():
             L.hd_decrypt_slots.argtypes = [VP, VP, VP, VP, C.c_size_t]
             L.hd_query_batch.argtypes = [VP, VP, VP, VP, C.c_size_t, VP, C.c_size_t]
             L.hd_eval_add_many.argtypes = [VP, VP, C.c_size_t, C.POINTER(VP)]
+            L.hd_baby_steps.argtypes = [VP, VP, VP, VP, C.c_uint32, C.c_uint32, VP]
+            L.hd_query_baby.argtypes = [VP, VP, VP, VP, VP, C.c_size_t]
             _lib = L
         return _lib
 
@@ -393,6 +396,19 @@ class Context(_Handle):
         _check("hd_query_batch", load().hd_query_batch(self.h, evk.h, db.h, qs, Q, arr, Q * nloc))
         res = [o if o is not None else Ciphertext(arr[i], self) for i, o in enumerate(flat)]
         return [res[q * nloc:(q + 1) * nloc] for q in range(Q)]
+
+    def baby_steps(self, evk, db, query, i_begin, i_end, r_dev_ptr):
+        """hd_baby_steps: r[i] for i in [i_begin, i_end) into the device buffer at r_dev_ptr."""
+        _check("hd_baby_steps", load().hd_baby_steps(self.h, evk.h, db.h, query.h, i_begin, i_end,
+                                                     C.c_void_p(r_dev_ptr)))
+
+    def query_baby(self, evk, db, r_dev_ptr, outs=None):
+        nloc = db.num_local
+        if outs is None:
+            outs = [None] * nloc
+        arr = (VP * nloc)(*[(o.h if o is not None else None) for o in outs])
+        _check("hd_query_baby", load().hd_query_baby(self.h, evk.h, db.h, C.c_void_p(r_dev_ptr), arr, nloc))
+        return [o if o is not None else Ciphertext(arr[i], self) for i, o in enumerate(outs)]
 
     def query_stats(self):
         """[baby, mac, rescale, giant, fold, baby_kip] ms averaged over the queries since the last call."""

@@ -59,14 +59,15 @@ static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
 // of the query two back has consumed the buffer).  With HD_SERIAL=1 both run on the
 // caller's stream.
 static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, uint32_t Q, cudaStream_t sa,
-                          cudaStream_t sb, hd_ciphertext **out, size_t n_out) {
+                          cudaStream_t sb, hd_ciphertext **out, size_t n_out, const uint64_t *r_ext = nullptr) {
   hd_context *c = db->ctx;
   const int n = c->n, L = c->L, n1 = (int)db->n1, nj = (int)db->js.size();
   const uint32_t A = db->A_loc;
   const size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * (L - 1) * n;
   const int par = (int)(db->qcount & 1);
   uint64_t *Sbuf = Q > 1 ? db->SB[par] : (par ? db->S2 : db->S);
-  uint64_t *rbase = Q > 1 ? db->rB : db->r;
+  // r_ext: baby steps supplied by the caller (hd_query_baby; written on the caller's stream)
+  uint64_t *rbase = r_ext ? const_cast<uint64_t *>(r_ext) : (Q > 1 ? db->rB : db->r);
   const size_t sL = (size_t)db->spoly * L * n;  // one giant-step sum
   const size_t sq = (size_t)A * nj * sL;         // the sums of one query
   cudaStream_t caller = c->stream;
@@ -78,7 +79,8 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, 
   // A depends only on the query's last writer (not on the caller's stream position), so
   // the baby steps + MAC of this query can run while B still finishes the previous one.
   HD_CUDA(cudaEventRecord(db->ev_in, caller));
-  for (uint32_t qi = 0; qi < Q; qi++) {
+  if (r_ext) HD_CUDA(cudaStreamWaitEvent(sa, db->ev_in, 0));  // after the caller's baby-step writers
+  for (uint32_t qi = 0; qi < Q && !r_ext; qi++) {
     HD_CUDA(cudaStreamWaitEvent(sa, queries[qi]->ready, 0));
     hd_ciphertext *qmut = const_cast<hd_ciphertext *>(queries[qi]);  // reader bookkeeping only
     if (!qmut->used) {
@@ -90,12 +92,12 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, 
   if (db->qcount >= 2) HD_CUDA(cudaStreamWaitEvent(sa, db->ev_sfree[par], 0));
   c->stream = sa;
   cudaEventRecord(E[0], sa);
-  if (n1 <= 1) {  // no baby-step key inner product: an empty KIP phase
+  if (n1 <= 1 || r_ext) {  // no baby-step key inner product here: an empty KIP phase
     cudaEventRecord(E[7], sa);
     cudaEventRecord(E[8], sa);
   }
   // ---- baby steps: r[0] = q; r[i] = Rot_i(q), hoisted (per query) ----
-  for (uint32_t qi = 0; qi < Q; qi++) {
+  for (uint32_t qi = 0; qi < Q && !r_ext; qi++) {
     const hd_ciphertext *query = queries[qi];
     uint64_t *rq = rbase + (size_t)qi * n1 * ctL;
     HD_CUDA(cudaMemcpyAsync(rq, query->data, ctL * 8, cudaMemcpyDeviceToDevice, sa));
@@ -343,6 +345,87 @@ extern "C" hd_status hd_query_batch(hd_context *c, const hd_eval_keys *evk, cons
   }
   cudaStream_t caller = c->stream;
   s = run_scan(db, queries, Q, sa, sb, outs.data(), n_out);
+  c->stream = caller;
+  if (s) {
+    for (auto *f : fresh) hd_ciphertext_destroy(f);
+    return s;
+  }
+  for (size_t i = 0; i < n_out; i++) out[i] = outs[i];
+  HD_CUDA(cudaGetLastError());
+  db->has_run = true;
+  return HD_OK;
+}
+
+// Baby steps r[i], i in [i_begin, i_end), of one query into a caller device buffer laid out
+// [n1][2][L][n] (multi-GPU: each rank computes a slice, an all-gather assembles r).
+extern "C" hd_status hd_baby_steps(hd_context *c, const hd_eval_keys *evk, const hd_database *dbc,
+                                   const hd_ciphertext *query, uint32_t i_begin, uint32_t i_end, void *r_dev) {
+  if (!c || !evk || !dbc || !query || !r_dev) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  hd_database *db = const_cast<hd_database *>(dbc);
+  if (db->ctx != c || evk->ctx != c || query->ctx != c) return hd_fail(HD_E_STATE, "objects from another context");
+  if (query->limbs != (uint32_t)c->L) return hd_fail(HD_E_LEVEL, "query must be at L limbs");
+  if (i_begin > i_end || i_end > db->n1) return hd_fail(HD_E_INVALID_ARG, "baby-step range outside [0, n1]");
+  hd_status s = bind_keys(db, evk);
+  if (s) return s;
+  const int n = c->n, L = c->L;
+  const size_t ctL = (size_t)2 * L * n;
+  uint64_t *r = static_cast<uint64_t *>(r_dev);
+  HD_CUDA(cudaStreamWaitEvent(c->stream, query->ready, 0));
+  if (i_begin == 0 && i_end > 0)
+    HD_CUDA(cudaMemcpyAsync(r, query->data, ctL * 8, cudaMemcpyDeviceToDevice, c->stream));
+  const uint32_t i0 = i_begin > 1 ? i_begin : 1;
+  if (i_end > i0) {
+    const uint32_t K = i_end - i0;  // rotations i0 .. i_end - 1 use key slots i0 - 1 ..
+    if ((s = ks_modup(c, query->data + (size_t)L * n, 0, 1, L, db->dig_b, db->tmp_b))) return s;
+    if ((s = ks_kip(c, db->dig_b, query->data + (size_t)L * n, 0, 1, K, L, db->kptr + (i0 - 1), db->gal + (i0 - 1),
+                    db->u_b)))
+      return s;
+    if ((s = ks_moddown(c, db->u_b, K, K, L, db->gal + (i0 - 1), query->data, 0, r + (size_t)i0 * ctL, ctL, false,
+                        db->tmp_b)))
+      return s;
+  }
+  hd_ciphertext *qmut = const_cast<hd_ciphertext *>(query);  // reader bookkeeping only
+  if (!qmut->used) HD_CUDA(cudaEventCreateWithFlags(&qmut->used, cudaEventDisableTiming));
+  HD_CUDA(cudaEventRecord(qmut->used, c->stream));
+  HD_CUDA(cudaGetLastError());
+  return HD_OK;
+}
+
+// The scan from caller-supplied baby steps (all n1 of them, [n1][2][L][n] on the device).
+extern "C" hd_status hd_query_baby(hd_context *c, const hd_eval_keys *evk, const hd_database *dbc, const void *r_dev,
+                                   hd_ciphertext **out, size_t n_out) {
+  if (!c || !evk || !dbc || !r_dev || (!out && n_out)) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  hd_database *db = const_cast<hd_database *>(dbc);
+  if (db->ctx != c || evk->ctx != c) return hd_fail(HD_E_STATE, "objects from another context");
+  if (n_out != db->A_loc) return hd_fail(HD_E_INVALID_ARG, "n_out must equal agg_end - agg_begin");
+  if (db->needs_prerotation) return hd_fail(HD_E_STATE, "FLAT_TBS database: call hd_database_prerotate first");
+  const int L = c->L;
+  hd_status s = bind_keys(db, evk);
+  if (s) return s;
+  for (size_t i = 0; i < n_out; i++)
+    if (out[i] && (out[i]->ctx != c || out[i]->limbs != (uint32_t)(L - 1)))
+      return hd_fail(HD_E_LEVEL, "reused output ciphertext has the wrong shape");
+  std::vector<hd_ciphertext *> fresh;
+  std::vector<hd_ciphertext *> outs(out, out + n_out);
+  for (size_t i = 0; i < n_out; i++)
+    if (!out[i]) {
+      hd_ciphertext *ct;
+      if ((s = alloc_ct(c, L - 1, &ct))) {
+        for (auto *f : fresh) hd_ciphertext_destroy(f);
+        return s;
+      }
+      fresh.push_back(ct);
+      outs[i] = ct;
+    }
+  const char *serial = getenv("HD_SERIAL");
+  cudaStream_t sa = c->stream, sb = c->stream;
+  if (!(serial && serial[0] == '1')) {
+    if ((s = ensure_streams(c))) return s;
+    sa = c->sA;
+    sb = c->sB;
+  }
+  cudaStream_t caller = c->stream;
+  s = run_scan(db, nullptr, 1, sa, sb, outs.data(), n_out, static_cast<const uint64_t *>(r_dev));
   c->stream = caller;
   if (s) {
     for (auto *f : fresh) hd_ciphertext_destroy(f);

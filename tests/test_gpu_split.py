@@ -1,0 +1,48 @@
+"""GPU parity of the split baby steps (hd_baby_steps / hd_query_baby).  With the
+database sharded over P GPUs each rank computes a slice of the n1 - 1 baby rotations and an
+all-gather assembles r; here the slices (ragged, as for P = 3) are written into one device
+buffer on one GPU, and the scan from that buffer must equal hd_query bit for bit, also for
+aggregate shards of the database."""
+import numpy as np
+import pytest
+
+from synth_inputs import CONFIGS, ENC_SEED_BASE, make_dataset
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2604_00546_b200 as hd  # noqa: E402
+
+
+@pytest.mark.parametrize("name,packing", [("C2", "replicated"), ("C1", "flat")])
+def test_split_baby_steps_equal_hd_query(name, packing):
+    cfg = CONFIGS[name]
+    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
+    db_vecs, q, _ = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    sk, evk = ctx.keygen(ctx.rotation_steps(cfg.dim, cfg.n1, packing=packing))
+    db = ctx.enroll(db_vecs, cfg.n1, packing=packing)
+    qct = ctx.encrypt_query(sk, q, ENC_SEED_BASE)
+    ref = [ctx.ciphertext_residues(o) for o in ctx.query(evk, db, qct)]
+    n1, L, n = cfg.n1, cfg.limbs, 1 << cfg.log_n
+    r = torch.zeros(n1 * 2 * L * n, dtype=torch.int64, device="cuda")
+    bounds = [0, n1 // 3, (2 * n1) // 3 + 1, n1]            # three ragged "rank" slices
+    for i0, i1 in zip(bounds[:-1], bounds[1:]):
+        ctx.baby_steps(evk, db, qct, i0, i1, r.data_ptr())
+    outs = ctx.query_baby(evk, db, r.data_ptr())
+    torch.cuda.synchronize()
+    for a, o in enumerate(outs):
+        assert (ctx.ciphertext_residues(o) == ref[a]).all(), a
+    # aggregate shards (one database handle per "rank") scanned from the same gathered r
+    A = db.num_local
+    if A > 1:
+        for a0, a1 in ((0, A // 2), (A // 2, A)):
+            part = ctx.enroll(db_vecs, cfg.n1, a0, a1, packing=packing)
+            got = ctx.query_baby(evk, part, r.data_ptr())
+            torch.cuda.synchronize()
+            for i, o in enumerate(got):
+                assert (ctx.ciphertext_residues(o) == ref[a0 + i]).all(), (a0, i)
+    with pytest.raises(hd.HDError):
+        ctx.baby_steps(evk, db, qct, 0, n1 + 1, r.data_ptr())
