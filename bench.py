@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--batch", type=int, default=1,
                     help="queries per step through hd_query_batch (NEXT-4: one diagonal stream serves up to 4 "
                          "queries); 1 = hd_query")
+    ap.add_argument("--split-baby", action="store_true",
+                    help="N > 1: each rank computes a slice of the baby steps, NCCL all-gathers r "
+                         "(hd_baby_steps / hd_query_baby) instead of every rank recomputing all of them")
     ap.add_argument("--kappa", type=int, default=8, help="comparison depth budget (P:L721: 8 -> degree 13)")
     ap.add_argument("--delta", type=float, default=0.5, help="comparison threshold")
     ap.add_argument("--limbs", type=int, default=0, help="RNS limbs (default 3; 6 for the comparison scenarios)")
@@ -344,6 +347,14 @@ def main():
     nloc = a1 - a0
     outs = None
     outs_b = None  # hd_query_batch outputs [Q][nloc]
+    split = None
+    ct_l = 2 * cfg.limbs * (1 << cfg.log_n)  # u64 words of one baby-step ciphertext
+    if args.split_baby and world > 1 and Q == 1:
+        chunk = -(-cfg.n1 // world)  # baby steps per rank (the last slice may be short)
+        r_full = torch.empty(world * chunk * ct_l, dtype=torch.int64, device=dev)
+        r_mine = torch.empty(chunk * ct_l, dtype=torch.int64, device=dev)
+        i0, i1 = min(cfg.n1, rank * chunk), min(cfg.n1, (rank + 1) * chunk)
+        split = (r_full, r_mine, i0, i1)
     cmps = None
     mem = None
     part = [None]   # membership under sharding: this rank's EvalAddMany
@@ -367,6 +378,11 @@ def main():
         if Q > 1:  # NEXT-4: Q queries per diagonal pass
             outs_b = ctx.query_batch(evk, db, qcts, outs_b)
             outs = [o for row in outs_b for o in row]
+        elif split is not None:  # baby-step slice per rank + NCCL all-gather of r (8(e))
+            r_full, r_mine, i0, i1 = split
+            ctx.baby_steps(evk, db, qct, i0, i1, r_mine.data_ptr() - i0 * ct_l * 8)
+            dist.all_gather_into_tensor(r_full, r_mine)
+            outs = ctx.query_baby(evk, db, r_full.data_ptr(), outs)
         else:
             outs = ctx.query(evk, db, qct, outs)
         if tail:  # NEXT-3: ChebyshevCompare of every score ciphertext (+ membership sum)
@@ -554,7 +570,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": mac_bytes, "avg_launch_ms": mac_avg_ms},
             "keyswitch": keyswitch, "query_roofline": query_roofline, "tail_ms": tail_ms,
-            "scenario": args.scenario, "queries_per_step": Q,
+            "scenario": args.scenario, "queries_per_step": Q, "split_baby": split is not None,
             "clocks": clocks, "e2e": e2e}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import multiprocessing
