@@ -118,8 +118,8 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, 
   if (Q > 1) {
     if ((s = mac_batch_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat, Q))) return s;
   } else if (db->encrypted) {
-    if ((s = mac_ct_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js, db->flat))) return s;
-  } else if ((s = mac_run(c, db->D, db->r, Sbuf, A, n1, (int)db->N, db->js, db->flat))) {
+    if ((s = mac_ct_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat))) return s;
+  } else if ((s = mac_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat))) {
     return s;
   }
   cudaEventRecord(E[2], sa);

@@ -23,9 +23,10 @@ def test_split_baby_steps_equal_hd_query(name, packing):
     ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
     db_vecs, q, _ = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
     sk, evk = ctx.keygen(ctx.rotation_steps(cfg.dim, cfg.n1, packing=packing))
-    db = ctx.enroll(db_vecs, cfg.n1, packing=packing)
     qct = ctx.encrypt_query(sk, q, ENC_SEED_BASE)
-    ref = [ctx.ciphertext_residues(o) for o in ctx.query(evk, db, qct)]
+    db_ref = ctx.enroll(db_vecs, cfg.n1, packing=packing)
+    ref = [ctx.ciphertext_residues(o) for o in ctx.query(evk, db_ref, qct)]
+    db = ctx.enroll(db_vecs, cfg.n1, packing=packing)  # fresh handle: nothing left from hd_query
     n1, L, n = cfg.n1, cfg.limbs, 1 << cfg.log_n
     r = torch.zeros(n1 * 2 * L * n, dtype=torch.int64, device="cuda")
     bounds = [0, n1 // 3, (2 * n1) // 3 + 1, n1]            # three ragged "rank" slices
