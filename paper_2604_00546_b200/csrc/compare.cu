@@ -222,9 +222,7 @@ struct Eval {
     Batch ab = mul(a, b);
     if (err) return Batch{};
     Lin k{};
-    if (c_ct) {
-      const int ell = std::min(ab.ell, c_ct->ell);
-      (void)ell;
+    if (c_ct) {  // MatchLevel inside lincomb
       for (int l = 0; l < c->L; l++) {
         k.ka[l] = 2 % c->mod[l];
         k.kb[l] = c->mod[l] - 1;
