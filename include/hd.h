@@ -187,6 +187,13 @@ hd_status hd_enroll_ex(hd_context *ctx, const hd_enroll_options *opt, const floa
                        uint64_t num_vectors, uint32_t vector_dim, uint32_t n1, uint32_t agg_begin,
                        uint32_t agg_end, hd_database **out);
 hd_status hd_database_layout(const hd_database *db, hd_layout *out);
+/* Online database aggregation (NEXT-4; Alg. online-aggr, membership only): a new
+ * handle with ONE aggregate whose diagonals are the sums (mod q) of the diagonals of all
+ * aggregates of db (plaintext or encrypted, any packing; a FLAT_TBS database must be
+ * pre-rotated first).  hd_query on it returns one ciphertext whose slots hold the per-slot
+ * sums of every aggregate's scores (the scan is linear); the paper then compares that
+ * aggregated score and EvalSums it (hd_compare, hd_membership). */
+hd_status hd_database_aggregate(hd_context *ctx, const hd_database *db, hd_database **out);
 /* Keys of the TBS pre-rotation: {numSlots - j n1 : 1 <= j < ceil(N/n1)} (ascending). */
 hd_status hd_prerotation_steps(const hd_context *ctx, uint32_t vector_dim, uint32_t n1, int32_t *steps,
                                size_t cap, size_t *count);

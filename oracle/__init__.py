@@ -438,6 +438,15 @@ class Oracle:
                                                         _p(np.ascontiguousarray(rlk)), _p(out)))
         return out
 
+    def aggregate_diagonals(self, Ds):
+        """Online DB aggregation (Alg. online-aggr Step 2): the per-aggregate diagonals summed."""
+        D = np.ascontiguousarray(np.stack(Ds), dtype=np.uint64)
+        A, N = D.shape[0], D.shape[1]
+        dpoly = 2 if D.ndim == 5 else 1
+        out = np.zeros(D.shape[1:], dtype=np.uint64)
+        _check("aggregate_diagonals", lib().or_aggregate_diagonals(C.byref(self.p), _p(D), A, N, dpoly, _p(out)))
+        return out
+
     def membership(self, cts, steps, keys):
         """EvalAddMany + RotateAndSum over numSlots (Alg. membership)."""
         cts = np.ascontiguousarray(cts, dtype=np.uint64)

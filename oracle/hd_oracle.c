@@ -1838,3 +1838,18 @@ int or_membership(const or_params *p, const uint64_t *cts, int32_t count, int32_
   free(R);
   return rc;
 }
+
+/* Online database aggregation (Alg. online-aggr Step 2): diag_i summed over the
+ * A aggregates, residue by residue.  D: A x N diagonals of dpoly polynomials of L limbs
+ * ([a][k][poly][limb][n]); out: N x dpoly x L x n. */
+int or_aggregate_diagonals(const or_params *p, const uint64_t *D, int32_t A, int32_t N, int32_t dpoly, uint64_t *out) {
+  int n = p->n, L = p->L;
+  if (A < 1 || N < 1 || dpoly < 1) return OR_E_ARG;
+  size_t per = (size_t)N * dpoly * L * n;
+  for (size_t e = 0; e < per; e++) {
+    uint64_t q = p->mod[(e / (size_t)n) % (size_t)L], acc = 0;
+    for (int a = 0; a < A; a++) acc = addmod(acc, D[(size_t)a * per + e], q);
+    out[e] = acc;
+  }
+  return OR_OK;
+}

@@ -37,7 +37,7 @@ ABI_FUNCTIONS = [
     "hd_enroll_ex", "hd_rotation_steps_ex", "hd_prerotation_steps", "hd_database_prerotate",
     "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
     "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch", "hd_eval_add_many", "hd_baby_steps",
-    "hd_query_baby",
+    "hd_query_baby", "hd_database_aggregate",
 ]
 
 
@@ -146,6 +146,7 @@ def load():
             L.hd_eval_add_many.argtypes = [VP, VP, C.c_size_t, C.POINTER(VP)]
             L.hd_baby_steps.argtypes = [VP, VP, VP, VP, C.c_uint32, C.c_uint32, VP]
             L.hd_query_baby.argtypes = [VP, VP, VP, VP, VP, C.c_size_t]
+            L.hd_database_aggregate.argtypes = [VP, VP, C.POINTER(VP)]
             _lib = L
         return _lib
 
@@ -322,6 +323,14 @@ class Context(_Handle):
         _check("hd_prerotation_steps", load().hd_prerotation_steps(self.h, vector_dim, n1, _ptr(steps), cnt.value,
                                                                    C.byref(cnt)))
         return steps
+
+    def database_aggregate(self, db):
+        """hd_database_aggregate: one aggregate holding the sums of db's diagonals (NEXT-4)."""
+        out = VP()
+        _check("hd_database_aggregate", load().hd_database_aggregate(self.h, db.h, C.byref(out)))
+        agg = Database(out.value, self)
+        agg.encrypted = getattr(db, "encrypted", False)
+        return agg
 
     def database_prerotate(self, evk, db):
         _check("hd_database_prerotate", load().hd_database_prerotate(self.h, evk.h, db.h))

@@ -266,33 +266,19 @@ extern "C" void hd_database_destroy(hd_database *db) {
   delete db;
 }
 
-// pk == NULL: plaintext diagonals (the north-star pt x ct scan); else every diagonal
-// plaintext is encrypted under pk (encrypted-database mode, NEXT-1, R26).
-static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_key *pk, uint64_t enc_seed,
-                             const float *vectors, uint64_t num_vectors, uint32_t vector_dim, uint32_t n1,
-                             uint32_t agg_begin, uint32_t agg_end, hd_database **out) {
-  if (!c || !vectors || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
-  if (pk && pk->ctx != c) return hd_fail(HD_E_STATE, "public key from another context");
-  if (packing == HD_PACKING_FLAT_TBS && !pk)
-    return hd_fail(HD_E_INVALID_ARG, "FLAT_TBS packing needs a public key (encrypted diagonals)");
-  *out = nullptr;
-  hd_layout lay;
-  hd_status s = layout_make(c, num_vectors, vector_dim, n1, packing, &lay);
-  if (s) return s;
-  if (agg_end == 0) agg_end = (uint32_t)lay.num_aggregates;
-  if (agg_begin >= agg_end || agg_end > lay.num_aggregates) return hd_fail(HD_E_INVALID_ARG, "bad aggregate range");
-  lay.agg_begin = agg_begin;
-  lay.agg_end = agg_end;
+// Device objects of a database handle: diagonals D (uninitialised), query workspaces, events.
+static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing, bool encrypted, uint32_t n1,
+                          hd_database **out) {
   HD_CUDA(cudaSetDevice(c->device));
   hd_database *db = new hd_database();
   db->ctx = c;
   db->lay = lay;
-  db->N = vector_dim;
+  db->N = lay.vector_dim;
   db->M = lay.blocks_m;
   db->n1 = n1;
-  db->A_loc = agg_end - agg_begin;
-  db->encrypted = pk != nullptr;
-  db->spoly = pk ? 3 : 2;
+  db->A_loc = lay.agg_end - lay.agg_begin;
+  db->encrypted = encrypted;
+  db->spoly = encrypted ? 3 : 2;
   const int N = (int)db->N, L = c->L, n = c->n, ns = c->ns;
   db->flat = packing != HD_PACKING_REPLICATED;
   db->needs_prerotation = packing == HD_PACKING_FLAT_TBS;
@@ -320,14 +306,14 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
   size_t u_e = A * 2 * L * n;
   size_t tmp_e = std::max({A * 2 * (L - 1) * n, rescale_chunk * 2 * n, (size_t)L * n});
   const size_t sL = (size_t)db->spoly * L * n;  // one giant-step sum
-  if (pk) {  // relinearisation of A sums at a time at L limbs (ModUp digits, KIP, ModDown)
+  if (encrypted) {  // relinearisation of A sums at a time at L limbs (ModUp digits, KIP, ModDown)
     db->relin_chunk = (uint32_t)A;
     dig_e = std::max(dig_e, A * L * L * n);
     u_e = std::max(u_e, A * 2 * (L + 1) * n);
     tmp_e = std::max(tmp_e, A * 2 * L * n);
   }
-  const size_t dstride = (pk ? 2 : 1) * (size_t)L * n;  // one diagonal (pt, or ct)
-  size_t tmp2_e = pk ? A * 2 * (L - 1) * n : 1;  // CRT remainders of the fused relinearise-rescale
+  const size_t dstride = (encrypted ? 2 : 1) * (size_t)L * n;  // one diagonal (pt, or ct)
+  size_t tmp2_e = encrypted ? A * 2 * (L - 1) * n : 1;  // CRT remainders of the fused relinearise-rescale
   size_t digb_e = (size_t)L * L * n, ub_e = nb * 2 * (L + 1) * n, tmpb_e = std::max(nb * 2 * L * n, (size_t)L * n);
   db->rescale_chunk = (uint32_t)rescale_chunk;
   struct Req {
@@ -374,6 +360,31 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
       hd_database_destroy(db);
       return hd_fail(HD_E_CUDA, "event creation");
     }
+  *out = db;
+  return HD_OK;
+}
+
+// pk == NULL: plaintext diagonals (the north-star pt x ct scan); else every diagonal
+// plaintext is encrypted under pk (encrypted-database mode, NEXT-1, R26).
+static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_key *pk, uint64_t enc_seed,
+                             const float *vectors, uint64_t num_vectors, uint32_t vector_dim, uint32_t n1,
+                             uint32_t agg_begin, uint32_t agg_end, hd_database **out) {
+  if (!c || !vectors || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  if (pk && pk->ctx != c) return hd_fail(HD_E_STATE, "public key from another context");
+  if (packing == HD_PACKING_FLAT_TBS && !pk)
+    return hd_fail(HD_E_INVALID_ARG, "FLAT_TBS packing needs a public key (encrypted diagonals)");
+  *out = nullptr;
+  hd_layout lay;
+  hd_status s = layout_make(c, num_vectors, vector_dim, n1, packing, &lay);
+  if (s) return s;
+  if (agg_end == 0) agg_end = (uint32_t)lay.num_aggregates;
+  if (agg_begin >= agg_end || agg_end > lay.num_aggregates) return hd_fail(HD_E_INVALID_ARG, "bad aggregate range");
+  lay.agg_begin = agg_begin;
+  lay.agg_end = agg_end;
+  hd_database *db = nullptr;
+  if ((s = db_alloc(c, lay, packing, pk != nullptr, n1, &db))) return s;
+  const int N = (int)db->N, L = c->L, n = c->n, ns = c->ns;
+  const size_t dstride = (pk ? 2 : 1) * (size_t)L * n;  // one diagonal (pt, or ct)
   // enrollment scratch: rows of one aggregate (float + double), FFT buffers for a batch of diagonals
   const size_t rows_per_agg = (size_t)lay.groups_per_ct * N;
   const int KB = std::min(N, std::max(1, (int)((256ull << 20) / ((size_t)ns * 16))));
@@ -434,6 +445,43 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
   if (s) {
     hd_database_destroy(db);
     return s;
+  }
+  *out = db;
+  return HD_OK;
+}
+
+// D_out[k][.] = sum_a D[a][k][.] mod q_limb (Alg. online-aggr Step 2).
+__global__ void aggregate_kernel(const uint64_t *__restrict__ D, uint64_t *__restrict__ out, uint64_t per_agg,
+                                 uint32_t A, int logn, int L, ModTab mt) {
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= per_agg) return;
+  const int l = (int)((e >> logn) % (uint64_t)L);  // [k][poly][limb][coef] or [k][limb][coef]
+  const uint64_t q = mt.q[l];
+  uint64_t acc = 0;
+  for (uint32_t a = 0; a < A; a++) acc = addmod(acc, D[(uint64_t)a * per_agg + e], q);
+  out[e] = acc;
+}
+
+extern "C" hd_status hd_database_aggregate(hd_context *c, const hd_database *src, hd_database **out) {
+  if (!c || !src || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  if (src->ctx != c) return hd_fail(HD_E_STATE, "database from another context");
+  if (src->needs_prerotation) return hd_fail(HD_E_STATE, "FLAT_TBS database: call hd_database_prerotate first");
+  *out = nullptr;
+  hd_layout lay = src->lay;
+  lay.agg_end = lay.agg_begin + 1;
+  hd_database *db = nullptr;
+  hd_status s = db_alloc(c, lay, lay.packing, src->encrypted, src->n1, &db);
+  if (s) return s;
+  db->needs_prerotation = false;  // the source's diagonals are already in their final form
+  const uint64_t per_agg = (uint64_t)src->N * (src->encrypted ? 2 : 1) * c->L * c->n;
+  aggregate_kernel<<<(unsigned)((per_agg + TPB - 1) / TPB), TPB, 0, c->stream>>>(src->D, db->D, per_agg, src->A_loc,
+                                                                                c->logn, c->L, c->mt);
+  ++c->launches;
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) {
+    hd_database_destroy(db);
+    return hd_fail(HD_E_CUDA, cudaGetErrorString(e));
   }
   *out = db;
   return HD_OK;

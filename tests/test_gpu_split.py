@@ -47,3 +47,52 @@ def test_split_baby_steps_equal_hd_query(name, packing):
                 assert (ctx.ciphertext_residues(o) == ref[a0 + i]).all(), (a0, i)
     with pytest.raises(hd.HDError):
         ctx.baby_steps(evk, db, qct, 0, n1 + 1, r.data_ptr())
+
+
+@pytest.mark.parametrize("name,packing,encrypted", [("C2", "replicated", False), ("C1big", "flat", True)])
+def test_online_aggregation_bit_exact(name, packing, encrypted):
+    """Online DB aggregation (NEXT-4, Alg. online-aggr): the aggregated handle's
+    diagonals equal the oracle's residue-wise sum of every aggregate's diagonals, and its scan
+    output equals the oracle's scan of that sum, bit for bit."""
+    import dataclasses
+
+    import oracle
+    from synth_inputs import Config
+    cfg = CONFIGS["C2"] if name == "C2" else Config("agg", 12, 64, 5000, 8, index=12)
+    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
+    o = oracle.Oracle(cfg.log_n, cfg.limbs, seed=1)
+    db_vecs, q, _ = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    steps = ctx.rotation_steps(cfg.dim, cfg.n1, packing=packing)
+    sk, evk = ctx.keygen(steps)
+    pk = None
+    if encrypted:
+        ctx.relin_keygen(sk, evk)
+        pk = ctx.public_keygen(sk)
+    db = ctx.enroll(db_vecs, cfg.n1, packing=packing, pk=pk, enc_seed=7)
+    agg = ctx.database_aggregate(db)
+    assert agg.num_local == 1
+    out = ctx.query(evk, agg, ctx.encrypt_query(sk, q, ENC_SEED_BASE))
+    torch.cuda.synchronize()
+    _, s_ntt = o.secret_key()
+    st, keys = o.keyset(s_ntt, [int(x) for x in steps])
+    A = db.num_local
+    U = o.normalize_rows(db_vecs)
+    if packing == "flat":
+        per = o.ns
+        opk, orlk = o.public_key(s_ntt), o.relin_key(s_ntt)
+        Ds = [o.enroll_aggregate_flat_encrypted(U[a * per:(a + 1) * per], a * per, cfg.num_vectors, cfg.n1, a, opk, 7)
+              for a in range(A)]
+    else:
+        per = (o.ns // cfg.dim // 2) * cfg.dim
+        Ds = [o.enroll_aggregate(U[(a - a % 2) * per:(a - a % 2 + 2) * per], (a - a % 2) * per, cfg.num_vectors,
+                                 cfg.n1, a) for a in range(A)]
+    Dsum = o.aggregate_diagonals(Ds)
+    for k in (0, cfg.dim - 1):
+        assert (ctx.test_stage(agg, 4, 0, k) == Dsum[k]).all(), k
+    qct = o.encrypt(s_ntt, o.encode(o.query_slots(q), 2.0 ** 45, cfg.limbs), ENC_SEED_BASE)
+    r = o.baby_steps(qct, cfg.n1, st, keys)
+    if packing == "flat":
+        ref = o.scan_aggregate_flat_ct(r, cfg.n1, cfg.dim, Dsum, st, keys, orlk)
+    else:
+        ref = o.scan_aggregate(r, cfg.n1, cfg.dim, Dsum, st, keys)
+    assert (ctx.ciphertext_residues(out[0]) == ref).all()

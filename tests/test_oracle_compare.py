@@ -189,3 +189,26 @@ def test_compare_constant_series_is_rejected(oracle_mod, ring6):
     with pytest.raises(oracle_mod.OracleError) as e:
         o.cheb_compare(_encrypt_slots(o, s_ntt, np.zeros(o.ns), 5, 6), D45, np.array([1.0] + [0.0] * 13), rlk)
     assert e.value.code == oracle_mod.OR_E_ARG
+
+
+def test_online_aggregation_is_the_sum_of_the_scans(oracle_mod):
+    """Alg. online-aggr: the scan of the aggregated diagonals decrypts to the sum
+    of the per-aggregate scans (the scan is linear), slot by slot, within the CKKS noise."""
+    from synth_inputs import Config
+    cfg = Config("agg", 12, 64, 2500, 8, index=11)   # 3 aggregates of 1024 vectors, the last ragged
+    o = oracle_mod.Oracle(cfg.log_n, cfg.limbs, seed=1)
+    s, s_ntt = o.secret_key()
+    db, q, _ = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    st, keys = o.keyset(s_ntt, o.rotation_steps(cfg.dim, cfg.n1))
+    r = o.baby_steps(o.encrypt(s_ntt, o.encode(o.query_slots(q), D45, o.L), 1000), cfg.n1, st, keys)
+    U = o.normalize_rows(db)
+    per = (o.ns // cfg.dim // 2) * cfg.dim
+    # Alg. enroller_bsgs builds aggregates in (ctA, ctB) pairs from one temporary: pass the pair's rows
+    Ds = [o.enroll_aggregate(U[(a - a % 2) * per:(a - a % 2 + 2) * per], (a - a % 2) * per, cfg.num_vectors,
+                             cfg.n1, a) for a in range(3)]
+    Dsum = o.aggregate_diagonals(Ds)
+    mods = np.array(o.p.moduli[:o.L], dtype=object)[:, None]
+    assert ((sum(D.astype(object) for D in Ds) % mods) == Dsum.astype(object)).all()   # residue-wise sum
+    z_sum = o.decode(o.decrypt(s_ntt, o.scan_aggregate(r, cfg.n1, cfg.dim, Dsum, st, keys)), D45)
+    z_parts = sum(o.decode(o.decrypt(s_ntt, o.scan_aggregate(r, cfg.n1, cfg.dim, D, st, keys)), D45) for D in Ds)
+    assert np.abs(z_sum - z_parts).max() < 1e-6
