@@ -58,6 +58,9 @@ def parse():
     ap.add_argument("--split-baby", action="store_true",
                     help="N > 1: each rank computes a slice of the baby steps, NCCL all-gathers r "
                          "(hd_baby_steps / hd_query_baby) instead of every rank recomputing all of them")
+    ap.add_argument("--online-aggregate", action="store_true",
+                    help="membership only: scan the online-aggregated database (one aggregate holding the sum of "
+                         "all aggregates' diagonals, Alg. online-aggr; NEXT-4), built at setup")
     ap.add_argument("--kappa", type=int, default=8, help="comparison depth budget (P:L721: 8 -> degree 13)")
     ap.add_argument("--delta", type=float, default=0.5, help="comparison threshold")
     ap.add_argument("--limbs", type=int, default=0, help="RNS limbs (default 3; 6 for the comparison scenarios)")
@@ -318,6 +321,17 @@ def main():
         t_p = time.perf_counter()
         ctx.database_prerotate(evk, db)
         prerot_s = time.perf_counter() - t_p
+    aggr_s = None
+    if args.online_aggregate:  # setup (untimed): Alg. online-aggr Step 2, one aggregate per rank
+        if args.scenario != "membership":
+            raise SystemExit("--online-aggregate is a membership-only option (Alg. online-aggr)")
+        torch.cuda.synchronize()
+        t_p = time.perf_counter()
+        full_db, db = db, ctx.database_aggregate(db)
+        del full_db
+        torch.cuda.synchronize()
+        aggr_s = time.perf_counter() - t_p
+        A, a0, a1 = world, rank, rank + 1  # one aggregated ciphertext per rank
     # ---- the query: encrypted on rank 0, exported into a device buffer (NCCL-broadcast each step) ----
     # Q = --batch distinct queries (the first is the dataset's query with its planted matches)
     Q = max(1, args.batch)
@@ -571,6 +585,8 @@ def main():
                          "algorithmic_bytes_per_launch": mac_bytes, "avg_launch_ms": mac_avg_ms},
             "keyswitch": keyswitch, "query_roofline": query_roofline, "tail_ms": tail_ms,
             "scenario": args.scenario, "queries_per_step": Q, "split_baby": split is not None,
+            "online_aggregate": None if aggr_s is None else {"setup_s": aggr_s, "note": "Alg. online-aggr: the "
+                                "scan runs over one aggregate holding the sum of all diagonals"},
             "clocks": clocks, "e2e": e2e}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import multiprocessing
