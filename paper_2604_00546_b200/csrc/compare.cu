@@ -390,7 +390,7 @@ hd_status upload_keys(hd_context *c, const std::vector<const uint64_t *> &kp, co
   return HD_OK;
 }
 
-constexpr uint32_t kCompareChunk = 32;  // ciphertexts evaluated together (workspace bound)
+constexpr uint32_t kCompareChunk = 64;  // ciphertexts evaluated together (workspace ~2 GB at 2^16, L = 6)
 
 }  // namespace
 
