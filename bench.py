@@ -364,10 +364,9 @@ def main():
     split = None
     ct_l = 2 * cfg.limbs * (1 << cfg.log_n)  # u64 words of one baby-step ciphertext
     if args.split_baby and world > 1 and Q == 1:
-        chunk = -(-cfg.n1 // world)  # baby steps per rank (the last slice may be short)
+        chunk, i0, i1 = hdd.baby_slice(cfg.n1, rank, world)  # the last slice may be short
         r_full = torch.empty(world * chunk * ct_l, dtype=torch.int64, device=dev)
         r_mine = torch.empty(chunk * ct_l, dtype=torch.int64, device=dev)
-        i0, i1 = min(cfg.n1, rank * chunk), min(cfg.n1, (rank + 1) * chunk)
         split = (r_full, r_mine, i0, i1)
     cmps = None
     mem = None

@@ -21,6 +21,14 @@ def shard_range(num_aggregates: int, rank: int, world: int):
     return (num_aggregates * rank) // world, (num_aggregates * (rank + 1)) // world
 
 
+def baby_slice(n1: int, rank: int, world: int):
+    """Split baby steps (hd_baby_steps): rank r computes r[i] for i in [i0, i1) into its chunk of
+    ceil(n1 / world) slots; an all-gather of the equal-size chunks lays r out in order (the
+    padding slots past n1 are ignored).  Returns (chunk, i0, i1)."""
+    chunk = -(-n1 // world)
+    return chunk, min(n1, rank * chunk), min(n1, (rank + 1) * chunk)
+
+
 def rows_of_aggregates(agg_begin: int, agg_end: int, per_aggregate: int, num_vectors: int):
     return min(agg_begin * per_aggregate, num_vectors), min(agg_end * per_aggregate, num_vectors)
 

@@ -73,3 +73,44 @@ def test_broadcast_gather_and_sharding(world, oracle_mod):
     assert ranges[0][0] == 0 and ranges[-1][1] == 7
     assert all(ranges[i][1] == ranges[i + 1][0] for i in range(world - 1))
     assert all(v == world for k, v in res if k == "max")
+
+
+def _split_worker(rank, world, port, r_all, results):
+    """bench.py --split-baby on gloo: each rank fills its slice of the baby steps (here taken
+    from the oracle's r) into its chunk; all_gather_into_tensor must reassemble r in order."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n1, ct = r_all.shape[0], r_all[0].size
+        chunk, i0, i1 = hdd.baby_slice(n1, rank, world)
+        mine = torch.zeros(chunk * ct, dtype=torch.int64)
+        if i1 > i0:
+            mine[: (i1 - i0) * ct] = torch.from_numpy(r_all[i0:i1].reshape(-1).view(np.int64))
+        full = torch.empty(world * chunk * ct, dtype=torch.int64)
+        dist.all_gather_into_tensor(full, mine)
+        if rank == 0:
+            got = full.numpy()[: n1 * ct].view(np.uint64).reshape(r_all.shape)
+            results.put(("split", bool((got == r_all).all())))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_split_baby_all_gather(world, oracle_mod):
+    o = oracle_mod.Oracle(6, 3)
+    s, s_ntt = o.secret_key()
+    n1 = 8
+    steps, keys = o.keyset(s_ntt, list(range(1, n1)))
+    qct = o.encrypt(s_ntt, o.encode(np.linspace(-1, 1, o.ns), 2.0 ** 45, 3), 1000)
+    r_all = o.baby_steps(qct, n1, steps, keys)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_split_worker, args=(r, world, port, r_all, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert q.get() == ("split", True)
+    assert [hdd.baby_slice(n1, r, world)[1:] for r in range(world)][0][0] == 0
