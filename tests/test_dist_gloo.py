@@ -114,3 +114,43 @@ def test_split_baby_all_gather(world, oracle_mod):
         assert p.exitcode == 0
     assert q.get() == ("split", True)
     assert [hdd.baby_slice(n1, r, world)[1:] for r in range(world)][0][0] == 0
+
+
+def _membership_worker(rank, world, port, cts, mods, results):
+    """bench.py --scenario membership at N > 1: each rank sums (EvalAddMany) its comparison
+    ciphertexts, the partial sums are gathered to rank 0, which runs the membership tail."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        a0, a1 = hdd.shard_range(cts.shape[0], rank, world)
+        part = np.zeros(cts.shape[1:], dtype=object)
+        for a in range(a0, a1):
+            part = (part + cts[a].astype(object)) % mods
+        local = torch.from_numpy(part.astype(np.uint64).view(np.uint8).ravel().copy())
+        got = hdd.gather_bytes(local, local.numel(), 0)
+        if rank == 0:
+            results.put(("parts", [g.numpy().view(np.uint64).reshape(cts.shape[1:]) for g in got]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_membership_partial_sums(world, oracle_mod):
+    o = oracle_mod.Oracle(6, 3)
+    s, s_ntt = o.secret_key()
+    rng = np.random.default_rng(world)
+    cts = np.stack([o.encrypt(s_ntt, o.encode(rng.uniform(0, 1, o.ns) * 1e-3, 2.0 ** 45, 2), 50 + a)
+                    for a in range(5)])
+    mods = np.array(o.p.moduli[:2], dtype=object)[None, :, None]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_membership_worker, args=(r, world, port, cts, mods, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    _, parts = q.get()
+    st, keys = o.keyset(s_ntt, [1 << k for k in range(o.log_n - 1)])
+    assert (o.membership(np.stack(parts), st, keys) == o.membership(cts, st, keys)).all()
