@@ -418,16 +418,16 @@ class Oracle:
         return sc
 
     # -- encrypted comparison and scenario tail (NEXT-3, R29) ---------------------
-    def cheb_compare(self, ct, scale, coeffs, rlk):
-        """ChebyshevCompare (Alg. gpu-chebyshev, P:L734-789): returns (ct_out, scale_out)."""
+    def cheb_compare(self, ct, scale, coeffs, rlk, out_limbs=1):
+        """ChebyshevCompare (Alg. gpu-chebyshev) to out_limbs limbs: (ct_out, scale_out)."""
         ell = ct.shape[1]
         c = np.ascontiguousarray(coeffs, dtype=np.float64)
         out = u64((2, ell, self.n))
         eo = C.c_int32(0)
         so = C.c_double(0.0)
-        _check("cheb_compare", lib().or_cheb_compare(
+        _check("cheb_compare", lib().or_cheb_compare_at(
             C.byref(self.p), _p(np.ascontiguousarray(ct)), ell, C.c_double(scale), _p(c), len(c) - 1,
-            _p(np.ascontiguousarray(rlk)), _p(out), C.byref(eo), C.byref(so)))
+            _p(np.ascontiguousarray(rlk)), out_limbs, _p(out), C.byref(eo), C.byref(so)))
         return np.ascontiguousarray(out.reshape(-1)[: 2 * eo.value * self.n].reshape(2, eo.value, self.n)), so.value
 
     def relin_rescale(self, S3, rlk):

@@ -1762,6 +1762,16 @@ static or_val ps_eval(or_ps *S, const double *c0, int m, int need) {
  * (capacity 2 ell n), *scale_out its scale.  OR_E_RANGE if the levels run out. */
 int or_cheb_compare(const or_params *p, const uint64_t *in, int32_t ell, double scale, const double *c,
                     int32_t degree, const uint64_t *rlk, uint64_t *out, int32_t *ell_out, double *scale_out) {
+  return or_cheb_compare_at(p, in, ell, scale, c, degree, rlk, 1, out, ell_out, scale_out);
+}
+
+/* As or_cheb_compare with the result wanted at `need` limbs (R29): a membership sum over many
+ * slots needs the headroom of q_0 q_1 (the sum of 2^20 values near 1 at scale 2^45 exceeds
+ * q_0 / 2). */
+int or_cheb_compare_at(const or_params *p, const uint64_t *in, int32_t ell, double scale, const double *c,
+                       int32_t degree, const uint64_t *rlk, int32_t need, uint64_t *out, int32_t *ell_out,
+                       double *scale_out) {
+  if (need < 1 || need >= ell) return OR_E_ARG;
   if (ell < 1 || ell > p->L || degree < 1) return OR_E_ARG;
   or_ps S;
   memset(&S, 0, sizeof S);
@@ -1788,7 +1798,7 @@ int or_cheb_compare(const or_params *p, const uint64_t *in, int32_t ell, double 
   }
   /* Step 3: chunks and combination */
   int rc = OR_OK;
-  or_val V = ps_eval(&S, c, degree, 1); /* the result at one limb (q_0) */
+  or_val V = ps_eval(&S, c, degree, need); /* the result at `need` limbs (1: q_0 only) */
   if (!V.is_ct) {
     rc = OR_E_ARG; /* constant polynomial: nothing encrypted to return */
   } else if (g_cheb_range_err) {

@@ -190,6 +190,9 @@ int or_ps_split(int32_t n, int32_t *d1, int32_t *d2);
 int or_cheb_coeffs(double delta, int32_t n, double *c /* n + 1 */);
 int or_cheb_compare(const or_params *p, const uint64_t *in, int32_t ell, double scale, const double *c,
                     int32_t degree, const uint64_t *rlk, uint64_t *out, int32_t *ell_out, double *scale_out);
+int or_cheb_compare_at(const or_params *p, const uint64_t *in, int32_t ell, double scale, const double *c,
+                       int32_t degree, const uint64_t *rlk, int32_t need, uint64_t *out, int32_t *ell_out,
+                       double *scale_out);
 /* Relinearize + Rescale with one rounding by P q_{ell-1}: S3 [3][ell][n] -> out [2][ell-1][n]. */
 int or_relin_rescale(const or_params *p, const uint64_t *S3, int32_t ell, const uint64_t *rlk, uint64_t *out);
 int or_aggregate_diagonals(const or_params *p, const uint64_t *D, int32_t A, int32_t N, int32_t dpoly, uint64_t *out);

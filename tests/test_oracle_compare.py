@@ -212,3 +212,15 @@ def test_online_aggregation_is_the_sum_of_the_scans(oracle_mod):
     z_sum = o.decode(o.decrypt(s_ntt, o.scan_aggregate(r, cfg.n1, cfg.dim, Dsum, st, keys)), D45)
     z_parts = sum(o.decode(o.decrypt(s_ntt, o.scan_aggregate(r, cfg.n1, cfg.dim, D, st, keys)), D45) for D in Ds)
     assert np.abs(z_sum - z_parts).max() < 1e-6
+
+
+def test_compare_to_two_limbs(oracle_mod, ring6):
+    """The result requested at 2 limbs (membership headroom, R29): same series, one level more left."""
+    o, s_ntt, rlk = ring6
+    z = np.random.default_rng(77).uniform(-1, 1, o.ns)
+    c = oracle_mod.cheb_coeffs(0.5, 13)
+    out, scale = o.cheb_compare(_encrypt_slots(o, s_ntt, z, 6, 8), D45, c, rlk, out_limbs=2)
+    assert out.shape[1] == 2
+    assert np.abs(o.decode(o.decrypt(s_ntt, out), scale) - npcheb.chebval(z, c)).max() < 1e-5
+    with pytest.raises(oracle_mod.OracleError):   # 5 limbs leave no room for degree 13 at 2 limbs
+        o.cheb_compare(_encrypt_slots(o, s_ntt, z, 5, 8), D45, c, rlk, out_limbs=2)
