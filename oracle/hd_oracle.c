@@ -1801,7 +1801,7 @@ int or_cheb_compare_at(const or_params *p, const uint64_t *in, int32_t ell, doub
   or_val V = ps_eval(&S, c, degree, need); /* the result at `need` limbs (1: q_0 only) */
   if (!V.is_ct) {
     rc = OR_E_ARG; /* constant polynomial: nothing encrypted to return */
-  } else if (g_cheb_range_err) {
+  } else if (g_cheb_range_err || V.ct.ell < need) { /* no level left, or below the requested one */
     rc = OR_E_RANGE;
     cct_free(&V.ct);
   } else {
