@@ -152,7 +152,9 @@ def workload_cfg(args):
     """BASELINE config, with 6 RNS limbs when the comparison follows the scan (R29)."""
     import dataclasses
     cfg = CONFIGS[args.config]
-    limbs = args.limbs or (6 if args.scenario != "scan" else cfg.limbs)
+    # comparison scenarios: degree 13 needs 4 levels after the scan; membership keeps 2 limbs of
+    # headroom for its sum over all slots (R29) -> 6 limbs for identification, 7 for membership
+    limbs = args.limbs or {"scan": cfg.limbs, "identification": 6, "membership": 7}[args.scenario]
     if limbs != cfg.limbs:
         cfg = dataclasses.replace(cfg, limbs=limbs)
     if args.n1 and args.n1 != cfg.n1:
@@ -292,6 +294,7 @@ def main():
     if args.scenario == "membership":  # + the power-of-two keys of RotateAndSum
         steps = np.array(sorted(set(int(s) for s in steps) | set(int(s) for s in ctx.membership_steps())), np.int32)
     coeffs = hd.chebyshev_coefficients(args.delta, hd.chebyshev_degree(args.kappa)) if tail else None
+    out_limbs = 2 if args.scenario == "membership" else 1  # the membership sum's headroom (R29)
     if rank == 0:
         sk, evk = ctx.keygen(steps)
         if enc_db or tail:  # relinearisation key travels with the eval keys (reserved step 0)
@@ -399,7 +402,7 @@ def main():
         else:
             outs = ctx.query(evk, db, qct, outs)
         if tail:  # NEXT-3: ChebyshevCompare of every score ciphertext (+ membership sum)
-            cmps = ctx.compare(evk, outs, coeffs, cmps)
+            cmps = ctx.compare(evk, outs, coeffs, cmps, out_limbs=out_limbs)
             if args.scenario == "membership":
                 if world == 1:
                     mem = ctx.membership(evk, cmps, mem)
@@ -478,7 +481,7 @@ def main():
             else:
                 outs = ctx.query(evk, db, qin[k % 2][0], outs)
             if tail:
-                cmps = ctx.compare(evk, outs, coeffs, cmps)
+                cmps = ctx.compare(evk, outs, coeffs, cmps, out_limbs=out_limbs)
                 if args.scenario == "membership":
                     mem = ctx.membership(evk, cmps, mem)
             for i, o in enumerate(results()):
@@ -548,7 +551,7 @@ def main():
         torch.cuda.synchronize()
         e0.record(stream)
         for _ in range(reps):
-            cmps = ctx.compare(evk, outs, coeffs, cmps)
+            cmps = ctx.compare(evk, outs, coeffs, cmps, out_limbs=out_limbs)
         e1.record(stream)
         if args.scenario == "membership":
             for _ in range(reps):

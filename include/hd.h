@@ -315,6 +315,12 @@ hd_status hd_chebyshev_coefficients(double delta, uint32_t degree, double *coeff
  * (Alg. index) = hd_compare over the hd_query outputs. */
 hd_status hd_compare(hd_context *ctx, const hd_eval_keys *evk, const hd_ciphertext *const *in, size_t count,
                      const double *coeffs, uint32_t degree, hd_ciphertext **out);
+/* As hd_compare with the result at out_limbs limbs (hd_compare: 1).  A membership sum over many
+ * slots needs out_limbs = 2: the sum of up to 2^20 values near 1 at scale 2^45 exceeds q_0 / 2
+ * (R29; the membership scenario therefore runs at num_limbs = 7).  HD_E_LEVEL if the input
+ * has too few limbs for the degree at that output level. */
+hd_status hd_compare_ex(hd_context *ctx, const hd_eval_keys *evk, const hd_ciphertext *const *in, size_t count,
+                        const double *coeffs, uint32_t degree, uint32_t out_limbs, hd_ciphertext **out);
 /* Rotation steps of the membership RotateAndSum: 1, 2, 4, ..., numSlots / 2. */
 hd_status hd_membership_steps(const hd_context *ctx, int32_t *steps, size_t cap, size_t *count);
 /* Membership (Alg. membership, Alg. gpu-bsgs-membership): the sum

@@ -37,7 +37,7 @@ ABI_FUNCTIONS = [
     "hd_enroll_ex", "hd_rotation_steps_ex", "hd_prerotation_steps", "hd_database_prerotate",
     "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
     "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch", "hd_eval_add_many", "hd_baby_steps",
-    "hd_query_baby", "hd_database_aggregate",
+    "hd_query_baby", "hd_database_aggregate", "hd_compare_ex",
 ]
 
 
@@ -147,6 +147,7 @@ def load():
             L.hd_baby_steps.argtypes = [VP, VP, VP, VP, C.c_uint32, C.c_uint32, VP]
             L.hd_query_baby.argtypes = [VP, VP, VP, VP, VP, C.c_size_t]
             L.hd_database_aggregate.argtypes = [VP, VP, C.POINTER(VP)]
+            L.hd_compare_ex.argtypes = [VP, VP, VP, C.c_size_t, VP, C.c_uint32, C.c_uint32, VP]
             _lib = L
         return _lib
 
@@ -349,14 +350,15 @@ class Context(_Handle):
         return db
 
     # -- encrypted comparison and scenario tail (NEXT-3, R29) ---------------------------------
-    def compare(self, evk, cts, coeffs, outs=None):
-        """hd_compare: ChebyshevCompare of every ciphertext (identification, Alg. index)."""
+    def compare(self, evk, cts, coeffs, outs=None, out_limbs=1):
+        """hd_compare_ex: ChebyshevCompare of every ciphertext (identification, Alg. index)."""
         coeffs = np.ascontiguousarray(coeffs, dtype=np.float64)
         if outs is None:
             outs = [None] * len(cts)
         src = (VP * len(cts))(*[c.h for c in cts])
         arr = (VP * len(cts))(*[(o.h if o is not None else None) for o in outs])
-        _check("hd_compare", load().hd_compare(self.h, evk.h, src, len(cts), _ptr(coeffs), len(coeffs) - 1, arr))
+        _check("hd_compare_ex", load().hd_compare_ex(self.h, evk.h, src, len(cts), _ptr(coeffs), len(coeffs) - 1,
+                                                     out_limbs, arr))
         return [o if o is not None else Ciphertext(arr[i], self) for i, o in enumerate(outs)]
 
     def membership_steps(self):

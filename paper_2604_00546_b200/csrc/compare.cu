@@ -420,13 +420,24 @@ extern "C" hd_status hd_chebyshev_coefficients(double delta, uint32_t degree, do
   return HD_OK;
 }
 
+extern "C" hd_status hd_compare_ex(hd_context *c, const hd_eval_keys *evk, const hd_ciphertext *const *in,
+                                   size_t count, const double *coeffs, uint32_t degree, uint32_t out_limbs,
+                                   hd_ciphertext **out);
+
 extern "C" hd_status hd_compare(hd_context *c, const hd_eval_keys *evk, const hd_ciphertext *const *in, size_t count,
                                 const double *coeffs, uint32_t degree, hd_ciphertext **out) {
+  return hd_compare_ex(c, evk, in, count, coeffs, degree, 1, out);
+}
+
+extern "C" hd_status hd_compare_ex(hd_context *c, const hd_eval_keys *evk, const hd_ciphertext *const *in,
+                                   size_t count, const double *coeffs, uint32_t degree, uint32_t out_limbs,
+                                   hd_ciphertext **out) {
   uint32_t ell = 0;
   double scale = 0.0;
   hd_status s = check_inputs(c, in, count, ell, scale);
   if (s) return s;
   if (!evk || !coeffs || !out || degree < 1) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  if (out_limbs < 1 || out_limbs >= ell) return hd_fail(HD_E_LEVEL, "out_limbs must be in [1, input limbs)");
   if (evk->ctx != c) return hd_fail(HD_E_STATE, "keys from another context");
   const uint64_t *rk = evk->find(HD_RELIN_STEP);
   if (!rk) return hd_fail(HD_E_MISSING_KEY, "missing relinearisation key (hd_relin_keygen)");
@@ -457,9 +468,10 @@ extern "C" hd_status hd_compare(hd_context *c, const hd_eval_keys *evk, const hd
     while (!E.err && (d1 << P.G.size()) <= (int)degree) P.G.push_back(E.two_ab_minus(P.G.back(), P.G.back(), nullptr, 1.0));
     // Step 3: chunks and the Chebyshev-basis combination (R29)
     Val V;
-    if (!E.err) V = P.eval(cf, (int)degree, 1);  // the result at one limb (q_0)
+    if (!E.err) V = P.eval(cf, (int)degree, (int)out_limbs);  // the result at out_limbs limbs (R29)
     if (E.err) return E.err;
     if (!V.is_ct) return hd_fail(HD_E_INVALID_ARG, "constant series: nothing to evaluate");
+    if (V.ct.ell < (int)out_limbs) return hd_fail(HD_E_LEVEL, "not enough limbs for the requested output level");
     if (V.ct.lay != V.ct.ell) {  // a MatchLevel view: materialise before the copy-out
       Lin id{};
       for (int l = 0; l < c->L; l++) id.ka[l] = 1;

@@ -184,3 +184,50 @@ def test_compare_low_degrees_bit_exact(run, n):
     with pytest.raises(hd.HDError) as e:
         run.ctx.compare(run.evk, run.outs, np.array([1.0, 0.0, 0.0]))
     assert e.value.code == -1
+
+
+@pytest.mark.slow
+def test_membership_at_bench_configuration():
+    """`bench.py --scenario membership --packing flat` configuration (2^16 ring, 2^20 x 512, L = 7,
+    n1 = 128, 32 aggregates compared in one batch to 2 limbs): every slot of the membership ciphertext
+    decrypts to the sum over all 2^20 vectors of the Chebyshev series of their cosine (a
+    property that holds at any size; the ciphertext bits are pinned on the smaller configs)."""
+    cfg = dataclasses.replace(CONFIGS["C4"], limbs=7)   # membership keeps 2 limbs for its sum (R29)
+    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
+    db_vecs, q, _ = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    steps = sorted(set(int(s) for s in ctx.rotation_steps(cfg.dim, cfg.n1, packing="flat"))
+                   | set(int(s) for s in ctx.membership_steps()))
+    sk, evk = ctx.keygen(np.array(steps, np.int32))
+    ctx.relin_keygen(sk, evk)
+    db = ctx.enroll(db_vecs, cfg.n1, packing="flat")
+    outs = ctx.query(evk, db, ctx.encrypt_query(sk, q, ENC_SEED_BASE))
+    c = hd.chebyshev_coefficients(0.5, 13)
+    cmp = ctx.compare(evk, outs, c, out_limbs=2)
+    mem = ctx.membership(evk, cmp)
+    torch.cuda.synchronize()
+    assert len(cmp) == 32 and cmp[0].limbs == 2 and mem.limbs == 2
+    z = ctx.decrypt_slots(sk, mem)
+    cos = _cos(db_vecs, q)
+    pad = len(cmp) * ctx.ns - cfg.num_vectors
+    total = npcheb.chebval(cos, c).sum() + pad * npcheb.chebval(0.0, c)
+    assert np.abs(z - total).max() < 1e-3 * max(1.0, abs(total))
+    # identification on a sampled aggregate: slot v of comparison a = chebval(cos of vector a M N + v)
+    a = 13
+    zs = ctx.decrypt_slots(sk, cmp[a])
+    assert np.abs(zs - npcheb.chebval(cos[a * ctx.ns:(a + 1) * ctx.ns], c)).max() < 1e-5
+
+
+
+def test_compare_to_two_limbs_bit_exact(run):
+    """hd_compare_ex with out_limbs = 2 (the membership headroom, R29): degree 5 from 5 limbs,
+    bit-exact vs the oracle; a request the levels cannot meet is HD_E_LEVEL."""
+    c = hd.chebyshev_coefficients(0.5, 5)
+    cmp = run.ctx.compare(run.evk, run.outs, c, out_limbs=2)
+    torch.cuda.synchronize()
+    for got, ref in zip(cmp, run.ref_outs):
+        want, scale = run.o.cheb_compare(ref, D45, c, run.rlk, out_limbs=2)
+        assert got.limbs == 2 and (run.ctx.ciphertext_residues(got) == want).all()
+        assert run.ctx.ciphertext_scale(got) == scale
+    with pytest.raises(hd.HDError) as e:
+        run.ctx.compare(run.evk, run.outs, hd.chebyshev_coefficients(0.5, 13), out_limbs=2)
+    assert e.value.code == -6
