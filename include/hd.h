@@ -20,7 +20,11 @@
  *   - or the server thresholds them first (encrypted comparison, identification and
  *     membership tails; NEXT-3)
  *                                                     -> hd_chebyshev_coefficients,
- *                                                        hd_compare, hd_membership
+ *                                                        hd_compare(_ex), hd_membership
+ *   - serving variants (NEXT-4): several queries per call, the online-aggregated
+ *     database (Alg. online-aggr) -> hd_query_batch, hd_database_aggregate
+ *   - sharded scans over P GPUs: baby-step slices + all-gather
+ *                                                     -> hd_baby_steps, hd_query_baby
  *
  * Conventions
  *   - Every function returns hd_status (HD_OK = 0).  No C++ exception crosses the
