@@ -520,9 +520,13 @@ def main():
         step()
     torch.cuda.synchronize()
     ctx.query_stats()
+    l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0.record(stream)
     for _ in range(3):
         step()
+    l1.record(stream)
     torch.cuda.synchronize()
+    latency_ms = l0.elapsed_time(l1) / 3  # one step alone on one stream: the per-query latency
     phase_serial = ctx.query_stats()
     os.environ.pop("HD_SERIAL")
     # ---- key-switch HBM stream (north-star metric): the batched baby-step key inner product ----
@@ -586,7 +590,7 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": mac_bytes, "avg_launch_ms": mac_avg_ms},
             "keyswitch": keyswitch, "query_roofline": query_roofline, "tail_ms": tail_ms,
-            "scenario": args.scenario, "queries_per_step": Q, "split_baby": split is not None,
+            "latency_ms_serial": latency_ms, "scenario": args.scenario, "queries_per_step": Q, "split_baby": split is not None,
             "online_aggregate": None if aggr_s is None else {"setup_s": aggr_s, "note": "Alg. online-aggr: the "
                                 "scan runs over one aggregate holding the sum of all diagonals"},
             "clocks": clocks, "e2e": e2e}
