@@ -66,3 +66,30 @@ def test_host_chebyshev_coefficients_match_the_oracle(oracle_mod):
         hd.chebyshev_degree(6)
     for delta, n in ((0.5, 13), (-0.2, 5), (0.0, 27), (0.75, 59)):
         assert (hd.chebyshev_coefficients(delta, n) == oracle_mod.cheb_coeffs(delta, n)).all()
+
+
+def test_host_chebyshev_error_paths():
+    """Client-side host calls reject bad arguments (no device involved)."""
+    import ctypes as C
+
+    import numpy as np
+    import paper_2604_00546_b200 as hd
+    L = hd.load()
+    buf = np.zeros(4, np.float64)
+    assert L.hd_chebyshev_coefficients(C.c_double(0.5), 13, buf.ctypes.data_as(C.c_void_p), 4) == -1  # cap
+    assert L.hd_chebyshev_coefficients(C.c_double(0.5), 0, buf.ctypes.data_as(C.c_void_p), 4) == -1   # degree 0
+    d = C.c_uint32()
+    assert L.hd_chebyshev_degree(11, C.byref(d)) == -1 and L.hd_chebyshev_degree(8, C.byref(d)) == 0
+    assert d.value == 13
+
+
+def test_baby_slices_cover_every_step_once():
+    from paper_2604_00546_b200 import dist as hdd
+    for n1 in (1, 7, 8, 23, 128):
+        for world in (1, 2, 3, 4, 8):
+            got = []
+            for r in range(world):
+                chunk, i0, i1 = hdd.baby_slice(n1, r, world)
+                assert 0 <= i1 - i0 <= chunk and chunk * world >= n1
+                got += list(range(i0, i1))
+            assert got == list(range(n1))
