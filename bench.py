@@ -154,7 +154,7 @@ def workload_cfg(args):
     cfg = CONFIGS[args.config]
     # comparison scenarios: degree 13 needs 4 levels after the scan; membership keeps 2 limbs of
     # headroom for its sum over all slots (R29) -> 6 limbs for identification, 7 for membership
-    limbs = args.limbs or {"scan": cfg.limbs, "identification": 6, "membership": 7}[args.scenario]
+    limbs = args.limbs or {"scan": cfg.limbs, "identification": 6, "membership": 6}[args.scenario]
     if limbs != cfg.limbs:
         cfg = dataclasses.replace(cfg, limbs=limbs)
     if args.n1 and args.n1 != cfg.n1:
@@ -294,7 +294,17 @@ def main():
     if args.scenario == "membership":  # + the power-of-two keys of RotateAndSum
         steps = np.array(sorted(set(int(s) for s in steps) | set(int(s) for s in ctx.membership_steps())), np.int32)
     coeffs = hd.chebyshev_coefficients(args.delta, hd.chebyshev_degree(args.kappa)) if tail else None
-    out_limbs = 2 if args.scenario == "membership" else 1  # the membership sum's headroom (R29)
+    # membership headroom (R29): the sum over all slots of values near 1 at scale 2^45 must stay
+    # below q_0 / 2 ~ 2^59 at one limb -> the client scales the series by 2^-COUNT_SHIFT (the
+    # count decodes / 2^COUNT_SHIFT); with 7 limbs, --membership-limbs 2 keeps the exact count
+    out_limbs, count_shift = 1, 0
+    if args.scenario == "membership":
+        slots_total = A * cfg.num_slots
+        if cfg.limbs >= 7:
+            out_limbs = 2
+        else:
+            count_shift = max(0, int(np.ceil(np.log2(1.25 * slots_total))) + 45 - 58)
+            coeffs = coeffs * 2.0 ** -count_shift
     if rank == 0:
         sk, evk = ctx.keygen(steps)
         if enc_db or tail:  # relinearisation key travels with the eval keys (reserved step 0)
@@ -590,7 +600,8 @@ def main():
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": mac_bytes, "avg_launch_ms": mac_avg_ms},
             "keyswitch": keyswitch, "query_roofline": query_roofline, "tail_ms": tail_ms,
-            "latency_ms_serial": latency_ms, "scenario": args.scenario, "queries_per_step": Q, "split_baby": split is not None,
+            "latency_ms_serial": latency_ms, "scenario": args.scenario, "queries_per_step": Q,
+            "membership_count_shift": count_shift if args.scenario == "membership" else None, "split_baby": split is not None,
             "online_aggregate": None if aggr_s is None else {"setup_s": aggr_s, "note": "Alg. online-aggr: the "
                                 "scan runs over one aggregate holding the sum of all diagonals"},
             "clocks": clocks, "e2e": e2e}

@@ -319,10 +319,11 @@ hd_status hd_chebyshev_coefficients(double delta, uint32_t degree, double *coeff
  * (Alg. index) = hd_compare over the hd_query outputs. */
 hd_status hd_compare(hd_context *ctx, const hd_eval_keys *evk, const hd_ciphertext *const *in, size_t count,
                      const double *coeffs, uint32_t degree, hd_ciphertext **out);
-/* As hd_compare with the result at out_limbs limbs (hd_compare: 1).  A membership sum over many
- * slots needs out_limbs = 2: the sum of up to 2^20 values near 1 at scale 2^45 exceeds q_0 / 2
- * (R29; the membership scenario therefore runs at num_limbs = 7).  HD_E_LEVEL if the input
- * has too few limbs for the degree at that output level. */
+/* As hd_compare with the result at out_limbs limbs (hd_compare: 1).  A membership sum over S
+ * slots of values near 1 at scale 2^45 must stay below q_0 / 2 ~ 2^59 (R29): either the client
+ * scales the coefficients by 2^-k with 2^(45-k) S < 2^58 (k = 8 for 2^20 slots; the count
+ * decodes / 2^k; bench.py's default) or the comparison keeps out_limbs = 2 (num_limbs = 7).
+ * HD_E_LEVEL if the input has too few limbs for the degree at that output level. */
 hd_status hd_compare_ex(hd_context *ctx, const hd_eval_keys *evk, const hd_ciphertext *const *in, size_t count,
                         const double *coeffs, uint32_t degree, uint32_t out_limbs, hd_ciphertext **out);
 /* Rotation steps of the membership RotateAndSum: 1, 2, 4, ..., numSlots / 2. */

@@ -25,11 +25,11 @@ def test_reference_arm_json_line():
 
 
 def test_reference_arm_membership_scenario():
-    """NEXT-3: membership runs at seven limbs (its sum keeps two) and names the tail in the metric."""
+    """NEXT-3: the comparison scenarios run at six limbs and name the tail in the metric."""
     out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "C1",
                           "--steps", "1", "--warmup", "0", "--scenario", "membership"], capture_output=True, text=True,
                          timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
-    assert "membership" in d["metric"] and d["config"]["limbs"] == 7 and d["value"] > 0   # 2-limb headroom
+    assert "membership" in d["metric"] and d["config"]["limbs"] == 6 and d["value"] > 0
     assert "ChebyshevCompare" in d["cpu_baseline"]["sample"]

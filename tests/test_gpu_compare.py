@@ -231,3 +231,27 @@ def test_compare_to_two_limbs_bit_exact(run):
     with pytest.raises(hd.HDError) as e:
         run.ctx.compare(run.evk, run.outs, hd.chebyshev_coefficients(0.5, 13), out_limbs=2)
     assert e.value.code == -6
+
+
+
+@pytest.mark.slow
+def test_membership_at_bench_configuration_scaled_count():
+    """The bench's membership at L = 6: the client scales the series by 2^-8 so the 2^20-slot sum
+    stays below q_0 / 2 at one limb (R29); the decrypted total times 2^8 is the count."""
+    cfg = dataclasses.replace(CONFIGS["C4"], limbs=6)
+    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
+    db_vecs, q, _ = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    steps = sorted(set(int(s) for s in ctx.rotation_steps(cfg.dim, cfg.n1, packing="flat"))
+                   | set(int(s) for s in ctx.membership_steps()))
+    sk, evk = ctx.keygen(np.array(steps, np.int32))
+    ctx.relin_keygen(sk, evk)
+    db = ctx.enroll(db_vecs, cfg.n1, packing="flat")
+    outs = ctx.query(evk, db, ctx.encrypt_query(sk, q, ENC_SEED_BASE))
+    c = hd.chebyshev_coefficients(0.5, 13)
+    mem = ctx.membership(evk, ctx.compare(evk, outs, c * 2.0 ** -8))
+    torch.cuda.synchronize()
+    assert mem.limbs == 1
+    z = ctx.decrypt_slots(sk, mem) * 2.0 ** 8
+    cos = _cos(db_vecs, q)
+    total = npcheb.chebval(cos, c).sum() + (len(outs) * ctx.ns - cfg.num_vectors) * npcheb.chebval(0.0, c)
+    assert np.abs(z - total).max() < 1e-3 * max(1.0, abs(total))
