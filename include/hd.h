@@ -332,7 +332,9 @@ hd_status hd_membership_steps(const hd_context *ctx, int32_t *steps, size_t cap,
  * of the count comparison ciphertexts (EvalAddMany), then RotateAndSum over numSlots with the
  * power-of-two keys (HD_E_MISSING_KEY if one is absent): every slot of *out holds the sum of
  * all slots of all inputs (the approximate match count).  Meaningful on the FLAT packing
- * (every slot a vector or zero padding, R29).  *out: NULL -> allocated. */
+ * (every slot a vector or zero padding, R29).  The total must stay below q_0 / 2 at the
+ * inputs' level: scale the comparison coefficients by 2^-k or keep 2 limbs (hd_compare_ex).
+ * *out: NULL -> allocated. */
 hd_status hd_membership(hd_context *ctx, const hd_eval_keys *evk, const hd_ciphertext *const *in, size_t count,
                         hd_ciphertext **out);
 /* EvalAddMany (Alg. membership): *out = sum of the count ciphertexts (same level and
