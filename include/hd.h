@@ -122,11 +122,31 @@ typedef struct {
   uint64_t enc_seed;
 } hd_enroll_options;
 
+/* ---- device memory ------------------------------------------------------ */
+/* Device allocator of a context ("PyTorch is used only for device memory";
+ * the Python binding passes the torch caching allocator).  alloc returns a device pointer
+ * of at least `bytes` on the context's device, usable on `stream` (a cudaStream_t) and on
+ * streams ordered after it, or NULL (the call then fails with HD_E_CAPACITY).  free
+ * releases a pointer alloc returned; the library calls it only once no work on any of the
+ * context's streams can still touch the memory, or for per-call temporaries on `stream`
+ * in stream order.  Both must be callable from the thread that calls libhd.  `user` is
+ * passed through.  Every device allocation of libhd goes through it (tables, keys,
+ * databases, ciphertexts, workspaces); with a NULL allocator libhd uses the device's
+ * stream-ordered pool (cudaMallocAsync / cudaFreeAsync).  Objects made by a context must
+ * be destroyed before the context (they free through its allocator). */
+typedef struct {
+  void *(*alloc)(size_t bytes, void *stream, void *user);
+  void (*free)(void *ptr, void *stream, void *user);
+  void *user;
+} hd_allocator;
+
 /* ---- context ------------------------------------------------------------ */
 /* Creates the context: moduli (R5), primitive roots (R13), NTT/FFT tables.
- * cuda_stream: cudaStream_t of the caller (NULL = default stream).            */
+ * cuda_stream: cudaStream_t of the caller (NULL = default stream); one context = one
+ * device = one caller stream, and calls on a context are serialised by the caller.
+ * allocator: copied; NULL = the device's stream-ordered pool (see hd_allocator).       */
 hd_status hd_context_create(const hd_params *params, int cuda_device, void *cuda_stream,
-                            hd_context **out);
+                            const hd_allocator *allocator, hd_context **out);
 void hd_context_destroy(hd_context *ctx);
 hd_status hd_context_set_stream(hd_context *ctx, void *cuda_stream);
 /* moduli[0..L-1] = q_i, moduli[L] = P; psi likewise (host arrays, L+1 each). */
@@ -190,6 +210,14 @@ hd_status hd_enroll_encrypted(hd_context *ctx, const hd_public_key *pk, const fl
 hd_status hd_enroll_ex(hd_context *ctx, const hd_enroll_options *opt, const float *vectors,
                        uint64_t num_vectors, uint32_t vector_dim, uint32_t n1, uint32_t agg_begin,
                        uint32_t agg_end, hd_database **out);
+/* Device bytes the database handle of this enrollment would take (diagonals plus the
+ * query workspaces), without allocating: the paper's footprint check before the upload
+ * (P:L662-664).  With the default allocator hd_enroll* performs the check itself against
+ * free device memory (HD_E_CAPACITY); with a caller allocator the caller checks this
+ * figure against what it can hand out. */
+hd_status hd_enroll_footprint(hd_context *ctx, uint64_t num_vectors, uint32_t vector_dim, uint32_t n1,
+                              uint32_t agg_begin, uint32_t agg_end, const hd_enroll_options *opt,
+                              size_t *bytes);
 hd_status hd_database_layout(const hd_database *db, hd_layout *out);
 /* Online database aggregation (NEXT-4; Alg. online-aggr, membership only): a new
  * handle with ONE aggregate whose diagonals are the sums (mod q) of the diagonals of all
@@ -254,13 +282,22 @@ hd_status hd_query_stats(const hd_context *ctx, double *phase_ms, size_t n_phase
  * dst = NULL queries the size in *written. */
 hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, size_t cap, int dst_on_device,
                                size_t *written);
+/* Imports validate untrusted input before it reaches a kernel: HD_E_FORMAT unless the
+ * magic, ring and modulus-chain fingerprint match this context, the header's payload size
+ * equals the size its shape implies and fits in `bytes`, and every residue is below its
+ * modulus (one device pass); key sets also reject rotation steps outside [0, numSlots)
+ * and duplicates.  Synchronises the context stream. */
 hd_status hd_ciphertext_import(hd_context *ctx, const void *src, size_t bytes, int src_on_device,
                                hd_ciphertext **out);
 /* In-place import into an existing ciphertext of the same shape (no allocation).
  * Host sources are uploaded asynchronously on the context's upload stream, after the
  * ciphertext's last reader (the baby steps of an hd_query on it) and last writer; pinned
  * host memory keeps the copy asynchronous and must stay valid until the ciphertext is
- * next read or hd_context_synchronize().  Device sources are copied on the context stream. */
+ * next read or hd_context_synchronize().  Device sources are copied on the context stream.
+ * Unlike hd_ciphertext_import (which checks the header's payload size and that every
+ * residue is below its modulus, HD_E_FORMAT otherwise), this hot-path call checks only the
+ * header of host sources (shape and payload size) and nothing of device sources: it never
+ * synchronises.  Feed it buffers produced by hd_ciphertext_export(_async). */
 hd_status hd_ciphertext_import_into(hd_ciphertext *ct, const void *src, size_t bytes,
                                     int src_on_device);
 hd_status hd_ciphertext_limbs(const hd_ciphertext *ct, uint32_t *limbs);

@@ -11,6 +11,7 @@ and call the ``hd_*`` functions.
 """
 from __future__ import annotations
 
+import atexit
 import ctypes as C
 import os
 import threading
@@ -37,7 +38,7 @@ ABI_FUNCTIONS = [
     "hd_enroll_ex", "hd_rotation_steps_ex", "hd_prerotation_steps", "hd_database_prerotate",
     "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
     "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch", "hd_eval_add_many", "hd_baby_steps",
-    "hd_query_baby", "hd_database_aggregate", "hd_compare_ex",
+    "hd_query_baby", "hd_database_aggregate", "hd_compare_ex", "hd_enroll_footprint",
 ]
 
 
@@ -95,7 +96,9 @@ def load():
                          "hd_secret_key_destroy", "hd_database_destroy", "hd_public_key_destroy"):
                 getattr(L, name).restype = None
                 getattr(L, name).argtypes = [VP]
-            L.hd_context_create.argtypes = [C.POINTER(Params), C.c_int, VP, C.POINTER(VP)]
+            L.hd_context_create.argtypes = [C.POINTER(Params), C.c_int, VP, C.POINTER(Allocator), C.POINTER(VP)]
+            L.hd_enroll_footprint.argtypes = [VP, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32, VP,
+                                              C.POINTER(C.c_size_t)]
             L.hd_context_set_stream.argtypes = [VP, VP]
             L.hd_context_moduli.argtypes = [VP, VP, VP, C.c_size_t]
             L.hd_rotation_steps.argtypes = [VP, C.c_uint32, C.c_uint32, VP, C.c_size_t, C.POINTER(C.c_size_t)]
@@ -157,6 +160,53 @@ def _status_string(code):
         return load().hd_status_string(code).decode()
     except Exception:  # noqa: BLE001
         return "?"
+
+
+# ---- device memory: the torch caching allocator behind hd_allocator (include/hd.h) ----------------
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_void_p, C.c_void_p)
+
+
+class Allocator(C.Structure):
+    _fields_ = [("alloc", ALLOC_FN), ("free", FREE_FN), ("user", VP)]
+
+
+_ALLOCATORS = {}    # device -> Allocator (the ctypes callbacks must outlive every context)
+_FINALIZING = False  # at interpreter exit frees become no-ops (the process releases the memory)
+
+
+def _at_exit():
+    global _FINALIZING
+    _FINALIZING = True
+
+
+atexit.register(_at_exit)
+
+
+def torch_allocator(device: int) -> Allocator:
+    """hd_allocator over torch.cuda.caching_allocator_alloc/delete on ``device``: libhd's
+    device memory then lives in (and is accounted by) PyTorch's caching allocator."""
+    if device in _ALLOCATORS:
+        return _ALLOCATORS[device]
+    import torch
+
+    def _alloc(nbytes, stream, _user):
+        try:
+            return torch.cuda.caching_allocator_alloc(int(nbytes), device=device, stream=int(stream or 0))
+        except Exception:  # noqa: BLE001  (out of memory -> NULL -> HD_E_CAPACITY)
+            return None
+
+    def _free(ptr, _stream, _user):
+        if _FINALIZING or not ptr:
+            return
+        try:
+            torch.cuda.caching_allocator_delete(int(ptr))
+        except Exception:  # noqa: BLE001
+            pass
+
+    a = Allocator(ALLOC_FN(_alloc), FREE_FN(_free), None)
+    _ALLOCATORS[device] = a
+    return a
 
 
 def _check(fn, rc):
@@ -229,13 +279,19 @@ class Context(_Handle):
 
     _destroy = "hd_context_destroy"
 
-    def __init__(self, log_n, limbs=3, seed=1, device=0, stream=None, scale_bits=45, q0_bits=60):
+    def __init__(self, log_n, limbs=3, seed=1, device=0, stream=None, scale_bits=45, q0_bits=60,
+                 allocator="torch"):
+        """allocator: "torch" (default: PyTorch's caching allocator owns libhd's device
+        memory) or None (libhd's default, the device's stream-ordered pool)."""
         p = Params(log_n=log_n, num_limbs=limbs, q0_bits=q0_bits, scale_bits=scale_bits,
                    special_bits=q0_bits, num_special=1, digit_limbs=1, reserved=0, seed=seed)
         h = VP()
+        alloc = C.byref(torch_allocator(device)) if allocator == "torch" else None
         _check("hd_context_create", load().hd_context_create(C.byref(p), device, _stream_handle(stream),
-                                                             C.byref(h)))
+                                                             alloc, C.byref(h)))
         super().__init__(h.value)
+        self.device = device
+        self.allocator = allocator
         self.log_n, self.L, self.n, self.ns = log_n, limbs, 1 << log_n, 1 << (log_n - 1)
 
     def set_stream(self, stream):
@@ -288,9 +344,33 @@ class Context(_Handle):
         return out
 
     # -- enroller / server ---------------------------------------------------------------------------
+    def enroll_footprint(self, num_vectors, vector_dim, n1, agg_begin=0, agg_end=0, packing="replicated",
+                         encrypted=False):
+        """hd_enroll_footprint: device bytes of the database handle (P:L662-664 pre-check)."""
+        opt = EnrollOptions(PACKING[packing], 0, VP(1) if encrypted else None, 0)  # only pk != NULL matters
+        b = C.c_size_t()
+        _check("hd_enroll_footprint", load().hd_enroll_footprint(self.h, num_vectors, vector_dim, n1, agg_begin,
+                                                                 agg_end, C.byref(opt), C.byref(b)))
+        return b.value
+
+    def _precheck(self, num_vectors, vector_dim, n1, agg_begin, agg_end, packing, encrypted):
+        """The paper's footprint check before the upload against what the torch
+        allocator can hand out: free device memory plus its own cached, unused blocks."""
+        if self.allocator != "torch":
+            return  # libhd checks against free device memory itself
+        import torch
+        need = self.enroll_footprint(num_vectors, vector_dim, n1, agg_begin, agg_end, packing, encrypted)
+        free = torch.cuda.mem_get_info(self.device)[0]
+        cached = torch.cuda.memory_reserved(self.device) - torch.cuda.memory_allocated(self.device)
+        if need + (256 << 20) > free + cached:
+            raise HDError("hd_enroll_footprint", HD_E_CAPACITY,
+                          f"database of {need >> 20} MiB exceeds available device memory "
+                          f"({(free + cached) >> 20} MiB); shard the aggregates over more GPUs")
+
     def enroll(self, vectors, n1, agg_begin=0, agg_end=0, packing="replicated", pk=None, enc_seed=0):
         """hd_enroll_ex: plaintext (pk None) or encrypted (NEXT-1) diagonals, replicated or flat (NEXT-2)."""
         vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+        self._precheck(vectors.shape[0], vectors.shape[1], n1, agg_begin, agg_end, packing, pk is not None)
         opt = EnrollOptions(PACKING[packing], 0, pk.h if pk is not None else None, enc_seed)
         out = VP()
         _check("hd_enroll_ex", load().hd_enroll_ex(self.h, C.byref(opt), _ptr(vectors), vectors.shape[0],
@@ -341,6 +421,7 @@ class Context(_Handle):
 
     def enroll_encrypted(self, pk, vectors, n1, enc_seed, agg_begin=0, agg_end=0):
         vectors = np.ascontiguousarray(vectors, dtype=np.float32)
+        self._precheck(vectors.shape[0], vectors.shape[1], n1, agg_begin, agg_end, "replicated", True)
         out = VP()
         _check("hd_enroll_encrypted", load().hd_enroll_encrypted(
             self.h, pk.h, _ptr(vectors), vectors.shape[0], vectors.shape[1], n1, agg_begin, agg_end,

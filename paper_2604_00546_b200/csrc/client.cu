@@ -285,8 +285,8 @@ extern "C" hd_status hd_keygen(hd_context *c, const int32_t *steps, size_t count
     hd_eval_keys_destroy(evk);
     return s;
   };
-  cudaError_t e = cudaMalloc(&sk->s_ntt, (size_t)(L + 1) * n * 8);
-  if (!e && count) e = cudaMalloc(&evk->keys, evk->key_elems * count * 8);
+  cudaError_t e = dev_alloc(c, &sk->s_ntt, (size_t)(L + 1) * n * 8);
+  if (!e && count) e = dev_alloc(c, &evk->keys, evk->key_elems * count * 8);
   if (e) return fail(hd_fail(HD_E_CAPACITY, cudaGetErrorString(e)));
   const uint64_t seed = c->params.seed;
   secret_kernel<<<(n + TPB - 1) / TPB, TPB, 0, c->stream>>>(seed, n, L + 1, sk->s_ntt, c->mt); ++c->launches;
@@ -334,10 +334,10 @@ extern "C" hd_status hd_encrypt_query(hd_context *c, const hd_secret_key *sk, co
   hd_ciphertext *ct = nullptr;
   hd_status s = alloc_ct(c, L, &ct);
   if (s) return s;
-  cudaError_t e = cudaMalloc(&dq, N * 4);
-  if (!e) e = cudaMalloc(&U, N * 8);
-  if (!e) e = cudaMalloc(&re, (size_t)ns * 8);
-  if (!e) e = cudaMalloc(&im, (size_t)ns * 8);
+  cudaError_t e = dev_alloc(c, &dq, N * 4);
+  if (!e) e = dev_alloc(c, &U, N * 8);
+  if (!e) e = dev_alloc(c, &re, (size_t)ns * 8);
+  if (!e) e = dev_alloc(c, &im, (size_t)ns * 8);
   if (!e) e = cudaMemcpyAsync(dq, q, N * 4, cudaMemcpyHostToDevice, c->stream);
   if (e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
   if (!s) s = normalize_on_device(c, dq, 1, N, U);
@@ -359,10 +359,10 @@ extern "C" hd_status hd_encrypt_query(hd_context *c, const hd_secret_key *sk, co
     enc_combine_kernel<<<dim3((n + TPB - 1) / TPB, L), TPB, 0, c->stream>>>(enc_seed, n, L, sk->s_ntt, ct->data, c->mt); ++c->launches;
     s = check_flag(c);
   }
-  cudaFree(dq);
-  cudaFree(U);
-  cudaFree(re);
-  cudaFree(im);
+  dev_free(c, dq);
+  dev_free(c, U);
+  dev_free(c, re);
+  dev_free(c, im);
   if (s) {
     hd_ciphertext_destroy(ct);
     return s;
@@ -387,11 +387,11 @@ extern "C" hd_status hd_decrypt(hd_context *c, const hd_secret_key *sk, const hd
   const size_t need = (size_t)ct->limbs * c->n;
   if (cap < need) return hd_fail(HD_E_INVALID_ARG, "capacity too small");
   uint64_t *m;
-  HD_CUDA(cudaMalloc(&m, need * 8));
+  HD_CUDA(dev_alloc(c, &m, need * 8));
   hd_status s = decrypt_to(c, sk, ct, m);
   cudaError_t e = cudaMemcpyAsync(pt_host, m, need * 8, cudaMemcpyDeviceToHost, c->stream);
   if (!e) e = cudaStreamSynchronize(c->stream);
-  cudaFree(m);
+  dev_free(c, m);
   if (!s && e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
   return s;
 }
@@ -438,10 +438,10 @@ extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, c
   uint64_t *m = nullptr;
   double *re = nullptr, *im = nullptr, *dsc = nullptr;
   const size_t nsc = (size_t)(v_end - v_first);
-  cudaError_t e = cudaMalloc(&m, (size_t)nl * n * 8);
-  if (!e) e = cudaMalloc(&re, (size_t)ns * 8);
-  if (!e) e = cudaMalloc(&im, (size_t)ns * 8);
-  if (!e) e = cudaMalloc(&dsc, nsc * 8);
+  cudaError_t e = dev_alloc(c, &m, (size_t)nl * n * 8);
+  if (!e) e = dev_alloc(c, &re, (size_t)ns * 8);
+  if (!e) e = dev_alloc(c, &im, (size_t)ns * 8);
+  if (!e) e = dev_alloc(c, &dsc, nsc * 8);
   hd_status s = e ? hd_fail(HD_E_CUDA, cudaGetErrorString(e)) : HD_OK;
   const double delta = std::ldexp(1.0, (int)c->params.scale_bits);
   RowMap rm{};
@@ -465,10 +465,10 @@ extern "C" hd_status hd_decrypt_scores(hd_context *c, const hd_secret_key *sk, c
     if (!e) e = cudaStreamSynchronize(c->stream);
     if (e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
   }
-  cudaFree(m);
-  cudaFree(re);
-  cudaFree(im);
-  cudaFree(dsc);
+  dev_free(c, m);
+  dev_free(c, re);
+  dev_free(c, im);
+  dev_free(c, dsc);
   if (!s && written) *written = nsc;
   return s;
 }
@@ -483,9 +483,9 @@ extern "C" hd_status hd_decrypt_slots(hd_context *c, const hd_secret_key *sk, co
   const CrtTab ctab = crt_table(c, nl);
   uint64_t *m = nullptr;
   double *re = nullptr, *im = nullptr;
-  cudaError_t e = cudaMalloc(&m, (size_t)nl * n * 8);
-  if (!e) e = cudaMalloc(&re, (size_t)ns * 8);
-  if (!e) e = cudaMalloc(&im, (size_t)ns * 8);
+  cudaError_t e = dev_alloc(c, &m, (size_t)nl * n * 8);
+  if (!e) e = dev_alloc(c, &re, (size_t)ns * 8);
+  if (!e) e = dev_alloc(c, &im, (size_t)ns * 8);
   hd_status s = e ? hd_fail(HD_E_CUDA, cudaGetErrorString(e)) : HD_OK;
   RowMap rm{};
   rm.gsize = 1u << 30;
@@ -505,9 +505,9 @@ extern "C" hd_status hd_decrypt_slots(hd_context *c, const hd_secret_key *sk, co
     if (!e) e = cudaStreamSynchronize(c->stream);
     if (e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
   }
-  cudaFree(m);
-  cudaFree(re);
-  cudaFree(im);
+  dev_free(c, m);
+  dev_free(c, re);
+  dev_free(c, im);
   return s;
 }
 
@@ -531,7 +531,7 @@ extern "C" hd_status hd_public_keygen(hd_context *c, const hd_secret_key *sk, hd
   HD_CUDA(cudaSetDevice(c->device));
   const int n = c->n, L = c->L;
   hd_public_key *pk = new hd_public_key{c, nullptr};
-  if (cudaMalloc(&pk->pk, (size_t)2 * L * n * 8) != cudaSuccess) {
+  if (dev_alloc(c, &pk->pk, (size_t)2 * L * n * 8) != cudaSuccess) {
     delete pk;
     return hd_fail(HD_E_CAPACITY, "public key alloc");
   }
@@ -552,7 +552,7 @@ extern "C" hd_status hd_public_keygen(hd_context *c, const hd_secret_key *sk, hd
 
 extern "C" void hd_public_key_destroy(hd_public_key *pk) {
   if (!pk) return;
-  cudaFree(pk->pk);
+  dev_free(pk->ctx, pk->pk);
   delete pk;
 }
 
@@ -572,7 +572,7 @@ extern "C" hd_status hd_public_key_import(hd_context *c, const uint64_t *src, si
   for (size_t i = 0; i < need; i++)
     if (src[i] >= c->mod[(i / c->n) % c->L]) return hd_fail(HD_E_FORMAT, "public key residue out of range");
   hd_public_key *pk = new hd_public_key{c, nullptr};
-  if (cudaMalloc(&pk->pk, need * 8) != cudaSuccess) {
+  if (dev_alloc(c, &pk->pk, need * 8) != cudaSuccess) {
     delete pk;
     return hd_fail(HD_E_CAPACITY, "public key alloc");
   }
@@ -592,7 +592,7 @@ extern "C" hd_status hd_relin_keygen(hd_context *c, const hd_secret_key *sk, hd_
   const int n = c->n, L = c->L;
   const size_t cnt = evk->steps.size(), ke = (size_t)L * 2 * (L + 1) * n;
   uint64_t *keys = nullptr;
-  if (cudaMalloc(&keys, ke * (cnt + 1) * 8) != cudaSuccess) return hd_fail(HD_E_CAPACITY, "relinearisation key alloc");
+  if (dev_alloc(c, &keys, ke * (cnt + 1) * 8) != cudaSuccess) return hd_fail(HD_E_CAPACITY, "relinearisation key alloc");
   if (cnt) HD_CUDA(cudaMemcpyAsync(keys, evk->keys, ke * cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
   uint64_t *key = keys + ke * cnt;
   const uint64_t seed = c->params.seed;
@@ -600,7 +600,7 @@ extern "C" hd_status hd_relin_keygen(hd_context *c, const hd_secret_key *sk, hd_
   RowMap rk = limb_rows(L + 1, L + 1, (uint64_t)2 * (L + 1) * n);  // rows (d, l) of the b halves
   hd_status s = ntt_rows(c, key, L * (L + 1), rk, false);
   if (s) {
-    cudaFree(keys);
+    dev_free(c, keys);
     return s;
   }
   InvTab2 pmod{};
@@ -608,12 +608,13 @@ extern "C" hd_status hd_relin_keygen(hd_context *c, const hd_secret_key *sk, hd_
   key_combine_kernel<<<dim3((n + TPB - 1) / TPB, L * (L + 1)), TPB, 0, c->stream>>>(
       seed, 0, TAG_RLK_A, 0, c->logn, L, sk->s_ntt, key, c->mt, pmod); ++c->launches;
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
-    cudaFree(keys);
+    dev_free(c, keys);
     return hd_fail(HD_E_CUDA, "relinearisation keygen");
   }
-  cudaFree(evk->keys);
+  dev_free(c, evk->keys);
   evk->keys = keys;
   evk->key_elems = ke;
+  evk->gen = hd_next_generation();  // invalidates every database's cached key pointers
   evk->steps.push_back(HD_RELIN_STEP);
   return HD_OK;
 }

@@ -194,18 +194,48 @@ constexpr static int kPhaseEvents = 9;
   cudaStream_t sA = nullptr, sB = nullptr;  // internal streams of the query pipeline
   cudaStream_t sIO = nullptr;               // device->host result downloads (export_async)
   cudaStream_t sUp = nullptr;               // host->device uploads (import_into from host)
+  // Device memory: the caller's allocator (the torch caching allocator in the
+  // Python binding) or, without one, the device's stream-ordered pool (cudaMallocAsync).
+  hd_allocator alloc{};
+  bool has_alloc = false;
+  // Stream-ordered workspace cache for per-call temporaries (hd_compare): blocks freed by a
+  // call are reused by the next one on the same stream without touching the allocator.
+  struct WsBlock {
+    void *p;
+    size_t bytes;
+    cudaStream_t stream;
+  };
+  std::vector<WsBlock> ws_free;
 };
+
+// Every device allocation of the library goes through these (no other cudaMalloc).
+// dev_alloc / dev_free: long-lived objects; dev_free first waits for the context's streams
+// (the memory may still be read by the query pipeline).  ws_alloc / ws_free: stream-ordered
+// temporaries of one call on c->stream, cached per context (never returned mid-run).
+cudaError_t dev_alloc(hd_context *c, void **p, size_t bytes);
+void dev_free(hd_context *c, void *p);
+void *ws_alloc(hd_context *c, size_t bytes);
+void ws_free(hd_context *c, void *p, size_t bytes);
+template <class T>
+static inline cudaError_t dev_alloc(hd_context *c, T **p, size_t bytes) {
+  return dev_alloc(c, reinterpret_cast<void **>(p), bytes);
+}
 
 struct hd_secret_key {
   hd_context *ctx;
   uint64_t *s_ntt;  // [(L+1)][n]
 };
 
+// process-unique generation ids: a key set gets a fresh one whenever its storage is
+// (re)allocated, so caches keyed on it never outlive the storage (no address ABA)
+uint64_t hd_next_generation();
+
 struct hd_eval_keys {
   hd_context *ctx;
   std::vector<int32_t> steps;
   uint64_t *keys = nullptr;  // [count][L][2][L+1][n]
   size_t key_elems = 0;      // per key
+  uint64_t gen = hd_next_generation();
   const uint64_t *find(int32_t step) const {
     for (size_t i = 0; i < steps.size(); i++)
       if (steps[i] == step) return keys + key_elems * i;
@@ -266,10 +296,15 @@ struct hd_database {
   uint64_t *rB = nullptr, *SB[2] = {nullptr, nullptr};
   uint32_t qb_cap = 0;
   cudaEvent_t ev_in = nullptr, ev_mac = nullptr, ev_done = nullptr, ev_sfree[2] = {nullptr, nullptr};
+  // last hd_baby_steps on the caller's stream: the next scan's stream A waits on it before
+  // reusing the baby-step workspaces (dig_b, u_b, tmp_b)
+  cudaEvent_t ev_bs = nullptr;
+  bool bs_pending = false;
   // rotation-key tables for the (db, evk) pair last used: [0, n1-1) baby i = 1..n1-1,
   // [n1-1, n1-1+nj) giant j (NULL key when preRot = 0), [n1-1+nj] fold
   // [n1+nj] relinearisation key (encrypted mode), gal 1 (identity permutation)
   const hd_eval_keys *keyed_for = nullptr;
+  uint64_t keyed_gen = 0;        // hd_eval_keys::gen of the bound key storage
   const uint64_t **kptr = nullptr;
   uint32_t *gal = nullptr;
   uint32_t relin_chunk = 1;      // giant-step sums relinearised per batch (encrypted mode)

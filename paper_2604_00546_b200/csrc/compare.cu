@@ -105,27 +105,27 @@ struct Eval {
     Batch r;
     r.ell = r.lay = ell;
     r.scale = scale;
-    uint64_t *p = nullptr;
     if (err) return r;
-    cudaError_t e = cudaMallocAsync(&p, (size_t)B * 2 * ell * c->n * 8, c->stream);
-    if (e != cudaSuccess) {
-      err = hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, "comparison workspace");
+    const size_t bytes = (size_t)B * 2 * ell * c->n * 8;
+    uint64_t *p = static_cast<uint64_t *>(ws_alloc(c, bytes));
+    if (!p) {
+      err = hd_fail(HD_E_CAPACITY, "comparison workspace");
       return r;
     }
-    cudaStream_t s = c->stream;
-    r.d = std::shared_ptr<uint64_t>(p, [s](uint64_t *q) { cudaFreeAsync(q, s); });
+    hd_context *cc = c;
+    r.d = std::shared_ptr<uint64_t>(p, [cc, bytes](uint64_t *q) { ws_free(cc, q, bytes); });
     return r;
   }
   uint64_t *scratch(size_t elems, std::shared_ptr<uint64_t> &keep) {
-    uint64_t *p = nullptr;
     if (err) return nullptr;
-    cudaError_t e = cudaMallocAsync(&p, elems * 8, c->stream);
-    if (e != cudaSuccess) {
-      err = hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, "comparison workspace");
+    const size_t bytes = elems * 8;
+    uint64_t *p = static_cast<uint64_t *>(ws_alloc(c, bytes));
+    if (!p) {
+      err = hd_fail(HD_E_CAPACITY, "comparison workspace");
       return nullptr;
     }
-    cudaStream_t s = c->stream;
-    keep = std::shared_ptr<uint64_t>(p, [s](uint64_t *q) { cudaFreeAsync(q, s); });
+    hd_context *cc = c;
+    keep = std::shared_ptr<uint64_t>(p, [cc, bytes](uint64_t *q) { ws_free(cc, q, bytes); });
     return p;
   }
   void launch_check() {
@@ -380,10 +380,9 @@ hd_status upload_keys(hd_context *c, const std::vector<const uint64_t *> &kp, co
   std::vector<char> host(bytes);
   memcpy(host.data(), kp.data(), cnt * sizeof(uint64_t *));
   memcpy(host.data() + cnt * sizeof(uint64_t *), gl.data(), cnt * sizeof(uint32_t));
-  void *p = nullptr;
-  HD_CUDA(cudaMallocAsync(&p, bytes, c->stream));
-  cudaStream_t s = c->stream;
-  dk.mem = std::shared_ptr<void>(p, [s](void *q) { cudaFreeAsync(q, s); });
+  void *p = ws_alloc(c, bytes);
+  if (!p) return hd_fail(HD_E_CAPACITY, "comparison key table");
+  dk.mem = std::shared_ptr<void>(p, [c, bytes](void *q) { ws_free(c, q, bytes); });
   HD_CUDA(cudaMemcpyAsync(p, host.data(), bytes, cudaMemcpyHostToDevice, c->stream));
   dk.kp = (const uint64_t *const *)p;
   dk.gal = (const uint32_t *)((char *)p + cnt * sizeof(uint64_t *));

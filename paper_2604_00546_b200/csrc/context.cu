@@ -6,6 +6,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
+#include <atomic>
 #include <mutex>
 
 #include "common.cuh"
@@ -17,6 +19,11 @@ static thread_local std::string g_last_error;
 hd_status hd_fail(hd_status s, const std::string &msg) {
   g_last_error = msg;
   return s;
+}
+
+uint64_t hd_next_generation() {
+  static std::atomic<uint64_t> g{1};
+  return g.fetch_add(1);
 }
 
 extern "C" const char *hd_last_error(void) { return g_last_error.c_str(); }
@@ -103,8 +110,61 @@ static uint32_t bitrev_host(uint32_t x, int bits) {
   return r;
 }
 
+// ---------------------------------------------------------------------------
+// device memory: the caller's allocator or the device's stream-ordered pool
+// ---------------------------------------------------------------------------
+cudaError_t dev_alloc(hd_context *c, void **p, size_t bytes) {
+  *p = nullptr;
+  if (bytes == 0) bytes = 8;
+  if (c->has_alloc) {
+    *p = c->alloc.alloc(bytes, (void *)c->stream, c->alloc.user);
+    return *p ? cudaSuccess : cudaErrorMemoryAllocation;
+  }
+  cudaError_t e = cudaMallocAsync(p, bytes, c->stream);
+  // the allocation is ordered on the caller's stream; the pipeline streams may use it next
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  return e;
+}
+
+static void quiesce(hd_context *c) {
+  for (cudaStream_t s : {c->stream, c->sA, c->sB, c->sIO, c->sUp})
+    if (s || s == c->stream) cudaStreamSynchronize(s);
+}
+
+void dev_free(hd_context *c, void *p) {
+  if (!p) return;
+  quiesce(c);  // no stream of the context may still touch the memory
+  if (c->has_alloc)
+    c->alloc.free(p, (void *)c->stream, c->alloc.user);
+  else
+    cudaFreeAsync(p, c->stream);
+}
+
+void *ws_alloc(hd_context *c, size_t bytes) {
+  // smallest cached block that fits and is not more than twice as large
+  size_t best = SIZE_MAX;
+  for (size_t i = 0; i < c->ws_free.size(); i++) {
+    const auto &b = c->ws_free[i];
+    if (b.bytes >= bytes && b.bytes <= 2 * bytes + (1u << 20) && (best == SIZE_MAX || b.bytes < c->ws_free[best].bytes))
+      best = i;
+  }
+  if (best != SIZE_MAX) {
+    auto b = c->ws_free[best];
+    c->ws_free.erase(c->ws_free.begin() + best);
+    if (b.stream != c->stream) cudaStreamSynchronize(b.stream);  // freed in another stream's order
+    return b.p;
+  }
+  void *p = nullptr;
+  if (c->has_alloc) return c->alloc.alloc(bytes, (void *)c->stream, c->alloc.user);
+  return cudaMallocAsync(&p, bytes, c->stream) == cudaSuccess ? p : nullptr;
+}
+
+void ws_free(hd_context *c, void *p, size_t bytes) {
+  if (p) c->ws_free.push_back({p, bytes, c->stream});  // reusable in c->stream's order
+}
+
 extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device, void *cuda_stream,
-                                       hd_context **out) {
+                                       const hd_allocator *allocator, hd_context **out) {
   if (!params || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
   *out = nullptr;
   hd_params p = *params;
@@ -123,7 +183,9 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
     return hd_fail(HD_E_CUDA, "no CUDA device (libhd has no CPU fallback)");
   if (cuda_device < 0 || cuda_device >= ndev) return hd_fail(HD_E_INVALID_ARG, "bad device index");
   HD_CUDA(cudaSetDevice(cuda_device));
-  {  // stream-ordered workspaces of the comparison (compare.cu) stay mapped between calls
+  if (allocator && (!allocator->alloc || !allocator->free))
+    return hd_fail(HD_E_INVALID_ARG, "allocator needs both alloc and free");
+  if (!allocator) {  // the default pool keeps freed memory mapped for reuse between calls
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
       uint64_t keep = UINT64_MAX;
@@ -131,6 +193,10 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
     }
   }
   hd_context *c = new hd_context();
+  if (allocator) {
+    c->alloc = *allocator;
+    c->has_alloc = true;
+  }
   c->params = p;
   c->device = cuda_device;
   c->stream = (cudaStream_t)cuda_stream;
@@ -194,10 +260,10 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
     return hd_fail(HD_E_CUDA, std::string("context tables: ") + cudaGetErrorString(e));
   };
   cudaError_t e;
-  if ((e = cudaMalloc(&c->tw2, tw.size() * 8)) || (e = cudaMalloc(&c->itw2, itw.size() * 8)) ||
-      (e = cudaMalloc(&c->ninv_dev, nv.size() * 8)) ||
-      (e = cudaMalloc(&c->xi_re, two_n * 8)) || (e = cudaMalloc(&c->xi_im, two_n * 8)) ||
-      (e = cudaMalloc(&c->rotg, c->ns * 4)) || (e = cudaMalloc(&c->d_flag, 64)))
+  if ((e = dev_alloc(c, &c->tw2, tw.size() * 8)) || (e = dev_alloc(c, &c->itw2, itw.size() * 8)) ||
+      (e = dev_alloc(c, &c->ninv_dev, nv.size() * 8)) ||
+      (e = dev_alloc(c, &c->xi_re, two_n * 8)) || (e = dev_alloc(c, &c->xi_im, two_n * 8)) ||
+      (e = dev_alloc(c, &c->rotg, c->ns * 4)) || (e = dev_alloc(c, &c->d_flag, 64)))
     return fail(e);
   if ((e = cudaMemcpy(c->tw2, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(c->itw2, itw.data(), itw.size() * 8, cudaMemcpyHostToDevice)) ||
@@ -217,14 +283,12 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
 extern "C" void hd_context_destroy(hd_context *c) {
   if (!c) return;
   cudaSetDevice(c->device);
-  cudaFree(c->tw2);
-  cudaFree(c->itw2);
-  cudaFree(c->ninv_dev);
-  cudaFree(c->xi_re);
-  cudaFree(c->xi_im);
-  cudaFree(c->rotg);
-  cudaFree(c->d_flag);
-  cudaFree(c->scratch);
+  quiesce(c);
+  for (void *p : {(void *)c->tw2, (void *)c->itw2, (void *)c->ninv_dev, (void *)c->xi_re, (void *)c->xi_im,
+                  (void *)c->rotg, (void *)c->d_flag, c->scratch})
+    dev_free(c, p);
+  for (auto &b : c->ws_free) dev_free(c, b.p);
+  c->ws_free.clear();
   if (c->sA) cudaStreamDestroy(c->sA);
   if (c->sB) cudaStreamDestroy(c->sB);
   if (c->sIO) cudaStreamDestroy(c->sIO);
@@ -289,10 +353,10 @@ cudaMemcpyKind kind_of(int dst_dev, int src_dev) {
 hd_status alloc_ct(hd_context *c, uint32_t limbs, hd_ciphertext **out) {
   hd_ciphertext *ct = new hd_ciphertext{c, limbs, nullptr};
   ct->scale = std::ldexp(1.0, (int)c->params.scale_bits);
-  cudaError_t e = cudaMalloc(&ct->data, sizeof(uint64_t) * 2 * limbs * c->n);
+  cudaError_t e = dev_alloc(c, &ct->data, sizeof(uint64_t) * 2 * limbs * c->n);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ct->ready, cudaEventDisableTiming);
   if (e != cudaSuccess) {
-    cudaFree(ct->data);
+    dev_free(c, ct->data);
     delete ct;
     return hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, "ciphertext alloc");
   }
@@ -329,6 +393,32 @@ extern "C" hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, si
   return HD_OK;
 }
 
+// Every residue row r (n words) must lie in [0, q_m) with m = chain[r % period]; rows of a
+// ciphertext [2][limbs][n] use chain = identity, period = limbs; rows of a key set
+// [count][L][2][L+1][n] use period L+1 (index L is the special prime P).  One pass on
+// the context's stream; the caller's import syncs on it anyway.
+__global__ void range_check_kernel(const uint64_t *__restrict__ d, size_t rows, int period, int logn, ModTab mt,
+                                   int *flag) {
+  const size_t total = rows << logn;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int m = (int)((i >> logn) % (size_t)period);
+    if (d[i] >= mt.q[m]) {
+      atomicOr(flag, 1);
+      return;
+    }
+  }
+}
+
+hd_status check_residues(hd_context *c, const uint64_t *d, size_t rows, int period) {
+  int f = 0;
+  HD_CUDA(cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->stream));
+  range_check_kernel<<<4 * 148, 256, 0, c->stream>>>(d, rows, period, c->logn, c->mt, c->d_flag); ++c->launches;
+  HD_CUDA(cudaMemcpyAsync(&f, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+  HD_CUDA(cudaStreamSynchronize(c->stream));
+  if (f) return hd_fail(HD_E_FORMAT, "serialised residue out of range [0, q)");
+  return HD_OK;
+}
+
 static hd_status read_header(hd_context *c, const void *src, size_t bytes, int src_dev, Header &h) {
   if (!src || bytes < sizeof(Header)) return hd_fail(HD_E_FORMAT, "short buffer");
   if (src_dev) {
@@ -352,16 +442,22 @@ extern "C" hd_status hd_ciphertext_import(hd_context *c, const void *src, size_t
   hd_status s = read_header(c, src, bytes, src_on_device, h);
   if (s) return s;
   if (h.kind != 1 || h.limbs < 1 || h.limbs > (uint32_t)c->L) return hd_fail(HD_E_FORMAT, "not a ciphertext");
+  if (h.payload != sizeof(uint64_t) * 2 * h.limbs * c->n)
+    return hd_fail(HD_E_FORMAT, "ciphertext payload size does not match its header");
+  if (!(h.scale >= 0.0) || std::isinf(h.scale)) return hd_fail(HD_E_FORMAT, "bad ciphertext scale");
   hd_ciphertext *ct;
   if ((s = alloc_ct(c, h.limbs, &ct))) return s;
   if (h.scale > 0.0) ct->scale = h.scale;
   cudaError_t e = cudaMemcpyAsync(ct->data, (const char *)src + sizeof(Header), h.payload,
                                   kind_of(1, src_on_device), c->stream);
   if (e == cudaSuccess) e = cudaEventRecord(ct->ready, c->stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) {
     hd_ciphertext_destroy(ct);
     return hd_fail(HD_E_CUDA, cudaGetErrorString(e));
+  }
+  if ((s = check_residues(c, ct->data, (size_t)2 * h.limbs, h.limbs))) {
+    hd_ciphertext_destroy(ct);
+    return s;
   }
   *out = ct;
   return HD_OK;
@@ -377,7 +473,7 @@ extern "C" hd_status hd_ciphertext_import_into(hd_ciphertext *ct, const void *sr
     Header h;
     hd_status s = read_header(c, src, bytes, 0, h);
     if (s) return s;
-    if (h.kind != 1 || h.limbs != ct->limbs) return hd_fail(HD_E_LEVEL, "shape mismatch");
+    if (h.kind != 1 || h.limbs != ct->limbs || h.payload != payload) return hd_fail(HD_E_LEVEL, "shape mismatch");
     ct->scale = h.scale > 0.0 ? h.scale : std::ldexp(1.0, (int)c->params.scale_bits);
   }
   // Host sources are uploaded on the context's upload stream, ordered only after the
@@ -453,7 +549,7 @@ extern "C" void hd_ciphertext_destroy(hd_ciphertext *ct) {
     cudaEventSynchronize(ct->used);
     cudaEventDestroy(ct->used);
   }
-  cudaFree(ct->data);
+  dev_free(ct->ctx, ct->data);
   delete ct;
 }
 
@@ -494,13 +590,26 @@ extern "C" hd_status hd_eval_keys_import(hd_context *c, const void *src, size_t 
   if (s) return s;
   if (h.kind != 2 || h.limbs != (uint32_t)c->L) return hd_fail(HD_E_FORMAT, "not an eval-key set");
   size_t nk = h.count, steps_bytes = ((nk * 4 + 63) / 64) * 64;
+  const size_t key_elems = (size_t)c->L * 2 * (c->L + 1) * c->n;
+  if (nk == 0 || nk > (size_t)c->ns + 1 || h.payload != steps_bytes + sizeof(uint64_t) * key_elems * nk)
+    return hd_fail(HD_E_FORMAT, "eval-key payload size does not match its header");
   hd_eval_keys *k = new hd_eval_keys();
   k->ctx = c;
   k->steps.resize(nk);
-  k->key_elems = (size_t)c->L * 2 * (c->L + 1) * c->n;
+  k->key_elems = key_elems;
   const char *p = (const char *)src + sizeof(Header);
   cudaError_t e = cudaMemcpyAsync(k->steps.data(), p, nk * 4, kind_of(0, src_on_device), c->stream);
-  if (e == cudaSuccess) e = cudaMalloc(&k->keys, sizeof(uint64_t) * k->key_elems * nk);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  if (e == cudaSuccess) {  // steps: each in [0, numSlots) (0 = relinearisation key), no duplicates
+    std::vector<int32_t> st(k->steps);
+    std::sort(st.begin(), st.end());
+    for (size_t i = 0; i < nk; i++)
+      if (st[i] < 0 || st[i] >= c->ns || (i && st[i] == st[i - 1])) {
+        hd_eval_keys_destroy(k);
+        return hd_fail(HD_E_FORMAT, "eval-key set has an out-of-range or duplicate rotation step");
+      }
+  }
+  if (e == cudaSuccess) e = dev_alloc(c, &k->keys, sizeof(uint64_t) * k->key_elems * nk);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(k->keys, p + steps_bytes, sizeof(uint64_t) * k->key_elems * nk, kind_of(1, src_on_device),
                         c->stream);
@@ -509,13 +618,17 @@ extern "C" hd_status hd_eval_keys_import(hd_context *c, const void *src, size_t 
     hd_eval_keys_destroy(k);
     return hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, cudaGetErrorString(e));
   }
+  if ((s = check_residues(c, k->keys, nk * c->L * 2 * (c->L + 1), c->L + 1))) {
+    hd_eval_keys_destroy(k);
+    return s;
+  }
   *out = k;
   return HD_OK;
 }
 
 extern "C" void hd_eval_keys_destroy(hd_eval_keys *k) {
   if (!k) return;
-  cudaFree(k->keys);
+  dev_free(k->ctx, k->keys);
   delete k;
 }
 
@@ -530,7 +643,7 @@ extern "C" hd_status hd_secret_key_export(const hd_secret_key *sk, uint64_t *dst
 
 extern "C" void hd_secret_key_destroy(hd_secret_key *sk) {
   if (!sk) return;
-  cudaFree(sk->s_ntt);
+  dev_free(sk->ctx, sk->s_ntt);
   delete sk;
 }
 
@@ -541,7 +654,7 @@ extern "C" hd_status hd_test_ntt(hd_context *c, uint64_t *data, uint32_t n_rows,
     if (modulus_idx[r] > (uint32_t)c->L) return hd_fail(HD_E_INVALID_ARG, "modulus index > L");
   uint64_t *d;
   size_t bytes = (size_t)n_rows * c->n * 8;
-  HD_CUDA(cudaMalloc(&d, bytes));
+  HD_CUDA(dev_alloc(c, &d, bytes));
   HD_CUDA(cudaMemcpy(d, data, bytes, cudaMemcpyHostToDevice));
   // rows may have arbitrary moduli: launch one row-group per run of equal index
   hd_status s = HD_OK;
@@ -557,6 +670,6 @@ extern "C" hd_status hd_test_ntt(hd_context *c, uint64_t *data, uint32_t n_rows,
     if (e == cudaSuccess) e = cudaMemcpy(data, d, bytes, cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
   }
-  cudaFree(d);
+  dev_free(c, d);
   return s;
 }

@@ -242,33 +242,36 @@ extern "C" hd_status hd_database_layout(const hd_database *db, hd_layout *out) {
 
 extern "C" void hd_database_destroy(hd_database *db) {
   if (!db) return;
-  cudaFree(db->D);
-  cudaFree(db->r);
-  cudaFree(db->S);
-  cudaFree(db->Sp);
-  cudaFree(db->y);
-  cudaFree(db->dig);
-  cudaFree(db->u);
-  cudaFree(db->tmp);
-  cudaFree(db->tmp2);
-  cudaFree(db->outbuf);
-  cudaFree(db->kptr);
-  cudaFree(db->gal);
-  cudaFree(db->S2);
-  cudaFree(db->rB);
-  cudaFree(db->SB[0]);
-  cudaFree(db->SB[1]);
-  cudaFree(db->dig_b);
-  cudaFree(db->u_b);
-  cudaFree(db->tmp_b);
-  for (cudaEvent_t e : {db->ev_in, db->ev_mac, db->ev_done, db->ev_sfree[0], db->ev_sfree[1]})
+  hd_context *c = db->ctx;
+  dev_free(c, db->D);
+  dev_free(c, db->r);
+  dev_free(c, db->S);
+  dev_free(c, db->Sp);
+  dev_free(c, db->y);
+  dev_free(c, db->dig);
+  dev_free(c, db->u);
+  dev_free(c, db->tmp);
+  dev_free(c, db->tmp2);
+  dev_free(c, db->outbuf);
+  dev_free(c, db->kptr);
+  dev_free(c, db->gal);
+  dev_free(c, db->S2);
+  dev_free(c, db->rB);
+  dev_free(c, db->SB[0]);
+  dev_free(c, db->SB[1]);
+  dev_free(c, db->dig_b);
+  dev_free(c, db->u_b);
+  dev_free(c, db->tmp_b);
+  for (cudaEvent_t e : {db->ev_in, db->ev_mac, db->ev_done, db->ev_sfree[0], db->ev_sfree[1], db->ev_bs})
     if (e) cudaEventDestroy(e);
   delete db;
 }
 
 // Device objects of a database handle: diagonals D (uninitialised), query workspaces, events.
+// footprint != NULL: only report the device bytes the handle needs (the paper's pre-upload
+// footprint check) and allocate nothing.
 static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing, bool encrypted, uint32_t n1,
-                          hd_database **out) {
+                          hd_database **out, size_t *footprint = nullptr) {
   HD_CUDA(cudaSetDevice(c->device));
   hd_database *db = new hd_database();
   db->ctx = c;
@@ -335,33 +338,56 @@ static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing,
               {(void **)&db->tmp_b, tmpb_e * 8}};
   size_t total = 0;
   for (auto &q : reqs) total += q.bytes;
-  size_t fr = 0, tot = 0;
-  {  // return the comparison's stream-ordered workspaces (kept mapped between calls, context.cu)
-    HD_CUDA(cudaDeviceSynchronize());
+  if (footprint) {
+    *footprint = total;
+    delete db;
+    return HD_OK;
+  }
+  if (!c->has_alloc) {
+    // Default pool: free memory the pool holds but does not use (it keeps freed blocks
+    // mapped), then check the footprint before the upload.  With a caller
+    // allocator the caller checks hd_enroll_footprint against what it can hand out.
+    size_t fr = 0, tot = 0;
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
-  }
-  HD_CUDA(cudaMemGetInfo(&fr, &tot));
-  if (total + (256ull << 20) > fr) {
-    delete db;
-    return hd_fail(HD_E_CAPACITY, "database of " + std::to_string(total >> 20) + " MiB exceeds free device memory (" +
-                                      std::to_string(fr >> 20) + " MiB); shard the aggregates over more GPUs");
+    HD_CUDA(cudaMemGetInfo(&fr, &tot));
+    if (total + (256ull << 20) > fr) {
+      delete db;
+      return hd_fail(HD_E_CAPACITY, "database of " + std::to_string(total >> 20) + " MiB exceeds free device memory (" +
+                                        std::to_string(fr >> 20) + " MiB); shard the aggregates over more GPUs");
+    }
   }
   for (auto &q : reqs) {
-    cudaError_t e = cudaMalloc(q.p, q.bytes);
+    cudaError_t e = dev_alloc(c, q.p, q.bytes);
     if (e != cudaSuccess) {
       hd_database_destroy(db);
       return hd_fail(HD_E_CAPACITY, std::string("device allocation: ") + cudaGetErrorString(e));
     }
   }
   db->bytes = total;
-  for (cudaEvent_t *e : {&db->ev_in, &db->ev_mac, &db->ev_done, &db->ev_sfree[0], &db->ev_sfree[1]})
+  for (cudaEvent_t *e : {&db->ev_in, &db->ev_mac, &db->ev_done, &db->ev_sfree[0], &db->ev_sfree[1], &db->ev_bs})
     if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess) {
       hd_database_destroy(db);
       return hd_fail(HD_E_CUDA, "event creation");
     }
   *out = db;
   return HD_OK;
+}
+
+extern "C" hd_status hd_enroll_footprint(hd_context *c, uint64_t num_vectors, uint32_t vector_dim, uint32_t n1,
+                                         uint32_t agg_begin, uint32_t agg_end, const hd_enroll_options *opts,
+                                         size_t *bytes) {
+  if (!c || !bytes) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  const uint32_t packing = opts ? opts->packing : HD_PACKING_REPLICATED;
+  const bool encrypted = opts && opts->pk;
+  hd_layout lay;
+  hd_status s = layout_make(c, num_vectors, vector_dim, n1, packing, &lay);
+  if (s) return s;
+  if (agg_end == 0) agg_end = (uint32_t)lay.num_aggregates;
+  if (agg_begin >= agg_end || agg_end > lay.num_aggregates) return hd_fail(HD_E_INVALID_ARG, "bad aggregate range");
+  lay.agg_begin = agg_begin;
+  lay.agg_end = agg_end;
+  return db_alloc(c, lay, packing, encrypted, n1, nullptr, bytes);
 }
 
 // pk == NULL: plaintext diagonals (the north-star pt x ct scan); else every diagonal
@@ -390,20 +416,20 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
   const int KB = std::min(N, std::max(1, (int)((256ull << 20) / ((size_t)ns * 16))));
   float *dv = nullptr;
   double *U = nullptr, *re = nullptr, *im = nullptr;
-  cudaError_t e = cudaMalloc(&dv, rows_per_agg * N * 4);
-  if (!e) e = cudaMalloc(&U, rows_per_agg * N * 8);
-  if (!e) e = cudaMalloc(&re, (size_t)KB * ns * 8);
-  if (!e) e = cudaMalloc(&im, (size_t)KB * ns * 8);
+  cudaError_t e = dev_alloc(c, &dv, rows_per_agg * N * 4);
+  if (!e) e = dev_alloc(c, &U, rows_per_agg * N * 8);
+  if (!e) e = dev_alloc(c, &re, (size_t)KB * ns * 8);
+  if (!e) e = dev_alloc(c, &im, (size_t)KB * ns * 8);
   uint64_t *V = nullptr, *E0 = nullptr;  // public-key encryption scratch (v, e0 of a batch)
-  if (!e && pk) e = cudaMalloc(&V, (size_t)KB * L * n * 8);
-  if (!e && pk) e = cudaMalloc(&E0, (size_t)KB * L * n * 8);
+  if (!e && pk) e = dev_alloc(c, &V, (size_t)KB * L * n * 8);
+  if (!e && pk) e = dev_alloc(c, &E0, (size_t)KB * L * n * 8);
   auto cleanup = [&]() {
-    cudaFree(dv);
-    cudaFree(U);
-    cudaFree(re);
-    cudaFree(im);
-    cudaFree(V);
-    cudaFree(E0);
+    dev_free(c, dv);
+    dev_free(c, U);
+    dev_free(c, re);
+    dev_free(c, im);
+    dev_free(c, V);
+    dev_free(c, E0);
   };
   if (e) {
     cleanup();

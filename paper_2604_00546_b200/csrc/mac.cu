@@ -493,6 +493,7 @@ hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
                   const std::vector<int32_t> &js, bool flat) {
   if (js.empty() || A_loc == 0) return HD_OK;
+  if (mac_tma_supported(c, n1, N, flat, 1)) return mac_tma_run(c, D, r, S, A_loc, n1, N, js, 1);
   const int jmin = js.front(), nj = (int)js.size();
   // every giant step uses all n1 baby steps (replicated: n1 | N/2; flat: n1 | N)
   const bool full = (flat ? N % n1 : (N / 2) % n1) == 0 && n1 <= 256 && c->n % MAC_TPB == 0;
@@ -525,6 +526,17 @@ hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uin
   if (js.empty() || A_loc == 0 || Q == 0) return HD_OK;
   const int jmin = js.front(), nj = (int)js.size();
   const size_t ls = (size_t)c->L * c->n, rq = (size_t)n1 * 2 * ls, sq = (size_t)A_loc * nj * 2 * ls;
+  if (mac_tma_supported(c, n1, N, flat, 1)) {  // groups of up to 4 queries per diagonal pass
+    const char *g_env = getenv("HD_MAC_BATCH");    // max group size (default 4)
+    const uint32_t gmax = g_env ? std::max(1, std::min(4, atoi(g_env))) : 4;
+    for (uint32_t b0 = 0; b0 < Q;) {
+      const uint32_t g = std::min(gmax, Q - b0);
+      hd_status s = mac_tma_run(c, D, r + b0 * rq, S + b0 * sq, A_loc, n1, N, js, g);
+      if (s) return s;
+      b0 += g;
+    }
+    return HD_OK;
+  }
   const bool full = (flat ? N % n1 : (N / 2) % n1) == 0 && n1 <= 256 && c->n % MAC_TPB == 0;
   bool small_q = true;
   for (int l = 0; l < c->L; l++) small_q = small_q && c->mod[l] < (1ull << 60);

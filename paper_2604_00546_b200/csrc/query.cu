@@ -18,7 +18,7 @@ static hd_status scan_tail(hd_database *db, uint64_t *Sbuf, cudaEvent_t *E, bool
 
 static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
   hd_context *c = db->ctx;
-  if (db->keyed_for == evk && db->kptr) return HD_OK;
+  if (db->keyed_for == evk && db->keyed_gen == evk->gen && db->kptr) return HD_OK;
   const int n1 = (int)db->n1, nj = (int)db->js.size();
   const size_t cnt = (size_t)(n1 - 1) + nj + 1 + (db->encrypted ? 1 : 0);
   std::vector<const uint64_t *> kp(cnt, nullptr);
@@ -43,13 +43,14 @@ static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
       return hd_fail(HD_E_MISSING_KEY, "missing relinearisation key (hd_relin_keygen) for an encrypted database");
   }
   if (!db->kptr) {
-    HD_CUDA(cudaMalloc(&db->kptr, cnt * sizeof(uint64_t *)));
-    HD_CUDA(cudaMalloc(&db->gal, cnt * sizeof(uint32_t)));
+    HD_CUDA(dev_alloc(c, &db->kptr, cnt * sizeof(uint64_t *)));
+    HD_CUDA(dev_alloc(c, &db->gal, cnt * sizeof(uint32_t)));
   }
   HD_CUDA(cudaMemcpyAsync(db->kptr, kp.data(), cnt * sizeof(uint64_t *), cudaMemcpyHostToDevice, c->stream));
   HD_CUDA(cudaMemcpyAsync(db->gal, gl.data(), cnt * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
   HD_CUDA(cudaStreamSynchronize(c->stream));
   db->keyed_for = evk;
+  db->keyed_gen = evk->gen;
   return HD_OK;
 }
 
@@ -80,6 +81,10 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, 
   // the baby steps + MAC of this query can run while B still finishes the previous one.
   HD_CUDA(cudaEventRecord(db->ev_in, caller));
   if (r_ext) HD_CUDA(cudaStreamWaitEvent(sa, db->ev_in, 0));  // after the caller's baby-step writers
+  if (db->bs_pending) {  // an hd_baby_steps on the caller's stream still owns the workspaces
+    HD_CUDA(cudaStreamWaitEvent(sa, db->ev_bs, 0));
+    db->bs_pending = false;
+  }
   for (uint32_t qi = 0; qi < Q && !r_ext; qi++) {
     HD_CUDA(cudaStreamWaitEvent(sa, queries[qi]->ready, 0));
     hd_ciphertext *qmut = const_cast<hd_ciphertext *>(queries[qi]);  // reader bookkeeping only
@@ -309,18 +314,15 @@ extern "C" hd_status hd_query_batch(hd_context *c, const hd_eval_keys *evk, cons
   hd_status s = bind_keys(db, evk);
   if (s) return s;
   if (Q > 1 && Q > db->qb_cap) {  // setup-time allocation for this batch size (kept for later batches)
-    HD_CUDA(cudaDeviceSynchronize());
-    cudaMemPool_t pool;  // return the comparison's stream-ordered workspaces first
-    if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
-    cudaFree(db->rB);
-    cudaFree(db->SB[0]);
-    cudaFree(db->SB[1]);
+    dev_free(c, db->rB);  // dev_free waits for this context's streams only
+    dev_free(c, db->SB[0]);
+    dev_free(c, db->SB[1]);
     db->rB = db->SB[0] = db->SB[1] = nullptr;
     db->qb_cap = 0;
     const size_t ctL = (size_t)2 * L * n, sq = (size_t)db->A_loc * nj * 2 * L * n;
-    cudaError_t e = cudaMalloc(&db->rB, (size_t)Q * n1 * ctL * 8);
-    if (!e) e = cudaMalloc(&db->SB[0], (size_t)Q * sq * 8);
-    if (!e) e = cudaMalloc(&db->SB[1], (size_t)Q * sq * 8);
+    cudaError_t e = dev_alloc(c, &db->rB, (size_t)Q * n1 * ctL * 8);
+    if (!e) e = dev_alloc(c, &db->SB[0], (size_t)Q * sq * 8);
+    if (!e) e = dev_alloc(c, &db->SB[1], (size_t)Q * sq * 8);
     if (e) return hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, "query batch workspace");
     db->qb_cap = Q;
   }
@@ -387,6 +389,8 @@ extern "C" hd_status hd_baby_steps(hd_context *c, const hd_eval_keys *evk, const
   hd_ciphertext *qmut = const_cast<hd_ciphertext *>(query);  // reader bookkeeping only
   if (!qmut->used) HD_CUDA(cudaEventCreateWithFlags(&qmut->used, cudaEventDisableTiming));
   HD_CUDA(cudaEventRecord(qmut->used, c->stream));
+  HD_CUDA(cudaEventRecord(db->ev_bs, c->stream));
+  db->bs_pending = true;
   HD_CUDA(cudaGetLastError());
   return HD_OK;
 }
@@ -516,11 +520,11 @@ extern "C" hd_status hd_test_rotate(hd_context *c, const hd_eval_keys *evk, cons
   uint64_t *dig, *u, *tmp, **kp;
   uint32_t *g;
   uint32_t gh = (uint32_t)host_powmod(5, (uint64_t)step, 2ull * n);
-  HD_CUDA(cudaMalloc(&dig, (size_t)ell * (ell + 1) * n * 8));
-  HD_CUDA(cudaMalloc(&u, (size_t)2 * (ell + 1) * n * 8));
-  HD_CUDA(cudaMalloc(&tmp, (size_t)2 * (ell + 1) * n * 8));
-  HD_CUDA(cudaMalloc(&kp, sizeof(uint64_t *)));
-  HD_CUDA(cudaMalloc(&g, 4));
+  HD_CUDA(dev_alloc(c, &dig, (size_t)ell * (ell + 1) * n * 8));
+  HD_CUDA(dev_alloc(c, &u, (size_t)2 * (ell + 1) * n * 8));
+  HD_CUDA(dev_alloc(c, &tmp, (size_t)2 * (ell + 1) * n * 8));
+  HD_CUDA(dev_alloc(c, &kp, sizeof(uint64_t *)));
+  HD_CUDA(dev_alloc(c, &g, 4));
   HD_CUDA(cudaMemcpy(kp, &k, sizeof(uint64_t *), cudaMemcpyHostToDevice));
   HD_CUDA(cudaMemcpy(g, &gh, 4, cudaMemcpyHostToDevice));
   hd_ciphertext *o;
@@ -530,11 +534,11 @@ extern "C" hd_status hd_test_rotate(hd_context *c, const hd_eval_keys *evk, cons
   if (!s) s = ks_moddown(c, u, 1, 1, ell, g, ct->data, 0, o->data, 0, false, tmp);
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (!s && e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
-  cudaFree(dig);
-  cudaFree(u);
-  cudaFree(tmp);
-  cudaFree(kp);
-  cudaFree(g);
+  dev_free(c, dig);
+  dev_free(c, u);
+  dev_free(c, tmp);
+  dev_free(c, kp);
+  dev_free(c, g);
   (void)L;
   if (s) {
     hd_ciphertext_destroy(o);
@@ -551,15 +555,15 @@ extern "C" hd_status hd_test_rescale(hd_context *c, const hd_ciphertext *ct, hd_
   if (ct->limbs < 2) return hd_fail(HD_E_LEVEL, "cannot rescale a 1-limb ciphertext");
   const int n = c->n, ell = (int)ct->limbs;
   uint64_t *t1, *t2;
-  HD_CUDA(cudaMalloc(&t1, (size_t)2 * n * 8));
-  HD_CUDA(cudaMalloc(&t2, (size_t)2 * ell * n * 8));
+  HD_CUDA(dev_alloc(c, &t1, (size_t)2 * n * 8));
+  HD_CUDA(dev_alloc(c, &t2, (size_t)2 * ell * n * 8));
   hd_ciphertext *o;
   hd_status s = alloc_ct(c, ell - 1, &o);
   if (!s) s = ks_rescale(c, ct->data, 0, 1, ell, o->data, 0, t1, t2);
   cudaError_t e = cudaStreamSynchronize(c->stream);
   if (!s && e) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
-  cudaFree(t1);
-  cudaFree(t2);
+  dev_free(c, t1);
+  dev_free(c, t2);
   if (s) {
     hd_ciphertext_destroy(o);
     return s;
@@ -596,12 +600,12 @@ extern "C" hd_status hd_database_prerotate(hd_context *c, const hd_eval_keys *ev
   const uint32_t Bmax = (uint32_t)std::min(n1, N);
   uint64_t *dig = nullptr, *tmp = nullptr, *u = nullptr, *out = nullptr, **kp = nullptr;
   uint32_t *gal = nullptr;
-  cudaError_t e = cudaMalloc(&dig, (size_t)Bmax * L * L * n * 8);
-  if (!e) e = cudaMalloc(&tmp, (size_t)Bmax * 2 * L * n * 8);
-  if (!e) e = cudaMalloc(&u, (size_t)Bmax * 2 * (L + 1) * n * 8);
-  if (!e) e = cudaMalloc(&out, (size_t)Bmax * ct * 8);
-  if (!e) e = cudaMalloc(&kp, sizeof(uint64_t *));
-  if (!e) e = cudaMalloc(&gal, sizeof(uint32_t));
+  cudaError_t e = dev_alloc(c, &dig, (size_t)Bmax * L * L * n * 8);
+  if (!e) e = dev_alloc(c, &tmp, (size_t)Bmax * 2 * L * n * 8);
+  if (!e) e = dev_alloc(c, &u, (size_t)Bmax * 2 * (L + 1) * n * 8);
+  if (!e) e = dev_alloc(c, &out, (size_t)Bmax * ct * 8);
+  if (!e) e = dev_alloc(c, &kp, sizeof(uint64_t *));
+  if (!e) e = dev_alloc(c, &gal, sizeof(uint32_t));
   hd_status s = e ? hd_fail(HD_E_CAPACITY, "pre-rotation scratch") : HD_OK;
   for (int j = 1; !s && j * n1 < N; j++) {
     const int32_t step = c->ns - (j * n1) % c->ns;
@@ -629,12 +633,12 @@ extern "C" hd_status hd_database_prerotate(hd_context *c, const hd_eval_keys *ev
     if (!s && (e = cudaStreamSynchronize(c->stream))) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
   }
   if (!s && (e = cudaStreamSynchronize(c->stream))) s = hd_fail(HD_E_CUDA, cudaGetErrorString(e));
-  cudaFree(dig);
-  cudaFree(tmp);
-  cudaFree(u);
-  cudaFree(out);
-  cudaFree(kp);
-  cudaFree(gal);
+  dev_free(c, dig);
+  dev_free(c, tmp);
+  dev_free(c, u);
+  dev_free(c, out);
+  dev_free(c, kp);
+  dev_free(c, gal);
   if (!s) db->needs_prerotation = false;
   return s;
 }
