@@ -6,7 +6,7 @@
 A "step" is one pass of the whole hot path for one encrypted
 query over the whole database: hoisted baby steps, the diagonal MAC over every
 aggregate, rescale, giant rotations, fold.  Default workload (N = 1): BASELINE.json's
-north-star configuration "ring 2^16, VECTOR_DIM = 512, 2^20 db vectors" (C4, n1 = 64,
+north-star configuration "ring 2^16, VECTOR_DIM = 512, 2^20 db vectors" (C4, n1 = 128,
 all 64 aggregates on one B200; 51.5 GB of diagonal plaintexts, larger than L2, so no
 L2 flush is needed between steps).  Under torchrun (N > 1) the database is sharded by
 aggregate (strong scaling: the 2^20 database is fixed); rank 0 broadcasts the query
@@ -360,7 +360,21 @@ def main():
     if world > 1:
         dist.broadcast(nb, 0)
     ct_bytes = int(nb.item())
-    qbuf = torch.empty(Q * ct_bytes, dtype=torch.uint8, device=dev)
+    xch = None
+    # results leave a rank level-reduced to 1 limb (R24); the membership partial sums are
+    # inputs of rank 0's RotateAndSum and travel at their full level (out_limbs)
+    out_nl = 0 if args.scenario == "membership" else 1
+    if world > 1:
+        # per-step collectives on buffers sized once from the static shard map (no size
+        # exchange, no host sync, no allocation inside step()): the query broadcast and the
+        # gather of the exported results
+        res_limbs = out_limbs if args.scenario == "membership" else 1
+        out_ct_bytes = 64 + 2 * res_limbs * (1 << cfg.log_n) * 8
+        per_rank = [1] * world if args.scenario == "membership" else [Q * s for s in hdd.shard_sizes(A, world)]
+        xch = hdd.StepExchange(Q * ct_bytes, per_rank, out_ct_bytes, dev)
+        qbuf = xch.qbuf
+    else:
+        qbuf = torch.empty(Q * ct_bytes, dtype=torch.uint8, device=dev)
     if rank == 0:
         for i, qc in enumerate(qcts):
             ctx.ciphertext_export(qc, (qbuf.data_ptr() + i * ct_bytes, ct_bytes), on_device=True)
@@ -385,8 +399,7 @@ def main():
     mem = None
     part = [None]   # membership under sharding: this rank's EvalAddMany
     parts_in = []   # rank 0: the gathered partial sums
-    out_ct_bytes = None
-    gbuf = None
+    gathered = [None]  # rank 0: views (ptr, bytes) of every rank's exported results (last step)
 
     def results():
         """the step's result ciphertexts: scores, comparisons, or the (per-rank) membership sum"""
@@ -394,10 +407,13 @@ def main():
             return [mem]
         return cmps if tail else outs
 
+    def export_into(ct_, ptr, cap):
+        ctx.ciphertext_export_level(ct_, (ptr, cap), nlimbs=out_nl, on_device=True)
+
     def step():
-        nonlocal outs, outs_b, cmps, mem, out_ct_bytes, gbuf
+        nonlocal outs, outs_b, cmps, mem
         if world > 1:  # a1: query broadcast over NCCL, imported in place (no allocation)
-            dist.broadcast(qbuf, 0)
+            xch.broadcast_query()
             if rank != 0:
                 for i in range(Q):
                     ctx.ciphertext_import_into(qcts[i], qbuf.data_ptr() + i * ct_bytes, ct_bytes, on_device=True)
@@ -420,19 +436,15 @@ def main():
                     part[0] = ctx.eval_add_many(cmps, part[0])
         if world > 1:  # a9: result ciphertexts gathered to rank 0 over NCCL
             res = part if args.scenario == "membership" else results()
-            if out_ct_bytes is None:
-                out_ct_bytes = ctx.ciphertext_export_size(res[0])
-                gbuf = torch.empty(len(res) * out_ct_bytes, dtype=torch.uint8, device=dev)
-            for i, o in enumerate(res):
-                ctx.ciphertext_export(o, (gbuf.data_ptr() + i * out_ct_bytes, out_ct_bytes), on_device=True)
-            per_rank = 1 if args.scenario == "membership" else Q * ((A + world - 1) // world)
-            got = hdd.gather_bytes(gbuf, per_rank * out_ct_bytes, 0)
+            got = xch.gather(res, export_into)
+            gathered[0] = got
             if args.scenario == "membership" and rank == 0:
-                if not parts_in:  # setup on the first step: one ciphertext per rank
-                    parts_in.extend(ctx.ciphertext_import(g.data_ptr(), out_ct_bytes, on_device=True) for g in got)
+                views = [v for per in got for v in per]  # one partial sum per rank
+                if not parts_in:  # setup on the first (warm-up) step: one ciphertext per rank
+                    parts_in.extend(ctx.ciphertext_import(p_, b_, on_device=True) for p_, b_ in views)
                 else:
-                    for ct_, g in zip(parts_in, got):
-                        ctx.ciphertext_import_into(ct_, g.data_ptr(), out_ct_bytes, on_device=True)
+                    for ct_, (p_, b_) in zip(parts_in, views):
+                        ctx.ciphertext_import_into(ct_, p_, b_, on_device=True)
                 mem = ctx.membership(evk, parts_in, mem)
 
     clk = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ else local)

@@ -289,6 +289,13 @@ hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, size_t cap, i
  * and duplicates.  Synchronises the context stream. */
 hd_status hd_ciphertext_import(hd_context *ctx, const void *src, size_t bytes, int src_on_device,
                                hd_ciphertext **out);
+/* hd_ciphertext_export at a reduced level: the first nlimbs limbs of c0 and c1 (0 = all;
+ * dropping limbs is exact modular reduction, R24).  Stream-ordered on the context stream
+ * after the ciphertext's last writer: a device destination never synchronises the host
+ * (the multi-GPU result gather); a host destination is complete on return.
+ * HD_E_LEVEL if nlimbs > limbs. */
+hd_status hd_ciphertext_export_level(const hd_ciphertext *ct, uint32_t nlimbs, void *dst, size_t cap,
+                                     int dst_on_device, size_t *written);
 /* In-place import into an existing ciphertext of the same shape (no allocation).
  * Host sources are uploaded asynchronously on the context's upload stream, after the
  * ciphertext's last reader (the baby steps of an hd_query on it) and last writer; pinned

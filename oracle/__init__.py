@@ -47,12 +47,13 @@ def build(force: bool = False) -> str:
 class Params(C.Structure):
     _fields_ = [("log_n", C.c_int32), ("n", C.c_int32), ("num_slots", C.c_int32),
                 ("L", C.c_int32), ("q0_bits", C.c_int32), ("scale_bits", C.c_int32),
-                ("special_bits", C.c_int32), ("pad_", C.c_int32),
-                ("mod", C.c_uint64 * 8), ("psi", C.c_uint64 * 8), ("seed", C.c_uint64)]
+                ("special_bits", C.c_int32), ("K_sp", C.c_int32), ("alpha", C.c_int32), ("pad_", C.c_int32),
+                ("mod", C.c_uint64 * 20), ("psi", C.c_uint64 * 20), ("seed", C.c_uint64)]
 
     @property
     def moduli(self):
-        return [int(self.mod[i]) for i in range(self.L + 1)]
+        """q_0..q_{L-1}, then the special primes p_0..p_{K-1}"""
+        return [int(self.mod[i]) for i in range(self.L + self.K_sp)]
 
 
 def lib():
@@ -83,13 +84,23 @@ def u64(shape):
 class Oracle:
     """Thin stateful wrapper: parameters + convenience shapes."""
 
-    def __init__(self, log_n: int, L: int = 3, seed: int = 1):
+    def __init__(self, log_n: int, L: int = 3, seed: int = 1, K_sp: int = 1, alpha: int = 1):
+        """K_sp special primes and alpha limbs per key-switching digit (R31); the defaults are
+        the north-star profile (R11: alpha = 1, one special prime P)."""
         self.p = Params()
-        _check("or_params_init", lib().or_params_init(C.byref(self.p), log_n, L, C.c_uint64(seed)))
+        _check("or_params_init_ex", lib().or_params_init_ex(C.byref(self.p), log_n, L, K_sp, alpha,
+                                                            C.c_uint64(seed)))
         self.n = self.p.n
         self.ns = self.p.num_slots
         self.L = self.p.L
+        self.K = K_sp
+        self.alpha = alpha
+        self.M = self.L + K_sp          # moduli of a key: Q_L u P
+        self.beta = -(-self.L // alpha)  # digits of a top-level key
         self.log_n = log_n
+
+    def num_digits(self, ell):
+        return -(-ell // self.alpha)
 
     # -- ring --------------------------------------------------------------
     def ntt(self, a, l, inverse=False):
@@ -141,12 +152,12 @@ class Oracle:
     # -- keys / encryption --------------------------------------------------------
     def secret_key(self):
         s = np.zeros(self.n, dtype=np.int64)
-        s_ntt = u64((self.L + 1, self.n))
+        s_ntt = u64((self.M, self.n))
         _check("secret_key", lib().or_secret_key(C.byref(self.p), _p(s), _p(s_ntt)))
         return s, s_ntt
 
     def rotation_key(self, s_ntt, step):
-        key = u64((self.L, 2, self.L + 1, self.n))
+        key = u64((self.beta, 2, self.M, self.n))
         _check("rotation_key", lib().or_rotation_key(C.byref(self.p), _p(s_ntt), step, _p(key)))
         return key
 
@@ -166,9 +177,23 @@ class Oracle:
     # -- key switching -----------------------------------------------------------
     def modup(self, c1):
         ell = c1.shape[0]
-        dig = u64((ell, ell + 1, self.n))
+        dig = u64((self.num_digits(ell), ell + self.K, self.n))
         _check("modup", lib().or_modup(C.byref(self.p), _p(np.ascontiguousarray(c1)), ell, _p(dig)))
         return dig
+
+    def basis_convert(self, x, bidx, mi):
+        """R31 fast basis conversion of coefficient-form rows x[i] (modulo mod[bidx[i]]) into mod[mi]."""
+        x = np.ascontiguousarray(x, dtype=np.uint64)
+        b = np.ascontiguousarray(bidx, dtype=np.int32)
+        out = u64(self.n)
+        _check("basis_convert", lib().or_basis_convert(C.byref(self.p), _p(x), _p(b), len(b), mi, _p(out)))
+        return out
+
+    def moddown(self, u, ell):
+        u = np.ascontiguousarray(u, dtype=np.uint64)
+        out = u64((ell, self.n))
+        _check("moddown", lib().or_moddown(C.byref(self.p), _p(u), ell, _p(out)))
+        return out
 
     def rotate_hoisted(self, ct, dig, key, step):
         ell = ct.shape[1]
@@ -239,7 +264,7 @@ class Oracle:
 
     def keyset(self, s_ntt, steps):
         steps = np.asarray(steps, dtype=np.int32)
-        keys = u64((len(steps), self.L, 2, self.L + 1, self.n))
+        keys = u64((len(steps), self.beta, 2, self.M, self.n))
         for i, s in enumerate(steps):
             keys[i] = self.rotation_key(s_ntt, int(s))
         return steps, keys
@@ -371,7 +396,7 @@ class Oracle:
         return ct
 
     def relin_key(self, s_ntt):
-        key = u64((self.L, 2, self.L + 1, self.n))
+        key = u64((self.beta, 2, self.M, self.n))
         _check("relin_key", lib().or_relin_key(C.byref(self.p), _p(s_ntt), _p(key)))
         return key
 

@@ -104,8 +104,17 @@ static uint64_t min_root(uint64_t m, uint64_t n) {
 }
 
 int or_params_init(or_params *p, int32_t log_n, int32_t L, uint64_t seed) {
-  if (!p || log_n < 2 || log_n > 17 || L < 2 || L + 1 > OR_MAXMOD) return OR_E_PARAMS;
+  return or_params_init_ex(p, log_n, L, 1, 1, seed);
+}
+
+int32_t or_num_digits(const or_params *p, int32_t ell) { return (ell + p->alpha - 1) / p->alpha; }
+
+int or_params_init_ex(or_params *p, int32_t log_n, int32_t L, int32_t K_sp, int32_t alpha, uint64_t seed) {
+  if (!p || log_n < 2 || log_n > 17 || L < 2 || K_sp < 1 || alpha < 1 || alpha > L || L + K_sp > OR_MAXMOD)
+    return OR_E_PARAMS;
   memset(p, 0, sizeof(*p));
+  p->K_sp = K_sp;
+  p->alpha = alpha;
   p->log_n = log_n;
   p->n = 1 << log_n;
   p->num_slots = p->n / 2;
@@ -116,13 +125,14 @@ int or_params_init(or_params *p, int32_t log_n, int32_t L, uint64_t seed) {
   p->seed = seed;
   uint64_t two_n = 2 * (uint64_t)p->n;
   p->mod[0] = prev_ntt_prime((uint64_t)1 << p->q0_bits, two_n);
-  p->mod[L] = prev_ntt_prime(p->mod[0], two_n); /* P: next prime below q0 */
+  /* special primes: the next NTT primes below q0, descending (K = 1: P, R5) */
+  for (int k = 0; k < K_sp; k++) p->mod[L + k] = prev_ntt_prime(k ? p->mod[L + k - 1] : p->mod[0], two_n);
   uint64_t below = (uint64_t)1 << p->scale_bits;
   for (int i = 1; i < L; i++) {
     p->mod[i] = prev_ntt_prime(below, two_n);
     below = p->mod[i];
   }
-  for (int i = 0; i <= L; i++) {
+  for (int i = 0; i < L + K_sp; i++) {
     if (p->mod[i] == 0) return OR_E_PARAMS;
     p->psi[i] = min_root(p->mod[i], (uint64_t)p->n);
   }
@@ -133,7 +143,7 @@ int or_params_init(or_params *p, int32_t log_n, int32_t L, uint64_t seed) {
 /* NTT (R13).  Definition: a^[i] = sum_j a_j psi^{(2 br(i)+1) j} mod m.      */
 /* ------------------------------------------------------------------------ */
 int or_ntt_definition(const or_params *p, int32_t l, const uint64_t *a, uint64_t *out) {
-  if (l < 0 || l > p->L) return OR_E_ARG;
+  if (l < 0 || l >= p->L + p->K_sp) return OR_E_ARG;
   uint64_t m = p->mod[l];
   int n = p->n;
   for (int i = 0; i < n; i++) {
@@ -163,7 +173,7 @@ static uint64_t *psi_rev_table(const or_params *p, int32_t l, int inverse) {
 
 /* Cooley-Tukey, natural order in, bit-reversed evaluation order out. */
 int or_ntt_forward(const or_params *p, int32_t l, uint64_t *a) {
-  if (l < 0 || l > p->L) return OR_E_ARG;
+  if (l < 0 || l >= p->L + p->K_sp) return OR_E_ARG;
   uint64_t m = p->mod[l];
   int n = p->n;
   uint64_t *S = psi_rev_table(p, l, 0);
@@ -185,7 +195,7 @@ int or_ntt_forward(const or_params *p, int32_t l, uint64_t *a) {
 
 /* Gentleman-Sande inverse of the above, then multiply by n^{-1}. */
 int or_ntt_inverse(const or_params *p, int32_t l, uint64_t *a) {
-  if (l < 0 || l > p->L) return OR_E_ARG;
+  if (l < 0 || l >= p->L + p->K_sp) return OR_E_ARG;
   uint64_t m = p->mod[l];
   int n = p->n;
   uint64_t *S = psi_rev_table(p, l, 1);
@@ -500,7 +510,7 @@ int or_decode(const or_params *p, const uint64_t *pt, int32_t nlimbs, double del
 int or_secret_key(const or_params *p, int64_t *s_coeff, uint64_t *s_ntt) {
   int n = p->n;
   for (int j = 0; j < n; j++) s_coeff[j] = draw_ternary(p->seed, (uint32_t)j, 0, TAG_SECRET);
-  for (int l = 0; l <= p->L; l++) {
+  for (int l = 0; l < p->L + p->K_sp; l++) {
     uint64_t *row = s_ntt + (size_t)l * n;
     for (int j = 0; j < n; j++) row[j] = smod(s_coeff[j], p->mod[l]);
     or_ntt_forward(p, l, row);
@@ -508,23 +518,30 @@ int or_secret_key(const or_params *p, int64_t *s_coeff, uint64_t *s_ntt) {
   return OR_OK;
 }
 
-/* Hybrid key-switching key for sigma_g(s) -> s, alpha = 1 limb per digit,
- * one special prime P (R11):  b_d = -a_d s + e_d + [l == d] (P mod q_d) s'. */
-/* Switching key from s' to s (s' given in NTT form over all L+1 moduli):
- * b_d = -a_d s + e_d + [l == d] (P mod q_d) s', draws keyed by (obj, tag_a, tag_e). */
+/* P = prod_k p_k mod m */
+static uint64_t P_mod(const or_params *p, uint64_t m) {
+  uint64_t r = 1 % m;
+  for (int k = 0; k < p->K_sp; k++) r = mulmod(r, p->mod[p->L + k] % m, m);
+  return r;
+}
+
+/* Hybrid key-switching key (R11, R31) from s' to s (s' in NTT form over all L+K moduli):
+ * b_d = -a_d s + e_d + [l in I_d] (P mod q_l) s' for digit d = limbs I_d = [d alpha,
+ * (d+1) alpha) (alpha = K = 1: [l == d] (P mod q_d) s'); draws keyed by (obj, tag_a, tag_e),
+ * a at modulus index l in [q_0..q_{L-1}, p_0..p_{K-1}] (R14), sub = digit. */
 static void switch_key(const or_params *p, const uint64_t *s_ntt, const uint64_t *sp_ntt, uint32_t obj,
                        uint32_t tag_a, uint32_t tag_e, uint64_t *key) {
-  int n = p->n, L = p->L;
+  int n = p->n, L = p->L, M = p->L + p->K_sp, beta = or_num_digits(p, L);
   uint64_t *e_ntt = malloc(sizeof(uint64_t) * n);
-  for (int d = 0; d < L; d++) {
-    for (int l = 0; l <= L; l++) {
+  for (int d = 0; d < beta; d++) {
+    for (int l = 0; l < M; l++) {
       uint64_t m = p->mod[l];
       for (int j = 0; j < n; j++)
         e_ntt[j] = smod(draw_cbd21(p->seed, (uint32_t)j, obj, tag_e, (uint32_t)d), m);
       or_ntt_forward(p, l, e_ntt);
-      uint64_t *kb = key + (((size_t)d * 2 + 0) * (L + 1) + l) * n;
-      uint64_t *ka = key + (((size_t)d * 2 + 1) * (L + 1) + l) * n;
-      uint64_t gad = (l == d) ? p->mod[L] % m : 0; /* (P mod q_d) on limb d only */
+      uint64_t *kb = key + (((size_t)d * 2 + 0) * M + l) * n;
+      uint64_t *ka = key + (((size_t)d * 2 + 1) * M + l) * n;
+      uint64_t gad = (l < L && l / p->alpha == d) ? P_mod(p, m) : 0; /* (P mod q_l) on digit d's limbs */
       for (int j = 0; j < n; j++) {
         uint64_t a = draw_uniform(p->seed, (uint32_t)j, (uint32_t)l, obj, tag_a, (uint32_t)d, m);
         uint64_t b = submod(e_ntt[j], mulmod(a, s_ntt[(size_t)l * n + j], m), m);
@@ -543,10 +560,10 @@ int or_rotation_key(const or_params *p, const uint64_t *s_ntt, int64_t step, uin
   uint64_t g = or_galois_elt(p, step);
   /* s' = sigma_g(s) from the coefficient-domain definition */
   int64_t *s = malloc(sizeof(int64_t) * n), *sp = malloc(sizeof(int64_t) * n);
-  uint64_t *sp_ntt = malloc(sizeof(uint64_t) * (size_t)(L + 1) * n);
+  uint64_t *sp_ntt = malloc(sizeof(uint64_t) * (size_t)(L + p->K_sp) * n);
   for (int j = 0; j < n; j++) s[j] = draw_ternary(p->seed, (uint32_t)j, 0, TAG_SECRET);
   or_automorph_coeff(p, g, s, sp);
-  for (int l = 0; l <= L; l++) {
+  for (int l = 0; l < L + p->K_sp; l++) {
     uint64_t *row = sp_ntt + (size_t)l * n;
     for (int j = 0; j < n; j++) row[j] = smod(sp[j], p->mod[l]);
     or_ntt_forward(p, l, row);
@@ -560,8 +577,8 @@ int or_rotation_key(const or_params *p, const uint64_t *s_ntt, int64_t step, uin
  * s^2 in NTT form is the pointwise square of s_ntt (the negacyclic product). */
 int or_relin_key(const or_params *p, const uint64_t *s_ntt, uint64_t *key) {
   int n = p->n, L = p->L;
-  uint64_t *s2 = malloc(sizeof(uint64_t) * (size_t)(L + 1) * n);
-  for (int l = 0; l <= L; l++)
+  uint64_t *s2 = malloc(sizeof(uint64_t) * (size_t)(L + p->K_sp) * n);
+  for (int l = 0; l < L + p->K_sp; l++)
     for (int j = 0; j < n; j++) {
       size_t o = (size_t)l * n + j;
       s2[o] = mulmod(s_ntt[o], s_ntt[o], p->mod[l]);
@@ -652,29 +669,62 @@ int or_decrypt(const or_params *p, const uint64_t *s_ntt, const uint64_t *ct, in
 }
 
 /* ------------------------------------------------------------------------ */
-/* Key switching (P:L479-496 hoisting; R11, R12).                            */
-/* ext modulus index e in [0, ell]: e < ell -> q_e, e == ell -> P = mod[L].   */
+/* Key switching (P:L479-496 hoisting; R11, R12, R31).                       */
+/* ext modulus index e in [0, ell+K): e < ell -> q_e, e >= ell -> p_{e-ell}.  */
 /* ------------------------------------------------------------------------ */
-static int ext_mod_index(const or_params *p, int ell, int e) { return e < ell ? e : p->L; }
+static int ext_mod_index(const or_params *p, int ell, int e) { return e < ell ? e : p->L + (e - ell); }
 
-/* ModUp ("EvalFastRotationPrecompute"): digit d = centred INTT of limb d,
- * lifted into every other modulus of Q_ell u {P}, then NTT. */
-int or_modup(const or_params *p, const uint64_t *c1, int32_t ell, uint64_t *dig) {
+/* Fast basis conversion with centred digits (R12, R31): the residues x_i (coefficient
+ * form) of one integer X modulo the basis B = {b_i}, i < cnt, map to
+ *   sum_i y_i (B / b_i) mod m,   y_i = centred([x_i (B / b_i)^{-1}]_{b_i}),
+ * an integer congruent to X mod B with |.| <= cnt B / 2.  For one modulus (cnt = 1) this is
+ * the centred lift of x_0 (the alpha = K = 1 case of R12). */
+static void basis_convert(const or_params *p, const uint64_t *const *x, const int *bidx, int cnt, int mi,
+                          uint64_t *out) {
   int n = p->n;
+  uint64_t m = p->mod[mi];
+  for (int j = 0; j < n; j++) out[j] = 0;
+  for (int i = 0; i < cnt; i++) {
+    uint64_t b = p->mod[bidx[i]], hat_b = 1, hat_m = 1 % m; /* B / b_i mod b_i and mod m */
+    for (int k = 0; k < cnt; k++) {
+      if (k == i) continue;
+      hat_b = mulmod(hat_b, p->mod[bidx[k]] % b, b);
+      hat_m = mulmod(hat_m, p->mod[bidx[k]] % m, m);
+    }
+    uint64_t inv = invmod(hat_b, b);
+    for (int j = 0; j < n; j++) {
+      int64_t y = centre(mulmod(x[i][j], inv, b), b);
+      out[j] = addmod(out[j], mulmod(smod(y, m), hat_m, m), m);
+    }
+  }
+}
+
+/* ModUp ("EvalFastRotationPrecompute"): digit d = limbs I_d = [d alpha,
+ * min((d+1) alpha, ell)) of c1, INTT, fast-basis-converted (centred) into every modulus of
+ * Q_ell u P, NTT.  Rows of the digit's own limbs equal c1 (the conversion is exact there).
+ * dig: [beta(ell)][ell+K][n]. */
+int or_modup(const or_params *p, const uint64_t *c1, int32_t ell, uint64_t *dig) {
+  int n = p->n, ext = ell + p->K_sp, beta = or_num_digits(p, ell);
   if (ell < 1 || ell > p->L) return OR_E_ARG;
-  uint64_t *x = malloc(sizeof(uint64_t) * n);
-  for (int d = 0; d < ell; d++) {
-    uint64_t qd = p->mod[d];
-    memcpy(x, c1 + (size_t)d * n, sizeof(uint64_t) * n);
-    or_ntt_inverse(p, d, x);
-    for (int e = 0; e <= ell; e++) {
-      uint64_t *row = dig + ((size_t)d * (ell + 1) + e) * n;
+  uint64_t *x = malloc(sizeof(uint64_t) * (size_t)p->alpha * n);
+  const uint64_t *xr[OR_MAXMOD];
+  int bidx[OR_MAXMOD];
+  for (int d = 0; d < beta; d++) {
+    int lo = d * p->alpha, hi = lo + p->alpha < ell ? lo + p->alpha : ell, cnt = hi - lo;
+    for (int i = 0; i < cnt; i++) {
+      memcpy(x + (size_t)i * n, c1 + (size_t)(lo + i) * n, sizeof(uint64_t) * n);
+      or_ntt_inverse(p, lo + i, x + (size_t)i * n);
+      xr[i] = x + (size_t)i * n;
+      bidx[i] = lo + i;
+    }
+    for (int e = 0; e < ext; e++) {
+      uint64_t *row = dig + ((size_t)d * ext + e) * n;
       int mi = ext_mod_index(p, ell, e);
-      if (e == d) {
-        memcpy(row, c1 + (size_t)d * n, sizeof(uint64_t) * n);
+      if (e >= lo && e < hi) {
+        memcpy(row, c1 + (size_t)e * n, sizeof(uint64_t) * n);
         continue;
       }
-      for (int j = 0; j < n; j++) row[j] = smod(centre(x[j], qd), p->mod[mi]);
+      basis_convert(p, xr, bidx, cnt, mi, row);
       or_ntt_forward(p, mi, row);
     }
   }
@@ -682,39 +732,68 @@ int or_modup(const or_params *p, const uint64_t *c1, int32_t ell, uint64_t *dig)
   return OR_OK;
 }
 
-/* ModDown: u'[q] = (u[q] - NTT_q([INTT_P(u[P])]_centred)) * P^{-1} mod q. */
-static void moddown(const or_params *p, uint64_t *u /* (ell+1) x n */, int ell, uint64_t *out) {
-  int n = p->n;
-  uint64_t P = p->mod[p->L];
-  uint64_t *y = malloc(sizeof(uint64_t) * n), *t = malloc(sizeof(uint64_t) * n);
-  memcpy(y, u + (size_t)ell * n, sizeof(uint64_t) * n);
-  or_ntt_inverse(p, p->L, y);
+/* ModDown: u'[q] = (u[q] - NTT_q(Conv_{P->q}(INTT_P(u[P])))) * P^{-1} mod q, the conversion
+ * of the K special residues centred as in ModUp (K = 1: the centred lift of INTT_P(u[P])).
+ * u: (ell+K) x n. */
+static void moddown(const or_params *p, uint64_t *u, int ell, uint64_t *out) {
+  int n = p->n, K = p->K_sp;
+  uint64_t *y = malloc(sizeof(uint64_t) * (size_t)K * n), *t = malloc(sizeof(uint64_t) * n);
+  const uint64_t *yr[OR_MAXMOD];
+  int bidx[OR_MAXMOD];
+  for (int k = 0; k < K; k++) {
+    memcpy(y + (size_t)k * n, u + (size_t)(ell + k) * n, sizeof(uint64_t) * n);
+    or_ntt_inverse(p, p->L + k, y + (size_t)k * n);
+    yr[k] = y + (size_t)k * n;
+    bidx[k] = p->L + k;
+  }
   for (int l = 0; l < ell; l++) {
     uint64_t q = p->mod[l];
-    for (int j = 0; j < n; j++) t[j] = smod(centre(y[j], P), q);
+    basis_convert(p, yr, bidx, K, l, t);
     or_ntt_forward(p, l, t);
-    uint64_t pinv = invmod(P % q, q);
+    uint64_t pinv = invmod(P_mod(p, q), q);
     for (int j = 0; j < n; j++) out[(size_t)l * n + j] = mulmod(submod(u[(size_t)l * n + j], t[j], q), pinv, q);
   }
   free(y); free(t);
 }
 
-/* "EvalFastRotation": permute digits by pi_g in the NTT domain, key
- * inner product over Q_ell u {P}, ModDown, add pi_g(c0). */
+int or_basis_convert(const or_params *p, const uint64_t *x, const int32_t *bidx, int32_t cnt, int32_t mi,
+                     uint64_t *out) {
+  const uint64_t *xr[OR_MAXMOD];
+  int bi[OR_MAXMOD];
+  if (cnt < 1 || cnt > OR_MAXMOD || mi < 0 || mi >= p->L + p->K_sp) return OR_E_ARG;
+  for (int i = 0; i < cnt; i++) {
+    if (bidx[i] < 0 || bidx[i] >= p->L + p->K_sp) return OR_E_ARG;
+    xr[i] = x + (size_t)i * p->n;
+    bi[i] = bidx[i];
+  }
+  basis_convert(p, xr, bi, cnt, mi, out);
+  return OR_OK;
+}
+
+int or_moddown(const or_params *p, const uint64_t *u, int32_t ell, uint64_t *out) {
+  if (ell < 1 || ell > p->L) return OR_E_ARG;
+  size_t sz = sizeof(uint64_t) * (size_t)(ell + p->K_sp) * p->n;
+  uint64_t *w = malloc(sz);
+  memcpy(w, u, sz);
+  moddown(p, w, ell, out);
+  free(w);
+  return OR_OK;
+}
+
 /* Key inner product in the extended basis: u[pp][e] += sum_d pi_g(dig_d)[e] * key[d][pp][e]
- * (u: 2 x (ell+1) x n, accumulated, so several rotations can share one ModDown). */
+ * (u: 2 x (ell+K) x n, accumulated, so several rotations can share one ModDown). */
 static void kip_accumulate(const or_params *p, const uint64_t *dig, int32_t ell, const uint64_t *key,
                            uint64_t g, uint64_t *u) {
-  int n = p->n, L = p->L;
+  int n = p->n, M = p->L + p->K_sp, ext = ell + p->K_sp, beta = or_num_digits(p, ell);
   uint64_t *perm = malloc(sizeof(uint64_t) * n);
-  for (int d = 0; d < ell; d++) {
-    for (int e = 0; e <= ell; e++) {
+  for (int d = 0; d < beta; d++) {
+    for (int e = 0; e < ext; e++) {
       int mi = ext_mod_index(p, ell, e);
       uint64_t m = p->mod[mi];
-      or_automorph_ntt(p, g, dig + ((size_t)d * (ell + 1) + e) * n, perm);
+      or_automorph_ntt(p, g, dig + ((size_t)d * ext + e) * n, perm);
       for (int pp = 0; pp < 2; pp++) {
-        const uint64_t *k = key + (((size_t)d * 2 + pp) * (L + 1) + mi) * n;
-        uint64_t *acc = u + ((size_t)pp * (ell + 1) + e) * n;
+        const uint64_t *k = key + (((size_t)d * 2 + pp) * M + mi) * n;
+        uint64_t *acc = u + ((size_t)pp * ext + e) * n;
         for (int j = 0; j < n; j++) acc[j] = addmod(acc[j], mulmod(perm[j], k[j], m), m);
       }
     }
@@ -722,17 +801,19 @@ static void kip_accumulate(const or_params *p, const uint64_t *dig, int32_t ell,
   free(perm);
 }
 
+/* "EvalFastRotation": permute digits by pi_g in the NTT domain, key inner
+ * product over Q_ell u P, ModDown, add pi_g(c0). */
 int or_rotate_hoisted(const or_params *p, const uint64_t *ct, const uint64_t *dig, int32_t ell,
                       const uint64_t *key, int64_t step, uint64_t *out) {
-  int n = p->n, L = p->L;
+  int n = p->n, L = p->L, ext = ell + p->K_sp;
   if (ell < 1 || ell > L) return OR_E_ARG;
   uint64_t g = or_galois_elt(p, step);
-  uint64_t *u = calloc((size_t)2 * (ell + 1) * n, sizeof(uint64_t));
+  uint64_t *u = calloc((size_t)2 * ext * n, sizeof(uint64_t));
   uint64_t *perm = malloc(sizeof(uint64_t) * n);
   kip_accumulate(p, dig, ell, key, g, u);
   uint64_t *u0 = malloc(sizeof(uint64_t) * (size_t)ell * n), *u1 = malloc(sizeof(uint64_t) * (size_t)ell * n);
   moddown(p, u, ell, u0);
-  moddown(p, u + (size_t)(ell + 1) * n, ell, u1);
+  moddown(p, u + (size_t)ext * n, ell, u1);
   for (int l = 0; l < ell; l++) {
     uint64_t q = p->mod[l];
     or_automorph_ntt(p, g, ct + (size_t)l * n, perm);
@@ -745,10 +826,14 @@ int or_rotate_hoisted(const or_params *p, const uint64_t *ct, const uint64_t *di
   return OR_OK;
 }
 
+static size_t dig_elems(const or_params *p, int ell) {
+  return (size_t)or_num_digits(p, ell) * (ell + p->K_sp) * p->n;
+}
+
 int or_rotate(const or_params *p, const uint64_t *ct, int32_t ell, const uint64_t *key,
               int64_t step, uint64_t *out) {
   int n = p->n;
-  uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)ell * (ell + 1) * n);
+  uint64_t *dig = malloc(sizeof(uint64_t) * dig_elems(p, ell));
   int rc = or_modup(p, ct + (size_t)ell * n, ell, dig);
   if (rc == OR_OK) rc = or_rotate_hoisted(p, ct, dig, ell, key, step, out);
   free(dig);
@@ -1092,7 +1177,7 @@ int or_rotation_steps(const or_params *p, int32_t N, int32_t n1, int32_t *steps,
 
 static const uint64_t *find_key(const or_params *p, const int32_t *steps, int32_t nkeys,
                                 const uint64_t *keys, int64_t step) {
-  size_t ksz = (size_t)p->L * 2 * (p->L + 1) * p->n;
+  size_t ksz = (size_t)or_num_digits(p, p->L) * 2 * (p->L + p->K_sp) * p->n;
   for (int i = 0; i < nkeys; i++)
     if (steps[i] == step) return keys + ksz * i;
   return NULL;
@@ -1103,7 +1188,7 @@ int or_baby_steps(const or_params *p, const uint64_t *q_ct, int32_t n1, const in
                   int32_t nkeys, const uint64_t *keys, uint64_t *r) {
   int n = p->n, L = p->L;
   size_t ctsz = (size_t)2 * L * n;
-  uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)L * (L + 1) * n);
+  uint64_t *dig = malloc(sizeof(uint64_t) * dig_elems(p, L));
   or_modup(p, q_ct + (size_t)L * n, L, dig); /* preV */
   memcpy(r, q_ct, sizeof(uint64_t) * ctsz);  /* r[0] = ct */
   int rc = OR_OK;
@@ -1191,8 +1276,8 @@ static int giant_sum_ct_range(const or_params *p, const uint64_t *r, int32_t n1,
 int or_relinearize(const or_params *p, const uint64_t *S3, int32_t ell, const uint64_t *rlk, uint64_t *out) {
   int n = p->n;
   if (ell < 1 || ell > p->L) return OR_E_ARG;
-  size_t ext = (size_t)(ell + 1) * n;
-  uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)ell * (ell + 1) * n);
+  size_t ext = (size_t)(ell + p->K_sp) * n;
+  uint64_t *dig = malloc(sizeof(uint64_t) * dig_elems(p, ell));
   uint64_t *u = calloc(2 * ext, sizeof(uint64_t));
   uint64_t *u0 = malloc(sizeof(uint64_t) * (size_t)ell * n), *u1 = malloc(sizeof(uint64_t) * (size_t)ell * n);
   or_modup(p, S3 + (size_t)2 * ell * n, ell, dig);
@@ -1330,12 +1415,11 @@ static int scan_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32
                         const uint64_t *Dct, const uint64_t *rlk, int flat, const int32_t *steps, int32_t nkeys,
                         const uint64_t *keys, uint64_t *out, uint64_t *y_out) {
   int n = p->n, L = p->L, ell = L - 1;
-  size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * ell * n, ext = (size_t)(ell + 1) * n;
-  uint64_t P = p->mod[L];
+  size_t ctL = (size_t)2 * L * n, ct1 = (size_t)2 * ell * n, ext = (size_t)(ell + p->K_sp) * n;
   uint64_t *S = malloc(sizeof(uint64_t) * ctL), *Sp = malloc(sizeof(uint64_t) * ct1);
   uint64_t *T = malloc(sizeof(uint64_t) * ct1), *y = malloc(sizeof(uint64_t) * ct1);
-  uint64_t *yx = calloc(2 * ext, sizeof(uint64_t)); /* [pp][e][t], e == ell: P */
-  uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)ell * (ell + 1) * n);
+  uint64_t *yx = calloc(2 * ext, sizeof(uint64_t)); /* [pp][e][t], e >= ell: p_{e-ell} */
+  uint64_t *dig = malloc(sizeof(uint64_t) * dig_elems(p, ell));
   uint64_t *perm = malloc(sizeof(uint64_t) * n);
   uint64_t *S3 = Dct ? malloc(sizeof(uint64_t) * (size_t)3 * L * n) : NULL;
   int jmin, jmax, rc = OR_OK;
@@ -1359,13 +1443,13 @@ static int scan_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32
     }
     or_rescale(p, S, L, Sp);                                      /* Step 2c */
     int s = flat ? (j * n1) % p->num_slots : or_pre_rot(N, n1, j); /* Step 2d */
-    if (s == 0) { /* y_ext += P T_j (P limb += 0) */
+    if (s == 0) { /* y_ext += P T_j (P limbs += 0) */
       for (int pp = 0; pp < 2; pp++)
         for (int l = 0; l < ell; l++) {
           uint64_t q = p->mod[l];
           for (int t = 0; t < n; t++) {
             size_t o = (size_t)pp * ext + (size_t)l * n + t;
-            yx[o] = addmod(yx[o], mulmod(P % q, Sp[((size_t)pp * ell + l) * n + t], q), q);
+            yx[o] = addmod(yx[o], mulmod(P_mod(p, q), Sp[((size_t)pp * ell + l) * n + t], q), q);
           }
         }
       continue;
@@ -1380,7 +1464,7 @@ static int scan_hoisted(const or_params *p, const uint64_t *r, int32_t n1, int32
       or_automorph_ntt(p, g, Sp + (size_t)l * n, perm);
       for (int t = 0; t < n; t++) {
         size_t o = (size_t)l * n + t;
-        yx[o] = addmod(yx[o], mulmod(P % q, perm[t], q), q);
+        yx[o] = addmod(yx[o], mulmod(P_mod(p, q), perm[t], q), q);
       }
     }
   }
@@ -1518,6 +1602,7 @@ static or_cct cct_drop(const or_params *p, const or_cct *a, int ell) {
 int or_relin_rescale(const or_params *p, const uint64_t *S3, int32_t ell, const uint64_t *rlk, uint64_t *out) {
   int n = p->n, L = p->L;
   if (ell < 2 || ell > L) return OR_E_ARG;
+  if (p->K_sp != 1 || p->alpha != 1) return OR_E_PARAMS; /* the two-modulus CRT identity needs one P */
   size_t ext = (size_t)(ell + 1) * n;
   uint64_t *dig = malloc(sizeof(uint64_t) * (size_t)ell * (ell + 1) * n);
   uint64_t *u = calloc(2 * ext, sizeof(uint64_t));

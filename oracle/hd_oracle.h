@@ -19,10 +19,11 @@
  *                          order  a^[i] = sum_j a_j psi^{(2 br(i)+1) j}   (R13)
  *   plaintext (ell limbs) [limb][n]
  *   ciphertext (ell) .... [poly 0..1][limb][n]
- *   rotation key ........ [digit d < L][poly (0=b,1=a)][modulus l <= L][n]
- *                          modulus index L is the special prime P.
- *   modup digits (ell) .. [digit d < ell][ext modulus e <= ell][n]
- *                          ext index e < ell is q_e, e == ell is P.
+ *   rotation key ........ [digit d < beta(L)][poly (0=b,1=a)][modulus l < L+K][n]
+ *                          modulus indices L..L+K-1 are the special primes p_k.
+ *   modup digits (ell) .. [digit d < beta(ell)][ext modulus e < ell+K][n]
+ *                          ext index e < ell is q_e, e >= ell is p_{e-ell}.
+ *   (alpha = K = 1, the north-star profile: beta(ell) = ell digits, one special prime P.)
  *
  * Every function returns 0 on success or a negative error code:
  */
@@ -41,7 +42,7 @@ extern "C" {
 #define OR_E_MISSING_KEY (-5)
 #define OR_E_RANGE (-6)
 
-#define OR_MAXMOD 8
+#define OR_MAXMOD 20
 
 typedef struct {
   int32_t log_n;      /* ring degree n = 2^log_n                         */
@@ -51,13 +52,22 @@ typedef struct {
   int32_t q0_bits;    /* 60                                              */
   int32_t scale_bits; /* 45  ("scaling factor is set to 45")     */
   int32_t special_bits; /* 60 */
+  int32_t K_sp;       /* special primes p_0..p_{K-1} (P = their product)  */
+  int32_t alpha;      /* limbs per key-switching digit (R11, R31)        */
   int32_t pad_;
-  uint64_t mod[OR_MAXMOD]; /* mod[0..L-1] = q_i, mod[L] = P              */
+  uint64_t mod[OR_MAXMOD]; /* mod[0..L-1] = q_i, mod[L..L+K-1] = p_k     */
   uint64_t psi[OR_MAXMOD]; /* smallest primitive 2n-th root of unity      */
   uint64_t seed;           /* Philox key for the secret / rotation keys   */
 } or_params;
 
 int or_params_init(or_params *p, int32_t log_n, int32_t L, uint64_t seed);
+/* General hybrid key-switching profile (R31; SURVEY 8(d) "paper-depth": L = 12, alpha = 4,
+ * K_sp = 4): K_sp special primes (the next NTT primes below q0, descending) and alpha
+ * limbs per digit.  or_params_init = or_params_init_ex(.., K_sp = 1, alpha = 1, ..). */
+int or_params_init_ex(or_params *p, int32_t log_n, int32_t L, int32_t K_sp, int32_t alpha, uint64_t seed);
+/* beta(ell) = ceil(ell / alpha) digits of a ciphertext at ell limbs; digit d holds limbs
+ * [d alpha, min((d+1) alpha, ell)). */
+int32_t or_num_digits(const or_params *p, int32_t ell);
 int or_is_prime(uint64_t x);
 
 /* NTT over modulus index l (0..L); fast (textbook CT / GS) and definitional. */
@@ -81,7 +91,7 @@ int or_encode_coeffs(const or_params *p, const double *z, double delta, int64_t 
 int or_decode(const or_params *p, const uint64_t *pt, int32_t nlimbs, double delta, double *z);
 
 /* Keys and encryption (R11, R14). */
-int or_secret_key(const or_params *p, int64_t *s_coeff, uint64_t *s_ntt /* (L+1) x n */);
+int or_secret_key(const or_params *p, int64_t *s_coeff, uint64_t *s_ntt /* (L+K) x n */);
 int or_rotation_key(const or_params *p, const uint64_t *s_ntt, int64_t step, uint64_t *key);
 int or_encrypt(const or_params *p, const uint64_t *s_ntt, const uint64_t *pt, int32_t nlimbs,
                uint64_t enc_seed, uint64_t *ct);
@@ -95,8 +105,14 @@ int or_encrypt_pk(const or_params *p, const uint64_t *pk, const uint64_t *pt, in
                   uint64_t enc_seed, uint32_t obj, uint64_t *ct);
 int or_relin_key(const or_params *p, const uint64_t *s_ntt, uint64_t *key);
 
-/* Key switching pieces (R11, R12) at ciphertext level `ell` (limbs q_0..q_{ell-1}). */
+/* Key switching pieces (R11, R12, R31) at ciphertext level `ell` (limbs q_0..q_{ell-1}). */
 int or_modup(const or_params *p, const uint64_t *c1, int32_t ell, uint64_t *dig);
+/* Fast basis conversion with centred digits (R31): x [cnt][n] coefficient-form residues of
+ * one integer per coefficient modulo mod[bidx[i]] -> out[n] modulo mod[mi]. */
+int or_basis_convert(const or_params *p, const uint64_t *x, const int32_t *bidx, int32_t cnt, int32_t mi,
+                     uint64_t *out);
+/* ModDown of one polynomial u [(ell+K)][n] (NTT form over Q_ell u P) -> out [ell][n]. */
+int or_moddown(const or_params *p, const uint64_t *u, int32_t ell, uint64_t *out);
 int or_rotate_hoisted(const or_params *p, const uint64_t *ct, const uint64_t *dig, int32_t ell,
                       const uint64_t *key, int64_t step, uint64_t *out);
 int or_rotate(const or_params *p, const uint64_t *ct, int32_t ell, const uint64_t *key,

@@ -39,6 +39,7 @@ ABI_FUNCTIONS = [
     "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
     "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch", "hd_eval_add_many", "hd_baby_steps",
     "hd_query_baby", "hd_database_aggregate", "hd_compare_ex", "hd_enroll_footprint",
+    "hd_ciphertext_export_level",
 ]
 
 
@@ -116,6 +117,7 @@ def load():
             L.hd_ciphertext_export.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(C.c_size_t)]
             L.hd_ciphertext_import.argtypes = [VP, VP, C.c_size_t, C.c_int, C.POINTER(VP)]
             L.hd_ciphertext_import_into.argtypes = [VP, VP, C.c_size_t, C.c_int]
+            L.hd_ciphertext_export_level.argtypes = [VP, C.c_uint32, VP, C.c_size_t, C.c_int, C.POINTER(C.c_size_t)]
             L.hd_ciphertext_export_async.argtypes = [VP, C.c_uint32, VP, C.c_size_t, C.c_int, C.POINTER(C.c_size_t)]
             L.hd_context_synchronize.argtypes = [VP]
             L.hd_enroll_encrypted.argtypes = [VP, VP, VP, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
@@ -537,6 +539,19 @@ class Context(_Handle):
             return w.value
         ptr, cap = dst
         _check("hd_ciphertext_export_async", load().hd_ciphertext_export_async(
+            ct.h, nlimbs, VP(ptr), cap, 1 if on_device else 0, C.byref(w)))
+        return w.value
+
+    def ciphertext_export_level(self, ct, dst, nlimbs=0, on_device=True):
+        """hd_ciphertext_export_level: stream-ordered level-reduced export into ``dst`` = (ptr, cap)
+        (None: return the size).  A device destination never synchronises the host."""
+        w = C.c_size_t()
+        if dst is None:
+            _check("hd_ciphertext_export_level",
+                   load().hd_ciphertext_export_level(ct.h, nlimbs, None, 0, 0, C.byref(w)))
+            return w.value
+        ptr, cap = dst
+        _check("hd_ciphertext_export_level", load().hd_ciphertext_export_level(
             ct.h, nlimbs, VP(ptr), cap, 1 if on_device else 0, C.byref(w)))
         return w.value
 

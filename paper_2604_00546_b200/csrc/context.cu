@@ -370,11 +370,14 @@ extern "C" hd_status hd_ciphertext_limbs(const hd_ciphertext *ct, uint32_t *limb
   return HD_OK;
 }
 
-extern "C" hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, size_t cap, int dst_on_device,
-                                          size_t *written) {
+extern "C" hd_status hd_ciphertext_export_level(const hd_ciphertext *ct, uint32_t nlimbs, void *dst, size_t cap,
+                                                int dst_on_device, size_t *written) {
   if (!ct) return hd_fail(HD_E_INVALID_ARG, "null ciphertext");
   const hd_context *c = ct->ctx;
-  size_t payload = sizeof(uint64_t) * 2 * ct->limbs * c->n, total = sizeof(Header) + payload;
+  if (nlimbs == 0) nlimbs = ct->limbs;
+  if (nlimbs > ct->limbs) return hd_fail(HD_E_LEVEL, "cannot export more limbs than the ciphertext has");
+  const size_t limb_bytes = sizeof(uint64_t) * c->n;
+  size_t payload = 2 * nlimbs * limb_bytes, total = sizeof(Header) + payload;
   if (written) *written = total;
   if (!dst) return HD_OK;
   if (cap < total) return hd_fail(HD_E_INVALID_ARG, "export capacity too small");
@@ -382,15 +385,28 @@ extern "C" hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, si
   memcpy(h.magic, "HDBSGS01", 8);
   h.kind = 1;
   h.log_n = c->logn;
-  h.limbs = ct->limbs;
+  h.limbs = nlimbs;
   h.mod_fp = mod_fingerprint(c);
   h.payload = payload;
   h.scale = ct->scale;
   HD_CUDA(cudaStreamWaitEvent(c->stream, ct->ready, 0));  // last writer (e.g. hd_query's stream B)
   HD_CUDA(cudaMemcpyAsync(dst, &h, sizeof(h), kind_of(dst_on_device, 0), c->stream));
-  HD_CUDA(cudaMemcpyAsync((char *)dst + sizeof(h), ct->data, payload, kind_of(dst_on_device, 1), c->stream));
+  char *p = (char *)dst + sizeof(h);
+  const cudaMemcpyKind kind = kind_of(dst_on_device, 1);
+  if (nlimbs == ct->limbs) {
+    HD_CUDA(cudaMemcpyAsync(p, ct->data, payload, kind, c->stream));
+  } else {  // c0 limbs 0..nlimbs-1, then c1 limbs 0..nlimbs-1 (dropping the top limbs: R24)
+    HD_CUDA(cudaMemcpyAsync(p, ct->data, nlimbs * limb_bytes, kind, c->stream));
+    HD_CUDA(cudaMemcpyAsync(p + nlimbs * limb_bytes, ct->data + (size_t)ct->limbs * c->n, nlimbs * limb_bytes, kind,
+                            c->stream));
+  }
   if (!dst_on_device) HD_CUDA(cudaStreamSynchronize(c->stream));  // host copy complete on return
   return HD_OK;
+}
+
+extern "C" hd_status hd_ciphertext_export(const hd_ciphertext *ct, void *dst, size_t cap, int dst_on_device,
+                                          size_t *written) {
+  return hd_ciphertext_export_level(ct, 0, dst, cap, dst_on_device, written);
 }
 
 // Every residue row r (n words) must lie in [0, q_m) with m = chain[r % period]; rows of a

@@ -29,7 +29,6 @@
 
 namespace {
 constexpr int TC = 128;  // coefficients per aggregate per unit (one per consumer thread)
-constexpr int SPS = 4;   // baby steps per pipeline stage
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -102,13 +101,55 @@ __device__ __forceinline__ Unit decode(uint32_t u, uint32_t nag, int ngrp, int t
   return x;
 }
 
-// AG aggregates x TC coefficients consumer threads + one producer warp.
+// Producer state: the next (unit, baby-step block) to load and the ring slot it goes to.
+template <int AG, int JT, int QB, int SPS>
+struct Producer {
+  uint32_t u, units, nag, step;
+  int sb, nsb, ngrp, tiles, stage, stages, jmin, n1, N, qrows;
+  uint32_t phase;
+  uint64_t pol_stream, pol_keep;
+  __device__ __forceinline__ bool more() const { return u < units; }
+  // wait until the slot is free, then issue its TMA loads (D boxes evict-first, r evict-last)
+  __device__ __forceinline__ void issue(unsigned char *smem, uint64_t *full, uint64_t *empty, const CUtensorMap *tmD,
+                                        const CUtensorMap *tmR) {
+    constexpr int D_WORDS = AG * JT * SPS * TC, R_WORDS = QB * SPS * 2 * TC;
+    constexpr uint32_t STAGE_BYTES = (D_WORDS + R_WORDS) * 8;
+    const Unit x = decode(u, nag, ngrp, tiles, AG);
+    mbar_wait(&empty[stage], phase ^ 1);
+    mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+    uint64_t *base = reinterpret_cast<uint64_t *>(smem + (size_t)stage * STAGE_BYTES);
+#pragma unroll
+    for (int g = 0; g < AG; g++)
+#pragma unroll
+      for (int jj = 0; jj < JT; jj++) {
+        const int j = jmin + x.jg * JT + jj;
+        const int k0 = ((j * n1 + sb * SPS) % N + N) % N;  // SPS consecutive diagonals (no wrap)
+        tma_load_3d(base + (g * JT + jj) * SPS * TC, tmD, x.tile * TC, x.m, (int)((x.a0 + g) * N + k0), &full[stage],
+                    pol_stream);
+      }
+#pragma unroll
+    for (int b = 0; b < QB; b++)
+      tma_load_3d(base + D_WORDS + b * SPS * 2 * TC, tmR, x.tile * TC, x.m, b * qrows + sb * SPS * 2, &full[stage],
+                  pol_keep);
+    if (++stage == stages) {
+      stage = 0;
+      phase ^= 1;
+    }
+    if (++sb == nsb) {
+      sb = 0;
+      u += step;
+    }
+  }
+};
+
+// AG aggregates x TC coefficients consumer threads (+ one producer warp unless INLINE: then
+// thread 0 also issues the loads, one slot per iteration, and all 4 AG warps compute).
 // Stage layout (u64): D[AG][JT][SPS][TC], then r[QB][SPS][2][TC].
-template <int AG, int JT, int QB, bool FLUSH>
-__global__ void __launch_bounds__(AG *TC + 32, 1)
+template <int AG, int JT, int QB, int SPS, bool FLUSH, bool INLINE>
+__global__ void __launch_bounds__(AG *TC + (INLINE ? 0 : 32), 1)
     mac_tma_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmR,
                    uint64_t *__restrict__ S, int n1, int N, int L, int logn, int jmin, int nj, uint32_t A,
-                   int stages, int qrows, size_t s_query_stride, ModTab mt) {
+                   int stages, int qrows, size_t s_query_stride, ModTab mt, int dry) {
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int D_WORDS = AG * JT * SPS * TC, R_WORDS = QB * SPS * 2 * TC;
   constexpr uint32_t STAGE_BYTES = (D_WORDS + R_WORDS) * 8;
@@ -125,41 +166,35 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-
-  if (threadIdx.x >= CONSUMERS) {  // ---------------- producer warp ----------------
-    if (threadIdx.x != CONSUMERS) return;
-    uint64_t pol_stream, pol_keep;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
-    int stage = 0;
-    uint32_t phase = 0;
-    for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-      const Unit x = decode(u, nag, ngrp, tiles, AG);
-      for (int sb = 0; sb < nsb; sb++) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-        uint64_t *base = reinterpret_cast<uint64_t *>(smem + (size_t)stage * STAGE_BYTES);
-#pragma unroll
-        for (int g = 0; g < AG; g++)
-#pragma unroll
-          for (int jj = 0; jj < JT; jj++) {
-            const int j = jmin + x.jg * JT + jj;
-            const int k0 = ((j * n1 + sb * SPS) % N + N) % N;  // SPS consecutive diagonals (no wrap)
-            tma_load_3d(base + (g * JT + jj) * SPS * TC, &tmD, x.tile * TC, x.m, (int)((x.a0 + g) * N + k0),
-                        &full[stage], pol_stream);
-          }
-#pragma unroll
-        for (int b = 0; b < QB; b++)
-          tma_load_3d(base + D_WORDS + b * SPS * 2 * TC, &tmR, x.tile * TC, x.m, b * qrows + sb * SPS * 2,
-                      &full[stage], pol_keep);
-        if (++stage == stages) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
+  Producer<AG, JT, QB, SPS> pr;
+  const bool is_producer = INLINE ? threadIdx.x == 0 : threadIdx.x == CONSUMERS;
+  if (is_producer) {
+    pr.u = blockIdx.x;
+    pr.units = units;
+    pr.nag = nag;
+    pr.step = gridDim.x;
+    pr.sb = 0;
+    pr.nsb = nsb;
+    pr.ngrp = ngrp;
+    pr.tiles = tiles;
+    pr.stage = 0;
+    pr.stages = stages;
+    pr.jmin = jmin;
+    pr.n1 = n1;
+    pr.N = N;
+    pr.qrows = qrows;
+    pr.phase = 0;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pr.pol_stream));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pr.pol_keep));
+  }
+  if (!INLINE && threadIdx.x >= CONSUMERS) {  // ---------------- producer warp ----------------
+    if (is_producer)
+      while (pr.more()) pr.issue(smem, full, empty, &tmD, &tmR);
     return;
   }
+  if (INLINE && is_producer)  // prefill every slot (fresh slots are free)
+    for (int k = 0; k < stages && pr.more(); k++) pr.issue(smem, full, empty, &tmD, &tmR);
+  bool first = true;
 
   // ---------------- consumers: thread = (aggregate g of the group, coefficient t) ----------------
   const int g = threadIdx.x / TC, t = threadIdx.x % TC;
@@ -178,7 +213,19 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
         part[b][jj][0] = part[b][jj][1] = 0;
       }
     for (int sb = 0; sb < nsb; sb++) {
+      // inline producer: refill the slot the CTA released last iteration (waits for the
+      // slowest warp to finish it), `stages - 1` blocks ahead of this one
+      if (INLINE && is_producer && !first && pr.more()) pr.issue(smem, full, empty, &tmD, &tmR);
+      first = false;
       mbar_wait(&full[stage], phase);
+      if (dry) {  // measurement only (HD_MAC_TMA_DRY=1): the TMA stream without the arithmetic
+        mbar_arrive(&empty[stage]);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+        continue;
+      }
       const uint64_t *Ds = reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + g * JT * SPS * TC + t;
       const uint64_t *Rs = reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + D_WORDS + t;
 #pragma unroll
@@ -203,7 +250,7 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
         stage = 0;
         phase ^= 1;
       }
-      if (sb & 1) {  // 8 baby steps: 16 mid terms < 2^64
+      if ((((sb + 1) * SPS) & 7) == 0) {  // every 8 baby steps: 16 mid terms < 2^64
 #pragma unroll
         for (int b = 0; b < QB; b++)
 #pragma unroll
@@ -274,38 +321,51 @@ hd_status make_map(CUtensorMap *map, const uint64_t *base, int n, int L, uint64_
 
 int g_num_sms = 0;
 
-template <int AG, int JT, int QB, bool FLUSH>
+template <int AG, int JT, int QB, int SPS, bool FLUSH, bool INLINE>
 hd_status launch(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int jmin,
                  int nj, uint32_t A, int qrows, size_t sq) {
   constexpr size_t STAGE_BYTES = (size_t)(AG * JT * SPS * TC + QB * SPS * 2 * TC) * 8;
   const size_t budget = 227 * 1024 - 256;
   int stages = (int)std::min<size_t>(8, budget / STAGE_BYTES);
+  if (const char *e = getenv("HD_MAC_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));  // A/B knob
   if (stages < 2) return hd_fail(HD_E_PARAMS, "MAC stage does not fit shared memory");
   const size_t smem = stages * STAGE_BYTES + 2 * stages * sizeof(uint64_t);
-  auto kern = mac_tma_kernel<AG, JT, QB, FLUSH>;
+  auto kern = mac_tma_kernel<AG, JT, QB, SPS, FLUSH, INLINE>;
   HD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (!g_num_sms) HD_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, c->device));
   const uint32_t units = (A / AG) * (uint32_t)(nj / JT) * (uint32_t)(c->n / TC) * (uint32_t)c->L;
   const uint32_t grid = std::min<uint32_t>(units, (uint32_t)g_num_sms);
-  kern<<<grid, AG * TC + 32, smem, c->stream>>>(mD, mR, S, n1, N, c->L, c->logn, jmin, nj, A, stages, qrows, sq,
-                                                c->mt);
+  const char *dry = getenv("HD_MAC_TMA_DRY");
+  kern<<<grid, AG * TC + (INLINE ? 0 : 32), smem, c->stream>>>(mD, mR, S, n1, N, c->L, c->logn, jmin, nj, A, stages, qrows, sq,
+                                                c->mt, dry && dry[0] == '1');
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;
 }
 
-template <int AG, int JT, int QB>
+// Per-launch choice: AG aggregates per CTA (consumer warps = 4 AG), SPS baby steps per stage.
+template <int JT, int QB>
 hd_status launch_f(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int jmin,
-                   int nj, uint32_t A, int qrows, size_t sq) {
-  return n1 > 128 ? launch<AG, JT, QB, true>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)
-                  : launch<AG, JT, QB, false>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq);
+                   int nj, uint32_t A, int qrows, size_t sq, int ag, int sps) {
+#define HD_MAC_L(AG_, SPS_, IN_)                                                                               \
+  return n1 > 128 ? launch<AG_, JT, QB, SPS_, true, IN_>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)            \
+                  : launch<AG_, JT, QB, SPS_, false, IN_>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)
+  const char *in_env = getenv("HD_MAC_INLINE");
+  const bool inl = !(in_env && in_env[0] == '0');
+  if (ag == 4 && inl) { HD_MAC_L(4, 2, true); }
+  if (ag == 4) { HD_MAC_L(4, 2, false); }
+  if (ag == 2 && sps == 2) { HD_MAC_L(2, 2, false); }
+  if (ag == 2) { HD_MAC_L(2, 4, false); }
+  if (sps == 2) { HD_MAC_L(1, 2, false); }
+  HD_MAC_L(1, 4, false);
+#undef HD_MAC_L
 }
 }  // namespace
 
 bool mac_tma_supported(const hd_context *c, int n1, int N, bool flat, uint32_t Q) {
   const char *v = getenv("HD_MAC_VARIANT");  // 'c': the LDG kernels of mac.cu ('g': generic)
   if (v && (v[0] == 'c' || v[0] == 'g')) return false;
-  if (c->n % TC || n1 % SPS || n1 > 256 || Q < 1 || Q > 4) return false;
+  if (c->n % TC || n1 % 2 || n1 > 256 || Q < 1 || Q > 4) return false;
   if ((flat ? N % n1 : (N / 2) % n1) != 0) return false;  // full giant-step ranges only
   for (int l = 0; l < c->L; l++)
     if (c->mod[l] >= (1ull << 60)) return false;  // carry-save operand split
@@ -317,32 +377,32 @@ hd_status mac_tma_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint6
                       const std::vector<int32_t> &js, uint32_t Q) {
   if (js.empty() || A == 0) return HD_OK;
   const int jmin = js.front(), nj = (int)js.size();
+  // aggregates per CTA (HD_MAC_AG, A/B knob): 4 -> 16 consumer warps per SM with the producer
+  // inline (128 registers each); 2 / 1 with a separate producer warp
+  const char *ag_env = getenv("HD_MAC_AG");
+  int ag = ag_env ? atoi(ag_env) : 4;
+  if (ag != 1 && ag != 2 && ag != 4) ag = 4;
+  while (ag > 1 && A % ag) ag /= 2;
+  const char *sps_env = getenv("HD_MAC_SPS");
+  const int sps = (sps_env && atoi(sps_env) == 2) || n1 % 4 || ag == 4 ? 2 : 4;  // baby steps per stage
   CUtensorMap mD, mR;
   hd_status s;
-  if ((s = make_map(&mD, D, c->n, c->L, (uint64_t)A * N, SPS))) return s;
-  if ((s = make_map(&mR, r, c->n, c->L, (uint64_t)Q * 2 * n1, 2 * SPS))) return s;
+  if ((s = make_map(&mD, D, c->n, c->L, (uint64_t)A * N, sps))) return s;
+  if ((s = make_map(&mR, r, c->n, c->L, (uint64_t)Q * 2 * n1, 2 * sps))) return s;
   const size_t sq = (size_t)A * nj * 2 * c->L * c->n;
   const int qrows = 2 * n1;
-  const bool ag2 = A % 2 == 0;
   // giant steps per thread: all of them up to 4 (each r word then serves JT diagonal words)
   const int jt = nj % 4 == 0 ? 4 : (nj % 2 == 0 ? 2 : 1);
   if (Q == 1) {
-    if (jt == 4) return ag2 ? launch_f<2, 4, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)
-                            : launch_f<1, 4, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq);
-    if (jt == 2) return ag2 ? launch_f<2, 2, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)
-                            : launch_f<1, 2, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq);
-    return ag2 ? launch_f<2, 1, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)
-               : launch_f<1, 1, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq);
+    if (jt == 4) return launch_f<4, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
+    if (jt == 2) return launch_f<2, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
+    return launch_f<1, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
   }
   // query batches (NEXT-4): every diagonal word staged once serves QB queries; QB x JT <= 4
   if (Q == 2) {
-    if (jt >= 2) return ag2 ? launch_f<2, 2, 2>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)
-                            : launch_f<1, 2, 2>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq);
-    return ag2 ? launch_f<2, 1, 2>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)
-               : launch_f<1, 1, 2>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq);
+    if (jt >= 2) return launch_f<2, 2>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
+    return launch_f<1, 2>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
   }
-  if (Q == 3) return ag2 ? launch_f<2, 1, 3>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)
-                         : launch_f<1, 1, 3>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq);
-  return ag2 ? launch_f<2, 1, 4>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)
-             : launch_f<1, 1, 4>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq);
+  if (Q == 3) return launch_f<1, 3>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
+  return launch_f<1, 4>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
 }

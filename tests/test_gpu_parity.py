@@ -2,8 +2,8 @@
 every RNS residue; decrypted scores vs brute-force cosine within 1e-3 (north star).
 
 Sizes: the toy config C1 (every stage, every aggregate), C2 (2^15 ring, all
-aggregates), and the bench configuration C4 (2^16 ring, 2^20 x 512, n1 = 64) on
-a sampled aggregate the oracle computes one by one.
+aggregates), and the bench configuration C4 (2^16 ring, 2^20 x 512, n1 = 128) in the
+bench's timed pipeline mode, on a sampled aggregate the oracle computes one by one.
 """
 import numpy as np
 import pytest
@@ -264,21 +264,61 @@ def test_streamed_host_queries_match_serial(monkeypatch):
 
 
 @pytest.mark.slow
-def test_c4_bench_config_sampled_aggregate():
-    """The bench launch configuration (2^16 ring, 2^20 x 512, n1 = 128, all 64 aggregates
-    on one GPU): bit-exact on a sampled aggregate, scores everywhere vs cosine."""
+def test_c4_timed_pipeline_full_size(monkeypatch):
+    """The bench's timed mode at its full size (2^16 ring, 2^20 x 512, n1 = 128, all 64
+    aggregates on one GPU), exactly as bench.py runs it: back-to-back hd_query calls on the
+    two-stream pipeline (S double-buffered, outputs reused in place, no host sync between
+    steps) over two alternating query ciphertexts, every step's outputs downloaded
+    asynchronously (R24 path at full level).  Every output of every step equals the serial
+    (HD_SERIAL=1, one stream) result bit for bit; a sampled aggregate of the serial result
+    equals the oracle's (or_scan_aggregate_hoisted, R23) bit for bit; and the decrypted
+    scores of both queries are within the noise budget (1e-6, north star 1e-3)
+    with the planted matches on top."""
     cfg = CONFIGS["C4"]
     run = Run(cfg)
-    o = run.o
-    s_ntt, steps, keys = run.oracle_keys()
-    r = o.baby_steps(run.oracle_query_ct(), cfg.n1, steps, keys)
-    assert (run.ctx.test_stage(run.db, 0, 0, cfg.n1 - 1) == r[-1]).all()
+    ctx, o = run.ctx, run.o
+    q2v = run.q[::-1].copy()
+    qs = [run.qct, ctx.encrypt_query(run.sk, q2v, ENC_SEED_BASE + 1)]
+    monkeypatch.setenv("HD_SERIAL", "1")
+    refs = []
+    for qq in qs:
+        outs = ctx.query(run.evk, run.db, qq)
+        refs.append([ctx.ciphertext_residues(x) for x in outs])
+    monkeypatch.setenv("HD_SERIAL", "0")
+    A = len(refs[0])
+    sz = ctx.ciphertext_export_async(run.outs[0], None)
+    steps = 4
+    host = torch.empty(steps * A * sz, dtype=torch.uint8, pin_memory=True)
+    outs = run.outs
+    torch.cuda.synchronize()
+    for k in range(steps):
+        outs = ctx.query(run.evk, run.db, qs[k % 2], outs)
+        for i, x in enumerate(outs):
+            ctx.ciphertext_export_async(x, (host.data_ptr() + (k * A + i) * sz, sz))
+    ctx.synchronize()
+    buf = host.numpy()
+    for k in range(steps):
+        for i in range(A):
+            off = (k * A + i) * sz
+            got = buf[off + 64:off + sz].view(np.uint64).reshape(2, -1, ctx.n)
+            assert (got == refs[k % 2][i]).all(), (k, i)
+    # the oracle on a sampled aggregate (serial result of query 1)
+    s_ntt, steps_, keys = run.oracle_keys()
+    r = o.baby_steps(run.oracle_query_ct(), cfg.n1, steps_, keys)
+    assert (ctx.test_stage(run.db, 0, 0, cfg.n1 - 1) == r[-1]).all()
     a = 37
-    D = run.oracle_D(a)
-    out = o.scan_aggregate(r, cfg.n1, cfg.dim, D, steps, keys)
-    assert (run.ctx.ciphertext_residues(run.outs[a]) == out).all()
-    sc = run.ctx.decrypt_scores(run.sk, run.db.layout, run.outs)
-    assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-3
+    out = o.scan_aggregate(r, cfg.n1, cfg.dim, run.oracle_D(a), steps_, keys)
+    assert (refs[0][a] == out).all()
+    # scores of both queries, from the last two pipelined steps' downloads
+    for k, qv in ((steps - 2, run.q), (steps - 1, q2v)):
+        cts = [ctx.ciphertext_import(buf[(k * A + i) * sz:(k * A + i + 1) * sz].copy()) for i in range(A)]
+        sc = ctx.decrypt_scores(run.sk, run.db.layout, cts)
+        err = float(np.abs(sc - _cos(run.db_vecs, qv)).max())
+        print(f"C4 step {k}: max |score - cos| = {err:.3e}")
+        assert err < 1e-6
+    sc = ctx.decrypt_scores(run.sk, run.db.layout, [ctx.ciphertext_import(buf[((steps - 2) * A + i) * sz:
+                                                                               ((steps - 2) * A + i + 1) * sz].copy())
+                                                    for i in range(A)])
     assert sorted(np.argsort(-sc)[:3]) == sorted(run.pos.tolist())
 
 
