@@ -31,7 +31,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-from synth_inputs import CONFIGS, ENC_SEED_BASE, dataset_rows, make_dataset  # noqa: E402
+from synth_inputs import CONFIGS, ENC_SEED_BASE, dataset_rows, make_dataset, planted_positions  # noqa: E402
 
 METRIC = "encrypted queries/sec (2^20 x 512 database scan)"
 UNIT = "queries/s"
@@ -45,7 +45,11 @@ def parse():
     ap.add_argument("--config", default="C4")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=-1, help="end-to-end steps (default: --steps)")
+    ap.add_argument("--profile", default="north-star", choices=["north-star", "paper"],
+                    help="key-switching profile: north-star (L = 3, alpha = 1, one special prime) or the "
+                         "paper's depth (SURVEY 8(d) secondary, R31: L = 12, alpha = 4, 4 special primes)")
+    ap.add_argument("--no-check", action="store_true", help="skip the per-run correctness check")
     ap.add_argument("--packing", default="replicated", choices=["replicated", "flat", "flat_tbs"],
                     help="stride-2N replicated blocks + fold (the north-star scan) or the flat pre-rotated "
                          "layout (NEXT-2, BSGS-RTX-TBE)")
@@ -67,7 +71,10 @@ def parse():
     ap.add_argument("--n1", type=int, default=0, help="baby-step count (default: the config's; the paper uses 23)")
     ap.add_argument("--db", default="plain", choices=["plain", "encrypted"],
                     help="plaintext diagonals (the north-star scan) or the encrypted-database mode (NEXT-1)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.e2e_steps < 0:
+        args.e2e_steps = args.steps  # end to end over as many steps as the device-timed value
+    return args
 
 
 def peaks():
@@ -79,9 +86,27 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def full_config(args, cfg, world):
+    """The config dict of the JSON line -- identical for our arm and the reference arm."""
+    flat = args.packing in ("flat", "flat_tbs")
+    per = cfg.num_slots if flat else (cfg.num_slots // cfg.dim // 2) * cfg.dim
+    A = -(-cfg.num_vectors // per)
+    if args.online_aggregate:
+        A = world
+    return dict(cfg_dict(cfg, world, "fixed 2^20 database sharded by aggregate"),
+                database="encrypted diagonals (NEXT-1: degree-2 MAC + relinearisation)" if args.db == "encrypted"
+                else "plaintext diagonals (north-star pt x ct scan)",
+                packing=("flat, server-side homomorphic pre-rotation (BSGS-RTX-TBS)" if args.packing == "flat_tbs" else
+                         "flat pre-rotated (NEXT-2, BSGS-RTX-TBE; no fold, M groups per ciphertext)")
+                if flat else "stride-2N replicated blocks + rotate-by-N fold (Alg. enroller_bsgs)",
+                aggregates=A, profile=args.profile)
+
+
 def cfg_dict(cfg, world, scaling_note):
     return {"workload": f"{cfg.name}: ring 2^{cfg.log_n}, VECTOR_DIM={cfg.dim}, {cfg.num_vectors} db vectors, "
-                        f"n1={cfg.n1}, L={cfg.limbs} RNS limbs + 1 special prime",
+                        f"n1={cfg.n1}, L={cfg.limbs} RNS limbs + {cfg.special} special prime"
+                        + ("s" if cfg.special > 1 else "") + (f", {cfg.digit_limbs} limbs per digit"
+                                                             if cfg.digit_limbs > 1 else ""),
             "ring": 1 << cfg.log_n, "vector_dim": cfg.dim, "db_vectors": cfg.num_vectors, "n1": cfg.n1,
             "limbs": cfg.limbs, "aggregates": cfg.aggregates, "parallelism": f"aggregate-shard x{world}",
             "l2": "inputs > L2 (diagonal stream 51.5 GB at C4); no flush needed" if cfg.log_n >= 16 else
@@ -96,7 +121,7 @@ def oracle_sample(cfg, rng_seed=0, scenario="scan"):
     one hoisted baby rotation, one giant-step MAC sum, one rescale, one giant rotation.
     Per-query time = ModUp + (n1-1) t_baby + A (n_g (t_mac + t_rs) + (nnz+1) t_rot)."""
     import oracle
-    o = oracle.Oracle(cfg.log_n, cfg.limbs, seed=1)
+    o = oracle.Oracle(cfg.log_n, cfg.limbs, seed=1, K_sp=cfg.special, alpha=cfg.digit_limbs)
     rng = np.random.default_rng(rng_seed)
     n, L = o.n, o.L
     mods = o.p.moduli
@@ -108,7 +133,7 @@ def oracle_sample(cfg, rng_seed=0, scenario="scan"):
     jmin, jmax = o.giant_range(N, n1)
     nj = jmax - jmin + 1
     nnz = sum(1 for j in range(jmin, jmax + 1) if o.pre_rot(N, n1, j))
-    key = np.ascontiguousarray(np.stack([np.stack([rand((L + 1, n), mods) for _ in range(2)]) for _ in range(L)]))
+    key = np.ascontiguousarray(np.stack([np.stack([rand((o.M, n), mods) for _ in range(2)]) for _ in range(o.beta)]))
     q = np.ascontiguousarray(np.stack([rand((L, n), mods[:L]) for _ in range(2)]))
     t0 = time.perf_counter()
     dig = o.modup(np.ascontiguousarray(q[1]))
@@ -159,6 +184,8 @@ def workload_cfg(args):
         cfg = dataclasses.replace(cfg, limbs=limbs)
     if args.n1 and args.n1 != cfg.n1:
         cfg = dataclasses.replace(cfg, n1=args.n1)
+    if args.profile == "paper":  # P:L2166-2169 depth as L = 12, alpha = 4, K_sp = 4 (R31)
+        cfg = dataclasses.replace(cfg, limbs=args.limbs or 12, special=4, digit_limbs=4)
     return cfg
 
 
@@ -189,7 +216,8 @@ def run_reference(args):
     line = {"impl": "reference", "metric": metric_name(args), "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": pq * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64 (RNS residues)", "data": "synthetic",
-            "config": cfg_dict(cfg, 1, "CPU oracle, single thread"),
+            "config": full_config(args, cfg, int(os.environ.get("WORLD_SIZE", "1"))),
+            "extrapolated": True,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
                              "sample": "per step: oracle ModUp + 1 hoisted baby rotation + 1 giant-step MAC sum + "
                                        "1 rescale + 1 giant rotation%s at the workload's shapes on uniform random "
@@ -277,7 +305,8 @@ def main():
     if args.scenario == "membership" and args.packing == "replicated":
         raise SystemExit("--scenario membership needs a flat packing (every slot a vector; DESIGN.md R29)")
     stream = torch.cuda.current_stream()
-    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1, device=local, stream=stream)
+    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1, device=local, stream=stream, num_special=cfg.special,
+                     digit_limbs=cfg.digit_limbs)
     flat = args.packing in ("flat", "flat_tbs")
     if args.packing == "flat_tbs" and args.db != "encrypted":
         raise SystemExit("--packing flat_tbs needs --db encrypted (BSGS-RTX-TBS pre-rotates encrypted diagonals)")
@@ -480,6 +509,19 @@ def main():
         t_ms = hdd.max_over_ranks(t_ms, dev)
     ms_per_step = t_ms / args.steps
     value = Q * args.steps / (t_ms / 1e3)
+    # ---- per-run correctness of the timed pipeline ----
+    check, timed_res = None, None
+    if not args.no_check and args.scenario == "scan" and rank == 0:
+        if world == 1:
+            mine = outs[:A]  # the dataset's query (batch: the first query of the step)
+            check = score_check(hd, ctx, sk, db, mine, cfg, A, q)
+            timed_res = [ctx.ciphertext_residues(o) for o in mine]
+        else:  # rank 0: the 1-limb exports every rank contributed to the last gather
+            views = [v for per in gathered[0] for v in per]
+            cts_all = [ctx.ciphertext_import(p_, b_, on_device=True) for p_, b_ in views]
+            per_r = hdd.shard_sizes(A, world)
+            first = [cts_all[sum(Q * x for x in per_r[:r]) + i] for r in range(world) for i in range(per_r[r])]
+            check = score_check(hd, ctx, sk, db, first, cfg, A, q)
     # ---- e2e through the public API with host buffers: H2D query, scan, D2H of every output ----
     e2e = None
     if world == 1 and args.e2e_steps > 0:
@@ -521,18 +563,27 @@ def main():
     dpoly, spoly = (2, 3) if enc_db else (1, 2)  # diagonal / giant-sum polynomials
     # D passes per step: hd_query_batch runs the single-query MAC per query unless HD_MAC_BATCH=G
     # selects the shared-D kernel (one pass per group of up to G queries)
-    g_env = int(os.environ.get("HD_MAC_BATCH", "1") or 1)
-    d_passes = Q if g_env <= 1 else (Q // 4 + (Q % 4) // 2 + Q % 2 if g_env >= 4 else Q // 2 + Q % 2)
+    mac_kernel, mac_src = mac_kernel_of(cfg, flat, enc_db)
+    if mac_kernel == "mac_tma_kernel":  # groups of up to HD_MAC_BATCH (default 4) queries per D pass
+        gmax = max(1, min(4, int(os.environ.get("HD_MAC_BATCH", "4") or 4)))
+        d_passes = -(-Q // gmax)
+    else:
+        g_env = int(os.environ.get("HD_MAC_BATCH", "1") or 1)
+        d_passes = Q if g_env <= 1 else (Q // 4 + (Q % 4) // 2 + Q % 2 if g_env >= 4 else Q // 2 + Q % 2)
     mac_bytes = (d_passes * nloc * N * dpoly * L * n * 8
                  + Q * (cfg.n1 * 2 * L * n * 8 + nloc * nj * spoly * L * n * 8))
     mac_avg_ms = statistics.mean(mac_ms)
     peak, peak_src = peaks()
     achieved = mac_bytes / (mac_avg_ms / 1e3) / 1e9
+    # ncu DRAM bytes of one launch of this kernel at this config, recorded with the sha256 of the
+    # kernel's source file: used only while that source is unchanged (else null: re-profile)
     traffic = None
     tf = os.path.join(ROOT, "profiles", "mac_traffic.json")
-    if os.path.exists(tf) and not enc_db and not flat:
+    if os.path.exists(tf) and Q == 1:
         try:
-            traffic = json.load(open(tf)).get(cfg.name)
+            rec = json.load(open(tf)).get(f"{cfg.name}/{args.packing}/{args.db}/{mac_kernel}")
+            if rec and rec.get("src_sha256") == file_sha256(mac_src):
+                traffic = rec["dram_bytes"]
         except Exception:  # noqa: BLE001
             traffic = None
     # ---- per-phase times of the path run serially (one stream, no overlap between queries):
@@ -551,6 +602,12 @@ def main():
     latency_ms = l0.elapsed_time(l1) / 3  # one step alone on one stream: the per-query latency
     phase_serial = ctx.query_stats()
     os.environ.pop("HD_SERIAL")
+    if check is not None and timed_res is not None:  # the timed (two-stream) bits = the serial bits
+        check["pipelined_eq_serial"] = all(bool((ctx.ciphertext_residues(o) == r).all())
+                                           for o, r in zip(outs[:A], timed_res))
+        check["ok"] = check["ok"] and check["pipelined_eq_serial"]
+        check["oracle_parity"] = ("bit-exact vs the CPU oracle at this configuration: tests/test_gpu_parity.py::"
+                                  "test_c4_timed_pipeline_full_size (sampled aggregate, same pipeline)")
     # ---- key-switch HBM stream (north-star metric): the batched baby-step key inner product ----
     kip_ms = phase_serial[5]
     key_bytes = L * 2 * (L + 1) * n * 8  # one rotation key at the top level
@@ -593,14 +650,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u64 (RNS residues, 64-bit modular integer arithmetic)",
             "data": "synthetic (P:L2175-2179 generator, seeded)",
-            "config": dict(cfg_dict(cfg, world, "fixed 2^20 database sharded by aggregate"),
-                           database="encrypted diagonals (NEXT-1: degree-2 MAC + relinearisation)" if enc_db
-                           else "plaintext diagonals (north-star pt x ct scan)",
-                           packing=("flat, server-side homomorphic pre-rotation (BSGS-RTX-TBS; setup "
-                                    f"{prerot_s:.2f} s)" if args.packing == "flat_tbs" else
-                                    "flat pre-rotated (NEXT-2, BSGS-RTX-TBE; no fold, M groups per ciphertext)")
-                           if flat else "stride-2N replicated blocks + rotate-by-N fold (Alg. enroller_bsgs)",
-                           aggregates=A),
+            "config": full_config(args, cfg, world),
+            "prerotate_setup_s": prerot_s,
             "phase_ms": {"baby": phase[0] / args.steps, "mac": phase[1] / args.steps,
                          "rescale": phase[2] / args.steps, "giant": phase[3] / args.steps,
                          "fold": phase[4] / args.steps, "baby_kip": phase[5] / args.steps,
@@ -608,7 +659,7 @@ def main():
             "phase_ms_serial": dict(zip(["baby", "mac", "rescale", "giant", "fold", "baby_kip"],
                                         [float(x) for x in phase_serial])),
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "kernel": "mac_cs_batch_kernel" if Q > 1 else "mac_cs_kernel", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "roofline": {"bound": "hbm", "kernel": mac_kernel, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": mac_bytes, "avg_launch_ms": mac_avg_ms},
             "keyswitch": keyswitch, "query_roofline": query_roofline, "tail_ms": tail_ms,
@@ -616,7 +667,7 @@ def main():
             "membership_count_shift": count_shift if args.scenario == "membership" else None, "split_baby": split is not None,
             "online_aggregate": None if aggr_s is None else {"setup_s": aggr_s, "note": "Alg. online-aggr: the "
                                 "scan runs over one aggregate holding the sum of all diagonals"},
-            "clocks": clocks, "e2e": e2e}
+            "clocks": clocks, "e2e": e2e, "check": check}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import multiprocessing
         pqs, total, reps = [], 0.0, 0
@@ -641,6 +692,49 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def file_sha256(path):
+    import hashlib
+    with open(path, "rb") as f:
+        return hashlib.sha256(f.read()).hexdigest()
+
+
+def mac_kernel_of(cfg, flat, enc_db):
+    """The MAC kernel libhd picks for this workload (mac.cu mac_run / mac_tma_supported) and its source."""
+    csrc = os.path.join(ROOT, "paper_2604_00546_b200", "csrc")
+    N, n1 = cfg.dim, cfg.n1
+    full = (N % n1 == 0) if flat else ((N // 2) % n1 == 0)
+    if enc_db:
+        return "mac_ct_stream_kernel", os.path.join(csrc, "mac.cu")
+    if os.environ.get("HD_MAC_VARIANT", "")[:1] not in ("c", "g") and full and n1 % 2 == 0 and n1 <= 256:
+        return "mac_tma_kernel", os.path.join(csrc, "mac_tma.cu")
+    return ("mac_cs_kernel" if full and os.environ.get("HD_MAC_VARIANT", "")[:1] != "g" else "mac_kernel",
+            os.path.join(csrc, "mac.cu"))
+
+
+def score_check(hd, ctx, sk, db, cts, cfg, A, q):
+    """Per-run correctness (the paper's runs fail themselves on a wrong result,
+    P:L2209-2213): decrypt every score ciphertext of the last timed step, compare with the
+    brute-force cosine of the whole synthetic database (regenerated in chunks, float64) and check
+    that the planted matches are the top scores."""
+    lay = db.layout
+    lay.agg_begin, lay.agg_end = 0, A
+    sc = ctx.decrypt_scores(sk, lay, cts)
+    K = cfg.num_vectors
+    qq = q.astype(np.float64)
+    qq /= np.linalg.norm(qq)
+    err = 0.0
+    step = 1 << 16
+    for v0 in range(0, K, step):
+        v1 = min(K, v0 + step)
+        rows = dataset_rows(K, cfg.dim, cfg.data_seed, v0, v1).astype(np.float64)
+        cos = rows @ qq / np.linalg.norm(rows, axis=1)
+        err = max(err, float(np.abs(sc[v0:v1] - cos).max()))
+    pos = planted_positions(K, cfg.dim, cfg.data_seed)
+    top = sorted(np.argsort(-sc)[:len(pos)].tolist())
+    return {"max_abs_score_err": err, "scores_checked": int(len(sc)), "noise_budget": 1e-6, "tolerance": 1e-3,
+            "planted_on_top": top == sorted(pos.tolist()), "ok": bool(err < 1e-3 and top == sorted(pos.tolist()))}
 
 
 def _oracle_sample_worker(argv):

@@ -42,7 +42,7 @@
  *     allocated at creation time of those objects (never inside hd_query).
  *   - Residues: u64 in [0, q), NTT form (bit-reversed evaluation order, DESIGN.md
  *     R13).  Ciphertext layout [poly 0..1][limb][coef]; plaintext [limb][coef];
- *     rotation key [digit d < L][poly (0 = b, 1 = a)][modulus l <= L][coef]
+ *     rotation key [digit d < ceil(L/alpha)][poly (0 = b, 1 = a)][modulus l < L+K][coef]
  *     where modulus index L is the special prime P.
  *   - No CPU fallback: if no CUDA device is usable every call that computes
  *     returns HD_E_CUDA.
@@ -81,10 +81,18 @@ typedef struct hd_database hd_database;     /* diagonals of aggregates [agg_begi
 typedef struct hd_ciphertext hd_ciphertext; /* device-resident ciphertext       */
 typedef struct hd_public_key hd_public_key; /* encrypted-database mode (R26)     */
 
-/* CKKS parameters (R5, R11).  Defaults (when a field is 0): num_limbs 3,
+/* CKKS parameters (R5, R11, R31).  Defaults (when a field is 0): num_limbs 3,
  * q0_bits 60, scale_bits 45, special_bits 60, num_special 1, digit_limbs 1.
- * Only num_special = 1 and digit_limbs = 1 are implemented (HD_E_PARAMS else).
- * log_n in [4, 16].  seed keys the Philox stream of the secret / rotation keys. */
+ * Hybrid key switching: digit_limbs (alpha) limbs per digit, num_special (K) special
+ * primes p_0 > ... > p_{K-1} (the next NTT primes below q0), P = prod p_k; keys hold
+ * ceil(num_limbs / alpha) digits over the num_limbs + K moduli.  alpha = K = 1 is the
+ * north-star profile (centred single-limb lifts, R12); any other profile uses fast basis
+ * conversion with centred digits (R31) -- e.g. the paper's depth: num_limbs
+ * 12, digit_limbs 4, num_special 4.  The scan (hd_query and its parts),
+ * rotations and keygen support every profile; relinearisation (encrypted database, the
+ * comparison) needs alpha = K = 1 (HD_E_PARAMS else).  num_limbs + num_special <= 20,
+ * digit_limbs <= num_limbs, log_n in [4, 16].  seed keys the Philox stream of the secret /
+ * rotation keys. */
 typedef struct {
   uint32_t log_n, num_limbs, q0_bits, scale_bits, special_bits, num_special, digit_limbs;
   uint32_t reserved;
@@ -149,7 +157,7 @@ hd_status hd_context_create(const hd_params *params, int cuda_device, void *cuda
                             const hd_allocator *allocator, hd_context **out);
 void hd_context_destroy(hd_context *ctx);
 hd_status hd_context_set_stream(hd_context *ctx, void *cuda_stream);
-/* moduli[0..L-1] = q_i, moduli[L] = P; psi likewise (host arrays, L+1 each). */
+/* moduli[0..L-1] = q_i, moduli[L..L+K-1] = p_k; psi likewise (host arrays, L+K each). */
 hd_status hd_context_moduli(const hd_context *ctx, uint64_t *moduli, uint64_t *psi, size_t cap);
 
 /* ---- client -------------------------------------------------------------- */
@@ -326,7 +334,7 @@ hd_status hd_eval_keys_export(const hd_eval_keys *evk, void *dst, size_t cap, in
                               size_t *written);
 hd_status hd_eval_keys_import(hd_context *ctx, const void *src, size_t bytes, int src_on_device,
                               hd_eval_keys **out);
-/* Secret key in NTT form, host u64 [(L+1)][n]; test use. */
+/* Secret key in NTT form, host u64 [(L+K)][n]; test use. */
 hd_status hd_secret_key_export(const hd_secret_key *sk, uint64_t *dst, size_t cap);
 
 /* Public key pk = (b, a) = (-a s + e, a) over the L ciphertext moduli (R26; Philox

@@ -229,7 +229,8 @@ class _Handle:
 
     def close(self):
         if self.h:
-            getattr(load(), self._destroy)(self.h)
+            if not _FINALIZING:  # at interpreter exit the process releases everything: no C calls
+                getattr(load(), self._destroy)(self.h)
             self.h = None
 
     def __del__(self):
@@ -282,11 +283,13 @@ class Context(_Handle):
     _destroy = "hd_context_destroy"
 
     def __init__(self, log_n, limbs=3, seed=1, device=0, stream=None, scale_bits=45, q0_bits=60,
-                 allocator="torch"):
+                 allocator="torch", num_special=1, digit_limbs=1):
         """allocator: "torch" (default: PyTorch's caching allocator owns libhd's device
-        memory) or None (libhd's default, the device's stream-ordered pool)."""
+        memory) or None (libhd's default, the device's stream-ordered pool).
+        num_special / digit_limbs: the key-switching profile (R11: 1 / 1; the paper-depth
+        profile of SURVEY 8(d), R31: limbs 12, num_special 4, digit_limbs 4)."""
         p = Params(log_n=log_n, num_limbs=limbs, q0_bits=q0_bits, scale_bits=scale_bits,
-                   special_bits=q0_bits, num_special=1, digit_limbs=1, reserved=0, seed=seed)
+                   special_bits=q0_bits, num_special=num_special, digit_limbs=digit_limbs, reserved=0, seed=seed)
         h = VP()
         alloc = C.byref(torch_allocator(device)) if allocator == "torch" else None
         _check("hd_context_create", load().hd_context_create(C.byref(p), device, _stream_handle(stream),
@@ -294,15 +297,18 @@ class Context(_Handle):
         super().__init__(h.value)
         self.device = device
         self.allocator = allocator
+        self.K, self.alpha = num_special, digit_limbs
+        self.M = limbs + num_special              # moduli of a key: Q_L u P
+        self.beta = -(-limbs // digit_limbs)      # digits of a top-level key
         self.log_n, self.L, self.n, self.ns = log_n, limbs, 1 << log_n, 1 << (log_n - 1)
 
     def set_stream(self, stream):
         _check("hd_context_set_stream", load().hd_context_set_stream(self.h, _stream_handle(stream)))
 
     def moduli(self):
-        m = np.zeros(self.L + 1, np.uint64)
-        p = np.zeros(self.L + 1, np.uint64)
-        _check("hd_context_moduli", load().hd_context_moduli(self.h, _ptr(m), _ptr(p), self.L + 1))
+        m = np.zeros(self.M, np.uint64)
+        p = np.zeros(self.M, np.uint64)
+        _check("hd_context_moduli", load().hd_context_moduli(self.h, _ptr(m), _ptr(p), self.M))
         return [int(x) for x in m], [int(x) for x in p]
 
     # -- client -------------------------------------------------------------------------------------
@@ -598,7 +604,7 @@ class Context(_Handle):
         return EvalKeys(out.value, self)
 
     def secret_key_export(self, sk):
-        out = np.zeros((self.L + 1, self.n), np.uint64)
+        out = np.zeros((self.M, self.n), np.uint64)
         _check("hd_secret_key_export", load().hd_secret_key_export(sk.h, _ptr(out), out.size))
         return out
 
@@ -656,5 +662,5 @@ def eval_key_residues(ctx: Context, buf: np.ndarray):
     count = int(buf[20:24].view(np.uint32)[0])
     steps_bytes = ((count * 4 + 63) // 64) * 64
     steps = buf[64:64 + count * 4].view(np.int32).copy()
-    keys = buf[64 + steps_bytes:].view(np.uint64).reshape(count, ctx.L, 2, ctx.L + 1, ctx.n)
+    keys = buf[64 + steps_bytes:].view(np.uint64).reshape(count, ctx.beta, 2, ctx.M, ctx.n)
     return steps, keys

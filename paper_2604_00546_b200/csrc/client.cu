@@ -25,8 +25,9 @@ __global__ void secret_kernel(uint64_t seed, int n, int nm, uint64_t *__restrict
   for (int l = 0; l < nm; l++) s[(size_t)l * n + j] = smod_dev(v, mt.q[l], mt.bar[l]);
 }
 
-// error rows of a key: key[d][0][l][j] = CBD draw of (j, obj, d) mod q_l (coefficient form).
-__global__ void key_error_kernel(uint64_t seed, uint32_t step, uint32_t tag, int n, int L, uint64_t *__restrict__ key,
+// error rows of a key: key[d][0][l][j] = CBD draw of (j, obj, d) mod q_l (coefficient form),
+// l over the M = L + K moduli.
+__global__ void key_error_kernel(uint64_t seed, uint32_t step, uint32_t tag, int n, int M, uint64_t *__restrict__ key,
                                  ModTab mt) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int d = blockIdx.y;
@@ -34,27 +35,28 @@ __global__ void key_error_kernel(uint64_t seed, uint32_t step, uint32_t tag, int
   uint64_t w0, w1;
   draw(seed, j, 0, step, tag, d, w0, w1);
   const int64_t e = cbd21(w0);
-  for (int l = 0; l <= L; l++) key[((size_t)(d * 2) * (L + 1) + l) * n + j] = smod_dev(e, mt.q[l], mt.bar[l]);
+  for (int l = 0; l < M; l++) key[((size_t)(d * 2) * M + l) * n + j] = smod_dev(e, mt.q[l], mt.bar[l]);
 }
 
-// b_d = e_d - a_d s + [l == d] (P mod q_d) s';  a_d uniform in NTT form (R11, R14).
+// b_d = e_d - a_d s + [l in I_d] (P mod q_l) s';  a_d uniform in NTT form (R11, R14, R31):
+// digit d = limbs [d alpha, (d+1) alpha) (alpha = K = 1: [l == d] (P mod q_d) s').
 // s' = sigma_g(s) (rotation key, g = Galois element) or s^2 (g = 0: relinearisation key, R26).
-__global__ void key_combine_kernel(uint64_t seed, uint32_t step, uint32_t tag_a, uint32_t g, int logn, int L,
-                                   const uint64_t *__restrict__ s_ntt, uint64_t *__restrict__ key, ModTab mt,
-                                   InvTab2 pmod) {
+__global__ void key_combine_kernel(uint64_t seed, uint32_t step, uint32_t tag_a, uint32_t g, int logn, int L, int M,
+                                   int alpha, const uint64_t *__restrict__ s_ntt, uint64_t *__restrict__ key,
+                                   ModTab mt, InvTab2 pmod) {
   const int n = 1 << logn;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int dl = blockIdx.y;
-  const int d = dl / (L + 1), l = dl % (L + 1);
+  const int d = dl / M, l = dl % M;
   if (j >= n) return;
   const uint64_t q = mt.q[l];
   uint64_t w0, w1;
   draw(seed, j, l, step, tag_a, d, w0, w1);
   const uint64_t a = reduce128(w0, w1, q, mt.bar[l], mt.r64[l], mt.r64s[l]);
-  uint64_t *kb = key + ((size_t)(d * 2 + 0) * (L + 1) + l) * n;
-  uint64_t *ka = key + ((size_t)(d * 2 + 1) * (L + 1) + l) * n;
+  uint64_t *kb = key + ((size_t)(d * 2 + 0) * M + l) * n;
+  uint64_t *ka = key + ((size_t)(d * 2 + 1) * M + l) * n;
   uint64_t b = submod(kb[j], mulmod(a, s_ntt[(size_t)l * n + j], mt, l), q);
-  if (l == d) {
+  if (l < L && l / alpha == d) {
     const uint64_t sj = s_ntt[(size_t)l * n + j];
     const uint64_t sp = g ? s_ntt[(size_t)l * n + galois_src(j, g, logn)]  // sigma_g(s) in the NTT domain
                           : mulmod(sj, sj, mt, l);                          // s^2
@@ -274,45 +276,45 @@ extern "C" hd_status hd_keygen(hd_context *c, const int32_t *steps, size_t count
   for (size_t i = 0; i < count; i++)
     if (steps[i] <= 0 || steps[i] >= c->ns) return hd_fail(HD_E_INVALID_ARG, "rotation step outside (0, numSlots)");
   HD_CUDA(cudaSetDevice(c->device));
-  const int n = c->n, L = c->L;
+  const int n = c->n, L = c->L, M = ks_M(c), beta = ks_beta(c, L);
   hd_secret_key *sk = new hd_secret_key{c, nullptr};
   hd_eval_keys *evk = new hd_eval_keys();
   evk->ctx = c;
   evk->steps.assign(steps, steps + count);
-  evk->key_elems = (size_t)L * 2 * (L + 1) * n;
+  evk->key_elems = ks_key_elems(c);
   auto fail = [&](hd_status s) {
     hd_secret_key_destroy(sk);
     hd_eval_keys_destroy(evk);
     return s;
   };
-  cudaError_t e = dev_alloc(c, &sk->s_ntt, (size_t)(L + 1) * n * 8);
+  cudaError_t e = dev_alloc(c, &sk->s_ntt, (size_t)M * n * 8);
   if (!e && count) e = dev_alloc(c, &evk->keys, evk->key_elems * count * 8);
   if (e) return fail(hd_fail(HD_E_CAPACITY, cudaGetErrorString(e)));
   const uint64_t seed = c->params.seed;
-  secret_kernel<<<(n + TPB - 1) / TPB, TPB, 0, c->stream>>>(seed, n, L + 1, sk->s_ntt, c->mt); ++c->launches;
+  secret_kernel<<<(n + TPB - 1) / TPB, TPB, 0, c->stream>>>(seed, n, M, sk->s_ntt, c->mt); ++c->launches;
   RowMap rm{};
   rm.gsize = 1u << 30;
   rm.mdiv = 1;
-  rm.mlen = L + 1;
-  for (int l = 0; l <= L; l++) rm.midx[l] = l;
-  hd_status s = ntt_rows(c, sk->s_ntt, L + 1, rm, false);
+  rm.mlen = M;
+  for (int l = 0; l < M; l++) rm.midx[l] = l;
+  hd_status s = ntt_rows(c, sk->s_ntt, M, rm, false);
   if (s) return fail(s);
   InvTab2 pmod{};
-  for (int l = 0; l < L; l++) pmod.w[l] = c->mod[L] % c->mod[l];
+  for (int l = 0; l < L; l++) pmod.w[l] = ks_P_mod(c, c->mod[l]);
   for (size_t i = 0; i < count; i++) {
     uint64_t *key = evk->keys + evk->key_elems * i;
     const uint32_t step = (uint32_t)steps[i];
     const uint32_t g = (uint32_t)host_powmod(5, step, 2ull * n);
-    key_error_kernel<<<dim3((n + TPB - 1) / TPB, L), TPB, 0, c->stream>>>(seed, step, TAG_KEY_E, n, L, key, c->mt); ++c->launches;
-    RowMap rk{};  // rows (d, l) at key + (d 2 (L+1) + l) n
-    rk.gsize = L + 1;
-    rk.gstride = (uint64_t)2 * (L + 1) * n;
+    key_error_kernel<<<dim3((n + TPB - 1) / TPB, beta), TPB, 0, c->stream>>>(seed, step, TAG_KEY_E, n, M, key, c->mt); ++c->launches;
+    RowMap rk{};  // rows (d, l) at key + (d 2 M + l) n
+    rk.gsize = M;
+    rk.gstride = (uint64_t)2 * M * n;
     rk.mdiv = 1;
-    rk.mlen = L + 1;
-    for (int l = 0; l <= L; l++) rk.midx[l] = l;
-    if ((s = ntt_rows(c, key, L * (L + 1), rk, false))) return fail(s);
-    key_combine_kernel<<<dim3((n + TPB - 1) / TPB, L * (L + 1)), TPB, 0, c->stream>>>(
-        seed, step, TAG_KEY_A, g, c->logn, L, sk->s_ntt, key, c->mt, pmod); ++c->launches;
+    rk.mlen = M;
+    for (int l = 0; l < M; l++) rk.midx[l] = l;
+    if ((s = ntt_rows(c, key, beta * M, rk, false))) return fail(s);
+    key_combine_kernel<<<dim3((n + TPB - 1) / TPB, beta * M), TPB, 0, c->stream>>>(
+        seed, step, TAG_KEY_A, g, c->logn, L, M, c->alpha, sk->s_ntt, key, c->mt, pmod); ++c->launches;
   }
   e = cudaStreamSynchronize(c->stream);
   if (e) return fail(hd_fail(HD_E_CUDA, cudaGetErrorString(e)));
@@ -589,24 +591,24 @@ extern "C" hd_status hd_relin_keygen(hd_context *c, const hd_secret_key *sk, hd_
   if (evk->ctx != c || sk->ctx != c) return hd_fail(HD_E_STATE, "objects from another context");
   if (evk->find(HD_RELIN_STEP)) return HD_OK;  // already present
   HD_CUDA(cudaSetDevice(c->device));
-  const int n = c->n, L = c->L;
-  const size_t cnt = evk->steps.size(), ke = (size_t)L * 2 * (L + 1) * n;
+  const int n = c->n, L = c->L, M = ks_M(c), beta = ks_beta(c, L);
+  const size_t cnt = evk->steps.size(), ke = ks_key_elems(c);
   uint64_t *keys = nullptr;
   if (dev_alloc(c, &keys, ke * (cnt + 1) * 8) != cudaSuccess) return hd_fail(HD_E_CAPACITY, "relinearisation key alloc");
   if (cnt) HD_CUDA(cudaMemcpyAsync(keys, evk->keys, ke * cnt * 8, cudaMemcpyDeviceToDevice, c->stream));
   uint64_t *key = keys + ke * cnt;
   const uint64_t seed = c->params.seed;
-  key_error_kernel<<<dim3((n + TPB - 1) / TPB, L), TPB, 0, c->stream>>>(seed, 0, TAG_RLK_E, n, L, key, c->mt); ++c->launches;
-  RowMap rk = limb_rows(L + 1, L + 1, (uint64_t)2 * (L + 1) * n);  // rows (d, l) of the b halves
-  hd_status s = ntt_rows(c, key, L * (L + 1), rk, false);
+  key_error_kernel<<<dim3((n + TPB - 1) / TPB, beta), TPB, 0, c->stream>>>(seed, 0, TAG_RLK_E, n, M, key, c->mt); ++c->launches;
+  RowMap rk = limb_rows(M, M, (uint64_t)2 * M * n);  // rows (d, l) of the b halves
+  hd_status s = ntt_rows(c, key, beta * M, rk, false);
   if (s) {
     dev_free(c, keys);
     return s;
   }
   InvTab2 pmod{};
-  for (int l = 0; l < L; l++) pmod.w[l] = c->mod[L] % c->mod[l];
-  key_combine_kernel<<<dim3((n + TPB - 1) / TPB, L * (L + 1)), TPB, 0, c->stream>>>(
-      seed, 0, TAG_RLK_A, 0, c->logn, L, sk->s_ntt, key, c->mt, pmod); ++c->launches;
+  for (int l = 0; l < L; l++) pmod.w[l] = ks_P_mod(c, c->mod[l]);
+  key_combine_kernel<<<dim3((n + TPB - 1) / TPB, beta * M), TPB, 0, c->stream>>>(
+      seed, 0, TAG_RLK_A, 0, c->logn, L, M, c->alpha, sk->s_ntt, key, c->mt, pmod); ++c->launches;
   if (cudaStreamSynchronize(c->stream) != cudaSuccess) {
     dev_free(c, keys);
     return hd_fail(HD_E_CUDA, "relinearisation keygen");

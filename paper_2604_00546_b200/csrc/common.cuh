@@ -15,7 +15,7 @@
 
 #include "../../include/hd.h"
 
-#define HD_MAXMOD 8
+#define HD_MAXMOD 20  // q_0..q_{L-1} and the K special primes (paper-depth profile: 12 + 4)
 
 // ---------------------------------------------------------------------------
 // Per-modulus constants, passed to kernels by value.
@@ -172,6 +172,7 @@ struct hd_context {
   int device = 0;
   cudaStream_t stream = nullptr;
   int logn = 0, n = 0, ns = 0, L = 0;
+  int K = 1, alpha = 1;  // special primes, limbs per key-switching digit (R11; general: R31)
   uint64_t mod[HD_MAXMOD] = {0};  // q_0..q_{L-1}, P at index L
   uint64_t psi[HD_MAXMOD] = {0};
   ModTab mt;
@@ -207,6 +208,22 @@ constexpr static int kPhaseEvents = 9;
   };
   std::vector<WsBlock> ws_free;
 };
+
+// Key-switching geometry (R11, R31).  Extended basis of a ciphertext at ell limbs: ext index
+// e < ell is q_e, e >= ell the special prime p_{e-ell} (modulus index L + e - ell); a key
+// holds beta(L) digits over the M = L + K moduli.  The alpha = K = 1 profile (the north-star
+// scan) keeps its fused single-limb lifts; any other profile runs the general conversions.
+inline bool ks_general(const hd_context *c) { return c->K != 1 || c->alpha != 1; }
+inline int ks_M(const hd_context *c) { return c->L + c->K; }
+inline int ks_beta(const hd_context *c, int ell) { return (ell + c->alpha - 1) / c->alpha; }
+inline int ks_ext_mod(const hd_context *c, int ell, int e) { return e < ell ? e : c->L + (e - ell); }
+// ModUp digit rows per ciphertext: alpha = K = 1 keeps ell slots per digit (the own limb is
+// read from c1), the general layout every one of the ell + K moduli per digit
+inline size_t ks_dig_elems(const hd_context *c, int ell) {
+  return ks_general(c) ? (size_t)ks_beta(c, ell) * (ell + c->K) * c->n : (size_t)ell * ell * c->n;
+}
+inline size_t ks_key_elems(const hd_context *c) { return (size_t)ks_beta(c, c->L) * 2 * ks_M(c) * c->n; }
+uint64_t ks_P_mod(const hd_context *c, uint64_t q);  // prod_k p_k mod q (host)
 
 // Every device allocation of the library goes through these (no other cudaMalloc).
 // dev_alloc / dev_free: long-lived objects; dev_free first waits for the context's streams

@@ -435,6 +435,8 @@ extern "C" hd_status hd_compare_ex(hd_context *c, const hd_eval_keys *evk, const
   double scale = 0.0;
   hd_status s = check_inputs(c, in, count, ell, scale);
   if (s) return s;
+  if (ks_general(c))  // relinearise-rescale in one rounding needs one special prime (R29)
+    return hd_fail(HD_E_PARAMS, "the comparison is implemented for num_special = digit_limbs = 1 only");
   if (!evk || !coeffs || !out || degree < 1) return hd_fail(HD_E_INVALID_ARG, "null argument");
   if (out_limbs < 1 || out_limbs >= ell) return hd_fail(HD_E_LEVEL, "out_limbs must be in [1, input limbs)");
   if (evk->ctx != c) return hd_fail(HD_E_STATE, "keys from another context");

@@ -174,10 +174,11 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
   if (!p.special_bits) p.special_bits = 60;
   if (!p.num_special) p.num_special = 1;
   if (!p.digit_limbs) p.digit_limbs = 1;
-  if (p.log_n < 4 || p.log_n > 16 || p.num_limbs < 2 || p.num_limbs + 1 > HD_MAXMOD ||
-      p.num_special != 1 || p.digit_limbs != 1 || p.q0_bits > 60 || p.special_bits != p.q0_bits ||
-      p.scale_bits > 60 || p.scale_bits < 20)
-    return hd_fail(HD_E_PARAMS, "supported: log_n in [4,16], num_special = digit_limbs = 1, moduli <= 60 bits");
+  if (p.log_n < 4 || p.log_n > 16 || p.num_limbs < 2 || p.num_limbs + p.num_special > HD_MAXMOD ||
+      p.digit_limbs > p.num_limbs || p.q0_bits > 60 || p.special_bits != p.q0_bits || p.scale_bits > 60 ||
+      p.scale_bits < 20)
+    return hd_fail(HD_E_PARAMS, "supported: log_n in [4,16], num_limbs + num_special <= 20, digit_limbs <= num_limbs, "
+                                "moduli <= 60 bits");
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     return hd_fail(HD_E_CUDA, "no CUDA device (libhd has no CPU fallback)");
@@ -204,12 +205,15 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
   c->n = 1 << c->logn;
   c->ns = c->n / 2;
   c->L = (int)p.num_limbs;
+  c->K = (int)p.num_special;
+  c->alpha = (int)p.digit_limbs;
   const uint64_t two_n = 2 * (uint64_t)c->n;
   c->mod[0] = ntt_prime_below(1ull << p.q0_bits, two_n);
-  c->mod[c->L] = ntt_prime_below(c->mod[0], two_n);
+  // special primes: the next NTT primes below q0, descending (K = 1: P, R5; R31)
+  for (int k = 0; k < c->K; k++) c->mod[c->L + k] = ntt_prime_below(k ? c->mod[c->L + k - 1] : c->mod[0], two_n);
   uint64_t bound = 1ull << p.scale_bits;
   for (int i = 1; i < c->L; i++) bound = c->mod[i] = ntt_prime_below(bound, two_n);
-  for (int i = 0; i <= c->L; i++) {
+  for (int i = 0; i < c->L + c->K; i++) {
     if (!c->mod[i]) { delete c; return hd_fail(HD_E_PARAMS, "no NTT prime"); }
     c->psi[i] = smallest_primitive_root(c->mod[i], c->n);
     uint64_t q = c->mod[i];
@@ -219,7 +223,7 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
     c->mt.r64s[i] = host_shoup(c->mt.r64[i], q);
   }
   // NTT twiddles psi^{br(k)} and inverse, Shoup companions, n^{-1}
-  const int n = c->n, M = c->L + 1;
+  const int n = c->n, M = c->L + c->K;
   // interleaved {w, shoup(w)} per index (one 128-bit load per butterfly group)
   std::vector<uint64_t> tw((size_t)2 * M * n), itw((size_t)2 * M * n), nv(2 * HD_MAXMOD, 0);
   for (int l = 0; l < M; l++) {
@@ -311,9 +315,15 @@ extern "C" hd_status hd_context_set_stream(hd_context *c, void *s) {
   return HD_OK;
 }
 
+uint64_t ks_P_mod(const hd_context *c, uint64_t q) {
+  uint64_t r = 1 % q;
+  for (int k = 0; k < c->K; k++) r = host_mulmod(r, c->mod[c->L + k] % q, q);
+  return r;
+}
+
 extern "C" hd_status hd_context_moduli(const hd_context *c, uint64_t *moduli, uint64_t *psi, size_t cap) {
-  if (!c || cap < (size_t)c->L + 1) return hd_fail(HD_E_INVALID_ARG, "capacity < L+1");
-  for (int i = 0; i <= c->L; i++) {
+  if (!c || cap < (size_t)(c->L + c->K)) return hd_fail(HD_E_INVALID_ARG, "capacity < L + K");
+  for (int i = 0; i < c->L + c->K; i++) {
     if (moduli) moduli[i] = c->mod[i];
     if (psi) psi[i] = c->psi[i];
   }
@@ -339,7 +349,7 @@ static_assert(sizeof(Header) == 64, "header");
 
 uint64_t mod_fingerprint(const hd_context *c) {
   uint64_t h = 1469598103934665603ull;
-  for (int i = 0; i <= c->L; i++) h = (h ^ c->mod[i]) * 1099511628211ull;
+  for (int i = 0; i < c->L + c->K; i++) h = (h ^ c->mod[i]) * 1099511628211ull;
   return h;
 }
 cudaMemcpyKind kind_of(int dst_dev, int src_dev) {
@@ -606,7 +616,7 @@ extern "C" hd_status hd_eval_keys_import(hd_context *c, const void *src, size_t 
   if (s) return s;
   if (h.kind != 2 || h.limbs != (uint32_t)c->L) return hd_fail(HD_E_FORMAT, "not an eval-key set");
   size_t nk = h.count, steps_bytes = ((nk * 4 + 63) / 64) * 64;
-  const size_t key_elems = (size_t)c->L * 2 * (c->L + 1) * c->n;
+  const size_t key_elems = ks_key_elems(c);
   if (nk == 0 || nk > (size_t)c->ns + 1 || h.payload != steps_bytes + sizeof(uint64_t) * key_elems * nk)
     return hd_fail(HD_E_FORMAT, "eval-key payload size does not match its header");
   hd_eval_keys *k = new hd_eval_keys();
@@ -634,7 +644,7 @@ extern "C" hd_status hd_eval_keys_import(hd_context *c, const void *src, size_t 
     hd_eval_keys_destroy(k);
     return hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, cudaGetErrorString(e));
   }
-  if ((s = check_residues(c, k->keys, nk * c->L * 2 * (c->L + 1), c->L + 1))) {
+  if ((s = check_residues(c, k->keys, nk * ks_beta(c, c->L) * 2 * ks_M(c), ks_M(c)))) {
     hd_eval_keys_destroy(k);
     return s;
   }
@@ -651,7 +661,7 @@ extern "C" void hd_eval_keys_destroy(hd_eval_keys *k) {
 extern "C" hd_status hd_secret_key_export(const hd_secret_key *sk, uint64_t *dst, size_t cap) {
   if (!sk || !dst) return hd_fail(HD_E_INVALID_ARG, "null argument");
   const hd_context *c = sk->ctx;
-  size_t need = (size_t)(c->L + 1) * c->n;
+  size_t need = (size_t)ks_M(c) * c->n;
   if (cap < need) return hd_fail(HD_E_INVALID_ARG, "capacity too small");
   HD_CUDA(cudaMemcpy(dst, sk->s_ntt, need * 8, cudaMemcpyDeviceToHost));
   return HD_OK;
@@ -667,7 +677,7 @@ extern "C" hd_status hd_test_ntt(hd_context *c, uint64_t *data, uint32_t n_rows,
                                  int inverse) {
   if (!c || !data || !modulus_idx) return hd_fail(HD_E_INVALID_ARG, "null argument");
   for (uint32_t r = 0; r < n_rows; r++)
-    if (modulus_idx[r] > (uint32_t)c->L) return hd_fail(HD_E_INVALID_ARG, "modulus index > L");
+    if (modulus_idx[r] >= (uint32_t)(c->L + c->K)) return hd_fail(HD_E_INVALID_ARG, "modulus index >= L + K");
   uint64_t *d;
   size_t bytes = (size_t)n_rows * c->n * 8;
   HD_CUDA(dev_alloc(c, &d, bytes));

@@ -305,19 +305,19 @@ static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing,
   const size_t rescale_chunk = std::min<size_t>(A * nj, 256);
   const size_t nb = n1 > 1 ? n1 - 1 : 1;
   // giant / fold / rescale scratch (stream B) and baby-step scratch (stream A)
-  size_t dig_e = A * (L - 1) * (L - 1) * n;
-  size_t u_e = A * 2 * L * n;
+  size_t dig_e = A * ks_dig_elems(c, L - 1);
+  size_t u_e = A * 2 * (L - 1 + c->K) * n;
   size_t tmp_e = std::max({A * 2 * (L - 1) * n, rescale_chunk * 2 * n, (size_t)L * n});
   const size_t sL = (size_t)db->spoly * L * n;  // one giant-step sum
   if (encrypted) {  // relinearisation of A sums at a time at L limbs (ModUp digits, KIP, ModDown)
     db->relin_chunk = (uint32_t)A;
-    dig_e = std::max(dig_e, A * L * L * n);
-    u_e = std::max(u_e, A * 2 * (L + 1) * n);
+    dig_e = std::max(dig_e, A * ks_dig_elems(c, L));
+    u_e = std::max(u_e, A * 2 * (L + c->K) * n);
     tmp_e = std::max(tmp_e, A * 2 * L * n);
   }
   const size_t dstride = (encrypted ? 2 : 1) * (size_t)L * n;  // one diagonal (pt, or ct)
   size_t tmp2_e = encrypted ? A * 2 * (L - 1) * n : 1;  // CRT remainders of the fused relinearise-rescale
-  size_t digb_e = (size_t)L * L * n, ub_e = nb * 2 * (L + 1) * n, tmpb_e = std::max(nb * 2 * L * n, (size_t)L * n);
+  size_t digb_e = ks_dig_elems(c, L), ub_e = nb * 2 * (L + c->K) * n, tmpb_e = std::max(nb * 2 * L * n, (size_t)L * n);
   db->rescale_chunk = (uint32_t)rescale_chunk;
   struct Req {
     void **p;

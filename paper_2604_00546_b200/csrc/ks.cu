@@ -12,6 +12,8 @@
 #include "common.cuh"
 #include "ks.cuh"
 
+#include <vector>
+
 namespace {
 constexpr int TPB = 256;
 
@@ -76,13 +78,13 @@ __global__ void __launch_bounds__(TPB) kip_kernel(const uint64_t *__restrict__ d
 // dst[b][p][e] += P src[b][p][e] for e < ell (the P limb of P src is 0): a giant step
 // without rotation, in the extended basis (R23).  dst rows [b][p][ell+1][n], src [b][p][ell][n].
 __global__ void add_pscaled_kernel(uint64_t *__restrict__ dst, size_t dst_stride, const uint64_t *__restrict__ src,
-                                   size_t src_stride, int ell, int n, ModTab mt, KipAcc ka) {
+                                   size_t src_stride, int ell, int ext, int n, ModTab mt, KipAcc ka) {
   const uint32_t t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
   const uint32_t bpl = blockIdx.y;
   const uint32_t l = bpl % ell, bp = bpl / ell, b = bp / 2, p = bp % 2;
   if (t >= (uint32_t)n) return;
   const uint64_t q = mt.q[l];
-  ulonglong2 *o = reinterpret_cast<ulonglong2 *>(dst + (size_t)b * dst_stride + ((size_t)p * (ell + 1) + l) * n + t);
+  ulonglong2 *o = reinterpret_cast<ulonglong2 *>(dst + (size_t)b * dst_stride + ((size_t)p * ext + l) * n + t);
   const ulonglong2 sv =
       *reinterpret_cast<const ulonglong2 *>(src + (size_t)b * src_stride + ((size_t)p * ell + l) * n + t);
   const ulonglong2 dv = *o;
@@ -126,10 +128,132 @@ KipAcc kip_acc(const hd_context *c, int ell, const uint64_t *c0, size_t c0_strid
   ka.c0 = c0;
   ka.c0_stride = c0_stride;
   for (int l = 0; l < ell; l++) {
-    ka.pw[l] = c->mod[c->L] % c->mod[l];
+    ka.pw[l] = ks_P_mod(c, c->mod[l]);
     ka.pws[l] = host_shoup(ka.pw[l], c->mod[l]);
   }
   return ka;
+}
+
+// ---- general hybrid key switching (R31: alpha limbs per digit, K special primes) ----------
+// Fast basis conversion with centred digits: from the coefficient-form residues x_i of one
+// integer modulo the source moduli b_i (i < cnt), out_j = sum_i y_i (B/b_i) mod m_j with
+// y_i = centred([x_i (B/b_i)^{-1}]_{b_i}) -- for one source modulus the centred lift (R12).
+constexpr int CONV_MAXSRC = 8, CONV_MAXTGT = 24;
+struct ConvTab {
+  int cnt = 0, ntgt = 0;
+  uint8_t src_m[CONV_MAXSRC] = {}, tgt_m[CONV_MAXTGT] = {};
+  uint64_t inv[CONV_MAXSRC] = {}, invs[CONV_MAXSRC] = {};
+  uint64_t hat[CONV_MAXSRC][CONV_MAXTGT] = {}, hats[CONV_MAXSRC][CONV_MAXTGT] = {};
+};
+// src rows of group g: src + g src_gs + i n (i < cnt); out rows: out + g out_gs + j n (j < ntgt)
+__global__ void __launch_bounds__(TPB) conv_kernel(const uint64_t *__restrict__ src, size_t src_gs,
+                                                   uint64_t *__restrict__ out, size_t out_gs, int n, ModTab mt,
+                                                   ConvTab ct) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t g = blockIdx.y;
+  if (t >= (uint32_t)n) return;
+  uint64_t mag[CONV_MAXSRC];
+  bool neg[CONV_MAXSRC];
+  for (int i = 0; i < ct.cnt; i++) {
+    const int bm = ct.src_m[i];
+    const uint64_t b = mt.q[bm];
+    const uint64_t y = shoup(src[(size_t)g * src_gs + (size_t)i * n + t], ct.inv[i], ct.invs[i], b);
+    neg[i] = y > (b >> 1);
+    mag[i] = neg[i] ? b - y : y;
+  }
+  for (int j = 0; j < ct.ntgt; j++) {
+    const int m = ct.tgt_m[j];
+    const uint64_t q = mt.q[m], bar = mt.bar[m];
+    uint64_t acc = 0;
+    for (int i = 0; i < ct.cnt; i++) {
+      const uint64_t v = shoup(reduce64(mag[i], q, bar), ct.hat[i][j], ct.hats[i][j], q);
+      acc = addmod(acc, neg[i] ? (v ? q - v : 0) : v, q);
+    }
+    out[(size_t)g * out_gs + (size_t)j * n + t] = acc;
+  }
+}
+
+ConvTab conv_table(const hd_context *c, const std::vector<int> &srcm, const std::vector<int> &tgtm) {
+  ConvTab ct;
+  ct.cnt = (int)srcm.size();
+  ct.ntgt = (int)tgtm.size();
+  for (int i = 0; i < ct.cnt; i++) {
+    const uint64_t b = c->mod[srcm[i]];
+    uint64_t hb = 1 % b;
+    for (int k = 0; k < ct.cnt; k++)
+      if (k != i) hb = host_mulmod(hb, c->mod[srcm[k]] % b, b);
+    ct.src_m[i] = (uint8_t)srcm[i];
+    ct.inv[i] = host_powmod(hb, b - 2, b);
+    ct.invs[i] = host_shoup(ct.inv[i], b);
+    for (int j = 0; j < ct.ntgt; j++) {
+      const uint64_t m = c->mod[tgtm[j]];
+      uint64_t h = 1 % m;
+      for (int k = 0; k < ct.cnt; k++)
+        if (k != i) h = host_mulmod(h, c->mod[srcm[k]] % m, m);
+      ct.hat[i][j] = h;
+      ct.hats[i][j] = host_shoup(h, m);
+    }
+  }
+  for (int j = 0; j < ct.ntgt; j++) ct.tgt_m[j] = (uint8_t)tgtm[j];
+  return ct;
+}
+
+hd_status conv_run(hd_context *c, const uint64_t *src, size_t src_gs, uint32_t groups, uint64_t *out, size_t out_gs,
+                   const ConvTab &ct) {
+  if (ct.cnt > CONV_MAXSRC || ct.ntgt > CONV_MAXTGT) return hd_fail(HD_E_PARAMS, "basis conversion too wide");
+  conv_kernel<<<dim3((c->n + TPB - 1) / TPB, groups), TPB, 0, c->stream>>>(src, src_gs, out, out_gs, c->n, c->mt, ct);
+  ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  return HD_OK;
+}
+
+// Key inner product over the general extended basis; x = b * K + k, output u[x][p][e],
+// e < ell + Ksp.  dig [b][d][e][n] (every modulus per digit, NTT form), key [d][p][M][n].
+// Accumulate mode as kip_kernel (R23).  Two coefficients per thread.
+__global__ void __launch_bounds__(TPB) kipg_kernel(const uint64_t *__restrict__ dig, uint64_t *__restrict__ u, int ell,
+                                                   int ext, int beta, int K, int L, int M, int logn,
+                                                   const uint64_t *const *__restrict__ kptr,
+                                                   const uint32_t *__restrict__ gal, ModTab mt, KipAcc ka,
+                                                   FDiv f_ext, FDiv f_K) {
+  const int n = 1 << logn;
+  const uint32_t t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const uint32_t xe = blockIdx.y;
+  const uint32_t x = fdiv_q(xe, f_ext), e = xe - x * ext;
+  const uint32_t b = fdiv_q(x, f_K), k = x - b * K;
+  if (t >= (uint32_t)n) return;
+  const int gm = (int)e < ell ? (int)e : L + ((int)e - ell);
+  const uint32_t g = gal[k];
+  const uint32_t s0 = galois_src(t, g, logn), s1 = galois_src(t + 1, g, logn);
+  const uint64_t *key = kptr[k];
+  const uint64_t *dg = dig + (size_t)b * beta * ext * n + (size_t)e * n;
+  uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0, b0l = 0, b0h = 0, b1l = 0, b1h = 0;
+  for (int d = 0; d < beta; d++) {
+    const uint64_t *row = dg + (size_t)d * ext * n;
+    const uint64_t v0 = row[s0], v1 = row[s1];
+    const ulonglong2 k0 = *reinterpret_cast<const ulonglong2 *>(key + ((size_t)(d * 2 + 0) * M + gm) * n + t);
+    const ulonglong2 k1 = *reinterpret_cast<const ulonglong2 *>(key + ((size_t)(d * 2 + 1) * M + gm) * n + t);
+    mac128(a0l, a0h, v0, k0.x);
+    mac128(b0l, b0h, v1, k0.y);
+    mac128(a1l, a1h, v0, k1.x);
+    mac128(b1l, b1h, v1, k1.y);
+  }
+  const uint64_t q = mt.q[gm], bar = mt.bar[gm], r64 = mt.r64[gm], r64s = mt.r64s[gm];
+  ulonglong2 *o0 = reinterpret_cast<ulonglong2 *>(u + ((size_t)(x * 2 + 0) * ext + e) * n + t);
+  ulonglong2 *o1 = reinterpret_cast<ulonglong2 *>(u + ((size_t)(x * 2 + 1) * ext + e) * n + t);
+  ulonglong2 v0 = make_ulonglong2(reduce128(a0h, a0l, q, bar, r64, r64s), reduce128(b0h, b0l, q, bar, r64, r64s));
+  ulonglong2 v1 = make_ulonglong2(reduce128(a1h, a1l, q, bar, r64, r64s), reduce128(b1h, b1l, q, bar, r64, r64s));
+  if (ka.c0) {
+    const ulonglong2 p0 = *o0, p1 = *o1;
+    v0 = make_ulonglong2(addmod(v0.x, p0.x, q), addmod(v0.y, p0.y, q));
+    v1 = make_ulonglong2(addmod(v1.x, p1.x, q), addmod(v1.y, p1.y, q));
+    if ((int)e < ell) {
+      const uint64_t *c0r = ka.c0 + (size_t)b * ka.c0_stride + (size_t)e * n;
+      v0.x = addmod(v0.x, shoup(c0r[s0], ka.pw[e], ka.pws[e], q), q);
+      v0.y = addmod(v0.y, shoup(c0r[s1], ka.pw[e], ka.pws[e], q), q);
+    }
+  }
+  *o0 = v0;
+  *o1 = v1;
 }
 
 inline dim3 grid_pairs(int n, uint32_t rows) { return dim3((n / 2 + TPB - 1) / TPB, rows); }
@@ -153,6 +277,27 @@ hd_status ks_modup(hd_context *c, const uint64_t *c1, size_t c1_stride, uint32_t
   src.map.gstride = c1_stride;
   hd_status s = ntt_run(c, tmp, B * ell, rt, true, &src, nullptr);
   if (s) return s;
+  if (ks_general(c)) {
+    // 2. digit d (limbs [d alpha, min((d+1) alpha, ell))): fast basis conversion with centred
+    //    digits into every modulus e of Q_ell u P (own limbs reproduce c1), rows dig[b][d][e]
+    const int ext = ell + c->K, beta = ks_beta(c, ell);
+    std::vector<int> tg(ext);
+    for (int e = 0; e < ext; e++) tg[e] = ks_ext_mod(c, ell, e);
+    for (int d = 0; d < beta; d++) {
+      const int lo = d * c->alpha, cnt = std::min(c->alpha, ell - lo);
+      std::vector<int> sm(cnt);
+      for (int i = 0; i < cnt; i++) sm[i] = lo + i;
+      if ((s = conv_run(c, tmp + (size_t)lo * n, (size_t)ell * n, B, dig + (size_t)d * ext * n,
+                        (size_t)beta * ext * n, conv_table(c, sm, tg))))
+        return s;
+    }
+    // 3. NTT of every digit row
+    RowMap rd{};
+    rd.mdiv = 1;
+    rd.mlen = ext;
+    for (int e = 0; e < ext; e++) rd.midx[e] = (uint8_t)tg[e];
+    return ntt_run(c, dig, B * beta * ext, rd, false, nullptr, nullptr);
+  }
   // 2. rows (b, d, slot) of dig: NTT over ext modulus e = slot < d ? slot : slot + 1 of the
   //    centred lift of tmp[b][d] (source modulus q_d)
   RowMap rd{};
@@ -177,6 +322,15 @@ hd_status ks_modup(hd_context *c, const uint64_t *c1, size_t c1_stride, uint32_t
 
 hd_status ks_kip(hd_context *c, const uint64_t *dig, const uint64_t *c1, size_t c1_stride, uint32_t B, uint32_t K,
                  int ell, const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u) {
+  if (ks_general(c)) {
+    const int ext = ell + c->K;
+    kipg_kernel<<<grid_pairs(c->n, B * K * ext), TPB, 0, c->stream>>>(
+        dig, u, ell, ext, ks_beta(c, ell), K, c->L, ks_M(c), c->logn, kptr_dev, gal_dev, c->mt, KipAcc{},
+        fdiv_make(ext), fdiv_make(K));
+    ++c->launches;
+    HD_CUDA(cudaGetLastError());
+    return HD_OK;
+  }
   kip_kernel<<<grid_pairs(c->n, B * K * (ell + 1)), TPB, 0, c->stream>>>(dig, c1, c1_stride, u, ell, K, c->L, c->logn,
                                                                         kptr_dev, gal_dev, c->mt, KipAcc{},
                                                                         fdiv_make(ell + 1), fdiv_make(K));
@@ -187,6 +341,15 @@ hd_status ks_kip(hd_context *c, const uint64_t *dig, const uint64_t *c1, size_t 
 
 hd_status ks_kip_accumulate(hd_context *c, const uint64_t *dig, const uint64_t *ct, size_t ct_stride, uint32_t B,
                             int ell, const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u) {
+  if (ks_general(c)) {
+    const int ext = ell + c->K;
+    kipg_kernel<<<grid_pairs(c->n, B * ext), TPB, 0, c->stream>>>(
+        dig, u, ell, ext, ks_beta(c, ell), 1, c->L, ks_M(c), c->logn, kptr_dev, gal_dev, c->mt,
+        kip_acc(c, ell, ct, ct_stride), fdiv_make(ext), fdiv_make(1));
+    ++c->launches;
+    HD_CUDA(cudaGetLastError());
+    return HD_OK;
+  }
   kip_kernel<<<grid_pairs(c->n, B * (ell + 1)), TPB, 0, c->stream>>>(
       dig, ct + (size_t)ell * c->n, ct_stride, u, ell, 1, c->L, c->logn, kptr_dev, gal_dev, c->mt,
       kip_acc(c, ell, ct, ct_stride), fdiv_make(ell + 1), fdiv_make(1));
@@ -197,7 +360,7 @@ hd_status ks_kip_accumulate(hd_context *c, const uint64_t *dig, const uint64_t *
 
 hd_status ks_add_pscaled(hd_context *c, uint64_t *u, const uint64_t *ct, size_t ct_stride, uint32_t B, int ell) {
   add_pscaled_kernel<<<grid_pairs(c->n, B * 2 * ell), TPB, 0, c->stream>>>(
-      u, (size_t)2 * (ell + 1) * c->n, ct, ct_stride, ell, c->n, c->mt, kip_acc(c, ell, nullptr, 0));
+      u, (size_t)2 * (ell + c->K) * c->n, ct, ct_stride, ell, ell + c->K, c->n, c->mt, kip_acc(c, ell, nullptr, 0));
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;
@@ -207,6 +370,45 @@ hd_status ks_moddown(hd_context *c, uint64_t *u, uint32_t X, uint32_t K, int ell
                      const uint64_t *c0, size_t c0_stride, uint64_t *dst, size_t dst_stride, bool accumulate,
                      uint64_t *tmp) {
   const int n = c->n, L = c->L;
+  if (ks_general(c)) {
+    const int Ksp = c->K, ext = ell + Ksp;
+    // 1. INTT of the K special limbs of both polys, in place: rows (x*2 + p, k) at u + (r ext + ell + k) n
+    RowMap rp{};
+    rp.gsize = Ksp;
+    rp.gstride = (uint64_t)ext * n;
+    rp.mdiv = 1;
+    rp.mlen = Ksp;
+    for (int k = 0; k < Ksp; k++) rp.midx[k] = (uint8_t)(L + k);
+    hd_status s = ntt_run(c, u + (size_t)ell * n, 2 * X * Ksp, rp, true, nullptr, nullptr);
+    if (s) return s;
+    // 2. fast basis conversion (centred digits) from P = prod p_k into q_0 .. q_{ell-1}: tmp [x][p][l]
+    std::vector<int> sm(Ksp), tg(ell);
+    for (int k = 0; k < Ksp; k++) sm[k] = L + k;
+    for (int l = 0; l < ell; l++) tg[l] = l;
+    if ((s = conv_run(c, u + (size_t)ell * n, (size_t)ext * n, 2 * X, tmp, (size_t)ell * n, conv_table(c, sm, tg))))
+      return s;
+    // 3. NTT_l of the converted rows, final store dst_x[p][l] (+)= (u[x][p][l] - .) P^{-1} (+ pi_g(c0_b)[l])
+    RowMap rq = mods_seq(RowMap{}, 1, ell);
+    NttEpi epi;
+    epi.mode = c0 ? 2 : 1;
+    epi.acc = accumulate;
+    epi.ell = ell;
+    epi.K = K;
+    epi.A = u;
+    epi.amap.gsize = ell;
+    epi.amap.gstride = (uint64_t)ext * n;
+    epi.out = dst;
+    epi.omap.gsize = 2 * ell;
+    epi.omap.gstride = dst_stride;
+    epi.c0 = c0;
+    epi.c0_stride = c0_stride;
+    epi.gal = gal_dev;
+    for (int l = 0; l < ell; l++) {
+      epi.w[l] = host_powmod(ks_P_mod(c, c->mod[l]), c->mod[l] - 2, c->mod[l]);
+      epi.ws[l] = host_shoup(epi.w[l], c->mod[l]);
+    }
+    return ntt_run(c, tmp, 2 * X * ell, rq, false, nullptr, &epi);
+  }
   // 1. INTT of the P limb of both polys, in place: rows r = x*2 + p at u + (r (ell+1) + ell) n
   RowMap rp = rowmap_simple(1, {L}, 1, (uint64_t)(ell + 1) * n);
   hd_status s = ntt_run(c, u + (size_t)ell * n, 2 * X, rp, true, nullptr, nullptr);
@@ -288,6 +490,8 @@ hd_status ks_rescale(hd_context *c, const uint64_t *S, size_t s_stride, uint32_t
 hd_status ks_relin_rescale(hd_context *c, uint64_t *S3, uint32_t B, int ell, const uint64_t *const *rlk_dev,
                            const uint32_t *gal_dev, uint64_t *out, uint64_t *dig, uint64_t *u, uint64_t *tmp,
                            uint64_t *V) {
+  if (ks_general(c))  // the two-modulus CRT rounding needs one special prime (R29)
+    return hd_fail(HD_E_PARAMS, "relinearisation is implemented for num_special = digit_limbs = 1 only");
   const int n = c->n, L = c->L, lo = ell - 1;
   const size_t s3 = (size_t)3 * ell * n;
   uint64_t *d2 = S3 + (size_t)2 * ell * n;

@@ -49,7 +49,7 @@ hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t 
 // diagonal pass; r [Q][n1][2][L][n], S [Q][A][nj][2][L][n].  HD_MAC_VARIANT=c selects mac.cu.
 bool mac_tma_supported(const hd_context *c, int n1, int N, bool flat, uint32_t Q);
 hd_status mac_tma_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A, int n1, int N,
-                      const std::vector<int32_t> &js, uint32_t Q);
+                      const std::vector<int32_t> &js, uint32_t Q, bool flat);
 
 // Query batching (NEXT-4): Q queries per D pass; r [Q][n1][2][L][n], S [Q][A][nj][2][L][n].
 hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1,

@@ -493,7 +493,7 @@ hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
                   const std::vector<int32_t> &js, bool flat) {
   if (js.empty() || A_loc == 0) return HD_OK;
-  if (mac_tma_supported(c, n1, N, flat, 1)) return mac_tma_run(c, D, r, S, A_loc, n1, N, js, 1);
+  if (mac_tma_supported(c, n1, N, flat, 1)) return mac_tma_run(c, D, r, S, A_loc, n1, N, js, 1, flat);
   const int jmin = js.front(), nj = (int)js.size();
   // every giant step uses all n1 baby steps (replicated: n1 | N/2; flat: n1 | N)
   const bool full = (flat ? N % n1 : (N / 2) % n1) == 0 && n1 <= 256 && c->n % MAC_TPB == 0;
@@ -531,7 +531,7 @@ hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uin
     const uint32_t gmax = g_env ? std::max(1, std::min(4, atoi(g_env))) : 4;
     for (uint32_t b0 = 0; b0 < Q;) {
       const uint32_t g = std::min(gmax, Q - b0);
-      hd_status s = mac_tma_run(c, D, r + b0 * rq, S + b0 * sq, A_loc, n1, N, js, g);
+      hd_status s = mac_tma_run(c, D, r + b0 * rq, S + b0 * sq, A_loc, n1, N, js, g, flat);
       if (s) return s;
       b0 += g;
     }

@@ -4,20 +4,20 @@
 //   S[b][a][j][p][m][t] = sum_{i < n1} r[b][i][p][m][t] * D[a][k(j,i)][m][t]  mod q_m,
 //   k(j,i) = (j n1 + i) mod N   (replicated: preshifted giant steps; flat: j n1 + i < N)
 //
-// for full giant-step ranges (every j uses all n1 baby steps), q_m < 2^60, b < QB queries.
+// for full giant-step ranges (n1 | N/2 replicated, n1 | N flat), q_m < 2^60, b < QB queries.
 //
-// Why this shape: the LDG kernel (mac.cu, mac_cs_kernel) spends ~40
-// SASS per diagonal word -- address formation, predicated prefetch, register staging -- and
-// sits at ~63 % issue, i.e. it is issue-bound below the HBM roofline.  Here a producer warp
-// streams the diagonals with 3-D TMA boxes (128 coefficients x 1 limb x SPS consecutive
-// diagonals, evict-first) and the baby-step rows (r, L2-resident) into a ring of shared-memory
-// stages; consumer threads own one coefficient of one aggregate and ALL JT giant steps of
+// Design.  Giant step j reads the diagonal block G(j) = k(j,0) / n1 of
+// n1 consecutive diagonals, so D of one aggregate is a 5-D tensor (coefficient, limb, diagonal
+// within a block, block, aggregate).  A producer warp streams, per pipeline stage, ONE TMA box
+// of 128 coefficients x 1 limb x SPS baby steps x JT blocks x AG aggregates (evict-first) plus
+// one box of the baby-step rows r (L2-resident, evict-last) into a ring of shared-memory
+// stages.  Consumer threads own one coefficient of one aggregate and all JT giant steps of
 // their unit, so each r word read from shared memory serves JT diagonal words and each
-// diagonal word costs two carry-save products plus one LDS.  The ring keeps ~200 KB of loads
-// in flight per SM without a register per byte.
+// diagonal word costs one LDS and two carry-save 64x64 products (no address arithmetic, no
+// register staging of loads in flight).
 //
-// Work unit = (AG consecutive aggregates, giant-step group of JT, 128-coefficient tile, limb);
-// one persistent CTA per SM walks units u = blockIdx.x, + gridDim.x, ... with the aggregate
+// Work unit = (AG aggregates, JT consecutive blocks, 128-coefficient tile, limb); one
+// persistent CTA per SM walks units u = blockIdx.x, + gridDim.x, ... with the aggregate
 // group fastest so concurrently resident CTAs share few r tiles (L2 reuse).
 #include "common.cuh"
 #include "ks.cuh"
@@ -60,6 +60,15 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4,
+                                            uint64_t *bar, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)),
+      "l"(policy)
+      : "memory");
+}
 
 // carry-save 64x64 multiply-accumulate, as mac.cu (a1, b1 < 2^28): value = lo + mid 2^32 +
 // (hi + cnt) 2^64; mid folded every 8 products
@@ -87,121 +96,78 @@ __device__ __forceinline__ void acc_fold(Acc &A) {
 }
 
 struct Unit {
-  uint32_t a0;  // first aggregate of the group
-  int jg, tile, m;
+  uint32_t a0;       // first aggregate of the group
+  int gg0, tile, m;  // first diagonal block, coefficient tile, limb
 };
-__device__ __forceinline__ Unit decode(uint32_t u, uint32_t nag, int ngrp, int tiles, int AG) {
+__device__ __forceinline__ Unit decode(uint32_t u, uint32_t nag, int ngrp, int tiles, int AG, int JT) {
   Unit x;
   x.a0 = (u % nag) * AG;
   u /= nag;
-  x.jg = (int)(u % ngrp);
+  x.gg0 = (int)(u % ngrp) * JT;
   u /= ngrp;
   x.tile = (int)(u % tiles);
   x.m = (int)(u / tiles);
   return x;
 }
 
-// Producer state: the next (unit, baby-step block) to load and the ring slot it goes to.
-template <int AG, int JT, int QB, int SPS>
-struct Producer {
-  uint32_t u, units, nag, step;
-  int sb, nsb, ngrp, tiles, stage, stages, jmin, n1, N, qrows;
-  uint32_t phase;
-  uint64_t pol_stream, pol_keep;
-  __device__ __forceinline__ bool more() const { return u < units; }
-  // wait until the slot is free, then issue its TMA loads (D boxes evict-first, r evict-last)
-  __device__ __forceinline__ void issue(unsigned char *smem, uint64_t *full, uint64_t *empty, const CUtensorMap *tmD,
-                                        const CUtensorMap *tmR) {
-    constexpr int D_WORDS = AG * JT * SPS * TC, R_WORDS = QB * SPS * 2 * TC;
-    constexpr uint32_t STAGE_BYTES = (D_WORDS + R_WORDS) * 8;
-    const Unit x = decode(u, nag, ngrp, tiles, AG);
-    mbar_wait(&empty[stage], phase ^ 1);
-    mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-    uint64_t *base = reinterpret_cast<uint64_t *>(smem + (size_t)stage * STAGE_BYTES);
-#pragma unroll
-    for (int g = 0; g < AG; g++)
-#pragma unroll
-      for (int jj = 0; jj < JT; jj++) {
-        const int j = jmin + x.jg * JT + jj;
-        const int k0 = ((j * n1 + sb * SPS) % N + N) % N;  // SPS consecutive diagonals (no wrap)
-        tma_load_3d(base + (g * JT + jj) * SPS * TC, tmD, x.tile * TC, x.m, (int)((x.a0 + g) * N + k0), &full[stage],
-                    pol_stream);
-      }
-#pragma unroll
-    for (int b = 0; b < QB; b++)
-      tma_load_3d(base + D_WORDS + b * SPS * 2 * TC, tmR, x.tile * TC, x.m, b * qrows + sb * SPS * 2, &full[stage],
-                  pol_keep);
-    if (++stage == stages) {
-      stage = 0;
-      phase ^= 1;
-    }
-    if (++sb == nsb) {
-      sb = 0;
-      u += step;
-    }
-  }
-};
-
-// AG aggregates x TC coefficients consumer threads (+ one producer warp unless INLINE: then
-// thread 0 also issues the loads, one slot per iteration, and all 4 AG warps compute).
-// Stage layout (u64): D[AG][JT][SPS][TC], then r[QB][SPS][2][TC].
-template <int AG, int JT, int QB, int SPS, bool FLUSH, bool INLINE>
-__global__ void __launch_bounds__(AG *TC + (INLINE ? 0 : 32), 1)
+// AG aggregates x TC coefficients consumer threads + one producer warp.
+// Stage layout (u64): D[AG][JT][SPS][TC] (the 5-D box), then r[QB][SPS][2][TC].
+// flags (measurement only): 1 = stream without arithmetic, 2 = arithmetic without the stream.
+template <int AG, int JT, int QB, int SPS, bool FLUSH>
+__global__ void __launch_bounds__(AG *TC + 32, 1)
     mac_tma_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmR,
-                   uint64_t *__restrict__ S, int n1, int N, int L, int logn, int jmin, int nj, uint32_t A,
-                   int stages, int qrows, size_t s_query_stride, ModTab mt, int dry) {
+                   uint64_t *__restrict__ S, int n1, int N, int L, int logn, int nj, uint32_t A, int flat, int stages,
+                   int qrows, size_t s_query_stride, ModTab mt, int flags) {
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int D_WORDS = AG * JT * SPS * TC, R_WORDS = QB * SPS * 2 * TC;
   constexpr uint32_t STAGE_BYTES = (D_WORDS + R_WORDS) * 8;
   constexpr int CONSUMERS = AG * TC;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)stages * STAGE_BYTES);
   uint64_t *empty = full + stages;
-  const int n = 1 << logn, tiles = n / TC, ngrp = nj / JT, nsb = n1 / SPS;
+  const int n = 1 << logn, tiles = n / TC, G = N / n1, ngrp = G / JT, nsb = n1 / SPS;
   const uint32_t nag = A / AG, units = nag * (uint32_t)ngrp * (uint32_t)tiles * (uint32_t)L;
   if (threadIdx.x == 0) {
     for (int s = 0; s < stages; s++) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CONSUMERS);
+      mbar_init(&empty[s], CONSUMERS / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  Producer<AG, JT, QB, SPS> pr;
-  const bool is_producer = INLINE ? threadIdx.x == 0 : threadIdx.x == CONSUMERS;
-  if (is_producer) {
-    pr.u = blockIdx.x;
-    pr.units = units;
-    pr.nag = nag;
-    pr.step = gridDim.x;
-    pr.sb = 0;
-    pr.nsb = nsb;
-    pr.ngrp = ngrp;
-    pr.tiles = tiles;
-    pr.stage = 0;
-    pr.stages = stages;
-    pr.jmin = jmin;
-    pr.n1 = n1;
-    pr.N = N;
-    pr.qrows = qrows;
-    pr.phase = 0;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pr.pol_stream));
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pr.pol_keep));
-  }
-  if (!INLINE && threadIdx.x >= CONSUMERS) {  // ---------------- producer warp ----------------
-    if (is_producer)
-      while (pr.more()) pr.issue(smem, full, empty, &tmD, &tmR);
+
+  if (threadIdx.x >= CONSUMERS) {  // ---------------- producer warp ----------------
+    if (threadIdx.x != CONSUMERS || (flags & 2)) return;
+    uint64_t pol_stream, pol_keep;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    int stage = 0;
+    uint32_t phase = 0;
+    for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
+      for (int sb = 0; sb < nsb; sb++) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+        uint64_t *base = reinterpret_cast<uint64_t *>(smem + (size_t)stage * STAGE_BYTES);
+        tma_load_5d(base, &tmD, x.tile * TC, x.m, sb * SPS, x.gg0, (int)x.a0, &full[stage], pol_stream);
+#pragma unroll
+        for (int b = 0; b < QB; b++)
+          tma_load_3d(base + D_WORDS + b * SPS * 2 * TC, &tmR, x.tile * TC, x.m, b * qrows + sb * SPS * 2,
+                      &full[stage], pol_keep);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
     return;
   }
-  if (INLINE && is_producer)  // prefill every slot (fresh slots are free)
-    for (int k = 0; k < stages && pr.more(); k++) pr.issue(smem, full, empty, &tmD, &tmR);
-  bool first = true;
 
   // ---------------- consumers: thread = (aggregate g of the group, coefficient t) ----------------
   const int g = threadIdx.x / TC, t = threadIdx.x % TC;
   int stage = 0;
   uint32_t phase = 0;
   for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const Unit x = decode(u, nag, ngrp, tiles, AG);
+    const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
     const uint64_t q = mt.q[x.m], bar = mt.bar[x.m], r64 = mt.r64[x.m], r64s = mt.r64s[x.m];
     Acc acc[QB][JT][2];
     uint64_t part[QB][JT][2];
@@ -213,39 +179,33 @@ __global__ void __launch_bounds__(AG *TC + (INLINE ? 0 : 32), 1)
         part[b][jj][0] = part[b][jj][1] = 0;
       }
     for (int sb = 0; sb < nsb; sb++) {
-      // inline producer: refill the slot the CTA released last iteration (waits for the
-      // slowest warp to finish it), `stages - 1` blocks ahead of this one
-      if (INLINE && is_producer && !first && pr.more()) pr.issue(smem, full, empty, &tmD, &tmR);
-      first = false;
-      mbar_wait(&full[stage], phase);
-      if (dry) {  // measurement only (HD_MAC_TMA_DRY=1): the TMA stream without the arithmetic
-        mbar_arrive(&empty[stage]);
-        if (++stage == stages) {
-          stage = 0;
-          phase ^= 1;
-        }
-        continue;
-      }
-      const uint64_t *Ds = reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + g * JT * SPS * TC + t;
-      const uint64_t *Rs = reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + D_WORDS + t;
+      if (!(flags & 2)) mbar_wait(&full[stage], phase);
+      if (!(flags & 1)) {
+        const uint64_t *Ds =
+            reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + g * JT * SPS * TC + t;
+        const uint64_t *Rs = reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + D_WORDS + t;
 #pragma unroll
-      for (int s = 0; s < SPS; s++) {
-        uint64_t d[JT];
+        for (int s = 0; s < SPS; s++) {
+          uint64_t d[JT];
 #pragma unroll
-        for (int jj = 0; jj < JT; jj++) d[jj] = Ds[(jj * SPS + s) * TC];
+          for (int jj = 0; jj < JT; jj++) d[jj] = Ds[(jj * SPS + s) * TC];
 #pragma unroll
-        for (int b = 0; b < QB; b++) {
-          const uint64_t r0 = Rs[(b * SPS * 2 + 2 * s) * TC], r1 = Rs[(b * SPS * 2 + 2 * s + 1) * TC];
-          const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1, r11 = (uint32_t)(r1 >> 32);
+          for (int b = 0; b < QB; b++) {
+            const uint64_t r0 = Rs[(b * SPS * 2 + 2 * s) * TC], r1 = Rs[(b * SPS * 2 + 2 * s + 1) * TC];
+            const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1,
+                           r11 = (uint32_t)(r1 >> 32);
 #pragma unroll
-          for (int jj = 0; jj < JT; jj++) {
-            const uint32_t b0 = (uint32_t)d[jj], b1 = (uint32_t)(d[jj] >> 32);
-            acc_mac(acc[b][jj][0], r00, r01, b0, b1);
-            acc_mac(acc[b][jj][1], r10, r11, b0, b1);
+            for (int jj = 0; jj < JT; jj++) {
+              const uint32_t b0 = (uint32_t)d[jj], b1 = (uint32_t)(d[jj] >> 32);
+              acc_mac(acc[b][jj][0], r00, r01, b0, b1);
+              acc_mac(acc[b][jj][1], r10, r11, b0, b1);
+            }
           }
         }
       }
-      mbar_arrive(&empty[stage]);  // this thread's reads of the stage are done
+      // one arrival per warp once every lane's shared-memory reads of the stage are done
+      __syncwarp();
+      if (!(flags & 2) && (threadIdx.x & 31) == 0) mbar_arrive(&empty[stage]);
       if (++stage == stages) {
         stage = 0;
         phase ^= 1;
@@ -276,10 +236,14 @@ __global__ void __launch_bounds__(AG *TC + (INLINE ? 0 : 32), 1)
     const size_t ls = (size_t)L * n;
     const uint32_t a = x.a0 + g;
 #pragma unroll
-    for (int b = 0; b < QB; b++)
+    for (int jj = 0; jj < JT; jj++) {
+      // diagonal block gg holds giant step j with (j n1) mod N = gg n1: flat j = gg;
+      // replicated j = gg for gg n1 < N/2, else gg - N/n1; S slot j - jmin
+      const int gg = x.gg0 + jj;
+      const int jslot = flat ? gg : (gg < G / 2 ? gg + G / 2 : gg - G / 2);
 #pragma unroll
-      for (int jj = 0; jj < JT; jj++) {
-        uint64_t *Sa = S + b * s_query_stride + ((size_t)a * nj + x.jg * JT + jj) * 2 * ls + (size_t)x.m * n +
+      for (int b = 0; b < QB; b++) {
+        uint64_t *Sa = S + b * s_query_stride + ((size_t)a * nj + jslot) * 2 * ls + (size_t)x.m * n +
                        (size_t)x.tile * TC + t;
 #pragma unroll
         for (int p = 0; p < 2; p++) {
@@ -288,6 +252,7 @@ __global__ void __launch_bounds__(AG *TC + (INLINE ? 0 : 32), 1)
           Sa[(size_t)p * ls] = addmod(part[b][jj][p], reduce128(X.hi + X.cnt, X.lo, q, bar, r64, r64s), q);
         }
       }
+    }
   }
 }
 
@@ -303,17 +268,13 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// rows of n u64 coefficients grouped as [rows][L][n]: a 3-D map (coef, limb, row), box
-// (TC, 1, box_rows)
-hd_status make_map(CUtensorMap *map, const uint64_t *base, int n, int L, uint64_t rows, uint32_t box_rows) {
+hd_status encode(CUtensorMap *map, const uint64_t *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides,
+                 const cuuint32_t *box) {
   auto fn = encode_fn();
   if (!fn) return hd_fail(HD_E_CUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)L, (cuuint64_t)rows};
-  cuuint64_t strides[2] = {(cuuint64_t)n * 8, (cuuint64_t)L * n * 8};
-  cuuint32_t box[3] = {(cuuint32_t)TC, 1, box_rows};
-  cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, const_cast<uint64_t *>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+  cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, (cuuint32_t)rank, const_cast<uint64_t *>(base), dims, strides,
+                  box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return hd_fail(HD_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return HD_OK;
@@ -321,43 +282,43 @@ hd_status make_map(CUtensorMap *map, const uint64_t *base, int n, int L, uint64_
 
 int g_num_sms = 0;
 
-template <int AG, int JT, int QB, int SPS, bool FLUSH, bool INLINE>
-hd_status launch(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int jmin,
-                 int nj, uint32_t A, int qrows, size_t sq) {
+template <int AG, int JT, int QB, int SPS, bool FLUSH>
+hd_status launch(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int nj,
+                 uint32_t A, bool flat, int qrows, size_t sq) {
   constexpr size_t STAGE_BYTES = (size_t)(AG * JT * SPS * TC + QB * SPS * 2 * TC) * 8;
   const size_t budget = 227 * 1024 - 256;
-  int stages = (int)std::min<size_t>(8, budget / STAGE_BYTES);
+  int stages = (int)std::min<size_t>(16, budget / STAGE_BYTES);
   if (const char *e = getenv("HD_MAC_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));  // A/B knob
   if (stages < 2) return hd_fail(HD_E_PARAMS, "MAC stage does not fit shared memory");
   const size_t smem = stages * STAGE_BYTES + 2 * stages * sizeof(uint64_t);
-  auto kern = mac_tma_kernel<AG, JT, QB, SPS, FLUSH, INLINE>;
+  auto kern = mac_tma_kernel<AG, JT, QB, SPS, FLUSH>;
   HD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (!g_num_sms) HD_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, c->device));
   const uint32_t units = (A / AG) * (uint32_t)(nj / JT) * (uint32_t)(c->n / TC) * (uint32_t)c->L;
   const uint32_t grid = std::min<uint32_t>(units, (uint32_t)g_num_sms);
-  const char *dry = getenv("HD_MAC_TMA_DRY");
-  kern<<<grid, AG * TC + (INLINE ? 0 : 32), smem, c->stream>>>(mD, mR, S, n1, N, c->L, c->logn, jmin, nj, A, stages, qrows, sq,
-                                                c->mt, dry && dry[0] == '1');
+  const char *dry = getenv("HD_MAC_TMA_DRY"), *co = getenv("HD_MAC_COMPUTE_ONLY");  // measurement only
+  const int flags = (dry && dry[0] == '1' ? 1 : 0) | (co && co[0] == '1' ? 2 : 0);
+  kern<<<grid, AG * TC + 32, smem, c->stream>>>(mD, mR, S, n1, N, c->L, c->logn, nj, A, flat ? 1 : 0, stages, qrows,
+                                                sq, c->mt, flags);
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;
 }
 
-// Per-launch choice: AG aggregates per CTA (consumer warps = 4 AG), SPS baby steps per stage.
 template <int JT, int QB>
-hd_status launch_f(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int jmin,
-                   int nj, uint32_t A, int qrows, size_t sq, int ag, int sps) {
-#define HD_MAC_L(AG_, SPS_, IN_)                                                                               \
-  return n1 > 128 ? launch<AG_, JT, QB, SPS_, true, IN_>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)            \
-                  : launch<AG_, JT, QB, SPS_, false, IN_>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq)
-  const char *in_env = getenv("HD_MAC_INLINE");
-  const bool inl = !(in_env && in_env[0] == '0');
-  if (ag == 4 && inl) { HD_MAC_L(4, 2, true); }
-  if (ag == 4) { HD_MAC_L(4, 2, false); }
-  if (ag == 2 && sps == 2) { HD_MAC_L(2, 2, false); }
-  if (ag == 2) { HD_MAC_L(2, 4, false); }
-  if (sps == 2) { HD_MAC_L(1, 2, false); }
-  HD_MAC_L(1, 4, false);
+hd_status launch_f(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int nj,
+                   uint32_t A, bool flat, int qrows, size_t sq, int ag, int sps) {
+#define HD_MAC_L(AG_, SPS_)                                                                        \
+  return n1 > 128 ? launch<AG_, JT, QB, SPS_, true>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq) \
+                  : launch<AG_, JT, QB, SPS_, false>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq)
+  if (ag == 4 && sps == 2) { HD_MAC_L(4, 2); }
+  if (ag == 4) { HD_MAC_L(4, 4); }
+  if (ag == 2 && sps == 2) { HD_MAC_L(2, 2); }
+  if (ag == 2 && sps == 8) { HD_MAC_L(2, 8); }
+  if (ag == 2) { HD_MAC_L(2, 4); }
+  if (sps == 2) { HD_MAC_L(1, 2); }
+  if (sps == 8) { HD_MAC_L(1, 8); }
+  HD_MAC_L(1, 4);
 #undef HD_MAC_L
 }
 }  // namespace
@@ -372,37 +333,53 @@ bool mac_tma_supported(const hd_context *c, int n1, int N, bool flat, uint32_t Q
   return encode_fn() != nullptr;
 }
 
-// S [Q][A][nj][2][L][n]; r [Q][n1][2][L][n] (query stride n1 2 L n).
+// S [Q][A][nj][2][L][n]; r [Q][n1][2][L][n] (query stride n1 2 L n); D [A][N][L][n].
 hd_status mac_tma_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A, int n1, int N,
-                      const std::vector<int32_t> &js, uint32_t Q) {
+                      const std::vector<int32_t> &js, uint32_t Q, bool flat) {
   if (js.empty() || A == 0) return HD_OK;
-  const int jmin = js.front(), nj = (int)js.size();
-  // aggregates per CTA (HD_MAC_AG, A/B knob): 4 -> 16 consumer warps per SM with the producer
-  // inline (128 registers each); 2 / 1 with a separate producer warp
-  const char *ag_env = getenv("HD_MAC_AG");
-  int ag = ag_env ? atoi(ag_env) : 4;
-  if (ag != 1 && ag != 2 && ag != 4) ag = 4;
+  const int nj = (int)js.size(), G = N / n1;
+  if (nj != G) return hd_fail(HD_E_STATE, "TMA MAC expects one giant step per diagonal block");
+  // aggregates per CTA (HD_MAC_AG, A/B knob), baby steps per stage (HD_MAC_SPS)
+  const char *ag_env = getenv("HD_MAC_AG"), *sps_env = getenv("HD_MAC_SPS");
+  int ag = ag_env ? atoi(ag_env) : 2;
+  if (ag != 1 && ag != 2 && ag != 4) ag = 2;
   while (ag > 1 && A % ag) ag /= 2;
-  const char *sps_env = getenv("HD_MAC_SPS");
-  const int sps = (sps_env && atoi(sps_env) == 2) || n1 % 4 || ag == 4 ? 2 : 4;  // baby steps per stage
+  // measured at 2^20 x 512 (n1 = 128): AG 2 / SPS 8 (8 KB diagonal rows per block, 2 stages of
+  // 80 KB) 8.97 ms; SPS 4 9.35; SPS 2 10.4; AG 1 / SPS 8 10.7; AG 4 / SPS 2 10.3
+  int sps = sps_env ? atoi(sps_env) : 8;
+  if (sps != 2 && sps != 4 && sps != 8) sps = 8;
+  while (sps > 2 && n1 % sps) sps /= 2;
+  // giant steps (diagonal blocks) per thread: up to 4 (each r word then serves JT diagonal words)
+  const int jt = nj % 4 == 0 ? 4 : (nj % 2 == 0 ? 2 : 1);
+  const int jtq = Q == 1 ? jt : (Q == 2 ? std::min(jt, 2) : 1);  // QB x JT <= 4 accumulator pairs
+  const int L = c->L, n = c->n;
   CUtensorMap mD, mR;
   hd_status s;
-  if ((s = make_map(&mD, D, c->n, c->L, (uint64_t)A * N, sps))) return s;
-  if ((s = make_map(&mR, r, c->n, c->L, (uint64_t)Q * 2 * n1, 2 * sps))) return s;
-  const size_t sq = (size_t)A * nj * 2 * c->L * c->n;
+  {  // D: (coefficient, limb, diagonal within block, block, aggregate)
+    const cuuint64_t dims[5] = {(cuuint64_t)n, (cuuint64_t)L, (cuuint64_t)n1, (cuuint64_t)G, (cuuint64_t)A};
+    const cuuint64_t strides[4] = {(cuuint64_t)n * 8, (cuuint64_t)L * n * 8, (cuuint64_t)n1 * L * n * 8,
+                                   (cuuint64_t)N * L * n * 8};
+    const cuuint32_t box[5] = {(cuuint32_t)TC, 1, (cuuint32_t)sps, (cuuint32_t)jtq, (cuuint32_t)ag};
+    if ((s = encode(&mD, D, 5, dims, strides, box))) return s;
+  }
+  {  // r: (coefficient, limb, row = (query, baby step, poly))
+    const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)L, (cuuint64_t)Q * 2 * n1};
+    const cuuint64_t strides[2] = {(cuuint64_t)n * 8, (cuuint64_t)L * n * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)TC, 1, (cuuint32_t)(2 * sps)};
+    if ((s = encode(&mR, r, 3, dims, strides, box))) return s;
+  }
+  const size_t sq = (size_t)A * nj * 2 * L * n;
   const int qrows = 2 * n1;
-  // giant steps per thread: all of them up to 4 (each r word then serves JT diagonal words)
-  const int jt = nj % 4 == 0 ? 4 : (nj % 2 == 0 ? 2 : 1);
   if (Q == 1) {
-    if (jt == 4) return launch_f<4, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
-    if (jt == 2) return launch_f<2, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
-    return launch_f<1, 1>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
+    if (jtq == 4) return launch_f<4, 1>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq, ag, sps);
+    if (jtq == 2) return launch_f<2, 1>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq, ag, sps);
+    return launch_f<1, 1>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq, ag, sps);
   }
-  // query batches (NEXT-4): every diagonal word staged once serves QB queries; QB x JT <= 4
+  // query batches (NEXT-4): every diagonal word staged once serves QB queries
   if (Q == 2) {
-    if (jt >= 2) return launch_f<2, 2>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
-    return launch_f<1, 2>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
+    if (jtq == 2) return launch_f<2, 2>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq, ag, sps);
+    return launch_f<1, 2>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq, ag, sps);
   }
-  if (Q == 3) return launch_f<1, 3>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
-  return launch_f<1, 4>(c, mD, mR, S, n1, N, jmin, nj, A, qrows, sq, ag, sps);
+  if (Q == 3) return launch_f<1, 3>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq, ag, sps);
+  return launch_f<1, 4>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq, ag, sps);
 }

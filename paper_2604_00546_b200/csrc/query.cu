@@ -195,7 +195,7 @@ static hd_status giant_and_fold(hd_database *db, cudaEvent_t *E) {
   // ---- giant rotations and sum (R2), accumulated in Q u {P} with one
   //      ModDown per aggregate (R23) ----
   const int ell = L - 1;
-  const size_t ext = (size_t)2 * (ell + 1) * n;  // u: [A][2][ell+1][n]
+  const size_t ext = (size_t)2 * (ell + c->K) * n;  // u: [A][2][ell+K][n]
   HD_CUDA(cudaMemsetAsync(db->u, 0, (size_t)A * ext * 8, c->stream));
   const size_t sp_stride = (size_t)nj * ct1;  // between aggregates for fixed j
   for (int jj = 0; jj < nj; jj++) {
@@ -520,9 +520,9 @@ extern "C" hd_status hd_test_rotate(hd_context *c, const hd_eval_keys *evk, cons
   uint64_t *dig, *u, *tmp, **kp;
   uint32_t *g;
   uint32_t gh = (uint32_t)host_powmod(5, (uint64_t)step, 2ull * n);
-  HD_CUDA(dev_alloc(c, &dig, (size_t)ell * (ell + 1) * n * 8));
-  HD_CUDA(dev_alloc(c, &u, (size_t)2 * (ell + 1) * n * 8));
-  HD_CUDA(dev_alloc(c, &tmp, (size_t)2 * (ell + 1) * n * 8));
+  HD_CUDA(dev_alloc(c, &dig, ks_dig_elems(c, ell) * 8));
+  HD_CUDA(dev_alloc(c, &u, (size_t)2 * (ell + c->K) * n * 8));
+  HD_CUDA(dev_alloc(c, &tmp, (size_t)2 * (ell + c->K) * n * 8));
   HD_CUDA(dev_alloc(c, &kp, sizeof(uint64_t *)));
   HD_CUDA(dev_alloc(c, &g, 4));
   HD_CUDA(cudaMemcpy(kp, &k, sizeof(uint64_t *), cudaMemcpyHostToDevice));
@@ -600,9 +600,9 @@ extern "C" hd_status hd_database_prerotate(hd_context *c, const hd_eval_keys *ev
   const uint32_t Bmax = (uint32_t)std::min(n1, N);
   uint64_t *dig = nullptr, *tmp = nullptr, *u = nullptr, *out = nullptr, **kp = nullptr;
   uint32_t *gal = nullptr;
-  cudaError_t e = dev_alloc(c, &dig, (size_t)Bmax * L * L * n * 8);
+  cudaError_t e = dev_alloc(c, &dig, (size_t)Bmax * ks_dig_elems(c, L) * 8);
   if (!e) e = dev_alloc(c, &tmp, (size_t)Bmax * 2 * L * n * 8);
-  if (!e) e = dev_alloc(c, &u, (size_t)Bmax * 2 * (L + 1) * n * 8);
+  if (!e) e = dev_alloc(c, &u, (size_t)Bmax * 2 * (L + c->K) * n * 8);
   if (!e) e = dev_alloc(c, &out, (size_t)Bmax * ct * 8);
   if (!e) e = dev_alloc(c, &kp, sizeof(uint64_t *));
   if (!e) e = dev_alloc(c, &gal, sizeof(uint32_t));

@@ -32,6 +32,8 @@ class Config:
     limbs: int = 3      # L (R5)
     index: int = 1      # BASELINE.json configs[] position (+1): data seed offset
     planted: int = 3    # K_m
+    special: int = 1    # K_sp special primes (R11; paper-depth profile 4, R31)
+    digit_limbs: int = 1  # alpha limbs per key-switching digit (R11; paper-depth profile 4)
 
     @property
     def num_slots(self):
@@ -65,6 +67,10 @@ CONFIGS = {
     "C4n256": Config("C4-n256", 16, 512, 1 << 20, 256, index=4),
     "C2n256": Config("C2-n256", 15, 512, 1 << 14, 256, index=2),
 }
+# SURVEY 8(d) "secondary": the paper's depth (depth 11, scale 45) as L = 12 limbs,
+# alpha = 4 limbs per digit, K_sp = 4 special primes (R31), on C3 (P = 1) and the toy workload
+CONFIGS["C3p"] = Config("C3-paper-depth", 15, 512, 1 << 17, 16, limbs=12, index=3, special=4, digit_limbs=4)
+CONFIGS["C1p"] = Config("C1-paper-depth", 12, 64, 256, 8, limbs=12, index=1, special=4, digit_limbs=4)
 for _n1 in (4, 8, 16, 32, 64):
     CONFIGS[f"C5n{_n1}"] = Config(f"C5-n1={_n1}", 15, 512, 1 << 17, _n1, index=5)
 
@@ -82,6 +88,14 @@ def make_dataset(num_vectors: int, dim: int, seed: int, planted: int = 3):
     pos = np.sort(rng.choice(num_vectors, size=planted, replace=False)) if planted else np.zeros(0, np.int64)
     db = dataset_rows(num_vectors, dim, seed, 0, num_vectors, query=query, planted_pos=pos)
     return db, query, pos
+
+
+def planted_positions(num_vectors: int, dim: int, seed: int, planted: int = 3):
+    """The planted-match positions make_dataset(num_vectors, dim, seed) draws (no rows made)."""
+    rng = np.random.default_rng(seed)
+    rng.integers(-99, 100, size=dim)
+    planted = min(planted, num_vectors)
+    return np.sort(rng.choice(num_vectors, size=planted, replace=False)) if planted else np.zeros(0, np.int64)
 
 
 _CHUNK = 4096
