@@ -140,8 +140,10 @@ typedef struct {
  * in stream order.  Both must be callable from the thread that calls libhd.  `user` is
  * passed through.  Every device allocation of libhd goes through it (tables, keys,
  * databases, ciphertexts, workspaces); with a NULL allocator libhd uses the device's
- * stream-ordered pool (cudaMallocAsync / cudaFreeAsync).  Objects made by a context must
- * be destroyed before the context (they free through its allocator). */
+ * stream-ordered pool (cudaMallocAsync / cudaFreeAsync).  Objects made by a context keep it
+ * alive: hd_context_destroy releases the caller's reference and the context's tables go
+ * with its last object, so handles may be destroyed in any order (e.g. by a garbage
+ * collector); the allocator must stay callable until then. */
 typedef struct {
   void *(*alloc)(size_t bytes, void *stream, void *user);
   void (*free)(void *ptr, void *stream, void *user);

@@ -280,6 +280,8 @@ extern "C" hd_status hd_keygen(hd_context *c, const int32_t *steps, size_t count
   hd_secret_key *sk = new hd_secret_key{c, nullptr};
   hd_eval_keys *evk = new hd_eval_keys();
   evk->ctx = c;
+  ctx_retain(c);
+  ctx_retain(c);
   evk->steps.assign(steps, steps + count);
   evk->key_elems = ks_key_elems(c);
   auto fail = [&](hd_status s) {
@@ -533,8 +535,9 @@ extern "C" hd_status hd_public_keygen(hd_context *c, const hd_secret_key *sk, hd
   HD_CUDA(cudaSetDevice(c->device));
   const int n = c->n, L = c->L;
   hd_public_key *pk = new hd_public_key{c, nullptr};
+  ctx_retain(c);
   if (dev_alloc(c, &pk->pk, (size_t)2 * L * n * 8) != cudaSuccess) {
-    delete pk;
+    hd_public_key_destroy(pk);
     return hd_fail(HD_E_CAPACITY, "public key alloc");
   }
   const uint64_t seed = c->params.seed;
@@ -554,8 +557,10 @@ extern "C" hd_status hd_public_keygen(hd_context *c, const hd_secret_key *sk, hd
 
 extern "C" void hd_public_key_destroy(hd_public_key *pk) {
   if (!pk) return;
-  dev_free(pk->ctx, pk->pk);
+  hd_context *c = pk->ctx;
+  dev_free(c, pk->pk);
   delete pk;
+  ctx_release(c);
 }
 
 extern "C" hd_status hd_public_key_export(const hd_public_key *pk, uint64_t *dst, size_t cap) {
@@ -574,8 +579,9 @@ extern "C" hd_status hd_public_key_import(hd_context *c, const uint64_t *src, si
   for (size_t i = 0; i < need; i++)
     if (src[i] >= c->mod[(i / c->n) % c->L]) return hd_fail(HD_E_FORMAT, "public key residue out of range");
   hd_public_key *pk = new hd_public_key{c, nullptr};
+  ctx_retain(c);
   if (dev_alloc(c, &pk->pk, need * 8) != cudaSuccess) {
-    delete pk;
+    hd_public_key_destroy(pk);
     return hd_fail(HD_E_CAPACITY, "public key alloc");
   }
   if (cudaMemcpy(pk->pk, src, need * 8, cudaMemcpyHostToDevice) != cudaSuccess) {

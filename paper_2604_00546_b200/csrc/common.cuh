@@ -207,7 +207,13 @@ constexpr static int kPhaseEvents = 9;
     cudaStream_t stream;
   };
   std::vector<WsBlock> ws_free;
+  // lifetime: 1 for the caller's handle + 1 per live object made by this context (keys,
+  // ciphertexts, databases); hd_context_destroy drops the caller's reference and the tables
+  // go when the last object goes, so objects may be destroyed in any order (e.g. by a GC)
+  int refs = 1;
 };
+void ctx_retain(hd_context *c);
+void ctx_release(hd_context *c);
 
 // Key-switching geometry (R11, R31).  Extended basis of a ciphertext at ell limbs: ext index
 // e < ell is q_e, e >= ell the special prime p_{e-ell} (modulus index L + e - ell); a key

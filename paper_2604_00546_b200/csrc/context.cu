@@ -284,8 +284,26 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
   return HD_OK;
 }
 
+static std::mutex g_ctx_mu;
+void ctx_retain(hd_context *c) {
+  std::lock_guard<std::mutex> g(g_ctx_mu);
+  ++c->refs;
+}
+static void context_teardown(hd_context *c);
+void ctx_release(hd_context *c) {
+  bool last;
+  {
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    last = --c->refs == 0;
+  }
+  if (last) context_teardown(c);
+}
+
 extern "C" void hd_context_destroy(hd_context *c) {
-  if (!c) return;
+  if (c) ctx_release(c);
+}
+
+static void context_teardown(hd_context *c) {
   cudaSetDevice(c->device);
   quiesce(c);
   for (void *p : {(void *)c->tw2, (void *)c->itw2, (void *)c->ninv_dev, (void *)c->xi_re, (void *)c->xi_im,
@@ -362,12 +380,14 @@ cudaMemcpyKind kind_of(int dst_dev, int src_dev) {
 
 hd_status alloc_ct(hd_context *c, uint32_t limbs, hd_ciphertext **out) {
   hd_ciphertext *ct = new hd_ciphertext{c, limbs, nullptr};
+  ctx_retain(c);
   ct->scale = std::ldexp(1.0, (int)c->params.scale_bits);
   cudaError_t e = dev_alloc(c, &ct->data, sizeof(uint64_t) * 2 * limbs * c->n);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ct->ready, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     dev_free(c, ct->data);
     delete ct;
+    ctx_release(c);
     return hd_fail(e == cudaErrorMemoryAllocation ? HD_E_CAPACITY : HD_E_CUDA, "ciphertext alloc");
   }
   *out = ct;
@@ -575,8 +595,10 @@ extern "C" void hd_ciphertext_destroy(hd_ciphertext *ct) {
     cudaEventSynchronize(ct->used);
     cudaEventDestroy(ct->used);
   }
-  dev_free(ct->ctx, ct->data);
+  hd_context *c = ct->ctx;
+  dev_free(c, ct->data);
   delete ct;
+  ctx_release(c);
 }
 
 extern "C" hd_status hd_eval_keys_export(const hd_eval_keys *k, void *dst, size_t cap, int dst_on_device,
@@ -621,6 +643,7 @@ extern "C" hd_status hd_eval_keys_import(hd_context *c, const void *src, size_t 
     return hd_fail(HD_E_FORMAT, "eval-key payload size does not match its header");
   hd_eval_keys *k = new hd_eval_keys();
   k->ctx = c;
+  ctx_retain(c);
   k->steps.resize(nk);
   k->key_elems = key_elems;
   const char *p = (const char *)src + sizeof(Header);
@@ -654,8 +677,10 @@ extern "C" hd_status hd_eval_keys_import(hd_context *c, const void *src, size_t 
 
 extern "C" void hd_eval_keys_destroy(hd_eval_keys *k) {
   if (!k) return;
-  dev_free(k->ctx, k->keys);
+  hd_context *c = k->ctx;
+  dev_free(c, k->keys);
   delete k;
+  ctx_release(c);
 }
 
 extern "C" hd_status hd_secret_key_export(const hd_secret_key *sk, uint64_t *dst, size_t cap) {
@@ -669,8 +694,10 @@ extern "C" hd_status hd_secret_key_export(const hd_secret_key *sk, uint64_t *dst
 
 extern "C" void hd_secret_key_destroy(hd_secret_key *sk) {
   if (!sk) return;
-  dev_free(sk->ctx, sk->s_ntt);
+  hd_context *c = sk->ctx;
+  dev_free(c, sk->s_ntt);
   delete sk;
+  ctx_release(c);
 }
 
 extern "C" hd_status hd_test_ntt(hd_context *c, uint64_t *data, uint32_t n_rows, const uint32_t *modulus_idx,

@@ -265,6 +265,7 @@ extern "C" void hd_database_destroy(hd_database *db) {
   for (cudaEvent_t e : {db->ev_in, db->ev_mac, db->ev_done, db->ev_sfree[0], db->ev_sfree[1], db->ev_bs})
     if (e) cudaEventDestroy(e);
   delete db;
+  ctx_release(c);
 }
 
 // Device objects of a database handle: diagonals D (uninitialised), query workspaces, events.
@@ -275,6 +276,7 @@ static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing,
   HD_CUDA(cudaSetDevice(c->device));
   hd_database *db = new hd_database();
   db->ctx = c;
+  ctx_retain(c);
   db->lay = lay;
   db->N = lay.vector_dim;
   db->M = lay.blocks_m;
@@ -298,7 +300,7 @@ static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing,
   }
   for (size_t i = 1; i < db->js.size(); i++)
     if (db->js[i] != db->js[i - 1] + 1) {
-      delete db;
+      hd_database_destroy(db);
       return hd_fail(HD_E_LAYOUT, "non-contiguous giant steps");
     }
   const size_t A = db->A_loc, nj = db->js.size(), ctL = (size_t)2 * L * n, ct1 = (size_t)2 * (L - 1) * n;
@@ -340,7 +342,7 @@ static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing,
   for (auto &q : reqs) total += q.bytes;
   if (footprint) {
     *footprint = total;
-    delete db;
+    hd_database_destroy(db);
     return HD_OK;
   }
   if (!c->has_alloc) {
@@ -352,7 +354,7 @@ static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing,
     if (cudaDeviceGetDefaultMemPool(&pool, c->device) == cudaSuccess) cudaMemPoolTrimTo(pool, 0);
     HD_CUDA(cudaMemGetInfo(&fr, &tot));
     if (total + (256ull << 20) > fr) {
-      delete db;
+      hd_database_destroy(db);
       return hd_fail(HD_E_CAPACITY, "database of " + std::to_string(total >> 20) + " MiB exceeds free device memory (" +
                                         std::to_string(fr >> 20) + " MiB); shard the aggregates over more GPUs");
     }

@@ -234,10 +234,11 @@ static hd_status ensure_streams(hd_context *c) {
   // of the remaining CTAs of the HBM-bound MAC grid running on A.
   int lo = 0, hi = 0;
   HD_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  // HD_PRIO (A/B knob): unset / "B" -> stream B high; "A" -> stream A high; "0" -> equal
   const char *pr = getenv("HD_PRIO");
-  const bool prio = !(pr && pr[0] == '0');
-  if (!c->sA) HD_CUDA(cudaStreamCreateWithPriority(&c->sA, cudaStreamNonBlocking, lo));
-  if (!c->sB) HD_CUDA(cudaStreamCreateWithPriority(&c->sB, cudaStreamNonBlocking, prio ? hi : lo));
+  const bool a_hi = pr && pr[0] == 'A', b_hi = !(pr && (pr[0] == '0' || pr[0] == 'A'));
+  if (!c->sA) HD_CUDA(cudaStreamCreateWithPriority(&c->sA, cudaStreamNonBlocking, a_hi ? hi : lo));
+  if (!c->sB) HD_CUDA(cudaStreamCreateWithPriority(&c->sB, cudaStreamNonBlocking, b_hi ? hi : lo));
   return HD_OK;
 }
 

@@ -154,3 +154,70 @@ def test_sharded_membership_partial_sums(world, oracle_mod):
     _, parts = q.get()
     st, keys = o.keyset(s_ntt, [1 << k for k in range(o.log_n - 1)])
     assert (o.membership(np.stack(parts), st, keys) == o.membership(cts, st, keys)).all()
+
+
+def _exchange_worker(rank, world, port, qbytes, cts, results):
+    """bench.py's per-step exchange (StepExchange) on gloo with oracle ciphertext payloads: the
+    C-ABI export is replaced by a byte copy into the send slab at the pointer StepExchange hands
+    out; every step reuses the same buffers (no allocation) and sizes never travel."""
+    import ctypes
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A = cts.shape[0]
+        a0, a1 = hdd.shard_range(A, rank, world)
+        ob = cts[0].nbytes
+        xch = hdd.StepExchange(qbytes.nbytes, hdd.shard_sizes(A, world), ob, "cpu")
+        ptrs = (xch.qbuf.data_ptr(), xch.send.data_ptr(),
+                [b.data_ptr() for b in xch.recv] if xch.recv is not None else None)
+
+        def export_into(a, ptr, cap):  # stands in for hd_ciphertext_export_level(.., device dst)
+            src = np.ascontiguousarray(cts[a]).view(np.uint8)
+            assert cap == src.nbytes
+            ctypes.memmove(ptr, src.ctypes.data, cap)
+
+        ok = True
+        for step in range(3):
+            if rank == 0:
+                xch.qbuf.copy_(torch.from_numpy(np.roll(qbytes, step)))
+            got_q = xch.broadcast_query().numpy()
+            ok = ok and bool((got_q == np.roll(qbytes, step)).all())
+            views = xch.gather(list(range(a0, a1)), export_into)
+            same = (xch.qbuf.data_ptr(), xch.send.data_ptr(),
+                    [b.data_ptr() for b in xch.recv] if xch.recv is not None else None) == ptrs
+            ok = ok and same
+            if rank == 0:
+                flat = [v for per in views for v in per]
+                assert len(flat) == A
+                for a, (p_, n_) in enumerate(flat):
+                    buf = (ctypes.c_uint8 * n_).from_address(p_)
+                    ok = ok and bool((np.frombuffer(buf, np.uint8) == cts[a].view(np.uint8).ravel()).all())
+        results.put(("exchange", rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_step_exchange_fixed_buffers(world, oracle_mod):
+    """The N > 1 timed step's collectives (a1 query broadcast, a9 gather of 1-limb result
+    exports) on persistent buffers sized from the static shard map, with ragged shards
+    (A = 7 over 2 or 3 ranks): every gathered ciphertext arrives bit for bit in aggregate order."""
+    o = oracle_mod.Oracle(6, 3)
+    s, s_ntt = o.secret_key()
+    rng = np.random.default_rng(world)
+    cts = np.stack([np.ascontiguousarray(o.encrypt(s_ntt, o.encode(rng.uniform(-1, 1, o.ns), 2.0 ** 45, 3),
+                                                   300 + a)[:, :1]) for a in range(7)])  # 1-limb exports
+    qct = o.encrypt(s_ntt, o.encode(np.linspace(-1, 1, o.ns), 2.0 ** 45, 3), 1000)
+    qbytes = qct.view(np.uint8).ravel().copy()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_exchange_worker, args=(r, world, port, qbytes, cts, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    res = [q.get() for _ in range(world)]
+    assert all(ok for _, _, ok in res), res

@@ -24,7 +24,9 @@ def main():
     ik, im, iv = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value")
     kern, vals = None, {}
     for r in rows[1:]:
-        kern = r[ik].split("<")[0].split("(")[0].split("::")[-1].strip()
+        import re
+        mm = re.search(r"(mac_\w+?)(<|\(|$)", r[ik])
+        kern = mm.group(1) if mm else r[ik]
         v = float(r[iv].replace(",", ""))
         unit = r[hdr.index("Metric Unit")] if "Metric Unit" in hdr else ""
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}.get(unit, 1)
