@@ -113,10 +113,8 @@ __device__ __forceinline__ Unit decode(uint32_t u, uint32_t nag, int ngrp, int t
 // AG aggregates x TC coefficients consumer threads + one producer warp.
 // Stage layout (u64): D[AG][JT][SPS][TC] (the 5-D box), then r[QB][SPS][2][TC].
 // flags (measurement only): 1 = stream without arithmetic, 2 = arithmetic without the stream.
-// MAXREG caps the registers (__maxnreg__) so that a key-switching CTA of the other pipeline
-// stream (256 threads x 80 registers) can stay resident beside the MAC CTA (stream overlap).
-template <int AG, int JT, int QB, int SPS, bool FLUSH, int MAXREG>
-__global__ void __maxnreg__(MAXREG)
+template <int AG, int JT, int QB, int SPS, bool FLUSH>
+__global__ void __launch_bounds__(AG *TC + 32, 1)
     mac_tma_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmR,
                    uint64_t *__restrict__ S, int n1, int N, int L, int logn, int nj, uint32_t A, int flat, int stages,
                    int qrows, size_t s_query_stride, ModTab mt, int flags) {
@@ -284,7 +282,7 @@ hd_status encode(CUtensorMap *map, const uint64_t *base, int rank, const cuuint6
 
 int g_num_sms = 0;
 
-template <int AG, int JT, int QB, int SPS, bool FLUSH, int MAXREG = 65536 / (AG * TC + 32) / 8 * 8>
+template <int AG, int JT, int QB, int SPS, bool FLUSH>
 hd_status launch(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int nj,
                  uint32_t A, bool flat, int qrows, size_t sq) {
   constexpr size_t STAGE_BYTES = (size_t)(AG * JT * SPS * TC + QB * SPS * 2 * TC) * 8;
@@ -293,7 +291,7 @@ hd_status launch(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, ui
   if (const char *e = getenv("HD_MAC_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));  // A/B knob
   if (stages < 2) return hd_fail(HD_E_PARAMS, "MAC stage does not fit shared memory");
   const size_t smem = stages * STAGE_BYTES + 2 * stages * sizeof(uint64_t);
-  auto kern = mac_tma_kernel<AG, JT, QB, SPS, FLUSH, (MAXREG > 255 ? 255 : MAXREG)>;
+  auto kern = mac_tma_kernel<AG, JT, QB, SPS, FLUSH>;
   HD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   if (!g_num_sms) HD_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, c->device));
   const uint32_t units = (A / AG) * (uint32_t)(nj / JT) * (uint32_t)(c->n / TC) * (uint32_t)c->L;
@@ -316,11 +314,6 @@ hd_status launch_f(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, 
   if (ag == 4 && sps == 2) { HD_MAC_L(4, 2); }
   if (ag == 4) { HD_MAC_L(4, 4); }
   if (ag == 2 && sps == 2) { HD_MAC_L(2, 2); }
-  const char *rc = getenv("HD_MAC_REGCAP");  // 128 registers: room for a key-switching CTA per SM
-  if (ag == 2 && sps == 8 && rc && rc[0] == '1') {
-    return n1 > 128 ? launch<2, JT, QB, 8, true, 128>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq)
-                    : launch<2, JT, QB, 8, false, 128>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq);
-  }
   if (ag == 2 && sps == 8) { HD_MAC_L(2, 8); }
   if (ag == 2) { HD_MAC_L(2, 4); }
   if (sps == 2) { HD_MAC_L(1, 2); }
