@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 from synth_inputs import CONFIGS, ENC_SEED_BASE, dataset_rows, make_dataset, planted_positions  # noqa: E402
 
 METRIC = "encrypted queries/sec (2^20 x 512 database scan)"
+SCALE_BITS, Q0_BITS = 45, 60  # the Context's scale (Delta_q = 2^45) and q0 bits (R5)
 UNIT = "queries/s"
 
 
@@ -177,8 +178,8 @@ def workload_cfg(args):
     """BASELINE config, with 6 RNS limbs when the comparison follows the scan (R29)."""
     import dataclasses
     cfg = CONFIGS[args.config]
-    # comparison scenarios: degree 13 needs 4 levels after the scan; membership keeps 2 limbs of
-    # headroom for its sum over all slots (R29) -> 6 limbs for identification, 7 for membership
+    # comparison scenarios: degree 13 needs 4 levels after the scan -> 6 limbs (the membership
+    # count is scaled by 2^-count_shift to fit q_0; --limbs 7 keeps 2-limb results instead, R29)
     limbs = args.limbs or {"scan": cfg.limbs, "identification": 6, "membership": 6}[args.scenario]
     if limbs != cfg.limbs:
         cfg = dataclasses.replace(cfg, limbs=limbs)
@@ -306,7 +307,7 @@ def main():
         raise SystemExit("--scenario membership needs a flat packing (every slot a vector; DESIGN.md R29)")
     stream = torch.cuda.current_stream()
     ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1, device=local, stream=stream, num_special=cfg.special,
-                     digit_limbs=cfg.digit_limbs)
+                     digit_limbs=cfg.digit_limbs, scale_bits=SCALE_BITS, q0_bits=Q0_BITS)
     flat = args.packing in ("flat", "flat_tbs")
     if args.packing == "flat_tbs" and args.db != "encrypted":
         raise SystemExit("--packing flat_tbs needs --db encrypted (BSGS-RTX-TBS pre-rotates encrypted diagonals)")
@@ -322,17 +323,24 @@ def main():
     enc_db = args.db == "encrypted"
     if args.scenario == "membership":  # + the power-of-two keys of RotateAndSum
         steps = np.array(sorted(set(int(s) for s in steps) | set(int(s) for s in ctx.membership_steps())), np.int32)
-    coeffs = hd.chebyshev_coefficients(args.delta, hd.chebyshev_degree(args.kappa)) if tail else None
-    # membership headroom (R29): the sum over all slots of values near 1 at scale 2^45 must stay
-    # below q_0 / 2 ~ 2^59 at one limb -> the client scales the series by 2^-COUNT_SHIFT (the
-    # count decodes / 2^COUNT_SHIFT); with 7 limbs, --membership-limbs 2 keeps the exact count
+    # online aggregation (R30): each rank's aggregated score sums G = its aggregate
+    # count of per-slot scores; the client encrypts q / f_G, f_G = 1 + (G - 1) 2 / sqrt(l), and
+    # the comparison threshold becomes delta / f_G, so the compared value stays in [-1, 1]
+    agg_terms = -(-A // world) if args.online_aggregate else 1
+    f_G = 1.0 + (agg_terms - 1) * 2.0 / np.sqrt(cfg.dim) if args.online_aggregate else 1.0
+    coeffs = hd.chebyshev_coefficients(args.delta / f_G, hd.chebyshev_degree(args.kappa)) if tail else None
+    # membership headroom (R29): the sum over all slots of values near 1 at scale 2^SCALE_BITS must
+    # stay below q_0 / 2 at one limb -> the client scales the series by 2^-count_shift (the count
+    # decodes / 2^count_shift); with --limbs 7 the comparison keeps 2 limbs and the exact count
     out_limbs, count_shift = 1, 0
     if args.scenario == "membership":
-        slots_total = A * cfg.num_slots
+        # slots summed by RotateAndSum: every slot of the compared ciphertexts (online
+        # aggregation: one aggregated ciphertext per rank)
+        slots_total = (world if args.online_aggregate else A) * cfg.num_slots
         if cfg.limbs >= 7:
             out_limbs = 2
         else:
-            count_shift = max(0, int(np.ceil(np.log2(1.25 * slots_total))) + 45 - 58)
+            count_shift = max(0, int(np.ceil(np.log2(1.25 * slots_total))) + SCALE_BITS - (Q0_BITS - 2))
             coeffs = coeffs * 2.0 ** -count_shift
     if rank == 0:
         sk, evk = ctx.keygen(steps)
@@ -383,7 +391,7 @@ def main():
     if rank == 0:
         qrng = np.random.default_rng(99)
         qvecs = [q] + [qrng.integers(-99, 100, cfg.dim).astype(np.float32) for _ in range(Q - 1)]
-        qcts = [ctx.encrypt_query(sk, v, ENC_SEED_BASE + i) for i, v in enumerate(qvecs)]
+        qcts = [ctx.encrypt_query(sk, v, ENC_SEED_BASE + i, msg_scale=1.0 / f_G) for i, v in enumerate(qvecs)]
         ct_bytes = ctx.ciphertext_export_size(qcts[0])
     nb = torch.tensor([ct_bytes], device=dev)
     if world > 1:
@@ -665,7 +673,8 @@ def main():
             "keyswitch": keyswitch, "query_roofline": query_roofline, "tail_ms": tail_ms,
             "latency_ms_serial": latency_ms, "scenario": args.scenario, "queries_per_step": Q,
             "membership_count_shift": count_shift if args.scenario == "membership" else None, "split_baby": split is not None,
-            "online_aggregate": None if aggr_s is None else {"setup_s": aggr_s, "note": "Alg. online-aggr: the "
+            "online_aggregate": None if aggr_s is None else {"setup_s": aggr_s, "f_G": f_G, "G": agg_terms,
+                                                             "note": "Alg. online-aggr: the "
                                 "scan runs over one aggregate holding the sum of all diagonals"},
             "clocks": clocks, "e2e": e2e, "check": check}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -181,6 +181,12 @@ hd_status hd_keygen(hd_context *ctx, const int32_t *steps, size_t count, hd_secr
  * Philox stream keyed by enc_seed (R14).  q: host float32[vector_dim]. */
 hd_status hd_encrypt_query(hd_context *ctx, const hd_secret_key *sk, const float *q,
                            uint32_t vector_dim, uint64_t enc_seed, hd_ciphertext **out);
+/* As hd_encrypt_query with the normalised query multiplied by msg_scale in (0, 1] before
+ * encoding: the online-aggregated membership encrypts q / f_G, f_G = 1 + (G-1) 2/sqrt(l),
+ * so the aggregated score stays in the comparison's [-1, 1] (R30).
+ * msg_scale = 1 is hd_encrypt_query bit for bit. */
+hd_status hd_encrypt_query_ex(hd_context *ctx, const hd_secret_key *sk, const float *q,
+                              uint32_t vector_dim, uint64_t enc_seed, double msg_scale, hd_ciphertext **out);
 /* Decrypt + decode the n_ct output ciphertexts of aggregates
  * [layout->agg_begin, layout->agg_begin + n_ct) and write the score of every
  * database vector they hold, in vector order (R4): scores[v - v_first] for

@@ -39,7 +39,7 @@ ABI_FUNCTIONS = [
     "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
     "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch", "hd_eval_add_many", "hd_baby_steps",
     "hd_query_baby", "hd_database_aggregate", "hd_compare_ex", "hd_enroll_footprint",
-    "hd_ciphertext_export_level",
+    "hd_ciphertext_export_level", "hd_encrypt_query_ex",
 ]
 
 
@@ -105,6 +105,7 @@ def load():
             L.hd_rotation_steps.argtypes = [VP, C.c_uint32, C.c_uint32, VP, C.c_size_t, C.POINTER(C.c_size_t)]
             L.hd_keygen.argtypes = [VP, VP, C.c_size_t, C.POINTER(VP), C.POINTER(VP)]
             L.hd_encrypt_query.argtypes = [VP, VP, VP, C.c_uint32, C.c_uint64, C.POINTER(VP)]
+            L.hd_encrypt_query_ex.argtypes = [VP, VP, VP, C.c_uint32, C.c_uint64, C.c_double, C.POINTER(VP)]
             L.hd_decrypt_scores.argtypes = [VP, VP, C.POINTER(Layout), VP, C.c_size_t, VP, C.c_size_t,
                                             C.POINTER(C.c_size_t)]
             L.hd_decrypt.argtypes = [VP, VP, VP, VP, C.c_size_t]
@@ -328,11 +329,16 @@ class Context(_Handle):
         _check("hd_keygen", load().hd_keygen(self.h, _ptr(steps), len(steps), C.byref(sk), C.byref(evk)))
         return SecretKey(sk.value, self), EvalKeys(evk.value, self)
 
-    def encrypt_query(self, sk, q, enc_seed):
+    def encrypt_query(self, sk, q, enc_seed, msg_scale=1.0):
+        """hd_encrypt_query (msg_scale 1) / hd_encrypt_query_ex (the normalised query times msg_scale)."""
         q = np.ascontiguousarray(q, dtype=np.float32)
         out = VP()
-        _check("hd_encrypt_query", load().hd_encrypt_query(self.h, sk.h, _ptr(q), len(q), C.c_uint64(enc_seed),
-                                                           C.byref(out)))
+        if msg_scale == 1.0:
+            _check("hd_encrypt_query", load().hd_encrypt_query(self.h, sk.h, _ptr(q), len(q), C.c_uint64(enc_seed),
+                                                               C.byref(out)))
+        else:
+            _check("hd_encrypt_query_ex", load().hd_encrypt_query_ex(
+                self.h, sk.h, _ptr(q), len(q), C.c_uint64(enc_seed), C.c_double(msg_scale), C.byref(out)))
         return Ciphertext(out.value, self)
 
     def decrypt_scores(self, sk, layout, cts):

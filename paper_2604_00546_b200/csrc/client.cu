@@ -92,10 +92,10 @@ __global__ void enc_combine_kernel(uint64_t seed, int n, int nl, const uint64_t 
 
 // query slots: z_s = u_{s mod N} (R8)
 __global__ void query_slots_kernel(const double *__restrict__ u, int N, int ns, double *__restrict__ re,
-                                   double *__restrict__ im) {
+                                   double *__restrict__ im, double msg_scale) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= ns) return;
-  re[s] = u[s % N];
+  re[s] = msg_scale == 1.0 ? u[s % N] : __dmul_rn(u[s % N], msg_scale);
   im[s] = 0.0;
 }
 
@@ -327,7 +327,13 @@ extern "C" hd_status hd_keygen(hd_context *c, const int32_t *steps, size_t count
 
 extern "C" hd_status hd_encrypt_query(hd_context *c, const hd_secret_key *sk, const float *q, uint32_t vector_dim,
                                       uint64_t enc_seed, hd_ciphertext **out) {
+  return hd_encrypt_query_ex(c, sk, q, vector_dim, enc_seed, 1.0, out);
+}
+
+extern "C" hd_status hd_encrypt_query_ex(hd_context *c, const hd_secret_key *sk, const float *q, uint32_t vector_dim,
+                                         uint64_t enc_seed, double msg_scale, hd_ciphertext **out) {
   if (!c || !sk || !q || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  if (!(msg_scale > 0.0) || msg_scale > 1.0) return hd_fail(HD_E_INVALID_ARG, "msg_scale must be in (0, 1]");
   *out = nullptr;
   if (vector_dim < 2 || (vector_dim & (vector_dim - 1)) || (uint32_t)c->ns % (2 * vector_dim))
     return hd_fail(HD_E_LAYOUT, "vector_dim must be a power of two with numSlots % (2 vector_dim) == 0");
@@ -347,7 +353,7 @@ extern "C" hd_status hd_encrypt_query(hd_context *c, const hd_secret_key *sk, co
   if (!s) s = normalize_on_device(c, dq, 1, N, U);
   if (!s) s = check_flag(c);
   if (!s) {
-    query_slots_kernel<<<(ns + TPB - 1) / TPB, TPB, 0, c->stream>>>(U, N, ns, re, im); ++c->launches;
+    query_slots_kernel<<<(ns + TPB - 1) / TPB, TPB, 0, c->stream>>>(U, N, ns, re, im, msg_scale); ++c->launches;
     s = encode_batch(c, re, im, 1, std::ldexp(1.0, (int)c->params.scale_bits), L, ct->data, (size_t)2 * L * n);
   }
   if (!s) {

@@ -22,6 +22,8 @@
 // combine (A - v) w (+ pi_g(c0)), written or accumulated into a third row map.
 #include "common.cuh"
 
+#include <cstdlib>
+
 namespace {
 
 constexpr int E = 16;  // elements per thread
@@ -445,8 +447,14 @@ hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &ma
     }
     c->ntt_attr_set = true;
   }
-  for (uint32_t r0 = 0; r0 < rows; r0 += 65535) {
-    const uint32_t rr = rows - r0 < 65535 ? rows - r0 : 65535;
+  // HD_NTT_CHUNK (A/B knob): rows per launch pair, so the intermediate of the two kernels stays
+  // L2-resident.  Measured slower at 2^20 x 512 (96 rows: 61.4 vs 62.4 q/s; 24 rows: 55.4):
+  // the kernels are issue-bound and the extra fill / drain costs more; default one batch.
+  uint32_t chunk = 65535;
+  if (const char *ce = getenv("HD_NTT_CHUNK"))
+    if (atol(ce) > 0) chunk = (uint32_t)std::min(65535L, atol(ce));
+  for (uint32_t r0 = 0; r0 < rows; r0 += chunk) {
+    const uint32_t rr = rows - r0 < chunk ? rows - r0 : chunk;
     const dim3 ga(s1 ? (1u << s2) / tpc_a : 1, rr), gb((1u << s1) / tpc_b, rr);
     if (!inverse) {
       if (s1) {

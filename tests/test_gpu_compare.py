@@ -255,3 +255,38 @@ def test_membership_at_bench_configuration_scaled_count():
     cos = _cos(db_vecs, q)
     total = npcheb.chebval(cos, c).sum() + (len(outs) * ctx.ns - cfg.num_vectors) * npcheb.chebval(0.0, c)
     assert np.abs(z - total).max() < 1e-3 * max(1.0, abs(total))
+
+
+def test_online_aggregated_membership_accuracy(run):
+    """Online aggregation (R30, Alg. online-aggr) with the paper's query rescaling
+    (P:L2463-2490): the client encrypts q / f_G, f_G = 1 + (G - 1) 2 / sqrt(l), the server scans
+    the summed diagonals and compares against delta / f_G.  Every slot of the comparison decodes
+    to the Chebyshev series at S[j] / f_G, S[j] = the sum of that slot's cosines over the G
+    aggregates (plaintext, float64), which stays inside [-1, 1] (where the series is valid), and
+    the membership total is the series summed over every slot.  (How well a degree-13 step
+    separates S / f_G around delta / f_G is the paper's false-positive caveat.)"""
+    ctx, cfg = run.ctx, run.cfg
+    G = len(run.outs)
+    f = 1.0 + (G - 1) * 2.0 / np.sqrt(cfg.dim)
+    agg = ctx.database_aggregate(run.db)
+    qct = ctx.encrypt_query(run.sk, run.q, ENC_SEED_BASE + 7, msg_scale=1.0 / f)
+    out = ctx.query(run.evk, agg, qct)
+    assert len(out) == 1
+    delta = 0.5
+    c = hd.chebyshev_coefficients(delta / f, 13)
+    cmp = ctx.compare(run.evk, out, c)
+    mem = ctx.membership(run.evk, cmp)
+    torch.cuda.synchronize()
+    # plaintext aggregated score per slot: slot j of aggregate a holds vector a ns + j (flat)
+    S = np.zeros(ctx.ns)
+    for a in range(G):
+        v0, v1 = a * ctx.ns, min(cfg.num_vectors, (a + 1) * ctx.ns)
+        S[: v1 - v0] += run.cos[v0:v1]
+    assert np.abs(S / f).max() <= 1.0  # the rescaled input stays in the series' interval
+    slots = ctx.decrypt_slots(run.sk, cmp[0])
+    assert np.abs(slots - npcheb.chebval(S / f, c)).max() < 1e-4
+    total = float(ctx.decrypt_slots(run.sk, mem)[0])
+    want = float(npcheb.chebval(S / f, c).sum())
+    assert abs(total - want) < 1e-3 * max(1.0, abs(want)), (total, want)
+    # the planted matches are the slots with the largest aggregated score
+    assert (S >= delta).sum() >= 1 and slots[S >= delta].min() > np.median(slots)
