@@ -84,7 +84,8 @@ def load():
     global _lib
     with _lock:
         if _lib is None:
-            path = _build_lib()
+            # HD_LIBHD: an alternative in-tree build of libhd (kernel A/B runs; tools/ntt_variants.sh)
+            path = os.environ.get("HD_LIBHD") or _build_lib()
             L = C.CDLL(path)
             L.hd_status_string.restype = C.c_char_p
             L.hd_status_string.argtypes = [C.c_int]
