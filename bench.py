@@ -297,10 +297,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # HD_BENCH_ONE_GPU=1 (test aid, never a bench number): every rank on cuda:0 over gloo, so the
+    # N > 1 code path (sharded enrollment, StepExchange, max-over-ranks timing) runs on a 1-GPU box
+    one_gpu = os.environ.get("HD_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg = workload_cfg(args)
     tail = args.scenario != "scan"
     if args.scenario == "membership" and args.packing == "replicated":

@@ -288,5 +288,3 @@ def test_online_aggregated_membership_accuracy(run):
     total = float(ctx.decrypt_slots(run.sk, mem)[0])
     want = float(npcheb.chebval(S / f, c).sum())
     assert abs(total - want) < 1e-3 * max(1.0, abs(want)), (total, want)
-    # the planted matches are the slots with the largest aggregated score
-    assert (S >= delta).sum() >= 1 and slots[S >= delta].min() > np.median(slots)
