@@ -51,6 +51,8 @@ def parse():
                     help="key-switching profile: north-star (L = 3, alpha = 1, one special prime) or the "
                          "paper's depth (SURVEY 8(d) secondary, R31: L = 12, alpha = 4, 4 special primes)")
     ap.add_argument("--no-check", action="store_true", help="skip the per-run correctness check")
+    ap.add_argument("--no-size-curve", dest="size_curve", action="store_false",
+                    help="skip the queries/s-versus-database-size points (2^14, 2^17 vectors)")
     ap.add_argument("--packing", default="replicated", choices=["replicated", "flat", "flat_tbs"],
                     help="stride-2N replicated blocks + fold (the north-star scan) or the flat pre-rotated "
                          "layout (NEXT-2, BSGS-RTX-TBE)")
@@ -685,6 +687,14 @@ def main():
                                                              "note": "Alg. online-aggr: the "
                                 "scan runs over one aggregate holding the sum of all diagonals"},
             "clocks": clocks, "e2e": e2e, "check": check}
+    # queries/s versus database size (BASELINE metric "queries/sec vs DB size"): the same packing
+    # and mode at 2^14 and 2^17 vectors (ring 2^15) measured in this run next to the headline size
+    if (world == 1 and args.size_curve and args.scenario == "scan" and args.db == "plain" and Q == 1
+            and args.profile == "north-star"):
+        curve = [size_point(hd, torch, stream, args, name) for name in ("C2", "C3") if CONFIGS[name].num_vectors < cfg.num_vectors]
+        curve.append({"db_vectors": cfg.num_vectors, "config": cfg.name, "n1": cfg.n1, "queries_per_s": value,
+                      "ms_per_query": ms_per_step})
+        line["size_curve"] = curve
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         import multiprocessing
         pqs, total, reps = [], 0.0, 0
@@ -787,6 +797,31 @@ def db_js(cfg, flat=False):
 
 
 DB_ENC_SEED = 4242  # encrypted-database mode: Philox key of the enroller's encryption
+
+
+def size_point(hd, torch, stream, args, name, n1=64, steps=20, warmup=5):
+    """Device-resident queries/s of one smaller database (own context, keys and enrollment)."""
+    import dataclasses
+    cfg = dataclasses.replace(CONFIGS[name], n1=n1)
+    ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1, stream=stream, scale_bits=SCALE_BITS, q0_bits=Q0_BITS)
+    db_vecs, q, _ = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    _, evk = sk_evk = ctx.keygen(ctx.rotation_steps(cfg.dim, cfg.n1, packing=args.packing))
+    qct = ctx.encrypt_query(sk_evk[0], q, ENC_SEED_BASE)
+    db = ctx.enroll(db_vecs, cfg.n1, packing=args.packing)
+    outs = None
+    for _ in range(warmup):
+        outs = ctx.query(evk, db, qct, outs)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        outs = ctx.query(evk, db, qct, outs)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    del outs, db, evk, sk_evk, qct
+    return {"db_vectors": cfg.num_vectors, "config": cfg.name, "n1": cfg.n1, "queries_per_s": 1e3 / ms,
+            "ms_per_query": ms}
 
 
 def enroll_rows(hd, ctx, rows, v0, cfg, a0, a1, pk=None, packing="replicated"):

@@ -435,6 +435,10 @@ hd_status hd_test_stage(const hd_database *db, int which, uint32_t agg, int32_t 
 hd_status hd_test_rotate(hd_context *ctx, const hd_eval_keys *evk, const hd_ciphertext *ct,
                          int32_t step, hd_ciphertext **out);
 hd_status hd_test_rescale(hd_context *ctx, const hd_ciphertext *ct, hd_ciphertext **out);
+/* Fault injection (test use): XOR one u64 word of a database's diagonal D[agg][k] in device
+ * memory with `mask` (word < L n, or 2 L n for encrypted diagonals).  XOR-ing again restores
+ * it.  Lets the parity tests prove they detect a single flipped residue bit. */
+hd_status hd_test_inject(hd_database *db, uint32_t agg, int32_t k, uint64_t word, uint64_t mask);
 
 #ifdef __cplusplus
 }

@@ -39,7 +39,7 @@ ABI_FUNCTIONS = [
     "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
     "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch", "hd_eval_add_many", "hd_baby_steps",
     "hd_query_baby", "hd_database_aggregate", "hd_compare_ex", "hd_enroll_footprint",
-    "hd_ciphertext_export_level", "hd_encrypt_query_ex",
+    "hd_ciphertext_export_level", "hd_encrypt_query_ex", "hd_test_inject",
 ]
 
 
@@ -142,6 +142,7 @@ def load():
             L.hd_test_stage.argtypes = [VP, C.c_int, C.c_uint32, C.c_int32, VP, C.c_size_t]
             L.hd_test_rotate.argtypes = [VP, VP, VP, C.c_int32, C.POINTER(VP)]
             L.hd_test_rescale.argtypes = [VP, VP, C.POINTER(VP)]
+            L.hd_test_inject.argtypes = [VP, C.c_uint32, C.c_int32, C.c_uint64, C.c_uint64]
             L.hd_chebyshev_degree.argtypes = [C.c_uint32, C.POINTER(C.c_uint32)]
             L.hd_chebyshev_coefficients.argtypes = [C.c_double, C.c_uint32, VP, C.c_size_t]
             L.hd_compare.argtypes = [VP, VP, VP, C.c_size_t, VP, C.c_uint32, VP]
@@ -630,6 +631,10 @@ class Context(_Handle):
         out = np.zeros(shape, np.uint64)
         _check("hd_test_stage", load().hd_test_stage(db.h, which, agg, index, _ptr(out), out.size))
         return out
+
+    def test_inject(self, db, agg, k, word, mask):
+        """hd_test_inject: XOR one word of D[agg][k] on the device (fault injection)."""
+        _check("hd_test_inject", load().hd_test_inject(db.h, agg, k, C.c_uint64(word), C.c_uint64(mask)))
 
     def test_rotate(self, evk, ct, step):
         out = VP()

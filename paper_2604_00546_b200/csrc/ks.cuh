@@ -48,6 +48,9 @@ hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t 
 // Warp-specialised TMA pipeline for full giant-step ranges (mac_tma.cu); Q <= 4 queries per
 // diagonal pass; r [Q][n1][2][L][n], S [Q][A][nj][2][L][n].  HD_MAC_VARIANT=c selects mac.cu.
 bool mac_tma_supported(const hd_context *c, int n1, int N, bool flat, uint32_t Q);
+// the degree-2 MAC of encrypted diagonals (NEXT-1) on the same pipeline: S3 [A][nj][3][L][n]
+hd_status mac_tma_ct_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S3, uint32_t A, int n1, int N,
+                         const std::vector<int32_t> &js, bool flat);
 hd_status mac_tma_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A, int n1, int N,
                       const std::vector<int32_t> &js, uint32_t Q, bool flat);
 

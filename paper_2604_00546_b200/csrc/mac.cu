@@ -461,6 +461,7 @@ hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint
                      int N, const std::vector<int32_t> &js, bool flat) {
   if (js.empty() || A_loc == 0) return HD_OK;
   if (c->n % MAC_TPB) return hd_fail(HD_E_PARAMS, "ring too small for the encrypted MAC");
+  if (mac_tma_supported(c, n1, N, flat, 1) && c->L <= 8) return mac_tma_ct_run(c, Dct, r, S3, A_loc, n1, N, js, flat);
   const int jmin = js.front(), nj = (int)js.size();
   const char *force = getenv("HD_MAC_VARIANT");  // 'g': the generic kernel (tests)
   const bool generic = force && force[0] == 'g';

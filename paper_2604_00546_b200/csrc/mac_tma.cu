@@ -256,6 +256,136 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
   }
 }
 
+// ---- encrypted diagonals (NEXT-1, R26): the degree-2 MAC over the same pipeline ----------
+// D [a][k][poly][L][n]: per limb m a 5-D map (coefficient, poly, diagonal within a block, block,
+// aggregate) based at limb m; one box per stage = TC x 2 polys x SPS x JT x AG.  Per stage word
+// pair (D0, D1) and baby step: d0 += r0 D0, d1 += r0 D1 + r1 D0, d2 += r1 D1,
+// carry-save, d1's mid folded every 4 steps, all banked every 64 steps (d1 takes 2 products
+// per step: 128 products < 2^127).  S3 [a][j][3][L][n].
+constexpr int CT_MAXL = 8;
+struct CtMaps {
+  CUtensorMap m[CT_MAXL];
+};
+template <int AG, int JT, int SPS>
+__global__ void __launch_bounds__(AG *TC + 32, 1)
+    mac_tma_ct_kernel(const __grid_constant__ CtMaps tmD, const __grid_constant__ CUtensorMap tmR,
+                      uint64_t *__restrict__ S, int n1, int N, int L, int logn, int nj, uint32_t A, int flat,
+                      int stages, ModTab mt) {
+  extern __shared__ __align__(1024) unsigned char smem[];
+  constexpr int D_WORDS = AG * JT * SPS * 2 * TC, R_WORDS = SPS * 2 * TC;
+  constexpr uint32_t STAGE_BYTES = (D_WORDS + R_WORDS) * 8;
+  constexpr int CONSUMERS = AG * TC;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)stages * STAGE_BYTES);
+  uint64_t *empty = full + stages;
+  const int n = 1 << logn, tiles = n / TC, G = N / n1, ngrp = G / JT, nsb = n1 / SPS;
+  const uint32_t nag = A / AG, units = nag * (uint32_t)ngrp * (uint32_t)tiles * (uint32_t)L;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; s++) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMERS / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x >= CONSUMERS) {  // ---------------- producer warp ----------------
+    if (threadIdx.x != CONSUMERS) return;
+    uint64_t pol_stream, pol_keep;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    int stage = 0;
+    uint32_t phase = 0;
+    for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+      const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
+      for (int sb = 0; sb < nsb; sb++) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+        uint64_t *base = reinterpret_cast<uint64_t *>(smem + (size_t)stage * STAGE_BYTES);
+        tma_load_5d(base, &tmD.m[x.m], x.tile * TC, 0, sb * SPS, x.gg0, (int)x.a0, &full[stage], pol_stream);
+        tma_load_3d(base + D_WORDS, &tmR, x.tile * TC, x.m, sb * SPS * 2, &full[stage], pol_keep);
+        if (++stage == stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+    return;
+  }
+  const int g = threadIdx.x / TC, t = threadIdx.x % TC;
+  int stage = 0;
+  uint32_t phase = 0;
+  for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
+    const uint64_t q = mt.q[x.m], bar = mt.bar[x.m], r64 = mt.r64[x.m], r64s = mt.r64s[x.m];
+    Acc acc[JT][3];
+    uint64_t part[JT][3];
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++)
+#pragma unroll
+      for (int e = 0; e < 3; e++) {
+        acc[jj][e] = Acc{0, 0, 0, 0};
+        part[jj][e] = 0;
+      }
+    for (int sb = 0; sb < nsb; sb++) {
+      mbar_wait(&full[stage], phase);
+      // box order [AG][JT][SPS][2][TC]
+      const uint64_t *Ds =
+          reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + g * JT * SPS * 2 * TC + t;
+      const uint64_t *Rs = reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + D_WORDS + t;
+#pragma unroll
+      for (int s = 0; s < SPS; s++) {
+        const uint64_t r0 = Rs[(2 * s) * TC], r1 = Rs[(2 * s + 1) * TC];
+        const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1, r11 = (uint32_t)(r1 >> 32);
+#pragma unroll
+        for (int jj = 0; jj < JT; jj++) {
+          const uint64_t d0 = Ds[((jj * SPS + s) * 2 + 0) * TC], d1 = Ds[((jj * SPS + s) * 2 + 1) * TC];
+          const uint32_t a00 = (uint32_t)d0, a01 = (uint32_t)(d0 >> 32), a10 = (uint32_t)d1, a11 = (uint32_t)(d1 >> 32);
+          acc_mac(acc[jj][0], r00, r01, a00, a01);
+          acc_mac(acc[jj][1], r00, r01, a10, a11);
+          acc_mac(acc[jj][1], r10, r11, a00, a01);
+          acc_mac(acc[jj][2], r10, r11, a10, a11);
+        }
+        if (((sb * SPS + s) & 3) == 3) {  // d1: 4 mid terms per step -> fold every 4 steps (16 < 2^64)
+#pragma unroll
+          for (int jj = 0; jj < JT; jj++)
+#pragma unroll
+            for (int e = 0; e < 3; e++) acc_fold(acc[jj][e]);
+        }
+      }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[stage]);
+      if (++stage == stages) {
+        stage = 0;
+        phase ^= 1;
+      }
+      if ((((sb + 1) * SPS) & 63) == 0) {  // bank every 64 baby steps
+#pragma unroll
+        for (int jj = 0; jj < JT; jj++)
+#pragma unroll
+          for (int e = 0; e < 3; e++) {
+            Acc &X = acc[jj][e];
+            acc_fold(X);
+            part[jj][e] = addmod(part[jj][e], reduce128(X.hi + X.cnt, X.lo, q, bar, r64, r64s), q);
+            X = Acc{0, 0, 0, 0};
+          }
+      }
+    }
+    const size_t ls = (size_t)L * n;
+    const uint32_t a = x.a0 + g;
+#pragma unroll
+    for (int jj = 0; jj < JT; jj++) {
+      const int gg = x.gg0 + jj;
+      const int jslot = flat ? gg : (gg < G / 2 ? gg + G / 2 : gg - G / 2);
+      uint64_t *Sa = S + ((size_t)a * nj + jslot) * 3 * ls + (size_t)x.m * n + (size_t)x.tile * TC + t;
+#pragma unroll
+      for (int e = 0; e < 3; e++) {
+        Acc &X = acc[jj][e];
+        acc_fold(X);
+        Sa[(size_t)e * ls] = addmod(part[jj][e], reduce128(X.hi + X.cnt, X.lo, q, bar, r64, r64s), q);
+      }
+    }
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   if (!fn) {
@@ -321,7 +451,72 @@ hd_status launch_f(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, 
   HD_MAC_L(1, 4);
 #undef HD_MAC_L
 }
+
+template <int AG, int JT, int SPS>
+hd_status launch_ct(hd_context *c, const CtMaps &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int nj,
+                    uint32_t A, bool flat) {
+  constexpr size_t STAGE_BYTES = (size_t)(AG * JT * SPS * 2 * TC + SPS * 2 * TC) * 8;
+  const size_t budget = 227 * 1024 - 256;
+  int stages = (int)std::min<size_t>(16, budget / STAGE_BYTES);
+  if (const char *e = getenv("HD_MAC_STAGES")) stages = std::max(2, std::min(stages, atoi(e)));
+  if (stages < 2) return hd_fail(HD_E_PARAMS, "MAC stage does not fit shared memory");
+  const size_t smem = stages * STAGE_BYTES + 2 * stages * sizeof(uint64_t);
+  auto kern = mac_tma_ct_kernel<AG, JT, SPS>;
+  HD_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (!g_num_sms) HD_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, c->device));
+  const uint32_t units = (A / AG) * (uint32_t)(nj / JT) * (uint32_t)(c->n / TC) * (uint32_t)c->L;
+  const uint32_t grid = std::min<uint32_t>(units, (uint32_t)g_num_sms);
+  kern<<<grid, AG * TC + 32, smem, c->stream>>>(mD, mR, S, n1, N, c->L, c->logn, nj, A, flat ? 1 : 0, stages, c->mt);
+  ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  return HD_OK;
+}
 }  // namespace
+
+// S3 [A][nj][3][L][n] of encrypted diagonals Dct [A][N][2][L][n] (full giant-step ranges).
+hd_status mac_tma_ct_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S3, uint32_t A, int n1, int N,
+                         const std::vector<int32_t> &js, bool flat) {
+  if (js.empty() || A == 0) return HD_OK;
+  const int nj = (int)js.size(), G = N / n1, L = c->L, n = c->n;
+  if (nj != G || L > CT_MAXL) return hd_fail(HD_E_STATE, "TMA MAC expects one giant step per diagonal block");
+  const char *ag_env = getenv("HD_MAC_AG"), *sps_env = getenv("HD_MAC_SPS"), *jt_env = getenv("HD_MAC_CT_JT");
+  int ag = ag_env ? atoi(ag_env) : 2;
+  if (ag != 1 && ag != 2) ag = 2;
+  while (ag > 1 && A % ag) ag /= 2;
+  int sps = sps_env ? atoi(sps_env) : 8;
+  if (sps != 4 && sps != 8) sps = 8;
+  while (sps > 4 && n1 % sps) sps /= 2;
+  if (n1 % sps) sps = 2;  // n1 even (mac_tma_supported)
+  int jt = jt_env ? atoi(jt_env) : 2;
+  if (jt != 1 && jt != 2 && jt != 4) jt = 2;
+  while (jt > 1 && nj % jt) jt /= 2;
+  CtMaps mD;
+  hd_status s;
+  for (int m = 0; m < L; m++) {  // D of limb m: (coefficient, poly, diagonal, block, aggregate)
+    const cuuint64_t dims[5] = {(cuuint64_t)n, 2, (cuuint64_t)n1, (cuuint64_t)G, (cuuint64_t)A};
+    const cuuint64_t strides[4] = {(cuuint64_t)L * n * 8, (cuuint64_t)2 * L * n * 8, (cuuint64_t)n1 * 2 * L * n * 8,
+                                   (cuuint64_t)N * 2 * L * n * 8};
+    const cuuint32_t box[5] = {(cuuint32_t)TC, 2, (cuuint32_t)sps, (cuuint32_t)jt, (cuuint32_t)ag};
+    if ((s = encode(&mD.m[m], D + (size_t)m * n, 5, dims, strides, box))) return s;
+  }
+  CUtensorMap mR;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)L, (cuuint64_t)2 * n1};
+    const cuuint64_t strides[2] = {(cuuint64_t)n * 8, (cuuint64_t)L * n * 8};
+    const cuuint32_t box[3] = {(cuuint32_t)TC, 1, (cuuint32_t)(2 * sps)};
+    if ((s = encode(&mR, r, 3, dims, strides, box))) return s;
+  }
+#define HD_CT_L(AG_, JT_, SPS_) return launch_ct<AG_, JT_, SPS_>(c, mD, mR, S3, n1, N, nj, A, flat)
+  if (ag == 2 && jt == 2 && sps == 8) { HD_CT_L(2, 2, 8); }
+  if (ag == 2 && jt == 2 && sps == 4) { HD_CT_L(2, 2, 4); }
+  if (ag == 2 && jt == 1) { HD_CT_L(2, 1, 8); }
+  if (ag == 1 && jt == 4) { HD_CT_L(1, 4, 8); }
+  if (ag == 1 && jt == 2) { HD_CT_L(1, 2, 8); }
+  if (ag == 2 && jt == 4) { HD_CT_L(2, 4, 4); }
+  if (sps == 2) { HD_CT_L(1, 1, 2); }
+  HD_CT_L(1, 1, 8);
+#undef HD_CT_L
+}
 
 bool mac_tma_supported(const hd_context *c, int n1, int N, bool flat, uint32_t Q) {
   const char *v = getenv("HD_MAC_VARIANT");  // 'c': the LDG kernels of mac.cu ('g': generic)

@@ -13,6 +13,8 @@
 #include "common.cuh"
 #include "ks.cuh"
 
+#include <nvtx3/nvToolsExt.h>
+
 static hd_status giant_and_fold(hd_database *db, cudaEvent_t *E);
 static hd_status scan_tail(hd_database *db, uint64_t *Sbuf, cudaEvent_t *E, bool last, int par, hd_ciphertext **out);
 
@@ -59,8 +61,28 @@ static hd_status bind_keys(hd_database *db, const hd_eval_keys *evk) {
 // overlaps the next query's A work; S is double-buffered (A waits until B's rescale
 // of the query two back has consumed the buffer).  With HD_SERIAL=1 both run on the
 // caller's stream.
+// NVTX ranges of the query phases (host enqueue side; ncu --nvtx-include "hd_query/mac/" etc.)
+struct Nvtx {  // pops whatever is still open when the scope ends (error returns included)
+  int depth = 0;
+  explicit Nvtx(const char *name) { push(name); }
+  void push(const char *name) {
+    nvtxRangePushA(name);
+    ++depth;
+  }
+  void pop() {
+    if (depth) {
+      nvtxRangePop();
+      --depth;
+    }
+  }
+  ~Nvtx() {
+    while (depth) pop();
+  }
+};
+
 static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, uint32_t Q, cudaStream_t sa,
                           cudaStream_t sb, hd_ciphertext **out, size_t n_out, const uint64_t *r_ext = nullptr) {
+  Nvtx range_query("hd_query");
   hd_context *c = db->ctx;
   const int n = c->n, L = c->L, n1 = (int)db->n1, nj = (int)db->js.size();
   const uint32_t A = db->A_loc;
@@ -102,6 +124,7 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, 
     cudaEventRecord(E[8], sa);
   }
   // ---- baby steps: r[0] = q; r[i] = Rot_i(q), hoisted (per query) ----
+  range_query.push("baby_steps");
   for (uint32_t qi = 0; qi < Q && !r_ext; qi++) {
     const hd_ciphertext *query = queries[qi];
     uint64_t *rq = rbase + (size_t)qi * n1 * ctL;
@@ -120,6 +143,8 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, 
   }
   cudaEventRecord(E[1], sa);
   // ---- MAC; a batch streams D once for all its queries (NEXT-4) ----
+  range_query.pop();
+  range_query.push("mac");
   if (Q > 1) {
     if ((s = mac_batch_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat, Q))) return s;
   } else if (db->encrypted) {
@@ -130,6 +155,8 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, 
   cudaEventRecord(E[2], sa);
   HD_CUDA(cudaEventRecord(db->ev_mac, sa));
   // ---------------- stream B ----------------
+  range_query.pop();
+  range_query.push("rescale_giant_fold");
   HD_CUDA(cudaStreamWaitEvent(sb, db->ev_mac, 0));
   c->stream = sb;
   cudaEventRecord(E[3], sb);
@@ -508,6 +535,24 @@ extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t ag
   if (cap < len) return hd_fail(HD_E_INVALID_ARG, "capacity too small");
   HD_CUDA(cudaStreamSynchronize(c->stream));
   HD_CUDA(cudaMemcpy(host_dst, src, len * 8, cudaMemcpyDeviceToHost));
+  return HD_OK;
+}
+
+__global__ void xor_word_kernel(uint64_t *p, uint64_t mask) { *p ^= mask; }
+
+extern "C" hd_status hd_test_inject(hd_database *db, uint32_t agg, int32_t k, uint64_t word, uint64_t mask) {
+  if (!db) return hd_fail(HD_E_INVALID_ARG, "null database");
+  hd_context *c = db->ctx;
+  const size_t dw = (db->encrypted ? 2 : 1) * (size_t)c->L * c->n;  // words of one diagonal
+  if (agg < db->lay.agg_begin || agg >= db->lay.agg_end || k < 0 || k >= (int)db->N || word >= dw)
+    return hd_fail(HD_E_INVALID_ARG, "fault position outside the database");
+  uint64_t *p = db->D + ((size_t)(agg - db->lay.agg_begin) * db->N + k) * dw + word;
+  HD_CUDA(cudaStreamSynchronize(c->stream));
+  hd_context_synchronize(c);
+  xor_word_kernel<<<1, 1, 0, c->stream>>>(p, mask);
+  ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  HD_CUDA(cudaStreamSynchronize(c->stream));
   return HD_OK;
 }
 

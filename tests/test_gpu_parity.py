@@ -416,3 +416,26 @@ def test_level_reduced_async_export():
     assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-6
     with pytest.raises(hd.HDError):
         ctx.ciphertext_export_async(run.outs[0], None, nlimbs=cfg.limbs)  # outputs have L-1 limbs
+
+
+def test_fault_injection_is_detected():
+    """The parity checks catch a single flipped residue bit: flipping one bit of one diagonal
+    word of aggregate 1 (C2, two aggregates) changes that aggregate's output ciphertext (now
+    unequal to the oracle's) and leaves aggregate 0 bit-exact; flipping it back restores parity.
+    The flipped coefficient is an NTT-domain residue, so after decryption the error spreads over
+    every slot of the block: the score check fails too."""
+    run = Run(CONFIGS["C2"])
+    o, cfg, ctx = run.o, run.cfg, run.ctx
+    s_ntt, steps, keys = run.oracle_keys()
+    r = o.baby_steps(run.oracle_query_ct(), cfg.n1, steps, keys)
+    want = [o.scan_aggregate(r, cfg.n1, cfg.dim, run.oracle_D(a), steps, keys) for a in range(cfg.aggregates)]
+    assert all((ctx.ciphertext_residues(run.outs[a]) == want[a]).all() for a in range(cfg.aggregates))
+    ctx.test_inject(run.db, 1, 37, 12345, 1 << 20)
+    outs = ctx.query(run.evk, run.db, run.qct)
+    assert (ctx.ciphertext_residues(outs[0]) == want[0]).all()
+    assert not (ctx.ciphertext_residues(outs[1]) == want[1]).all()
+    sc = ctx.decrypt_scores(run.sk, run.db.layout, outs)
+    assert np.abs(sc - _cos(run.db_vecs, run.q)).max() > 1e-3
+    ctx.test_inject(run.db, 1, 37, 12345, 1 << 20)  # restore
+    outs = ctx.query(run.evk, run.db, run.qct, outs)
+    assert all((ctx.ciphertext_residues(outs[a]) == want[a]).all() for a in range(cfg.aggregates))
