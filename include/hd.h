@@ -25,6 +25,13 @@
  *     database (Alg. online-aggr) -> hd_query_batch, hd_database_aggregate
  *   - sharded scans over P GPUs: baby-step slices + all-gather
  *                                                     -> hd_baby_steps, hd_query_baby
+ *     and the stream-ordered, level-reduced result export of the gather
+ *                                                     -> hd_ciphertext_export_level
+ *   - device memory from the caller's allocator (the Python binding
+ *     passes PyTorch's caching allocator), the pre-upload footprint check
+ *                                         -> hd_context_create, hd_enroll_footprint
+ *   - the paper-depth key-switching profile (alpha limbs per digit, K special primes,
+ *     R31)                                            -> hd_params.digit_limbs / num_special
  *
  * Conventions
  *   - Every function returns hd_status (HD_OK = 0).  No C++ exception crosses the
@@ -38,12 +45,14 @@
  *   - Device: one hd_context is bound to one CUDA device and one CUDA stream (the
  *     caller's, e.g. torch.cuda.current_stream().cuda_stream; NULL = the legacy
  *     default stream).  Calls on one context must be serialised by the caller.
+ *     Internally the scan pipelines two queries on two context-owned streams ordered
+ *     by events against the caller's stream; nothing synchronises the device.
  *     All device memory of a context, its keys, databases and ciphertexts is
  *     allocated at creation time of those objects (never inside hd_query).
  *   - Residues: u64 in [0, q), NTT form (bit-reversed evaluation order, DESIGN.md
  *     R13).  Ciphertext layout [poly 0..1][limb][coef]; plaintext [limb][coef];
  *     rotation key [digit d < ceil(L/alpha)][poly (0 = b, 1 = a)][modulus l < L+K][coef]
- *     where modulus index L is the special prime P.
+ *     where modulus indices L..L+K-1 are the special primes p_k.
  *   - No CPU fallback: if no CUDA device is usable every call that computes
  *     returns HD_E_CUDA.
  */

@@ -24,6 +24,12 @@
 
 #include <cstdlib>
 
+// 1: the chunk kernel stages its chunks' twiddles in shared memory at start (2 CTAs per SM
+// instead of 3); 0: read from L1/L2 during the passes (A/B)
+#ifndef HD_NTT_TW_SMEM
+#define HD_NTT_TW_SMEM 0
+#endif
+
 namespace {
 
 constexpr int E = 16;  // elements per thread
@@ -228,8 +234,8 @@ __global__ void __launch_bounds__(256, 3) ntt_cols_kernel(uint64_t *base, RowMap
   cols_rec<INV, S, 0>(v, A);
 }
 
-template <bool INV, int S, int P>
-__device__ __forceinline__ void chunks_rec(uint64_t (&v)[E], uint32_t tid, uint64_t *smt, const TwGlobal &tw,
+template <bool INV, int S, int P, class TW>
+__device__ __forceinline__ void chunks_rec(uint64_t (&v)[E], uint32_t tid, uint64_t *smt, const TW &tw,
                                            uint64_t q) {
   using PP = Pass<INV, S, P>;
 #pragma unroll
@@ -239,7 +245,7 @@ __device__ __forceinline__ void chunks_rec(uint64_t (&v)[E], uint32_t tid, uint6
 #pragma unroll
   for (int i = 0; i < E; i++) smt[pad_idx(elem_of<PP::KP, PP::REM, S>(i, tid))] = v[i];
   __syncthreads();
-  if constexpr (P < PP::NP - 1) chunks_rec<INV, S, P + 1>(v, tid, smt, tw, q);
+  if constexpr (P < PP::NP - 1) chunks_rec<INV, S, P + 1, TW>(v, tid, smt, tw, q);
 }
 
 // ---- chunks kernel: the S low stages on contiguous chunks of 2^S; tpc chunks per CTA ----
@@ -285,8 +291,24 @@ __global__ void __launch_bounds__(256, 3) ntt_chunks_kernel(uint64_t *base, RowM
       sm[t0 * PS + pad_idx(x0 + 1)] = w1;
     }
   }
+#if HD_NTT_TW_SMEM
+  ulonglong2 *tws = reinterpret_cast<ulonglong2 *>(sm + tpc * PS);
+  for (int k = 0; k < S; k++) {
+    const uint32_t cnt = (uint32_t)tpc << k;
+    const ulonglong2 *srcw = twv.T + ((size_t)((1u << s1) + chunk0) << k);
+    ulonglong2 *dstw = tws + (size_t)tpc * ((1u << k) - 1);
+    for (uint32_t i = threadIdx.x; i < cnt; i += blockDim.x) dstw[i] = __ldg(srcw + i);
+  }
   __syncthreads();
-  chunks_rec<INV, S, 0>(v, tid, sm + tr * PS, twv, q);
+  TwShared twsm;
+  twsm.sm = tws;
+  twsm.tr = tr;
+  twsm.tpc = tpc;
+  chunks_rec<INV, S, 0, TwShared>(v, tid, sm + tr * PS, twsm, q);
+#else
+  __syncthreads();
+  chunks_rec<INV, S, 0, TwGlobal>(v, tid, sm + tr * PS, twv, q);
+#endif
   const bool scale = INV && s1 == 0;
   const bool fin = !INV && final_out;
   // epilogue rows: r = (x 2 + p) ell + l
@@ -428,7 +450,8 @@ hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &ma
   if (inverse && epi.mode) return hd_fail(HD_E_INVALID_ARG, "epilogue only on forward transforms");
   const int tpt_b = 1 << (s2 - 4);
   const int tpc_b = std::max(1, std::min(256 / tpt_b, 1 << s1));
-  const size_t smem_b = sizeof(uint64_t) * tpc_b * (size_t)((1 << s2) + ((1 << s2) >> 4));
+  const size_t smem_b = sizeof(uint64_t) * tpc_b * (size_t)((1 << s2) + ((1 << s2) >> 4)) +
+                        (HD_NTT_TW_SMEM ? 16 * (size_t)tpc_b * ((1 << s2) - 1) : 0);
   const int tpt_a = s1 >= 4 ? 1 << (s1 - 4) : 1;
   const int tpc_a = std::max(1, std::min(256 / tpt_a, 1 << s2));
   const size_t smem_a = sizeof(uint64_t) * (tpc_a * (size_t)((1 << s1) + ((1 << s1) >> 4) + 1) + 2) +
