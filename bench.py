@@ -324,6 +324,8 @@ def main():
     per = cfg.num_slots if flat else (cfg.num_slots // cfg.dim // 2) * cfg.dim  # vectors per aggregate
     A = -(-cfg.num_vectors // per)
     a0, a1 = hdd.shard_range(A, rank, world)
+    if A < world:  # every rank needs at least one aggregate (C2 has 2)
+        raise SystemExit(f"{A} aggregates cannot be sharded over {world} ranks")
     # ---- setup (untimed): keys on rank 0 -> NCCL broadcast; local enrollment of this shard ----
     _, q, _ = make_dataset(16, cfg.dim, cfg.data_seed)  # query only (rows drawn per shard below)
     steps = ctx.rotation_steps(cfg.dim, cfg.n1, packing=args.packing)

@@ -18,17 +18,18 @@ if not torch.cuda.is_available():
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("extra", [[], ["--packing", "flat", "--scenario", "membership"]])
+@pytest.mark.parametrize("extra", [["--config", "C2"],
+                                   ["--config", "C3", "--packing", "flat", "--scenario", "membership"]])
 def test_two_ranks_on_one_gpu(extra):
     env = dict(os.environ, HD_BENCH_ONE_GPU="1")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + len(extra)), os.path.join(ROOT, "bench.py"),
-           "--gpus", "2", "--config", "C2", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", *extra]
+           "--gpus", "2", "--steps", "2", "--warmup", "3", "--no-cpu-baseline", *extra]
     out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [json.loads(x) for x in out.stdout.splitlines() if x.startswith("{")]
     assert len(lines) == 1  # rank 0 prints once
     d = lines[0]
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "aggregate-shard x2"
-    if not extra:  # the scan: every score of both shards checked on rank 0
+    if "--scenario" not in extra:  # the scan: every score of both shards checked on rank 0
         assert d["check"]["ok"] and d["check"]["scores_checked"] == 1 << 14

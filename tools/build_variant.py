@@ -1,6 +1,6 @@
 """Build an A/B variant of libhd.so with a sed-style substitution in one source file.
 
-    python tools/build_variant.py NAME FILE 'OLD' 'NEW'   -> paper_2604_00546_b200/libhd_NAME.so
+    python tools/build_variant.py NAME FILE 'OLD' 'NEW' ['OLD' 'NEW' ...]  -> paper_2604_00546_b200/libhd_NAME.so
 Use with HD_LIBHD=paper_2604_00546_b200/libhd_NAME.so python bench.py ...
 """
 import glob
@@ -15,14 +15,17 @@ CSRC = os.path.join(ROOT, "paper_2604_00546_b200", "csrc")
 
 
 def main():
-    name, fname, old, new = sys.argv[1:5]
+    name, fname = sys.argv[1:3]
+    pairs = list(zip(sys.argv[3::2], sys.argv[4::2]))  # one or more OLD NEW substitutions
     tmp = tempfile.mkdtemp()
     dst = os.path.join(tmp, "pkg", "csrc")  # the sources include ../../include/hd.h
     shutil.copytree(CSRC, dst)
     shutil.copytree(os.path.join(ROOT, "include"), os.path.join(tmp, "include"))
     src = open(os.path.join(dst, fname)).read()
-    assert old in src, f"pattern not found in {fname}"
-    open(os.path.join(dst, fname), "w").write(src.replace(old, new))
+    for old, new in pairs:
+        assert old in src, f"pattern not found in {fname}: {old}"
+        src = src.replace(old, new)
+    open(os.path.join(dst, fname), "w").write(src)
     objs = []
     procs = []
     for f in sorted(glob.glob(os.path.join(dst, "*.cu"))):
