@@ -45,16 +45,33 @@ __global__ void __launch_bounds__(TPB) kip_kernel(const uint64_t *__restrict__ d
   const uint64_t *dg = dig + (size_t)b * ell * ell * n;
   const uint64_t *cb = c1 + (size_t)b * c1_stride;
   uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0, b0l = 0, b0h = 0, b1l = 0, b1h = 0;
-  for (int d = 0; d < ell; d++) {
-    const uint64_t *row = ((int)e == d) ? cb + (size_t)d * n
-                                        : dg + ((size_t)d * ell + ((int)e < d ? (int)e : (int)e - 1)) * n;
-    const uint64_t v0 = row[s0], v1 = row[s1];
-    const ulonglong2 k0 = *reinterpret_cast<const ulonglong2 *>(key + ((size_t)(d * 2 + 0) * (L + 1) + gm) * n + t);
-    const ulonglong2 k1 = *reinterpret_cast<const ulonglong2 *>(key + ((size_t)(d * 2 + 1) * (L + 1) + gm) * n + t);
-    mac128(a0l, a0h, v0, k0.x);
-    mac128(b0l, b0h, v1, k0.y);
-    mac128(a1l, a1h, v0, k1.x);
-    mac128(b1l, b1h, v1, k1.y);
+  // digits in groups of KIP_DG: every load of a group (the Galois-gathered digit words and
+  // the key words) is issued before its products (the kernel is load-latency bound)
+  constexpr int KIP_DG = 4;
+  for (int d0 = 0; d0 < ell; d0 += KIP_DG) {
+    uint64_t v0[KIP_DG], v1[KIP_DG];
+    ulonglong2 k0[KIP_DG], k1[KIP_DG];
+#pragma unroll
+    for (int i = 0; i < KIP_DG; i++) {
+      const int d = d0 + i;
+      if (d < ell) {
+        const uint64_t *row = ((int)e == d) ? cb + (size_t)d * n
+                                            : dg + ((size_t)d * ell + ((int)e < d ? (int)e : (int)e - 1)) * n;
+        v0[i] = row[s0];
+        v1[i] = row[s1];
+        k0[i] = *reinterpret_cast<const ulonglong2 *>(key + ((size_t)(d * 2 + 0) * (L + 1) + gm) * n + t);
+        k1[i] = *reinterpret_cast<const ulonglong2 *>(key + ((size_t)(d * 2 + 1) * (L + 1) + gm) * n + t);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < KIP_DG; i++) {
+      if (d0 + i < ell) {
+        mac128(a0l, a0h, v0[i], k0[i].x);
+        mac128(b0l, b0h, v1[i], k0[i].y);
+        mac128(a1l, a1h, v0[i], k1[i].x);
+        mac128(b1l, b1h, v1[i], k1[i].y);
+      }
+    }
   }
   const uint64_t q = mt.q[gm], bar = mt.bar[gm], r64 = mt.r64[gm], r64s = mt.r64s[gm];
   ulonglong2 *o0 = reinterpret_cast<ulonglong2 *>(u + ((size_t)(x * 2 + 0) * (ell + 1) + e) * n + t);
