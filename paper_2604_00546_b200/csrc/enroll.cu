@@ -307,7 +307,11 @@ static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing,
   const size_t rescale_chunk = std::min<size_t>(A * nj, 256);
   const size_t nb = n1 > 1 ? n1 - 1 : 1;
   // giant / fold / rescale scratch (stream B) and baby-step scratch (stream A)
-  size_t dig_e = A * ks_dig_elems(c, L - 1);
+  // the giant steps' ModUp digits: one slice per rotated giant step (summed by one
+  // ks_giant_sum pass, alpha = K = 1), one slice otherwise
+  size_t nrot = 0;
+  for (int p : db->pre) nrot += p != 0;
+  size_t dig_e = A * ks_dig_elems(c, L - 1) * (ks_general(c) ? 1 : std::max<size_t>(1, nrot));
   size_t u_e = A * 2 * (L - 1 + c->K) * n;
   size_t tmp_e = std::max({A * 2 * (L - 1) * n, rescale_chunk * 2 * n, (size_t)L * n});
   const size_t sL = (size_t)db->spoly * L * n;  // one giant-step sum

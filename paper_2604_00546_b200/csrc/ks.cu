@@ -92,6 +92,78 @@ __global__ void __launch_bounds__(TPB) kip_kernel(const uint64_t *__restrict__ d
   *o1 = v1;
 }
 
+// The whole hoisted giant-step sum of R23 in one pass (alpha = K = 1): for every aggregate b,
+//   u[b][p][e] = sum_j ( KIP(pi_j(dig_j[b]))[p][e] + [p == 0, e < ell] P pi_j(c0_j[b])[e] )
+//              + [e < ell] P T0[b][p][e]
+// over the J rotated giant steps j (digits dig_j, sums ct_j at ct_j + b ct_stride, key slot j)
+// and the unrotated one T0 (optional).  Written once, instead of J read-modify-write passes
+// over u plus one add_pscaled pass.  Two coefficients per thread; 128-bit accumulation of
+// the J ell products per output (< 2^128 for J ell < 2^8).
+constexpr int GIANT_MAXJ = 8;
+struct GiantSet {
+  int J = 0;
+  const uint64_t *dig[GIANT_MAXJ] = {};  // [B][ell][ell][n] (alpha = 1 slot layout)
+  const uint64_t *ct[GIANT_MAXJ] = {};   // S'_j of aggregate b at ct[j] + b ct_stride ([2][ell][n])
+  int slot[GIANT_MAXJ] = {};             // key / Galois slot in kptr / gal
+  const uint64_t *t0 = nullptr;          // unrotated giant-step sum (or null)
+  size_t ct_stride = 0;
+};
+__global__ void __launch_bounds__(TPB) kip_giant_kernel(uint64_t *__restrict__ u, int ell, int L, int logn,
+                                                        const uint64_t *const *__restrict__ kptr,
+                                                        const uint32_t *__restrict__ gal, ModTab mt, KipAcc ka,
+                                                        GiantSet gs, FDiv f_ell1) {
+  const int n = 1 << logn;
+  const uint32_t t = 2 * (blockIdx.x * blockDim.x + threadIdx.x);
+  const uint32_t be = blockIdx.y;
+  const uint32_t b = fdiv_q(be, f_ell1), e = be - b * (ell + 1);
+  if (t >= (uint32_t)n) return;
+  const int gm = (int)e < ell ? (int)e : L;
+  const uint64_t q = mt.q[gm], bar = mt.bar[gm], r64 = mt.r64[gm], r64s = mt.r64s[gm];
+  uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0, b0l = 0, b0h = 0, b1l = 0, b1h = 0;
+  uint64_t c00 = 0, c01 = 0;  // sum_j pi_j(c0_j)[e] (mod q), p = 0 only
+  for (int jj = 0; jj < gs.J; jj++) {
+    const uint32_t g = gal[gs.slot[jj]];
+    const uint32_t s0 = galois_src(t, g, logn), s1 = galois_src(t + 1, g, logn);
+    const uint64_t *key = kptr[gs.slot[jj]];
+    const uint64_t *dg = gs.dig[jj] + (size_t)b * ell * ell * n;
+    const uint64_t *cb = gs.ct[jj] + (size_t)b * gs.ct_stride;  // c0 rows [0, ell), c1 rows [ell, 2 ell)
+    for (int d = 0; d < ell; d++) {
+      const uint64_t *row = ((int)e == d) ? cb + (size_t)(ell + d) * n
+                                          : dg + ((size_t)d * ell + ((int)e < d ? (int)e : (int)e - 1)) * n;
+      const uint64_t v0 = row[s0], v1 = row[s1];
+      const ulonglong2 k0 = *reinterpret_cast<const ulonglong2 *>(key + ((size_t)(d * 2 + 0) * (L + 1) + gm) * n + t);
+      const ulonglong2 k1 = *reinterpret_cast<const ulonglong2 *>(key + ((size_t)(d * 2 + 1) * (L + 1) + gm) * n + t);
+      mac128(a0l, a0h, v0, k0.x);
+      mac128(b0l, b0h, v1, k0.y);
+      mac128(a1l, a1h, v0, k1.x);
+      mac128(b1l, b1h, v1, k1.y);
+    }
+    if ((int)e < ell) {
+      const uint64_t *c0r = cb + (size_t)e * n;
+      c00 = addmod(c00, c0r[s0], q);
+      c01 = addmod(c01, c0r[s1], q);
+    }
+  }
+  ulonglong2 v0 = make_ulonglong2(reduce128(a0h, a0l, q, bar, r64, r64s), reduce128(b0h, b0l, q, bar, r64, r64s));
+  ulonglong2 v1 = make_ulonglong2(reduce128(a1h, a1l, q, bar, r64, r64s), reduce128(b1h, b1l, q, bar, r64, r64s));
+  if ((int)e < ell) {
+    const uint64_t pw = ka.pw[e], pws = ka.pws[e];
+    if (gs.t0) {  // + P T0 (both polys)
+      const ulonglong2 x0 = *reinterpret_cast<const ulonglong2 *>(gs.t0 + (size_t)b * gs.ct_stride + (size_t)e * n + t);
+      const ulonglong2 x1 =
+          *reinterpret_cast<const ulonglong2 *>(gs.t0 + (size_t)b * gs.ct_stride + (size_t)(ell + e) * n + t);
+      c00 = addmod(c00, x0.x, q);
+      c01 = addmod(c01, x0.y, q);
+      v1.x = addmod(v1.x, shoup(x1.x, pw, pws, q), q);
+      v1.y = addmod(v1.y, shoup(x1.y, pw, pws, q), q);
+    }
+    v0.x = addmod(v0.x, shoup(c00, pw, pws, q), q);
+    v0.y = addmod(v0.y, shoup(c01, pw, pws, q), q);
+  }
+  *reinterpret_cast<ulonglong2 *>(u + ((size_t)(b * 2 + 0) * (ell + 1) + e) * n + t) = v0;
+  *reinterpret_cast<ulonglong2 *>(u + ((size_t)(b * 2 + 1) * (ell + 1) + e) * n + t) = v1;
+}
+
 // dst[b][p][e] += P src[b][p][e] for e < ell (the P limb of P src is 0): a giant step
 // without rotation, in the extended basis (R23).  dst rows [b][p][ell+1][n], src [b][p][ell][n].
 __global__ void add_pscaled_kernel(uint64_t *__restrict__ dst, size_t dst_stride, const uint64_t *__restrict__ src,
@@ -370,6 +442,27 @@ hd_status ks_kip_accumulate(hd_context *c, const uint64_t *dig, const uint64_t *
   kip_kernel<<<grid_pairs(c->n, B * (ell + 1)), TPB, 0, c->stream>>>(
       dig, ct + (size_t)ell * c->n, ct_stride, u, ell, 1, c->L, c->logn, kptr_dev, gal_dev, c->mt,
       kip_acc(c, ell, ct, ct_stride), fdiv_make(ell + 1), fdiv_make(1));
+  ++c->launches;
+  HD_CUDA(cudaGetLastError());
+  return HD_OK;
+}
+
+hd_status ks_giant_sum(hd_context *c, uint32_t B, int ell, int J, const uint64_t *const *dig, const uint64_t *const *ct,
+                       const int *slot, const uint64_t *t0, size_t ct_stride, const uint64_t *const *kptr_dev,
+                       const uint32_t *gal_dev, uint64_t *u) {
+  if (ks_general(c) || J > GIANT_MAXJ) return hd_fail(HD_E_PARAMS, "combined giant sum: alpha = K = 1, J <= 8");
+  GiantSet gs;
+  gs.J = J;
+  for (int j = 0; j < J; j++) {
+    gs.dig[j] = dig[j];
+    gs.ct[j] = ct[j];
+    gs.slot[j] = slot[j];
+  }
+  gs.t0 = t0;
+  gs.ct_stride = ct_stride;
+  kip_giant_kernel<<<grid_pairs(c->n, B * (ell + 1)), TPB, 0, c->stream>>>(u, ell, c->L, c->logn, kptr_dev, gal_dev,
+                                                                          c->mt, kip_acc(c, ell, nullptr, 0), gs,
+                                                                          fdiv_make(ell + 1));
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;

@@ -15,6 +15,12 @@ hd_status ks_kip(hd_context *c, const uint64_t *dig, const uint64_t *c1, size_t 
 //   u_b += KIP(pi_g(dig_b)) + (P pi_g(ct_b.c0), 0)   (a rotation before its ModDown)
 hd_status ks_kip_accumulate(hd_context *c, const uint64_t *dig, const uint64_t *ct, size_t ct_stride, uint32_t B,
                             int ell, const uint64_t *const *kptr_dev, const uint32_t *gal_dev, uint64_t *u);
+// The hoisted giant-step sum of R23 in one pass (alpha = K = 1): u_b = sum_j (KIP_j + (P pi_j(c0_j), 0))
+// + P T0_b over J rotated steps (digits dig[j], sums ct[j] + b ct_stride, key slot[j]) and the
+// unrotated sum T0 (may be null); u [B][2][ell+1][n] is written, not accumulated.
+hd_status ks_giant_sum(hd_context *c, uint32_t B, int ell, int J, const uint64_t *const *dig, const uint64_t *const *ct,
+                       const int *slot, const uint64_t *t0, size_t ct_stride, const uint64_t *const *kptr_dev,
+                       const uint32_t *gal_dev, uint64_t *u);
 //   u_b += (P ct_b, with P limb 0)                    (a giant step without rotation)
 hd_status ks_add_pscaled(hd_context *c, uint64_t *u, const uint64_t *ct, size_t ct_stride, uint32_t B, int ell);
 // ModDown of u [X][2][ell+1][n] (P limb INTT'd in place) -> dst_x (+ pi_{g_k}(c0_b)).

@@ -223,8 +223,32 @@ static hd_status giant_and_fold(hd_database *db, cudaEvent_t *E) {
   //      ModDown per aggregate (R23) ----
   const int ell = L - 1;
   const size_t ext = (size_t)2 * (ell + c->K) * n;  // u: [A][2][ell+K][n]
-  HD_CUDA(cudaMemsetAsync(db->u, 0, (size_t)A * ext * 8, c->stream));
   const size_t sp_stride = (size_t)nj * ct1;  // between aggregates for fixed j
+  int nrot = 0, nzero = 0;
+  for (int jj = 0; jj < nj; jj++) (db->pre[jj] ? nrot : nzero)++;
+  if (!ks_general(c) && nrot <= 8 && nzero <= 1) {
+    // every rotated step's ModUp into its own digit slice, then the whole sum in one pass
+    const size_t dslice = (size_t)A * ks_dig_elems(c, ell);
+    std::vector<const uint64_t *> digs, cts;
+    std::vector<int> slots;
+    const uint64_t *t0 = nullptr;
+    for (int jj = 0; jj < nj; jj++) {
+      const uint64_t *Sj = db->Sp + (size_t)jj * ct1;
+      if (db->pre[jj] == 0) {
+        t0 = Sj;
+        continue;
+      }
+      uint64_t *dj = db->dig + digs.size() * dslice;
+      if ((s = ks_modup(c, Sj + (size_t)ell * n, sp_stride, A, ell, dj, db->tmp))) return s;
+      digs.push_back(dj);
+      cts.push_back(Sj);
+      slots.push_back(n1 - 1 + jj);
+    }
+    if ((s = ks_giant_sum(c, A, ell, (int)digs.size(), digs.data(), cts.data(), slots.data(), t0, sp_stride, db->kptr,
+                          db->gal, db->u)))
+      return s;
+  } else {  // general profile: accumulate rotation by rotation
+  HD_CUDA(cudaMemsetAsync(db->u, 0, (size_t)A * ext * 8, c->stream));
   for (int jj = 0; jj < nj; jj++) {
     const uint64_t *Sj = db->Sp + (size_t)jj * ct1;
     if (db->pre[jj] == 0) {
@@ -234,6 +258,7 @@ static hd_status giant_and_fold(hd_database *db, cudaEvent_t *E) {
     const size_t slot = (size_t)(n1 - 1) + jj;
     if ((s = ks_modup(c, Sj + (size_t)ell * n, sp_stride, A, ell, db->dig, db->tmp))) return s;
     if ((s = ks_kip_accumulate(c, db->dig, Sj, sp_stride, A, ell, db->kptr + slot, db->gal + slot, db->u))) return s;
+  }
   }
   if ((s = ks_moddown(c, db->u, A, 1, ell, db->gal, nullptr, 0, db->y, ct1, false, db->tmp))) return s;
   cudaEventRecord(E[5], c->stream);

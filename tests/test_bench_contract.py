@@ -33,3 +33,30 @@ def test_reference_arm_membership_scenario():
     d = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][0])
     assert "membership" in d["metric"] and d["config"]["limbs"] == 6 and d["value"] > 0
     assert "ChebyshevCompare" in d["cpu_baseline"]["sample"]
+
+
+def test_planted_positions_match_make_dataset():
+    """bench.py's score check regenerates the planted-match positions without the rows."""
+    from synth_inputs import make_dataset, planted_positions
+    for K, dim, seed in ((256, 64, 260400547), (5000, 64, 7), (1 << 14, 512, 260400548)):
+        _, _, pos = make_dataset(K, dim, seed)
+        assert (planted_positions(K, dim, seed) == pos).all()
+
+
+def test_reference_arm_config_equals_ours():
+    """The reference arm's config dict is built by the same function as ours (same_config)."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    import sys
+    argv = sys.argv
+    try:
+        sys.argv = ["bench.py"]
+        args = bench.parse()
+    finally:
+        sys.argv = argv
+    cfg = bench.workload_cfg(args)
+    assert bench.full_config(args, cfg, 1)["aggregates"] == cfg.aggregates
+    assert args.e2e_steps == args.steps
