@@ -226,6 +226,7 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
   const int n = c->n, M = c->L + c->K;
   // interleaved {w, shoup(w)} per index (one 128-bit load per butterfly group)
   std::vector<uint64_t> tw((size_t)2 * M * n), itw((size_t)2 * M * n), nv(2 * HD_MAXMOD, 0);
+  std::vector<double> twd((size_t)M * n, 0.0), itwd((size_t)M * n, 0.0);
   for (int l = 0; l < M; l++) {
     uint64_t q = c->mod[l], g = c->psi[l], gi = host_powmod(g, q - 2, q);
     std::vector<uint64_t> pw(n), ipw(n);
@@ -240,6 +241,10 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
       tw[2 * ((size_t)l * n + k) + 1] = host_shoup(pw[b], q);
       itw[2 * ((size_t)l * n + k)] = ipw[b];
       itw[2 * ((size_t)l * n + k) + 1] = host_shoup(ipw[b], q);
+      if (q < kNttFp64Bound) {  // exact as doubles (< 2^46)
+        twd[(size_t)l * n + k] = (double)pw[b];
+        itwd[(size_t)l * n + k] = (double)ipw[b];
+      }
     }
     c->ninv[l] = host_powmod((uint64_t)n, q - 2, q);
     c->ninvs[l] = host_shoup(c->ninv[l], q);
@@ -265,12 +270,15 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
   };
   cudaError_t e;
   if ((e = dev_alloc(c, &c->tw2, tw.size() * 8)) || (e = dev_alloc(c, &c->itw2, itw.size() * 8)) ||
+      (e = dev_alloc(c, &c->twd, twd.size() * 8)) || (e = dev_alloc(c, &c->itwd, itwd.size() * 8)) ||
       (e = dev_alloc(c, &c->ninv_dev, nv.size() * 8)) ||
       (e = dev_alloc(c, &c->xi_re, two_n * 8)) || (e = dev_alloc(c, &c->xi_im, two_n * 8)) ||
       (e = dev_alloc(c, &c->rotg, c->ns * 4)) || (e = dev_alloc(c, &c->d_flag, 64)))
     return fail(e);
   if ((e = cudaMemcpy(c->tw2, tw.data(), tw.size() * 8, cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(c->itw2, itw.data(), itw.size() * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(c->twd, twd.data(), twd.size() * 8, cudaMemcpyHostToDevice)) ||
+      (e = cudaMemcpy(c->itwd, itwd.data(), itwd.size() * 8, cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(c->ninv_dev, nv.data(), nv.size() * 8, cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(c->xi_re, xr.data(), two_n * 8, cudaMemcpyHostToDevice)) ||
       (e = cudaMemcpy(c->xi_im, xim.data(), two_n * 8, cudaMemcpyHostToDevice)) ||
@@ -306,7 +314,7 @@ extern "C" void hd_context_destroy(hd_context *c) {
 static void context_teardown(hd_context *c) {
   cudaSetDevice(c->device);
   quiesce(c);
-  for (void *p : {(void *)c->tw2, (void *)c->itw2, (void *)c->ninv_dev, (void *)c->xi_re, (void *)c->xi_im,
+  for (void *p : {(void *)c->tw2, (void *)c->itw2, (void *)c->twd, (void *)c->itwd, (void *)c->ninv_dev, (void *)c->xi_re, (void *)c->xi_im,
                   (void *)c->rotg, (void *)c->d_flag, c->scratch})
     dev_free(c, p);
   for (auto &b : c->ws_free) dev_free(c, b.p);
