@@ -590,7 +590,9 @@ def main():
     else:
         g_env = int(os.environ.get("HD_MAC_BATCH", "1") or 1)
         d_passes = Q if g_env <= 1 else (Q // 4 + (Q % 4) // 2 + Q % 2 if g_env >= 4 else Q // 2 + Q % 2)
-    mac_bytes = (d_passes * nloc * N * dpoly * L * n * 8
+    # bytes of one stored diagonal: 45-bit limbs packed into 6 bytes (R34), else dpoly L n u64
+    d_bytes, d_packed = db.diagonal_bytes
+    mac_bytes = (d_passes * nloc * N * d_bytes
                  + Q * (cfg.n1 * 2 * L * n * 8 + nloc * nj * spoly * L * n * 8))
     mac_avg_ms = statistics.mean(mac_ms)
     peak, peak_src = peaks()
@@ -641,12 +643,17 @@ def main():
     # ---- whole-query compulsory bytes against the step time ----
     # giant keys (+ the fold key for the replicated packing)
     n_gkeys = (nj - 1) if flat else sum(1 for j in db_js(cfg) if ((cfg.n1 * j) % N + N) % N != 0) + 1
-    q_bytes = (d_passes * nloc * N * dpoly * L * n * 8
-               + Q * ((cfg.n1 - 1) * key_bytes + n_gkeys * (L - 1) * 2 * L * n * 8
-                      + 2 * L * n * 8 + nloc * 2 * (L - 1) * n * 8 + (nj * key_bytes if enc_db else 0)))
+    rest = Q * ((cfg.n1 - 1) * key_bytes + n_gkeys * (L - 1) * 2 * L * n * 8
+                + 2 * L * n * 8 + nloc * 2 * (L - 1) * n * 8 + (nj * key_bytes if enc_db else 0))
+    q_bytes = d_passes * nloc * N * d_bytes + rest
+    q_bytes_u64 = d_passes * nloc * N * dpoly * L * n * 8 + rest  # 8 B per residue
     query_roofline = {"bytes": q_bytes, "achieved": q_bytes / (ms_per_step / 1e3) / 1e9, "peak": peak,
                       "unit": "GB/s", "frac": q_bytes / (ms_per_step / 1e3) / 1e9 / peak,
-                      "roofline_queries_per_s": Q * peak * 1e9 / q_bytes}  # every rank serves every query
+                      "roofline_queries_per_s": Q * peak * 1e9 / q_bytes,  # every rank serves every query
+                      "diagonals": "packed 45-bit residues, %d B per diagonal (R34)" % d_bytes if d_packed
+                      else "u64 residues, %d B per diagonal" % d_bytes,
+                      "bytes_u64_residues": q_bytes_u64,
+                      "frac_u64_residues": q_bytes_u64 / (ms_per_step / 1e3) / 1e9 / peak}
     tail_ms = None
     if tail:  # CUDA events around the comparison (and membership) of the last scan's outputs
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))

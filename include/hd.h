@@ -244,6 +244,13 @@ hd_status hd_enroll_footprint(hd_context *ctx, uint64_t num_vectors, uint32_t ve
                               uint32_t agg_begin, uint32_t agg_end, const hd_enroll_options *opt,
                               size_t *bytes);
 hd_status hd_database_layout(const hd_database *db, hd_layout *out);
+/* Device bytes of one stored diagonal (R34).  Plaintext diagonals served by the TMA
+ * MAC are stored packed: a limb whose modulus is below 2^47 keeps its residues in 6 bytes (a
+ * 31-bit low and a 16-bit high plane), other limbs in 8; at L = 3 (one 60-bit and two 45-bit
+ * limbs) a diagonal takes 20 n bytes instead of 24 n.  *packed = 1 when that applies, else the
+ * diagonal is L n u64 words (2 L n for encrypted diagonals).  Residue values are unchanged:
+ * hd_test_stage returns them as u64 either way. */
+hd_status hd_database_diagonal_bytes(const hd_database *db, size_t *bytes, int *packed);
 /* Online database aggregation (NEXT-4; Alg. online-aggr, membership only): a new
  * handle with ONE aggregate whose diagonals are the sums (mod q) of the diagonals of all
  * aggregates of db (plaintext or encrypted, any packing; a FLAT_TBS database must be

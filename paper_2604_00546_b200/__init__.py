@@ -39,7 +39,7 @@ ABI_FUNCTIONS = [
     "hd_chebyshev_degree", "hd_chebyshev_coefficients", "hd_compare", "hd_membership_steps", "hd_membership",
     "hd_ciphertext_scale", "hd_decrypt_slots", "hd_query_batch", "hd_eval_add_many", "hd_baby_steps",
     "hd_query_baby", "hd_database_aggregate", "hd_compare_ex", "hd_enroll_footprint",
-    "hd_ciphertext_export_level", "hd_encrypt_query_ex", "hd_test_inject",
+    "hd_ciphertext_export_level", "hd_encrypt_query_ex", "hd_test_inject", "hd_database_diagonal_bytes",
 ]
 
 
@@ -113,6 +113,7 @@ def load():
             L.hd_enroll.argtypes = [VP, VP, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                     C.POINTER(VP)]
             L.hd_database_layout.argtypes = [VP, C.POINTER(Layout)]
+            L.hd_database_diagonal_bytes.argtypes = [VP, C.POINTER(C.c_size_t), C.POINTER(C.c_int)]
             L.hd_query.argtypes = [VP, VP, VP, VP, VP, C.c_size_t]
             L.hd_query_stats.argtypes = [VP, VP, C.c_size_t]
             L.hd_launch_count.argtypes = [VP, C.POINTER(C.c_uint64)]
@@ -273,6 +274,13 @@ class Database(_Handle):
         lay = Layout()
         _check("hd_database_layout", load().hd_database_layout(self.h, C.byref(lay)))
         return lay
+
+    @property
+    def diagonal_bytes(self):
+        """(bytes of one stored diagonal, packed?) -- hd_database_diagonal_bytes (R34)."""
+        b, p = C.c_size_t(0), C.c_int(0)
+        _check("hd_database_diagonal_bytes", load().hd_database_diagonal_bytes(self.h, C.byref(b), C.byref(p)))
+        return b.value, bool(p.value)
 
     @property
     def num_local(self):

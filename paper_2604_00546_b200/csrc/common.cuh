@@ -292,14 +292,49 @@ struct hd_ciphertext {
                                   // writers wait on it before overwriting data
 };
 
+// Packed plaintext diagonals (R34).  A residue of a limb whose modulus is below 2^47
+// ("narrow": the 45-bit scaling limbs) is stored in 6 bytes, not 8: bits 0..30 in a u32 low
+// plane, bits 31..46 in a u16 high plane (the 31-bit split is the one the MAC's Karatsuba
+// products use); other limbs ("wide") stay u64 words.  One diagonal is
+//   [wide limbs: W x n u64][narrow low planes: R x n u32][narrow high planes: R x n u16]
+// = (8 W + 6 R) n bytes (20 n instead of 24 n at L = 3).  Unpacked: W = L, R = 0.
+constexpr uint64_t kNarrowBound = 1ull << 47;
+struct DPack {
+  bool on = false;
+  int W = 0, R = 0;
+  uint8_t cls[HD_MAXMOD] = {0};  // 0 wide, 1 narrow
+  uint8_t idx[HD_MAXMOD] = {0};  // position within its class
+  size_t diag_bytes = 0;         // one diagonal
+};
+DPack dpack_make(const hd_context *c, bool on);
+__host__ __device__ __forceinline__ uint64_t dp_get(const uint8_t *diag, const DPack &P, int limb, size_t t, size_t n) {
+  if (!P.cls[limb]) return reinterpret_cast<const uint64_t *>(diag)[(size_t)P.idx[limb] * n + t];
+  const uint32_t lo = reinterpret_cast<const uint32_t *>(diag + 8 * (size_t)P.W * n)[(size_t)P.idx[limb] * n + t];
+  const uint16_t hi =
+      reinterpret_cast<const uint16_t *>(diag + (8 * (size_t)P.W + 4 * (size_t)P.R) * n)[(size_t)P.idx[limb] * n + t];
+  return lo | ((uint64_t)hi << 31);
+}
+__host__ __device__ __forceinline__ void dp_put(uint8_t *diag, const DPack &P, int limb, size_t t, size_t n,
+                                                uint64_t v) {
+  if (!P.cls[limb]) {
+    reinterpret_cast<uint64_t *>(diag)[(size_t)P.idx[limb] * n + t] = v;
+    return;
+  }
+  reinterpret_cast<uint32_t *>(diag + 8 * (size_t)P.W * n)[(size_t)P.idx[limb] * n + t] = (uint32_t)(v & 0x7fffffffu);
+  reinterpret_cast<uint16_t *>(diag + (8 * (size_t)P.W + 4 * (size_t)P.R) * n)[(size_t)P.idx[limb] * n + t] =
+      (uint16_t)(v >> 31);
+}
+
 struct hd_database {
   hd_context *ctx;
   hd_layout lay;
   uint32_t N, M, n1, A_loc;
   std::vector<int32_t> js;       // giant steps j (contiguous, non-empty ranges)
   std::vector<int32_t> pre;      // preRot(j) per j
-  uint64_t *D = nullptr;         // [A_loc][N][L][n] diagonal plaintexts, or
-                                 // [A_loc][N][2][L][n] diagonal ciphertexts (encrypted)
+  uint64_t *D = nullptr;         // [A_loc][N][L][n] diagonal plaintexts (packed: [A_loc][N] x
+                                 // dp.diag_bytes, R34), or [A_loc][N][2][L][n] diagonal
+                                 // ciphertexts (encrypted; never packed)
+  DPack dp;                      // packing of the plaintext diagonals
   bool encrypted = false;        // encrypted-database mode (NEXT-1, R26)
   bool flat = false;             // flat pre-rotated packing (NEXT-2, R27): no fold
   bool needs_prerotation = false;  // FLAT_TBS before hd_database_prerotate

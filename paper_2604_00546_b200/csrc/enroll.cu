@@ -240,6 +240,14 @@ extern "C" hd_status hd_database_layout(const hd_database *db, hd_layout *out) {
   return HD_OK;
 }
 
+extern "C" hd_status hd_database_diagonal_bytes(const hd_database *db, size_t *bytes, int *packed) {
+  if (!db || !bytes) return hd_fail(HD_E_INVALID_ARG, "null argument");
+  const hd_context *c = db->ctx;
+  *bytes = db->dp.on ? db->dp.diag_bytes : (db->encrypted ? 2 : 1) * (size_t)c->L * c->n * 8;
+  if (packed) *packed = db->dp.on ? 1 : 0;
+  return HD_OK;
+}
+
 extern "C" void hd_database_destroy(hd_database *db) {
   if (!db) return;
   hd_context *c = db->ctx;
@@ -266,6 +274,29 @@ extern "C" void hd_database_destroy(hd_database *db) {
     if (e) cudaEventDestroy(e);
   delete db;
   ctx_release(c);
+}
+
+DPack dpack_make(const hd_context *c, bool on) {
+  DPack P;
+  P.on = on;
+  for (int l = 0; l < c->L; l++) {
+    const bool narrow = on && c->mod[l] < kNarrowBound;
+    P.cls[l] = narrow ? 1 : 0;
+    P.idx[l] = (uint8_t)(narrow ? P.R++ : P.W++);
+  }
+  if (P.R == 0) P.on = false;  // nothing to pack
+  P.diag_bytes = (8 * (size_t)P.W + 6 * (size_t)P.R) * c->n;
+  return P;
+}
+
+// u64 rows [B][L][n] -> B packed diagonals (R34)
+__global__ void pack_d_kernel(const uint64_t *__restrict__ src, uint8_t *__restrict__ dst, DPack P, int L, int logn) {
+  const uint32_t n = 1u << logn;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const uint32_t b = blockIdx.y;
+  uint8_t *diag = dst + (size_t)b * P.diag_bytes;
+  for (int l = 0; l < L; l++) dp_put(diag, P, l, t, n, src[((size_t)b * L + l) * n + t]);
 }
 
 // Device objects of a database handle: diagonals D (uninitialised), query workspaces, events.
@@ -322,13 +353,18 @@ static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing,
     tmp_e = std::max(tmp_e, A * 2 * L * n);
   }
   const size_t dstride = (encrypted ? 2 : 1) * (size_t)L * n;  // one diagonal (pt, or ct)
+  // plaintext diagonals are packed (R34) whenever the TMA MAC (the only kernel that reads the
+  // packed form) serves this layout; HD_PACK_D=0 keeps u64 words (A/B knob)
+  const char *pk_env = getenv("HD_PACK_D");
+  db->dp = dpack_make(c, !encrypted && !(pk_env && pk_env[0] == '0') && mac_tma_supported(c, (int)n1, N, db->flat, 1));
+  const size_t d_bytes = db->dp.on ? db->dp.diag_bytes : dstride * 8;
   size_t tmp2_e = encrypted ? A * 2 * (L - 1) * n : 1;  // CRT remainders of the fused relinearise-rescale
   size_t digb_e = ks_dig_elems(c, L), ub_e = nb * 2 * (L + c->K) * n, tmpb_e = std::max(nb * 2 * L * n, (size_t)L * n);
   db->rescale_chunk = (uint32_t)rescale_chunk;
   struct Req {
     void **p;
     size_t bytes;
-  } reqs[] = {{(void **)&db->D, A * N * dstride * 8},
+  } reqs[] = {{(void **)&db->D, A * N * d_bytes},
               {(void **)&db->r, (size_t)n1 * ctL * 8},
               {(void **)&db->S, A * nj * sL * 8},
               {(void **)&db->Sp, A * nj * ct1 * 8},
@@ -426,6 +462,8 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
   if (!e) e = dev_alloc(c, &U, rows_per_agg * N * 8);
   if (!e) e = dev_alloc(c, &re, (size_t)KB * ns * 8);
   if (!e) e = dev_alloc(c, &im, (size_t)KB * ns * 8);
+  uint64_t *Pt = nullptr;  // packed diagonals: the u64 rows of a batch before packing (R34)
+  if (!e && db->dp.on) e = dev_alloc(c, &Pt, (size_t)KB * L * n * 8);
   uint64_t *V = nullptr, *E0 = nullptr;  // public-key encryption scratch (v, e0 of a batch)
   if (!e && pk) e = dev_alloc(c, &V, (size_t)KB * L * n * 8);
   if (!e && pk) e = dev_alloc(c, &E0, (size_t)KB * L * n * 8);
@@ -436,6 +474,7 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
     dev_free(c, im);
     dev_free(c, V);
     dev_free(c, E0);
+    dev_free(c, Pt);
   };
   if (e) {
     cleanup();
@@ -466,6 +505,16 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
                                                                            N, db->M, n1, a, k0, ns, re, im);
       ++c->launches;
       // plaintext rows (into c0 of each diagonal ciphertext in encrypted mode)
+      if (db->dp.on) {  // encode into u64 rows, then pack (R34)
+        s = encode_batch(c, re, im, kb, delta, L, Pt, (size_t)L * n);
+        if (!s) {
+          uint8_t *Dp = reinterpret_cast<uint8_t *>(db->D) + ((size_t)(a - agg_begin) * N + k0) * db->dp.diag_bytes;
+          pack_d_kernel<<<dim3((n + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(Pt, Dp, db->dp, L, c->logn);
+          ++c->launches;
+          if (cudaGetLastError() != cudaSuccess) s = hd_fail(HD_E_CUDA, "pack_d_kernel");
+        }
+        continue;
+      }
       s = encode_batch(c, re, im, kb, delta, L, Da + (size_t)k0 * dstride, dstride);
       if (!s && pk)  // Enc_pk with object id a N + k (R26), the oracle's or_enroll_aggregate_encrypted
         s = pk_encrypt_rows(c, pk, Da + (size_t)k0 * dstride, dstride, (uint32_t)kb, enc_seed,
@@ -494,6 +543,21 @@ __global__ void aggregate_kernel(const uint64_t *__restrict__ D, uint64_t *__res
   out[e] = acc;
 }
 
+// the same over packed diagonals (R34): element e = (k, limb, coefficient)
+__global__ void aggregate_packed_kernel(const uint8_t *__restrict__ D, uint8_t *__restrict__ out, uint32_t N,
+                                        uint32_t A, int logn, int L, ModTab mt, DPack P) {
+  const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const uint64_t n = 1ull << logn;
+  if (e >= (uint64_t)N * L * n) return;
+  const uint64_t t = e & (n - 1), kl = e >> logn;
+  const int l = (int)(kl % (uint64_t)L);
+  const uint64_t k = kl / (uint64_t)L;
+  const uint64_t q = mt.q[l];
+  uint64_t acc = 0;
+  for (uint32_t a = 0; a < A; a++) acc = addmod(acc, dp_get(D + ((uint64_t)a * N + k) * P.diag_bytes, P, l, t, n), q);
+  dp_put(out + k * P.diag_bytes, P, l, t, n, acc);
+}
+
 extern "C" hd_status hd_database_aggregate(hd_context *c, const hd_database *src, hd_database **out) {
   if (!c || !src || !out) return hd_fail(HD_E_INVALID_ARG, "null argument");
   if (src->ctx != c) return hd_fail(HD_E_STATE, "database from another context");
@@ -506,8 +570,17 @@ extern "C" hd_status hd_database_aggregate(hd_context *c, const hd_database *src
   if (s) return s;
   db->needs_prerotation = false;  // the source's diagonals are already in their final form
   const uint64_t per_agg = (uint64_t)src->N * (src->encrypted ? 2 : 1) * c->L * c->n;
-  aggregate_kernel<<<(unsigned)((per_agg + TPB - 1) / TPB), TPB, 0, c->stream>>>(src->D, db->D, per_agg, src->A_loc,
-                                                                                c->logn, c->L, c->mt);
+  if (src->dp.on != db->dp.on) {
+    hd_database_destroy(db);
+    return hd_fail(HD_E_STATE, "aggregate database packing differs from its source");
+  }
+  if (src->dp.on)
+    aggregate_packed_kernel<<<(unsigned)((per_agg + TPB - 1) / TPB), TPB, 0, c->stream>>>(
+        reinterpret_cast<const uint8_t *>(src->D), reinterpret_cast<uint8_t *>(db->D), src->N, src->A_loc, c->logn,
+        c->L, c->mt, src->dp);
+  else
+    aggregate_kernel<<<(unsigned)((per_agg + TPB - 1) / TPB), TPB, 0, c->stream>>>(src->D, db->D, per_agg, src->A_loc,
+                                                                                  c->logn, c->L, c->mt);
   ++c->launches;
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);

@@ -48,8 +48,9 @@ struct MacPlan {
 hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint64_t *S3, uint32_t A_loc, int n1,
                      int N, const std::vector<int32_t> &js, bool flat);
 // flat: the giant-step ranges of the flat packing (R27)
+// dp: packed diagonals (R34; only the TMA MAC reads them)
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
-                  const std::vector<int32_t> &js, bool flat);
+                  const std::vector<int32_t> &js, bool flat, const DPack &dp);
 
 // Warp-specialised TMA pipeline for full giant-step ranges (mac_tma.cu); Q <= 4 queries per
 // diagonal pass; r [Q][n1][2][L][n], S [Q][A][nj][2][L][n].  HD_MAC_VARIANT=c selects mac.cu.
@@ -58,11 +59,11 @@ bool mac_tma_supported(const hd_context *c, int n1, int N, bool flat, uint32_t Q
 hd_status mac_tma_ct_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S3, uint32_t A, int n1, int N,
                          const std::vector<int32_t> &js, bool flat);
 hd_status mac_tma_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A, int n1, int N,
-                      const std::vector<int32_t> &js, uint32_t Q, bool flat);
+                      const std::vector<int32_t> &js, uint32_t Q, bool flat, const DPack &dp);
 
 // Query batching (NEXT-4): Q queries per D pass; r [Q][n1][2][L][n], S [Q][A][nj][2][L][n].
 hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1,
-                        int N, const std::vector<int32_t> &js, bool flat, uint32_t Q);
+                        int N, const std::vector<int32_t> &js, bool flat, uint32_t Q, const DPack &dp);
 
 // Public-key encryption of count ciphertexts in place (c0 of ct_x = ct + x*ct_stride holds
 // the plaintext on entry); object ids obj0 + x; V, E0: count*L*n scratch each (client.cu).

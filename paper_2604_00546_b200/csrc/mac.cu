@@ -492,9 +492,10 @@ hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint
 }
 
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
-                  const std::vector<int32_t> &js, bool flat) {
+                  const std::vector<int32_t> &js, bool flat, const DPack &dp) {
   if (js.empty() || A_loc == 0) return HD_OK;
-  if (mac_tma_supported(c, n1, N, flat, 1)) return mac_tma_run(c, D, r, S, A_loc, n1, N, js, 1, flat);
+  if (mac_tma_supported(c, n1, N, flat, 1)) return mac_tma_run(c, D, r, S, A_loc, n1, N, js, 1, flat, dp);
+  if (dp.on) return hd_fail(HD_E_STATE, "packed diagonals (R34) need the TMA MAC (HD_MAC_VARIANT set after enrollment?)");
   const int jmin = js.front(), nj = (int)js.size();
   // every giant step uses all n1 baby steps (replicated: n1 | N/2; flat: n1 | N)
   const bool full = (flat ? N % n1 : (N / 2) % n1) == 0 && n1 <= 256 && c->n % MAC_TPB == 0;
@@ -523,7 +524,7 @@ hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t 
 }
 
 hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1,
-                        int N, const std::vector<int32_t> &js, bool flat, uint32_t Q) {
+                        int N, const std::vector<int32_t> &js, bool flat, uint32_t Q, const DPack &dp) {
   if (js.empty() || A_loc == 0 || Q == 0) return HD_OK;
   const int jmin = js.front(), nj = (int)js.size();
   const size_t ls = (size_t)c->L * c->n, rq = (size_t)n1 * 2 * ls, sq = (size_t)A_loc * nj * 2 * ls;
@@ -532,12 +533,13 @@ hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uin
     const uint32_t gmax = g_env ? std::max(1, std::min(4, atoi(g_env))) : 4;
     for (uint32_t b0 = 0; b0 < Q;) {
       const uint32_t g = std::min(gmax, Q - b0);
-      hd_status s = mac_tma_run(c, D, r + b0 * rq, S + b0 * sq, A_loc, n1, N, js, g, flat);
+      hd_status s = mac_tma_run(c, D, r + b0 * rq, S + b0 * sq, A_loc, n1, N, js, g, flat, dp);
       if (s) return s;
       b0 += g;
     }
     return HD_OK;
   }
+  if (dp.on) return hd_fail(HD_E_STATE, "packed diagonals (R34) need the TMA MAC");
   const bool full = (flat ? N % n1 : (N / 2) % n1) == 0 && n1 <= 256 && c->n % MAC_TPB == 0;
   bool small_q = true;
   for (int l = 0; l < c->L; l++) small_q = small_q && c->mod[l] < (1ull << 60);
@@ -549,7 +551,7 @@ hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uin
   const char *g_env = getenv("HD_MAC_BATCH");
   if (!(full && small_q) || !g_env) {  // per-query kernels
     for (uint32_t b = 0; b < Q; b++) {
-      hd_status s = mac_run(c, D, r + b * rq, S + b * sq, A_loc, n1, N, js, flat);
+      hd_status s = mac_run(c, D, r + b * rq, S + b * sq, A_loc, n1, N, js, flat, dp);
       if (s) return s;
     }
     return HD_OK;

@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <type_traits>
 
 namespace {
 constexpr int TC = 128;  // coefficients per aggregate per unit (one per consumer thread)
@@ -95,6 +96,61 @@ __device__ __forceinline__ void acc_fold(Acc &A) {
   A.mid = 0;
 }
 
+// Karatsuba accumulation (R35).  With r = rl + rh 2^31 and d = dl + dh 2^31 (rl, dl < 2^31;
+// rh < 2^29 for residues below 2^60, dh < 2^16 for a packed narrow limb),
+//   r d = rl dl + ((rl + rh)(dl + dh) - rl dl - rh dh) 2^31 + rh dh 2^62,
+// and (rl + rh), (dl + dh) < 2^32.  The three products are summed over the baby steps
+// separately (the identity is linear) and combined once per unit: 2 IMAD.WIDE + 1 IMAD per
+// product for a narrow limb (rh dh < 2^32), 3 IMAD.WIDE for a wide one, against the 4
+// IMAD.WIDE of the schoolbook 32-bit split -- the MAC's compute is bound by that pipe.
+// Sums: s0 = sum rl dl and sm = sum (rl+rh)(dl+dh) as 64-bit words plus 32-bit carry counts
+// (< 2^71 for 128 terms), s2 = sum rh dh likewise (narrow: < 2^32 per term).
+struct KAcc {
+  uint64_t s0, sm, s2;
+  uint32_t c0, cm, c2;
+};
+template <bool NARROW>
+__device__ __forceinline__ void kmac(KAcc &A, uint32_t rl, uint32_t rh, uint32_t rs, uint32_t dl, uint32_t dh,
+                                     uint32_t ds) {
+  asm("{\n\t.reg .u64 t;\n\t"
+      "mul.wide.u32 t, %4, %6;\n\t"
+      "add.cc.u64 %0, %0, t;\n\t"
+      "addc.u32 %2, %2, 0;\n\t"
+      "mul.wide.u32 t, %5, %7;\n\t"
+      "add.cc.u64 %1, %1, t;\n\t"
+      "addc.u32 %3, %3, 0;\n\t"
+      "}"
+      : "+l"(A.s0), "+l"(A.sm), "+r"(A.c0), "+r"(A.cm)
+      : "r"(rl), "r"(rs), "r"(dl), "r"(ds));
+  if (NARROW) {
+    asm("{\n\t.reg .u32 l, h;\n\t"
+        "mov.b64 {l, h}, %0;\n\t"
+        "mad.lo.cc.u32 l, %1, %2, l;\n\t"
+        "addc.u32 h, h, 0;\n\t"
+        "mov.b64 %0, {l, h};\n\t"
+        "}"
+        : "+l"(A.s2)
+        : "r"(rh), "r"(dh));
+  } else {
+    asm("{\n\t.reg .u64 t;\n\t"
+        "mul.wide.u32 t, %2, %3;\n\t"
+        "add.cc.u64 %0, %0, t;\n\t"
+        "addc.u32 %1, %1, 0;\n\t"
+        "}"
+        : "+l"(A.s2), "+r"(A.c2)
+        : "r"(rh), "r"(dh));
+  }
+}
+// sum r d = s0 + (sm - s0 - s2) 2^31 + s2 2^62 (< 2^127 for 128 terms below 2^60) mod q
+__device__ __forceinline__ uint64_t kacc_reduce(const KAcc &A, uint64_t q, uint64_t bar, uint64_t r64,
+                                                uint64_t r64s) {
+  const unsigned __int128 x0 = ((unsigned __int128)A.c0 << 64) | A.s0;
+  const unsigned __int128 xm = ((unsigned __int128)A.cm << 64) | A.sm;
+  const unsigned __int128 x2 = ((unsigned __int128)A.c2 << 64) | A.s2;
+  const unsigned __int128 x = x0 + ((xm - x0 - x2) << 31) + (x2 << 62);
+  return reduce128((uint64_t)(x >> 64), (uint64_t)x, q, bar, r64, r64s);
+}
+
 struct Unit {
   uint32_t a0;       // first aggregate of the group
   int gg0, tile, m;  // first diagonal block, coefficient tile, limb
@@ -113,14 +169,22 @@ __device__ __forceinline__ Unit decode(uint32_t u, uint32_t nag, int ngrp, int t
 // AG aggregates x TC coefficients consumer threads + one producer warp.
 // Stage layout (u64): D[AG][JT][SPS][TC] (the 5-D box), then r[QB][SPS][2][TC].
 // flags (measurement only): 1 = stream without arithmetic, 2 = arithmetic without the stream.
+// Limb classes of packed diagonals (R34): cls 1 = narrow (u32 low + u16 high planes, maps tmLo /
+// tmHi), 0 = wide (u64, map tmD); idx = the limb's coordinate in its map.
+struct PackCls {
+  uint8_t cls[8], idx[8];
+};
+
 template <int AG, int JT, int QB, int SPS, bool FLUSH>
 __global__ void __launch_bounds__(AG *TC + 32, 1)
-    mac_tma_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmR,
+    mac_tma_kernel(const __grid_constant__ CUtensorMap tmD, const __grid_constant__ CUtensorMap tmLo,
+                   const __grid_constant__ CUtensorMap tmHi, const __grid_constant__ CUtensorMap tmR,
                    uint64_t *__restrict__ S, int n1, int N, int L, int logn, int nj, uint32_t A, int flat, int stages,
-                   int qrows, size_t s_query_stride, ModTab mt, int flags) {
+                   int qrows, size_t s_query_stride, ModTab mt, int flags, PackCls pk) {
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int D_WORDS = AG * JT * SPS * TC, R_WORDS = QB * SPS * 2 * TC;
   constexpr uint32_t STAGE_BYTES = (D_WORDS + R_WORDS) * 8;
+  constexpr uint32_t NARROW_STAGE_BYTES = D_WORDS * 6 + R_WORDS * 8;  // packed limb (R34)
   constexpr int CONSUMERS = AG * TC;
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + (size_t)stages * STAGE_BYTES);
   uint64_t *empty = full + stages;
@@ -144,11 +208,20 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
     uint32_t phase = 0;
     for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
       const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
+      const bool narrow = pk.cls[x.m];
+      const int mi = pk.idx[x.m];
       for (int sb = 0; sb < nsb; sb++) {
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
         uint64_t *base = reinterpret_cast<uint64_t *>(smem + (size_t)stage * STAGE_BYTES);
-        tma_load_5d(base, &tmD, x.tile * TC, x.m, sb * SPS, x.gg0, (int)x.a0, &full[stage], pol_stream);
+        if (!narrow) {
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_5d(base, &tmD, x.tile * TC, mi, sb * SPS, x.gg0, (int)x.a0, &full[stage], pol_stream);
+        } else {  // low plane (4 B per word) then high plane (2 B) in the stage's diagonal area
+          mbar_arrive_expect_tx(&full[stage], NARROW_STAGE_BYTES);
+          tma_load_5d(base, &tmLo, x.tile * TC, mi, sb * SPS, x.gg0, (int)x.a0, &full[stage], pol_stream);
+          tma_load_5d(reinterpret_cast<unsigned char *>(base) + 4 * D_WORDS, &tmHi, x.tile * TC, mi, sb * SPS, x.gg0,
+                      (int)x.a0, &full[stage], pol_stream);
+        }
 #pragma unroll
         for (int b = 0; b < QB; b++)
           tma_load_3d(base + D_WORDS + b * SPS * 2 * TC, &tmR, x.tile * TC, x.m, b * qrows + sb * SPS * 2,
@@ -168,40 +241,60 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
   uint32_t phase = 0;
   for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
     const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
+    const bool narrow = pk.cls[x.m];
     const uint64_t q = mt.q[x.m], bar = mt.bar[x.m], r64 = mt.r64[x.m], r64s = mt.r64s[x.m];
-    Acc acc[QB][JT][2];
+    KAcc acc[QB][JT][2];
     uint64_t part[QB][JT][2];
 #pragma unroll
     for (int b = 0; b < QB; b++)
 #pragma unroll
       for (int jj = 0; jj < JT; jj++) {
-        acc[b][jj][0] = acc[b][jj][1] = Acc{0, 0, 0, 0};
+        acc[b][jj][0] = acc[b][jj][1] = KAcc{0, 0, 0, 0, 0, 0};
         part[b][jj][0] = part[b][jj][1] = 0;
       }
     for (int sb = 0; sb < nsb; sb++) {
       if (!(flags & 2)) mbar_wait(&full[stage], phase);
       if (!(flags & 1)) {
-        const uint64_t *Ds =
-            reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + g * JT * SPS * TC + t;
-        const uint64_t *Rs = reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + D_WORDS + t;
+        const unsigned char *sbase = smem + (size_t)stage * STAGE_BYTES;
+        const uint64_t *Rs = reinterpret_cast<const uint64_t *>(sbase) + D_WORDS + t;
+        // one stage: the 31-bit halves of every diagonal word and of its baby step's two r
+        // words, three Karatsuba products per (word, r word)
+        auto consume = [&](auto narrow_tag) {
+          constexpr bool NARROW = decltype(narrow_tag)::value;
+          const uint64_t *Ds = reinterpret_cast<const uint64_t *>(sbase) + g * JT * SPS * TC + t;
+          const uint32_t *Dl = reinterpret_cast<const uint32_t *>(sbase) + g * JT * SPS * TC + t;
+          const uint16_t *Dh = reinterpret_cast<const uint16_t *>(sbase + 4 * D_WORDS) + g * JT * SPS * TC + t;
 #pragma unroll
-        for (int s = 0; s < SPS; s++) {
-          uint64_t d[JT];
-#pragma unroll
-          for (int jj = 0; jj < JT; jj++) d[jj] = Ds[(jj * SPS + s) * TC];
-#pragma unroll
-          for (int b = 0; b < QB; b++) {
-            const uint64_t r0 = Rs[(b * SPS * 2 + 2 * s) * TC], r1 = Rs[(b * SPS * 2 + 2 * s + 1) * TC];
-            const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1,
-                           r11 = (uint32_t)(r1 >> 32);
+          for (int s = 0; s < SPS; s++) {
+            uint32_t dl[JT], dh[JT], ds[JT];
 #pragma unroll
             for (int jj = 0; jj < JT; jj++) {
-              const uint32_t b0 = (uint32_t)d[jj], b1 = (uint32_t)(d[jj] >> 32);
-              acc_mac(acc[b][jj][0], r00, r01, b0, b1);
-              acc_mac(acc[b][jj][1], r10, r11, b0, b1);
+              if (NARROW) {  // stored split at bit 31 (R34)
+                dl[jj] = Dl[(jj * SPS + s) * TC];
+                dh[jj] = Dh[(jj * SPS + s) * TC];
+              } else {
+                const uint64_t d = Ds[(jj * SPS + s) * TC];
+                dl[jj] = (uint32_t)d & 0x7fffffffu;
+                dh[jj] = (uint32_t)(d >> 31);
+              }
+              ds[jj] = dl[jj] + dh[jj];
+            }
+#pragma unroll
+            for (int b = 0; b < QB; b++) {
+#pragma unroll
+              for (int p = 0; p < 2; p++) {
+                const uint64_t r = Rs[(b * SPS * 2 + 2 * s + p) * TC];
+                const uint32_t rl = (uint32_t)r & 0x7fffffffu, rh = (uint32_t)(r >> 31), rs = rl + rh;
+#pragma unroll
+                for (int jj = 0; jj < JT; jj++) kmac<NARROW>(acc[b][jj][p], rl, rh, rs, dl[jj], dh[jj], ds[jj]);
+              }
             }
           }
-        }
+        };
+        if (narrow)
+          consume(std::true_type{});
+        else
+          consume(std::false_type{});
       }
       // one arrival per warp once every lane's shared-memory reads of the stage are done
       __syncwarp();
@@ -210,15 +303,6 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
         stage = 0;
         phase ^= 1;
       }
-      if ((((sb + 1) * SPS) & 7) == 0) {  // every 8 baby steps: 16 mid terms < 2^64
-#pragma unroll
-        for (int b = 0; b < QB; b++)
-#pragma unroll
-          for (int jj = 0; jj < JT; jj++) {
-            acc_fold(acc[b][jj][0]);
-            acc_fold(acc[b][jj][1]);
-          }
-      }
       if (FLUSH && (sb % (128 / SPS)) == (128 / SPS) - 1) {  // n1 > 128: bank every 128 terms
 #pragma unroll
         for (int b = 0; b < QB; b++)
@@ -226,10 +310,8 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
           for (int jj = 0; jj < JT; jj++)
 #pragma unroll
             for (int p = 0; p < 2; p++) {
-              Acc &X = acc[b][jj][p];
-              acc_fold(X);
-              part[b][jj][p] = addmod(part[b][jj][p], reduce128(X.hi + X.cnt, X.lo, q, bar, r64, r64s), q);
-              X = Acc{0, 0, 0, 0};
+              part[b][jj][p] = addmod(part[b][jj][p], kacc_reduce(acc[b][jj][p], q, bar, r64, r64s), q);
+              acc[b][jj][p] = KAcc{0, 0, 0, 0, 0, 0};
             }
       }
     }
@@ -246,11 +328,8 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
         uint64_t *Sa = S + b * s_query_stride + ((size_t)a * nj + jslot) * 2 * ls + (size_t)x.m * n +
                        (size_t)x.tile * TC + t;
 #pragma unroll
-        for (int p = 0; p < 2; p++) {
-          Acc &X = acc[b][jj][p];
-          acc_fold(X);
-          Sa[(size_t)p * ls] = addmod(part[b][jj][p], reduce128(X.hi + X.cnt, X.lo, q, bar, r64, r64s), q);
-        }
+        for (int p = 0; p < 2; p++)
+          Sa[(size_t)p * ls] = addmod(part[b][jj][p], kacc_reduce(acc[b][jj][p], q, bar, r64, r64s), q);
       }
     }
   }
@@ -398,22 +477,31 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-hd_status encode(CUtensorMap *map, const uint64_t *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides,
-                 const cuuint32_t *box) {
+hd_status encode_t(CUtensorMap *map, const void *base, CUtensorMapDataType dt, int rank, const cuuint64_t *dims,
+                   const cuuint64_t *strides, const cuuint32_t *box) {
   auto fn = encode_fn();
   if (!fn) return hd_fail(HD_E_CUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT64, (cuuint32_t)rank, const_cast<uint64_t *>(base), dims, strides,
+  CUresult r = fn(map, dt, (cuuint32_t)rank, const_cast<void *>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return hd_fail(HD_E_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
   return HD_OK;
 }
+hd_status encode(CUtensorMap *map, const uint64_t *base, int rank, const cuuint64_t *dims, const cuuint64_t *strides,
+                 const cuuint32_t *box) {
+  return encode_t(map, base, CU_TENSOR_MAP_DATA_TYPE_UINT64, rank, dims, strides, box);
+}
 
 int g_num_sms = 0;
 
+struct DMaps {  // the diagonal maps of one launch (R34)
+  CUtensorMap w, lo, hi;
+  PackCls pk;
+};
+
 template <int AG, int JT, int QB, int SPS, bool FLUSH>
-hd_status launch(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int nj,
+hd_status launch(hd_context *c, const DMaps &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int nj,
                  uint32_t A, bool flat, int qrows, size_t sq) {
   constexpr size_t STAGE_BYTES = (size_t)(AG * JT * SPS * TC + QB * SPS * 2 * TC) * 8;
   const size_t budget = 227 * 1024 - 256;
@@ -428,15 +516,15 @@ hd_status launch(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, ui
   const uint32_t grid = std::min<uint32_t>(units, (uint32_t)g_num_sms);
   const char *dry = getenv("HD_MAC_TMA_DRY"), *co = getenv("HD_MAC_COMPUTE_ONLY");  // measurement only
   const int flags = (dry && dry[0] == '1' ? 1 : 0) | (co && co[0] == '1' ? 2 : 0);
-  kern<<<grid, AG * TC + 32, smem, c->stream>>>(mD, mR, S, n1, N, c->L, c->logn, nj, A, flat ? 1 : 0, stages, qrows,
-                                                sq, c->mt, flags);
+  kern<<<grid, AG * TC + 32, smem, c->stream>>>(mD.w, mD.lo, mD.hi, mR, S, n1, N, c->L, c->logn, nj, A, flat ? 1 : 0,
+                                                stages, qrows, sq, c->mt, flags, mD.pk);
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;
 }
 
 template <int JT, int QB>
-hd_status launch_f(hd_context *c, const CUtensorMap &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int nj,
+hd_status launch_f(hd_context *c, const DMaps &mD, const CUtensorMap &mR, uint64_t *S, int n1, int N, int nj,
                    uint32_t A, bool flat, int qrows, size_t sq, int ag, int sps) {
 #define HD_MAC_L(AG_, SPS_)                                                                        \
   return n1 > 128 ? launch<AG_, JT, QB, SPS_, true>(c, mD, mR, S, n1, N, nj, A, flat, qrows, sq) \
@@ -530,7 +618,7 @@ bool mac_tma_supported(const hd_context *c, int n1, int N, bool flat, uint32_t Q
 
 // S [Q][A][nj][2][L][n]; r [Q][n1][2][L][n] (query stride n1 2 L n); D [A][N][L][n].
 hd_status mac_tma_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A, int n1, int N,
-                      const std::vector<int32_t> &js, uint32_t Q, bool flat) {
+                      const std::vector<int32_t> &js, uint32_t Q, bool flat, const DPack &dp) {
   if (js.empty() || A == 0) return HD_OK;
   const int nj = (int)js.size(), G = N / n1;
   if (nj != G) return hd_fail(HD_E_STATE, "TMA MAC expects one giant step per diagonal block");
@@ -548,14 +636,30 @@ hd_status mac_tma_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint6
   const int jt = nj % 4 == 0 ? 4 : (nj % 2 == 0 ? 2 : 1);
   const int jtq = Q == 1 ? jt : (Q == 2 ? std::min(jt, 2) : 1);  // QB x JT <= 4 accumulator pairs
   const int L = c->L, n = c->n;
-  CUtensorMap mD, mR;
+  DMaps mD;
+  CUtensorMap mR;
   hd_status s;
-  {  // D: (coefficient, limb, diagonal within block, block, aggregate)
-    const cuuint64_t dims[5] = {(cuuint64_t)n, (cuuint64_t)L, (cuuint64_t)n1, (cuuint64_t)G, (cuuint64_t)A};
-    const cuuint64_t strides[4] = {(cuuint64_t)n * 8, (cuuint64_t)L * n * 8, (cuuint64_t)n1 * L * n * 8,
-                                   (cuuint64_t)N * L * n * 8};
+  {  // D: (coefficient, limb, diagonal within block, block, aggregate); packed (R34): the wide
+     // limbs as u64 words, the narrow limbs' low / high planes as u32 / u16 (same box, 6 B per word)
+    const size_t db = dp.on ? dp.diag_bytes : (size_t)L * n * 8;  // bytes of one diagonal
+    const int W = dp.on ? dp.W : L, R = dp.on ? dp.R : 0;
     const cuuint32_t box[5] = {(cuuint32_t)TC, 1, (cuuint32_t)sps, (cuuint32_t)jtq, (cuuint32_t)ag};
-    if ((s = encode(&mD, D, 5, dims, strides, box))) return s;
+    auto enc_plane = [&](CUtensorMap *m, const uint8_t *base, int count, int esize, CUtensorMapDataType dt) {
+      const cuuint64_t dims[5] = {(cuuint64_t)n, (cuuint64_t)std::max(1, count), (cuuint64_t)n1, (cuuint64_t)G,
+                                  (cuuint64_t)A};
+      const cuuint64_t strides[4] = {(cuuint64_t)n * esize, (cuuint64_t)db, (cuuint64_t)n1 * db, (cuuint64_t)N * db};
+      return encode_t(m, base, dt, 5, dims, strides, box);
+    };
+    const uint8_t *Db = reinterpret_cast<const uint8_t *>(D);
+    if ((s = enc_plane(&mD.w, Db, W, 8, CU_TENSOR_MAP_DATA_TYPE_UINT64))) return s;
+    if ((s = enc_plane(&mD.lo, Db + 8 * (size_t)W * n, R, 4, CU_TENSOR_MAP_DATA_TYPE_UINT32))) return s;
+    if ((s = enc_plane(&mD.hi, Db + (8 * (size_t)W + 4 * (size_t)R) * n, R, 2, CU_TENSOR_MAP_DATA_TYPE_UINT16)))
+      return s;
+    for (int l = 0; l < 8; l++) {
+      mD.pk.cls[l] = l < L && dp.on ? dp.cls[l] : 0;
+      mD.pk.idx[l] = l < L ? (dp.on ? dp.idx[l] : (uint8_t)l) : 0;
+    }
+    if (L > 8) return hd_fail(HD_E_PARAMS, "TMA MAC: more than 8 limbs");
   }
   {  // r: (coefficient, limb, row = (query, baby step, poly))
     const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)L, (cuuint64_t)Q * 2 * n1};

@@ -146,10 +146,10 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, 
   range_query.pop();
   range_query.push("mac");
   if (Q > 1) {
-    if ((s = mac_batch_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat, Q))) return s;
+    if ((s = mac_batch_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat, Q, db->dp))) return s;
   } else if (db->encrypted) {
     if ((s = mac_ct_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat))) return s;
-  } else if ((s = mac_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat))) {
+  } else if ((s = mac_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat, db->dp))) {
     return s;
   }
   cudaEventRecord(E[2], sa);
@@ -551,6 +551,16 @@ extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t ag
     case 4:
       if (index < 0 || index >= (int)db->N) return hd_fail(HD_E_INVALID_ARG, "diagonal index");
       len = (db->encrypted ? 2 : 1) * ptL;  // plaintext, or the diagonal ciphertext
+      if (db->dp.on) {  // packed (R34): copy the diagonal's bytes, unpack on the host
+        if (cap < len) return hd_fail(HD_E_INVALID_ARG, "capacity too small");
+        std::vector<uint8_t> buf(db->dp.diag_bytes);
+        HD_CUDA(cudaStreamSynchronize(c->stream));
+        HD_CUDA(cudaMemcpy(buf.data(), reinterpret_cast<const uint8_t *>(db->D) + (a * db->N + index) * db->dp.diag_bytes,
+                           buf.size(), cudaMemcpyDeviceToHost));
+        for (int l = 0; l < L; l++)
+          for (int t = 0; t < n; t++) host_dst[(size_t)l * n + t] = dp_get(buf.data(), db->dp, l, t, n);
+        return HD_OK;
+      }
       src = db->D + (a * db->N + index) * len;
       break;
     default:
@@ -564,6 +574,8 @@ extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t ag
 }
 
 __global__ void xor_word_kernel(uint64_t *p, uint64_t mask) { *p ^= mask; }
+__global__ void xor_u32_kernel(uint32_t *p, uint32_t mask) { *p ^= mask; }
+__global__ void xor_u16_kernel(uint16_t *p, uint16_t mask) { *p ^= mask; }
 
 extern "C" hd_status hd_test_inject(hd_database *db, uint32_t agg, int32_t k, uint64_t word, uint64_t mask) {
   if (!db) return hd_fail(HD_E_INVALID_ARG, "null database");
@@ -571,10 +583,29 @@ extern "C" hd_status hd_test_inject(hd_database *db, uint32_t agg, int32_t k, ui
   const size_t dw = (db->encrypted ? 2 : 1) * (size_t)c->L * c->n;  // words of one diagonal
   if (agg < db->lay.agg_begin || agg >= db->lay.agg_end || k < 0 || k >= (int)db->N || word >= dw)
     return hd_fail(HD_E_INVALID_ARG, "fault position outside the database");
-  uint64_t *p = db->D + ((size_t)(agg - db->lay.agg_begin) * db->N + k) * dw + word;
+  const size_t diag = (size_t)(agg - db->lay.agg_begin) * db->N + k;
   HD_CUDA(cudaStreamSynchronize(c->stream));
   hd_context_synchronize(c);
-  xor_word_kernel<<<1, 1, 0, c->stream>>>(p, mask);
+  if (db->dp.on) {  // packed (R34): the limb's u64 word, or its low (u32) and high (u16) parts
+    const int l = (int)(word / c->n);
+    const size_t t = word % c->n;
+    uint8_t *dg = reinterpret_cast<uint8_t *>(db->D) + diag * db->dp.diag_bytes;
+    if (!db->dp.cls[l]) {
+      xor_word_kernel<<<1, 1, 0, c->stream>>>(reinterpret_cast<uint64_t *>(dg) + (size_t)db->dp.idx[l] * c->n + t, mask);
+    } else {
+      if (mask >> 47) return hd_fail(HD_E_INVALID_ARG, "mask beyond the 47 bits of a packed residue");
+      xor_u32_kernel<<<1, 1, 0, c->stream>>>(
+          reinterpret_cast<uint32_t *>(dg + 8 * (size_t)db->dp.W * c->n) + (size_t)db->dp.idx[l] * c->n + t,
+          (uint32_t)(mask & 0x7fffffffu));
+      xor_u16_kernel<<<1, 1, 0, c->stream>>>(
+          reinterpret_cast<uint16_t *>(dg + (8 * (size_t)db->dp.W + 4 * (size_t)db->dp.R) * c->n) +
+              (size_t)db->dp.idx[l] * c->n + t,
+          (uint16_t)(mask >> 31));
+      ++c->launches;
+    }
+  } else {
+    xor_word_kernel<<<1, 1, 0, c->stream>>>(db->D + diag * dw + word, mask);
+  }
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   HD_CUDA(cudaStreamSynchronize(c->stream));
