@@ -164,6 +164,61 @@ __global__ void __launch_bounds__(TPB) kip_giant_kernel(uint64_t *__restrict__ u
   *reinterpret_cast<ulonglong2 *>(u + ((size_t)(b * 2 + 1) * (ell + 1) + e) * n + t) = v1;
 }
 
+// The same sum with (J, ell) known at compile time and one coefficient per thread: every
+// Galois-gathered digit word and key word of the J rotations is loaded before the first
+// product (the gathers are scattered; the generic kernel above waits on each in turn at two
+// CTAs per SM and ran at 2.3 TB/s, long_scoreboard 4.5 stalls per issue).
+template <int J, int ELL>
+__global__ void __launch_bounds__(TPB) kip_giant1_kernel(uint64_t *__restrict__ u, int L, int logn,
+                                                         const uint64_t *const *__restrict__ kptr,
+                                                         const uint32_t *__restrict__ gal, ModTab mt, KipAcc ka,
+                                                         GiantSet gs) {
+  const int n = 1 << logn;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t b = blockIdx.y / (ELL + 1), e = blockIdx.y % (ELL + 1);
+  if (t >= (uint32_t)n) return;
+  const int gm = (int)e < ELL ? (int)e : L;
+  const uint64_t q = mt.q[gm], bar = mt.bar[gm], r64 = mt.r64[gm], r64s = mt.r64s[gm];
+  uint64_t v[J][ELL], k0[J][ELL], k1[J][ELL], cz[J];
+#pragma unroll
+  for (int jj = 0; jj < J; jj++) {
+    const uint32_t s = galois_src(t, gal[gs.slot[jj]], logn);
+    const uint64_t *key = kptr[gs.slot[jj]];
+    const uint64_t *dg = gs.dig[jj] + (size_t)b * ELL * ELL * n;
+    const uint64_t *cb = gs.ct[jj] + (size_t)b * gs.ct_stride;  // c0 rows [0, ell), c1 rows [ell, 2 ell)
+#pragma unroll
+    for (int d = 0; d < ELL; d++) {
+      const uint64_t *row = ((int)e == d) ? cb + (size_t)(ELL + d) * n
+                                          : dg + ((size_t)d * ELL + ((int)e < d ? (int)e : (int)e - 1)) * n;
+      v[jj][d] = row[s];
+      k0[jj][d] = __ldg(key + ((size_t)(d * 2 + 0) * (L + 1) + gm) * n + t);
+      k1[jj][d] = __ldg(key + ((size_t)(d * 2 + 1) * (L + 1) + gm) * n + t);
+    }
+    cz[jj] = (int)e < ELL ? cb[(size_t)e * n + s] : 0;
+  }
+  uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0, c0 = 0;
+#pragma unroll
+  for (int jj = 0; jj < J; jj++) {
+#pragma unroll
+    for (int d = 0; d < ELL; d++) {
+      mac128(a0l, a0h, v[jj][d], k0[jj][d]);
+      mac128(a1l, a1h, v[jj][d], k1[jj][d]);
+    }
+    c0 = addmod(c0, cz[jj], q);
+  }
+  uint64_t o0 = reduce128(a0h, a0l, q, bar, r64, r64s), o1 = reduce128(a1h, a1l, q, bar, r64, r64s);
+  if ((int)e < ELL) {
+    const uint64_t pw = ka.pw[e], pws = ka.pws[e];
+    if (gs.t0) {  // + P T0 (both polys)
+      c0 = addmod(c0, gs.t0[(size_t)b * gs.ct_stride + (size_t)e * n + t], q);
+      o1 = addmod(o1, shoup(gs.t0[(size_t)b * gs.ct_stride + (size_t)(ELL + e) * n + t], pw, pws, q), q);
+    }
+    o0 = addmod(o0, shoup(c0, pw, pws, q), q);
+  }
+  u[((size_t)(b * 2 + 0) * (ELL + 1) + e) * n + t] = o0;
+  u[((size_t)(b * 2 + 1) * (ELL + 1) + e) * n + t] = o1;
+}
+
 // dst[b][p][e] += P src[b][p][e] for e < ell (the P limb of P src is 0): a giant step
 // without rotation, in the extended basis (R23).  dst rows [b][p][ell+1][n], src [b][p][ell][n].
 __global__ void add_pscaled_kernel(uint64_t *__restrict__ dst, size_t dst_stride, const uint64_t *__restrict__ src,
@@ -460,9 +515,19 @@ hd_status ks_giant_sum(hd_context *c, uint32_t B, int ell, int J, const uint64_t
   }
   gs.t0 = t0;
   gs.ct_stride = ct_stride;
+  const KipAcc ka = kip_acc(c, ell, nullptr, 0);
+  const dim3 g1((c->n + TPB - 1) / TPB, B * (ell + 1));
+#define HD_KG(J_, E_)                                                                                          \
+  if (J == J_ && ell == E_) {                                                                                  \
+    kip_giant1_kernel<J_, E_><<<g1, TPB, 0, c->stream>>>(u, c->L, c->logn, kptr_dev, gal_dev, c->mt, ka, gs); \
+    ++c->launches;                                                                                             \
+    HD_CUDA(cudaGetLastError());                                                                               \
+    return HD_OK;                                                                                              \
+  }
+  HD_KG(1, 1) HD_KG(1, 2) HD_KG(2, 1) HD_KG(2, 2) HD_KG(3, 1) HD_KG(3, 2) HD_KG(3, 3) HD_KG(1, 3) HD_KG(2, 3)
+#undef HD_KG
   kip_giant_kernel<<<grid_pairs(c->n, B * (ell + 1)), TPB, 0, c->stream>>>(u, ell, c->L, c->logn, kptr_dev, gal_dev,
-                                                                          c->mt, kip_acc(c, ell, nullptr, 0), gs,
-                                                                          fdiv_make(ell + 1));
+                                                                          c->mt, ka, gs, fdiv_make(ell + 1));
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;

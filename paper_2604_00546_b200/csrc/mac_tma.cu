@@ -172,7 +172,7 @@ __device__ __forceinline__ Unit decode(uint32_t u, uint32_t nag, int ngrp, int t
 // Limb classes of packed diagonals (R34): cls 1 = narrow (u32 low + u16 high planes, maps tmLo /
 // tmHi), 0 = wide (u64, map tmD); idx = the limb's coordinate in its map.
 struct PackCls {
-  uint8_t cls[8], idx[8];
+  uint8_t cls[HD_MAXMOD], idx[HD_MAXMOD];
 };
 
 template <int AG, int JT, int QB, int SPS, bool FLUSH>
@@ -655,11 +655,10 @@ hd_status mac_tma_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint6
     if ((s = enc_plane(&mD.lo, Db + 8 * (size_t)W * n, R, 4, CU_TENSOR_MAP_DATA_TYPE_UINT32))) return s;
     if ((s = enc_plane(&mD.hi, Db + (8 * (size_t)W + 4 * (size_t)R) * n, R, 2, CU_TENSOR_MAP_DATA_TYPE_UINT16)))
       return s;
-    for (int l = 0; l < 8; l++) {
+    for (int l = 0; l < HD_MAXMOD; l++) {
       mD.pk.cls[l] = l < L && dp.on ? dp.cls[l] : 0;
       mD.pk.idx[l] = l < L ? (dp.on ? dp.idx[l] : (uint8_t)l) : 0;
     }
-    if (L > 8) return hd_fail(HD_E_PARAMS, "TMA MAC: more than 8 limbs");
   }
   {  // r: (coefficient, limb, row = (query, baby step, poly))
     const cuuint64_t dims[3] = {(cuuint64_t)n, (cuuint64_t)L, (cuuint64_t)Q * 2 * n1};

@@ -43,10 +43,46 @@ __device__ __forceinline__ uint64_t q_chain(uint64_t a, uint64_t s) {
   return ((uint64_t)h1 << 32) | h0;
 }
 
+
+// V4: the whole lazy Shoup product in 32-bit PTX (exact quotient, carries on add.cc/addc)
+__device__ __forceinline__ uint64_t mul_v4(uint64_t a, uint64_t w, uint64_t ws, uint64_t q) {
+  uint32_t r0, r1;
+  asm("{\n\t.reg .u32 a0, a1, s0, s1, w0, w1, q0, q1, t, m0, m1, m2, h0, h1, p0, p1, x0, x1;\n\t"
+      "mov.b64 {a0, a1}, %2;\n\t"
+      "mov.b64 {s0, s1}, %4;\n\t"
+      "mov.b64 {w0, w1}, %3;\n\t"
+      "mov.b64 {q0, q1}, %5;\n\t"
+      // h = umulhi(a, ws)
+      "mul.hi.u32 t, a0, s0;\n\t"
+      "mad.lo.cc.u32 m0, a0, s1, t;\n\t"
+      "madc.hi.u32 m1, a0, s1, 0;\n\t"
+      "mad.lo.cc.u32 m0, a1, s0, m0;\n\t"
+      "madc.hi.cc.u32 m1, a1, s0, m1;\n\t"
+      "addc.u32 m2, 0, 0;\n\t"
+      "mad.lo.cc.u32 h0, a1, s1, m1;\n\t"
+      "madc.hi.u32 h1, a1, s1, m2;\n\t"
+      // p = a * w mod 2^64
+      "mul.lo.u32 p0, a0, w0;\n\t"
+      "mul.hi.u32 p1, a0, w0;\n\t"
+      "mad.lo.u32 p1, a0, w1, p1;\n\t"
+      "mad.lo.u32 p1, a1, w0, p1;\n\t"
+      // x = h * q mod 2^64
+      "mul.lo.u32 x0, h0, q0;\n\t"
+      "mul.hi.u32 x1, h0, q0;\n\t"
+      "mad.lo.u32 x1, h0, q1, x1;\n\t"
+      "mad.lo.u32 x1, h1, q0, x1;\n\t"
+      "sub.cc.u32 %0, p0, x0;\n\t"
+      "subc.u32 %1, p1, x1;\n\t"
+      "}"
+      : "=r"(r0), "=r"(r1) : "l"(a), "l"(w), "l"(ws), "l"(q));
+  return ((uint64_t)r1 << 32) | r0;
+}
+
 template <int V>
 __device__ __forceinline__ uint64_t mulw(uint64_t a, uint64_t w, uint64_t ws, uint64_t q, uint64_t two_q) {
   if (V == 0) return a * w - q_exact(a, ws) * q;
   if (V == 2) return a * w - q_chain(a, ws) * q;
+  if (V == 4) return mul_v4(a, w, ws, q);
   uint64_t t = a * w - q_trunc(a, ws) * q;  // [0, 4q)
   return t >= two_q ? t - two_q : t;
 }
@@ -167,13 +203,14 @@ int main() {
       t.y = (uint64_t)(((unsigned __int128)t.x << 64) / q);
     }
     cudaMemcpy(tw, T.data(), T.size() * 16, cudaMemcpyHostToDevice);
-    std::vector<uint64_t> H(N), R[3];
+    std::vector<uint64_t> H(N), R[5];
     for (auto &h : H) h = g() % q;
     for (int inv = 0; inv < 2; inv++) {
-      for (int V = 0; V < 3; V++) {
+      for (int V = 0; V < 5; V++) {
+        if (V == 3) continue;
         cudaMemcpy(d, H.data(), N * 8, cudaMemcpyHostToDevice);
-        auto kern = inv ? (V == 0 ? k<0, true> : V == 1 ? k<1, true> : k<2, true>)
-                        : (V == 0 ? k<0, false> : V == 1 ? k<1, false> : k<2, false>);
+        auto kern = inv ? (V == 0 ? k<0, true> : V == 1 ? k<1, true> : V == 2 ? k<2, true> : k<4, true>)
+                        : (V == 0 ? k<0, false> : V == 1 ? k<1, false> : V == 2 ? k<2, false> : k<4, false>);
         kern<<<blocks, 256>>>(d, tw, q, 1);  // warm
         cudaMemcpy(d, H.data(), N * 8, cudaMemcpyHostToDevice);
         cudaEvent_t a, b;
