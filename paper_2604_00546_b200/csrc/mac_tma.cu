@@ -71,31 +71,6 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, i
       : "memory");
 }
 
-// carry-save 64x64 multiply-accumulate, as mac.cu (a1, b1 < 2^28): value = lo + mid 2^32 +
-// (hi + cnt) 2^64; mid folded every 8 products
-struct Acc {
-  uint64_t lo, mid, hi;
-  uint32_t cnt;
-};
-__device__ __forceinline__ void acc_mac(Acc &A, uint32_t a0, uint32_t a1, uint32_t b0, uint32_t b1) {
-  asm("{\n\t.reg .u64 t;\n\t"
-      "mul.wide.u32 t, %4, %6;\n\t"
-      "add.cc.u64 %0, %0, t;\n\t"
-      "addc.u32 %3, %3, 0;\n\t"
-      "mad.wide.u32 %1, %4, %7, %1;\n\t"
-      "mad.wide.u32 %1, %5, %6, %1;\n\t"
-      "mad.wide.u32 %2, %5, %7, %2;\n\t"
-      "}"
-      : "+l"(A.lo), "+l"(A.mid), "+l"(A.hi), "+r"(A.cnt)
-      : "r"(a0), "r"(a1), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void acc_fold(Acc &A) {
-  const uint64_t ml = A.mid << 32, mh = A.mid >> 32;
-  asm("add.cc.u64 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+l"(A.lo), "+r"(A.cnt) : "l"(ml));
-  A.hi += mh;
-  A.mid = 0;
-}
-
 // Karatsuba accumulation (R35).  With r = rl + rh 2^31 and d = dl + dh 2^31 (rl, dl < 2^31;
 // rh < 2^29 for residues below 2^60, dh < 2^16 for a packed narrow limb),
 //   r d = rl dl + ((rl + rh)(dl + dh) - rl dl - rh dh) 2^31 + rh dh 2^62,
@@ -349,7 +324,7 @@ template <int AG, int JT, int SPS>
 __global__ void __launch_bounds__(AG *TC + 32, 1)
     mac_tma_ct_kernel(const __grid_constant__ CtMaps tmD, const __grid_constant__ CUtensorMap tmR,
                       uint64_t *__restrict__ S, int n1, int N, int L, int logn, int nj, uint32_t A, int flat,
-                      int stages, ModTab mt) {
+                      int stages, ModTab mt, uint32_t small_mask) {
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int D_WORDS = AG * JT * SPS * 2 * TC, R_WORDS = SPS * 2 * TC;
   constexpr uint32_t STAGE_BYTES = (D_WORDS + R_WORDS) * 8;
@@ -395,13 +370,15 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
   for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
     const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
     const uint64_t q = mt.q[x.m], bar = mt.bar[x.m], r64 = mt.r64[x.m], r64s = mt.r64s[x.m];
-    Acc acc[JT][3];
+    // Karatsuba sums (R35); limbs below 2^47 take the narrow form (r_h d_h < 2^32)
+    const bool small = (small_mask >> x.m) & 1u;
+    KAcc acc[JT][3];
     uint64_t part[JT][3];
 #pragma unroll
     for (int jj = 0; jj < JT; jj++)
 #pragma unroll
       for (int e = 0; e < 3; e++) {
-        acc[jj][e] = Acc{0, 0, 0, 0};
+        acc[jj][e] = KAcc{0, 0, 0, 0, 0, 0};
         part[jj][e] = 0;
       }
     for (int sb = 0; sb < nsb; sb++) {
@@ -410,41 +387,42 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
       const uint64_t *Ds =
           reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + g * JT * SPS * 2 * TC + t;
       const uint64_t *Rs = reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + D_WORDS + t;
+      auto consume = [&](auto small_tag) {
+        constexpr bool SMALL = decltype(small_tag)::value;
 #pragma unroll
-      for (int s = 0; s < SPS; s++) {
-        const uint64_t r0 = Rs[(2 * s) * TC], r1 = Rs[(2 * s + 1) * TC];
-        const uint32_t r00 = (uint32_t)r0, r01 = (uint32_t)(r0 >> 32), r10 = (uint32_t)r1, r11 = (uint32_t)(r1 >> 32);
+        for (int s = 0; s < SPS; s++) {
+          const uint64_t r0 = Rs[(2 * s) * TC], r1 = Rs[(2 * s + 1) * TC];
+          const uint32_t r0l = (uint32_t)r0 & 0x7fffffffu, r0h = (uint32_t)(r0 >> 31), r0s = r0l + r0h;
+          const uint32_t r1l = (uint32_t)r1 & 0x7fffffffu, r1h = (uint32_t)(r1 >> 31), r1s = r1l + r1h;
 #pragma unroll
-        for (int jj = 0; jj < JT; jj++) {
-          const uint64_t d0 = Ds[((jj * SPS + s) * 2 + 0) * TC], d1 = Ds[((jj * SPS + s) * 2 + 1) * TC];
-          const uint32_t a00 = (uint32_t)d0, a01 = (uint32_t)(d0 >> 32), a10 = (uint32_t)d1, a11 = (uint32_t)(d1 >> 32);
-          acc_mac(acc[jj][0], r00, r01, a00, a01);
-          acc_mac(acc[jj][1], r00, r01, a10, a11);
-          acc_mac(acc[jj][1], r10, r11, a00, a01);
-          acc_mac(acc[jj][2], r10, r11, a10, a11);
+          for (int jj = 0; jj < JT; jj++) {
+            const uint64_t d0 = Ds[((jj * SPS + s) * 2 + 0) * TC], d1 = Ds[((jj * SPS + s) * 2 + 1) * TC];
+            const uint32_t a0l = (uint32_t)d0 & 0x7fffffffu, a0h = (uint32_t)(d0 >> 31), a0s = a0l + a0h;
+            const uint32_t a1l = (uint32_t)d1 & 0x7fffffffu, a1h = (uint32_t)(d1 >> 31), a1s = a1l + a1h;
+            kmac<SMALL>(acc[jj][0], r0l, r0h, r0s, a0l, a0h, a0s);  // d0 += r0 D0
+            kmac<SMALL>(acc[jj][1], r0l, r0h, r0s, a1l, a1h, a1s);  // d1 += r0 D1 + r1 D0
+            kmac<SMALL>(acc[jj][1], r1l, r1h, r1s, a0l, a0h, a0s);
+            kmac<SMALL>(acc[jj][2], r1l, r1h, r1s, a1l, a1h, a1s);  // d2 += r1 D1
+          }
         }
-        if (((sb * SPS + s) & 3) == 3) {  // d1: 4 mid terms per step -> fold every 4 steps (16 < 2^64)
-#pragma unroll
-          for (int jj = 0; jj < JT; jj++)
-#pragma unroll
-            for (int e = 0; e < 3; e++) acc_fold(acc[jj][e]);
-        }
-      }
+      };
+      if (small)
+        consume(std::true_type{});
+      else
+        consume(std::false_type{});
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[stage]);
       if (++stage == stages) {
         stage = 0;
         phase ^= 1;
       }
-      if ((((sb + 1) * SPS) & 63) == 0) {  // bank every 64 baby steps
+      if ((((sb + 1) * SPS) & 63) == 0) {  // bank every 64 baby steps (d1: 128 products)
 #pragma unroll
         for (int jj = 0; jj < JT; jj++)
 #pragma unroll
           for (int e = 0; e < 3; e++) {
-            Acc &X = acc[jj][e];
-            acc_fold(X);
-            part[jj][e] = addmod(part[jj][e], reduce128(X.hi + X.cnt, X.lo, q, bar, r64, r64s), q);
-            X = Acc{0, 0, 0, 0};
+            part[jj][e] = addmod(part[jj][e], kacc_reduce(acc[jj][e], q, bar, r64, r64s), q);
+            acc[jj][e] = KAcc{0, 0, 0, 0, 0, 0};
           }
       }
     }
@@ -456,11 +434,7 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
       const int jslot = flat ? gg : (gg < G / 2 ? gg + G / 2 : gg - G / 2);
       uint64_t *Sa = S + ((size_t)a * nj + jslot) * 3 * ls + (size_t)x.m * n + (size_t)x.tile * TC + t;
 #pragma unroll
-      for (int e = 0; e < 3; e++) {
-        Acc &X = acc[jj][e];
-        acc_fold(X);
-        Sa[(size_t)e * ls] = addmod(part[jj][e], reduce128(X.hi + X.cnt, X.lo, q, bar, r64, r64s), q);
-      }
+      for (int e = 0; e < 3; e++) Sa[(size_t)e * ls] = addmod(part[jj][e], kacc_reduce(acc[jj][e], q, bar, r64, r64s), q);
     }
   }
 }
@@ -554,7 +528,11 @@ hd_status launch_ct(hd_context *c, const CtMaps &mD, const CUtensorMap &mR, uint
   if (!g_num_sms) HD_CUDA(cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, c->device));
   const uint32_t units = (A / AG) * (uint32_t)(nj / JT) * (uint32_t)(c->n / TC) * (uint32_t)c->L;
   const uint32_t grid = std::min<uint32_t>(units, (uint32_t)g_num_sms);
-  kern<<<grid, AG * TC + 32, smem, c->stream>>>(mD, mR, S, n1, N, c->L, c->logn, nj, A, flat ? 1 : 0, stages, c->mt);
+  uint32_t small_mask = 0;  // limbs whose residues stay below 2^47 (Karatsuba narrow form, R35)
+  for (int l = 0; l < c->L && l < 32; l++)
+    if (c->mod[l] < kNarrowBound) small_mask |= 1u << l;
+  kern<<<grid, AG * TC + 32, smem, c->stream>>>(mD, mR, S, n1, N, c->L, c->logn, nj, A, flat ? 1 : 0, stages, c->mt,
+                                                small_mask);
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;

@@ -762,11 +762,22 @@ hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &ma
   }
   // Rows by kind (R33): the map's modulus pattern repeats every mdiv * mlen rows; the positions
   // of FP64 rows (modulus < 2^46) and of integer rows within one period go to separate launches.
-  // A map with a longer period runs every row on the integer kernels.
+  // A map with a longer period runs every row on the integer kernels, and so does a small
+  // batch (below HD_NTT_SPLIT_MIN rows, default 96): there the second launch pair costs more
+  // than the FP64 butterflies save (launch-bound; C2's query 1.04 -> 1.29 ms when split).
   RowSel sel[2];
   const uint32_t period = map.mdiv * map.mlen;
   bool any[2] = {false, false};
+  static const uint32_t split_min = [] {
+    const char *e = getenv("HD_NTT_SPLIT_MIN");
+    return e ? (uint32_t)atol(e) : 96u;
+  }();
+  bool one_kind_fp = false;  // every row of the map has a modulus below 2^46
   if (twd && period <= 64) {
+    one_kind_fp = true;
+    for (uint32_t p = 0; p < period; p++) one_kind_fp &= c->mod[map.midx[(p / map.mdiv) % map.mlen]] < kNttFp64Bound;
+  }
+  if (twd && period <= 64 && (rows >= split_min || one_kind_fp)) {
     for (int k = 0; k < 2; k++) {
       sel[k].period = period;
       sel[k].count = 0;

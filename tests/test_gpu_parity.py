@@ -439,3 +439,30 @@ def test_fault_injection_is_detected():
     ctx.test_inject(run.db, 1, 37, 12345, 1 << 20)  # restore
     outs = ctx.query(run.evk, run.db, run.qct, outs)
     assert all((ctx.ciphertext_residues(outs[a]) == want[a]).all() for a in range(cfg.aggregates))
+
+
+def test_packed_and_unpacked_diagonals_bit_exact(monkeypatch):
+    """Packed plaintext diagonals (R34: the 45-bit limbs in 6 bytes, split at bit 31) are the
+    default where the TMA MAC serves the layout; HD_PACK_D=0 at enrollment keeps u64 words.
+    Both layouts give the oracle's bits on every aggregate, hd_test_stage returns the same
+    residues from either, and the reported diagonal size is 20 n / 24 n bytes at L = 3."""
+    cfg = CONFIGS["C2"]
+    packed = Run(cfg)
+    monkeypatch.setenv("HD_PACK_D", "0")
+    plain = Run(cfg)
+    monkeypatch.delenv("HD_PACK_D")
+    n = 1 << cfg.log_n
+    assert packed.db.diagonal_bytes == (20 * n, True)
+    assert plain.db.diagonal_bytes == (24 * n, False)
+    o = packed.o
+    s_ntt, steps, keys = packed.oracle_keys()
+    r = o.baby_steps(packed.oracle_query_ct(), cfg.n1, steps, keys)
+    for a in range(cfg.aggregates):
+        want = o.scan_aggregate(r, cfg.n1, cfg.dim, packed.oracle_D(a), steps, keys)
+        for run in (packed, plain):
+            assert (run.ctx.ciphertext_residues(run.outs[a]) == want).all(), a
+    for k in (0, 7, cfg.dim - 1):
+        dp = packed.ctx.test_stage(packed.db, 4, 1, k)
+        du = plain.ctx.test_stage(plain.db, 4, 1, k)
+        assert (dp == du).all()
+        assert (dp.reshape(cfg.limbs, n) == packed.oracle_D(1)[k]).all()
