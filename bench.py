@@ -584,8 +584,8 @@ def main():
     # D passes per step: hd_query_batch runs the single-query MAC per query unless HD_MAC_BATCH=G
     # selects the shared-D kernel (one pass per group of up to G queries)
     mac_kernel, mac_src = mac_kernel_of(cfg, flat, enc_db)
-    if mac_kernel == "mac_tma_kernel":  # groups of up to HD_MAC_BATCH (default 4) queries per D pass
-        gmax = max(1, min(4, int(os.environ.get("HD_MAC_BATCH", "4") or 4)))
+    if mac_kernel == "mac_tma_kernel":  # groups of up to HD_MAC_BATCH (default 2) queries per D pass
+        gmax = max(1, min(4, int(os.environ.get("HD_MAC_BATCH", "2") or 2)))
         d_passes = -(-Q // gmax)
     else:
         g_env = int(os.environ.get("HD_MAC_BATCH", "1") or 1)

@@ -528,9 +528,11 @@ hd_status mac_batch_run(hd_context *c, const uint64_t *D, const uint64_t *r, uin
   if (js.empty() || A_loc == 0 || Q == 0) return HD_OK;
   const int jmin = js.front(), nj = (int)js.size();
   const size_t ls = (size_t)c->L * c->n, rq = (size_t)n1 * 2 * ls, sq = (size_t)A_loc * nj * 2 * ls;
-  if (mac_tma_supported(c, n1, N, flat, 1)) {  // groups of up to 4 queries per diagonal pass
-    const char *g_env = getenv("HD_MAC_BATCH");    // max group size (default 4)
-    const uint32_t gmax = g_env ? std::max(1, std::min(4, atoi(g_env))) : 4;
+  if (mac_tma_supported(c, n1, N, flat, 1)) {  // groups of up to 2 (HD_MAC_BATCH: 1..4) queries per pass
+    // measured at 2^20 x 512 with the Karatsuba MAC: pairs (QB 2, JT 2) 80.7 q/s, groups of 4
+    // (QB 4, JT 1: each r word serves one diagonal word) 77.3, single queries 73.2
+    const char *g_env = getenv("HD_MAC_BATCH");
+    const uint32_t gmax = g_env ? std::max(1, std::min(4, atoi(g_env))) : 2;
     for (uint32_t b0 = 0; b0 < Q;) {
       const uint32_t g = std::min(gmax, Q - b0);
       hd_status s = mac_tma_run(c, D, r + b0 * rq, S + b0 * sq, A_loc, n1, N, js, g, flat, dp);

@@ -71,61 +71,6 @@ __device__ __forceinline__ void tma_load_5d(void *dst, const CUtensorMap *map, i
       : "memory");
 }
 
-// Karatsuba accumulation (R35).  With r = rl + rh 2^31 and d = dl + dh 2^31 (rl, dl < 2^31;
-// rh < 2^29 for residues below 2^60, dh < 2^16 for a packed narrow limb),
-//   r d = rl dl + ((rl + rh)(dl + dh) - rl dl - rh dh) 2^31 + rh dh 2^62,
-// and (rl + rh), (dl + dh) < 2^32.  The three products are summed over the baby steps
-// separately (the identity is linear) and combined once per unit: 2 IMAD.WIDE + 1 IMAD per
-// product for a narrow limb (rh dh < 2^32), 3 IMAD.WIDE for a wide one, against the 4
-// IMAD.WIDE of the schoolbook 32-bit split -- the MAC's compute is bound by that pipe.
-// Sums: s0 = sum rl dl and sm = sum (rl+rh)(dl+dh) as 64-bit words plus 32-bit carry counts
-// (< 2^71 for 128 terms), s2 = sum rh dh likewise (narrow: < 2^32 per term).
-struct KAcc {
-  uint64_t s0, sm, s2;
-  uint32_t c0, cm, c2;
-};
-template <bool NARROW>
-__device__ __forceinline__ void kmac(KAcc &A, uint32_t rl, uint32_t rh, uint32_t rs, uint32_t dl, uint32_t dh,
-                                     uint32_t ds) {
-  asm("{\n\t.reg .u64 t;\n\t"
-      "mul.wide.u32 t, %4, %6;\n\t"
-      "add.cc.u64 %0, %0, t;\n\t"
-      "addc.u32 %2, %2, 0;\n\t"
-      "mul.wide.u32 t, %5, %7;\n\t"
-      "add.cc.u64 %1, %1, t;\n\t"
-      "addc.u32 %3, %3, 0;\n\t"
-      "}"
-      : "+l"(A.s0), "+l"(A.sm), "+r"(A.c0), "+r"(A.cm)
-      : "r"(rl), "r"(rs), "r"(dl), "r"(ds));
-  if (NARROW) {
-    asm("{\n\t.reg .u32 l, h;\n\t"
-        "mov.b64 {l, h}, %0;\n\t"
-        "mad.lo.cc.u32 l, %1, %2, l;\n\t"
-        "addc.u32 h, h, 0;\n\t"
-        "mov.b64 %0, {l, h};\n\t"
-        "}"
-        : "+l"(A.s2)
-        : "r"(rh), "r"(dh));
-  } else {
-    asm("{\n\t.reg .u64 t;\n\t"
-        "mul.wide.u32 t, %2, %3;\n\t"
-        "add.cc.u64 %0, %0, t;\n\t"
-        "addc.u32 %1, %1, 0;\n\t"
-        "}"
-        : "+l"(A.s2), "+r"(A.c2)
-        : "r"(rh), "r"(dh));
-  }
-}
-// sum r d = s0 + (sm - s0 - s2) 2^31 + s2 2^62 (< 2^127 for 128 terms below 2^60) mod q
-__device__ __forceinline__ uint64_t kacc_reduce(const KAcc &A, uint64_t q, uint64_t bar, uint64_t r64,
-                                                uint64_t r64s) {
-  const unsigned __int128 x0 = ((unsigned __int128)A.c0 << 64) | A.s0;
-  const unsigned __int128 xm = ((unsigned __int128)A.cm << 64) | A.sm;
-  const unsigned __int128 x2 = ((unsigned __int128)A.c2 << 64) | A.s2;
-  const unsigned __int128 x = x0 + ((xm - x0 - x2) << 31) + (x2 << 62);
-  return reduce128((uint64_t)(x >> 64), (uint64_t)x, q, bar, r64, r64s);
-}
-
 struct Unit {
   uint32_t a0;       // first aggregate of the group
   int gg0, tile, m;  // first diagonal block, coefficient tile, limb
