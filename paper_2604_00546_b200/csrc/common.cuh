@@ -365,11 +365,13 @@ constexpr uint64_t kNarrowBound = 1ull << 47;
 struct DPack {
   bool on = false;
   int W = 0, R = 0;
+  int polys = 1;                 // 2: encrypted diagonals, one packed block per polynomial
   uint8_t cls[HD_MAXMOD] = {0};  // 0 wide, 1 narrow
   uint8_t idx[HD_MAXMOD] = {0};  // position within its class
-  size_t diag_bytes = 0;         // one diagonal
+  size_t pp_bytes = 0;           // one polynomial: (8 W + 6 R) n
+  size_t diag_bytes = 0;         // one diagonal: polys x pp_bytes
 };
-DPack dpack_make(const hd_context *c, bool on);
+DPack dpack_make(const hd_context *c, bool on, int polys = 1);
 __host__ __device__ __forceinline__ uint64_t dp_get(const uint8_t *diag, const DPack &P, int limb, size_t t, size_t n) {
   if (!P.cls[limb]) return reinterpret_cast<const uint64_t *>(diag)[(size_t)P.idx[limb] * n + t];
   const uint32_t lo = reinterpret_cast<const uint32_t *>(diag + 8 * (size_t)P.W * n)[(size_t)P.idx[limb] * n + t];

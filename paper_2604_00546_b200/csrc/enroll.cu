@@ -276,34 +276,38 @@ extern "C" void hd_database_destroy(hd_database *db) {
   ctx_release(c);
 }
 
-DPack dpack_make(const hd_context *c, bool on) {
+DPack dpack_make(const hd_context *c, bool on, int polys) {
   DPack P;
   P.on = on;
+  P.polys = polys;
   for (int l = 0; l < c->L; l++) {
     const bool narrow = on && c->mod[l] < kNarrowBound;
     P.cls[l] = narrow ? 1 : 0;
     P.idx[l] = (uint8_t)(narrow ? P.R++ : P.W++);
   }
   if (P.R == 0) P.on = false;  // nothing to pack
-  P.diag_bytes = (8 * (size_t)P.W + 6 * (size_t)P.R) * c->n;
+  P.pp_bytes = (8 * (size_t)P.W + 6 * (size_t)P.R) * c->n;
+  P.diag_bytes = (size_t)polys * P.pp_bytes;
   return P;
 }
 
-// u64 rows [B][L][n] -> B packed diagonals (R34)
+// u64 rows [B][polys][L][n] -> B packed diagonals (R34)
 __global__ void pack_d_kernel(const uint64_t *__restrict__ src, uint8_t *__restrict__ dst, DPack P, int L, int logn) {
   const uint32_t n = 1u << logn;
   const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   const uint32_t b = blockIdx.y;
-  uint8_t *diag = dst + (size_t)b * P.diag_bytes;
-  for (int l = 0; l < L; l++) dp_put(diag, P, l, t, n, src[((size_t)b * L + l) * n + t]);
+  for (int p = 0; p < P.polys; p++) {
+    uint8_t *blk = dst + (size_t)b * P.diag_bytes + (size_t)p * P.pp_bytes;
+    for (int l = 0; l < L; l++) dp_put(blk, P, l, t, n, src[(((size_t)b * P.polys + p) * L + l) * n + t]);
+  }
 }
 
 // Device objects of a database handle: diagonals D (uninitialised), query workspaces, events.
 // footprint != NULL: only report the device bytes the handle needs (the paper's pre-upload
 // footprint check) and allocate nothing.
 static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing, bool encrypted, uint32_t n1,
-                          hd_database **out, size_t *footprint = nullptr) {
+                          hd_database **out, size_t *footprint = nullptr, int pack_override = -1) {
   HD_CUDA(cudaSetDevice(c->device));
   hd_database *db = new hd_database();
   db->ctx = c;
@@ -356,7 +360,10 @@ static hd_status db_alloc(hd_context *c, const hd_layout &lay, uint32_t packing,
   // plaintext diagonals are packed (R34) whenever the TMA MAC (the only kernel that reads the
   // packed form) serves this layout; HD_PACK_D=0 keeps u64 words (A/B knob)
   const char *pk_env = getenv("HD_PACK_D");
-  db->dp = dpack_make(c, !encrypted && !(pk_env && pk_env[0] == '0') && mac_tma_supported(c, (int)n1, N, db->flat, 1));
+  const bool tma_ok = encrypted ? mac_tma_ct_supported(c, (int)n1, N, db->flat) && !db->needs_prerotation
+                                : mac_tma_supported(c, (int)n1, N, db->flat, 1);
+  const bool pack = pack_override >= 0 ? pack_override != 0 : !(pk_env && pk_env[0] == '0') && tma_ok;
+  db->dp = dpack_make(c, pack, encrypted ? 2 : 1);
   const size_t d_bytes = db->dp.on ? db->dp.diag_bytes : dstride * 8;
   size_t tmp2_e = encrypted ? A * 2 * (L - 1) * n : 1;  // CRT remainders of the fused relinearise-rescale
   size_t digb_e = ks_dig_elems(c, L), ub_e = nb * 2 * (L + c->K) * n, tmpb_e = std::max(nb * 2 * L * n, (size_t)L * n);
@@ -463,7 +470,7 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
   if (!e) e = dev_alloc(c, &re, (size_t)KB * ns * 8);
   if (!e) e = dev_alloc(c, &im, (size_t)KB * ns * 8);
   uint64_t *Pt = nullptr;  // packed diagonals: the u64 rows of a batch before packing (R34)
-  if (!e && db->dp.on) e = dev_alloc(c, &Pt, (size_t)KB * L * n * 8);
+  if (!e && db->dp.on) e = dev_alloc(c, &Pt, (size_t)KB * dstride * 8);
   uint64_t *V = nullptr, *E0 = nullptr;  // public-key encryption scratch (v, e0 of a batch)
   if (!e && pk) e = dev_alloc(c, &V, (size_t)KB * L * n * 8);
   if (!e && pk) e = dev_alloc(c, &E0, (size_t)KB * L * n * 8);
@@ -505,8 +512,10 @@ static hd_status enroll_impl(hd_context *c, uint32_t packing, const hd_public_ke
                                                                            N, db->M, n1, a, k0, ns, re, im);
       ++c->launches;
       // plaintext rows (into c0 of each diagonal ciphertext in encrypted mode)
-      if (db->dp.on) {  // encode into u64 rows, then pack (R34)
-        s = encode_batch(c, re, im, kb, delta, L, Pt, (size_t)L * n);
+      if (db->dp.on) {  // encode (and encrypt) into u64 rows, then pack (R34)
+        s = encode_batch(c, re, im, kb, delta, L, Pt, dstride);
+        if (!s && pk)
+          s = pk_encrypt_rows(c, pk, Pt, dstride, (uint32_t)kb, enc_seed, (uint32_t)((uint64_t)a * N + k0), V, E0);
         if (!s) {
           uint8_t *Dp = reinterpret_cast<uint8_t *>(db->D) + ((size_t)(a - agg_begin) * N + k0) * db->dp.diag_bytes;
           pack_d_kernel<<<dim3((n + TPB - 1) / TPB, kb), TPB, 0, c->stream>>>(Pt, Dp, db->dp, L, c->logn);
@@ -548,14 +557,15 @@ __global__ void aggregate_packed_kernel(const uint8_t *__restrict__ D, uint8_t *
                                         uint32_t A, int logn, int L, ModTab mt, DPack P) {
   const uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const uint64_t n = 1ull << logn;
-  if (e >= (uint64_t)N * L * n) return;
-  const uint64_t t = e & (n - 1), kl = e >> logn;
-  const int l = (int)(kl % (uint64_t)L);
-  const uint64_t k = kl / (uint64_t)L;
+  if (e >= (uint64_t)N * P.polys * L * n) return;
+  const uint64_t t = e & (n - 1), kpl = e >> logn;  // (k, poly, limb)
+  const int l = (int)(kpl % (uint64_t)L);
+  const uint64_t kp = kpl / (uint64_t)L, k = kp / (uint64_t)P.polys, p = kp % (uint64_t)P.polys;
   const uint64_t q = mt.q[l];
   uint64_t acc = 0;
-  for (uint32_t a = 0; a < A; a++) acc = addmod(acc, dp_get(D + ((uint64_t)a * N + k) * P.diag_bytes, P, l, t, n), q);
-  dp_put(out + k * P.diag_bytes, P, l, t, n, acc);
+  for (uint32_t a = 0; a < A; a++)
+    acc = addmod(acc, dp_get(D + ((uint64_t)a * N + k) * P.diag_bytes + p * P.pp_bytes, P, l, t, n), q);
+  dp_put(out + k * P.diag_bytes + p * P.pp_bytes, P, l, t, n, acc);
 }
 
 extern "C" hd_status hd_database_aggregate(hd_context *c, const hd_database *src, hd_database **out) {
@@ -566,7 +576,7 @@ extern "C" hd_status hd_database_aggregate(hd_context *c, const hd_database *src
   hd_layout lay = src->lay;
   lay.agg_end = lay.agg_begin + 1;
   hd_database *db = nullptr;
-  hd_status s = db_alloc(c, lay, lay.packing, src->encrypted, src->n1, &db);
+  hd_status s = db_alloc(c, lay, lay.packing, src->encrypted, src->n1, &db, nullptr, src->dp.on ? 1 : 0);
   if (s) return s;
   db->needs_prerotation = false;  // the source's diagonals are already in their final form
   const uint64_t per_agg = (uint64_t)src->N * (src->encrypted ? 2 : 1) * c->L * c->n;
@@ -574,7 +584,7 @@ extern "C" hd_status hd_database_aggregate(hd_context *c, const hd_database *src
     hd_database_destroy(db);
     return hd_fail(HD_E_STATE, "aggregate database packing differs from its source");
   }
-  if (src->dp.on)
+  if (src->dp.on)  // per_agg = N polys L n elements either way
     aggregate_packed_kernel<<<(unsigned)((per_agg + TPB - 1) / TPB), TPB, 0, c->stream>>>(
         reinterpret_cast<const uint8_t *>(src->D), reinterpret_cast<uint8_t *>(db->D), src->N, src->A_loc, c->logn,
         c->L, c->mt, src->dp);

@@ -46,7 +46,7 @@ struct MacPlan {
 };
 // Encrypted diagonals (NEXT-1): degree-2 sums S3 [a][j][3][L][n] of Dct [a][k][2][L][n].
 hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint64_t *S3, uint32_t A_loc, int n1,
-                     int N, const std::vector<int32_t> &js, bool flat);
+                     int N, const std::vector<int32_t> &js, bool flat, const DPack &dp);
 // flat: the giant-step ranges of the flat packing (R27)
 // dp: packed diagonals (R34; only the TMA MAC reads them)
 hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A_loc, int n1, int N,
@@ -57,7 +57,8 @@ hd_status mac_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t 
 bool mac_tma_supported(const hd_context *c, int n1, int N, bool flat, uint32_t Q);
 // the degree-2 MAC of encrypted diagonals (NEXT-1) on the same pipeline: S3 [A][nj][3][L][n]
 hd_status mac_tma_ct_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S3, uint32_t A, int n1, int N,
-                         const std::vector<int32_t> &js, bool flat);
+                         const std::vector<int32_t> &js, bool flat, const DPack &dp);
+bool mac_tma_ct_supported(const hd_context *c, int n1, int N, bool flat);
 hd_status mac_tma_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S, uint32_t A, int n1, int N,
                       const std::vector<int32_t> &js, uint32_t Q, bool flat, const DPack &dp);
 

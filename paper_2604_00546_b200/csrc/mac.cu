@@ -458,10 +458,11 @@ void launch_batch(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t 
 }  // namespace
 
 hd_status mac_ct_run(hd_context *c, const uint64_t *Dct, const uint64_t *r, uint64_t *S3, uint32_t A_loc, int n1,
-                     int N, const std::vector<int32_t> &js, bool flat) {
+                     int N, const std::vector<int32_t> &js, bool flat, const DPack &dp) {
   if (js.empty() || A_loc == 0) return HD_OK;
   if (c->n % MAC_TPB) return hd_fail(HD_E_PARAMS, "ring too small for the encrypted MAC");
-  if (mac_tma_supported(c, n1, N, flat, 1) && c->L <= 8) return mac_tma_ct_run(c, Dct, r, S3, A_loc, n1, N, js, flat);
+  if (mac_tma_ct_supported(c, n1, N, flat)) return mac_tma_ct_run(c, Dct, r, S3, A_loc, n1, N, js, flat, dp);
+  if (dp.on) return hd_fail(HD_E_STATE, "packed diagonals (R34) need the TMA MAC (HD_MAC_VARIANT set after enrollment?)");
   const int jmin = js.front(), nj = (int)js.size();
   const char *force = getenv("HD_MAC_VARIANT");  // 'g': the generic kernel (tests)
   const bool generic = force && force[0] == 'g';

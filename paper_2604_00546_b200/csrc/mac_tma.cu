@@ -262,14 +262,15 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
 // carry-save, d1's mid folded every 4 steps, all banked every 64 steps (d1 takes 2 products
 // per step: 128 products < 2^127).  S3 [a][j][3][L][n].
 constexpr int CT_MAXL = 8;
-struct CtMaps {
-  CUtensorMap m[CT_MAXL];
+struct CtMaps {  // per limb: the u64 map (wide) or the u32 low-plane map (narrow, R34) + its u16 map
+  CUtensorMap m[CT_MAXL], hi[CT_MAXL];
+  uint8_t narrow[CT_MAXL];
 };
 template <int AG, int JT, int SPS>
 __global__ void __launch_bounds__(AG *TC + 32, 1)
     mac_tma_ct_kernel(const __grid_constant__ CtMaps tmD, const __grid_constant__ CUtensorMap tmR,
                       uint64_t *__restrict__ S, int n1, int N, int L, int logn, int nj, uint32_t A, int flat,
-                      int stages, ModTab mt, uint32_t small_mask) {
+                      int stages, ModTab mt, uint32_t small_mask, int flags) {
   extern __shared__ __align__(1024) unsigned char smem[];
   constexpr int D_WORDS = AG * JT * SPS * 2 * TC, R_WORDS = SPS * 2 * TC;
   constexpr uint32_t STAGE_BYTES = (D_WORDS + R_WORDS) * 8;
@@ -287,7 +288,7 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
   }
   __syncthreads();
   if (threadIdx.x >= CONSUMERS) {  // ---------------- producer warp ----------------
-    if (threadIdx.x != CONSUMERS) return;
+    if (threadIdx.x != CONSUMERS || (flags & 2)) return;
     uint64_t pol_stream, pol_keep;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_stream));
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
@@ -297,9 +298,16 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
       const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
       for (int sb = 0; sb < nsb; sb++) {
         mbar_wait(&empty[stage], phase ^ 1);
-        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
         uint64_t *base = reinterpret_cast<uint64_t *>(smem + (size_t)stage * STAGE_BYTES);
-        tma_load_5d(base, &tmD.m[x.m], x.tile * TC, 0, sb * SPS, x.gg0, (int)x.a0, &full[stage], pol_stream);
+        if (!tmD.narrow[x.m]) {
+          mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+          tma_load_5d(base, &tmD.m[x.m], x.tile * TC, 0, sb * SPS, x.gg0, (int)x.a0, &full[stage], pol_stream);
+        } else {  // packed limb: low plane (4 B per word) then high plane (2 B)
+          mbar_arrive_expect_tx(&full[stage], D_WORDS * 6 + R_WORDS * 8);
+          tma_load_5d(base, &tmD.m[x.m], x.tile * TC, 0, sb * SPS, x.gg0, (int)x.a0, &full[stage], pol_stream);
+          tma_load_5d(reinterpret_cast<unsigned char *>(base) + 4 * D_WORDS, &tmD.hi[x.m], x.tile * TC, 0, sb * SPS,
+                      x.gg0, (int)x.a0, &full[stage], pol_stream);
+        }
         tma_load_3d(base + D_WORDS, &tmR, x.tile * TC, x.m, sb * SPS * 2, &full[stage], pol_keep);
         if (++stage == stages) {
           stage = 0;
@@ -327,13 +335,15 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
         part[jj][e] = 0;
       }
     for (int sb = 0; sb < nsb; sb++) {
-      mbar_wait(&full[stage], phase);
+      if (!(flags & 2)) mbar_wait(&full[stage], phase);
       // box order [AG][JT][SPS][2][TC]
-      const uint64_t *Ds =
-          reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + g * JT * SPS * 2 * TC + t;
-      const uint64_t *Rs = reinterpret_cast<const uint64_t *>(smem + (size_t)stage * STAGE_BYTES) + D_WORDS + t;
-      auto consume = [&](auto small_tag) {
-        constexpr bool SMALL = decltype(small_tag)::value;
+      const unsigned char *sbase = smem + (size_t)stage * STAGE_BYTES;
+      const uint64_t *Ds = reinterpret_cast<const uint64_t *>(sbase) + g * JT * SPS * 2 * TC + t;
+      const uint32_t *Dl = reinterpret_cast<const uint32_t *>(sbase) + g * JT * SPS * 2 * TC + t;
+      const uint16_t *Dh = reinterpret_cast<const uint16_t *>(sbase + 4 * D_WORDS) + g * JT * SPS * 2 * TC + t;
+      const uint64_t *Rs = reinterpret_cast<const uint64_t *>(sbase) + D_WORDS + t;
+      auto consume = [&](auto small_tag, auto packed_tag) {
+        constexpr bool SMALL = decltype(small_tag)::value, PACKED = decltype(packed_tag)::value;
 #pragma unroll
         for (int s = 0; s < SPS; s++) {
           const uint64_t r0 = Rs[(2 * s) * TC], r1 = Rs[(2 * s + 1) * TC];
@@ -341,9 +351,21 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
           const uint32_t r1l = (uint32_t)r1 & 0x7fffffffu, r1h = (uint32_t)(r1 >> 31), r1s = r1l + r1h;
 #pragma unroll
           for (int jj = 0; jj < JT; jj++) {
-            const uint64_t d0 = Ds[((jj * SPS + s) * 2 + 0) * TC], d1 = Ds[((jj * SPS + s) * 2 + 1) * TC];
-            const uint32_t a0l = (uint32_t)d0 & 0x7fffffffu, a0h = (uint32_t)(d0 >> 31), a0s = a0l + a0h;
-            const uint32_t a1l = (uint32_t)d1 & 0x7fffffffu, a1h = (uint32_t)(d1 >> 31), a1s = a1l + a1h;
+            uint32_t a0l, a0h, a1l, a1h;
+            const int w0 = ((jj * SPS + s) * 2 + 0) * TC, w1 = w0 + TC;
+            if (PACKED) {  // stored split at bit 31 (R34)
+              a0l = Dl[w0];
+              a0h = Dh[w0];
+              a1l = Dl[w1];
+              a1h = Dh[w1];
+            } else {
+              const uint64_t d0 = Ds[w0], d1 = Ds[w1];
+              a0l = (uint32_t)d0 & 0x7fffffffu;
+              a0h = (uint32_t)(d0 >> 31);
+              a1l = (uint32_t)d1 & 0x7fffffffu;
+              a1h = (uint32_t)(d1 >> 31);
+            }
+            const uint32_t a0s = a0l + a0h, a1s = a1l + a1h;
             kmac<SMALL>(acc[jj][0], r0l, r0h, r0s, a0l, a0h, a0s);  // d0 += r0 D0
             kmac<SMALL>(acc[jj][1], r0l, r0h, r0s, a1l, a1h, a1s);  // d1 += r0 D1 + r1 D0
             kmac<SMALL>(acc[jj][1], r1l, r1h, r1s, a0l, a0h, a0s);
@@ -351,12 +373,16 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
           }
         }
       };
-      if (small)
-        consume(std::true_type{});
-      else
-        consume(std::false_type{});
+      if (flags & 1) {
+      } else if (tmD.narrow[x.m]) {
+        consume(std::true_type{}, std::true_type{});
+      } else if (small) {
+        consume(std::true_type{}, std::false_type{});
+      } else {
+        consume(std::false_type{}, std::false_type{});
+      }
       __syncwarp();
-      if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[stage]);
+      if (!(flags & 2) && (threadIdx.x & 31) == 0) mbar_arrive(&empty[stage]);
       if (++stage == stages) {
         stage = 0;
         phase ^= 1;
@@ -476,8 +502,10 @@ hd_status launch_ct(hd_context *c, const CtMaps &mD, const CUtensorMap &mR, uint
   uint32_t small_mask = 0;  // limbs whose residues stay below 2^47 (Karatsuba narrow form, R35)
   for (int l = 0; l < c->L && l < 32; l++)
     if (c->mod[l] < kNarrowBound) small_mask |= 1u << l;
+  const char *dry = getenv("HD_MAC_TMA_DRY"), *co = getenv("HD_MAC_COMPUTE_ONLY");  // measurement only
+  const int flags = (dry && dry[0] == '1' ? 1 : 0) | (co && co[0] == '1' ? 2 : 0);
   kern<<<grid, AG * TC + 32, smem, c->stream>>>(mD, mR, S, n1, N, c->L, c->logn, nj, A, flat ? 1 : 0, stages, c->mt,
-                                                small_mask);
+                                                small_mask, flags);
   ++c->launches;
   HD_CUDA(cudaGetLastError());
   return HD_OK;
@@ -486,7 +514,7 @@ hd_status launch_ct(hd_context *c, const CtMaps &mD, const CUtensorMap &mR, uint
 
 // S3 [A][nj][3][L][n] of encrypted diagonals Dct [A][N][2][L][n] (full giant-step ranges).
 hd_status mac_tma_ct_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint64_t *S3, uint32_t A, int n1, int N,
-                         const std::vector<int32_t> &js, bool flat) {
+                         const std::vector<int32_t> &js, bool flat, const DPack &dp) {
   if (js.empty() || A == 0) return HD_OK;
   const int nj = (int)js.size(), G = N / n1, L = c->L, n = c->n;
   if (nj != G || L > CT_MAXL) return hd_fail(HD_E_STATE, "TMA MAC expects one giant step per diagonal block");
@@ -503,12 +531,29 @@ hd_status mac_tma_ct_run(hd_context *c, const uint64_t *D, const uint64_t *r, ui
   while (jt > 1 && nj % jt) jt /= 2;
   CtMaps mD;
   hd_status s;
-  for (int m = 0; m < L; m++) {  // D of limb m: (coefficient, poly, diagonal, block, aggregate)
-    const cuuint64_t dims[5] = {(cuuint64_t)n, 2, (cuuint64_t)n1, (cuuint64_t)G, (cuuint64_t)A};
-    const cuuint64_t strides[4] = {(cuuint64_t)L * n * 8, (cuuint64_t)2 * L * n * 8, (cuuint64_t)n1 * 2 * L * n * 8,
-                                   (cuuint64_t)N * 2 * L * n * 8};
-    const cuuint32_t box[5] = {(cuuint32_t)TC, 2, (cuuint32_t)sps, (cuuint32_t)jt, (cuuint32_t)ag};
-    if ((s = encode(&mD.m[m], D + (size_t)m * n, 5, dims, strides, box))) return s;
+  // D of limb m: (coefficient, poly, diagonal, block, aggregate); packed (R34): per polynomial
+  // block the wide limbs as u64 rows, the narrow limbs as u32 low / u16 high planes
+  const size_t pp = dp.on ? dp.pp_bytes : (size_t)L * n * 8, db = 2 * pp;
+  const int W = dp.on ? dp.W : L, R = dp.on ? dp.R : 0;
+  const uint8_t *Db = reinterpret_cast<const uint8_t *>(D);
+  const cuuint32_t box[5] = {(cuuint32_t)TC, 2, (cuuint32_t)sps, (cuuint32_t)jt, (cuuint32_t)ag};
+  const cuuint64_t dims[5] = {(cuuint64_t)n, 2, (cuuint64_t)n1, (cuuint64_t)G, (cuuint64_t)A};
+  const cuuint64_t strides[4] = {(cuuint64_t)pp, (cuuint64_t)db, (cuuint64_t)n1 * db, (cuuint64_t)N * db};
+  for (int m = 0; m < L; m++) {
+    const bool nw = dp.on && dp.cls[m];
+    const int ix = dp.on ? dp.idx[m] : m;
+    mD.narrow[m] = nw ? 1 : 0;
+    if (!nw) {
+      if ((s = encode_t(&mD.m[m], Db + (size_t)ix * n * 8, CU_TENSOR_MAP_DATA_TYPE_UINT64, 5, dims, strides, box)))
+        return s;
+      mD.hi[m] = mD.m[m];
+    } else {
+      if ((s = encode_t(&mD.m[m], Db + (8 * (size_t)W + 4 * (size_t)ix) * n, CU_TENSOR_MAP_DATA_TYPE_UINT32, 5, dims,
+                        strides, box)) ||
+          (s = encode_t(&mD.hi[m], Db + (8 * (size_t)W + 4 * (size_t)R + 2 * (size_t)ix) * n,
+                        CU_TENSOR_MAP_DATA_TYPE_UINT16, 5, dims, strides, box)))
+        return s;
+    }
   }
   CUtensorMap mR;
   {
@@ -527,6 +572,10 @@ hd_status mac_tma_ct_run(hd_context *c, const uint64_t *D, const uint64_t *r, ui
   if (sps == 2) { HD_CT_L(1, 1, 2); }
   HD_CT_L(1, 1, 8);
 #undef HD_CT_L
+}
+
+bool mac_tma_ct_supported(const hd_context *c, int n1, int N, bool flat) {
+  return mac_tma_supported(c, n1, N, flat, 1) && c->L <= CT_MAXL;
 }
 
 bool mac_tma_supported(const hd_context *c, int n1, int N, bool flat, uint32_t Q) {

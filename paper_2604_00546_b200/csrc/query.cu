@@ -148,7 +148,7 @@ static hd_status run_scan(hd_database *db, const hd_ciphertext *const *queries, 
   if (Q > 1) {
     if ((s = mac_batch_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat, Q, db->dp))) return s;
   } else if (db->encrypted) {
-    if ((s = mac_ct_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat))) return s;
+    if ((s = mac_ct_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat, db->dp))) return s;
   } else if ((s = mac_run(c, db->D, rbase, Sbuf, A, n1, (int)db->N, db->js, db->flat, db->dp))) {
     return s;
   }
@@ -557,8 +557,10 @@ extern "C" hd_status hd_test_stage(const hd_database *db, int which, uint32_t ag
         HD_CUDA(cudaStreamSynchronize(c->stream));
         HD_CUDA(cudaMemcpy(buf.data(), reinterpret_cast<const uint8_t *>(db->D) + (a * db->N + index) * db->dp.diag_bytes,
                            buf.size(), cudaMemcpyDeviceToHost));
-        for (int l = 0; l < L; l++)
-          for (int t = 0; t < n; t++) host_dst[(size_t)l * n + t] = dp_get(buf.data(), db->dp, l, t, n);
+        for (int p = 0; p < db->dp.polys; p++)
+          for (int l = 0; l < L; l++)
+            for (int t = 0; t < n; t++)
+              host_dst[((size_t)p * L + l) * n + t] = dp_get(buf.data() + p * db->dp.pp_bytes, db->dp, l, t, n);
         return HD_OK;
       }
       src = db->D + (a * db->N + index) * len;
@@ -587,9 +589,9 @@ extern "C" hd_status hd_test_inject(hd_database *db, uint32_t agg, int32_t k, ui
   HD_CUDA(cudaStreamSynchronize(c->stream));
   hd_context_synchronize(c);
   if (db->dp.on) {  // packed (R34): the limb's u64 word, or its low (u32) and high (u16) parts
-    const int l = (int)(word / c->n);
+    const int pl = (int)(word / c->n), p = pl / c->L, l = pl % c->L;  // [poly][limb][coef]
     const size_t t = word % c->n;
-    uint8_t *dg = reinterpret_cast<uint8_t *>(db->D) + diag * db->dp.diag_bytes;
+    uint8_t *dg = reinterpret_cast<uint8_t *>(db->D) + diag * db->dp.diag_bytes + (size_t)p * db->dp.pp_bytes;
     if (!db->dp.cls[l]) {
       xor_word_kernel<<<1, 1, 0, c->stream>>>(reinterpret_cast<uint64_t *>(dg) + (size_t)db->dp.idx[l] * c->n + t, mask);
     } else {
