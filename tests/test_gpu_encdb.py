@@ -105,6 +105,12 @@ def test_encrypted_c2_all_aggregates_bit_exact():
         assert (run.ctx.ciphertext_residues(run.outs[a]) == out).all(), a
     sc = run.ctx.decrypt_scores(run.sk, run.db.layout, run.outs)
     assert np.abs(sc - _cos(run.db_vecs, run.q)).max() < 1e-6
+    # the encrypted diagonals are stored packed (R34: both polynomials, 45-bit limbs in 6
+    # bytes) and hd_test_stage returns the oracle's residues from them
+    n = 1 << cfg.log_n
+    assert run.db.diagonal_bytes == (2 * 20 * n, True)
+    for k in (0, cfg.dim - 1):
+        assert (run.ctx.test_stage(run.db, 4, 1, k) == run.oracle_Dct(1)[k]).all()
 
 
 def test_missing_relinearisation_key_and_public_key_roundtrip(toy):
