@@ -352,10 +352,12 @@ hd_status conv_run(hd_context *c, const uint64_t *src, size_t src_gs, uint32_t g
 }
 
 // Key inner product over the general extended basis; x = b * K + k, output u[x][p][e],
-// e < ell + Ksp.  dig [b][d][e][n] (every modulus per digit, NTT form), key [d][p][M][n].
+// e < ell + Ksp.  dig [b][d][slot][n] (the digit's non-own moduli, NTT form; its own limbs are
+// c1's rows c1 + b c1_stride + e n), key [d][p][M][n].
 // Accumulate mode as kip_kernel (R23).  Two coefficients per thread.
-__global__ void __launch_bounds__(TPB) kipg_kernel(const uint64_t *__restrict__ dig, uint64_t *__restrict__ u, int ell,
-                                                   int ext, int beta, int K, int L, int M, int logn,
+__global__ void __launch_bounds__(TPB) kipg_kernel(const uint64_t *__restrict__ dig, const uint64_t *__restrict__ c1,
+                                                   size_t c1_stride, uint64_t *__restrict__ u, int ell, int ext,
+                                                   int beta, int alpha, int K, int L, int M, int logn,
                                                    const uint64_t *const *__restrict__ kptr,
                                                    const uint32_t *__restrict__ gal, ModTab mt, KipAcc ka,
                                                    FDiv f_ext, FDiv f_K) {
@@ -369,10 +371,15 @@ __global__ void __launch_bounds__(TPB) kipg_kernel(const uint64_t *__restrict__ 
   const uint32_t g = gal[k];
   const uint32_t s0 = galois_src(t, g, logn), s1 = galois_src(t + 1, g, logn);
   const uint64_t *key = kptr[k];
-  const uint64_t *dg = dig + (size_t)b * beta * ext * n + (size_t)e * n;
+  const uint64_t *dg = dig + (size_t)b * beta * ext * n;
   uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0, b0l = 0, b0h = 0, b1l = 0, b1h = 0;
   for (int d = 0; d < beta; d++) {
-    const uint64_t *row = dg + (size_t)d * ext * n;
+    // digit d's own limbs [lo, lo + cnt) are c1's rows (the conversion reproduces them exactly,
+    // R31); its other moduli sit in slots e (e < lo) and e - cnt (e >= lo + cnt)
+    const int lo = d * alpha, cnt = min(alpha, ell - lo);
+    const uint64_t *row = ((int)e >= lo && (int)e < lo + cnt)
+                              ? c1 + (size_t)b * c1_stride + (size_t)e * n
+                              : dg + ((size_t)d * ext + ((int)e < lo ? (int)e : (int)e - cnt)) * n;
     const uint64_t v0 = row[s0], v1 = row[s1];
     const ulonglong2 k0 = *reinterpret_cast<const ulonglong2 *>(key + ((size_t)(d * 2 + 0) * M + gm) * n + t);
     const ulonglong2 k1 = *reinterpret_cast<const ulonglong2 *>(key + ((size_t)(d * 2 + 1) * M + gm) * n + t);
@@ -424,23 +431,28 @@ hd_status ks_modup(hd_context *c, const uint64_t *c1, size_t c1_stride, uint32_t
   if (ks_general(c)) {
     // 2. digit d (limbs [d alpha, min((d+1) alpha, ell))): fast basis conversion with centred
     //    digits into every modulus e of Q_ell u P (own limbs reproduce c1), rows dig[b][d][e]
+    //    except the digit's own limbs, which reproduce c1 (the KIP reads c1's rows there): slots
+    //    [0, ext - cnt) of dig[b][d] hold the other moduli in order
     const int ext = ell + c->K, beta = ks_beta(c, ell);
-    std::vector<int> tg(ext);
-    for (int e = 0; e < ext; e++) tg[e] = ks_ext_mod(c, ell, e);
     for (int d = 0; d < beta; d++) {
       const int lo = d * c->alpha, cnt = std::min(c->alpha, ell - lo);
-      std::vector<int> sm(cnt);
+      std::vector<int> sm(cnt), tg;
       for (int i = 0; i < cnt; i++) sm[i] = lo + i;
-      if ((s = conv_run(c, tmp + (size_t)lo * n, (size_t)ell * n, B, dig + (size_t)d * ext * n,
-                        (size_t)beta * ext * n, conv_table(c, sm, tg))))
+      for (int e = 0; e < ext; e++)
+        if (e < lo || e >= lo + cnt) tg.push_back(ks_ext_mod(c, ell, e));
+      uint64_t *dd = dig + (size_t)d * ext * n;
+      if ((s = conv_run(c, tmp + (size_t)lo * n, (size_t)ell * n, B, dd, (size_t)beta * ext * n, conv_table(c, sm, tg))))
         return s;
+      // 3. NTT of the digit's rows: B groups of ext - cnt rows
+      RowMap rd{};
+      rd.gsize = (uint32_t)tg.size();
+      rd.gstride = (uint64_t)beta * ext * n;
+      rd.mdiv = 1;
+      rd.mlen = (uint32_t)tg.size();
+      for (size_t i = 0; i < tg.size(); i++) rd.midx[i] = (uint8_t)tg[i];
+      if ((s = ntt_run(c, dd, B * (uint32_t)tg.size(), rd, false, nullptr, nullptr))) return s;
     }
-    // 3. NTT of every digit row
-    RowMap rd{};
-    rd.mdiv = 1;
-    rd.mlen = ext;
-    for (int e = 0; e < ext; e++) rd.midx[e] = (uint8_t)tg[e];
-    return ntt_run(c, dig, B * beta * ext, rd, false, nullptr, nullptr);
+    return HD_OK;
   }
   // 2. rows (b, d, slot) of dig: NTT over ext modulus e = slot < d ? slot : slot + 1 of the
   //    centred lift of tmp[b][d] (source modulus q_d)
@@ -469,8 +481,8 @@ hd_status ks_kip(hd_context *c, const uint64_t *dig, const uint64_t *c1, size_t 
   if (ks_general(c)) {
     const int ext = ell + c->K;
     kipg_kernel<<<grid_pairs(c->n, B * K * ext), TPB, 0, c->stream>>>(
-        dig, u, ell, ext, ks_beta(c, ell), K, c->L, ks_M(c), c->logn, kptr_dev, gal_dev, c->mt, KipAcc{},
-        fdiv_make(ext), fdiv_make(K));
+        dig, c1, c1_stride, u, ell, ext, ks_beta(c, ell), c->alpha, K, c->L, ks_M(c), c->logn, kptr_dev, gal_dev,
+        c->mt, KipAcc{}, fdiv_make(ext), fdiv_make(K));
     ++c->launches;
     HD_CUDA(cudaGetLastError());
     return HD_OK;
@@ -488,8 +500,8 @@ hd_status ks_kip_accumulate(hd_context *c, const uint64_t *dig, const uint64_t *
   if (ks_general(c)) {
     const int ext = ell + c->K;
     kipg_kernel<<<grid_pairs(c->n, B * ext), TPB, 0, c->stream>>>(
-        dig, u, ell, ext, ks_beta(c, ell), 1, c->L, ks_M(c), c->logn, kptr_dev, gal_dev, c->mt,
-        kip_acc(c, ell, ct, ct_stride), fdiv_make(ext), fdiv_make(1));
+        dig, ct + (size_t)ell * c->n, ct_stride, u, ell, ext, ks_beta(c, ell), c->alpha, 1, c->L, ks_M(c), c->logn,
+        kptr_dev, gal_dev, c->mt, kip_acc(c, ell, ct, ct_stride), fdiv_make(ext), fdiv_make(1));
     ++c->launches;
     HD_CUDA(cudaGetLastError());
     return HD_OK;

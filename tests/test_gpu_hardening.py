@@ -5,6 +5,8 @@
 * a database's cached rotation-key pointers are invalidated when hd_relin_keygen
   reallocates the key storage (query -> relin_keygen -> query stays bit-identical).
 """
+import gc
+
 import numpy as np
 import pytest
 
@@ -115,6 +117,7 @@ def test_torch_allocator_owns_device_memory():
     footprint hd_enroll_footprint reports, and destroying it returns them."""
     cfg = CONFIGS["C2"]
     db_vecs, q, _ = make_dataset(cfg.num_vectors, cfg.dim, cfg.data_seed)
+    gc.collect()  # earlier tests' handles: free them now, not in the middle of the measurement
     torch.cuda.synchronize()
     base = torch.cuda.memory_allocated(0)
     ctx = hd.Context(cfg.log_n, cfg.limbs, seed=1)
