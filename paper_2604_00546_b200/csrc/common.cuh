@@ -21,7 +21,7 @@
 // Per-modulus constants, passed to kernels by value.
 // ---------------------------------------------------------------------------
 // Moduli below this bound run the FP64 NTT butterflies of ntt.cu (R33).
-constexpr uint64_t kNttFp64Bound = 1ull << 46;
+constexpr uint64_t kNttFp64Bound = 1ull << 45;
 
 struct ModTab {
   uint64_t q[HD_MAXMOD];
@@ -245,7 +245,7 @@ struct hd_context {
   // device tables
   uint64_t *tw2 = nullptr, *itw2 = nullptr;  // [L+1][n] x {w, shoup(w)}: psi^{br(k)}, psi^{-br(k)}
   uint64_t *ninv_dev = nullptr;              // [2 HD_MAXMOD]: n^{-1} mod q_l, then Shoup companions
-  // the same twiddles as doubles (exact: moduli below 2^46 only, else 0) for the FP64
+  // the same twiddles as doubles (exact: moduli below 2^45 only, else 0) for the FP64
   // butterflies of ntt.cu (R33)
   double *twd = nullptr, *itwd = nullptr;  // [L+K][n]
   bool ntt_attr_set = false;

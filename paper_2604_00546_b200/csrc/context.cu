@@ -241,7 +241,7 @@ extern "C" hd_status hd_context_create(const hd_params *params, int cuda_device,
       tw[2 * ((size_t)l * n + k) + 1] = host_shoup(pw[b], q);
       itw[2 * ((size_t)l * n + k)] = ipw[b];
       itw[2 * ((size_t)l * n + k) + 1] = host_shoup(ipw[b], q);
-      if (q < kNttFp64Bound) {  // exact as doubles (< 2^46)
+      if (q < kNttFp64Bound) {  // exact as doubles (< 2^45)
         twd[(size_t)l * n + k] = (double)pw[b];
         itwd[(size_t)l * n + k] = (double)ipw[b];
       }

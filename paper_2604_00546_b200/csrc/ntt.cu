@@ -21,7 +21,7 @@
 // rescale lifts, R12); the final forward store may apply the ModDown / rescale
 // combine (A - v) w (+ pi_g(c0)), written or accumulated into a third row map.
 //
-// Rows whose modulus is below 2^46 (the 45-bit scaling limbs) run the same passes with FP64
+// Rows whose modulus is below 2^45 (the 45-bit scaling limbs) run the same passes with FP64
 // butterflies instead (R33, below): the integer Shoup product is bound by the IMAD pipe, the
 // FP64 one runs on the FP64 pipe at ~2.2x the butterfly rate (tools/micro/bfly_bench.cu).
 #include "common.cuh"
@@ -187,15 +187,16 @@ __device__ __forceinline__ uint64_t final_reduce(uint64_t x, uint64_t q) {  // [
   return x;
 }
 
-// ---- FP64 butterflies for moduli q < 2^46 (R33) ----
+// ---- FP64 butterflies for moduli q < 2^45 (R33) ----
 // The 64-bit Shoup product above costs ~15 IMAD-class instructions on the integer multiply
-// (fmaheavy) pipe, which bounds the integer NTT.  Below 2^46 a residue is an exact double, and
+// (fmaheavy) pipe, which bounds the integer NTT.  Below 2^45 a residue is an exact double, and
 // y w mod q follows from an error-free product ph + pl = y w (DMUL + DFMA), a rounded quotient
 // Q = rint(ph / q) and t = (ph - Q q) + pl, both steps exact (|ph - Q q| < 2^53): 7 FP64
 // operations on the FP64 pipe, |t| <= 1.25 q for |y| < 2^51.  Values stay signed and unreduced:
 // forward, |X| <= q + 1.25 q per stage (<= 21 q after 16 stages); inverse, every radix-16 pass
 // starts by reducing its 16 values to |x| <= q/2 (X + Y doubles per stage: <= 10 q after a
-// pass).  Every bound stays below 2^51, where the 1.5 * 2^52 rounding constant is exact.
+// pass).  Every bound stays below 2^51, where the 1.5 * 2^52 rounding constant is exact, for
+// inputs up to 4q (Harvey-lazy rows from any caller): the bound 2^45 leaves that margin.
 // Between the two kernels of one transform a row holds these doubles (bit patterns) in place.
 constexpr double kRnd = 6755399441055744.0;  // 1.5 * 2^52: x + kRnd - kRnd = rint(x), |x| < 2^51
 __device__ __forceinline__ double f_mulmod(double y, double w, double q, double qinv) {
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(256, 3) ntt_cols_kernel(uint64_t *base, RowMap
   const uint32_t row = sel_row(sel, r0, blockIdx.y);
   if (row >= sel.end) return;
   const int m = row_mod(rm, row);
-  if constexpr (FP) {  // FP64 butterflies: every row of this launch has a modulus below 2^46
+  if constexpr (FP) {  // FP64 butterflies: every row of this launch has a modulus below 2^45
     (void)tw;
     ColArgsF A;
     A.s2 = logn - S;
@@ -719,7 +720,7 @@ hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &ma
   const int s1 = logn - s2;              // column stages (0, or 5..8)
   const ulonglong2 *tw = reinterpret_cast<const ulonglong2 *>(inverse ? c->itw2 : c->tw2);
   const uint64_t *ninv = c->ninv_dev;
-  // FP64 butterflies for the moduli below 2^46 (R33); HD_NTT_FP64=0 keeps every row on the
+  // FP64 butterflies for the moduli below 2^45 (R33); HD_NTT_FP64=0 keeps every row on the
   // integer path (A/B knob)
   static const bool fp64_off = [] {
     const char *e = getenv("HD_NTT_FP64");
@@ -761,7 +762,7 @@ hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &ma
     c->ntt_attr_set = true;
   }
   // Rows by kind (R33): the map's modulus pattern repeats every mdiv * mlen rows; the positions
-  // of FP64 rows (modulus < 2^46) and of integer rows within one period go to separate launches.
+  // of FP64 rows (modulus < 2^45) and of integer rows within one period go to separate launches.
   // A map with a longer period runs every row on the integer kernels, and so does a small
   // batch (below HD_NTT_SPLIT_MIN rows, default 96): there the second launch pair costs more
   // than the FP64 butterflies save (launch-bound; C2's query 1.04 -> 1.29 ms when split).
@@ -772,7 +773,7 @@ hd_status ntt_run(hd_context *c, uint64_t *data, uint32_t rows, const RowMap &ma
     const char *e = getenv("HD_NTT_SPLIT_MIN");
     return e ? (uint32_t)atol(e) : 96u;
   }();
-  bool one_kind_fp = false;  // every row of the map has a modulus below 2^46
+  bool one_kind_fp = false;  // every row of the map has a modulus below 2^45
   if (twd && period <= 64) {
     one_kind_fp = true;
     for (uint32_t p = 0; p < period; p++) one_kind_fp &= c->mod[map.midx[(p / map.mdiv) % map.mlen]] < kNttFp64Bound;

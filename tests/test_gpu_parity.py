@@ -96,6 +96,15 @@ def test_ntt_bit_exact(log_n):
         for v in (0, m - 1):
             row = np.full((1, o.n), v, np.uint64)
             assert (ctx.test_ntt(row, [l])[0] == o.ntt(row[0], l)).all()
+    # Harvey-lazy inputs in [q, 2q) (the kernels accept [0, 2q); the FP64 rows' bounds, R33,
+    # hold up to 4q): the transform of x equals the oracle's transform of x mod q
+    for l, m in enumerate(o.p.moduli):
+        x = rng.integers(0, m, o.n, dtype=np.uint64)
+        lazy = (x + np.uint64(m)).reshape(1, -1)
+        for inv in (False, True):
+            assert (ctx.test_ntt(lazy, [l], inverse=inv)[0] == o.ntt(x, l, inverse=inv)).all(), (l, inv)
+        top = np.full((1, o.n), 2 * m - 1, np.uint64)
+        assert (ctx.test_ntt(top, [l], inverse=True)[0] == o.ntt(top[0] - np.uint64(m), l, inverse=True)).all()
 
 
 def test_keys_bit_exact(toy):
