@@ -92,6 +92,53 @@ __global__ void __launch_bounds__(TPB) kip_kernel(const uint64_t *__restrict__ d
   *o1 = v1;
 }
 
+// kip_kernel with ell known at compile time and one coefficient per thread: the ell Galois
+// gathers and 2 ell key words of a thread are all loaded before the first product (the
+// two-coefficient kernel above holds 78 registers, 3 CTAs per SM, and waits on its gathers).
+template <int ELL>
+__global__ void __launch_bounds__(TPB) kip1_kernel(const uint64_t *__restrict__ dig, const uint64_t *__restrict__ c1,
+                                                   size_t c1_stride, uint64_t *__restrict__ u, int K, int L, int logn,
+                                                   const uint64_t *const *__restrict__ kptr,
+                                                   const uint32_t *__restrict__ gal, ModTab mt, KipAcc ka, FDiv f_K) {
+  const int n = 1 << logn;
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t x = blockIdx.y / (ELL + 1), e = blockIdx.y % (ELL + 1);
+  const uint32_t b = fdiv_q(x, f_K), k = x - b * K;
+  if (t >= (uint32_t)n) return;
+  const int gm = (int)e < ELL ? (int)e : L;
+  const uint32_t s = galois_src(t, gal[k], logn);
+  const uint64_t *key = kptr[k];
+  const uint64_t *dg = dig + (size_t)b * ELL * ELL * n;
+  const uint64_t *cb = c1 + (size_t)b * c1_stride;
+  uint64_t v[ELL], k0[ELL], k1[ELL];
+#pragma unroll
+  for (int d = 0; d < ELL; d++) {
+    const uint64_t *row = ((int)e == d) ? cb + (size_t)d * n
+                                        : dg + ((size_t)d * ELL + ((int)e < d ? (int)e : (int)e - 1)) * n;
+    v[d] = row[s];
+    k0[d] = __ldg(key + ((size_t)(d * 2 + 0) * (L + 1) + gm) * n + t);
+    k1[d] = __ldg(key + ((size_t)(d * 2 + 1) * (L + 1) + gm) * n + t);
+  }
+  uint64_t a0l = 0, a0h = 0, a1l = 0, a1h = 0;
+#pragma unroll
+  for (int d = 0; d < ELL; d++) {
+    mac128(a0l, a0h, v[d], k0[d]);
+    mac128(a1l, a1h, v[d], k1[d]);
+  }
+  const uint64_t q = mt.q[gm], bar = mt.bar[gm], r64 = mt.r64[gm], r64s = mt.r64s[gm];
+  uint64_t o0 = reduce128(a0h, a0l, q, bar, r64, r64s), o1 = reduce128(a1h, a1l, q, bar, r64, r64s);
+  uint64_t *p0 = u + ((size_t)(x * 2 + 0) * (ELL + 1) + e) * n + t;
+  uint64_t *p1 = u + ((size_t)(x * 2 + 1) * (ELL + 1) + e) * n + t;
+  if (ka.c0) {
+    o0 = addmod(o0, *p0, q);
+    o1 = addmod(o1, *p1, q);
+    if ((int)e < ELL)
+      o0 = addmod(o0, shoup(ka.c0[(size_t)b * ka.c0_stride + (size_t)e * n + s], ka.pw[e], ka.pws[e], q), q);
+  }
+  *p0 = o0;
+  *p1 = o1;
+}
+
 // The whole hoisted giant-step sum of R23 in one pass (alpha = K = 1): for every aggregate b,
 //   u[b][p][e] = sum_j ( KIP(pi_j(dig_j[b]))[p][e] + [p == 0, e < ell] P pi_j(c0_j[b])[e] )
 //              + [e < ell] P T0[b][p][e]
@@ -483,6 +530,16 @@ hd_status ks_kip(hd_context *c, const uint64_t *dig, const uint64_t *c1, size_t 
     kipg_kernel<<<grid_pairs(c->n, B * K * ext), TPB, 0, c->stream>>>(
         dig, c1, c1_stride, u, ell, ext, ks_beta(c, ell), c->alpha, K, c->L, ks_M(c), c->logn, kptr_dev, gal_dev,
         c->mt, KipAcc{}, fdiv_make(ext), fdiv_make(K));
+    ++c->launches;
+    HD_CUDA(cudaGetLastError());
+    return HD_OK;
+  }
+  const dim3 g1((c->n + TPB - 1) / TPB, B * K * (ell + 1));
+  const char *kv = getenv("HD_KIP1");  // A/B knob: 0 keeps the two-coefficient kernel
+  if (!(kv && kv[0] == '0') && ell >= 1 && ell <= 4 && B * K * (ell + 1) <= 65535u) {
+    auto kern = ell == 1 ? kip1_kernel<1> : ell == 2 ? kip1_kernel<2> : ell == 3 ? kip1_kernel<3> : kip1_kernel<4>;
+    kern<<<g1, TPB, 0, c->stream>>>(dig, c1, c1_stride, u, K, c->L, c->logn, kptr_dev, gal_dev, c->mt, KipAcc{},
+                                    fdiv_make(K));
     ++c->launches;
     HD_CUDA(cudaGetLastError());
     return HD_OK;
