@@ -468,19 +468,20 @@ __device__ __forceinline__ void chunks_rec(uint64_t (&v)[E], uint32_t tid, uint6
 
 template <bool INV, int S, int P>
 __device__ __forceinline__ void chunks_rec_f(double (&v)[E], uint32_t tid, double *smt, const TwGlobalD &tw,
-                                             const FMod &F, bool reduce0) {
+                                             const FMod &F) {
   using PP = Pass<INV, S, P>;
 #pragma unroll
   for (int i = 0; i < E; i++) {
     v[i] = smt[pad_idx(elem_of<PP::KP, PP::REM, S>(i, tid))];
-    if (INV && (P > 0 || reduce0)) v[i] = f_red(v[i], F.q, F.qinv);
+    // the inverse reduces at every pass but the first (its inputs are residues below 4 q)
+    if (INV && P > 0) v[i] = f_red(v[i], F.q, F.qinv);
   }
   radix_pass_f<INV, PP::KP, PP::REM, S>(v, tid, tw, F);
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < E; i++) smt[pad_idx(elem_of<PP::KP, PP::REM, S>(i, tid))] = v[i];
   __syncthreads();
-  if constexpr (P < PP::NP - 1) chunks_rec_f<INV, S, P + 1>(v, tid, smt, tw, F, reduce0);
+  if constexpr (P < PP::NP - 1) chunks_rec_f<INV, S, P + 1>(v, tid, smt, tw, F);
 }
 
 // ---- chunks kernel: the S low stages on contiguous chunks of 2^S; tpc chunks per CTA ----
@@ -546,7 +547,7 @@ __device__ __forceinline__ void chunks_body(uint64_t *base, const RowMap &rm, co
     twf.T = twd + (size_t)m * n;
     twf.blk = (1u << s1) + chunk0 + tr;
     double vf[E];
-    chunks_rec_f<INV, S, 0>(vf, tid, reinterpret_cast<double *>(sm) + tr * PS, twf, F, raw_in);
+    chunks_rec_f<INV, S, 0>(vf, tid, reinterpret_cast<double *>(sm) + tr * PS, twf, F);
     ninv_f = u2d(ninv[m]);
   } else {
 #if HD_NTT_TW_SMEM
