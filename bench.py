@@ -62,9 +62,11 @@ def parse():
     ap.add_argument("--batch", type=int, default=1,
                     help="queries per step through hd_query_batch (NEXT-4: one diagonal stream serves up to 4 "
                          "queries); 1 = hd_query")
-    ap.add_argument("--split-baby", action="store_true",
+    ap.add_argument("--split-baby", dest="split_baby", action="store_true", default=None,
                     help="N > 1: each rank computes a slice of the baby steps, NCCL all-gathers r "
-                         "(hd_baby_steps / hd_query_baby) instead of every rank recomputing all of them")
+                         "(hd_baby_steps / hd_query_baby) instead of every rank recomputing all of them "
+                         "(default: on for N >= 4, DESIGN.md section 8)")
+    ap.add_argument("--no-split-baby", dest="split_baby", action="store_false")
     ap.add_argument("--online-aggregate", action="store_true",
                     help="membership only: scan the online-aggregated database (one aggregate holding the sum of "
                          "all aggregates' diagonals, Alg. online-aggr; NEXT-4), built at setup")
@@ -439,7 +441,10 @@ def main():
     outs_b = None  # hd_query_batch outputs [Q][nloc]
     split = None
     ct_l = 2 * cfg.limbs * (1 << cfg.log_n)  # u64 words of one baby-step ciphertext
-    if args.split_baby and world > 1 and Q == 1:
+    # default: split for N >= 4, where the per-rank baby steps (1.6 ms replicated) would
+    # be the largest term of the step and the all-gather of r (384 MiB) costs well under that
+    want_split = args.split_baby if args.split_baby is not None else world >= 4
+    if want_split and world > 1 and Q == 1:
         chunk, i0, i1 = hdd.baby_slice(cfg.n1, rank, world)  # the last slice may be short
         r_full = torch.empty(world * chunk * ct_l, dtype=torch.int64, device=dev)
         r_mine = torch.empty(chunk * ct_l, dtype=torch.int64, device=dev)

@@ -19,6 +19,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.mark.parametrize("extra", [["--config", "C2"],
+                                   ["--config", "C2", "--split-baby"],
                                    ["--config", "C3", "--packing", "flat", "--scenario", "membership"]])
 def test_two_ranks_on_one_gpu(extra):
     env = dict(os.environ, HD_BENCH_ONE_GPU="1")
@@ -31,5 +32,6 @@ def test_two_ranks_on_one_gpu(extra):
     assert len(lines) == 1  # rank 0 prints once
     d = lines[0]
     assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "aggregate-shard x2"
+    assert d["split_baby"] == ("--split-baby" in extra)
     if "--scenario" not in extra:  # the scan: every score of both shards checked on rank 0
         assert d["check"]["ok"] and d["check"]["scores_checked"] == 1 << 14
