@@ -75,10 +75,17 @@ struct Unit {
   uint32_t a0;       // first aggregate of the group
   int gg0, tile, m;  // first diagonal block, coefficient tile, limb
 };
-__device__ __forceinline__ Unit decode(uint32_t u, uint32_t nag, int ngrp, int tiles, int AG, int JT) {
+__device__ __forceinline__ Unit decode(uint32_t u, uint32_t nag, int ngrp, int tiles, int AG, int JT, int L = 0) {
   Unit x;
   x.a0 = (u % nag) * AG;
   u /= nag;
+  if (L) {  // limb second-fastest (A/B order: concurrent CTAs mix wide and packed limbs)
+    x.m = (int)(u % (uint32_t)L);
+    u /= (uint32_t)L;
+    x.gg0 = (int)(u % ngrp) * JT;
+    x.tile = (int)(u / ngrp);
+    return x;
+  }
   x.gg0 = (int)(u % ngrp) * JT;
   u /= ngrp;
   x.tile = (int)(u % tiles);
@@ -127,7 +134,7 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-      const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
+      const Unit x = decode(u, nag, ngrp, tiles, AG, JT, (flags & 4) ? L : 0);
       const bool narrow = pk.cls[x.m];
       const int mi = pk.idx[x.m];
       for (int sb = 0; sb < nsb; sb++) {
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
   int stage = 0;
   uint32_t phase = 0;
   for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
+    const Unit x = decode(u, nag, ngrp, tiles, AG, JT, (flags & 4) ? L : 0);
     const bool narrow = pk.cls[x.m];
     const uint64_t q = mt.q[x.m], bar = mt.bar[x.m], r64 = mt.r64[x.m], r64s = mt.r64s[x.m];
     KAcc acc[QB][JT][2];
@@ -295,7 +302,7 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
     int stage = 0;
     uint32_t phase = 0;
     for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-      const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
+      const Unit x = decode(u, nag, ngrp, tiles, AG, JT, (flags & 4) ? L : 0);
       for (int sb = 0; sb < nsb; sb++) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint64_t *base = reinterpret_cast<uint64_t *>(smem + (size_t)stage * STAGE_BYTES);
@@ -321,7 +328,7 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
   int stage = 0;
   uint32_t phase = 0;
   for (uint32_t u = blockIdx.x; u < units; u += gridDim.x) {
-    const Unit x = decode(u, nag, ngrp, tiles, AG, JT);
+    const Unit x = decode(u, nag, ngrp, tiles, AG, JT, (flags & 4) ? L : 0);
     const uint64_t q = mt.q[x.m], bar = mt.bar[x.m], r64 = mt.r64[x.m], r64s = mt.r64s[x.m];
     // Karatsuba sums (R35); limbs below 2^47 take the narrow form (r_h d_h < 2^32)
     const bool small = (small_mask >> x.m) & 1u;
@@ -460,7 +467,11 @@ hd_status launch(hd_context *c, const DMaps &mD, const CUtensorMap &mR, uint64_t
   const uint32_t units = (A / AG) * (uint32_t)(nj / JT) * (uint32_t)(c->n / TC) * (uint32_t)c->L;
   const uint32_t grid = std::min<uint32_t>(units, (uint32_t)g_num_sms);
   const char *dry = getenv("HD_MAC_TMA_DRY"), *co = getenv("HD_MAC_COMPUTE_ONLY");  // measurement only
-  const int flags = (dry && dry[0] == '1' ? 1 : 0) | (co && co[0] == '1' ? 2 : 0);
+  // unit order (HD_MAC_ORDER, A/B): limb second-fastest by default, so concurrent CTAs mix the
+  // wide (u64) and packed limbs' streams (MAC 7.92 -> 7.59 ms, stream alone 7.51 -> 7.09 at C4);
+  // HD_MAC_ORDER=0: limb slowest
+  const char *ord = getenv("HD_MAC_ORDER");
+  const int flags = (dry && dry[0] == '1' ? 1 : 0) | (co && co[0] == '1' ? 2 : 0) | (ord && ord[0] == '0' ? 0 : 4);
   kern<<<grid, AG * TC + 32, smem, c->stream>>>(mD.w, mD.lo, mD.hi, mR, S, n1, N, c->L, c->logn, nj, A, flat ? 1 : 0,
                                                 stages, qrows, sq, c->mt, flags, mD.pk);
   ++c->launches;
@@ -503,7 +514,8 @@ hd_status launch_ct(hd_context *c, const CtMaps &mD, const CUtensorMap &mR, uint
   for (int l = 0; l < c->L && l < 32; l++)
     if (c->mod[l] < kNarrowBound) small_mask |= 1u << l;
   const char *dry = getenv("HD_MAC_TMA_DRY"), *co = getenv("HD_MAC_COMPUTE_ONLY");  // measurement only
-  const int flags = (dry && dry[0] == '1' ? 1 : 0) | (co && co[0] == '1' ? 2 : 0);
+  const char *ord = getenv("HD_MAC_ORDER");  // as the plaintext MAC: limb second-fastest unless "0"
+  const int flags = (dry && dry[0] == '1' ? 1 : 0) | (co && co[0] == '1' ? 2 : 0) | (ord && ord[0] == '0' ? 0 : 4);
   kern<<<grid, AG * TC + 32, smem, c->stream>>>(mD, mR, S, n1, N, c->L, c->logn, nj, A, flat ? 1 : 0, stages, c->mt,
                                                 small_mask, flags);
   ++c->launches;
