@@ -9,16 +9,18 @@
 // Design.  Giant step j reads the diagonal block G(j) = k(j,0) / n1 of
 // n1 consecutive diagonals, so D of one aggregate is a 5-D tensor (coefficient, limb, diagonal
 // within a block, block, aggregate).  A producer warp streams, per pipeline stage, ONE TMA box
-// of 128 coefficients x 1 limb x SPS baby steps x JT blocks x AG aggregates (evict-first) plus
-// one box of the baby-step rows r (L2-resident, evict-last) into a ring of shared-memory
-// stages.  Consumer threads own one coefficient of one aggregate and all JT giant steps of
-// their unit, so each r word read from shared memory serves JT diagonal words and each
-// diagonal word costs one LDS and two carry-save 64x64 products (no address arithmetic, no
+// of 128 coefficients x 1 limb x SPS baby steps x JT blocks x AG aggregates (evict-first; for
+// a packed 45-bit limb, R34, a u32 box and a u16 box with the same coordinates) plus one box
+// of the baby-step rows r (L2-resident, evict-last) into a ring of shared-memory stages.
+// Consumer threads own one coefficient of one aggregate and all JT giant steps of their unit,
+// so each r word read from shared memory serves JT diagonal words and each diagonal word
+// costs one or two LDS and two Karatsuba 64x64 products (R35; no address arithmetic, no
 // register staging of loads in flight).
 //
 // Work unit = (AG aggregates, JT consecutive blocks, 128-coefficient tile, limb); one
 // persistent CTA per SM walks units u = blockIdx.x, + gridDim.x, ... with the aggregate
-// group fastest so concurrently resident CTAs share few r tiles (L2 reuse).
+// group fastest (concurrently resident CTAs share few r tiles: L2 reuse) and the limb next
+// (they mix the u64 and packed limbs' streams).
 #include "common.cuh"
 #include "ks.cuh"
 
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(AG *TC + 32, 1)
 // D [a][k][poly][L][n]: per limb m a 5-D map (coefficient, poly, diagonal within a block, block,
 // aggregate) based at limb m; one box per stage = TC x 2 polys x SPS x JT x AG.  Per stage word
 // pair (D0, D1) and baby step: d0 += r0 D0, d1 += r0 D1 + r1 D0, d2 += r1 D1,
-// carry-save, d1's mid folded every 4 steps, all banked every 64 steps (d1 takes 2 products
+// Karatsuba sums (R35), all banked every 64 steps (d1 takes 2 products
 // per step: 128 products < 2^127).  S3 [a][j][3][L][n].
 constexpr int CT_MAXL = 8;
 struct CtMaps {  // per limb: the u64 map (wide) or the u32 low-plane map (narrow, R34) + its u16 map
@@ -596,7 +598,7 @@ bool mac_tma_supported(const hd_context *c, int n1, int N, bool flat, uint32_t Q
   if (c->n % TC || n1 % 2 || n1 > 256 || Q < 1 || Q > 4) return false;
   if ((flat ? N % n1 : (N / 2) % n1) != 0) return false;  // full giant-step ranges only
   for (int l = 0; l < c->L; l++)
-    if (c->mod[l] >= (1ull << 60)) return false;  // carry-save operand split
+    if (c->mod[l] >= (1ull << 60)) return false;  // Karatsuba split: r_l + r_h < 2^32
   return encode_fn() != nullptr;
 }
 
