@@ -7,10 +7,12 @@ A "step" is one pass of the whole hot path for one encrypted
 query over the whole database: hoisted baby steps, the diagonal MAC over every
 aggregate, rescale, giant rotations, fold.  Default workload (N = 1): BASELINE.json's
 north-star configuration "ring 2^16, VECTOR_DIM = 512, 2^20 db vectors" (C4, n1 = 128,
-all 64 aggregates on one B200; 51.5 GB of diagonal plaintexts, larger than L2, so no
-L2 flush is needed between steps).  Under torchrun (N > 1) the database is sharded by
-aggregate (strong scaling: the 2^20 database is fixed); rank 0 broadcasts the query
-ciphertext and gathers the score ciphertexts over NCCL inside every timed step.
+all 64 aggregates on one B200; 42.9 GB of diagonal plaintexts (51.5 GB as u64 residues,
+R34), larger than L2, so no L2 flush is needed between steps).  Under torchrun (N > 1) the
+database is sharded by aggregate (strong scaling: the 2^20 database is fixed); rank 0
+broadcasts the query ciphertext and gathers the score ciphertexts over NCCL inside every
+timed step (N >= 4: each rank computes a slice of the baby steps and an all-gather assembles
+them).
 
 Prints ONE JSON line on rank 0.  ``--impl reference`` times the CPU oracle (oracle/,
 plain C) on a bounded sample of the same workload (there is no reference code).
@@ -114,7 +116,7 @@ def cfg_dict(cfg, world, scaling_note):
                                                              if cfg.digit_limbs > 1 else ""),
             "ring": 1 << cfg.log_n, "vector_dim": cfg.dim, "db_vectors": cfg.num_vectors, "n1": cfg.n1,
             "limbs": cfg.limbs, "aggregates": cfg.aggregates, "parallelism": f"aggregate-shard x{world}",
-            "l2": "inputs > L2 (diagonal stream 51.5 GB at C4); no flush needed" if cfg.log_n >= 16 else
+            "l2": "inputs > L2 (diagonal stream 42.9 GB packed at C4); no flush needed" if cfg.log_n >= 16 else
                   "inputs > L2", "scaling_note": scaling_note}
 
 
