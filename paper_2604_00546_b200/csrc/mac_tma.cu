@@ -613,9 +613,11 @@ hd_status mac_tma_run(hd_context *c, const uint64_t *D, const uint64_t *r, uint6
   int ag = ag_env ? atoi(ag_env) : 2;
   if (ag != 1 && ag != 2 && ag != 4) ag = 2;
   while (ag > 1 && A % ag) ag /= 2;
-  // measured at 2^20 x 512 (n1 = 128): AG 2 / SPS 8 (8 KB diagonal rows per block, 2 stages of
-  // 80 KB) 8.97 ms; SPS 4 9.35; SPS 2 10.4; AG 1 / SPS 8 10.7; AG 4 / SPS 2 10.3
-  int sps = sps_env ? atoi(sps_env) : 8;
+  // measured at 2^20 x 512 (n1 = 128), round 2 (u64 diagonals, carry-save): AG 2 / SPS 8 (2 stages
+  // of 80 KB) 8.97 ms; SPS 4 9.35; SPS 2 10.4; AG 1 / SPS 8 10.7; AG 4 / SPS 2 10.3.  Round 3
+  // (packed diagonals, Karatsuba, limb-second order): SPS 4 (5 stages of 40 KB) 7.30-7.34 ms vs
+  // SPS 8 7.53 (the deeper ring absorbs the compute's jitter); AG 4 / SPS 4 9.8; AG 1 9.0
+  int sps = sps_env ? atoi(sps_env) : 4;
   if (sps != 2 && sps != 4 && sps != 8) sps = 8;
   while (sps > 2 && n1 % sps) sps /= 2;
   // giant steps (diagonal blocks) per thread: up to 4 (each r word then serves JT diagonal words)
