@@ -543,6 +543,12 @@ hd_status mac_tma_ct_run(hd_context *c, const uint64_t *D, const uint64_t *r, ui
   int jt = jt_env ? atoi(jt_env) : 2;
   if (jt != 1 && jt != 2 && jt != 4) jt = 2;
   while (jt > 1 && nj % jt) jt /= 2;
+  // resolve to an instantiated (AG, JT, SPS) before the maps are encoded: the boxes must have
+  // the kernel's SPS (the (2, 4) kernel is built for SPS 4 only; SPS 4 exists for AG 2 only)
+  if (ag == 2 && jt == 4) sps = 4;
+  else if (!(ag == 2 && jt == 2)) sps = 8;  // (2, 2) keeps the requested 4 or 8
+  if (sps != 2 && n1 % sps) sps = 2;        // n1 even (mac_tma_supported)
+  if (sps == 2) ag = jt = 1;                // the SPS-2 kernel is (1, 1, 2)
   CtMaps mD;
   hd_status s;
   // D of limb m: (coefficient, poly, diagonal, block, aggregate); packed (R34): per polynomial
@@ -577,13 +583,13 @@ hd_status mac_tma_ct_run(hd_context *c, const uint64_t *D, const uint64_t *r, ui
     if ((s = encode(&mR, r, 3, dims, strides, box))) return s;
   }
 #define HD_CT_L(AG_, JT_, SPS_) return launch_ct<AG_, JT_, SPS_>(c, mD, mR, S3, n1, N, nj, A, flat)
+  if (sps == 2) { HD_CT_L(1, 1, 2); }
   if (ag == 2 && jt == 2 && sps == 8) { HD_CT_L(2, 2, 8); }
   if (ag == 2 && jt == 2 && sps == 4) { HD_CT_L(2, 2, 4); }
+  if (ag == 2 && jt == 4) { HD_CT_L(2, 4, 4); }
   if (ag == 2 && jt == 1) { HD_CT_L(2, 1, 8); }
   if (ag == 1 && jt == 4) { HD_CT_L(1, 4, 8); }
   if (ag == 1 && jt == 2) { HD_CT_L(1, 2, 8); }
-  if (ag == 2 && jt == 4) { HD_CT_L(2, 4, 4); }
-  if (sps == 2) { HD_CT_L(1, 1, 2); }
   HD_CT_L(1, 1, 8);
 #undef HD_CT_L
 }
